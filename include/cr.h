@@ -1,0 +1,126 @@
+/* cr.h -- C ABI of libcr.so: Z/2 persistence barcodes of the weighted cubical complex
+ * (V-construction) of a 1D/2D/3D float32 image, computed on a B200 (sm_100a).
+ *
+ * The operation:
+ *   - an image phi is a float32 array over a regular grid; voxels with value +inf lie
+ *     outside the (possibly non-rectangular) domain X (reading R5 in DESIGN.md);
+ *   - K(phi) has one d-cell per d-dimensional unit cube whose 2^d vertex voxels are all in X;
+ *     its birth is the max of its vertex values;
+ *   - the barcode lists, per dimension d = 0..min(maxdim, ndim-1), the intervals [birth, death)
+ *     of the sublevel-set filtration, death = +inf for classes that never die.
+ *
+ * Cell index (kidx).  With shape (nz, ny, nx) -- x is the LAST, fastest axis; 1D/2D images get
+ * leading sizes of 1 -- a cell is a point (X, Y, Z) of the Khalimsky grid
+ * 0 <= X <= 2nx-2, 0 <= Y <= 2ny-2, 0 <= Z <= 2nz-2; axis a is spanned iff its coordinate is odd,
+ * and kidx = (Z*(2ny-1) + Y)*(2nx-1) + X.  The voxel of a 0-cell is (X/2, Y/2, Z/2).
+ *
+ * Total order (reading R1): (birth, dim, kidx) ascending.  The barcode multiset does not depend
+ * on it; the cell pairing returned by cr_pairing does, and is unique given it.
+ *
+ * Conventions for every call:
+ *   - pointers documented "device" are CUDA device pointers on the current device; "host" are
+ *     ordinary (pageable or pinned) host pointers.  The library never frees or retains them.
+ *   - work is enqueued on `stream` (a cudaStream_t; NULL means the legacy default stream).
+ *     Workspace is allocated stream-ordered on that stream and released before return.
+ *     Calls are blocking: they return after the result is complete.
+ *   - no global mutable state; calls on different streams/devices from different host threads
+ *     are safe.  cr_status_string's CUDA error text and cr_last_stats are thread-local.
+ *   - on any error, outputs are unspecified; nothing is thrown across the ABI.
+ */
+#ifndef CR_H_
+#define CR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* cr_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  CR_OK = 0,
+  CR_EINVAL = -1,   /* null pointer, ndim not in {1,2,3}, shape entry < 1, Khalimsky size >= 2^32-2,
+                       maxdim < 0, batch < 0, or a NaN in the image                              */
+  CR_ERANGE = -2,   /* out_capacity too small; *n_pairs holds the required count                 */
+  CR_ENOMEM = -3,   /* device allocation failed                                                  */
+  CR_ECUDA = -4,    /* CUDA runtime error; see cr_status_string                                  */
+  CR_EINTERNAL = -5 /* internal invariant violated (a bug); see cr_status_string                 */
+} cr_status;
+
+/* One bar [birth, death) of dimension dim.  death = +INFINITY for essential classes.
+ * birth is always finite.  12 bytes, packed. */
+typedef struct {
+  int32_t dim;
+  float birth;
+  float death;
+} cr_pair;
+
+/* Barcode of one image (computePH(arr, maxdim) -> rows (dim, birth, death, ...)).
+ *   image           device, float32, C-contiguous, prod(shape) values.  May contain +inf (outside the
+ *                   domain) and -inf; -0.0 is treated as +0.0; NaN -> CR_EINVAL.
+ *   shape           host, ndim int64 entries, slowest axis first (x last).
+ *   ndim            1, 2 or 3.
+ *   maxdim          >= 0; dimensions 0..min(maxdim, ndim-1) are reported.
+ *   out_pairs       device, out_capacity entries, caller-owned.  Receives the bars with
+ *                   death > birth plus all essential bars, ordered by (dim, birth cell kidx)
+ *                   ascending -- each bar has a distinct birth cell, so the order is total.
+ *   out_birth_cells device or NULL; if non-NULL, out_capacity uint32 entries receiving the kidx of
+ *                   each bar's birth cell (the "location" of PAPER.md:331, 438-441).
+ *   out_capacity    entries available; cr_max_pairs() is always enough.
+ *   n_pairs         host; number of bars written, or the required count on CR_ERANGE.  */
+cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int maxdim,
+                      cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
+                      int64_t* n_pairs, cr_stream_t stream);
+
+/* Same as cr_barcodes with HOST image and HOST outputs: the library copies the image in and the
+ * bars out on `stream` (end-to-end entry point; pinned host memory is fastest). */
+cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int ndim, int maxdim,
+                           cr_pair* host_out_pairs, uint32_t* host_out_birth_cells,
+                           int64_t out_capacity, int64_t* n_pairs, cr_stream_t stream);
+
+/* Barcodes of `batch` independent images of identical shape stored back to back
+ * (images: device, batch*prod(shape) float32).  Bars of image b occupy
+ * out_pairs[out_offsets[b] .. out_offsets[b+1]) in the per-image order of cr_barcodes;
+ * out_birth_cells (optional) holds kidx within the image.
+ * out_offsets: device, batch+1 int64.  n_pairs: host, total bars (or required on CR_ERANGE). */
+cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t* shape, int ndim,
+                              int maxdim, cr_pair* out_pairs, uint32_t* out_birth_cells,
+                              int64_t out_capacity, int64_t* out_offsets, int64_t* n_pairs,
+                              cr_stream_t stream);
+
+/* Full cell pairing, all dimensions (validation).  partner: device, Khalimsky-size uint32:
+ * partner[k] = kidx of the cell paired with cell k (zero-length pairs included),
+ * CR_PARTNER_ESSENTIAL if k never dies / is never killed, CR_PARTNER_ABSENT if k has a +inf vertex. */
+#define CR_PARTNER_ESSENTIAL 0xFFFFFFFFu
+#define CR_PARTNER_ABSENT 0xFFFFFFFEu
+cr_status cr_pairing(const float* image, const int64_t* shape, int ndim, uint32_t* partner,
+                     cr_stream_t stream);
+
+/* Number of cells of dims 0..min(maxdim, ndim-1): a safe out_capacity (each bar has a distinct
+ * birth cell).  Returns -1 on invalid shape. */
+int64_t cr_max_pairs(const int64_t* shape, int ndim, int maxdim);
+
+/* Number of Khalimsky cells prod(2*shape[i]-1), the partner array length; -1 on invalid shape. */
+int64_t cr_num_cells(const int64_t* shape, int ndim);
+
+/* Static description of a status code, or (for CR_ECUDA / CR_EINTERNAL) the thread-local text of
+ * the last such error raised on this thread. */
+const char* cr_status_string(cr_status s);
+
+/* Counters of the last successful call on this host thread (thread-local). */
+typedef struct {
+  int64_t cells[4];       /* finite cells per dim                                   */
+  int64_t apparent[4];    /* apparent pairs whose lower cell has dim d              */
+  int64_t columns[4];     /* residual columns reduced in dim d (d >= 1); basins in [0] */
+  int64_t rounds[4];      /* parallel rounds: H0 merge rounds in [0], reduction rounds in [d] */
+  int64_t pairs[4];       /* bars with death > birth per dim                        */
+  int64_t essential[4];   /* essential bars per dim                                 */
+  int64_t path;           /* 1 = 1D path, 2 = general path, 3 = batched small-image path */
+} cr_stats;
+void cr_last_stats(cr_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CR_H_ */

@@ -1,0 +1,227 @@
+"""paper_2005_12692_b200 -- B200-native Cubical Ripser hot path (arXiv 2005.12692).
+
+Thin Python binding over the C ABI of ``libcr.so`` (include/cr.h).  This module only marshals
+arguments: every step of the computation runs in the sm_100a CUDA kernels behind the ABI.
+PyTorch provides device memory and the current stream.  There is no CPU fallback: if the
+library is missing or fails to load, importing this package raises.
+
+Public names mirror the ABI: ``barcodes``, ``barcodes_host``, ``barcodes_batched``, ``pairing``,
+``max_pairs``, ``num_cells``, ``last_stats``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcr.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libcr.so not built ({LIB_PATH}); run `python -m paper_2005_12692_b200.build` "
+                      "or __graft_entry__.build()")
+_lib = ctypes.CDLL(LIB_PATH)
+
+CR_OK, CR_EINVAL, CR_ERANGE, CR_ENOMEM, CR_ECUDA, CR_EINTERNAL = 0, -1, -2, -3, -4, -5
+PARTNER_ESSENTIAL = 0xFFFFFFFF
+PARTNER_ABSENT = 0xFFFFFFFE
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class CrStats(ctypes.Structure):
+    _fields_ = [("cells", _i64 * 4), ("apparent", _i64 * 4), ("columns", _i64 * 4),
+                ("rounds", _i64 * 4), ("pairs", _i64 * 4), ("essential", _i64 * 4),
+                ("path", _i64)]
+
+    def as_dict(self):
+        return {f: (list(getattr(self, f)) if f != "path" else int(self.path)) for f, _ in self._fields_}
+
+
+_lib.cr_barcodes.restype = ctypes.c_int
+_lib.cr_barcodes.argtypes = [_vp, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _i64p, _vp]
+_lib.cr_barcodes_host.restype = ctypes.c_int
+_lib.cr_barcodes_host.argtypes = [_vp, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _i64p, _vp]
+_lib.cr_barcodes_batched.restype = ctypes.c_int
+_lib.cr_barcodes_batched.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64,
+                                     _vp, _i64p, _vp]
+_lib.cr_pairing.restype = ctypes.c_int
+_lib.cr_pairing.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _vp]
+_lib.cr_max_pairs.restype = _i64
+_lib.cr_max_pairs.argtypes = [_i64p, ctypes.c_int, ctypes.c_int]
+_lib.cr_num_cells.restype = _i64
+_lib.cr_num_cells.argtypes = [_i64p, ctypes.c_int]
+_lib.cr_status_string.restype = ctypes.c_char_p
+_lib.cr_status_string.argtypes = [ctypes.c_int]
+_lib.cr_last_stats.restype = None
+_lib.cr_last_stats.argtypes = [ctypes.POINTER(CrStats)]
+
+EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
+            "cr_num_cells", "cr_status_string", "cr_last_stats"]
+
+
+class CrError(RuntimeError):
+    def __init__(self, status: int):
+        self.status = status
+        super().__init__(f"cr status {status}: {_lib.cr_status_string(status).decode()}")
+
+
+def _shape(shape):
+    return (ctypes.c_int64 * len(shape))(*[int(s) for s in shape])
+
+
+def _check(st):
+    if st != CR_OK:
+        raise CrError(st)
+
+
+def max_pairs(shape, maxdim: int) -> int:
+    n = _lib.cr_max_pairs(_shape(shape), len(shape), int(maxdim))
+    if n < 0:
+        raise CrError(CR_EINVAL)
+    return int(n)
+
+
+def num_cells(shape) -> int:
+    n = _lib.cr_num_cells(_shape(shape), len(shape))
+    if n < 0:
+        raise CrError(CR_EINVAL)
+    return int(n)
+
+
+def last_stats() -> dict:
+    s = CrStats()
+    _lib.cr_last_stats(ctypes.byref(s))
+    return s.as_dict()
+
+
+@dataclass
+class Barcode:
+    """Bars ordered by (dim, birth cell kidx).  ``pairs`` is the raw (M,3) int32 buffer of
+    cr_pair {int32 dim; float birth; float death}."""
+    pairs: "object"           # torch int32 (M,3) or numpy
+    cells: "object | None"    # uint32 (as int32 storage) kidx of birth cells, or None
+
+    @property
+    def dim(self):
+        return self.pairs[:, 0]
+
+    @property
+    def birth(self):
+        return self.pairs[:, 1].view(_float_dtype(self.pairs))
+
+    @property
+    def death(self):
+        return self.pairs[:, 2].view(_float_dtype(self.pairs))
+
+    def numpy(self):
+        p = self.pairs.cpu().numpy() if hasattr(self.pairs, "cpu") else np.asarray(self.pairs)
+        c = None
+        if self.cells is not None:
+            c = (self.cells.cpu().numpy() if hasattr(self.cells, "cpu") else np.asarray(self.cells))
+            c = c.view(np.uint32)
+        return p[:, 0].copy(), p[:, 1].view(np.float32).copy(), p[:, 2].view(np.float32).copy(), c
+
+
+def _float_dtype(arr):
+    if isinstance(arr, np.ndarray):
+        return np.float32
+    import torch
+    return torch.float32
+
+
+def _stream_ptr(torch, device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def barcodes(image, maxdim: int = 1, cells: bool = False, capacity: int | None = None,
+             out=None) -> Barcode:
+    """Barcode of one image (torch CUDA float32 tensor, 1-3 dims, x = last axis).
+
+    ``out``: optional preallocated (pairs int32 (cap,3), cells int32 (cap,) or None) buffers.
+    """
+    import torch
+    if not (isinstance(image, torch.Tensor) and image.is_cuda and image.dtype == torch.float32):
+        raise TypeError("image must be a CUDA float32 tensor")
+    image = image.contiguous()
+    shape = tuple(image.shape)
+    if out is None:
+        cap = max_pairs(shape, maxdim) if capacity is None else int(capacity)
+        pairs = torch.empty((max(cap, 1), 3), dtype=torch.int32, device=image.device)
+        cbuf = torch.empty((max(cap, 1),), dtype=torch.int32, device=image.device) if cells else None
+    else:
+        pairs, cbuf = out
+        cap = pairs.shape[0]
+    n = ctypes.c_int64(0)
+    st = _lib.cr_barcodes(image.data_ptr(), _shape(shape), len(shape), int(maxdim), pairs.data_ptr(),
+                          cbuf.data_ptr() if cbuf is not None else None, cap, ctypes.byref(n),
+                          _stream_ptr(torch, image.device))
+    _check(st)
+    m = int(n.value)
+    return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None)
+
+
+def barcodes_host(image: np.ndarray, maxdim: int = 1, cells: bool = False, out=None,
+                  stream=None) -> Barcode:
+    """End-to-end entry: host (numpy, ideally pinned) image in, host bars out."""
+    import torch
+    img = np.ascontiguousarray(image, dtype=np.float32) if isinstance(image, np.ndarray) else image
+    shape = tuple(img.shape)
+    if out is None:
+        cap = max_pairs(shape, maxdim)
+        pairs = np.empty((max(cap, 1), 3), np.int32)
+        cbuf = np.empty((max(cap, 1),), np.uint32) if cells else None
+    else:
+        pairs, cbuf = out
+        cap = pairs.shape[0]
+    ptr_img = img.ctypes.data if isinstance(img, np.ndarray) else img.data_ptr()
+    ptr_out = pairs.ctypes.data if isinstance(pairs, np.ndarray) else pairs.data_ptr()
+    ptr_c = None
+    if cbuf is not None:
+        ptr_c = cbuf.ctypes.data if isinstance(cbuf, np.ndarray) else cbuf.data_ptr()
+    n = ctypes.c_int64(0)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    st = _lib.cr_barcodes_host(ptr_img, _shape(shape), len(shape), int(maxdim), ptr_out, ptr_c, cap,
+                               ctypes.byref(n), ctypes.c_void_p(s.cuda_stream))
+    _check(st)
+    m = int(n.value)
+    return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None)
+
+
+def barcodes_batched(images, maxdim: int = 1, cells: bool = False, capacity: int | None = None):
+    """Barcodes of a batch (torch CUDA float32 tensor (B, *shape)).  Returns (Barcode, offsets)
+    with offsets an int64 CUDA tensor of B+1 CSR offsets."""
+    import torch
+    if not (isinstance(images, torch.Tensor) and images.is_cuda and images.dtype == torch.float32):
+        raise TypeError("images must be a CUDA float32 tensor")
+    images = images.contiguous()
+    B = int(images.shape[0])
+    shape = tuple(images.shape[1:])
+    cap = (max_pairs(shape, maxdim) * B) if capacity is None else int(capacity)
+    pairs = torch.empty((max(cap, 1), 3), dtype=torch.int32, device=images.device)
+    cbuf = torch.empty((max(cap, 1),), dtype=torch.int32, device=images.device) if cells else None
+    offsets = torch.empty((B + 1,), dtype=torch.int64, device=images.device)
+    n = ctypes.c_int64(0)
+    st = _lib.cr_barcodes_batched(images.data_ptr(), B, _shape(shape), len(shape), int(maxdim),
+                                  pairs.data_ptr(), cbuf.data_ptr() if cbuf is not None else None,
+                                  cap, offsets.data_ptr(), ctypes.byref(n),
+                                  _stream_ptr(torch, images.device))
+    _check(st)
+    m = int(n.value)
+    return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None), offsets
+
+
+def pairing(image):
+    """Full cell pairing (uint32 stored in an int32 CUDA tensor of Khalimsky size)."""
+    import torch
+    image = image.contiguous()
+    shape = tuple(image.shape)
+    part = torch.empty((num_cells(shape),), dtype=torch.int32, device=image.device)
+    st = _lib.cr_pairing(image.data_ptr(), _shape(shape), len(shape), part.data_ptr(),
+                         _stream_ptr(torch, image.device))
+    _check(st)
+    return part

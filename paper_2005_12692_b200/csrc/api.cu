@@ -1,0 +1,344 @@
+// api.cu -- the extern "C" boundary of libcr.so (include/cr.h).
+#include <cub/cub.cuh>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "pipeline.cuh"
+
+namespace cr {
+const char* last_error_text();
+static thread_local cr_stats g_last_stats;
+
+namespace {
+
+bool valid_shape(const int64_t* shape, int ndim) {
+  if (!shape || ndim < 1 || ndim > 3) return false;
+  int64_t n = 1;
+  for (int i = 0; i < ndim; ++i) {
+    if (shape[i] < 1 || shape[i] > (int64_t(1) << 32)) return false;
+    n *= 2 * shape[i] - 1;
+    if (n >= (int64_t(1) << 32) - 2) return false;
+  }
+  return true;
+}
+
+bool force_general() {
+  const char* e = std::getenv("CR_FORCE_GENERAL");
+  return e && e[0] == '1';
+}
+
+cr_status fail(const Error& e) {
+  set_error_text(e.msg);
+  return e.st;
+}
+
+// Stack `batch` images along the slowest axis with one +inf separator layer between them, so the
+// complexes are disjoint (cells touching a separator are absent, reading R5).
+__global__ void k_stack(const float* __restrict__ src, int64_t per_img, int64_t layer,
+                        int64_t layers_per_img, int64_t total, float* __restrict__ dst) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int64_t L = i / layer;  // layer index in the stacked image
+  int64_t b = L / (layers_per_img + 1), l = L % (layers_per_img + 1);
+  dst[i] = (l == layers_per_img) ? __int_as_float(0x7F800000)
+                                 : src[b * per_img + l * layer + (i % layer)];
+}
+
+// Batched emission: keep bars, sort by (image, dim, local kidx), write CSR offsets.
+__global__ void k_batch_keys(const uint64_t* __restrict__ rec, int64_t n, int dim,
+                             const uint32_t* __restrict__ births, uint32_t cells_per_layer_k,
+                             uint32_t klayers_per_img, uint64_t* __restrict__ keys,
+                             uint64_t* __restrict__ vals, unsigned* __restrict__ nkeep) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool keep = false;
+  uint64_t key = 0, val = 0;
+  if (i < n) {
+    uint64_t r = rec[i];
+    uint32_t b = uint32_t(r >> 32), d = uint32_t(r);
+    uint32_t bo = births[b];
+    uint32_t dor = d == NONE32 ? 0xFFFFFFFFu : births[d];
+    keep = (d == NONE32) || (dor > bo);
+    // Khalimsky layer of the birth cell along the stacking axis -> image, local kidx
+    uint32_t KL = b / cells_per_layer_k;
+    uint32_t img = KL / klayers_per_img;
+    uint32_t local = b - img * klayers_per_img * cells_per_layer_k;
+    key = (uint64_t(img) << 34) | (uint64_t(dim) << 32) | local;
+    val = (uint64_t(bo) << 32) | dor;
+  }
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, keep);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(nkeep, __popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (keep) {
+    unsigned o = base + __popc(mask & ((1u << lane) - 1));
+    keys[o] = key;
+    vals[o] = val;
+  }
+}
+
+__global__ void k_batch_write(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals,
+                              int64_t n, int64_t cap, cr_pair* out, uint32_t* out_cells,
+                              unsigned* __restrict__ count) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = keys[i], v = vals[i];
+  uint32_t img = uint32_t(k >> 34);
+  atomicAdd(count + img, 1u);
+  if (i >= cap) return;
+  cr_pair p;
+  p.dim = int32_t((k >> 32) & 3);
+  p.birth = float_of_ord(uint32_t(v >> 32));
+  uint32_t dor = uint32_t(v);
+  p.death = dor == 0xFFFFFFFFu ? __int_as_float(0x7F800000) : float_of_ord(dor);
+  out[i] = p;
+  if (out_cells) out_cells[i] = uint32_t(k);
+}
+
+__global__ void k_offsets(const unsigned* __restrict__ count_scan, int64_t batch, int64_t total,
+                          int64_t* __restrict__ offsets) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < batch) offsets[i] = count_scan[i];
+  if (i == batch) offsets[i] = total;
+}
+
+int report_dmax(const Geom& g, int maxdim) {
+  int top = g.D - 1;
+  if (top < 0) top = 0;
+  return maxdim < top ? maxdim : top;
+}
+
+}  // namespace
+}  // namespace cr
+
+using namespace cr;
+
+extern "C" {
+
+int64_t cr_num_cells(const int64_t* shape, int ndim) {
+  if (!valid_shape(shape, ndim)) return -1;
+  return make_geom(shape, ndim).ncells;
+}
+
+int64_t cr_max_pairs(const int64_t* shape, int ndim, int maxdim) {
+  if (!valid_shape(shape, ndim) || maxdim < 0) return -1;
+  Geom g = make_geom(shape, ndim);
+  int64_t n = 0;
+  for (int Z = 0; Z < 2; ++Z)
+    for (int Y = 0; Y < 2; ++Y)
+      for (int X = 0; X < 2; ++X)
+        if (X + Y + Z <= maxdim)
+          n += ((g.KZ - Z + 1) / 2) * ((g.KY - Y + 1) / 2) * ((g.KX - X + 1) / 2);
+  return n;
+}
+
+const char* cr_status_string(cr_status s) {
+  switch (s) {
+    case CR_OK: return "ok";
+    case CR_EINVAL: return "invalid argument (null pointer, bad shape/ndim/maxdim, or NaN in image)";
+    case CR_ERANGE: return "output capacity too small (n_pairs holds the required count)";
+    case CR_ENOMEM: return "device allocation failed";
+    case CR_ECUDA:
+    case CR_EINTERNAL: return cr::last_error_text();
+  }
+  return "unknown status";
+}
+
+void cr_last_stats(cr_stats* out) {
+  if (out) *out = g_last_stats;
+}
+
+cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int maxdim,
+                      cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
+                      int64_t* n_pairs, cr_stream_t stream) {
+  if (!image || !n_pairs || !valid_shape(shape, ndim) || maxdim < 0 || out_capacity < 0 ||
+      (out_capacity > 0 && !out_pairs))
+    return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Geom g = make_geom(shape, ndim);
+    Workspace ws(s);
+    HostScalars hs;
+    cr_stats st{};
+    int64_t n;
+    if (g.D <= 1 && !force_general()) {
+      st.path = 1;
+      n = barcodes_1d(image, g.nvox, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
+    } else {
+      st.path = 2;
+      GeneralState S;
+      int dm = report_dmax(g, maxdim);
+      run_general(image, g, dm, ws, hs, S, st);
+      n = emit_bars(S, dm, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
+    }
+    CR_CUDA(cudaStreamSynchronize(s));
+    *n_pairs = n;
+    if (n > out_capacity) return CR_ERANGE;
+    g_last_stats = st;
+    return CR_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int ndim, int maxdim,
+                           cr_pair* host_out_pairs, uint32_t* host_out_birth_cells,
+                           int64_t out_capacity, int64_t* n_pairs, cr_stream_t stream) {
+  if (!host_image || !n_pairs || !valid_shape(shape, ndim) || maxdim < 0 || out_capacity < 0 ||
+      (out_capacity > 0 && !host_out_pairs))
+    return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Geom g = make_geom(shape, ndim);
+    float* dimg = nullptr;
+    cr_pair* dout = nullptr;
+    uint32_t* dcells = nullptr;
+    CR_CUDA(cudaMallocAsync(&dimg, g.nvox * sizeof(float), s));
+    int64_t cap = out_capacity > 0 ? out_capacity : 1;
+    cudaError_t e1 = cudaMallocAsync(&dout, cap * sizeof(cr_pair), s);
+    cudaError_t e2 = host_out_birth_cells ? cudaMallocAsync(&dcells, cap * sizeof(uint32_t), s)
+                                          : cudaSuccess;
+    cr_status rs = CR_OK;
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      rs = CR_ENOMEM;
+    } else {
+      CR_CUDA(cudaMemcpyAsync(dimg, host_image, g.nvox * sizeof(float), cudaMemcpyHostToDevice, s));
+      rs = cr_barcodes(dimg, shape, ndim, maxdim, dout, dcells, out_capacity, n_pairs, stream);
+      if (rs == CR_OK && *n_pairs > 0) {
+        CR_CUDA(cudaMemcpyAsync(host_out_pairs, dout, *n_pairs * sizeof(cr_pair),
+                                cudaMemcpyDeviceToHost, s));
+        if (host_out_birth_cells)
+          CR_CUDA(cudaMemcpyAsync(host_out_birth_cells, dcells, *n_pairs * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, s));
+      }
+    }
+    cudaFreeAsync(dimg, s);
+    if (dout) cudaFreeAsync(dout, s);
+    if (dcells) cudaFreeAsync(dcells, s);
+    CR_CUDA(cudaStreamSynchronize(s));
+    return rs;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t* shape, int ndim,
+                              int maxdim, cr_pair* out_pairs, uint32_t* out_birth_cells,
+                              int64_t out_capacity, int64_t* out_offsets, int64_t* n_pairs,
+                              cr_stream_t stream) {
+  if (!n_pairs || !out_offsets || batch < 0 || !valid_shape(shape, ndim) || maxdim < 0 ||
+      out_capacity < 0 || (out_capacity > 0 && !out_pairs) || (batch > 0 && !images))
+    return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Geom g1 = make_geom(shape, ndim);
+    if (batch == 0) {
+      CR_CUDA(cudaMemsetAsync(out_offsets, 0, sizeof(int64_t), s));
+      CR_CUDA(cudaStreamSynchronize(s));
+      *n_pairs = 0;
+      return CR_OK;
+    }
+    // Stack the images along their own slowest axis with one +inf separator layer between
+    // consecutive images: the stacked complex is the disjoint union of the images' complexes
+    // (every cell touching a separator is absent, reading R5), so its bars are theirs.
+    const int64_t L = shape[0];
+    int64_t layer = 1;
+    for (int i = 1; i < ndim; ++i) layer *= shape[i];
+    int64_t stacked[3];
+    for (int i = 0; i < ndim; ++i) stacked[i] = shape[i];
+    stacked[0] = batch * (L + 1) - 1;
+    if (!valid_shape(stacked, ndim)) return CR_EINVAL;
+    Geom g = make_geom(stacked, ndim);
+    const int64_t layers = L;
+    Workspace ws(s);
+    HostScalars hs;
+    cr_stats st{};
+    st.path = 3;
+    float* simg = ws.alloc<float>(g.nvox);
+    k_stack<<<grid_for(g.nvox, 256), 256, 0, s>>>(images, layers * layer, layer, layers, g.nvox,
+                                                   simg);
+    CR_CHECK_LAUNCH();
+    GeneralState S;
+    int dm = report_dmax(g1, maxdim);
+    run_general(simg, g, dm, ws, hs, S, st);
+    ws.release(simg);
+    // batched emission
+    int64_t nrec = 0;
+    for (int d = 0; d <= dm; ++d) nrec += S.R.n[d];
+    uint64_t* keys = ws.alloc<uint64_t>(nrec + 1);
+    uint64_t* vals = ws.alloc<uint64_t>(nrec + 1);
+    unsigned* nkeep = ws.alloc<unsigned>(1);
+    CR_CUDA(cudaMemsetAsync(nkeep, 0, sizeof(unsigned), s));
+    // Khalimsky cells per layer of the stacking axis, and Khalimsky layers per image period
+    uint32_t CL = 1;
+    for (int i = 1; i < ndim; ++i) CL *= uint32_t(2 * shape[i] - 1);
+    const uint32_t KPI = uint32_t(2 * (L + 1));
+    for (int d = 0; d <= dm; ++d)
+      if (S.R.n[d] > 0) {
+        k_batch_keys<<<grid_for(S.R.n[d], 256), 256, 0, s>>>(S.R.rec[d], S.R.n[d], d, S.births,
+                                                             CL, KPI, keys, vals, nkeep);
+        CR_CHECK_LAUNCH();
+      }
+    unsigned nk = read_scalar(nkeep, s, hs);
+    // sort (image, dim, local kidx) with values
+    if (nk > 1) {
+      uint64_t* k2 = ws.alloc<uint64_t>(nk);
+      uint64_t* v2 = ws.alloc<uint64_t>(nk);
+      cub::DoubleBuffer<uint64_t> dk(keys, k2), dv(vals, v2);
+      size_t tmp = 0;
+      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(nk), 0, 64, s));
+      void* t = ws.alloc_bytes(tmp);
+      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(nk), 0, 64, s));
+      keys = dk.Current();
+      vals = dv.Current();
+    }
+    unsigned* count = ws.alloc<unsigned>(batch + 1);
+    unsigned* scan = ws.alloc<unsigned>(batch + 1);
+    CR_CUDA(cudaMemsetAsync(count, 0, (batch + 1) * sizeof(unsigned), s));
+    if (nk > 0) {
+      k_batch_write<<<grid_for(nk, 256), 256, 0, s>>>(keys, vals, nk, out_capacity, out_pairs,
+                                                      out_birth_cells, count);
+      CR_CHECK_LAUNCH();
+    }
+    exclusive_sum_u32(count, scan, batch + 1, ws);
+    k_offsets<<<grid_for(batch + 1, 256), 256, 0, s>>>(scan, batch, nk, out_offsets);
+    CR_CHECK_LAUNCH();
+    CR_CUDA(cudaStreamSynchronize(s));
+    *n_pairs = nk;
+    if (int64_t(nk) > out_capacity) return CR_ERANGE;
+    g_last_stats = st;
+    return CR_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+cr_status cr_pairing(const float* image, const int64_t* shape, int ndim, uint32_t* partner,
+                     cr_stream_t stream) {
+  if (!image || !partner || !valid_shape(shape, ndim)) return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Geom g = make_geom(shape, ndim);
+    Workspace ws(s);
+    HostScalars hs;
+    cr_stats st{};
+    if (g.D <= 1 && !force_general()) {
+      st.path = 1;
+      pairing_1d(image, g.nvox, partner, ws, hs, st);
+    } else {
+      st.path = 2;
+      GeneralState S;
+      run_general(image, g, g.D - 1, ws, hs, S, st);
+      emit_partner(S, partner, ws);
+    }
+    CR_CUDA(cudaStreamSynchronize(s));
+    g_last_stats = st;
+    return CR_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+}  // extern "C"

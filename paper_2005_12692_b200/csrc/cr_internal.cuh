@@ -1,0 +1,101 @@
+// cr_internal.cuh -- shared device/host helpers of libcr.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/cr.h"
+
+namespace cr {
+
+constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+constexpr uint64_t NONE64 = 0xFFFFFFFFFFFFFFFFull;
+// ord(+inf): +inf cells are absent from K (reading R5); every finite ord is smaller.
+constexpr uint32_t ABSENT_ORD = 0xFF800000u;
+
+// Order-preserving map float32 -> uint32 after -0.0 -> +0.0 (reading R7): a < b as floats
+// iff ord(a) < ord(b).  NaN never reaches it (rejected first).
+__host__ __device__ __forceinline__ uint32_t ord_of(float f) {
+#ifdef __CUDA_ARCH__
+  uint32_t u = __float_as_uint(f);
+#else
+  uint32_t u;
+  memcpy(&u, &f, 4);
+#endif
+  if (u == 0x80000000u) u = 0u;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float float_of_ord(uint32_t o) {
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+__host__ __device__ __forceinline__ uint64_t make_key(uint32_t ord, uint32_t kidx) {
+  return (uint64_t(ord) << 32) | kidx;
+}
+__host__ __device__ __forceinline__ uint32_t key_ord(uint64_t k) { return uint32_t(k >> 32); }
+__host__ __device__ __forceinline__ uint32_t key_kidx(uint64_t k) { return uint32_t(k); }
+
+// Khalimsky geometry.  Cell (X,Y,Z), kidx = (Z*KY + Y)*KX + X.
+struct Geom {
+  int64_t nx, ny, nz;      // voxels per axis (x fastest)
+  int64_t KX, KY, KZ;      // 2n-1
+  int64_t ncells;          // KX*KY*KZ
+  int64_t nvox;            // nx*ny*nz
+  int D;                   // number of axes with extent > 1 (0 for a single voxel)
+  __host__ __device__ __forceinline__ int64_t stride(int axis) const {
+    return axis == 0 ? 1 : (axis == 1 ? KX : KX * KY);
+  }
+};
+
+// Per-cell tag (u8): kind in bits 6-7, partner direction in bits 0-2.
+//   kind 0: residual (not an apparent pair)
+//   kind 1: DOWN  -- upper cell of an apparent pair (partner is a facet)
+//   kind 2: UP    -- lower cell of an apparent pair (partner is a cofacet)
+//   kind 3: CLEARED -- residual cell that is the death cell of a pair one dimension below
+// direction dir = 2*axis + (sign > 0): partner kidx = kidx + (sign)*stride(axis).
+constexpr uint8_t KIND_RESIDUAL = 0, KIND_DOWN = 1, KIND_UP = 2, KIND_CLEARED = 3;
+__host__ __device__ __forceinline__ uint8_t tag_kind(uint8_t t) { return t >> 6; }
+__host__ __device__ __forceinline__ int tag_dir(uint8_t t) { return t & 7; }
+__host__ __device__ __forceinline__ uint8_t make_tag(uint8_t kind, int dir) {
+  return uint8_t((kind << 6) | dir);
+}
+__host__ __device__ __forceinline__ int64_t dir_offset(const Geom& g, int dir) {
+  int64_t s = g.stride(dir >> 1);
+  return (dir & 1) ? s : -s;
+}
+
+// Error plumbing (host).
+struct Error {
+  cr_status st;
+  std::string msg;
+};
+void set_error_text(const std::string& s);
+
+#define CR_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      throw ::cr::Error{e_ == cudaErrorMemoryAllocation ? CR_ENOMEM : CR_ECUDA,             \
+                        std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +         \
+                            __FILE__ + ":" + std::to_string(__LINE__)};                     \
+    }                                                                                       \
+  } while (0)
+
+#define CR_CHECK_LAUNCH() CR_CUDA(cudaGetLastError())
+
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 0x7FFFFFFF) g = 0x7FFFFFFF;
+  return unsigned(g);
+}
+
+}  // namespace cr

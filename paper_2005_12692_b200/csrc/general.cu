@@ -1,0 +1,544 @@
+// general.cu -- the general (1D/2D/3D, one image) path: K1 filtration, K2 apparent pairs,
+// K4 dimension-0 pairing (union-find with the elder rule), bar/partner emission.
+// The dims >= 1 reduction (K5) is in reduce.cu.
+#include <cub/cub.cuh>
+
+#include "pipeline.cuh"
+
+namespace cr {
+
+Geom make_geom(const int64_t* shape, int ndim) {
+  Geom g{};
+  int64_t s[3] = {1, 1, 1};
+  for (int i = 0; i < ndim; ++i) s[3 - ndim + i] = shape[i];
+  g.nz = s[0];
+  g.ny = s[1];
+  g.nx = s[2];
+  g.KX = 2 * g.nx - 1;
+  g.KY = 2 * g.ny - 1;
+  g.KZ = 2 * g.nz - 1;
+  g.ncells = g.KX * g.KY * g.KZ;
+  g.nvox = g.nx * g.ny * g.nz;
+  g.D = (g.nx > 1) + (g.ny > 1) + (g.nz > 1);
+  return g;
+}
+
+namespace {
+
+__device__ __forceinline__ void coords_of(const Geom& g, uint32_t k, uint32_t& X, uint32_t& Y,
+                                          uint32_t& Z) {
+  uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  X = k % KX;
+  uint32_t r = k / KX;
+  Y = r % KY;
+  Z = r / KY;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1: cell births.  One thread per voxel writes the (up to) 8 Khalimsky cells
+// whose lowest vertex is that voxel; birth = max over the cell's vertices of ord(phi).  Since
+// ord(+inf) is the largest ord of any non-NaN float, a cell with a +inf vertex gets ABSENT_ORD.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_births(const float* __restrict__ img, Geom g, uint32_t* __restrict__ births,
+                         int* __restrict__ nan_flag) {
+  int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= g.nvox) return;
+  int64_t x = v % g.nx, t = v / g.nx, y = t % g.ny, z = t / g.ny;
+  float f = img[v];
+  if (f != f) atomicOr(nan_flag, 1);
+  const int hx = x + 1 < g.nx, hy = y + 1 < g.ny, hz = z + 1 < g.nz;
+  uint32_t o[2][2][2];
+  for (int dz = 0; dz <= hz; ++dz)
+    for (int dy = 0; dy <= hy; ++dy)
+      for (int dx = 0; dx <= hx; ++dx)
+        o[dz][dy][dx] = ord_of(__ldg(img + v + dz * g.nx * g.ny + dy * g.nx + dx));
+  for (int a = 0; a <= hz; ++a)
+    for (int b = 0; b <= hy; ++b)
+      for (int c = 0; c <= hx; ++c) {
+        uint32_t m = 0;
+        for (int dz = 0; dz <= a; ++dz)
+          for (int dy = 0; dy <= b; ++dy)
+            for (int dx = 0; dx <= c; ++dx) m = max(m, o[dz][dy][dx]);
+        births[((2 * z + a) * g.KY + 2 * y + b) * g.KX + 2 * x + c] = m;
+      }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2: apparent pairs (Ripser's shortcut, inherited per PAPER.md:44-45).  For a finite cell s:
+//   UP   : t = min-key cofacet of s, and s is the max-key facet of t  -> (s, t) is a pair;
+//   DOWN : r = max-key facet of s, and s is the min-key cofacet of r   -> (r, s) is a pair.
+// Keys are (ord(birth), kidx); the pair always has death == birth (birth(t) = max facet birth).
+// Each thread writes only its own tag, so no two threads touch the same byte.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_tags(const uint32_t* __restrict__ births, Geom g, uint8_t* __restrict__ tags,
+                       unsigned long long* __restrict__ app_cnt) {
+  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (kk >= g.ncells) return;
+  const uint32_t k = uint32_t(kk);
+  const uint32_t bo = births[k];
+  if (bo == ABSENT_ORD) {
+    tags[k] = 0;
+    return;
+  }
+  uint32_t c[3];
+  coords_of(g, k, c[0], c[1], c[2]);
+  const uint32_t ext[3] = {uint32_t(g.KX), uint32_t(g.KY), uint32_t(g.KZ)};
+  const int64_t st[3] = {1, g.KX, g.KX * g.KY};
+  const uint64_t mykey = make_key(bo, k);
+  const int dim = (c[0] & 1) + (c[1] & 1) + (c[2] & 1);
+  uint8_t tag = 0;
+  // UP
+  {
+    uint64_t best = NONE64;
+    int bdir = -1;
+    for (int a = 0; a < 3; ++a) {
+      if (c[a] & 1) continue;
+      for (int s = 0; s < 2; ++s) {
+        if (s == 0 ? c[a] == 0 : c[a] + 1 >= ext[a]) continue;
+        uint32_t t = uint32_t(int64_t(k) + (s ? st[a] : -st[a]));
+        uint32_t tb = __ldg(births + t);
+        if (tb == ABSENT_ORD) continue;
+        uint64_t key = make_key(tb, t);
+        if (key < best) { best = key; bdir = 2 * a + s; }
+      }
+    }
+    if (bdir >= 0) {
+      uint32_t t = key_kidx(best);
+      int ta = bdir >> 1;
+      bool is_max = true;
+      for (int a = 0; a < 3 && is_max; ++a) {
+        bool odd = (a == ta) ? true : (c[a] & 1);
+        if (!odd) continue;
+        for (int s = 0; s < 2; ++s) {
+          uint32_t f = uint32_t(int64_t(t) + (s ? st[a] : -st[a]));
+          if (f == k) continue;
+          if (make_key(__ldg(births + f), f) > mykey) { is_max = false; break; }
+        }
+      }
+      if (is_max) tag = make_tag(KIND_UP, bdir);
+    }
+  }
+  // DOWN
+  if (!tag && dim >= 1) {
+    uint64_t best = 0;
+    int bdir = -1;
+    for (int a = 0; a < 3; ++a) {
+      if (!(c[a] & 1)) continue;
+      for (int s = 0; s < 2; ++s) {
+        uint32_t f = uint32_t(int64_t(k) + (s ? st[a] : -st[a]));
+        uint64_t key = make_key(__ldg(births + f), f);
+        if (bdir < 0 || key > best) { best = key; bdir = 2 * a + s; }
+      }
+    }
+    uint32_t r = key_kidx(best);
+    int ra = bdir >> 1;
+    bool is_min = true;
+    for (int a = 0; a < 3 && is_min; ++a) {
+      bool odd = (a == ra) ? false : (c[a] & 1);
+      if (odd) continue;
+      uint32_t ca = (a == ra) ? c[a] + ((bdir & 1) ? 1 : -1) : c[a];
+      for (int s = 0; s < 2; ++s) {
+        if (s == 0 ? ca == 0 : ca + 1 >= ext[a]) continue;
+        uint32_t t = uint32_t(int64_t(r) + (s ? st[a] : -st[a]));
+        if (t == k) continue;
+        uint32_t tb = __ldg(births + t);
+        if (tb == ABSENT_ORD) continue;
+        if (make_key(tb, t) < mykey) { is_min = false; break; }
+      }
+    }
+    if (is_min) tag = make_tag(KIND_DOWN, bdir);
+  }
+  tags[k] = tag;
+  if (tag_kind(tag) == KIND_UP) atomicAdd(app_cnt + dim, 1ull);
+}
+
+__global__ void k_count_cells(const uint32_t* __restrict__ births, Geom g,
+                              unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned long long s[4];
+  if (threadIdx.x < 4) s[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (kk < g.ncells && births[kk] != ABSENT_ORD) {
+    uint32_t X, Y, Z;
+    coords_of(g, uint32_t(kk), X, Y, Z);
+    atomicAdd(&s[(X & 1) + (Y & 1) + (Z & 1)], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s[threadIdx.x]) atomicAdd(cnt + threadIdx.x, s[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K4: H0 by union-find with the elder rule.
+//  (1) every apparent vertex v (UP, paired with its earliest edge e_v) hangs under the other
+//      endpoint of e_v, which is older; roots are the non-apparent vertices ("basins").
+//  (2) pointer jumping flattens the forest.
+//  (3) a residual edge whose endpoints share a root is positive (a cycle); the others are
+//      inter-basin candidates.
+//  (4) mutual-minimum rounds: every component takes its minimum candidate edge; an edge that is
+//      the minimum at both of its components is exactly the next Kruskal merge there, so it is
+//      committed: the younger root dies at it (elder rule) and is linked under the elder.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t vox_kidx(const Geom& g, uint32_t v) {
+  uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
+  uint32_t x = v % nx, r = v / nx, y = r % ny, z = r / ny;
+  return (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
+}
+__device__ __forceinline__ uint32_t kidx_vox(const Geom& g, uint32_t k) {
+  uint32_t X, Y, Z;
+  coords_of(g, k, X, Y, Z);
+  return ((Z >> 1) * uint32_t(g.ny) + (Y >> 1)) * uint32_t(g.nx) + (X >> 1);
+}
+
+__global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
+                            Geom g, uint32_t* __restrict__ parent) {
+  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vv >= g.nvox) return;
+  uint32_t v = uint32_t(vv);
+  uint32_t k = vox_kidx(g, v);
+  uint8_t t = tags[k];
+  uint32_t p = v;
+  if (births[k] != ABSENT_ORD && tag_kind(t) == KIND_UP) {
+    int d = tag_dir(t);
+    int64_t vs = (d >> 1) == 0 ? 1 : ((d >> 1) == 1 ? g.nx : g.nx * g.ny);
+    p = uint32_t(int64_t(v) + ((d & 1) ? vs : -vs));
+  }
+  parent[v] = p;
+}
+
+__global__ void k_pointer_jump(uint32_t* parent, int64_t n) {
+  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vv >= n) return;
+  uint32_t v = uint32_t(vv);
+  uint32_t p = parent[v];
+  while (true) {
+    uint32_t pp = *(volatile uint32_t*)(parent + p);
+    if (pp == p) break;
+    p = pp;
+    parent[v] = p;
+  }
+}
+
+struct Cand {
+  uint64_t key;  // edge key
+  uint32_t a, b; // current component roots (voxel ids)
+};
+
+__global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
+                           Geom g, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
+                           unsigned int* __restrict__ ncand) {
+  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool emit = false;
+  Cand c;
+  if (kk < g.ncells) {
+    uint32_t k = uint32_t(kk);
+    uint32_t X, Y, Z;
+    coords_of(g, k, X, Y, Z);
+    int dim = (X & 1) + (Y & 1) + (Z & 1);
+    uint32_t bo = births[k];
+    if (dim == 1 && bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+      int64_t s = (X & 1) ? 1 : ((Y & 1) ? g.KX : g.KX * g.KY);
+      uint32_t va = kidx_vox(g, uint32_t(k - s)), vb = kidx_vox(g, uint32_t(k + s));
+      uint32_t ra = parent[va], rb = parent[vb];
+      if (ra != rb) {
+        emit = true;
+        c.key = make_key(bo, k);
+        c.a = ra;
+        c.b = rb;
+      }
+    }
+  }
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(ncand, __popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (emit) cand[base + __popc(mask & ((1u << lane) - 1))] = c;
+}
+
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
+  uint32_t p = *(volatile uint32_t*)(parent + v);
+  if (p == v) return v;
+  while (true) {
+    uint32_t pp = *(volatile uint32_t*)(parent + p);
+    if (pp == p) break;
+    p = pp;
+  }
+  return p;
+}
+
+__global__ void k_mm_find(Cand* cand, unsigned n, uint32_t* parent, unsigned long long* best,
+                          uint8_t* alive) {
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Cand c = cand[i];
+  uint32_t a = uf_find(parent, c.a), b = uf_find(parent, c.b);
+  cand[i].a = a;
+  cand[i].b = b;
+  if (a == b) {  // connected through strictly smaller edges: positive
+    alive[i] = 0;
+    return;
+  }
+  alive[i] = 1;
+  atomicMin(best + a, (unsigned long long)c.key);
+  atomicMin(best + b, (unsigned long long)c.key);
+}
+
+__global__ void k_mm_commit(const Cand* cand, unsigned n, const uint32_t* __restrict__ births,
+                            Geom g, uint32_t* parent, const unsigned long long* best,
+                            uint8_t* alive, uint8_t* tags, uint64_t* rec,
+                            unsigned long long* nrec) {
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !alive[i]) return;
+  Cand c = cand[i];
+  if (best[c.a] != c.key || best[c.b] != c.key) return;
+  uint32_t ka = vox_kidx(g, c.a), kb = vox_kidx(g, c.b);
+  uint64_t keya = make_key(births[ka], ka), keyb = make_key(births[kb], kb);
+  uint32_t young = keya > keyb ? c.a : c.b, old = keya > keyb ? c.b : c.a;
+  uint32_t kyoung = keya > keyb ? ka : kb;
+  parent[young] = old;  // elder rule: the younger component dies
+  tags[key_kidx(c.key)] = make_tag(KIND_CLEARED, 0);  // a death edge: cleared for dim 1
+  unsigned long long r = atomicAdd(nrec, 1ull);
+  rec[r] = (uint64_t(kyoung) << 32) | key_kidx(c.key);
+  alive[i] = 2;
+}
+
+__global__ void k_mm_reset(Cand* cand, unsigned n, unsigned long long* best, const uint8_t* alive,
+                           Cand* next, unsigned* nnext) {
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  Cand c;
+  if (i < n) {
+    c = cand[i];
+    if (alive[i]) {
+      best[c.a] = NONE64;
+      best[c.b] = NONE64;
+    }
+    keep = alive[i] == 1;
+  }
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, keep);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(nnext, __popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (keep) next[base + __popc(mask & ((1u << lane) - 1))] = c;
+}
+
+__global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
+                               const uint32_t* __restrict__ parent, uint64_t* rec,
+                               unsigned long long* nrec, unsigned long long* nroots) {
+  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool emit = false;
+  uint32_t k = 0;
+  if (vv < g.nvox) {
+    uint32_t v = uint32_t(vv);
+    k = vox_kidx(g, v);
+    emit = parent[v] == v && births[k] != ABSENT_ORD;
+  }
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(nrec, (unsigned long long)__popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
+}
+
+__global__ void k_count_basins(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
+                               Geom g, const uint32_t* __restrict__ parent,
+                               unsigned long long* cnt) {
+  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool b = false;
+  if (vv < g.nvox) {
+    uint32_t k = vox_kidx(g, uint32_t(vv));
+    b = births[k] != ABSENT_ORD && tag_kind(tags[k]) != KIND_UP;
+  }
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, b);
+  if ((threadIdx.x & 31) == 0 && mask) atomicAdd(cnt, (unsigned long long)__popc(mask));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Output: records -> bars: keep death > birth or essential.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_bar_flags(const uint64_t* __restrict__ rec, int64_t n,
+                            const uint32_t* __restrict__ births, uint32_t* __restrict__ flag) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t r = rec[i];
+  uint32_t b = uint32_t(r >> 32), d = uint32_t(r);
+  flag[i] = (d == NONE32) || (births[d] > births[b]);
+}
+
+__global__ void k_bar_scatter(const uint64_t* __restrict__ rec, int64_t n,
+                              const uint32_t* __restrict__ births,
+                              const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                              int dim, int64_t base, int64_t cap, cr_pair* out,
+                              uint32_t* out_cells) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  int64_t o = base + pos[i];
+  if (o >= cap) return;
+  uint64_t r = rec[i];
+  uint32_t b = uint32_t(r >> 32), d = uint32_t(r);
+  cr_pair p;
+  p.dim = dim;
+  p.birth = float_of_ord(births[b]);
+  p.death = d == NONE32 ? __int_as_float(0x7F800000) : float_of_ord(births[d]);
+  out[o] = p;
+  if (out_cells) out_cells[o] = b;
+}
+
+__global__ void k_partner_init(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
+                               Geom g, uint32_t* __restrict__ partner) {
+  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (kk >= g.ncells) return;
+  uint32_t k = uint32_t(kk);
+  if (births[k] == ABSENT_ORD) {
+    partner[k] = CR_PARTNER_ABSENT;
+    return;
+  }
+  uint8_t t = tags[k];
+  uint8_t kind = tag_kind(t);
+  partner[k] = (kind == KIND_UP || kind == KIND_DOWN)
+                   ? uint32_t(int64_t(k) + dir_offset(g, tag_dir(t)))
+                   : CR_PARTNER_ESSENTIAL;
+}
+
+__global__ void k_partner_records(const uint64_t* __restrict__ rec, int64_t n,
+                                  uint32_t* __restrict__ partner) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t r = rec[i];
+  uint32_t b = uint32_t(r >> 32), d = uint32_t(r);
+  if (d != NONE32) {
+    partner[b] = d;
+    partner[d] = b;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, HostScalars& hs,
+                 GeneralState& S, cr_stats& st) {
+  cudaStream_t s = ws.stream();
+  S.g = g;
+  const int B = 256;
+  S.births = ws.alloc<uint32_t>(g.ncells);
+  S.tags = ws.alloc<uint8_t>(g.ncells);
+  unsigned long long* cnt = ws.alloc<unsigned long long>(32);
+  CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
+  int* nan_flag = reinterpret_cast<int*>(cnt + 31);
+
+  k_births<<<grid_for(g.nvox, B), B, 0, s>>>(image, g, S.births, nan_flag);
+  CR_CHECK_LAUNCH();
+  k_tags<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, S.tags, cnt + 0);
+  CR_CHECK_LAUNCH();
+  k_count_cells<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, cnt + 4);
+  CR_CHECK_LAUNCH();
+
+  // ---- H0
+  uint32_t* parent = ws.alloc<uint32_t>(g.nvox);
+  k_h0_parent<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent);
+  CR_CHECK_LAUNCH();
+  k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
+  CR_CHECK_LAUNCH();
+  k_count_basins<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
+  CR_CHECK_LAUNCH();
+
+  // NaN check + counts (one sync)
+  CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  if (*reinterpret_cast<int*>(hs.p + 31)) throw Error{CR_EINVAL, "NaN in image"};
+  for (int d = 0; d < 4; ++d) {
+    st.apparent[d] = int64_t(hs.p[d]);
+    st.cells[d] = int64_t(hs.p[4 + d]);
+  }
+  st.columns[0] = int64_t(hs.p[8]);
+  const int64_t nedges = st.cells[1];
+
+  Cand* cand = ws.alloc<Cand>(nedges);
+  Cand* cand2 = ws.alloc<Cand>(nedges);
+  unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
+  k_h0_edges<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
+  CR_CHECK_LAUNCH();
+  unsigned n = read_scalar(ncand, s, hs);
+
+  // vertex records: at most one per finite vertex
+  S.R.rec[0] = ws.alloc<uint64_t>(st.cells[0]);
+  unsigned long long* nrec0 = cnt + 13;
+  unsigned long long* best = ws.alloc<unsigned long long>(g.nvox);
+  CR_CUDA(cudaMemsetAsync(best, 0xFF, g.nvox * sizeof(unsigned long long), s));
+  uint8_t* alive = ws.alloc<uint8_t>(nedges);
+  unsigned* nnext = reinterpret_cast<unsigned*>(cnt + 14);
+  int64_t rounds = 0;
+  while (n > 0) {
+    k_mm_find<<<grid_for(n, B), B, 0, s>>>(cand, n, parent, best, alive);
+    CR_CHECK_LAUNCH();
+    k_mm_commit<<<grid_for(n, B), B, 0, s>>>(cand, n, S.births, g, parent, best, alive, S.tags,
+                                             S.R.rec[0], nrec0);
+    CR_CHECK_LAUNCH();
+    CR_CUDA(cudaMemsetAsync(nnext, 0, sizeof(unsigned), s));
+    k_mm_reset<<<grid_for(n, B), B, 0, s>>>(cand, n, best, alive, cand2, nnext);
+    CR_CHECK_LAUNCH();
+    std::swap(cand, cand2);
+    n = read_scalar(nnext, s, hs);
+    ++rounds;
+  }
+  st.rounds[0] = rounds;
+  // flatten once more so that roots are exact, then essential classes
+  k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
+  CR_CHECK_LAUNCH();
+  k_h0_essential<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
+                                                    nullptr);
+  CR_CHECK_LAUNCH();
+  S.R.n[0] = int64_t(read_scalar(nrec0, s, hs));
+  ws.release(cand);
+  ws.release(cand2);
+  ws.release(best);
+  ws.release(alive);
+  ws.release(parent);
+
+  for (int d = 1; d <= dmax; ++d) reduce_dimension(S, d, ws, hs, st);
+}
+
+int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out_cells,
+                  int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st) {
+  cudaStream_t s = ws.stream();
+  const int B = 256;
+  int64_t total = 0;
+  for (int d = 0; d <= maxdim && d < 4; ++d) {
+    int64_t n = S.R.n[d];
+    if (n == 0 || !S.R.rec[d]) continue;
+    sort_keys_u64(S.R.rec[d], n, false, 64, ws);
+    uint32_t* flag = ws.alloc<uint32_t>(n + 1);
+    uint32_t* pos = ws.alloc<uint32_t>(n + 1);
+    k_bar_flags<<<grid_for(n, B), B, 0, s>>>(S.R.rec[d], n, S.births, flag);
+    CR_CHECK_LAUNCH();
+    CR_CUDA(cudaMemsetAsync(flag + n, 0, sizeof(uint32_t), s));
+    exclusive_sum_u32(flag, pos, n + 1, ws);
+    uint32_t cnt = read_scalar(pos + n, s, hs);
+    k_bar_scatter<<<grid_for(n, B), B, 0, s>>>(S.R.rec[d], n, S.births, flag, pos, d, total, cap,
+                                               out, out_cells);
+    CR_CHECK_LAUNCH();
+    total += cnt;
+    ws.release(flag);
+    ws.release(pos);
+  }
+  return total;
+}
+
+void emit_partner(const GeneralState& S, uint32_t* partner, Workspace& ws) {
+  cudaStream_t s = ws.stream();
+  const int B = 256;
+  k_partner_init<<<grid_for(S.g.ncells, B), B, 0, s>>>(S.births, S.tags, S.g, partner);
+  CR_CHECK_LAUNCH();
+  for (int d = 0; d < 4; ++d)
+    if (S.R.n[d] > 0) {
+      k_partner_records<<<grid_for(S.R.n[d], B), B, 0, s>>>(S.R.rec[d], S.R.n[d], partner);
+      CR_CHECK_LAUNCH();
+    }
+}
+
+}  // namespace cr

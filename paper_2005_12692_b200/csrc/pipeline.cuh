@@ -1,0 +1,47 @@
+// pipeline.cuh -- host-side stages of the general (1D/2D/3D) path and the 1D path.
+#pragma once
+#include "workspace.cuh"
+
+namespace cr {
+
+// Pair records: (birth cell kidx << 32) | death cell kidx, death = NONE32 for essential classes.
+struct Records {
+  uint64_t* rec[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t n[4] = {0, 0, 0, 0};
+};
+
+struct GeneralState {
+  Geom g;
+  uint32_t* births = nullptr;  // ord(birth) per kidx, ABSENT_ORD for +inf
+  uint8_t* tags = nullptr;     // see cr_internal.cuh
+  Records R;
+};
+
+Geom make_geom(const int64_t* shape, int ndim);
+
+// K1 + K2 + H0 + reductions for dims 1..dmax (dmax <= D-1).  Throws Error.
+void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, HostScalars& hs,
+                 GeneralState& S, cr_stats& st);
+
+// Residual column reduction of dimension d (reduce.cu).  Appends records to R.rec[d].
+void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st);
+
+// Records (dims 0..maxdim) -> bars with death > birth plus essentials, ordered (dim, birth kidx).
+// Writes at most cap entries; returns the count needed.
+int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out_cells,
+                  int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st);
+
+// Full pairing from tags + records.
+void emit_partner(const GeneralState& S, uint32_t* partner, Workspace& ws);
+
+// 1D path (path1d.cu).  image has n voxels along one axis; cell kidx = 2i (vertex), 2i+1 (edge).
+int64_t barcodes_1d(const float* image, int64_t n, cr_pair* out, uint32_t* out_cells, int64_t cap,
+                    Workspace& ws, HostScalars& hs, cr_stats& st);
+void pairing_1d(const float* image, int64_t n, uint32_t* partner, Workspace& ws, HostScalars& hs,
+                cr_stats& st);
+
+// Device-wide helpers (util.cu).
+void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws);
+void exclusive_sum_u32(const uint32_t* in, uint32_t* out, int64_t n, Workspace& ws);
+
+}  // namespace cr

@@ -1,0 +1,45 @@
+// workspace.cuh -- stream-ordered scratch allocations and small host helpers.
+#pragma once
+#include <vector>
+
+#include "cr_internal.cuh"
+
+namespace cr {
+
+// All scratch is cudaMallocAsync'ed on the call's stream and freed (stream-ordered) on exit.
+// The device's default mempool keeps freed blocks (release threshold = max), so repeated
+// calls do not return memory to the driver.
+class Workspace {
+ public:
+  explicit Workspace(cudaStream_t s);
+  ~Workspace();
+  template <class T>
+  T* alloc(int64_t n) {
+    return static_cast<T*>(alloc_bytes(size_t(n < 1 ? 1 : n) * sizeof(T)));
+  }
+  void* alloc_bytes(size_t bytes);
+  void release(void* p);  // early stream-ordered free
+  cudaStream_t stream() const { return s_; }
+
+ private:
+  cudaStream_t s_;
+  std::vector<void*> ptrs_;
+};
+
+// Pinned host staging for small device->host reads.
+struct HostScalars {
+  HostScalars();
+  ~HostScalars();
+  unsigned long long* p;  // 64 entries
+};
+
+template <class T>
+inline T read_scalar(const T* dev, cudaStream_t s, HostScalars& hs) {
+  CR_CUDA(cudaMemcpyAsync(hs.p, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  T v;
+  memcpy(&v, hs.p, sizeof(T));
+  return v;
+}
+
+}  // namespace cr

@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar: bit-exact.  Every birth and death is an input value, so the (dim, birth, death) arrays --
+ordered by (dim, birth cell kidx) on both sides -- must be byte-identical, and so must the full
+cell pairing (partner array), whose tie-break both sides share (reading R1).
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import generators as gen
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def cr():
+    import torch
+    import paper_2005_12692_b200 as m
+    torch.cuda.init()
+    return m
+
+
+def gpu_bars(cr, img, maxdim):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(img, np.float32)).cuda()
+    bc = cr.barcodes(t, maxdim, cells=True)
+    d, b, e, c = bc.numpy()
+    return d, b, e, c
+
+
+def assert_bars_equal(g, o, ctx=""):
+    d, b, e, c = g
+    assert len(d) == len(o.dim), (ctx, len(d), len(o.dim))
+    assert np.array_equal(d, o.dim), ctx
+    assert np.array_equal(c, o.cell), ctx
+    assert np.array_equal(b.view(np.uint32), o.birth.view(np.uint32)), ctx
+    assert np.array_equal(e.view(np.uint32), o.death.view(np.uint32)), ctx
+
+
+def check_image(cr, img, maxdim, partner=True, ctx=""):
+    o = oracle.ph(img, maxdim, partner=partner)
+    assert_bars_equal(gpu_bars(cr, img, maxdim), o, ctx)
+    if partner:
+        import torch
+        p = cr.pairing(torch.from_numpy(np.ascontiguousarray(img, np.float32)).cuda())
+        gp = p.cpu().numpy().view(np.uint32)
+        assert np.array_equal(gp, o.partner), (ctx, np.flatnonzero(gp != o.partner)[:10])
+
+
+# ---------------------------------------------------------------- paper examples
+
+def test_golden_examples(cr):
+    for name in ["ttk_3x3.json", "fig2_h0.json"]:
+        g = json.load(open(os.path.join(GOLDEN, name)))
+        img = np.array(g["image"], np.float32)
+        d, b, e, _ = gpu_bars(cr, img, g["maxdim"])
+        got = sorted(zip(d.tolist(), b.tolist(), e.tolist()))
+        exp = sorted((int(x), float(y), float("inf") if z == "inf" else float(z)) for x, y, z in g["expected"])
+        assert got == exp, name
+        check_image(cr, img, g["maxdim"], ctx=name)
+
+
+def test_sin_example(cr):
+    x = np.linspace(0, 4 * np.pi, 100)
+    check_image(cr, (np.sin(x) + 0.1 * x).astype(np.float32), 1)
+
+
+# ---------------------------------------------------------------- exhaustive tiny sets
+
+def test_exhaustive_2x2_and_2x2x2(cr):
+    for vals in itertools.product([0, 1, 2], repeat=4):
+        check_image(cr, np.array(vals, np.float32).reshape(2, 2), 1, ctx=vals)
+    for vals in itertools.product([0, 1], repeat=8):
+        check_image(cr, np.array(vals, np.float32).reshape(2, 2, 2), 2, ctx=vals)
+
+
+def test_exhaustive_3x3_binary(cr):
+    for vals in itertools.product([0, 1], repeat=9):
+        check_image(cr, np.array(vals, np.float32).reshape(3, 3), 1, partner=False, ctx=vals)
+
+
+def test_fuzz_small_with_inf(cr):
+    rng = np.random.default_rng(777)
+    for t in range(300):
+        nd = int(rng.integers(1, 4))
+        shape = tuple(int(s) for s in rng.integers(1, 7 if nd < 3 else 5, size=nd))
+        img = gen.small_int_image(shape, 5, seed=int(rng.integers(1 << 30)),
+                                  inf_frac=0.2 if t % 2 else 0.0)
+        check_image(cr, img, 2, ctx=(t, shape))
+
+
+def test_general_path_on_1d(cr, monkeypatch):
+    """The general (K1/K2/H0) path and the 1D path agree with the oracle on 1D inputs."""
+    x = gen.random_walk(5000, seed=3)
+    x[[100, 101, 2500]] = np.inf
+    check_image(cr, x, 0, ctx="1d-path")
+    monkeypatch.setenv("CR_FORCE_GENERAL", "1")
+    check_image(cr, x, 0, ctx="general-path")
+    check_image(cr, x.reshape(1, -1), 1, ctx="general-path 1xN")
+
+
+# ---------------------------------------------------------------- configs (cropped / full)
+
+def test_c1_full(cr):
+    img, md = gen.config("c1")
+    check_image(cr, img, md, ctx="c1")
+
+
+def test_c2_cropped(cr):
+    for n in [1 << 12, (1 << 16) + 37]:
+        check_image(cr, gen.random_walk(n, seed=2), 0, ctx=n)
+
+
+def test_c3_subset_batched(cr):
+    import torch
+    imgs = gen.blobs(64, seed=3)
+    bc, off = cr.barcodes_batched(torch.from_numpy(imgs).cuda(), 1, cells=True)
+    d, b, e, c = bc.numpy()
+    off = off.cpu().numpy()
+    for i in range(len(imgs)):
+        o = oracle.ph(imgs[i], 1)
+        s = slice(off[i], off[i + 1])
+        assert_bars_equal((d[s], b[s], e[s], c[s]), o, ctx=i)
+        if i < 8:
+            check_image(cr, imgs[i], 1, ctx=("c3", i))
+
+
+def test_c4_cropped(cr):
+    v = gen.grf((40, 44, 36), 2.0, 4)
+    check_image(cr, v, 2, ctx="c4-crop")
+
+
+def test_c5_cropped_ball(cr):
+    v = gen.masked_grf((48, 48, 48), 3.0, 22.0, 5)
+    check_image(cr, v, 2, ctx="c5-crop")
+
+
+def test_batched_1d_and_3d(cr):
+    import torch
+    xs = np.stack([gen.small_int_image((9,), 3, seed=s) for s in range(50)])
+    bc, off = cr.barcodes_batched(torch.from_numpy(xs).cuda(), 0, cells=True)
+    d, b, e, c = bc.numpy()
+    off = off.cpu().numpy()
+    for i in range(len(xs)):
+        s = slice(off[i], off[i + 1])
+        assert_bars_equal((d[s], b[s], e[s], c[s]), oracle.ph(xs[i], 0), ctx=i)
+    vs = np.stack([gen.small_int_image((3, 4, 5), 4, seed=100 + s, inf_frac=0.1) for s in range(10)])
+    bc, off = cr.barcodes_batched(torch.from_numpy(vs).cuda(), 2, cells=True)
+    d, b, e, c = bc.numpy()
+    off = off.cpu().numpy()
+    for i in range(len(vs)):
+        s = slice(off[i], off[i + 1])
+        assert_bars_equal((d[s], b[s], e[s], c[s]), oracle.ph(vs[i], 2), ctx=i)
+
+
+def test_edge_cases(cr):
+    import torch
+    # single voxel, all +inf, -0.0, -inf, FLT_MAX
+    check_image(cr, np.array([[[5.0]]], np.float32), 2)
+    check_image(cr, np.full((3, 4), np.inf, np.float32), 1)
+    check_image(cr, np.array([[0.0, -0.0], [-0.0, 1.0]], np.float32), 1)
+    check_image(cr, np.array([[-np.inf, 1, 3.4e38], [2, -np.inf, 0]], np.float32), 1)
+    # NaN -> EINVAL
+    with pytest.raises(cr.CrError) as ei:
+        cr.barcodes(torch.tensor([1.0, float("nan")], device="cuda"), 0)
+    assert ei.value.status == cr.CR_EINVAL
+    with pytest.raises(cr.CrError) as ei:
+        cr.barcodes(torch.tensor([[1.0, float("nan")], [0.0, 2.0]], device="cuda"), 1)
+    assert ei.value.status == cr.CR_EINVAL
+    # capacity too small -> ERANGE with the needed count
+    t = torch.from_numpy(gen.iid_uniform((16, 16), 1)).cuda()
+    need = len(cr.barcodes(t, 1).pairs)
+    with pytest.raises(cr.CrError) as ei:
+        cr.barcodes(t, 1, capacity=need - 1)
+    assert ei.value.status == cr.CR_ERANGE
+
+
+def test_host_entry_point(cr):
+    img = gen.iid_uniform((40, 30), 9)
+    bc = cr.barcodes_host(img, 1, cells=True)
+    d, b, e, c = bc.numpy()
+    assert_bars_equal((d, b, e, c), oracle.ph(img, 1))

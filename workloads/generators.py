@@ -76,7 +76,8 @@ def grf(shape, sigma: float, seed: int | np.random.Generator) -> np.ndarray:
     grids = np.meshgrid(*freqs, indexing="ij", sparse=True)
     f2 = sum(g * g for g in grids)
     filt = np.exp(-2.0 * np.pi ** 2 * sigma ** 2 * f2)
-    out = np.fft.irfftn(np.fft.rfftn(w) * filt, s=shape)
+    axes = list(range(len(shape)))
+    out = np.fft.irfftn(np.fft.rfftn(w, axes=axes) * filt, s=shape, axes=axes)
     return out.astype(np.float32)
 
 
