@@ -116,9 +116,18 @@ typedef struct {
   int64_t rounds[4];      /* parallel rounds: H0 merge rounds in [0], reduction rounds in [d] */
   int64_t pairs[4];       /* bars with death > birth per dim                        */
   int64_t essential[4];   /* essential bars per dim                                 */
-  int64_t path;           /* 1 = 1D path, 2 = general path, 3 = batched small-image path */
+  int64_t path;           /* 1 = 1D path, 2 = general path, 3 = batched path           */
+  int32_t nstages;        /* stages timed (only when profiling is enabled)            */
+  float stage_ms[16];     /* device time of each stage, CUDA events on the call's stream */
+  char stage_name[16][24];
+  int64_t launches;       /* hand-written kernels launched by the call (CUB's not counted) */
 } cr_stats;
 void cr_last_stats(cr_stats* out);
+
+/* Enable (1) / disable (0) per-stage CUDA-event timing on this host thread (default off).
+ * When on, each call records an event after every pipeline stage on its stream and fills
+ * cr_stats.stage_ms / stage_name; the events add no synchronisation beyond the call's own. */
+void cr_set_profiling(int enable);
 
 #ifdef __cplusplus
 }

@@ -36,10 +36,17 @@ _i64p = ctypes.POINTER(ctypes.c_int64)
 class CrStats(ctypes.Structure):
     _fields_ = [("cells", _i64 * 4), ("apparent", _i64 * 4), ("columns", _i64 * 4),
                 ("rounds", _i64 * 4), ("pairs", _i64 * 4), ("essential", _i64 * 4),
-                ("path", _i64)]
+                ("path", _i64), ("nstages", ctypes.c_int32), ("stage_ms", ctypes.c_float * 16),
+                ("stage_name", (ctypes.c_char * 24) * 16), ("launches", _i64)]
 
     def as_dict(self):
-        return {f: (list(getattr(self, f)) if f != "path" else int(self.path)) for f, _ in self._fields_}
+        d = {f: list(getattr(self, f)) for f in ("cells", "apparent", "columns", "rounds", "pairs",
+                                                  "essential")}
+        d["path"] = int(self.path)
+        d["launches"] = int(self.launches)
+        d["stages"] = {self.stage_name[i].value.decode(): float(self.stage_ms[i])
+                       for i in range(int(self.nstages))}
+        return d
 
 
 _lib.cr_barcodes.restype = ctypes.c_int
@@ -59,9 +66,11 @@ _lib.cr_status_string.restype = ctypes.c_char_p
 _lib.cr_status_string.argtypes = [ctypes.c_int]
 _lib.cr_last_stats.restype = None
 _lib.cr_last_stats.argtypes = [ctypes.POINTER(CrStats)]
+_lib.cr_set_profiling.restype = None
+_lib.cr_set_profiling.argtypes = [ctypes.c_int]
 
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
-            "cr_num_cells", "cr_status_string", "cr_last_stats"]
+            "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling"]
 
 
 class CrError(RuntimeError):
@@ -91,6 +100,11 @@ def num_cells(shape) -> int:
     if n < 0:
         raise CrError(CR_EINVAL)
     return int(n)
+
+
+def set_profiling(enable: bool) -> None:
+    """Per-stage CUDA-event timing of subsequent calls on this thread (see cr_set_profiling)."""
+    _lib.cr_set_profiling(1 if enable else 0)
 
 
 def last_stats() -> dict:

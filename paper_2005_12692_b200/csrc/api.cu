@@ -8,6 +8,7 @@
 
 namespace cr {
 const char* last_error_text();
+void set_profiling(bool on);
 static thread_local cr_stats g_last_stats;
 
 namespace {
@@ -150,6 +151,8 @@ void cr_last_stats(cr_stats* out) {
   if (out) *out = g_last_stats;
 }
 
+void cr_set_profiling(int enable) { cr::set_profiling(enable != 0); }
+
 cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int maxdim,
                       cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
                       int64_t* n_pairs, cr_stream_t stream) {
@@ -162,6 +165,7 @@ cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int ma
     Workspace ws(s);
     HostScalars hs;
     cr_stats st{};
+    prof_begin(s);
     int64_t n;
     if (g.D <= 1 && !force_general()) {
       st.path = 1;
@@ -174,6 +178,7 @@ cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int ma
       n = emit_bars(S, dm, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
     }
     CR_CUDA(cudaStreamSynchronize(s));
+    prof_end(st);
     *n_pairs = n;
     if (n > out_capacity) return CR_ERANGE;
     g_last_stats = st;
@@ -256,6 +261,7 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
     HostScalars hs;
     cr_stats st{};
     st.path = 3;
+    prof_begin(s);
     float* simg = ws.alloc<float>(g.nvox);
     k_stack<<<grid_for(g.nvox, 256), 256, 0, s>>>(images, layers * layer, layer, layers, g.nvox,
                                                    simg);
@@ -303,9 +309,11 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
       CR_CHECK_LAUNCH();
     }
     exclusive_sum_u32(count, scan, batch + 1, ws);
+    prof_mark(s, "batch_emit");
     k_offsets<<<grid_for(batch + 1, 256), 256, 0, s>>>(scan, batch, nk, out_offsets);
     CR_CHECK_LAUNCH();
     CR_CUDA(cudaStreamSynchronize(s));
+    prof_end(st);
     *n_pairs = nk;
     if (int64_t(nk) > out_capacity) return CR_ERANGE;
     g_last_stats = st;

@@ -79,6 +79,11 @@ struct Error {
 };
 void set_error_text(const std::string& s);
 
+// Per-stage CUDA-event timing (thread-local, enabled by cr_set_profiling).
+void prof_begin(cudaStream_t s);
+void prof_mark(cudaStream_t s, const char* stage);  // the stage that just ended
+void prof_end(cr_stats& st);                         // after the call's final sync
+
 #define CR_CUDA(call)                                                                       \
   do {                                                                                      \
     cudaError_t e_ = (call);                                                                \
@@ -89,7 +94,12 @@ void set_error_text(const std::string& s);
     }                                                                                       \
   } while (0)
 
-#define CR_CHECK_LAUNCH() CR_CUDA(cudaGetLastError())
+extern thread_local int64_t g_launch_count;
+#define CR_CHECK_LAUNCH()                \
+  do {                                   \
+    CR_CUDA(cudaGetLastError());         \
+    ++::cr::g_launch_count;              \
+  } while (0)
 
 inline unsigned grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;

@@ -433,8 +433,10 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
 
   k_births<<<grid_for(g.nvox, B), B, 0, s>>>(image, g, S.births, nan_flag);
   CR_CHECK_LAUNCH();
+  prof_mark(s, "births");
   k_tags<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, S.tags, cnt + 0);
   CR_CHECK_LAUNCH();
+  prof_mark(s, "apparent");
   k_count_cells<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, cnt + 4);
   CR_CHECK_LAUNCH();
 
@@ -494,13 +496,18 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
                                                     nullptr);
   CR_CHECK_LAUNCH();
   S.R.n[0] = int64_t(read_scalar(nrec0, s, hs));
+  prof_mark(s, "h0");
   ws.release(cand);
   ws.release(cand2);
   ws.release(best);
   ws.release(alive);
   ws.release(parent);
 
-  for (int d = 1; d <= dmax; ++d) reduce_dimension(S, d, ws, hs, st);
+  static const char* names[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
+  for (int d = 1; d <= dmax; ++d) {
+    reduce_dimension(S, d, ws, hs, st);
+    prof_mark(s, names[d]);
+  }
 }
 
 int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out_cells,
@@ -523,9 +530,11 @@ int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out
                                                out, out_cells);
     CR_CHECK_LAUNCH();
     total += cnt;
+    st.pairs[d] = cnt;
     ws.release(flag);
     ws.release(pos);
   }
+  prof_mark(s, "emit");
   return total;
 }
 

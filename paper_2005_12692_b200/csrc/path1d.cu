@@ -320,6 +320,7 @@ void compress_and_solve(const float* x, int64_t n, Workspace& ws, HostScalars& h
   CR_CUDA(cudaMemsetAsync(cnt, 0, 2 * (nb + 1) * sizeof(uint32_t), s));
   k1_count<<<unsigned(nb), T1, 0, s>>>(x, n, cnt, cnt + nb + 1, nan_flag);
   CR_CHECK_LAUNCH();
+  prof_mark(s, "1d_count");
   exclusive_sum_u32(cnt, off, nb + 1, ws);
   exclusive_sum_u32(cnt + nb + 1, off + nb + 1, nb + 1, ws);
   CR_CUDA(cudaMemcpyAsync(hs.p, off + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
@@ -344,12 +345,14 @@ void compress_and_solve(const float* x, int64_t n, Workspace& ws, HostScalars& h
     ++levels;
   }
   if (levels > 40) throw Error{CR_EINTERNAL, "tree too deep"};
+  prof_mark(s, "1d_scan");
   C.bkey = ws.alloc<uint64_t>(K + total);
   C.mkey = ws.alloc<uint64_t>(K + total);
   C.bvert = ws.alloc<uint32_t>(K);
   C.medge = ws.alloc<uint32_t>(K);
   k1_scatter<<<unsigned(nb), T1, 0, s>>>(x, n, off, off + nb + 1, C.bkey, C.mkey, C.bvert, C.medge);
   CR_CHECK_LAUNCH();
+  prof_mark(s, "1d_scatter");
   Tree T;
   T.levels = levels;
   T.mn[0] = C.bkey;
@@ -365,9 +368,11 @@ void compress_and_solve(const float* x, int64_t n, Workspace& ws, HostScalars& h
     CR_CHECK_LAUNCH();
     o += T.size[l];
   }
+  prof_mark(s, "1d_tree");
   C.death = ws.alloc<uint64_t>(K);
   k1_deaths<<<grid_for(K, 256), 256, 0, s>>>(T, K, C.death);
   CR_CHECK_LAUNCH();
+  prof_mark(s, "1d_deaths");
 }
 
 }  // namespace
@@ -387,6 +392,7 @@ int64_t barcodes_1d(const float* x, int64_t n, cr_pair* out, uint32_t* out_cells
   k1_emit<<<grid_for(C.K, 256), 256, 0, s>>>(C.bkey, C.death, C.bvert, flag, pos, C.K, cap, out,
                                              out_cells);
   CR_CHECK_LAUNCH();
+  prof_mark(s, "1d_emit");
   uint32_t cnt = read_scalar(pos + C.K, s, hs);
   st.pairs[0] = cnt;
   return cnt;

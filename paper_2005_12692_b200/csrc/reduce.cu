@@ -402,6 +402,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       void* args[] = {&P};
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, 0, s));
+      ++g_launch_count;
       int e = read_scalar(err, s, hs);
       if (e == 0) break;
       if (e & 4) throw Error{CR_EINTERNAL, "reduction invariant violated"};

@@ -9,6 +9,64 @@ static thread_local std::string g_err_text;
 void set_error_text(const std::string& s) { g_err_text = s; }
 const char* last_error_text() { return g_err_text.c_str(); }
 
+namespace {
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  int used = 0;
+  std::vector<const char*> names;
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t next() {
+    if (used == int(pool.size())) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+thread_local Prof g_prof;
+}  // namespace
+
+thread_local int64_t g_launch_count = 0;
+
+void set_profiling(bool on) { g_prof.on = on; }
+
+void prof_begin(cudaStream_t s) {
+  g_launch_count = 0;
+  g_prof.used = 0;
+  g_prof.names.clear();
+  if (!g_prof.on) return;
+  cudaEvent_t e = g_prof.next();
+  if (e) cudaEventRecord(e, s);
+  g_prof.names.push_back("begin");
+}
+
+void prof_mark(cudaStream_t s, const char* stage) {
+  if (!g_prof.on || g_prof.names.empty()) return;
+  cudaEvent_t e = g_prof.next();
+  if (!e) return;
+  cudaEventRecord(e, s);
+  g_prof.names.push_back(stage);
+}
+
+void prof_end(cr_stats& st) {
+  st.launches = g_launch_count;
+  st.nstages = 0;
+  if (!g_prof.on) return;
+  int n = int(g_prof.names.size());
+  for (int i = 1; i < n && st.nstages < 16; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_prof.pool[i - 1], g_prof.pool[i]);
+    st.stage_ms[st.nstages] = ms;
+    strncpy(st.stage_name[st.nstages], g_prof.names[i], 23);
+    st.stage_name[st.nstages][23] = 0;
+    ++st.nstages;
+  }
+}
+
 Workspace::Workspace(cudaStream_t s) : s_(s) {
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) {
@@ -41,12 +99,23 @@ void Workspace::release(void* p) {
     }
 }
 
+namespace {
+// One pinned staging block per host thread, allocated on first use and kept for the life of the
+// thread (cudaMallocHost costs milliseconds; a per-call allocation dominated small calls).
+struct PinnedBlock {
+  unsigned long long* p = nullptr;
+  ~PinnedBlock() {
+    if (p) cudaFreeHost(p);
+  }
+};
+thread_local PinnedBlock g_pinned;
+}  // namespace
+
 HostScalars::HostScalars() : p(nullptr) {
-  CR_CUDA(cudaMallocHost(&p, 64 * sizeof(unsigned long long)));
+  if (!g_pinned.p) CR_CUDA(cudaMallocHost(&g_pinned.p, 64 * sizeof(unsigned long long)));
+  p = g_pinned.p;
 }
-HostScalars::~HostScalars() {
-  if (p) cudaFreeHost(p);
-}
+HostScalars::~HostScalars() {}
 
 void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws) {
   if (n <= 1) return;
