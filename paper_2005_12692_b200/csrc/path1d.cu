@@ -377,7 +377,7 @@ void compress_and_solve(const float* x, int64_t n, Workspace& ws, HostScalars& h
 
 }  // namespace
 
-int64_t barcodes_1d(const float* x, int64_t n, cr_pair* out, uint32_t* out_cells, int64_t cap,
+int64_t barcodes_1d_tree(const float* x, int64_t n, cr_pair* out, uint32_t* out_cells, int64_t cap,
                     Workspace& ws, HostScalars& hs, cr_stats& st) {
   cudaStream_t s = ws.stream();
   Compressed C;

@@ -1,5 +1,7 @@
 // pipeline.cuh -- host-side stages of the general (1D/2D/3D) path and the 1D path.
 #pragma once
+#include <cstdlib>
+
 #include "workspace.cuh"
 
 namespace cr {
@@ -35,8 +37,22 @@ int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out
 void emit_partner(const GeneralState& S, uint32_t* partner, Workspace& ws);
 
 // 1D path (path1d.cu).  image has n voxels along one axis; cell kidx = 2i (vertex), 2i+1 (edge).
-int64_t barcodes_1d(const float* image, int64_t n, cr_pair* out, uint32_t* out_cells, int64_t cap,
-                    Workspace& ws, HostScalars& hs, cr_stats& st);
+// Fused tile path (path1d_tiles.cu); returns -1 if its contraction levels did not finish
+// (adversarial inputs), in which case barcodes_1d falls back to the tree path (path1d.cu).
+int64_t barcodes_1d_tiles(const float* image, int64_t n, cr_pair* out, uint32_t* out_cells,
+                          int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st);
+int64_t barcodes_1d_tree(const float* image, int64_t n, cr_pair* out, uint32_t* out_cells,
+                         int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st);
+inline int64_t barcodes_1d(const float* image, int64_t n, cr_pair* out, uint32_t* out_cells,
+                           int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st) {
+  const char* e = std::getenv("CR_1D_TREE");
+  if (!(e && e[0] == '1')) {
+    int64_t r = barcodes_1d_tiles(image, n, out, out_cells, cap, ws, hs, st);
+    if (r >= 0) return r;
+    st.path = 4;  // tile levels did not converge: tree path
+  }
+  return barcodes_1d_tree(image, n, out, out_cells, cap, ws, hs, st);
+}
 void pairing_1d(const float* image, int64_t n, uint32_t* partner, Workspace& ws, HostScalars& hs,
                 cr_stats& st);
 

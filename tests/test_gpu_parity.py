@@ -186,3 +186,63 @@ def test_host_entry_point(cr):
     bc = cr.barcodes_host(img, 1, cells=True)
     d, b, e, c = bc.numpy()
     assert_bars_equal((d, b, e, c), oracle.ph(img, 1))
+
+
+# ---------------------------------------------------------------- 1D tile path edge cases
+
+def _series_cases():
+    rng = np.random.default_rng(99)
+    n = 3 * 4096 + 17
+    cases = {
+        "walk": gen.random_walk(5 * 4096 + 3, seed=11),
+        "stairs_up": (np.arange(n) // 2 + (np.arange(n) % 2) * 7.5).astype(np.float32),
+        "stairs_down": (-(np.arange(n) // 2) + (np.arange(n) % 2) * 7.5).astype(np.float32),
+        "monotone": np.arange(n, dtype=np.float32),
+        "monotone_down": -np.arange(n, dtype=np.float32),
+        "constant": np.zeros(n, np.float32),
+        "levels3": rng.integers(0, 3, n).astype(np.float32),
+        "plateaus": np.repeat(rng.integers(0, 6, n // 37 + 1), 37)[:n].astype(np.float32),
+        "one": np.array([4.0], np.float32),
+        "two": np.array([4.0, 1.0], np.float32),
+        "tile": gen.random_walk(4096, seed=3),
+        "tile_plus1": gen.random_walk(4097, seed=3),
+        # adversarial for tile contraction: minima getting older while barriers rise (every
+        # merge needs the far left), and minima getting younger while barriers rise
+        "adv_desc_min_asc_bar": np.where(np.arange(n) % 2 == 0, -np.arange(n),
+                                         np.arange(n)).astype(np.float32),
+        "adv_asc_min_asc_bar": np.where(np.arange(n) % 2 == 0, np.arange(n),
+                                        np.arange(n) + 100000).astype(np.float32),
+        # long plateau across tile boundaries: a basin undecided in its tile dies at zero
+        # persistence later (a hole in the staged output)
+        "plateau_across_tiles": np.concatenate([[5.0], np.full(9000, 3.0), [1.0], np.full(5000, 3.0),
+                                                [0.5]]).astype(np.float32),
+        "vee": np.abs(np.arange(n) - n // 2).astype(np.float32),
+        "peak": -np.abs(np.arange(n) - n // 2).astype(np.float32),
+    }
+    g = gen.random_walk(4 * 4096, seed=5)
+    g[[0, 4095, 4096, 8191, 8192, 9000, 9001, 9002, 16383]] = np.inf
+    cases["inf_at_tile_edges"] = g
+    h = gen.random_walk(20000, seed=6)
+    h[rng.random(20000) < 0.3] = np.inf
+    cases["inf_30pct"] = h
+    cases["all_inf"] = np.full(5000, np.inf, np.float32)
+    return cases
+
+
+@pytest.mark.parametrize("name", sorted(_series_cases()))
+def test_1d_tile_path_cases(cr, name):
+    x = _series_cases()[name]
+    check_image(cr, x, 0, partner=(len(x) < 20000), ctx=name)
+
+
+def test_1d_tile_vs_tree_large(cr, monkeypatch):
+    import torch
+    x = gen.random_walk(1 << 20, seed=8)
+    t = torch.from_numpy(x).cuda()
+    a = cr.barcodes(t, 0, cells=True).numpy()
+    assert cr.last_stats()["path"] == 1
+    monkeypatch.setenv("CR_1D_TREE", "1")
+    b = cr.barcodes(t, 0, cells=True).numpy()
+    for u, v in zip(a, b):
+        assert np.array_equal(np.asarray(u).view(np.uint32), np.asarray(v).view(np.uint32))
+    assert_bars_equal(a, oracle.ph(x, 0))
