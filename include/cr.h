@@ -121,6 +121,9 @@ typedef struct {
   float stage_ms[16];     /* device time of each stage, CUDA events on the call's stream */
   char stage_name[16][24];
   int64_t launches;       /* hand-written kernels launched by the call (CUB's not counted) */
+  int64_t additions[4];   /* column additions in the dim-d reduction                  */
+  int64_t addlen[4];      /* sum over additions of the working column length          */
+  int64_t maxlen[4];      /* longest working column in the dim-d reduction             */
 } cr_stats;
 void cr_last_stats(cr_stats* out);
 

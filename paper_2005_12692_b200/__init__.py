@@ -37,11 +37,12 @@ class CrStats(ctypes.Structure):
     _fields_ = [("cells", _i64 * 4), ("apparent", _i64 * 4), ("columns", _i64 * 4),
                 ("rounds", _i64 * 4), ("pairs", _i64 * 4), ("essential", _i64 * 4),
                 ("path", _i64), ("nstages", ctypes.c_int32), ("stage_ms", ctypes.c_float * 16),
-                ("stage_name", (ctypes.c_char * 24) * 16), ("launches", _i64)]
+                ("stage_name", (ctypes.c_char * 24) * 16), ("launches", _i64),
+                ("additions", _i64 * 4), ("addlen", _i64 * 4), ("maxlen", _i64 * 4)]
 
     def as_dict(self):
         d = {f: list(getattr(self, f)) for f in ("cells", "apparent", "columns", "rounds", "pairs",
-                                                  "essential")}
+                                                  "essential", "additions", "addlen", "maxlen")}
         d["path"] = int(self.path)
         d["launches"] = int(self.launches)
         d["stages"] = {self.stage_name[i].value.decode(): float(self.stage_ms[i])

@@ -345,6 +345,216 @@ __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
   if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
 }
 
+// ---- single-CTA variant for up to SMEM_BASINS basins: the same mutual-minimum rounds, with the
+// union-find forest and the per-component minimum in shared memory and __syncthreads between
+// phases (a round costs ~1 us instead of a host round trip).  Basins are renumbered by their rank
+// in elder order, so the elder of two roots is simply the smaller id; candidate edges are sorted
+// by key, so a component's minimum edge is the smallest edge index.
+constexpr int SMEM_BASINS = 56000;  // u32 union-find in <= 224 KB of shared memory; ranks < 2^16
+constexpr int H0_THREADS = 1024;
+
+__global__ void k_collect_roots(const uint32_t* __restrict__ births, Geom g,
+                                const uint32_t* __restrict__ parent, uint64_t* rootkey,
+                                unsigned* nroot) {
+  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool emit = false;
+  uint64_t key = 0;
+  if (vv < g.nvox) {
+    uint32_t v = uint32_t(vv);
+    uint32_t k = vox_kidx(g, v);
+    if (parent[v] == v && births[k] != ABSENT_ORD) {
+      emit = true;
+      key = make_key(births[k], k);
+    }
+  }
+  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
+  if (!mask) return;
+  int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(nroot, __popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (emit) rootkey[base + __popc(mask & ((1u << lane) - 1))] = key;
+}
+
+__global__ void k_rank_roots(const uint64_t* __restrict__ rootkey, unsigned nb, Geom g,
+                             uint32_t* rank_of) {
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nb) rank_of[kidx_vox(g, key_kidx(rootkey[i]))] = i;
+}
+
+__global__ void k_cand_pack(const Cand* __restrict__ cand, unsigned n,
+                            const uint32_t* __restrict__ rank_of, uint64_t* keys, uint32_t* ab) {
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Cand c = cand[i];
+  keys[i] = c.key;
+  ab[i] = (rank_of[c.a] << 16) | rank_of[c.b];
+}
+
+__device__ __forceinline__ uint32_t sfind(uint32_t* par, uint32_t x) {
+  while (true) {
+    const uint32_t p = par[x];
+    if (p == x) return x;
+    const uint32_t pp = par[p];
+    if (pp != p) par[x] = pp;  // path halving (benign under concurrency: both are ancestors)
+    x = pp;
+  }
+}
+
+// Boruvka on the basin graph (one CTA, union-find in shared memory): every component's minimum
+// edge is a minimum-spanning-forest edge (keys are distinct); components hook along them (of a
+// mutual pair only the larger id hooks) until no edge joins two components.  MSF edges are exactly
+// Kruskal's merge edges; the others close cycles (positive edges, dimension-1 columns).
+__global__ void __launch_bounds__(H0_THREADS) k_h0_boruvka(
+    const uint32_t* __restrict__ ab, unsigned n, unsigned nb, uint32_t* best, uint32_t* act0,
+    uint32_t* act1, uint32_t* hook, uint32_t* msf, unsigned* nmsf, unsigned long long* rounds_out) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* par = sh;
+  __shared__ unsigned s_nnext;
+  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) {
+    par[i] = i;
+    best[i] = 0xFFFFFFFFu;
+  }
+  for (unsigned i = threadIdx.x; i < n; i += H0_THREADS) act0[i] = i;
+  __syncthreads();
+  unsigned na = n;
+  uint32_t* act = act0;
+  uint32_t* nxt = act1;
+  unsigned long long rounds = 0;
+  while (na > 0) {
+    if (threadIdx.x == 0) s_nnext = 0;
+    __syncthreads();
+    for (unsigned t = threadIdx.x; t < na; t += H0_THREADS) {
+      const uint32_t e = act[t];
+      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
+      if (a == b) continue;  // closes a cycle: not an MSF edge
+      atomicMin(best + a, e);
+      atomicMin(best + b, e);
+      nxt[atomicAdd(&s_nnext, 1u)] = e;
+    }
+    __syncthreads();
+    // hook targets (computed before any hooking)
+    for (unsigned c = threadIdx.x; c < nb; c += H0_THREADS) {
+      uint32_t h = 0xFFFFFFFFu;
+      if (par[c] == c && best[c] != 0xFFFFFFFFu) {
+        const uint32_t e = best[c];
+        const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
+        const uint32_t o = a == c ? b : a;
+        if (!(best[o] == e && c < o)) h = o;  // of a mutual pair only the larger id hooks
+        if (best[o] != e || c < o) msf[atomicAdd(nmsf, 1u)] = e;  // record each edge once
+      }
+      hook[c] = h;
+    }
+    __syncthreads();
+    for (unsigned c = threadIdx.x; c < nb; c += H0_THREADS) {
+      if (hook[c] != 0xFFFFFFFFu) par[c] = hook[c];
+      best[c] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    na = s_nnext;
+    uint32_t* tmp = act;
+    act = nxt;
+    nxt = tmp;
+    ++rounds;
+  }
+  if (threadIdx.x == 0) *rounds_out = rounds;
+}
+
+// Elder-rule Kruskal over the MSF edges in key order (one thread; union-find in shared memory).
+__global__ void __launch_bounds__(H0_THREADS) k_h0_kruskal(
+    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ab,
+    const uint32_t* __restrict__ msf, unsigned nmsf, const uint64_t* __restrict__ rootkey,
+    unsigned nb, uint8_t* tags, uint64_t* rec, unsigned long long* nrec) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* par = sh;
+  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) par[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long r = *nrec;
+    for (unsigned t = 0; t < nmsf; ++t) {
+      const uint32_t e = msf[t];
+      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
+      const uint32_t young = a > b ? a : b, old = a > b ? b : a;  // elder = smaller rank
+      par[young] = old;
+      const uint32_t ke = key_kidx(keys[e]);
+      tags[ke] = make_tag(KIND_CLEARED, 0);
+      rec[r++] = (uint64_t(key_kidx(rootkey[young])) << 32) | ke;
+    }
+    *nrec = r;
+  }
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS)
+    if (par[i] == i) {
+      const unsigned long long r = atomicAdd(nrec, 1ull);
+      rec[r] = (uint64_t(key_kidx(rootkey[i])) << 32) | NONE32;
+    }
+}
+
+__global__ void __launch_bounds__(H0_THREADS) k_h0_smem(
+    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ab, unsigned n,
+    const uint64_t* __restrict__ rootkey, unsigned nb, uint32_t* act0, uint32_t* act1,
+    uint8_t* tags, uint64_t* rec, unsigned long long* nrec, unsigned long long* rounds_out) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* par = sh;
+  uint32_t* best = sh + nb;
+  __shared__ unsigned s_nnext;
+  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) {
+    par[i] = i;
+    best[i] = 0xFFFFFFFFu;
+  }
+  for (unsigned i = threadIdx.x; i < n; i += H0_THREADS) act0[i] = i;
+  __syncthreads();
+  unsigned na = n;
+  uint32_t* act = act0;
+  uint32_t* nxt = act1;
+  unsigned long long rounds = 0;
+  while (na > 0) {
+    // phase 1: components' minimum edges (edges inside one component are positive: dropped)
+    for (unsigned t = threadIdx.x; t < na; t += H0_THREADS) {
+      const uint32_t e = act[t];
+      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
+      if (a != b) {
+        atomicMin(best + a, e);
+        atomicMin(best + b, e);
+      }
+    }
+    if (threadIdx.x == 0) s_nnext = 0;
+    __syncthreads();
+    // phase 2: an edge minimal at both components is the next Kruskal merge there
+    for (unsigned t = threadIdx.x; t < na; t += H0_THREADS) {
+      const uint32_t e = act[t];
+      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
+      if (a == b) continue;  // positive edge
+      if (best[a] == e && best[b] == e) {
+        const uint32_t young = a > b ? a : b, old = a > b ? b : a;  // elder = smaller rank
+        par[young] = old;
+        const uint32_t ke = key_kidx(keys[e]);
+        tags[ke] = make_tag(KIND_CLEARED, 0);
+        const unsigned long long r = atomicAdd(nrec, 1ull);
+        rec[r] = (uint64_t(key_kidx(rootkey[young])) << 32) | ke;
+      } else {
+        nxt[atomicAdd(&s_nnext, 1u)] = e;
+      }
+    }
+    __syncthreads();
+    // phase 3: reset the minima; next round's active list
+    for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) best[i] = 0xFFFFFFFFu;
+    na = s_nnext;
+    uint32_t* tmp = act;
+    act = nxt;
+    nxt = tmp;
+    ++rounds;
+    __syncthreads();
+  }
+  // essential classes: the remaining roots
+  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS)
+    if (par[i] == i) {
+      const unsigned long long r = atomicAdd(nrec, 1ull);
+      rec[r] = (uint64_t(key_kidx(rootkey[i])) << 32) | NONE32;
+    }
+  if (threadIdx.x == 0) *rounds_out = rounds;
+}
+
 __global__ void k_count_basins(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                                Geom g, const uint32_t* __restrict__ parent,
                                unsigned long long* cnt) {
@@ -470,6 +680,75 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // vertex records: at most one per finite vertex
   S.R.rec[0] = ws.alloc<uint64_t>(st.cells[0]);
   unsigned long long* nrec0 = cnt + 13;
+  const unsigned nb = unsigned(st.columns[0]);
+  if (nb <= unsigned(SMEM_BASINS)) {
+    // few basins: shared-memory rounds in one CTA
+    uint64_t* rootkey = ws.alloc<uint64_t>(nb + 1);
+    unsigned* nroot = reinterpret_cast<unsigned*>(cnt + 15);
+    k_collect_roots<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, rootkey, nroot);
+    CR_CHECK_LAUNCH();
+    sort_keys_u64(rootkey, nb, false, 64, ws);
+    uint32_t* rank_of = ws.alloc<uint32_t>(g.nvox);
+    k_rank_roots<<<grid_for(nb, B), B, 0, s>>>(rootkey, nb, g, rank_of);
+    CR_CHECK_LAUNCH();
+    uint64_t* keys = ws.alloc<uint64_t>(n + 1);
+    uint32_t* ab = ws.alloc<uint32_t>(n + 1);
+    if (n > 0) {
+      k_cand_pack<<<grid_for(n, B), B, 0, s>>>(cand, n, rank_of, keys, ab);
+      CR_CHECK_LAUNCH();
+      uint64_t* k2 = ws.alloc<uint64_t>(n);
+      uint32_t* v2 = ws.alloc<uint32_t>(n);
+      cub::DoubleBuffer<uint64_t> dk(keys, k2);
+      cub::DoubleBuffer<uint32_t> dv(ab, v2);
+      size_t tmp = 0;
+      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 64, s));
+      void* t = ws.alloc_bytes(tmp);
+      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(n), 0, 64, s));
+      keys = dk.Current();
+      ab = dv.Current();
+    }
+    uint32_t* act0 = ws.alloc<uint32_t>(n + 1);
+    uint32_t* act1 = ws.alloc<uint32_t>(n + 1);
+    uint32_t* best32 = ws.alloc<uint32_t>(nb + 1);
+    uint32_t* hook = ws.alloc<uint32_t>(nb + 1);
+    uint32_t* msf = ws.alloc<uint32_t>(nb + 1);
+    unsigned* nmsf = reinterpret_cast<unsigned*>(cnt + 17);
+    const size_t smem = size_t(nb > 0 ? nb : 1) * 4;
+    CR_CUDA(cudaFuncSetAttribute(k_h0_boruvka, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    CR_CUDA(cudaFuncSetAttribute(k_h0_kruskal, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    k_h0_boruvka<<<1, H0_THREADS, smem, s>>>(ab, n, nb, best32, act0, act1, hook, msf, nmsf,
+                                             cnt + 16);
+    CR_CHECK_LAUNCH();
+    const unsigned nm = read_scalar(nmsf, s, hs);
+    if (nm > 1) {  // Kruskal order = edge index order (candidates are sorted by key)
+      uint32_t* m2 = ws.alloc<uint32_t>(nm);
+      cub::DoubleBuffer<uint32_t> dm(msf, m2);
+      size_t tmp = 0;
+      CR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, dm, int(nm), 0, 32, s));
+      void* t = ws.alloc_bytes(tmp);
+      CR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, dm, int(nm), 0, 32, s));
+      msf = dm.Current();
+    }
+    k_h0_kruskal<<<1, H0_THREADS, smem, s>>>(keys, ab, msf, nm, rootkey, nb, S.tags, S.R.rec[0],
+                                             nrec0);
+    CR_CHECK_LAUNCH();
+    CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    S.R.n[0] = int64_t(hs.p[0]);
+    st.rounds[0] = int64_t(hs.p[3]);
+    prof_mark(s, "h0");
+    ws.release(cand);
+    ws.release(cand2);
+    ws.release(parent);
+    static const char* names1[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
+    for (int d = 1; d <= dmax; ++d) {
+      reduce_dimension(S, d, ws, hs, st);
+      prof_mark(s, names1[d]);
+    }
+    return;
+  }
   unsigned long long* best = ws.alloc<unsigned long long>(g.nvox);
   CR_CUDA(cudaMemsetAsync(best, 0xFF, g.nvox * sizeof(unsigned long long), s));
   uint8_t* alive = ws.alloc<uint8_t>(nedges);

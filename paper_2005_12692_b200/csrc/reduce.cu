@@ -3,22 +3,29 @@
 // Columns are the finite d-cells that are neither apparent (K2) nor cleared (death cells of
 // dimension d-1), processed in DECREASING key order (the paper's order of
 // d-cells, "larger birth-time come first", with ties by kidx, reading R1).
-// A column is the coboundary delta(s) -- the finite cofacets of s -- kept as a sorted list of
-// (d+1)-cell keys; its pivot is the minimum key (the earliest coface).  While the pivot is owned,
-// the owner's column is added over Z/2 (symmetric difference):
+// A column is the coboundary delta(s) -- the finite cofacets of s -- as a set of (d+1)-cell keys;
+// its pivot is the minimum key (the earliest coface).  While the pivot is owned, the owner's
+// column is added over Z/2 (symmetric difference):
 //   - owner is apparent (the pivot t is the upper cell of an apparent pair (s', t)) -> add delta(s')
 //     enumerated on the fly (the implicit coboundary of PAPER.md:135-136);
 //   - owner is an earlier committed column -> add its stored reduced column.
 // A nonzero column with an unowned pivot t gives the pair (s, t): bar [birth s, birth t)
 // (PAPER.md:138-140); a zero column gives an essential class.
 //
-// Parallel schedule (one persistent cooperative kernel, one warp per window position): the
-// window holds the W columns lo..lo+W-1 (lo = first unfinished).  Each round every warp advances
-// its column by at most max_steps additions, publishing its current pivot cand(j) (a lower bound
-// of the final pivot: adding a column with the same pivot only moves the pivot later).  Column j
-// with an unowned pivot commits iff cand(j) < min{cand(i) : i < j unfinished}: no earlier column
-// can end on that pivot, so j's pivot is final, and any column committed while j is unfinished has
-// a pivot j can never reach -- the sequential reduction's pairs are reproduced exactly.
+// Working column (one warp per column): a sorted main array M in global memory plus a small
+// sorted "fresh" array F in shared memory, both consumed from the front (pivots only move later);
+// the column is M xor F, and equal heads cancel lazily when the pivot is taken.  Small addends
+// (apparent coboundaries, short stored columns) merge into F at O(|F|) cost; F is merged into M
+// only when it fills up, so a long column is not rewritten on every addition.
+//
+// Parallel schedule (one persistent cooperative kernel).  Warp w owns columns j = w (mod W), W =
+// resident warps; the window is the W columns lo..lo+W-1 (lo = first unfinished), one per warp.
+// Each round every warp advances its column by at most max_steps additions and publishes its
+// current pivot cand(j) at window position j - lo (a lower bound of its final pivot: adding a
+// column with the same pivot only moves the pivot later).  Column j with an unowned pivot commits
+// iff cand(j) < min{cand(i) : lo <= i < j}: no earlier column can end on that pivot, so j's pivot
+// is final, and any column committed while j is unfinished has a pivot j can never reach -- the
+// sequential reduction's pairs are reproduced exactly.
 #include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
@@ -29,6 +36,10 @@ namespace cg = cooperative_groups;
 
 namespace cr {
 namespace {
+
+constexpr int WPB = 8;  // warps per block
+constexpr int THREADS = WPB * 32;
+constexpr uint32_t FCAP = 256;  // fresh-array capacity per warp (shared memory, x2 ping-pong)
 
 struct RP {
   Geom g;
@@ -43,90 +54,91 @@ struct RP {
   unsigned long long pool_cap;
   unsigned long long* pool_off;
   uint32_t* pool_len;
-  uint64_t* work;
-  uint32_t work_cap;
-  uint32_t* slot_col;
-  uint32_t* slot_len;
-  uint32_t* slot_flags;  // bit0: current buffer, bit1: finished
-  uint64_t* cand;
-  uint64_t* blockmin;
-  unsigned* lo_buf;
+  uint64_t* work;      // per warp: 2 * mcap main-array entries
+  uint32_t mcap;
+  uint64_t* cand;      // per window position
+  uint64_t* chunkmin;  // per block (positions [WPB*b, WPB*b+WPB))
+  unsigned* lo_buf;    // [2]
   uint64_t* rec;
   unsigned long long* nrec;
   int* err;
   int max_steps;
-  unsigned long long* stats;  // [0] rounds, [1] additions
+  unsigned long long* stats;  // [0] rounds [1] additions [2] sum of lengths [3] max length
 };
 
-constexpr int WARPS_PER_BLOCK = 8;
-constexpr int THREADS = WARPS_PER_BLOCK * 32;
-
-__device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) { return __ldcg((const unsigned long long*)p); }
+__device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
+  return __ldcg((const unsigned long long*)p);
+}
+template <bool G>
+__device__ __forceinline__ uint64_t ld64(const uint64_t* p) {
+  return G ? ldcg64(p) : *p;
+}
 
 // Finite cofacets of cell s, sorted ascending, written to dst (<= 6 entries).  Warp-collective.
 __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
   const Geom& g = P.g;
-  uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  uint32_t c[3] = {s % KX, (s / KX) % KY, s / (KX * KY)};
-  uint32_t ext[3] = {KX, KY, uint32_t(g.KZ)};
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const uint32_t c[3] = {s % KX, (s / KX) % KY, s / (KX * KY)};
+  const uint32_t ext[3] = {KX, KY, uint32_t(g.KZ)};
   uint64_t key = NONE64;
   if (lane < 6) {
-    int a = lane >> 1, sg = lane & 1;
+    const int a = lane >> 1, sg = lane & 1;
     if (!(c[a] & 1) && (sg ? c[a] + 1 < ext[a] : c[a] > 0)) {
-      int64_t stv = g.stride(a);
-      uint32_t t = uint32_t(int64_t(s) + (sg ? stv : -stv));
-      uint32_t tb = __ldg(P.births + t);
+      const int64_t stv = g.stride(a);
+      const uint32_t t = uint32_t(int64_t(s) + (sg ? stv : -stv));
+      const uint32_t tb = __ldg(P.births + t);
       if (tb != ABSENT_ORD) key = make_key(tb, t);
     }
   }
-  unsigned valid = __ballot_sync(0xFFFFFFFFu, key != NONE64);
+  const unsigned valid = __ballot_sync(0xFFFFFFFFu, key != NONE64);
   int rank = 0;
-  for (int l = 0; l < 6; ++l) {
-    uint64_t o = __shfl_sync(0xFFFFFFFFu, key, l);
-    rank += (o < key);
-  }
+#pragma unroll
+  for (int l = 0; l < 6; ++l) rank += (__shfl_sync(0xFFFFFFFFu, key, l) < key);
   if (key != NONE64) dst[rank] = key;
   __syncwarp();
   return __popc(valid);
 }
 
-__device__ __forceinline__ uint32_t lower_bound(const uint64_t* B, uint32_t n, uint64_t x,
-                                                bool cg_load) {
+template <bool G>
+__device__ __forceinline__ uint32_t lower_bound(const uint64_t* B, uint32_t n, uint64_t x) {
   uint32_t lo = 0, hi = n;
   while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    uint64_t v = cg_load ? ldcg64(B + mid) : B[mid];
-    if (v < x) lo = mid + 1; else hi = mid;
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ld64<G>(B + mid) < x) lo = mid + 1;
+    else hi = mid;
   }
   return lo;
 }
 
-// C = A xor B (sorted, distinct entries each).  Warp-collective.  Returns |C|.
+// C = A xor B (sorted, distinct entries each), C distinct from A and B.  Warp-collective.
+// Output position of a kept A[i]: (#kept A before i) + (#kept B below A[i]); the number of common
+// values below A[i] equals the number of A's duplicates before i.
+template <bool AG, bool BG>
 __device__ uint32_t merge_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
-                                  bool b_cg, uint64_t* C, int lane) {
+                                  uint64_t* C, int lane) {
   const unsigned lt = (1u << lane) - 1;
   uint32_t carry = 0;
   for (uint32_t base = 0; base < a; base += 32) {
-    uint32_t i = base + lane;
-    bool valid = i < a;
-    uint64_t x = valid ? ldcg64(A + i) : 0;
-    uint32_t r = valid ? lower_bound(B, b, x, b_cg) : 0;
-    bool dup = valid && r < b && (b_cg ? ldcg64(B + r) : B[r]) == x;
-    unsigned m = __ballot_sync(0xFFFFFFFFu, dup);
-    uint32_t cb = carry + __popc(m & lt);
+    const uint32_t i = base + lane;
+    const bool valid = i < a;
+    const uint64_t x = valid ? ld64<AG>(A + i) : 0;
+    const uint32_t r = valid ? lower_bound<BG>(B, b, x) : 0;
+    const bool dup = valid && r < b && ld64<BG>(B + r) == x;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, dup);
+    const uint32_t cb = carry + __popc(m & lt);
     if (valid && !dup) C[(i - cb) + (r - cb)] = x;
     carry += __popc(m);
   }
   const uint32_t dups = carry;
   carry = 0;
   for (uint32_t base = 0; base < b; base += 32) {
-    uint32_t k = base + lane;
-    bool valid = k < b;
-    uint64_t x = valid ? (b_cg ? ldcg64(B + k) : B[k]) : 0;
-    uint32_t r = valid ? lower_bound(A, a, x, true) : 0;
-    bool dup = valid && r < a && ldcg64(A + r) == x;
-    unsigned m = __ballot_sync(0xFFFFFFFFu, dup);
-    uint32_t cb = carry + __popc(m & lt);
+    const uint32_t k = base + lane;
+    const bool valid = k < b;
+    const uint64_t x = valid ? ld64<BG>(B + k) : 0;
+    const uint32_t r = valid ? lower_bound<AG>(A, a, x) : 0;
+    const bool dup = valid && r < a && ld64<AG>(A + r) == x;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, dup);
+    const uint32_t cb = carry + __popc(m & lt);
     if (valid && !dup) C[(k - cb) + (r - cb)] = x;
     carry += __popc(m);
   }
@@ -134,141 +146,243 @@ __device__ uint32_t merge_symdiff(const uint64_t* A, uint32_t a, const uint64_t*
   return a + b - 2 * dups;
 }
 
+struct MinOp {
+  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
+    return a < b ? a : b;
+  }
+};
+typedef cub::BlockScan<uint64_t, THREADS> BScan;
+
+// The working column of a warp.
+struct Col {
+  uint64_t* M[2];  // global main arrays
+  uint64_t* F[2];  // shared fresh arrays
+  uint32_t mb, nm, h;
+  uint32_t fb, nf, f0;
+  uint64_t mhead;  // cached M[mb][h] (valid unless mstale)
+  bool mstale;
+  __device__ uint32_t len() const { return (nm - h) + (nf - f0); }
+};
+
+// pivot = min of (M[h:] xor F[f0:]), cancelling equal heads; NONE64 if the column is zero.
+// The head of M is cached in a register (mhead) and reloaded only when h moves or M changes.
+__device__ __forceinline__ uint64_t take_pivot(Col& c) {
+  while (true) {
+    if (c.mstale) {
+      c.mhead = c.h < c.nm ? ldcg64(c.M[c.mb] + c.h) : NONE64;
+      c.mstale = false;
+    }
+    const uint64_t a = c.mhead;
+    const uint64_t b = c.f0 < c.nf ? c.F[c.fb][c.f0] : NONE64;
+    if (a != b) return a < b ? a : b;
+    if (a == NONE64) return NONE64;
+    ++c.h;
+    ++c.f0;
+    c.mstale = true;
+  }
+}
+
+// M <- M[h:] xor F[f0:]   (returns false on capacity overflow)
+__device__ bool flush(Col& c, uint32_t mcap, int lane) {
+  const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
+  if (nb == 0) return true;
+  if (na + nb > mcap) return false;
+  const uint32_t n = merge_symdiff<true, false>(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
+                                                c.M[c.mb ^ 1], lane);
+  c.mb ^= 1;
+  c.nm = n;
+  c.h = 0;
+  c.nf = c.f0 = 0;
+  c.mstale = true;
+  return true;
+}
+
+// column += B (sorted; BG: B in global memory).  Returns false on capacity overflow.
+template <bool BG>
+__device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, uint32_t mcap, int lane) {
+  if ((c.nf - c.f0) + nb <= FCAP) {
+    const uint32_t n =
+        merge_symdiff<false, BG>(c.F[c.fb] + c.f0, c.nf - c.f0, B, nb, c.F[c.fb ^ 1], lane);
+    c.fb ^= 1;
+    c.nf = n;
+    c.f0 = 0;
+    return true;
+  }
+  if (!flush(c, mcap, lane)) return false;
+  if (nb <= FCAP) {  // F is empty now: B becomes F
+    for (uint32_t i = lane; i < nb; i += 32) c.F[c.fb][i] = ld64<BG>(B + i);
+    __syncwarp();
+    c.nf = nb;
+    c.f0 = 0;
+    return true;
+  }
+  if ((c.nm - c.h) + nb > mcap) return false;
+  const uint32_t n = merge_symdiff<true, BG>(c.M[c.mb] + c.h, c.nm - c.h, B, nb, c.M[c.mb ^ 1], lane);
+  c.mb ^= 1;
+  c.nm = n;
+  c.h = 0;
+  c.mstale = true;
+  return true;
+}
+
 __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ uint64_t s_small[WARPS_PER_BLOCK][8];
-  __shared__ uint64_t s_red[THREADS / 32];
-  __shared__ uint64_t s_wmin[WARPS_PER_BLOCK];
+  __shared__ uint64_t s_F[WPB][2][FCAP];
+  __shared__ uint64_t s_small[WPB][8];
+  __shared__ uint64_t s_pref[4 * THREADS];
+  __shared__ typename BScan::TempStorage s_scan;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t W = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t w = blockIdx.x * WARPS_PER_BLOCK + wib;
+  const uint32_t w = blockIdx.x * WPB + wib;
+  const uint32_t nblocks = gridDim.x;
+
+  Col c;
+  c.M[0] = P.work + uint64_t(w) * 2 * P.mcap;
+  c.M[1] = c.M[0] + P.mcap;
+  c.F[0] = s_F[wib][0];
+  c.F[1] = s_F[wib][1];
+  uint32_t j = w;
+  bool started = false, fin = false;
   uint32_t lo = 0;
-  const int sh = P.d;  // unused placeholder to keep P.d referenced
-  (void)sh;
 
   for (uint32_t round = 0;; ++round) {
-    // ---------------- phase A: advance my window position's column
-    const uint32_t j = lo + w;
+    // ---------------- phase A: advance my column
+    if (fin && j < lo) {
+      j += W;
+      started = false;
+      fin = false;
+    }
     uint64_t cval = NONE64;
-    bool ready = false, fin = true;
-    uint32_t len = 0, flags = 0, slot = 0;
-    uint64_t* wk = nullptr;
-    if (j < P.ncols) {
-      slot = j % W;
-      wk = P.work + uint64_t(slot) * 2 * P.work_cap;
-      const uint32_t scol = __ldcg(P.slot_col + slot);
-      if (scol != j) {  // a new column enters the window: its coboundary
-        uint32_t s = key_kidx(P.cols[j]);
-        len = coboundary(P, s, wk, lane);
-        flags = 0;
-        if (lane == 0) P.slot_col[slot] = j;
-      } else {
-        len = __ldcg(P.slot_len + slot);
-        flags = __ldcg(P.slot_flags + slot);
+    bool ready = false;
+    if (j < P.ncols && !fin) {
+      if (!started) {
+        started = true;
+        c.mb = c.fb = 0;
+        c.h = c.f0 = c.nm = 0;
+        c.mstale = true;
+        c.nf = coboundary(P, key_kidx(P.cols[j]), c.F[0], lane);
       }
-      fin = flags & 2;
-      if (!fin) {
-        int steps = 0;
-        unsigned long long adds = 0;
-        while (true) {
-          uint64_t* cur = wk + (flags & 1) * P.work_cap;
-          if (len == 0) break;
-          const uint64_t piv = ldcg64(cur);
-          const uint32_t pk = key_kidx(piv);
-          const uint8_t t = __ldg(P.tags + pk);
-          const uint64_t* add;
-          uint32_t alen;
-          bool add_cg;
-          if (tag_kind(t) == KIND_DOWN) {
-            // pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
-            uint32_t sp = uint32_t(int64_t(pk) + dir_offset(P.g, tag_dir(t)));
-            alen = coboundary(P, sp, s_small[wib], lane);
-            add = s_small[wib];
-            add_cg = false;
-          } else {
-            const uint32_t o = __ldcg(P.owner + pk);
-            if (o == NONE32) { ready = true; break; }
-            add = P.pool + __ldcg(P.pool_off + o);
-            alen = __ldcg(P.pool_len + o);
-            add_cg = true;
-          }
-          if (steps >= P.max_steps) break;
-          if (len + alen > P.work_cap) {
-            if (lane == 0) atomicOr(P.err, 1);
+      int steps = 0;
+      unsigned long long adds = 0, addlen = 0;
+      bool ok = true;
+      while (true) {
+        const uint64_t piv = take_pivot(c);
+        if (piv == NONE64) break;
+        const uint32_t pk = key_kidx(piv);
+        const uint8_t t = __ldg(P.tags + pk);
+        const uint64_t* add;
+        uint32_t alen;
+        bool glob;
+        if (tag_kind(t) == KIND_DOWN) {
+          // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
+          const uint32_t sp = uint32_t(int64_t(pk) + dir_offset(P.g, tag_dir(t)));
+          alen = coboundary(P, sp, s_small[wib], lane);
+          add = s_small[wib];
+          glob = false;
+        } else {
+          const uint32_t o = __ldcg(P.owner + pk);
+          if (o == NONE32) {
+            ready = true;
+            cval = piv;
             break;
           }
-          uint64_t* nxt = wk + ((flags & 1) ^ 1) * P.work_cap;
-          len = merge_symdiff(cur, len, add, alen, add_cg, nxt, lane);
-          flags ^= 1;
-          ++steps;
-          ++adds;
+          add = P.pool + __ldcg(P.pool_off + o);
+          alen = __ldcg(P.pool_len + o);
+          glob = true;
         }
-        if (lane == 0 && adds) atomicAdd(P.stats + 1, adds);
-        if (len == 0) {  // zero column: essential class (clearing makes this exact)
-          fin = true;
-          flags |= 2;
-          if (lane == 0) {
-            unsigned long long r = atomicAdd(P.nrec, 1ull);
-            P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | NONE32;
-          }
-        } else {
-          cval = ldcg64(wk + (flags & 1) * P.work_cap);
+        if (steps >= P.max_steps) {
+          cval = piv;
+          break;
+        }
+        addlen += c.len() + alen;
+        ok = glob ? add_column<true>(c, add, alen, P.mcap, lane)
+                  : add_column<false>(c, add, alen, P.mcap, lane);
+        if (!ok) {
+          if (lane == 0) atomicOr(P.err, 1);
+          break;
+        }
+        ++steps;
+        ++adds;
+      }
+      if (lane == 0 && adds) {
+        atomicAdd(P.stats + 1, adds);
+        atomicAdd(P.stats + 2, addlen);
+        atomicMax(P.stats + 3, (unsigned long long)c.len());
+      }
+      if (ok && !ready && cval == NONE64) {  // zero column: essential (exact given clearing)
+        fin = true;
+        if (lane == 0) {
+          const unsigned long long r = atomicAdd(P.nrec, 1ull);
+          P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | NONE32;
         }
       }
     }
-    if (lane == 0) P.cand[w] = fin ? NONE64 : cval;
-    // block min of the candidates (for the grid-wide prefix)
-    uint64_t mine = fin ? NONE64 : cval;
-    if (lane == 0) s_wmin[wib] = mine;
-    __syncthreads();
+    // publish at my window position (every position is owned by exactly one warp)
+    const uint32_t q = j - lo;
+    if (lane == 0 && q < W) P.cand[q] = (j < P.ncols && !fin) ? cval : NONE64;
+    grid.sync();
+
+    // ---------------- phase B: minima of the window's chunks of WPB positions
     if (threadIdx.x == 0) {
       uint64_t m = NONE64;
-      for (int q = 0; q < WARPS_PER_BLOCK; ++q) m = min(m, s_wmin[q]);
-      P.blockmin[blockIdx.x] = m;
+      for (int k = 0; k < WPB; ++k) m = min(m, ldcg64(P.cand + blockIdx.x * WPB + k));
+      P.chunkmin[blockIdx.x] = m;
     }
     grid.sync();
 
-    // ---------------- phase B: exclusive prefix-min over window positions < w
-    uint64_t pm = NONE64;
-    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += THREADS) pm = min(pm, (uint64_t)__ldcg((const unsigned long long*)P.blockmin + b));
-    for (int off = 16; off > 0; off >>= 1) pm = min(pm, __shfl_xor_sync(0xFFFFFFFFu, pm, off));
-    if (lane == 0) s_red[wib] = pm;
-    __syncthreads();
-    uint64_t prefix = NONE64;
-    for (int q = 0; q < WARPS_PER_BLOCK; ++q) prefix = min(prefix, s_red[q]);
-    for (int q = 0; q < wib; ++q) prefix = min(prefix, s_wmin[q]);
-
-    // ---------------- phase C: commit
-    if (j < P.ncols && !fin && ready && cval < prefix) {
-      uint64_t* cur = wk + (flags & 1) * P.work_cap;
-      unsigned long long off = 0;
-      if (lane == 0) off = atomicAdd(P.pool_top, (unsigned long long)len);
-      off = __shfl_sync(0xFFFFFFFFu, off, 0);
-      if (off + len > P.pool_cap) {
-        if (lane == 0) atomicOr(P.err, 2);
-      } else {
-        for (uint32_t i = lane; i < len; i += 32) P.pool[off + i] = ldcg64(cur + i);
-        if (lane == 0) {
-          P.pool_off[j] = off;
-          P.pool_len[j] = len;
-          __threadfence();
-          P.owner[key_kidx(cval)] = j;
-          unsigned long long r = atomicAdd(P.nrec, 1ull);
-          P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | key_kidx(cval);
-        }
-        fin = true;
-        flags |= 2;
+    // ---------------- phase C: exclusive prefix-min at my position, commit
+    {  // every block scans the chunk minima (nblocks <= 4 * THREADS) into s_pref
+      uint64_t v[4];
+      uint64_t tmin = NONE64;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t b = threadIdx.x * 4 + k;
+        v[k] = b < nblocks ? ldcg64(P.chunkmin + b) : NONE64;
+        tmin = min(tmin, v[k]);
+      }
+      uint64_t run;
+      BScan(s_scan).ExclusiveScan(tmin, run, NONE64, MinOp());
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t b = threadIdx.x * 4 + k;
+        if (b < nblocks) s_pref[b] = run;  // exclusive prefix of chunk b
+        run = min(run, v[k]);
       }
     }
-    if (j < P.ncols && lane == 0) {
-      P.slot_len[slot] = len;
-      P.slot_flags[slot] = flags;
+    __syncthreads();
+    if (j < P.ncols && !fin && ready && q < W) {
+      const uint32_t chunk = q / WPB;
+      uint64_t prefix = s_pref[chunk];
+      for (uint32_t k = chunk * WPB; k < q; ++k) prefix = min(prefix, ldcg64(P.cand + k));
+      if (cval < prefix) {
+        const uint32_t L = c.len();
+        unsigned long long off = 0;
+        if (lane == 0) off = atomicAdd(P.pool_top, (unsigned long long)L);
+        off = __shfl_sync(0xFFFFFFFFu, off, 0);
+        if (off + L > P.pool_cap) {
+          if (lane == 0) atomicOr(P.err, 2);
+        } else {
+          // reduced column = M[h:] xor F[f0:], written straight into the pool
+          const uint32_t n = merge_symdiff<true, false>(c.M[c.mb] + c.h, c.nm - c.h,
+                                                        c.F[c.fb] + c.f0, c.nf - c.f0,
+                                                        P.pool + off, lane);
+          if (lane == 0) {
+            P.pool_off[j] = off;
+            P.pool_len[j] = n;
+            __threadfence();
+            P.owner[key_kidx(cval)] = j;
+            const unsigned long long r = atomicAdd(P.nrec, 1ull);
+            P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | key_kidx(cval);
+          }
+          fin = true;
+        }
+      }
     }
-    // next lo = min(unfinished window column, lo + W)
+    // next lo = min(first unfinished window column, lo + W)
     if (lane == 0 && j < P.ncols && !fin) atomicMin(P.lo_buf + ((round + 1) & 1), j);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      uint64_t nl = uint64_t(lo) + W;
+      const uint64_t nl = uint64_t(lo) + W;
       atomicMin(P.lo_buf + ((round + 1) & 1), unsigned(nl < P.ncols ? nl : P.ncols));
       P.lo_buf[round & 1] = NONE32;
       atomicAdd(P.stats, 1ull);
@@ -342,37 +456,33 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     if (per_sm < 1) throw Error{CR_EINTERNAL, "k_reduce cannot be resident"};
     per_sm = per_sm > 4 ? 4 : per_sm;
     int64_t blocks = int64_t(nsm) * per_sm;
-    // do not launch more warps than columns (small problems)
-    int64_t need_blocks = (int64_t(ncols) + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+    const int64_t need_blocks = (int64_t(ncols) + WPB - 1) / WPB;  // small problems
     if (need_blocks < blocks) blocks = need_blocks;
-    const uint32_t W = uint32_t(blocks * WARPS_PER_BLOCK);
+    if (blocks > int64_t(THREADS) * 4) blocks = THREADS * 4;
+    const uint32_t W = uint32_t(blocks * WPB);
 
     uint32_t* owner = ws.alloc<uint32_t>(g.ncells);
     unsigned long long* pool_off = ws.alloc<unsigned long long>(ncols);
     uint32_t* pool_len = ws.alloc<uint32_t>(ncols);
-    uint32_t* slot_col = ws.alloc<uint32_t>(W);
-    uint32_t* slot_len = ws.alloc<uint32_t>(W);
-    uint32_t* slot_flags = ws.alloc<uint32_t>(W);
-    uint64_t* cand = ws.alloc<uint64_t>(W);
-    uint64_t* blockmin = ws.alloc<uint64_t>(blocks);
+    uint64_t* cand = ws.alloc<uint64_t>(W + blocks);
+    uint64_t* chunkmin = ws.alloc<uint64_t>(blocks);
     unsigned* lo_buf = reinterpret_cast<unsigned*>(ctr + 2);
     int* err = reinterpret_cast<int*>(ctr + 3);
     unsigned long long* nrec = ctr + 4;
     unsigned long long* pool_top = ctr + 5;
-    unsigned long long* stats = ctr + 6;  // [6] rounds [7] additions
+    unsigned long long* stats = ctr + 6;  // [6] rounds [7] additions [8] lengths [9] max length
 
-    uint32_t work_cap = 256;
-    unsigned long long pool_cap = std::max<unsigned long long>(4ull * ncols + 1024, 1ull << 20);
+    uint32_t mcap = 4096;
+    unsigned long long pool_cap = std::max<unsigned long long>(8ull * ncols + 4096, 1ull << 20);
     uint64_t* work = nullptr;
     uint64_t* pool = nullptr;
     for (int attempt = 0;; ++attempt) {
-      if (!work) work = ws.alloc<uint64_t>(int64_t(W) * 2 * work_cap);
+      if (!work) work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
       CR_CUDA(cudaMemsetAsync(owner, 0xFF, g.ncells * sizeof(uint32_t), s));
-      CR_CUDA(cudaMemsetAsync(slot_col, 0xFF, W * sizeof(uint32_t), s));
       CR_CUDA(cudaMemsetAsync(lo_buf, 0xFF, 2 * sizeof(unsigned), s));
       CR_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-      CR_CUDA(cudaMemsetAsync(nrec, 0, 4 * sizeof(unsigned long long), s));
+      CR_CUDA(cudaMemsetAsync(nrec, 0, 6 * sizeof(unsigned long long), s));
       RP P;
       P.g = g;
       P.d = d;
@@ -387,30 +497,26 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.pool_off = pool_off;
       P.pool_len = pool_len;
       P.work = work;
-      P.work_cap = work_cap;
-      P.slot_col = slot_col;
-      P.slot_len = slot_len;
-      P.slot_flags = slot_flags;
+      P.mcap = mcap;
       P.cand = cand;
-      P.blockmin = blockmin;
+      P.chunkmin = chunkmin;
       P.lo_buf = lo_buf;
       P.rec = S.R.rec[d];
       P.nrec = nrec;
       P.err = err;
-      P.max_steps = 64;
+      P.max_steps = 256;
       P.stats = stats;
       void* args[] = {&P};
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, 0, s));
       ++g_launch_count;
-      int e = read_scalar(err, s, hs);
+      const int e = read_scalar(err, s, hs);
       if (e == 0) break;
-      if (e & 4) throw Error{CR_EINTERNAL, "reduction invariant violated"};
       if (attempt > 12) throw Error{CR_ENOMEM, "reduction buffers exhausted"};
       if (e & 1) {
         ws.release(work);
         work = nullptr;
-        work_cap *= 4;
+        mcap *= 4;
       }
       if (e & 2) {
         ws.release(pool);
@@ -422,6 +528,9 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     CR_CUDA(cudaStreamSynchronize(s));
     S.R.n[d] = int64_t(hs.p[4]);
     st.rounds[d] = int64_t(hs.p[6]);
+    st.additions[d] = int64_t(hs.p[7]);
+    st.addlen[d] = int64_t(hs.p[8]);
+    st.maxlen[d] = int64_t(hs.p[9]);
     ws.release(work);
     ws.release(pool);
     ws.release(owner);
