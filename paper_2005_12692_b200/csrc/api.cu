@@ -267,6 +267,11 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
                                                    simg);
     CR_CHECK_LAUNCH();
     GeneralState S;
+    {  // Khalimsky cells per image period along the stacking axis: kidx / seg_cells = image
+      uint64_t cl = 1;
+      for (int i = 1; i < ndim; ++i) cl *= uint64_t(2 * shape[i] - 1);
+      S.seg_cells = uint32_t(cl * uint64_t(2 * (shape[0] + 1)));
+    }
     int dm = report_dmax(g1, maxdim);
     run_general(simg, g, dm, ws, hs, S, st);
     ws.release(simg);

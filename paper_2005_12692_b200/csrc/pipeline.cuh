@@ -16,6 +16,8 @@ struct GeneralState {
   Geom g;
   uint32_t* births = nullptr;  // ord(birth) per kidx, ABSENT_ORD for +inf
   uint8_t* tags = nullptr;     // see cr_internal.cuh
+  uint32_t seg_cells = 0;      // batched: Khalimsky cells per image period (kidx / seg_cells =
+                               // image); 0 for a single image
   Records R;
 };
 

@@ -58,12 +58,18 @@ struct RP {
   uint32_t mcap;
   uint64_t* cand;      // per window position
   uint64_t* chunkmin;  // per block (positions [WPB*b, WPB*b+WPB))
+  uint32_t* chunkflag; // per block: a segment starts inside the chunk
+  uint32_t* segpos;    // per window position: segment (image) of its column
+  uint32_t seg_cells;  // cells per segment (batched images), 0: one segment
   unsigned* lo_buf;    // [2]
   uint64_t* rec;
   unsigned long long* nrec;
   int* err;
   int max_steps;
   unsigned long long* stats;  // [0] rounds [1] additions [2] sum of lengths [3] max length
+                              // debug: [4] pool additions [5] pool lengths [7]/[8] cycles in
+                              // pool/apparent additions [9] cycles in pivot + owner lookups
+  int debug;
 };
 
 __device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
@@ -146,12 +152,62 @@ __device__ uint32_t merge_symdiff(const uint64_t* A, uint32_t a, const uint64_t*
   return a + b - 2 * dups;
 }
 
+// C = A xor B with A in global memory and B in global (BG) or shared memory, for long inputs:
+// merge-path chunks of <= CH elements are staged in shared memory (SA, SB: CH+1 entries each) and
+// merged there, so a long array is read once, coalesced, instead of one global binary search per
+// element.  Chunks split by the merge path with ties taken from A first; an equal pair split by a
+// chunk boundary is kept together by taking B's copy into the chunk too.
+template <bool BG>
+__device__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
+                                  uint64_t* C, uint64_t* SA, uint64_t* SB, int lane) {
+  constexpr uint32_t CH = FCAP - 1;
+  uint32_t i0 = 0, j0 = 0, out = 0;
+  while (i0 < a || j0 < b) {
+    const uint32_t ra = a - i0, rb = b - j0;
+    const uint32_t k = ra + rb < CH ? ra + rb : CH;
+    uint32_t i = 0;
+    if (lane == 0) {
+      uint32_t lo = k > rb ? k - rb : 0, hi = k < ra ? k : ra;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ldcg64(A + i0 + mid) <= ld64<BG>(B + j0 + k - mid - 1)) lo = mid + 1;
+        else hi = mid;
+      }
+      i = lo;
+    }
+    i = __shfl_sync(0xFFFFFFFFu, i, 0);
+    uint32_t j = k - i;
+    if (i > 0 && j < rb && ldcg64(A + i0 + i - 1) == ld64<BG>(B + j0 + j)) ++j;
+    for (uint32_t t = lane; t < i; t += 32) SA[t] = ldcg64(A + i0 + t);
+    const uint64_t* Bc = B + j0;
+    if (BG) {
+      for (uint32_t t = lane; t < j; t += 32) SB[t] = ldcg64(B + j0 + t);
+      Bc = SB;
+    }
+    __syncwarp();
+    out += merge_symdiff<false, false>(SA, i, Bc, j, C + out, lane);
+    i0 += i;
+    j0 += j;
+  }
+  return out;
+}
+
 struct MinOp {
   __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
     return a < b ? a : b;
   }
 };
-typedef cub::BlockScan<uint64_t, THREADS> BScan;
+// segmented minimum: (value, starts-a-segment) pairs
+struct SegMin {
+  uint64_t v;
+  uint32_t f;
+};
+struct SegOp {
+  __device__ __forceinline__ SegMin operator()(const SegMin& a, const SegMin& b) const {
+    return SegMin{b.f ? b.v : (a.v < b.v ? a.v : b.v), a.f | b.f};
+  }
+};
+typedef cub::BlockScan<SegMin, THREADS> SScan;
 
 // The working column of a warp.
 struct Col {
@@ -187,8 +243,8 @@ __device__ bool flush(Col& c, uint32_t mcap, int lane) {
   const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
   if (nb == 0) return true;
   if (na + nb > mcap) return false;
-  const uint32_t n = merge_symdiff<true, false>(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
-                                                c.M[c.mb ^ 1], lane);
+  const uint32_t n = merge_chunked<false>(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
+                                          c.M[c.mb ^ 1], c.F[c.fb ^ 1], nullptr, lane);
   c.mb ^= 1;
   c.nm = n;
   c.h = 0;
@@ -217,7 +273,8 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, uint32_t mcap
     return true;
   }
   if ((c.nm - c.h) + nb > mcap) return false;
-  const uint32_t n = merge_symdiff<true, BG>(c.M[c.mb] + c.h, c.nm - c.h, B, nb, c.M[c.mb ^ 1], lane);
+  const uint32_t n = merge_chunked<BG>(c.M[c.mb] + c.h, c.nm - c.h, B, nb, c.M[c.mb ^ 1],
+                                       c.F[0], c.F[1], lane);
   c.mb ^= 1;
   c.nm = n;
   c.h = 0;
@@ -230,7 +287,7 @@ __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
   __shared__ uint64_t s_F[WPB][2][FCAP];
   __shared__ uint64_t s_small[WPB][8];
   __shared__ uint64_t s_pref[4 * THREADS];
-  __shared__ typename BScan::TempStorage s_scan;
+  __shared__ typename SScan::TempStorage s_scan;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t W = (gridDim.x * blockDim.x) >> 5;
@@ -267,6 +324,7 @@ __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
       unsigned long long adds = 0, addlen = 0;
       bool ok = true;
       while (true) {
+        const long long tl0 = P.debug ? clock64() : 0;
         const uint64_t piv = take_pivot(c);
         if (piv == NONE64) break;
         const uint32_t pk = key_kidx(piv);
@@ -296,8 +354,20 @@ __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
           break;
         }
         addlen += c.len() + alen;
+        const long long t0 = clock64();
+        if (P.debug && lane == 0) atomicAdd(P.stats + 9, (unsigned long long)(t0 - tl0));
         ok = glob ? add_column<true>(c, add, alen, P.mcap, lane)
                   : add_column<false>(c, add, alen, P.mcap, lane);
+        if (P.debug && lane == 0) {
+          const unsigned long long dt = (unsigned long long)(clock64() - t0);
+          if (glob) {
+            atomicAdd(P.stats + 4, 1ull);
+            atomicAdd(P.stats + 5, (unsigned long long)alen);
+            atomicAdd(P.stats + 7, dt);
+          } else {
+            atomicAdd(P.stats + 8, dt);
+          }
+        }
         if (!ok) {
           if (lane == 0) atomicOr(P.err, 1);
           break;
@@ -318,43 +388,61 @@ __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
         }
       }
     }
-    // publish at my window position (every position is owned by exactly one warp)
+    // publish at my window position (every position is owned by exactly one warp), with the
+    // segment (image of a batch) of the column: columns of different images never interact, so
+    // a column is blocked only by unfinished earlier columns of its own segment
     const uint32_t q = j - lo;
-    if (lane == 0 && q < W) P.cand[q] = (j < P.ncols && !fin) ? cval : NONE64;
-    grid.sync();
-
-    // ---------------- phase B: minima of the window's chunks of WPB positions
-    if (threadIdx.x == 0) {
-      uint64_t m = NONE64;
-      for (int k = 0; k < WPB; ++k) m = min(m, ldcg64(P.cand + blockIdx.x * WPB + k));
-      P.chunkmin[blockIdx.x] = m;
+    if (lane == 0 && q < W) {
+      P.cand[q] = (j < P.ncols && !fin) ? cval : NONE64;
+      P.segpos[q] = (j < P.ncols && P.seg_cells) ? key_kidx(P.cols[j]) / P.seg_cells : 0xFFFFFFFFu;
     }
     grid.sync();
 
-    // ---------------- phase C: exclusive prefix-min at my position, commit
-    {  // every block scans the chunk minima (nblocks <= 4 * THREADS) into s_pref
-      uint64_t v[4];
-      uint64_t tmin = NONE64;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t b = threadIdx.x * 4 + k;
-        v[k] = b < nblocks ? ldcg64(P.chunkmin + b) : NONE64;
-        tmin = min(tmin, v[k]);
+    // ---------------- phase B: segmented minima of the window's chunks of WPB positions
+    if (threadIdx.x == 0) {
+      uint64_t m = NONE64;
+      uint32_t f = 0;
+      for (int k = 0; k < WPB; ++k) {
+        const uint32_t p = blockIdx.x * WPB + k;
+        if (p == 0 || __ldcg(P.segpos + p) != __ldcg(P.segpos + p - 1)) {
+          m = NONE64;  // a segment starts here
+          f = 1;
+        }
+        m = min(m, ldcg64(P.cand + p));
       }
-      uint64_t run;
-      BScan(s_scan).ExclusiveScan(tmin, run, NONE64, MinOp());
+      P.chunkmin[blockIdx.x] = m;
+      P.chunkflag[blockIdx.x] = f;
+    }
+    grid.sync();
+
+    // ---------------- phase C: exclusive segmented prefix-min at my position, commit
+    {  // every block scans the chunk aggregates (nblocks <= 4 * THREADS) into s_pref
+      SegMin v[4];
+      SegMin t{NONE64, 0};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t b = threadIdx.x * 4 + k;
-        if (b < nblocks) s_pref[b] = run;  // exclusive prefix of chunk b
-        run = min(run, v[k]);
+        v[k] = b < nblocks ? SegMin{ldcg64(P.chunkmin + b), __ldcg(P.chunkflag + b)}
+                           : SegMin{NONE64, 0};
+        t = SegOp()(t, v[k]);
+      }
+      SegMin run;
+      SScan(s_scan).ExclusiveScan(t, run, SegMin{NONE64, 0}, SegOp());
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t b = threadIdx.x * 4 + k;
+        if (b < nblocks) s_pref[b] = run.v;  // min over my segment's positions before chunk b
+        run = SegOp()(run, v[k]);
       }
     }
     __syncthreads();
     if (j < P.ncols && !fin && ready && q < W) {
       const uint32_t chunk = q / WPB;
       uint64_t prefix = s_pref[chunk];
-      for (uint32_t k = chunk * WPB; k < q; ++k) prefix = min(prefix, ldcg64(P.cand + k));
+      for (uint32_t k = chunk * WPB; k <= q; ++k) {
+        if (k == 0 || __ldcg(P.segpos + k) != __ldcg(P.segpos + k - 1)) prefix = NONE64;
+        if (k < q) prefix = min(prefix, ldcg64(P.cand + k));
+      }
       if (cval < prefix) {
         const uint32_t L = c.len();
         unsigned long long off = 0;
@@ -364,9 +452,9 @@ __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
           if (lane == 0) atomicOr(P.err, 2);
         } else {
           // reduced column = M[h:] xor F[f0:], written straight into the pool
-          const uint32_t n = merge_symdiff<true, false>(c.M[c.mb] + c.h, c.nm - c.h,
-                                                        c.F[c.fb] + c.f0, c.nf - c.f0,
-                                                        P.pool + off, lane);
+          const uint32_t n = merge_chunked<false>(c.M[c.mb] + c.h, c.nm - c.h, c.F[c.fb] + c.f0,
+                                                  c.nf - c.f0, P.pool + off, c.F[c.fb ^ 1],
+                                                  nullptr, lane);
           if (lane == 0) {
             P.pool_off[j] = off;
             P.pool_len[j] = n;
@@ -420,6 +508,12 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
   if (emit) cols[base + __popc(mask & ((1u << lane) - 1))] = key;
 }
 
+__global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32_t seg_cells,
+                           uint32_t* __restrict__ segk) {
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) segk[i] = key_kidx(cols[i]) / seg_cells;
+}
+
 __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint8_t* tags) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -448,6 +542,24 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
   st.columns[d] = ncols;
   if (ncols > 0) {
     sort_keys_u64(cols, ncols, /*descending=*/true, 64, ws);
+    if (S.seg_cells) {
+      // batched images: group the columns by image (stable, so each image keeps its decreasing
+      // key order); images are independent complexes, so their relative order is immaterial
+      uint32_t* segk = ws.alloc<uint32_t>(ncols);
+      uint32_t* segk2 = ws.alloc<uint32_t>(ncols);
+      uint64_t* cols2 = ws.alloc<uint64_t>(ncols);
+      k_seg_keys<<<grid_for(ncols, B), B, 0, s>>>(cols, ncols, S.seg_cells, segk);
+      CR_CHECK_LAUNCH();
+      cub::DoubleBuffer<uint32_t> dk(segk, segk2);
+      cub::DoubleBuffer<uint64_t> dv(cols, cols2);
+      size_t tmp = 0;
+      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(ncols), 0, 32, s));
+      void* t = ws.alloc_bytes(tmp);
+      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(ncols), 0, 32, s));
+      if (dv.Current() != cols)
+        CR_CUDA(cudaMemcpyAsync(cols, dv.Current(), ncols * sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, s));
+    }
 
     int dev = 0, nsm = 0, per_sm = 0;
     CR_CUDA(cudaGetDevice(&dev));
@@ -466,6 +578,8 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     uint32_t* pool_len = ws.alloc<uint32_t>(ncols);
     uint64_t* cand = ws.alloc<uint64_t>(W + blocks);
     uint64_t* chunkmin = ws.alloc<uint64_t>(blocks);
+    uint32_t* chunkflag = ws.alloc<uint32_t>(blocks);
+    uint32_t* segpos = ws.alloc<uint32_t>(W);
     unsigned* lo_buf = reinterpret_cast<unsigned*>(ctr + 2);
     int* err = reinterpret_cast<int*>(ctr + 3);
     unsigned long long* nrec = ctr + 4;
@@ -500,12 +614,16 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.mcap = mcap;
       P.cand = cand;
       P.chunkmin = chunkmin;
+      P.chunkflag = chunkflag;
+      P.segpos = segpos;
+      P.seg_cells = S.seg_cells;
       P.lo_buf = lo_buf;
       P.rec = S.R.rec[d];
       P.nrec = nrec;
       P.err = err;
       P.max_steps = 256;
       P.stats = stats;
+      P.debug = std::getenv("CR_DEBUG_STATS") != nullptr;
       void* args[] = {&P};
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, 0, s));
@@ -531,6 +649,11 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     st.additions[d] = int64_t(hs.p[7]);
     st.addlen[d] = int64_t(hs.p[8]);
     st.maxlen[d] = int64_t(hs.p[9]);
+    if (std::getenv("CR_DEBUG_STATS"))
+      fprintf(stderr,
+              "[cr] dim %d: cols %u rounds %llu adds %llu pool_adds %llu pool_len %llu "
+              "cyc_pool %llu cyc_app %llu cyc_lookup %llu W %u\n",
+              d, ncols, hs.p[6], hs.p[7], hs.p[10], hs.p[11], hs.p[13], hs.p[14], hs.p[15], W);
     ws.release(work);
     ws.release(pool);
     ws.release(owner);
