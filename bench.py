@@ -112,14 +112,15 @@ class ClockSampler:
 
 def make_input(cfg: str, rank: int, world: int):
     from workloads import generators as gen
+    from paper_2005_12692_b200.dist import shard_range
     if cfg == "c3":
         imgs = gen.blobs(65536, 3)
-        per = (len(imgs) + world - 1) // world
-        return imgs[rank * per:(rank + 1) * per], 1, len(imgs)
+        a, b = shard_range(len(imgs), rank, world)
+        return imgs[a:b], 1, len(imgs)
     if cfg == "c5b":
         vols, md = gen.config("c5b")
-        per = (len(vols) + world - 1) // world
-        return vols[rank * per:(rank + 1) * per], md, len(vols)
+        a, b = shard_range(len(vols), rank, world)
+        return vols[a:b], md, len(vols)
     img, md = gen.config(cfg)
     return img, md, 1
 
@@ -155,7 +156,12 @@ def run_ours(args, rank, world, local_rank):
                                              offsets.data_ptr(), ctypes.byref(n),
                                              ctypes.c_void_p(stream.cuda_stream))
             cr._check(st)
-            return int(n.value)
+            m = int(n.value)
+            if world > 1:  # the job ends with every shard's barcodes gathered in input order
+                from paper_2005_12692_b200.dist import gather_barcodes
+                p_all, _ = gather_barcodes(pairs[:m], offsets)
+                return int(p_all.shape[0])
+            return m
         return len(cr.barcodes(img, maxdim, out=(pairs, None)).pairs)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
@@ -275,6 +281,10 @@ def algorithmic_bytes(cfg, stage, nvox, st, n_out):
     K = st["columns"][0]
     if stage is None:
         return None
+    if stage == "1d_level1":
+        return 4 * nvox + 12 * n_out              # read the series, stage one 12-B bar per output bar
+    if stage == "1d_gather":
+        return 24 * n_out                         # read staged bars, write the output
     if stage.startswith("1d_count"):
         return 4 * nvox                           # read x
     if stage.startswith("1d_scatter"):
