@@ -116,7 +116,8 @@ typedef struct {
   int64_t rounds[4];      /* parallel rounds: H0 merge rounds in [0], reduction rounds in [d] */
   int64_t pairs[4];       /* bars with death > birth per dim                        */
   int64_t essential[4];   /* essential bars per dim                                 */
-  int64_t path;           /* 1 = 1D path, 2 = general path, 3 = batched path           */
+  int64_t path;           /* 1 = 1D tiles, 2 = general, 3 = batched (stacked), 4 = 1D tree,
+                             5 = batched small 2D (one CTA per image)                    */
   int32_t nstages;        /* stages timed (only when profiling is enabled)            */
   float stage_ms[16];     /* device time of each stage, CUDA events on the call's stream */
   char stage_name[16][24];

@@ -245,6 +245,25 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
       *n_pairs = 0;
       return CR_OK;
     }
+    if (g1.nz == 1 && batched_small_2d_fits(g1.ny, g1.nx) && !force_general()) {
+      // small 2D images: one CTA per image, everything in shared memory
+      Workspace ws(s);
+      HostScalars hs;
+      cr_stats st{};
+      st.path = 5;
+      prof_begin(s);
+      const int64_t n = barcodes_batched_small_2d(images, batch, g1.ny, g1.nx, maxdim, out_pairs,
+                                                  out_birth_cells, out_capacity, out_offsets, ws,
+                                                  hs, st);
+      if (n >= 0) {
+        CR_CUDA(cudaStreamSynchronize(s));
+        prof_end(st);
+        *n_pairs = n;
+        if (n > out_capacity) return CR_ERANGE;
+        g_last_stats = st;
+        return CR_OK;
+      }
+    }
     // Stack the images along their own slowest axis with one +inf separator layer between
     // consecutive images: the stacked complex is the disjoint union of the images' complexes
     // (every cell touching a separator is absent, reading R5), so its bars are theirs.

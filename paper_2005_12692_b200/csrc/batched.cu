@@ -1,0 +1,462 @@
+// batched.cu -- K7: the whole pipeline for one small 2D image per CTA, in shared memory
+// (batches of MNIST-like images, BASELINE config 3).  Same mathematics and the same total order as
+// the device-wide path (general.cu / reduce.cu), so both give identical pairings:
+//   births -> apparent pairs -> H0 by union-find with the elder rule over the
+//   residual edges in key order -> dimension-1 coboundary reduction with clearing over
+//   the residual, uncleared edges in decreasing key order -> bars in (dim, birth kidx)
+//   order into a per-image staging region.
+// Each image is independent, so a CTA never waits for another; a final gather copies the staged
+// bars to the output at the scanned per-image offsets.  Images that do not fit (reduced-column
+// pool overflow) are flagged and the caller recomputes the batch on the device-wide path.
+#include <cub/cub.cuh>
+
+#include "pipeline.cuh"
+
+namespace cr {
+namespace {
+
+constexpr int K7_THREADS = 256;
+constexpr int K7_IPT = 8;
+constexpr int K7_SORT = K7_THREADS * K7_IPT;  // 2048 keys
+constexpr int K7_MAXCELLS = 3072;  // Khalimsky cells per image (28x28 -> 3025)
+constexpr int K7_MAXVOX = 1024;
+constexpr int K7_POOL = 1024;  // stored reduced columns (u64 keys)
+constexpr int K7_WORK = 256;   // working column capacity (ping-pong)
+constexpr uint32_t D_NONE = 0xFFFFFFFFu, D_ZERO = 0xFFFFFFFEu, D_ESS = 0xFFFFFFFDu;
+
+struct K7Args {
+  const float* images;
+  int64_t batch;
+  int ny, nx;
+  int maxdim;
+  uint32_t* sbar;   // staging: 3 words per bar, cap per image
+  uint32_t* scell;  // staging: birth kidx (optional)
+  uint32_t* count;  // bars per image
+  int cap;          // bars per image region
+  int* flags;       // [0] NaN, [1] overflow
+};
+
+struct K7Smem {
+  uint32_t ord[K7_MAXVOX];
+  uint32_t births[K7_MAXCELLS];
+  uint32_t death[K7_MAXCELLS];
+  uint16_t owner[K7_MAXCELLS];
+  uint16_t vpar[K7_MAXVOX];
+  uint8_t tags[K7_MAXCELLS];
+  uint64_t pool[K7_POOL];
+  uint64_t work[2][K7_WORK];
+  uint16_t pool_off[K7_MAXCELLS / 2];
+  uint16_t pool_len[K7_MAXCELLS / 2];
+  union {  // the keys are held in registers while the sort uses its temporary storage
+    typename cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT>::TempStorage sort;
+    typename cub::BlockScan<uint32_t, K7_THREADS>::TempStorage scan;
+    uint64_t keys[K7_SORT];
+  } tmp;
+  uint32_t nkeys;
+  uint32_t changed;
+  uint32_t nbars;
+};
+
+__device__ __forceinline__ uint64_t cellkey(const K7Smem& S, uint32_t k) {
+  return make_key(S.births[k], k);
+}
+
+// sort S.tmp.keys[0..n) ascending (descending if desc) in place
+__device__ void k7_sort(K7Smem& S, uint32_t n, bool desc) {
+  uint64_t it[K7_IPT];
+#pragma unroll
+  for (int r = 0; r < K7_IPT; ++r) {
+    const uint32_t i = threadIdx.x * K7_IPT + r;
+    it[r] = i < n ? S.tmp.keys[i] : (desc ? 0ull : NONE64);
+  }
+  __syncthreads();
+  typedef cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT> BRS;
+  if (desc) BRS(S.tmp.sort).SortDescending(it);
+  else BRS(S.tmp.sort).Sort(it);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < K7_IPT; ++r) {
+    const uint32_t i = threadIdx.x * K7_IPT + r;
+    if (i < n) S.tmp.keys[i] = it[r];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t k7_find(uint16_t* par, uint32_t x) {
+  while (par[x] != x) {
+    par[x] = par[par[x]];
+    x = par[x];
+  }
+  return x;
+}
+
+// C = A xor B (sorted arrays), one thread
+__device__ uint32_t k7_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
+                               uint64_t* C) {
+  uint32_t i = 0, j = 0, n = 0;
+  while (i < a && j < b) {
+    const uint64_t x = A[i], y = B[j];
+    if (x < y) { C[n++] = x; ++i; }
+    else if (y < x) { C[n++] = y; ++j; }
+    else { ++i; ++j; }
+  }
+  while (i < a) C[n++] = A[i++];
+  while (j < b) C[n++] = B[j++];
+  return n;
+}
+
+__global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K7Smem& S = *reinterpret_cast<K7Smem*>(smem_raw);
+  const int64_t img = blockIdx.x;
+  const int nx = A.nx, ny = A.ny, nvox = nx * ny;
+  const int KX = 2 * nx - 1, KY = 2 * ny - 1, N = KX * KY;
+  // ---- 1. ords, births
+  bool nan = false;
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const float f = A.images[img * nvox + v];
+    nan |= f != f;
+    S.ord[v] = ord_of(f);
+  }
+  if (nan) atomicOr(A.flags, 1);
+  __syncthreads();
+  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+    const int X = k % KX, Y = k / KX;
+    uint32_t m = 0;
+    for (int y = Y >> 1; y <= (Y + 1) >> 1; ++y)
+      for (int x = X >> 1; x <= (X + 1) >> 1; ++x) m = max(m, S.ord[y * nx + x]);
+    S.births[k] = m;
+    S.death[k] = D_NONE;
+    S.owner[k] = 0xFFFFu;
+  }
+  __syncthreads();
+  // ---- 2. apparent pairs (same rule as k_tags)
+  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+    uint8_t tag = 0;
+    const uint32_t bo = S.births[k];
+    if (bo != ABSENT_ORD) {
+      const int c[2] = {k % KX, k / KX};
+      const int ext[2] = {KX, KY};
+      const int st[2] = {1, KX};
+      const uint64_t mykey = make_key(bo, k);
+      const int dim = (c[0] & 1) + (c[1] & 1);
+      uint64_t best = NONE64;
+      int bdir = -1;
+      for (int a = 0; a < 2; ++a) {
+        if (c[a] & 1) continue;
+        for (int s = 0; s < 2; ++s) {
+          if (s == 0 ? c[a] == 0 : c[a] + 1 >= ext[a]) continue;
+          const int t = k + (s ? st[a] : -st[a]);
+          if (S.births[t] == ABSENT_ORD) continue;
+          const uint64_t key = cellkey(S, t);
+          if (key < best) { best = key; bdir = 2 * a + s; }
+        }
+      }
+      if (bdir >= 0) {
+        const int t = int(key_kidx(best)), ta = bdir >> 1;
+        bool is_max = true;
+        for (int a = 0; a < 2 && is_max; ++a) {
+          if (!(a == ta || (c[a] & 1))) continue;
+          for (int s = 0; s < 2; ++s) {
+            const int f = t + (s ? st[a] : -st[a]);
+            if (f != k && cellkey(S, f) > mykey) { is_max = false; break; }
+          }
+        }
+        if (is_max) tag = make_tag(KIND_UP, bdir);
+      }
+      if (!tag && dim >= 1) {
+        uint64_t bestf = 0;
+        int fdir = -1;
+        for (int a = 0; a < 2; ++a) {
+          if (!(c[a] & 1)) continue;
+          for (int s = 0; s < 2; ++s) {
+            const int f = k + (s ? st[a] : -st[a]);
+            const uint64_t key = cellkey(S, f);
+            if (fdir < 0 || key > bestf) { bestf = key; fdir = 2 * a + s; }
+          }
+        }
+        const int r = int(key_kidx(bestf)), ra = fdir >> 1;
+        bool is_min = true;
+        for (int a = 0; a < 2 && is_min; ++a) {
+          if (a != ra && (c[a] & 1)) continue;
+          const int ca = a == ra ? c[a] + ((fdir & 1) ? 1 : -1) : c[a];
+          for (int s = 0; s < 2; ++s) {
+            if (s == 0 ? ca == 0 : ca + 1 >= ext[a]) continue;
+            const int t = r + (s ? st[a] : -st[a]);
+            if (t == k || S.births[t] == ABSENT_ORD) continue;
+            if (cellkey(S, t) < mykey) { is_min = false; break; }
+          }
+        }
+        if (is_min) tag = make_tag(KIND_DOWN, fdir);
+      }
+    }
+    S.tags[k] = tag;
+  }
+  __syncthreads();
+  // ---- 3. H0: apparent forest, roots, residual edges in key order, elder-rule union-find
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const int x = v % nx, y = v / nx, k = 2 * y * KX + 2 * x;
+    uint32_t p = v;
+    const uint8_t t = S.tags[k];
+    if (S.births[k] != ABSENT_ORD && tag_kind(t) == KIND_UP) {
+      const int d = tag_dir(t);
+      const int vs = (d >> 1) == 0 ? 1 : nx;
+      p = (d & 1) ? v + vs : v - vs;
+    }
+    S.vpar[v] = uint16_t(p);
+  }
+  if (threadIdx.x == 0) S.nkeys = 0;
+  __syncthreads();
+  do {  // pointer jumping
+    __syncthreads();
+    if (threadIdx.x == 0) S.changed = 0;
+    __syncthreads();
+    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+      const uint16_t p = S.vpar[v], pp = S.vpar[p];
+      if (p != pp) {
+        S.vpar[v] = pp;
+        S.changed = 1;
+      }
+    }
+    __syncthreads();
+  } while (S.changed);
+  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+    const int X = k % KX, Y = k / KX;
+    if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
+    if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
+    const int s = (X & 1) ? 1 : KX;
+    const int a = k - s, b = k + s;
+    const int va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
+    if (S.vpar[va] != S.vpar[vb]) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = cellkey(S, k);
+  }
+  __syncthreads();
+  const uint32_t nc = S.nkeys;
+  k7_sort(S, nc, false);
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < nc; ++i) {
+      const uint32_t k = key_kidx(S.tmp.keys[i]);
+      const int X = k % KX;
+      const int s = (X & 1) ? 1 : KX;
+      const int a = k - s, b = k + s;
+      const uint32_t va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
+      const uint32_t ra = k7_find(S.vpar, va), rb = k7_find(S.vpar, vb);
+      if (ra == rb) continue;  // positive edge
+      const uint32_t ka = 2 * (ra / nx) * KX + 2 * (ra % nx), kb = 2 * (rb / nx) * KX + 2 * (rb % nx);
+      const bool a_young = cellkey(S, ka) > cellkey(S, kb);
+      const uint32_t young = a_young ? ra : rb, old = a_young ? rb : ra;
+      const uint32_t ky = a_young ? ka : kb;
+      S.vpar[young] = uint16_t(old);  // elder rule
+      S.death[ky] = S.births[k] > S.births[ky] ? S.births[k] : D_ZERO;
+      S.tags[k] = make_tag(KIND_CLEARED, 0);
+    }
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const int k = 2 * (v / nx) * KX + 2 * (v % nx);
+    if (S.vpar[v] == v && S.births[k] != ABSENT_ORD) S.death[k] = D_ESS;
+  }
+  // ---- 4. dimension 1: residual, uncleared edges in decreasing key order
+  const bool do_d1 = A.maxdim >= 1 && nx > 1 && ny > 1;
+  if (threadIdx.x == 0) S.nkeys = 0;
+  __syncthreads();
+  if (do_d1) {
+    for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+      const int X = k % KX, Y = k / KX;
+      if (((X & 1) + (Y & 1)) == 1 && S.births[k] != ABSENT_ORD &&
+          tag_kind(S.tags[k]) == KIND_RESIDUAL)
+        S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = cellkey(S, k);
+    }
+    __syncthreads();
+    const uint32_t ncol = S.nkeys;
+    k7_sort(S, ncol, true);
+    if (threadIdx.x == 0) {
+      uint32_t ptop = 0;
+      bool overflow = false;
+      for (uint32_t ci = 0; ci < ncol && !overflow; ++ci) {
+        const uint32_t sk = key_kidx(S.tmp.keys[ci]);
+        // coboundary: the finite squares on both sides of the edge
+        auto cob = [&](uint32_t e, uint64_t* dst) -> uint32_t {
+          const int X = e % KX, Y = e / KX;
+          uint32_t n = 0;
+          uint64_t c0 = NONE64, c1 = NONE64;
+          if (X & 1) {  // horizontal edge: squares above and below
+            if (Y > 0 && S.births[e - KX] != ABSENT_ORD) c0 = cellkey(S, e - KX);
+            if (Y + 1 < KY && S.births[e + KX] != ABSENT_ORD) c1 = cellkey(S, e + KX);
+          } else {
+            if (X > 0 && S.births[e - 1] != ABSENT_ORD) c0 = cellkey(S, e - 1);
+            if (X + 1 < KX && S.births[e + 1] != ABSENT_ORD) c1 = cellkey(S, e + 1);
+          }
+          if (c0 > c1) { const uint64_t t = c0; c0 = c1; c1 = t; }
+          if (c0 != NONE64) dst[n++] = c0;
+          if (c1 != NONE64) dst[n++] = c1;
+          return n;
+        };
+        int cur = 0;
+        uint32_t len = cob(sk, S.work[0]);
+        uint64_t tmpc[2];
+        while (true) {
+          if (len == 0) {
+            S.death[sk] = D_ESS;
+            break;
+          }
+          const uint64_t p = S.work[cur][0];
+          const uint32_t pk = key_kidx(p);
+          const uint8_t t = S.tags[pk];
+          const uint64_t* add;
+          uint32_t alen;
+          if (tag_kind(t) == KIND_DOWN) {
+            const int d = tag_dir(t);
+            const int off = (d >> 1) == 0 ? 1 : KX;
+            alen = cob(uint32_t(int(pk) + ((d & 1) ? off : -off)), tmpc);
+            add = tmpc;
+          } else if (S.owner[pk] != 0xFFFFu) {
+            const uint32_t o = S.owner[pk];
+            add = S.pool + S.pool_off[o];
+            alen = S.pool_len[o];
+          } else {  // new pair (edge, square): bar [birth edge, birth square)
+            if (ptop + len > K7_POOL || ci >= K7_MAXCELLS / 2) {
+              overflow = true;
+              break;
+            }
+            for (uint32_t i = 0; i < len; ++i) S.pool[ptop + i] = S.work[cur][i];
+            S.pool_off[ci] = uint16_t(ptop);
+            S.pool_len[ci] = uint16_t(len);
+            ptop += len;
+            S.owner[pk] = uint16_t(ci);
+            S.death[sk] = S.births[pk] > S.births[sk] ? S.births[pk] : D_ZERO;
+            break;
+          }
+          if (len + alen > K7_WORK) {
+            overflow = true;
+            break;
+          }
+          len = k7_symdiff(S.work[cur], len, add, alen, S.work[cur ^ 1]);
+          cur ^= 1;
+        }
+      }
+      if (overflow) atomicOr(A.flags + 1, 1);
+    }
+  }
+  __syncthreads();
+  // ---- 5. bars in (dim, birth kidx) order: vertices, then edges
+  typedef cub::BlockScan<uint32_t, K7_THREADS> BS;
+  if (threadIdx.x == 0) S.nbars = 0;
+  __syncthreads();
+  const int64_t base = img * A.cap;
+  for (int dim = 0; dim <= (do_d1 ? 1 : 0); ++dim) {
+    for (int c0 = 0; c0 < N; c0 += K7_THREADS) {
+      const int k = c0 + threadIdx.x;
+      bool keep = false;
+      if (k < N) {
+        const int X = k % KX, Y = k / KX;
+        const uint32_t d = S.death[k];
+        keep = ((X & 1) + (Y & 1)) == dim && d != D_NONE && d != D_ZERO;
+      }
+      uint32_t pre, tot;
+      BS(S.tmp.scan).ExclusiveSum(uint32_t(keep), pre, tot);
+      if (keep) {
+        const uint32_t o = S.nbars + pre;
+        if (int(o) < A.cap) {
+          const uint32_t d = S.death[k];
+          uint32_t* w = A.sbar + 3 * (base + o);
+          w[0] = uint32_t(dim);
+          w[1] = __float_as_uint(float_of_ord(S.births[k]));
+          w[2] = d == D_ESS ? 0x7F800000u : __float_as_uint(float_of_ord(d));
+          if (A.scell) A.scell[base + o] = uint32_t(k);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) S.nbars += tot;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (int(S.nbars) > A.cap) atomicOr(A.flags + 1, 1);
+    A.count[img] = S.nbars;
+  }
+}
+
+__global__ void k7_gather(const uint32_t* __restrict__ sbar, const uint32_t* __restrict__ scell,
+                          const uint32_t* __restrict__ count, const int64_t* __restrict__ off,
+                          int cap, int64_t out_cap, cr_pair* out, uint32_t* cells) {
+  const int64_t img = blockIdx.x;
+  const uint32_t n = count[img];
+  const int64_t o0 = off[img];
+  const uint32_t* src = sbar + 3 * img * cap;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(out + o0);
+  const int64_t lim = out_cap - o0;
+  const uint32_t nw = lim <= 0 ? 0u : (int64_t(n) < lim ? n : uint32_t(lim));
+  for (uint32_t i = threadIdx.x; i < 3 * nw; i += blockDim.x) dst[i] = src[i];
+  if (cells)
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) cells[o0 + i] = scell[img * cap + i];
+}
+
+__global__ void __launch_bounds__(1024) k7_offsets(const uint32_t* __restrict__ count, int64_t batch, int64_t* off) {
+  // single block exclusive scan over batch counts (int64)
+  typedef cub::BlockScan<int64_t, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  int64_t run = 0;
+  for (int64_t c = 0; c < batch; c += 1024) {
+    const int64_t i = c + threadIdx.x;
+    const int64_t v = i < batch ? int64_t(count[i]) : 0;
+    int64_t pre, tot;
+    BS(tmp).ExclusiveSum(v, pre, tot);
+    if (i < batch) off[i] = run + pre;
+    run += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[batch] = run;
+}
+
+}  // namespace
+
+bool batched_small_2d_fits(int64_t ny, int64_t nx) {
+  return nx * ny <= K7_MAXVOX && (2 * nx - 1) * (2 * ny - 1) <= K7_MAXCELLS &&
+         (2 * nx - 1) * (2 * ny - 1) <= 65535;
+}
+
+// Returns -1 if some image did not fit the per-CTA buffers (caller falls back).
+int64_t barcodes_batched_small_2d(const float* images, int64_t batch, int64_t ny, int64_t nx,
+                                  int maxdim, cr_pair* out, uint32_t* out_cells, int64_t cap,
+                                  int64_t* out_offsets, Workspace& ws, HostScalars& hs,
+                                  cr_stats& st) {
+  cudaStream_t s = ws.stream();
+  const int cells = int((2 * nx - 1) * (2 * ny - 1));
+  const int vox = int(nx * ny);
+  // bars per image <= vertices + edges
+  const int per = int(std::min<int64_t>(cells, vox + (nx - 1) * ny + nx * (ny - 1)));
+  K7Args A;
+  A.images = images;
+  A.batch = batch;
+  A.ny = int(ny);
+  A.nx = int(nx);
+  A.maxdim = maxdim;
+  A.cap = per;
+  A.sbar = ws.alloc<uint32_t>(batch * int64_t(per) * 3);
+  A.scell = out_cells ? ws.alloc<uint32_t>(batch * int64_t(per)) : nullptr;
+  A.count = ws.alloc<uint32_t>(batch + 1);
+  A.flags = ws.alloc<int>(4);
+  CR_CUDA(cudaMemsetAsync(A.flags, 0, 4 * sizeof(int), s));
+  const size_t smem = sizeof(K7Smem);
+  CR_CUDA(cudaFuncSetAttribute(k7_image, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k7_image<<<unsigned(batch), K7_THREADS, smem, s>>>(A);
+  CR_CHECK_LAUNCH();
+  prof_mark(s, "k7_images");
+  k7_offsets<<<1, 1024, 0, s>>>(A.count, batch, out_offsets);
+  CR_CHECK_LAUNCH();
+  CR_CUDA(cudaMemcpyAsync(hs.p, A.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaMemcpyAsync(hs.p + 1, out_offsets + batch, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  const int* hf = reinterpret_cast<const int*>(hs.p);
+  if (hf[0]) throw Error{CR_EINVAL, "NaN in image"};
+  if (hf[1]) return -1;
+  const int64_t total = int64_t(hs.p[1]);
+  k7_gather<<<unsigned(batch), 128, 0, s>>>(A.sbar, A.scell, A.count, out_offsets, per, cap, out,
+                                            out_cells);
+  CR_CHECK_LAUNCH();
+  prof_mark(s, "k7_gather");
+  st.pairs[0] = total;
+  return total;
+}
+
+}  // namespace cr

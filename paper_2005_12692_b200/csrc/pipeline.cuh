@@ -58,6 +58,14 @@ inline int64_t barcodes_1d(const float* image, int64_t n, cr_pair* out, uint32_t
 void pairing_1d(const float* image, int64_t n, uint32_t* partner, Workspace& ws, HostScalars& hs,
                 cr_stats& st);
 
+// Batches of small 2D images, one CTA per image (batched.cu).  Returns -1 if an image did not fit
+// the per-CTA buffers (the caller then uses the stacked device-wide path).
+bool batched_small_2d_fits(int64_t ny, int64_t nx);
+int64_t barcodes_batched_small_2d(const float* images, int64_t batch, int64_t ny, int64_t nx,
+                                  int maxdim, cr_pair* out, uint32_t* out_cells, int64_t cap,
+                                  int64_t* out_offsets, Workspace& ws, HostScalars& hs,
+                                  cr_stats& st);
+
 // Device-wide helpers (util.cu).
 void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws);
 void exclusive_sum_u32(const uint32_t* in, uint32_t* out, int64_t n, Workspace& ws);

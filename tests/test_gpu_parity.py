@@ -246,3 +246,35 @@ def test_1d_tile_vs_tree_large(cr, monkeypatch):
     for u, v in zip(a, b):
         assert np.array_equal(np.asarray(u).view(np.uint32), np.asarray(v).view(np.uint32))
     assert_bars_equal(a, oracle.ph(x, 0))
+
+
+def test_batched_small_2d_vs_oracle_and_stacked(cr, monkeypatch):
+    """One-CTA-per-image kernel (K7) = oracle = stacked device-wide path, with ties and +inf."""
+    import torch
+    imgs = gen.blobs(300, seed=31)
+    rng = np.random.default_rng(5)
+    imgs[rng.random(imgs.shape) < 0.02] = np.inf
+    imgs[:10] = np.floor(imgs[:10] / 64)  # heavy ties
+    t = torch.from_numpy(imgs).cuda()
+    bc, off = cr.barcodes_batched(t, 1, cells=True)
+    assert cr.last_stats()["path"] == 5
+    a = bc.numpy()
+    offa = off.cpu().numpy()
+    for i in range(len(imgs)):
+        s = slice(offa[i], offa[i + 1])
+        assert_bars_equal(tuple(x[s] for x in a), oracle.ph(imgs[i], 1), ctx=i)
+    monkeypatch.setenv("CR_FORCE_GENERAL", "1")
+    bc2, off2 = cr.barcodes_batched(t, 1, cells=True)
+    assert cr.last_stats()["path"] == 3
+    assert np.array_equal(off2.cpu().numpy(), offa)
+    for u, v in zip(a, bc2.numpy()):
+        assert np.array_equal(np.asarray(u).view(np.uint32), np.asarray(v).view(np.uint32))
+    # maxdim 0 and 1xN / Nx1 shapes
+    for shp in [(5, 1, 9), (5, 9, 1), (7, 6, 5)]:
+        x = gen.small_int_image(shp, 4, seed=sum(shp))
+        bc3, off3 = cr.barcodes_batched(torch.from_numpy(x).cuda(), 0, cells=True)
+        d3 = bc3.numpy()
+        o3 = off3.cpu().numpy()
+        for i in range(shp[0]):
+            s = slice(o3[i], o3[i + 1])
+            assert_bars_equal(tuple(y[s] for y in d3), oracle.ph(x[i], 0), ctx=(shp, i))
