@@ -35,17 +35,20 @@ constexpr uint32_t DEATH_PENDING = 0xFFFFFFFEu;
 constexpr uint32_t DEATH_ESSENTIAL = 0xFFFFFFFFu;
 constexpr uint64_t KEY_NONE = 0;  // no barrier / unknown barrier: neutral for max
 
-constexpr int TILE = 4096;              // samples per level-1 tile
-constexpr int ITILE = 2048;             // items per level-k tile
-constexpr int THREADS = 512;
+#ifndef CR_1D_TILE
+#define CR_1D_TILE 2048
+#endif
+constexpr int TILE = CR_1D_TILE;        // samples per level-1 tile
+constexpr int ITILE = TILE / 2;         // items per level-k tile
+constexpr int THREADS = TILE / 8;
 constexpr int VPT = TILE / THREADS;
 constexpr int MAXITEMS = TILE / 2;  // basins in a level-1 tile (no two adjacent); == ITILE
 constexpr int NLEVELS = 5;              // contraction levels after level 1 (last must be final)
 constexpr int TREE_CAP = 2 * MAXITEMS;
 // dynamic shared memory: two trees, then death / kept-rank / kept-position / id arrays
-constexpr size_t SMEM = size_t(TREE_CAP) * 8 * 2 + size_t(MAXITEMS) * 4 * 4;
+constexpr size_t SMEM = size_t(TREE_CAP) * 8 * 2 + size_t(MAXITEMS) * 8 + size_t(MAXITEMS) * 4 * 4;
 
-// Shared-memory trees over n <= MAXITEMS (= 2048) items: mn = min of basin keys, mx = max of
+// Shared-memory trees over n <= MAXITEMS items: mn = min of basin keys, mx = max of
 // right-barrier keys.  Level l holds ceil(n / 2^l) nodes at offset 2*MAXITEMS - (2*MAXITEMS >> l);
 // node p of level l covers items [p 2^l, (p+1) 2^l).  Offsets are arithmetic so that the struct
 // stays in registers and every access is a plain LDS.
@@ -195,6 +198,8 @@ __device__ __forceinline__ uint32_t decide(const STree& T, int j, bool left_star
 // DEATH_RETRY if the step budget ends first (the tree search then decides).
 constexpr uint32_t DEATH_RETRY = 0xFFFFFFFDu;
 __device__ int g_scan_steps = 1;  // outward scan budget (tunable: CR_1D_SCAN; 1 measured best)
+__device__ int g_rounds = 1;      // contraction rounds before the tree (tunable: CR_1D_ROUNDS)
+__device__ int g_dbg = 0;         // phase-skipping mask for timing experiments (CR_1D_DBG)
 
 __device__ __forceinline__ uint32_t decide_quick(const STree& T, int j, bool left_start,
                                                  uint64_t lead) {
@@ -281,6 +286,7 @@ struct Smem {
   uint32_t* keep;  // staging slot (level 1)
   uint32_t* kpos;  // compacted item positions
   uint32_t* id;
+  uint64_t* okey;  // level 1: the original item keys (buffers A/B are reused)
 };
 
 __device__ __forceinline__ Smem carve(unsigned char* smem) {
@@ -291,46 +297,124 @@ __device__ __forceinline__ Smem carve(unsigned char* smem) {
   S.keep = S.death + MAXITEMS;
   S.kpos = S.keep + MAXITEMS;
   S.id = S.kpos + MAXITEMS;
+  S.okey = reinterpret_cast<uint64_t*>(S.id + MAXITEMS);
   return S;
 }
 
-// Decide all items of a tile (quick pass, then full searches on the compacted remainder).
-__device__ void decide_all(Smem& S, int n, bool left_start, uint64_t lead) {
-  typedef cub::BlockScan<uint32_t, THREADS> BS;
-  __shared__ typename BS::TempStorage s_scan;
-  __shared__ uint32_t s_nrest;
-  constexpr int CH = MAXITEMS / THREADS;
-  const int c0 = threadIdx.x * CH;
-  uint32_t rest = 0;
-#pragma unroll
-  for (int r = 0; r < CH; ++r) {
-    const int j = c0 + r;
-    if (j < n) {
-      const uint32_t d = decide_quick(S.T, j, left_start, lead);
-      S.death[j] = d;
-      rest += d == DEATH_RETRY;
-    }
-  }
-  uint32_t pre, tot;
-  BS(s_scan).ExclusiveSum(rest, pre, tot);
-#pragma unroll
-  for (int r = 0; r < CH; ++r) {
-    const int j = c0 + r;
-    if (j < n && S.death[j] == DEATH_RETRY) S.kpos[pre++] = j;
-  }
-  if (threadIdx.x == 0) s_nrest = tot;
-  __syncthreads();
-  const uint32_t nr = s_nrest;
-  for (uint32_t i = threadIdx.x; i < nr; i += THREADS) {
-    const int j = int(S.kpos[i]);
-    S.death[j] = decide(S.T, j, left_start, lead);
-  }
-  __syncthreads();
+// O(1) rule on the current (possibly contracted) sequence: keys K, right barriers R (R[n-1] may
+// be KEY_NONE = beyond the tile), lead = barrier left of item 0 (KEY_NONE if unknown).  An item
+// whose older neighbour sits across the lower of its two adjacent barriers dies there (the other
+// side's bottleneck is at least the higher one); an item between two infinite barriers is
+// essential.  Returns the death ord, DEATH_ESSENTIAL, or DEATH_PENDING (not decided by this rule).
+__device__ __forceinline__ uint32_t quick1(const uint64_t* K, const uint64_t* R, int n, int j,
+                                           bool left_start, uint64_t lead) {
+  const uint64_t q = K[j];
+  const uint64_t bl = j > 0 ? R[j - 1] : (left_start ? INF_KEY : lead);
+  const uint64_t br = R[j];
+  const bool linf = key_ord(bl) == INF_ORD, rinf = key_ord(br) == INF_ORD;
+  if (linf && rinf) return DEATH_ESSENTIAL;
+  if (j > 0 && K[j - 1] < q && !linf && br != KEY_NONE && bl < br) return key_ord(bl);
+  if (j + 1 < n && K[j + 1] < q && !rinf && bl != KEY_NONE && br < bl) return key_ord(br);
+  return DEATH_PENDING;
 }
 
-// Export the undecided items of a tile into its item region (kept rank order = item order).
-__device__ void export_kept(Smem& S, int n, uint64_t lead, const Items& O, uint32_t tile,
-                            uint32_t* slot_of /* nullptr: ids from S.id */, uint32_t slot_base) {
+// Decide the items of a tile.  (1) Contraction rounds: apply quick1 to every item, drop the decided
+// ones and fold their right barriers into the nearest kept item on their left (into the lead if
+// none) -- the contracted sequence has the same answers for the items it keeps.  Each round is
+// O(1) per item and fully parallel; a random walk's sequence shrinks ~3x per round.  (2) The few
+// items left when a round makes no progress get the full nearest-older tree search.
+// Buffers: A = (T.mn, T.mx, id) [0, MAXITEMS), B = (T.mn, T.mx)[MAXITEMS, 2 MAXITEMS) + kpos.
+// On return the residual sequence is in buffer A with its tree built; pending residual items are
+// flagged in s_pend; the tile's lead is returned.  sink(id, key, death) records each decision.
+__shared__ uint32_t s_pend[MAXITEMS / 32];
+
+template <class Sink>
+__device__ __forceinline__ int decide_tile(Smem& S, int n, bool left_start, uint64_t& lead, Sink sink) {
+  typedef cub::BlockScan<uint32_t, THREADS> BS;
+  __shared__ typename BS::TempStorage s_scan;
+  __shared__ uint64_t s_lead;
+  constexpr int CH = MAXITEMS / THREADS;
+  // buffer c: keys S.T.mn + c*MAXITEMS, barriers S.T.mx + c*MAXITEMS, ids S.id - c*MAXITEMS
+  // (= S.kpos for c = 1); arithmetic on the shared bases keeps every access an LDS/STS
+#define KB(c) (S.T.mn + (c) * MAXITEMS)
+#define RB(c) (S.T.mx + (c) * MAXITEMS)
+#define IB(c) (S.id - (c) * MAXITEMS)
+  int cur = 0;
+  const int c0 = threadIdx.x * CH;
+  for (int round = 0; round < g_rounds && n > 0; ++round) {
+    uint32_t kb = 0;
+#pragma unroll
+    for (int r = 0; r < CH; ++r) {
+      const int j = c0 + r;
+      if (j >= n) continue;
+      const uint32_t d = quick1(KB(cur), RB(cur), n, j, left_start, lead);
+      if (d != DEATH_PENDING) sink(IB(cur)[j], KB(cur)[j], d);
+      else kb |= 1u << r;
+    }
+    uint32_t pre, tot;
+    BS(s_scan).ExclusiveSum(uint32_t(__popc(kb)), pre, tot);
+    if (threadIdx.x == 0) s_lead = lead;
+    if (int(tot) == n) break;  // no progress: the tree decides the rest (uniform branch)
+    const int nx = cur ^ 1;
+    uint32_t p = pre;
+#pragma unroll
+    for (int r = 0; r < CH; ++r) {  // kept items move to their new slots
+      if (!(kb >> r & 1)) continue;
+      const int j = c0 + r;
+      KB(nx)[p] = KB(cur)[j];
+      RB(nx)[p] = RB(cur)[j];
+      IB(nx)[p] = IB(cur)[j];
+      ++p;
+    }
+    __syncthreads();
+    p = pre;
+#pragma unroll
+    for (int r = 0; r < CH; ++r) {  // a dropped item's barrier folds into the kept item on its left
+      const int j = c0 + r;
+      if (j >= n) continue;
+      if (kb >> r & 1) {
+        ++p;
+      } else {
+        const unsigned long long rb = RB(cur)[j];
+        if (p == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_lead), rb);
+        else atomicMax(reinterpret_cast<unsigned long long*>(RB(nx) + p - 1), rb);
+      }
+    }
+    __syncthreads();
+    lead = s_lead;
+    n = int(tot);
+    cur = nx;
+    __syncthreads();  // s_lead is rewritten next round
+  }
+  if (cur == 1) {  // residual into buffer A (the tree's level 0)
+    for (int j = threadIdx.x; j < n; j += THREADS) {
+      S.T.mn[j] = KB(1)[j];
+      S.T.mx[j] = RB(1)[j];
+      S.id[j] = IB(1)[j];
+    }
+    __syncthreads();
+  }
+  for (int w = threadIdx.x; w < MAXITEMS / 32; w += THREADS) s_pend[w] = 0;
+  __syncthreads();
+  stree_layout(S.T, n);
+  stree_build(S.T);
+  for (int j = threadIdx.x; j < n; j += THREADS) {
+    const uint32_t d = decide(S.T, j, left_start, lead);
+    if (d != DEATH_PENDING) sink(S.id[j], S.T.mn[j], d);
+    else atomicOr(&s_pend[j >> 5], 1u << (j & 31));
+  }
+  __syncthreads();
+  return n;
+#undef KB
+#undef RB
+#undef IB
+}
+
+// Export the residual's pending items (flags in s_pend) into the tile's item region, with their
+// contracted barriers (max up to the next pending item) and the tile's lead.
+template <class IdMap>
+__device__ __forceinline__ void export_pending(Smem& S, int n, uint64_t lead, const Items& O, uint32_t tile,
+                               IdMap idmap) {
   typedef cub::BlockScan<uint32_t, THREADS> BS;
   __shared__ typename BS::TempStorage s_scan;
   __shared__ uint32_t s_nk;
@@ -340,14 +424,14 @@ __device__ void export_kept(Smem& S, int n, uint64_t lead, const Items& O, uint3
 #pragma unroll
   for (int r = 0; r < CH; ++r) {
     const int j = c0 + r;
-    if (j < n) mine += S.death[j] == DEATH_PENDING;
+    if (j < n) mine += s_pend[j >> 5] >> (j & 31) & 1;
   }
   uint32_t pre, tot;
   BS(s_scan).ExclusiveSum(mine, pre, tot);
 #pragma unroll
   for (int r = 0; r < CH; ++r) {
     const int j = c0 + r;
-    if (j < n && S.death[j] == DEATH_PENDING) S.kpos[pre++] = j;
+    if (j < n && (s_pend[j >> 5] >> (j & 31) & 1)) S.kpos[pre++] = j;
   }
   if (threadIdx.x == 0) s_nk = tot;
   __syncthreads();
@@ -358,7 +442,7 @@ __device__ void export_kept(Smem& S, int n, uint64_t lead, const Items& O, uint3
     const int nxt = r + 1 < nk ? int(S.kpos[r + 1]) : n;
     O.key[base + r] = S.T.mn[j];
     O.rb[base + r] = stree_rmax(S.T, j, nxt - 1);
-    O.id[base + r] = slot_of ? slot_base + slot_of[j] : S.id[j];
+    O.id[base + r] = idmap(S.id[j]);
   }
   if (threadIdx.x == 0) {
     O.cnt[tile] = nk;
@@ -473,10 +557,17 @@ __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x
   }
   __syncthreads();
   if (open_end && threadIdx.x == 0) S.T.mx[NB - 1] = KEY_NONE;  // its right barrier is beyond
+  for (int j = threadIdx.x; j < int(NB); j += THREADS) {
+    S.id[j] = j;
+    S.okey[j] = S.T.mn[j];
+    S.death[j] = DEATH_PENDING;
+  }
   __syncthreads();
-  stree_build(S.T);
-  const uint64_t ld = s_lead;
-  decide_all(S, int(NB), t == 0, ld);
+  uint64_t ld = s_lead;
+  const int dbg = g_dbg;  // timing experiments only (CR_1D_DBG); 0 in production
+  const int nres = (dbg & 1) ? 0 : decide_tile(S, int(NB), t == 0, ld,
+                               [=](uint32_t id, uint64_t, uint32_t d) { S.death[id] = d; });
+  if (dbg & 8) return;
   // ---- 3. staging: candidates (bar or undecided) get consecutive slots in basin order
   {
     constexpr int CH = MAXITEMS / THREADS;
@@ -487,7 +578,7 @@ __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x
       const int j = c0 + r;
       if (j < int(NB)) {
         const uint32_t d = S.death[j];
-        mine += d == DEATH_PENDING || d == DEATH_ESSENTIAL || d > key_ord(S.T.mn[j]);
+        mine += d == DEATH_PENDING || d == DEATH_ESSENTIAL || d > key_ord(S.okey[j]);
       }
     }
     uint32_t pre, tot;
@@ -499,22 +590,25 @@ __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x
       const int j = c0 + r;
       if (j >= int(NB)) continue;
       const uint32_t d = S.death[j];
-      const uint32_t bord = key_ord(S.T.mn[j]);
+      const uint32_t bord = key_ord(S.okey[j]);
       if (!(d == DEATH_PENDING || d == DEATH_ESSENTIAL || d > bord)) continue;
       S.keep[j] = pre;
       const uint64_t o = sb + pre;
+      if (dbg & 2) { ++pre; continue; }
       G.bar[3 * o + 0] = 0u;
       G.bar[3 * o + 1] = __float_as_uint(float_of_ord(bord));
       G.bar[3 * o + 2] = d == DEATH_PENDING ? BAR_PENDING
                                             : (d == DEATH_ESSENTIAL ? 0x7F800000u
                                                                     : __float_as_uint(float_of_ord(d)));
-      if (G.cell) G.cell[o] = 2u * key_kidx(S.T.mn[j]);
+      if (G.cell) G.cell[o] = 2u * key_kidx(S.okey[j]);
       ++pre;
     }
     if (threadIdx.x == 0) G.ncand[t] = tot;
     __syncthreads();
   }
-  if (gridDim.x > 1) export_kept(S, int(NB), ld, O, t, S.keep, uint32_t(t) * MAXITEMS);
+  if (gridDim.x > 1 && !(dbg & 4))
+    export_pending(S, nres, ld, O, t,
+                   [=](uint32_t j) { return uint32_t(t) * MAXITEMS + S.keep[j]; });
 }
 
 // ------------------------------------------------------------------------------------------
@@ -594,17 +688,12 @@ __global__ void __launch_bounds__(THREADS) k1_level_items(LevelIn I, Items O, St
   }
   if (k0 == 0 && threadIdx.x == 0) s_lead0 = KEY_NONE;
   __syncthreads();
-  stree_layout(S.T, n);
-  stree_build(S.T);
-  const uint64_t ld = s_lead0;
-  decide_all(S, n, t == 0, ld);
-  for (int j = threadIdx.x; j < n; j += THREADS) {
-    const uint32_t d = S.death[j];
-    if (d != DEATH_PENDING) stage_death(G, S.id[j], key_ord(S.T.mn[j]), d);
-  }
+  uint64_t ld = s_lead0;
+  const int nres = decide_tile(S, n, t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
+    stage_death(G, id, key_ord(key), d);
+  });
   if (ntiles > 1) {
-    __syncthreads();
-    export_kept(S, n, ld, O, t, nullptr, 0);
+    export_pending(S, nres, ld, O, t, [](uint32_t id) { return id; });
   } else if (threadIdx.x == 0) {
     O.cnt[t] = 0;
     O.lead[t] = KEY_NONE;
@@ -708,6 +797,15 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   if (const char* e = std::getenv("CR_1D_SCAN")) {  // tuning knob (not part of the ABI)
     const int v = std::atoi(e);
     CR_CUDA(cudaMemcpyToSymbolAsync(g_scan_steps, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+  }
+  {
+    const char* e = std::getenv("CR_1D_DBG");  // timing experiments only: skips phases
+    const int v = e ? std::atoi(e) : 0;
+    CR_CUDA(cudaMemcpyToSymbolAsync(g_dbg, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+  }
+  if (const char* e = std::getenv("CR_1D_ROUNDS")) {  // tuning knob (not part of the ABI)
+    const int v = std::atoi(e);
+    CR_CUDA(cudaMemcpyToSymbolAsync(g_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
   }
   k1_level1<<<nt1, THREADS, SMEM, s>>>(x, n, L[0], G, flags + 0);
   CR_CHECK_LAUNCH();
