@@ -22,9 +22,13 @@
 // ends of the series are known and every death is decided.  A final single-pass compaction writes
 // the staged bars (death > birth, or essential) per tile to the output in basin (= birth kidx)
 // order; undecided basins that later turn out zero-length become holes that the gather drops.
+#include <cooperative_groups.h>
+
 #include <cub/cub.cuh>
 
 #include "pipeline.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace cr {
 namespace {
@@ -641,22 +645,11 @@ __global__ void __launch_bounds__(1024) k1_level_prefix(const uint32_t* cnt, int
   if (threadIdx.x == 0) prefix[P] = run;
 }
 
-__global__ void __launch_bounds__(THREADS) k1_level_items(LevelIn I, Items O, Stage G,
-                                                          int* overflow, int last_level) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Smem S = carve(smem);
+// One tile t (of ntiles) of an item level.
+__device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, const Stage& G,
+                                           Smem& S, uint32_t t, uint32_t total,
+                                           uint32_t ntiles) {
   const int P = I.ntiles;
-  const uint32_t total = I.prefix[P];
-  const uint32_t ntiles = (total + ITILE - 1) / ITILE;
-  if (ntiles > gridDim.x || (last_level && ntiles > 1)) {
-    if (threadIdx.x == 0) atomicOr(overflow, 1);
-    return;
-  }
-  if (blockIdx.x >= ntiles) {
-    if (threadIdx.x == 0) O.cnt[blockIdx.x] = 0, O.lead[blockIdx.x] = KEY_NONE;
-    return;
-  }
-  const uint32_t t = blockIdx.x;
   const uint32_t k0 = t * ITILE;
   const int n = int(total - k0 < uint32_t(ITILE) ? total - k0 : uint32_t(ITILE));
   // gather items k0..k0+n-1 (and item k0-1's barrier) from the previous level's tile regions
@@ -697,6 +690,75 @@ __global__ void __launch_bounds__(THREADS) k1_level_items(LevelIn I, Items O, St
   } else if (threadIdx.x == 0) {
     O.cnt[t] = 0;
     O.lead[t] = KEY_NONE;
+  }
+  __syncthreads();  // the shared buffers are reused by the CTA's next tile
+}
+
+// All item levels in one cooperative launch: per level, block 0 scans the previous level's
+// per-tile counts (grid sync), then the CTAs share the level's tiles (grid sync).  A level whose
+// items fit one tile is final: both series ends are known there and every basin is decided.
+struct LevelsArgs {
+  LevelIn in[NLEVELS];     // in[l].ntiles = capacity; the actual count comes from ltiles
+  Items out[NLEVELS];
+  uint32_t* ltiles;        // [0] level-1 tiles; [l+1] actual tiles of item level l
+  int64_t cap_tiles[NLEVELS];
+  Stage G;
+  int* overflow;
+};
+
+__global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  Smem S = carve(smem);
+  typedef cub::BlockScan<uint32_t, THREADS> BS;
+  __shared__ typename BS::TempStorage s_scan;
+  for (int l = 0; l < NLEVELS; ++l) {
+    LevelIn I = A.in[l];
+    I.ntiles = int(__ldcg(A.ltiles + l));
+    uint32_t* pref = const_cast<uint32_t*>(I.prefix);
+    if (blockIdx.x == 0) {
+      constexpr int PT = 16;  // counts per thread per pass
+      uint32_t run = 0;
+      for (int c = 0; c < I.ntiles; c += THREADS * PT) {
+        const int i0 = c + threadIdx.x * PT;
+        uint32_t v[PT], sum = 0;
+#pragma unroll
+        for (int r = 0; r < PT; ++r) {
+          v[r] = i0 + r < I.ntiles ? __ldcg(I.cnt + i0 + r) : 0u;
+          sum += v[r];
+        }
+        uint32_t pre, tot;
+        BS(s_scan).ExclusiveSum(sum, pre, tot);
+        pre += run;
+#pragma unroll
+        for (int r = 0; r < PT; ++r)
+          if (i0 + r < I.ntiles) {
+            pref[i0 + r] = pre;
+            pre += v[r];
+          }
+        run += tot;
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        pref[I.ntiles] = run;
+        const uint32_t nt = (run + ITILE - 1) / ITILE;
+        if (int64_t(nt) > A.cap_tiles[l] || (l == NLEVELS - 1 && nt > 1)) {
+          atomicOr(A.overflow, 1);
+          A.ltiles[l + 1] = 0;
+        } else {
+          A.ltiles[l + 1] = nt > 1 ? nt : 0;  // a final (single) tile exports nothing
+        }
+      }
+    }
+    grid.sync();
+    if (__ldcg(A.overflow)) return;
+    const uint32_t total = __ldcg(pref + I.ntiles);
+    const uint32_t ntiles = (total + ITILE - 1) / ITILE;
+    if (ntiles == 0) return;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      level_tile(I, A.out[l], A.G, S, t, total, ntiles);
+    if (ntiles == 1) return;
+    grid.sync();
   }
 }
 
@@ -792,7 +854,7 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     L[l].lead = ws.alloc<uint64_t>(tiles[l]);
   }
   CR_CUDA(cudaFuncSetAttribute(k1_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
-  CR_CUDA(cudaFuncSetAttribute(k1_level_items, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CR_CUDA(cudaFuncSetAttribute(k1_levels_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(SMEM)));
   if (const char* e = std::getenv("CR_1D_SCAN")) {  // tuning knob (not part of the ABI)
     const int v = std::atoi(e);
@@ -811,16 +873,31 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   CR_CHECK_LAUNCH();
   prof_mark(s, "1d_level1");
   if (nt1 > 1) {
+    LevelsArgs LA{};
     for (int l = 1; l <= NLEVELS; ++l) {
       uint32_t* prefix = ws.alloc<uint32_t>(tiles[l - 1] + 1);
-      k1_level_prefix<<<1, 1024, 0, s>>>(L[l - 1].cnt, int(tiles[l - 1]), prefix);
-      CR_CHECK_LAUNCH();
-      LevelIn I{L[l - 1].key, L[l - 1].rb, L[l - 1].id, L[l - 1].cnt, L[l - 1].lead, prefix,
-                int(tiles[l - 1])};
-      k1_level_items<<<unsigned(tiles[l]), THREADS, SMEM, s>>>(I, L[l], G, flags + 1,
-                                                               l == NLEVELS);
-      CR_CHECK_LAUNCH();
+      LA.in[l - 1] = LevelIn{L[l - 1].key, L[l - 1].rb, L[l - 1].id, L[l - 1].cnt, L[l - 1].lead,
+                             prefix, int(tiles[l - 1])};
+      LA.out[l - 1] = L[l];
+      LA.cap_tiles[l - 1] = tiles[l];
     }
+    LA.ltiles = ws.alloc<uint32_t>(NLEVELS + 2);
+    const uint32_t nt1u = uint32_t(nt1);
+    CR_CUDA(cudaMemcpyAsync(LA.ltiles, &nt1u, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    LA.G = G;
+    LA.overflow = flags + 1;
+    int dev = 0, nsm = 0, per_sm = 0;
+    CR_CUDA(cudaGetDevice(&dev));
+    CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_levels_coop, THREADS, SMEM));
+    if (per_sm < 1) throw Error{CR_EINTERNAL, "k1_levels_coop cannot be resident"};
+    // item levels are small (a random walk leaves < 1 % of basins undecided per tile): one CTA
+    // per SM keeps the grid syncs cheap; CTAs loop over tiles if there are more
+    const int64_t blocks = std::min<int64_t>(int64_t(nsm), std::max<int64_t>(1, tiles[1]));
+    void* args[] = {&LA};
+    CR_CUDA(cudaLaunchCooperativeKernel((void*)k1_levels_coop, dim3(unsigned(blocks)),
+                                        dim3(THREADS), args, SMEM, s));
+    ++g_launch_count;
   }
   prof_mark(s, "1d_levels");
   uint32_t* sizes = ws.alloc<uint32_t>(nt1 + 1);
