@@ -24,11 +24,12 @@ __host__ __device__ __forceinline__ uint32_t ord_of(float f) {
   uint32_t u;
   memcpy(&u, &f, 4);
 #endif
-  if (u == 0x80000000u) u = 0u;
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  u = u == 0x80000000u ? 0u : u;
+  // negative: ~u; non-negative: u | sign bit  (branch-free: xor with 0xFFFFFFFF or 0x80000000)
+  return u ^ (uint32_t(int32_t(u) >> 31) | 0x80000000u);
 }
 __host__ __device__ __forceinline__ float float_of_ord(uint32_t o) {
-  uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  const uint32_t u = o ^ (~uint32_t(int32_t(o) >> 31) | 0x80000000u);
 #ifdef __CUDA_ARCH__
   return __uint_as_float(u);
 #else

@@ -39,14 +39,14 @@ constexpr uint32_t DEATH_PENDING = 0xFFFFFFFEu;
 constexpr uint32_t DEATH_ESSENTIAL = 0xFFFFFFFFu;
 constexpr uint64_t KEY_NONE = 0;  // no barrier / unknown barrier: neutral for max
 
-#ifndef CR_1D_TILE
-#define CR_1D_TILE 2048
-#endif
-constexpr int TILE = CR_1D_TILE;        // samples per level-1 tile
-constexpr int ITILE = TILE / 2;         // items per level-k tile
-constexpr int THREADS = TILE / 8;
-constexpr int VPT = TILE / THREADS;
-constexpr int MAXITEMS = TILE / 2;  // basins in a level-1 tile (no two adjacent); == ITILE
+constexpr int THREADS = 256;
+constexpr int MAXITEMS = 512;           // items per CTA buffer (level-1 residual, level-k tile)
+constexpr int ITILE = MAXITEMS;         // items per level-k tile
+constexpr int L1_WARPS = THREADS / 32;
+constexpr int L1_SPW = 512;             // level-1 samples per warp region
+constexpr int L1_TILE = L1_WARPS * L1_SPW;  // level-1 samples per CTA
+constexpr int L1_IPW = L1_SPW / 2;      // basins per warp region (no two adjacent)
+constexpr int SLOTS1 = L1_TILE / 2;     // staging slots per level-1 tile
 constexpr int NLEVELS = 5;              // contraction levels after level 1 (last must be final)
 constexpr int TREE_CAP = 2 * MAXITEMS;
 // dynamic shared memory: two trees, then death / kept-rank / kept-position / id arrays
@@ -193,64 +193,11 @@ __device__ __forceinline__ uint32_t decide(const STree& T, int j, bool left_star
 }
 
 
-// quick decision (O(1)): an item whose lower adjacent barrier leads to an older neighbour dies there
-// when the other adjacent barrier is higher (the other side's bottleneck is at least that barrier).
-// Generalised to a bounded outward scan: both sides advance one item per step, each keeping the
-// highest barrier crossed (a lower bound of its bottleneck, exact once an older basin is met or an
-// infinite barrier is crossed).  The item is decided as soon as one side is exact and lower than
-// the other side's bound.  Returns DEATH_PENDING if both sides run out of tile undecided, and
-// DEATH_RETRY if the step budget ends first (the tree search then decides).
-constexpr uint32_t DEATH_RETRY = 0xFFFFFFFDu;
-__device__ int g_scan_steps = 1;  // outward scan budget (tunable: CR_1D_SCAN; 1 measured best)
 __device__ int g_rounds = 1;      // contraction rounds before the tree (tunable: CR_1D_ROUNDS)
-__device__ int g_dbg = 0;         // phase-skipping mask for timing experiments (CR_1D_DBG)
-
-__device__ __forceinline__ uint32_t decide_quick(const STree& T, int j, bool left_start,
-                                                 uint64_t lead) {
-  const uint64_t q = T.mn[j];
-  const int n = T.n;
-  uint64_t aL = KEY_NONE, aR = T.mx[j];
-  int pL = j - 1, pR = j + 1;
-  bool xL = false, xR = key_ord(aR) == INF_ORD;  // exact?
-  bool doneL = false, doneR = xR;                // stopped scanning?
-  if (xR) aR = INF_KEY;
-  const int budget = g_scan_steps;
-  for (int step = 0; step < budget; ++step) {
-    if (!doneL) {
-      if (pL < 0) {  // out of tile on the left
-        doneL = true;
-        aL = max(aL, lead);
-        if (left_start || key_ord(aL) == INF_ORD) { xL = true; aL = INF_KEY; }
-      } else {
-        aL = max(aL, T.mx[pL]);
-        if (key_ord(aL) == INF_ORD) { xL = doneL = true; aL = INF_KEY; }
-        else if (T.mn[pL] < q) { xL = doneL = true; }
-        else --pL;
-      }
-    }
-    if (!doneR) {
-      if (pR >= n) {
-        doneR = true;
-      } else if (T.mn[pR] < q) {
-        xR = doneR = true;
-      } else {
-        aR = max(aR, T.mx[pR]);
-        if (key_ord(aR) == INF_ORD) { xR = doneR = true; aR = INF_KEY; }
-        else ++pR;
-      }
-    }
-    if (xL && (xR || aR > aL)) {
-      const uint64_t d = xR ? min(aL, aR) : aL;
-      return d == INF_KEY ? DEATH_ESSENTIAL : key_ord(d);
-    }
-    if (xR && aL > aR) return aR == INF_KEY ? DEATH_ESSENTIAL : key_ord(aR);
-    if (doneL && doneR) return DEATH_PENDING;
-  }
-  return DEATH_RETRY;
-}
+__device__ int g_l1_rounds = 6;   // level-1 warp rounds incl. the register round (CR_1D_L1ROUNDS)
 
 // ------------------------------------------------------------------------------------------
-// Per-tile regions.  Level-1 tile t owns staging slots [t*MAXITEMS, (t+1)*MAXITEMS) for its output
+// Per-tile regions.  Level-1 tile t owns staging slots [t*SLOTS1, (t+1)*SLOTS1) for its output
 // candidates (bars with death > birth, essential bars, and undecided basins) in basin order, and an
 // item region of the same size for its undecided basins (the next level's input).  No tile waits
 // for another: the next kernel scans the per-tile counts.
@@ -264,24 +211,38 @@ struct Items {
 };
 
 struct Stage {
-  uint32_t* bar;      // 3 words per slot: dim, birth, death (float bits); dim = -1: hole
+  uint2* st;          // per slot: (birth, death) float bits; birth HOLE: zero-persistence basin
   uint32_t* cell;     // birth kidx per slot (optional)
-  uint32_t* ncand;    // per level-1 tile
-  uint32_t* holes;    // per level-1 tile: zero-persistence undecided basins found later
+  uint32_t* rcnt;     // per level-1 region: basins (slots in use)
+  uint32_t* holes;    // per level-1 region: zero-persistence basins
 };
 
 constexpr uint32_t BAR_PENDING = 0x7FC00001u;  // NaN payload marking an undecided death
+constexpr uint32_t HOLE = 0xFFFFFFFFu;
 
-__device__ __forceinline__ void stage_death(const Stage& G, uint32_t id, uint32_t birth_ord,
-                                            uint32_t d) {
+// Stage the decision d (death ord or DEATH_ESSENTIAL) of the basin with birth ord bo in its slot.
+__device__ __forceinline__ void stage_put(const Stage& G, uint64_t slot, uint32_t bo, uint32_t d) {
+  uint2 v;
   if (d == DEATH_ESSENTIAL) {
-    G.bar[3 * id + 2] = 0x7F800000u;
-  } else if (d > birth_ord) {
-    G.bar[3 * id + 2] = __float_as_uint(float_of_ord(d));
-  } else {  // zero persistence: becomes a hole
-    G.bar[3 * id + 0] = 0xFFFFFFFFu;
-    atomicAdd(G.holes + id / MAXITEMS, 1u);
+    v = make_uint2(__float_as_uint(float_of_ord(bo)), 0x7F800000u);
+  } else if (d > bo) {
+    v = make_uint2(__float_as_uint(float_of_ord(bo)), __float_as_uint(float_of_ord(d)));
+  } else {  // zero persistence: a hole that the gather drops
+    v = make_uint2(HOLE, 0u);
+    atomicAdd(G.holes + slot / L1_IPW, 1u);
   }
+  G.st[slot] = v;
+}
+
+// The same without the hole counter: returns whether the slot became a hole (the caller counts).
+__device__ __forceinline__ uint32_t stage_put_nh(const Stage& G, uint64_t slot, uint32_t bo,
+                                                 uint32_t d) {
+  const bool ess = d == DEATH_ESSENTIAL;
+  const bool hole = !ess && d <= bo;
+  const uint32_t bx = hole ? HOLE : __float_as_uint(float_of_ord(bo));
+  const uint32_t dy = ess ? 0x7F800000u : __float_as_uint(float_of_ord(d));
+  G.st[slot] = make_uint2(bx, dy);
+  return hole;
 }
 
 struct Smem {
@@ -458,161 +419,266 @@ __device__ __forceinline__ void export_pending(Smem& S, int n, uint64_t lead, co
 }
 
 // ------------------------------------------------------------------------------------------
+// Level 1.  A CTA owns L1_TILE samples; warp w owns the region of L1_SPW samples starting at
+// b0 = a + w*L1_SPW, lane l the 16 samples b0 + 16l .. b0 + 16l + 15 (four float4 loads).
+//  (a) each lane marks its basins and barriers in registers and exchanges with its neighbour
+//      lanes the events next to its chunk ends (the previous lane's last basin and the barrier
+//      after it, the next lane's first basin and the barrier before it);
+//  (b) each lane streams its basins in order and applies quick1 to each (the contraction rule of
+//      decide_tile: an item whose older neighbour lies across the lower of its two barriers dies
+//      there; an item between two infinite barriers is essential) -- one round on the raw
+//      sequence, in registers.  Decided basins are staged at once as (birth, death) in their
+//      slot (region * L1_IPW + basin index); survivors go to the warp's arrays with their right
+//      barrier, and a dropped basin's right barrier folds into the survivor on its left;
+//  (c) more quick1 rounds on the warp's survivors (shared memory, warp-synchronous);
+//  (d) the warps' residuals are concatenated (u64 keys; a barrier is keyed by its item's position,
+//      which preserves the order of barriers in distinct gaps) and decided by decide_tile (rounds,
+//      then the shared-memory tree search); the basins still undecided are exported to the next
+//      level and their slots marked pending.
+// Comparisons on 32-bit ords break ties by position: of two basins with equal ord the left one
+// is older; of two barriers with equal ord the left one is lower.
+// ------------------------------------------------------------------------------------------
+constexpr uint32_t ORD_NONE = 0u;  // unknown barrier: neutral for max (every finite ord is > 0)
+
+struct __align__(16) WarpBuf {
+  uint32_t K[L1_IPW];   // basin ords of the warp's residual sequence
+  uint32_t R[L1_IPW];   // right-barrier ords (ORD_NONE: beyond the region)
+  uint32_t PI[L1_IPW];  // (offset in region << 16) | basin index in region
+  uint32_t lead;        // max barrier before the first residual item
+  uint32_t n;           // residual items
+};
+struct WarpScratch {  // the lanes' ords, [i][lane]: conflict-free
+  uint32_t O[16][32];
+};
+static_assert(sizeof(WarpScratch) * L1_WARPS <= SMEM, "scratch aliases the CTA item buffers");
+constexpr size_t L1_SMEM = SMEM + sizeof(WarpBuf) * L1_WARPS;
+
+__device__ __forceinline__ uint32_t ord_at(const float* __restrict__ x, int64_t n, int64_t q,
+                                           bool& nan) {
+  if (q < 0 || q >= n) return ABSENT_ORD;
+  const float v = __ldg(x + q);
+  nan |= v != v;
+  return ord_of(v);
+}
+
+// quick1 on 32-bit ords: basin ord q, left/right barriers bl/br (ORD_NONE: unknown), neighbour
+// basin ords kp/kn (has_p/has_n: they exist).  Returns the death ord, DEATH_ESSENTIAL or
+// DEATH_PENDING.
+__device__ __forceinline__ uint32_t quick1_ord(uint32_t q, uint32_t bl, uint32_t br, bool has_p,
+                                               uint32_t kp, bool has_n, uint32_t kn) {
+  const bool linf = bl == INF_ORD, rinf = br == INF_ORD;
+  if (linf && rinf) return DEATH_ESSENTIAL;
+  if (has_p && kp <= q && !linf && bl != ORD_NONE && br != ORD_NONE && bl <= br) return bl;
+  if (has_n && kn < q && !rinf && br != ORD_NONE && bl != ORD_NONE && br < bl) return br;
+  return DEATH_PENDING;
+}
+
 __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x, int64_t n,
-                                                     Items O, Stage G, int* nan_flag) {
+                                                     Items O, Stage G, int* nan_flag,
+                                                     int* overflow) {
   extern __shared__ __align__(16) unsigned char smem[];
   Smem S = carve(smem);
-  uint32_t* s_ord = reinterpret_cast<uint32_t*>(S.T.mx);  // aliases the mx tree while loading
-  __shared__ uint32_t s_minpos, s_maxpos;
+  WarpBuf* WB = reinterpret_cast<WarpBuf*>(smem + SMEM);
+  __shared__ uint32_t s_off[L1_WARPS + 1];
   __shared__ uint64_t s_lead;
-  typedef cub::BlockScan<uint32_t, THREADS> BS;
-  __shared__ typename BS::TempStorage s_scan1;
-  if (threadIdx.x == 0) {
-    s_minpos = 0xFFFFFFFFu;
-    s_maxpos = 0;
-    s_lead = KEY_NONE;
-  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  WarpBuf& B = WB[w];
+  WarpScratch& SC = reinterpret_cast<WarpScratch*>(smem)[w];
   const uint32_t t = blockIdx.x;
-  const int64_t a = int64_t(t) * TILE;
-  // ---- 1. ords of samples [a-1, a+TILE]
+  const int64_t a = int64_t(t) * L1_TILE;
+  const int64_t b0 = a + int64_t(w) * L1_SPW;                    // region start
+  const uint64_t rslot = (uint64_t(t) * L1_WARPS + w) * L1_IPW;  // region's first slot
+  const bool left_start = (t == 0 && w == 0);
   bool nan = false;
-  {
-    const int64_t body = (n - a < int64_t(TILE)) ? n - a : int64_t(TILE);
-    if (body == TILE && (reinterpret_cast<uintptr_t>(x + a) & 15) == 0) {
-      const float4* x4 = reinterpret_cast<const float4*>(x + a);
-      for (int q = threadIdx.x; q < TILE / 4; q += THREADS) {
-        const float4 v = __ldcs(x4 + q);
-        nan |= (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
-        s_ord[1 + 4 * q] = ord_of(v.x);
-        s_ord[2 + 4 * q] = ord_of(v.y);
-        s_ord[3 + 4 * q] = ord_of(v.z);
-        s_ord[4 + 4 * q] = ord_of(v.w);
-      }
-    } else {
-      for (int q = threadIdx.x; q < TILE; q += THREADS) {
-        uint32_t o = ABSENT_ORD;
-        if (q < body) {
-          const float v = x[a + q];
-          nan |= v != v;
-          o = ord_of(v);
-        }
-        s_ord[1 + q] = o;
-      }
+  if (lane == 0) B.lead = ORD_NONE;
+
+  // ---------------- (a) samples and events
+  const int64_t q0 = b0 + 16 * lane;
+  uint32_t o[16];
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && q0 + 15 < n) {
+    const float4* x4 = reinterpret_cast<const float4*>(x + q0);
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldcs(x4 + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      nan |= (v[k].x != v[k].x) | (v[k].y != v[k].y) | (v[k].z != v[k].z) | (v[k].w != v[k].w);
+      o[4 * k + 0] = ord_of(v[k].x);
+      o[4 * k + 1] = ord_of(v[k].y);
+      o[4 * k + 2] = ord_of(v[k].z);
+      o[4 * k + 3] = ord_of(v[k].w);
     }
-    if (threadIdx.x == 0) s_ord[0] = a >= 1 ? ord_of(x[a - 1]) : ABSENT_ORD;
-    if (threadIdx.x == 1) s_ord[TILE + 1] = a + TILE < n ? ord_of(x[a + TILE]) : ABSENT_ORD;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] = ord_at(x, n, q0 + i, nan);
   }
+  uint32_t um = __shfl_up_sync(0xFFFFFFFFu, o[15], 1);
+  if (lane == 0) um = ord_at(x, n, q0 - 1, nan);
+  uint32_t up = __shfl_down_sync(0xFFFFFFFFu, o[0], 1);
+  if (lane == 31) up = ord_at(x, n, q0 + 16, nan);
   if (nan) atomicOr(nan_flag, 1);
-  __syncthreads();
-  // ---- 2. events of my VPT consecutive samples (registers until the ords are dead)
-  const int v0 = threadIdx.x * VPT;
-  uint32_t bmask = 0, mmask = 0;
-  uint32_t bo[VPT], mo[VPT];
+  // Events as bitmasks over my 16 samples: basin at sample i (bm), barrier after sample i (mm:
+  // the peak edge (i, i+1), or the end of a finite run, em, an infinite barrier).  Basins and
+  // barriers alternate: one barrier between consecutive basins.  The ords stay
+  // in shared memory ([i][lane], aliasing the warp's item arrays until the survivors are
+  // written) for the per-basin steps below.
+  uint32_t (*SO)[32] = SC.O;
+  // Dm bit i: o[i] > o[i+1] (a descent after sample i); A bit i: o[i] is absent (+inf).  Then
+  //   basin at i:     o[i-1] > o[i] <= o[i+1]                 = Gprev & ~G
+  //   peak edge i:    o[i-1] <= o[i] > o[i+1], both finite    = Dm & ~Gprev & ~Aprev & ~A
+  //   run end at i:   o[i] finite, o[i+1] absent              = Anext & ~A
+  // (ABSENT_ORD exceeds every finite ord, so Dm is never set before an absent sample.)
+  uint32_t Dm = 0, A = 0;
 #pragma unroll
-  for (int r = 0; r < VPT; ++r) {
-    const int q = v0 + r;
-    const uint32_t um = s_ord[q], u0 = s_ord[q + 1], u1 = s_ord[q + 2];
-    bo[r] = u0;
-    mo[r] = INF_ORD;
-    if (u0 == ABSENT_ORD || a + q >= n) continue;
-    if (um > u0 && u1 >= u0) bmask |= 1u << r;
-    if (u1 == ABSENT_ORD) {
-      mmask |= 1u << r;  // a finite run ends after this sample
-    } else if (u1 < u0 && um != ABSENT_ORD && um <= u0) {
-      mmask |= 1u << r;  // peak edge (q, q+1)
-      mo[r] = u0;
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t c = o[i], r = i == 15 ? up : o[i + 1];
+    SO[i][lane] = c;
+    Dm |= c > r ? (1u << i) : 0u;
+    A |= c == ABSENT_ORD ? (1u << i) : 0u;
+  }
+  const uint32_t Gprev = (Dm << 1) | (um > o[0] ? 1u : 0u);
+  const uint32_t Aprev = (A << 1) | (um == ABSENT_ORD ? 1u : 0u);
+  const uint32_t Anext = (A >> 1) | (up == ABSENT_ORD ? 0x8000u : 0u);
+  const uint32_t bm = Gprev & ~Dm & 0xFFFFu;
+  const uint32_t em = Anext & ~A;
+  const uint32_t mm = ((Dm & ~Gprev & ~Aprev & ~A) | em) & 0xFFFFu;
+  __syncwarp();
+  const uint32_t nb = __popc(bm);
+  // the barrier before my first basin (fB; the whole chunk if it has no basin), ORD_NONE if none
+  const int fi = nb ? __ffs(bm) - 1 : 16;
+  const uint32_t mlo = mm & ((1u << fi) - 1);
+  const int fj = mlo ? 31 - __clz(mlo) : 0;
+  const uint32_t fB = mlo ? ((em >> fj & 1) ? INF_ORD : SO[fj][lane]) : ORD_NONE;
+  // basin indices: exclusive warp scan of the per-lane counts
+  uint32_t inc = nb;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  const uint32_t nbw = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  const uint32_t idx0 = inc - nb;
+
+  // ---------------- (b) the warp's item list: basin ord K, right barrier R (ORD_NONE if it lies
+  // beyond my chunk; a barrier before a lane's first basin closes the previous item's gap),
+  // (offset << 16 | basin index) PI
+  {
+    uint32_t brem = bm, idx = idx0;
+    while (brem) {
+      const int i = __ffs(brem) - 1;
+      brem &= brem - 1;
+      const uint32_t mr = mm >> i;
+      const int j = mr ? i + __ffs(mr) - 1 : 32;
+      const bool mine = j < 16 && (brem == 0 || j < __ffs(brem) - 1);
+      B.K[idx] = SO[i][lane];
+      B.R[idx] = mine ? ((em >> j & 1) ? INF_ORD : SO[j][lane]) : ORD_NONE;
+      B.PI[idx] = (uint32_t(16 * lane + i) << 16) | idx;
+      if (G.cell) G.cell[rslot + idx] = 2u * uint32_t(q0 + i);
+      ++idx;
     }
   }
-  uint32_t bpre, mpre, NB, NM;
-  {
-    const uint32_t packed = (uint32_t(__popc(bmask)) << 16) | uint32_t(__popc(mmask));
-    uint32_t pre, tot;
-    BS(s_scan1).ExclusiveSum(packed, pre, tot);
-    bpre = pre >> 16;
-    mpre = pre & 0xFFFF;
-    NB = tot >> 16;
-    NM = tot & 0xFFFF;
+  __syncwarp();
+  if (fB != ORD_NONE) {
+    if (idx0 > 0) atomicMax(&B.R[idx0 - 1], fB);
+    else atomicMax(&B.lead, fB);
   }
-  if (bmask | mmask) {
-    const int fb = bmask ? __ffs(bmask) - 1 : 99, fm = mmask ? __ffs(mmask) - 1 : 99;
-    const uint32_t first = fb <= fm ? 2 * (v0 + fb) : 2 * (v0 + fm) + 1;
-    const int lb = bmask ? 31 - __clz(bmask) : -1, lm = mmask ? 31 - __clz(mmask) : -1;
-    const uint32_t last = lm >= lb ? 2 * (v0 + lm) + 1 : 2 * (v0 + lb);
-    atomicMin(&s_minpos, first);
-    atomicMax(&s_maxpos, last + 1);
-  }
-  __syncthreads();  // the ords are dead from here on
-  const int lead = (NB + NM > 0) && (s_minpos & 1);
-  const int open_end = (NB + NM > 0) && !((s_maxpos - 1) & 1);
-  stree_layout(S.T, int(NB));
-  {
-    uint32_t bi = bpre, mi = mpre;
-#pragma unroll
-    for (int r = 0; r < VPT; ++r) {
-      const uint32_t q = uint32_t(a + v0 + r);
-      if (bmask >> r & 1) S.T.mn[bi++] = make_key(bo[r], q);
-      if (mmask >> r & 1) {
-        const uint64_t key = make_key(mo[r], q);
-        if (lead && mi == 0) s_lead = key;
-        else S.T.mx[mi - lead] = key;
-        ++mi;
+  if (lane == 0) G.rcnt[rslot / L1_IPW] = nbw;
+  __syncwarp();
+
+  // ---------------- (c) quick1 rounds over the warp's items, 32 per step
+  uint32_t nn = nbw, holes = 0;
+#pragma unroll 1
+  for (int round = 0; round < g_l1_rounds && nn > 0; ++round) {
+    const uint32_t lead0 = B.lead;
+    uint32_t kept = 0, cK = 0, cR = 0;
+#pragma unroll 1
+    for (uint32_t c0 = 0; c0 < nn; c0 += 32) {
+      const uint32_t j = c0 + lane;
+      const bool valid = j < nn;
+      const uint32_t q = valid ? B.K[j] : 0u, r = valid ? B.R[j] : 0u;
+      const uint32_t pi = valid ? B.PI[j] : 0u;
+      uint32_t kp = __shfl_up_sync(0xFFFFFFFFu, q, 1), rp = __shfl_up_sync(0xFFFFFFFFu, r, 1);
+      if (lane == 0) {
+        kp = cK;
+        rp = cR;
       }
+      uint32_t kn = __shfl_down_sync(0xFFFFFFFFu, q, 1);
+      if (lane == 31 && j + 1 < nn) kn = B.K[j + 1];
+      cK = __shfl_sync(0xFFFFFFFFu, q, 31);
+      cR = __shfl_sync(0xFFFFFFFFu, r, 31);
+      const uint32_t bl = j > 0 ? rp : (left_start ? INF_ORD : lead0);
+      const uint32_t d = valid ? quick1_ord(q, bl, r, j > 0, kp, j + 1 < nn, kn) : DEATH_PENDING;
+      const bool keep = valid && d == DEATH_PENDING;
+      if (valid && !keep) holes += stage_put_nh(G, rslot + (pi & 0xFFFFu), q, d);
+      const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+      const uint32_t p = kept + __popc(km & lt);
+      __syncwarp();
+      if (keep) {
+        B.K[p] = q;
+        B.R[p] = r;
+        B.PI[p] = pi;
+      }
+      __syncwarp();
+      if (valid && !keep && r != ORD_NONE) {
+        if (p == 0) atomicMax(&B.lead, r);
+        else atomicMax(&B.R[p - 1], r);
+      }
+      kept += __popc(km);
+      __syncwarp();
+    }
+    const uint32_t dropped = nn - kept;
+    nn = kept;
+    if (dropped * 8 < nn + 8) break;  // little progress: the tree search decides the rest
+  }
+  holes = __reduce_add_sync(0xFFFFFFFFu, holes);
+  if (lane == 0 && holes) atomicAdd(G.holes + rslot / L1_IPW, holes);
+  if (lane == 0) B.n = nn;
+  __syncthreads();  // the scratch (aliasing the CTA buffers) is dead from here on
+
+  // ---------------- (d) CTA residual: concatenation of the warps' residuals
+  if (threadIdx.x == 0) {
+    uint32_t off = 0;
+    for (int v = 0; v < L1_WARPS; ++v) {
+      s_off[v] = off;
+      off += WB[v].n;
+    }
+    s_off[L1_WARPS] = off;
+    s_lead = KEY_NONE;
+    if (off > uint32_t(MAXITEMS)) atomicOr(overflow, 1);
+  }
+  __syncthreads();
+  const uint32_t m = s_off[L1_WARPS];
+  if (m > uint32_t(MAXITEMS)) return;  // adversarial input: the caller reruns on the tree path
+  {
+    const uint32_t off = s_off[w];
+    for (uint32_t j = lane; j < nn; j += 32) {
+      const uint32_t pi = B.PI[j];
+      const uint64_t pos = uint64_t(b0 + (pi >> 16));
+      const uint32_t r = B.R[j];
+      S.T.mn[off + j] = (uint64_t(B.K[j]) << 32) | pos;
+      S.T.mx[off + j] = r == ORD_NONE ? KEY_NONE : ((uint64_t(r) << 32) | pos);
+      S.id[off + j] = (uint32_t(w) * L1_IPW) | (pi & 0xFFFFu);  // tile-relative slot
     }
   }
   __syncthreads();
-  if (open_end && threadIdx.x == 0) S.T.mx[NB - 1] = KEY_NONE;  // its right barrier is beyond
-  for (int j = threadIdx.x; j < int(NB); j += THREADS) {
-    S.id[j] = j;
-    S.okey[j] = S.T.mn[j];
-    S.death[j] = DEATH_PENDING;
+  if (lane == 0 && B.lead != ORD_NONE) {  // my lead closes the gap after the previous item
+    const uint64_t key = (uint64_t(B.lead) << 32) | uint64_t(b0);
+    const uint32_t off = s_off[w];
+    if (off > 0) atomicMax(reinterpret_cast<unsigned long long*>(S.T.mx + off - 1), key);
+    else atomicMax(reinterpret_cast<unsigned long long*>(&s_lead), key);
   }
   __syncthreads();
   uint64_t ld = s_lead;
-  const int dbg = g_dbg;  // timing experiments only (CR_1D_DBG); 0 in production
-  const int nres = (dbg & 1) ? 0 : decide_tile(S, int(NB), t == 0, ld,
-                               [=](uint32_t id, uint64_t, uint32_t d) { S.death[id] = d; });
-  if (dbg & 8) return;
-  // ---- 3. staging: candidates (bar or undecided) get consecutive slots in basin order
-  {
-    constexpr int CH = MAXITEMS / THREADS;
-    const int c0 = threadIdx.x * CH;
-    uint32_t mine = 0;
-#pragma unroll
-    for (int r = 0; r < CH; ++r) {
-      const int j = c0 + r;
-      if (j < int(NB)) {
-        const uint32_t d = S.death[j];
-        mine += d == DEATH_PENDING || d == DEATH_ESSENTIAL || d > key_ord(S.okey[j]);
-      }
-    }
-    uint32_t pre, tot;
-    __syncthreads();
-    BS(s_scan1).ExclusiveSum(mine, pre, tot);
-    const uint64_t sb = uint64_t(t) * MAXITEMS;
-#pragma unroll
-    for (int r = 0; r < CH; ++r) {
-      const int j = c0 + r;
-      if (j >= int(NB)) continue;
-      const uint32_t d = S.death[j];
-      const uint32_t bord = key_ord(S.okey[j]);
-      if (!(d == DEATH_PENDING || d == DEATH_ESSENTIAL || d > bord)) continue;
-      S.keep[j] = pre;
-      const uint64_t o = sb + pre;
-      if (dbg & 2) { ++pre; continue; }
-      G.bar[3 * o + 0] = 0u;
-      G.bar[3 * o + 1] = __float_as_uint(float_of_ord(bord));
-      G.bar[3 * o + 2] = d == DEATH_PENDING ? BAR_PENDING
-                                            : (d == DEATH_ESSENTIAL ? 0x7F800000u
-                                                                    : __float_as_uint(float_of_ord(d)));
-      if (G.cell) G.cell[o] = 2u * key_kidx(S.okey[j]);
-      ++pre;
-    }
-    if (threadIdx.x == 0) G.ncand[t] = tot;
-    __syncthreads();
-  }
-  if (gridDim.x > 1 && !(dbg & 4))
-    export_pending(S, nres, ld, O, t,
-                   [=](uint32_t j) { return uint32_t(t) * MAXITEMS + S.keep[j]; });
+  const uint64_t tslot = uint64_t(t) * SLOTS1;
+  const int nres = decide_tile(S, int(m), t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
+    stage_put(G, tslot + id, key_ord(key), d);
+  });
+  for (int j = threadIdx.x; j < nres; j += THREADS)
+    if (s_pend[j >> 5] >> (j & 31) & 1)
+      G.st[tslot + S.id[j]] = make_uint2(__float_as_uint(float_of_ord(key_ord(S.T.mn[j]))), BAR_PENDING);
+  if (gridDim.x > 1)
+    export_pending(S, nres, ld, O, t, [=](uint32_t id) { return uint32_t(tslot) + id; });
 }
 
 // ------------------------------------------------------------------------------------------
@@ -683,7 +749,7 @@ __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, con
   __syncthreads();
   uint64_t ld = s_lead0;
   const int nres = decide_tile(S, n, t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
-    stage_death(G, id, key_ord(key), d);
+    stage_put(G, id, key_ord(key), d);
   });
   if (ntiles > 1) {
     export_pending(S, nres, ld, O, t, [](uint32_t id) { return id; });
@@ -763,61 +829,55 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Gather: per level-1 tile, copy its candidates (minus holes) to the output.
-__global__ void k1_tile_sizes(const uint32_t* ncand, const uint32_t* holes, int nt,
-                              uint32_t* sizes) {
+// Gather: warp per level-1 region; copy its staged bars (minus holes) to the output in basin
+// order, at the region's scanned offset.  Bars are staged per warp in shared memory so that the
+// 12-byte records go out as contiguous 4-byte stores.
+__global__ void k1_region_sizes(const uint32_t* rcnt, const uint32_t* holes, int nr,
+                                uint32_t* sizes) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nt) sizes[i] = ncand[i] - holes[i];
-  if (i == nt) sizes[i] = 0;
+  if (i < nr) sizes[i] = rcnt[i] - holes[i];
+  if (i == nr) sizes[i] = 0;
 }
 
-__global__ void __launch_bounds__(256) k1_gather(Stage G, const uint32_t* __restrict__ off,
-                                                 int64_t cap, cr_pair* __restrict__ out,
-                                                 uint32_t* __restrict__ cells, int* bad) {
-  typedef cub::BlockScan<uint32_t, 256> BS;
-  __shared__ typename BS::TempStorage s_scan;
-  __shared__ uint32_t s_run;
-  const uint32_t t = blockIdx.x;
-  const uint32_t nc = G.ncand[t];
-  const uint64_t sb = uint64_t(t) * MAXITEMS;
-  const uint64_t o0 = off[t];
-  if (G.holes[t] == 0) {
-    const int64_t lim = cap - int64_t(o0);
-    const uint32_t nw = lim <= 0 ? 0u : (int64_t(nc) < lim ? nc : uint32_t(lim));
-    const uint32_t* src = G.bar + 3 * sb;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(out + o0);
-    for (uint32_t i = threadIdx.x; i < 3 * nw; i += 256) {
-      const uint32_t v = src[i];
-      if (v == BAR_PENDING) atomicOr(bad, 1);
-      dst[i] = v;
-    }
-    if (cells)
-      for (uint32_t i = threadIdx.x; i < nw; i += 256) cells[o0 + i] = G.cell[sb + i];
-    return;
-  }
-  // rare: some undecided basins turned out zero-length; compact
-  if (threadIdx.x == 0) s_run = 0;
-  __syncthreads();
-  for (uint32_t c = 0; c < nc; c += 256) {
-    const uint32_t i = c + threadIdx.x;
-    const bool keep = i < nc && G.bar[3 * (sb + i)] != 0xFFFFFFFFu;
-    uint32_t pre, tot;
-    BS(s_scan).ExclusiveSum(uint32_t(keep), pre, tot);
+constexpr int GATHER_WARPS = 8;
+__global__ void __launch_bounds__(GATHER_WARPS * 32) k1_gather(Stage G, int nr,
+                                                               const uint32_t* __restrict__ off,
+                                                               int64_t cap,
+                                                               cr_pair* __restrict__ out,
+                                                               uint32_t* __restrict__ cells,
+                                                               int* bad) {
+  __shared__ uint32_t s_bar[GATHER_WARPS][96];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.x * GATHER_WARPS + w;
+  if (r >= nr) return;
+  const uint32_t nc = G.rcnt[r];
+  const uint64_t sb = uint64_t(r) * L1_IPW;
+  int64_t o = off[r];
+  bool badl = false;
+  for (uint32_t c0 = 0; c0 < nc; c0 += 32) {
+    const uint32_t i = c0 + lane;
+    uint2 v = make_uint2(HOLE, 0u);
+    if (i < nc) v = G.st[sb + i];
+    const bool keep = v.x != HOLE;
+    const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+    const uint32_t k = __popc(km & ((1u << lane) - 1));
     if (keep) {
-      const uint64_t o = o0 + s_run + pre;
-      if (int64_t(o) < cap) {
-        uint32_t* d = reinterpret_cast<uint32_t*>(out + o);
-        d[0] = G.bar[3 * (sb + i)];
-        d[1] = G.bar[3 * (sb + i) + 1];
-        d[2] = G.bar[3 * (sb + i) + 2];
-        if (d[2] == BAR_PENDING) atomicOr(bad, 1);
-        if (cells) cells[o] = G.cell[sb + i];
-      }
+      badl |= v.y == BAR_PENDING;
+      s_bar[w][3 * k + 0] = 0u;
+      s_bar[w][3 * k + 1] = v.x;
+      s_bar[w][3 * k + 2] = v.y;
+      if (cells && o + k < cap) cells[o + k] = G.cell[sb + i];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) s_run += tot;
-    __syncthreads();
+    __syncwarp();
+    const uint32_t nk = __popc(km);
+    const int64_t lim = cap - o;
+    const uint32_t nw = lim <= 0 ? 0u : (int64_t(nk) < lim ? nk : uint32_t(lim));
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out + o);
+    for (uint32_t q = lane; q < 3 * nw; q += 32) dst[q] = s_bar[w][q];
+    o += nk;
+    __syncwarp();
   }
+  if (__any_sync(0xFFFFFFFFu, badl) && lane == 0) atomicOr(bad, 1);
 }
 
 }  // namespace
@@ -825,7 +885,7 @@ __global__ void __launch_bounds__(256) k1_gather(Stage G, const uint32_t* __rest
 int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out_cells,
                           int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st) {
   cudaStream_t s = ws.stream();
-  const int nt1 = int((n + TILE - 1) / TILE);
+  const int nt1 = int((n + L1_TILE - 1) / L1_TILE);
   // level sizes (tiles), assuming each level contracts >= 4x (else: overflow -> tree path)
   int64_t tiles[NLEVELS + 1];
   tiles[0] = nt1;
@@ -839,11 +899,12 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   int* flags = ws.alloc<int>(4);  // nan, overflow, bad
   CR_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
   Stage G;
-  G.bar = ws.alloc<uint32_t>(int64_t(nt1) * MAXITEMS * 3);
-  G.cell = out_cells ? ws.alloc<uint32_t>(int64_t(nt1) * MAXITEMS) : nullptr;
-  G.ncand = ws.alloc<uint32_t>(nt1 + 1);
-  G.holes = ws.alloc<uint32_t>(nt1 + 1);
-  CR_CUDA(cudaMemsetAsync(G.holes, 0, (nt1 + 1) * sizeof(uint32_t), s));
+  const int nreg = nt1 * L1_WARPS;
+  G.st = ws.alloc<uint2>(int64_t(nreg) * L1_IPW);
+  G.cell = out_cells ? ws.alloc<uint32_t>(int64_t(nreg) * L1_IPW) : nullptr;
+  G.rcnt = ws.alloc<uint32_t>(nreg + 1);
+  G.holes = ws.alloc<uint32_t>(nreg + 1);
+  CR_CUDA(cudaMemsetAsync(G.holes, 0, (nreg + 1) * sizeof(uint32_t), s));
   Items L[NLEVELS + 1];
   for (int l = 0; l <= NLEVELS; ++l) {
     const int64_t cap_items = tiles[l] * int64_t(MAXITEMS);
@@ -853,23 +914,19 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     L[l].cnt = ws.alloc<uint32_t>(tiles[l]);
     L[l].lead = ws.alloc<uint64_t>(tiles[l]);
   }
-  CR_CUDA(cudaFuncSetAttribute(k1_level1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
+  CR_CUDA(cudaFuncSetAttribute(k1_level1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(L1_SMEM)));
   CR_CUDA(cudaFuncSetAttribute(k1_levels_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(SMEM)));
-  if (const char* e = std::getenv("CR_1D_SCAN")) {  // tuning knob (not part of the ABI)
-    const int v = std::atoi(e);
-    CR_CUDA(cudaMemcpyToSymbolAsync(g_scan_steps, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-  }
-  {
-    const char* e = std::getenv("CR_1D_DBG");  // timing experiments only: skips phases
-    const int v = e ? std::atoi(e) : 0;
-    CR_CUDA(cudaMemcpyToSymbolAsync(g_dbg, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-  }
   if (const char* e = std::getenv("CR_1D_ROUNDS")) {  // tuning knob (not part of the ABI)
     const int v = std::atoi(e);
     CR_CUDA(cudaMemcpyToSymbolAsync(g_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
   }
-  k1_level1<<<nt1, THREADS, SMEM, s>>>(x, n, L[0], G, flags + 0);
+  if (const char* e = std::getenv("CR_1D_L1ROUNDS")) {  // tuning knob (not part of the ABI)
+    const int v = std::atoi(e);
+    CR_CUDA(cudaMemcpyToSymbolAsync(g_l1_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+  }
+  k1_level1<<<nt1, THREADS, L1_SMEM, s>>>(x, n, L[0], G, flags + 0, flags + 1);
   CR_CHECK_LAUNCH();
   prof_mark(s, "1d_level1");
   if (nt1 > 1) {
@@ -900,16 +957,17 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     ++g_launch_count;
   }
   prof_mark(s, "1d_levels");
-  uint32_t* sizes = ws.alloc<uint32_t>(nt1 + 1);
-  uint32_t* off = ws.alloc<uint32_t>(nt1 + 1);
-  k1_tile_sizes<<<grid_for(nt1 + 1, 256), 256, 0, s>>>(G.ncand, G.holes, nt1, sizes);
+  uint32_t* sizes = ws.alloc<uint32_t>(nreg + 1);
+  uint32_t* off = ws.alloc<uint32_t>(nreg + 1);
+  k1_region_sizes<<<grid_for(nreg + 1, 256), 256, 0, s>>>(G.rcnt, G.holes, nreg, sizes);
   CR_CHECK_LAUNCH();
-  exclusive_sum_u32(sizes, off, nt1 + 1, ws);
-  k1_gather<<<nt1, 256, 0, s>>>(G, off, cap, out, out_cells, flags + 2);
+  exclusive_sum_u32(sizes, off, nreg + 1, ws);
+  k1_gather<<<grid_for(nreg, GATHER_WARPS), GATHER_WARPS * 32, 0, s>>>(G, nreg, off, cap, out,
+                                                                      out_cells, flags + 2);
   CR_CHECK_LAUNCH();
   prof_mark(s, "1d_gather");
   CR_CUDA(cudaMemcpyAsync(hs.p, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-  CR_CUDA(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(hs.p) + 4, off + nt1, sizeof(uint32_t),
+  CR_CUDA(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(hs.p) + 4, off + nreg, sizeof(uint32_t),
                           cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
   const int* hf = reinterpret_cast<const int*>(hs.p);

@@ -222,6 +222,10 @@ def _series_cases():
     g = gen.random_walk(4 * 4096, seed=5)
     g[[0, 4095, 4096, 8191, 8192, 9000, 9001, 9002, 16383]] = np.inf
     cases["inf_at_tile_edges"] = g
+    g = gen.random_walk(3 * 4096 + 5, seed=7)  # +inf at warp-region (512) and float4 edges
+    g[[1, 511, 512, 513, 1023, 1024, 1536, 2047, 2048, 4094, 4095, 4096, 4100, 6143]] = np.inf
+    cases["inf_at_warp_edges"] = g
+    cases["walk_unaligned"] = gen.random_walk(2 * 4096 + 1, seed=12)[1:]
     h = gen.random_walk(20000, seed=6)
     h[rng.random(20000) < 0.3] = np.inf
     cases["inf_30pct"] = h
