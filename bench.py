@@ -282,9 +282,9 @@ def algorithmic_bytes(cfg, stage, nvox, st, n_out):
     if stage is None:
         return None
     if stage == "1d_level1":
-        return 4 * nvox + 12 * n_out              # read the series, stage one 12-B bar per output bar
-    if stage == "1d_gather":
-        return 24 * n_out                         # read staged bars, write the output
+        return 4 * nvox + 8 * n_out               # read the series, stage (birth, death) per bar
+    if stage == "1d_levels_gather":
+        return 20 * n_out                         # read staged pairs, write 12-B output bars
     if stage.startswith("1d_count"):
         return 4 * nvox                           # read x
     if stage.startswith("1d_scatter"):

@@ -194,7 +194,7 @@ __device__ __forceinline__ uint32_t decide(const STree& T, int j, bool left_star
 
 
 __device__ int g_rounds = 1;      // contraction rounds before the tree (tunable: CR_1D_ROUNDS)
-__device__ int g_l1_rounds = 6;   // level-1 warp rounds incl. the register round (CR_1D_L1ROUNDS)
+__device__ int g_l1_rounds = 3;   // level-1 warp rounds incl. the register round (CR_1D_L1ROUNDS)
 
 // ------------------------------------------------------------------------------------------
 // Per-tile regions.  Level-1 tile t owns staging slots [t*SLOTS1, (t+1)*SLOTS1) for its output
@@ -211,14 +211,24 @@ struct Items {
 };
 
 struct Stage {
-  uint2* st;          // per slot: (birth, death) float bits; birth HOLE: zero-persistence basin
+  uint2* st;          // level-1 staging per slot: (birth, death) float bits; birth HOLE: zero
+                      // persistence; death BAR_PENDING, then PEND_TAG | rank: undecided
   uint32_t* cell;     // birth kidx per slot (optional)
   uint32_t* rcnt;     // per level-1 region: basins (slots in use)
   uint32_t* holes;    // per level-1 region: zero-persistence basins
+  uint32_t* regoff;   // per level-1 region: output offset of its first bar
+  cr_pair* out;       // final output (bars in basin order), capacity cap
+  uint32_t* out_cells;
+  int64_t cap;
+  unsigned long long* cnt;    // [0] undecided basins exported, [1] decided later, [2] of them
+                              // zero-persistence (holes in the output)
 };
 
 constexpr uint32_t BAR_PENDING = 0x7FC00001u;  // NaN payload marking an undecided death
 constexpr uint32_t HOLE = 0xFFFFFFFFu;
+// An undecided basin's staged death after level 1: a negative-NaN tag with its rank among the
+// bars of its region (< L1_IPW), from which a later level finds its output position.
+constexpr uint32_t PEND_TAG = 0xFFC00000u, PEND_RANK = 0x003FFFFFu;
 
 // Stage the decision d (death ord or DEATH_ESSENTIAL) of the basin with birth ord bo in its slot.
 __device__ __forceinline__ void stage_put(const Stage& G, uint64_t slot, uint32_t bo, uint32_t d) {
@@ -243,6 +253,18 @@ __device__ __forceinline__ uint32_t stage_put_nh(const Stage& G, uint64_t slot, 
   const uint32_t dy = ess ? 0x7F800000u : __float_as_uint(float_of_ord(d));
   G.st[slot] = make_uint2(bx, dy);
   return hole;
+}
+
+// A later level decides an undecided basin; oid = region * L1_IPW + its rank among the region's
+// bars.  The gather writes the record's birth; this writes its dim (-1: a hole) and death.
+__device__ __forceinline__ void final_put(const Stage& G, uint32_t oid, uint32_t bo, uint32_t d) {
+  atomicAdd(G.cnt + 1, 1ull);
+  const bool hole = d != DEATH_ESSENTIAL && d <= bo;
+  if (hole) atomicAdd(G.cnt + 2, 1ull);  // zero persistence: compacted away by the host's fix-up
+  const int64_t pos = int64_t(__ldcg(G.regoff + oid / L1_IPW)) + (oid % L1_IPW);
+  if (pos >= G.cap) return;
+  G.out[pos].dim = hole ? -1 : 0;
+  if (!hole) G.out[pos].death = d == DEATH_ESSENTIAL ? __int_as_float(0x7F800000) : float_of_ord(d);
 }
 
 struct Smem {
@@ -415,6 +437,56 @@ __device__ __forceinline__ void export_pending(Smem& S, int n, uint64_t lead, co
     uint64_t ld = lead;
     if (fk > 0) ld = max(ld, stree_rmax(S.T, 0, fk - 1));
     O.lead[tile] = ld;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Gather one level-1 region (warp-collective): its staged bars minus holes, in basin order, to the
+// output from position o.  All of the region's slots are loaded first (<= L1_IPW / 32 per lane);
+// bars are staged in shared memory (96 words per warp) so that the 12-byte records go out as
+// contiguous 4-byte stores.  An undecided basin's record gets its birth only: the level that
+// decides it writes its dim and death (distinct words, so the two may run concurrently).
+__device__ __forceinline__ void gather_region(const Stage& G, int r, int64_t o, uint32_t* sb96) {
+  constexpr int NCH = L1_IPW / 32;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nc = G.rcnt[r];
+  const uint64_t sb = uint64_t(r) * L1_IPW;
+  uint2 v[NCH];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    const uint32_t i = 32 * k + lane;
+    v[k] = i < nc ? __ldcs(G.st + sb + i) : make_uint2(HOLE, 0u);
+  }
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) {
+    if (32u * k >= nc) break;
+    const bool keep = v[k].x != HOLE;
+    const bool pend = (v[k].y & PEND_TAG) == PEND_TAG;
+    const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+    const unsigned pm = __ballot_sync(0xFFFFFFFFu, keep && pend);
+    const uint32_t q = __popc(km & ((1u << lane) - 1));
+    if (keep) {
+      sb96[3 * q + 0] = 0u;
+      sb96[3 * q + 1] = v[k].x;
+      sb96[3 * q + 2] = v[k].y;
+      if (G.out_cells && o + q < G.cap) G.out_cells[o + q] = G.cell[sb + 32 * k + lane];
+    }
+    __syncwarp();
+    const uint32_t nk = __popc(km);
+    const int64_t lim = G.cap - o;
+    const uint32_t nw = lim <= 0 ? 0u : (int64_t(nk) < lim ? nk : uint32_t(lim));
+    uint32_t* dst = reinterpret_cast<uint32_t*>(G.out + o);
+    if (!pm) {
+      for (uint32_t t = lane; t < 3 * nw; t += 32) dst[t] = sb96[t];
+    } else {  // skip the dim and death words of undecided basins
+      for (uint32_t t = lane; t < 3 * nw; t += 32) {
+        const uint32_t rec = t / 3, wd = t - 3 * rec;
+        const bool p = (sb96[3 * rec + 2] & PEND_TAG) == PEND_TAG;
+        if (!p || wd == 1) dst[t] = sb96[t];
+      }
+    }
+    o += nk;
+    __syncwarp();
   }
 }
 
@@ -674,11 +746,41 @@ __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x
   const int nres = decide_tile(S, int(m), t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
     stage_put(G, tslot + id, key_ord(key), d);
   });
+  __shared__ uint32_t s_npend;
+  if (threadIdx.x == 0) s_npend = 0;
+  __syncthreads();
   for (int j = threadIdx.x; j < nres; j += THREADS)
-    if (s_pend[j >> 5] >> (j & 31) & 1)
-      G.st[tslot + S.id[j]] = make_uint2(__float_as_uint(float_of_ord(key_ord(S.T.mn[j]))), BAR_PENDING);
+    if (s_pend[j >> 5] >> (j & 31) & 1) {
+      G.st[tslot + S.id[j]] =
+          make_uint2(__float_as_uint(float_of_ord(key_ord(S.T.mn[j]))), BAR_PENDING);
+      atomicAdd(&s_npend, 1u);
+    }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_npend) atomicAdd(G.cnt + 0, (unsigned long long)s_npend);
+  // ---------------- (e) ranks of the undecided basins among the bars of their region
+  if (s_npend) {  // the loads below go out together
+    constexpr int NCH = L1_IPW / 32;
+    uint2 v[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const uint32_t i = 32 * k + lane;
+      v[k] = i < nbw ? __ldcg(G.st + rslot + i) : make_uint2(HOLE, 0u);
+    }
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const unsigned km = __ballot_sync(0xFFFFFFFFu, v[k].x != HOLE);
+      if (v[k].x != HOLE && v[k].y == BAR_PENDING)
+        G.st[rslot + 32 * k + lane].y = PEND_TAG | (run + __popc(km & lt));
+      run += __popc(km);
+    }
+  }
+  __syncthreads();
   if (gridDim.x > 1)
-    export_pending(S, nres, ld, O, t, [=](uint32_t id) { return uint32_t(tslot) + id; });
+    export_pending(S, nres, ld, O, t, [=](uint32_t id) {
+      const uint64_t slot = tslot + id;
+      return uint32_t(slot - slot % L1_IPW) | (__ldcg(&G.st[slot].y) & PEND_RANK);
+    });
 }
 
 // ------------------------------------------------------------------------------------------
@@ -749,7 +851,7 @@ __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, con
   __syncthreads();
   uint64_t ld = s_lead0;
   const int nres = decide_tile(S, n, t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
-    stage_put(G, id, key_ord(key), d);
+    final_put(G, id, key_ord(key), d);
   });
   if (ntiles > 1) {
     export_pending(S, nres, ld, O, t, [](uint32_t id) { return id; });
@@ -760,9 +862,14 @@ __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, con
   __syncthreads();  // the shared buffers are reused by the CTA's next tile
 }
 
-// All item levels in one cooperative launch: per level, block 0 scans the previous level's
-// per-tile counts (grid sync), then the CTAs share the level's tiles (grid sync).  A level whose
-// items fit one tile is final: both series ends are known there and every basin is decided.
+// Item levels and the gather in one cooperative launch.
+//  (0) region offsets: every CTA sums the bar counts of its share of the level-1 regions; after a
+//      grid sync each CTA scans its share into G.regoff (a second grid sync publishes them);
+//  (1) item levels: per level, block 0 scans the previous level's per-tile counts (grid sync),
+//      then the CTAs share the level's tiles (grid sync).  A level whose items fit one tile is
+//      final: both series ends are known there and every basin is decided;
+//  (2) a CTA gathers its share of the regions as soon as it has no level tile to work on, so the
+//      gather overlaps the (few-CTA) item levels.
 struct LevelsArgs {
   LevelIn in[NLEVELS];     // in[l].ntiles = capacity; the actual count comes from ltiles
   Items out[NLEVELS];
@@ -770,7 +877,36 @@ struct LevelsArgs {
   int64_t cap_tiles[NLEVELS];
   Stage G;
   int* overflow;
+  int levels;              // 0: one level-1 tile (every basin decided there)
+  int nreg;                // level-1 regions
+  uint32_t* part;          // per CTA: bars in its regions
+  unsigned long long* total;
+  uint32_t* gctr;          // next gather chunk
+  uint32_t* done;          // [l]: level l's count scan done (1); [NLEVELS + l]: its tiles done
 };
+
+// Gather chunks of THREADS/32 regions (one per warp), taken from a global counter, until the
+// chunks run out or *until reaches goal (goal 0: no stop condition).  Returns false once exhausted.
+__device__ bool gather_until(const LevelsArgs& A, const uint32_t* until, uint32_t goal,
+                             uint32_t (*s_bar)[96], uint32_t* s_chunk) {
+  const int w = threadIdx.x >> 5;
+  const uint32_t nchunks = uint32_t((A.nreg + THREADS / 32 - 1) / (THREADS / 32));
+  while (true) {
+    if (threadIdx.x == 0) {
+      uint32_t c = 0xFFFFFFFFu;
+      if (!goal || *reinterpret_cast<const volatile uint32_t*>(until) < goal)
+        c = atomicAdd(A.gctr, 1u);
+      *s_chunk = c;
+    }
+    __syncthreads();
+    const uint32_t c = *s_chunk;
+    __syncthreads();
+    if (c == 0xFFFFFFFFu) return true;  // stop condition met
+    if (c >= nchunks) return false;
+    const int r = int(c) * (THREADS / 32) + w;
+    if (r < A.nreg) gather_region(A.G, r, int64_t(__ldcg(A.G.regoff + r)), s_bar[w]);
+  }
+}
 
 __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
   cg::grid_group grid = cg::this_grid();
@@ -778,7 +914,52 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
   Smem S = carve(smem);
   typedef cub::BlockScan<uint32_t, THREADS> BS;
   __shared__ typename BS::TempStorage s_scan;
-  for (int l = 0; l < NLEVELS; ++l) {
+  __shared__ uint32_t s_red[THREADS / 32];
+  __shared__ uint32_t s_bar[THREADS / 32][96];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // ---- (0) region offsets
+  const int per = (A.nreg + int(gridDim.x) - 1) / int(gridDim.x);
+  const int r0 = min(A.nreg, int(blockIdx.x) * per), r1 = min(A.nreg, r0 + per);
+  {
+    uint32_t sum = 0;
+    for (int r = r0 + threadIdx.x; r < r1; r += THREADS)
+      sum += __ldcg(A.G.rcnt + r) - __ldcg(A.G.holes + r);
+    sum = __reduce_add_sync(0xFFFFFFFFu, sum);
+    if (lane == 0) s_red[w] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int k = 0; k < THREADS / 32; ++k) t += s_red[k];
+      A.part[blockIdx.x] = t;
+    }
+  }
+  grid.sync();
+  {
+    uint32_t v = 0;
+    for (uint32_t k = threadIdx.x; k < blockIdx.x; k += THREADS) v += __ldcg(A.part + k);
+    v = __reduce_add_sync(0xFFFFFFFFu, v);
+    __syncthreads();
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    uint32_t base = 0;
+    for (int k = 0; k < THREADS / 32; ++k) base += s_red[k];
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
+      *A.total = base + __ldcg(A.part + blockIdx.x);
+    for (int c = r0; c < r1; c += THREADS) {
+      const int r = c + threadIdx.x;
+      const uint32_t sz = r < r1 ? __ldcg(A.G.rcnt + r) - __ldcg(A.G.holes + r) : 0u;
+      uint32_t pre, tot;
+      __syncthreads();
+      BS(s_scan).ExclusiveSum(sz, pre, tot);
+      if (r < r1) A.G.regoff[r] = base + pre;
+      base += tot;
+    }
+  }
+  grid.sync();
+  // ---- (1) item levels, (2) the gather when idle
+  __shared__ uint32_t s_chunk;
+  bool more = true;  // gather chunks left
+  for (int l = 0; l < NLEVELS && A.levels; ++l) {
     LevelIn I = A.in[l];
     I.ntiles = int(__ldcg(A.ltiles + l));
     uint32_t* pref = const_cast<uint32_t*>(I.prefix);
@@ -814,70 +995,47 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
         } else {
           A.ltiles[l + 1] = nt > 1 ? nt : 0;  // a final (single) tile exports nothing
         }
+        __threadfence();
+        atomicExch(A.done + l, 1u);
       }
+    } else if (more) {  // block 0 scans; the others gather meanwhile
+      more = gather_until(A, A.done + l, 1u, s_bar, &s_chunk);
     }
     grid.sync();
     if (__ldcg(A.overflow)) return;
     const uint32_t total = __ldcg(pref + I.ntiles);
     const uint32_t ntiles = (total + ITILE - 1) / ITILE;
-    if (ntiles == 0) return;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-      level_tile(I, A.out[l], A.G, S, t, total, ntiles);
-    if (ntiles == 1) return;
+    if (ntiles == 0) break;
+    if (blockIdx.x < ntiles) {
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        level_tile(I, A.out[l], A.G, S, t, total, ntiles);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(A.done + NLEVELS + l, 1u);
+      }
+    } else if (more && ntiles > 1) {
+      more = gather_until(A, A.done + NLEVELS + l, min(ntiles, gridDim.x), s_bar, &s_chunk);
+    }
+    if (ntiles == 1) break;
     grid.sync();
   }
+  if (more) gather_until(A, nullptr, 0u, s_bar, &s_chunk);
 }
 
-// ------------------------------------------------------------------------------------------
-// Gather: warp per level-1 region; copy its staged bars (minus holes) to the output in basin
-// order, at the region's scanned offset.  Bars are staged per warp in shared memory so that the
-// 12-byte records go out as contiguous 4-byte stores.
-__global__ void k1_region_sizes(const uint32_t* rcnt, const uint32_t* holes, int nr,
-                                uint32_t* sizes) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nr) sizes[i] = rcnt[i] - holes[i];
-  if (i == nr) sizes[i] = 0;
+__global__ void k1_hole_flags(const cr_pair* __restrict__ in, int64_t n, uint32_t* flag) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = in[i].dim != -1;
+  if (i == n) flag[i] = 0;
 }
-
-constexpr int GATHER_WARPS = 8;
-__global__ void __launch_bounds__(GATHER_WARPS * 32) k1_gather(Stage G, int nr,
-                                                               const uint32_t* __restrict__ off,
-                                                               int64_t cap,
-                                                               cr_pair* __restrict__ out,
-                                                               uint32_t* __restrict__ cells,
-                                                               int* bad) {
-  __shared__ uint32_t s_bar[GATHER_WARPS][96];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = blockIdx.x * GATHER_WARPS + w;
-  if (r >= nr) return;
-  const uint32_t nc = G.rcnt[r];
-  const uint64_t sb = uint64_t(r) * L1_IPW;
-  int64_t o = off[r];
-  bool badl = false;
-  for (uint32_t c0 = 0; c0 < nc; c0 += 32) {
-    const uint32_t i = c0 + lane;
-    uint2 v = make_uint2(HOLE, 0u);
-    if (i < nc) v = G.st[sb + i];
-    const bool keep = v.x != HOLE;
-    const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
-    const uint32_t k = __popc(km & ((1u << lane) - 1));
-    if (keep) {
-      badl |= v.y == BAR_PENDING;
-      s_bar[w][3 * k + 0] = 0u;
-      s_bar[w][3 * k + 1] = v.x;
-      s_bar[w][3 * k + 2] = v.y;
-      if (cells && o + k < cap) cells[o + k] = G.cell[sb + i];
-    }
-    __syncwarp();
-    const uint32_t nk = __popc(km);
-    const int64_t lim = cap - o;
-    const uint32_t nw = lim <= 0 ? 0u : (int64_t(nk) < lim ? nk : uint32_t(lim));
-    uint32_t* dst = reinterpret_cast<uint32_t*>(out + o);
-    for (uint32_t q = lane; q < 3 * nw; q += 32) dst[q] = s_bar[w][q];
-    o += nk;
-    __syncwarp();
-  }
-  if (__any_sync(0xFFFFFFFFu, badl) && lane == 0) atomicOr(bad, 1);
+__global__ void k1_hole_compact(const cr_pair* __restrict__ in, const uint32_t* __restrict__ icell,
+                                int64_t n, const uint32_t* __restrict__ flag,
+                                const uint32_t* __restrict__ pos, cr_pair* __restrict__ out,
+                                uint32_t* __restrict__ ocell) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  out[pos[i]] = in[i];
+  if (ocell) ocell[pos[i]] = icell[i];
 }
 
 }  // namespace
@@ -896,7 +1054,7 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     tiles[l] = std::max<int64_t>(1, (items + ITILE - 1) / ITILE);
     items = std::max<int64_t>(ITILE, items / 16);
   }
-  int* flags = ws.alloc<int>(4);  // nan, overflow, bad
+  int* flags = ws.alloc<int>(4);  // nan, overflow, bad, total bars
   CR_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
   Stage G;
   const int nreg = nt1 * L1_WARPS;
@@ -926,54 +1084,83 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     const int v = std::atoi(e);
     CR_CUDA(cudaMemcpyToSymbolAsync(g_l1_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
   }
+  G.out = out;
+  G.out_cells = out_cells;
+  G.cap = cap;
+  // counters, total bars, gather chunk counter + level flags: one memset
+  unsigned long long* meta = ws.alloc<unsigned long long>(4 + NLEVELS + 1);
+  CR_CUDA(cudaMemsetAsync(meta, 0, (4 + NLEVELS + 1) * sizeof(unsigned long long), s));
+  G.cnt = meta;
+  G.regoff = ws.alloc<uint32_t>(nreg);
   k1_level1<<<nt1, THREADS, L1_SMEM, s>>>(x, n, L[0], G, flags + 0, flags + 1);
   CR_CHECK_LAUNCH();
   prof_mark(s, "1d_level1");
-  if (nt1 > 1) {
-    LevelsArgs LA{};
-    for (int l = 1; l <= NLEVELS; ++l) {
-      uint32_t* prefix = ws.alloc<uint32_t>(tiles[l - 1] + 1);
-      LA.in[l - 1] = LevelIn{L[l - 1].key, L[l - 1].rb, L[l - 1].id, L[l - 1].cnt, L[l - 1].lead,
-                             prefix, int(tiles[l - 1])};
-      LA.out[l - 1] = L[l];
-      LA.cap_tiles[l - 1] = tiles[l];
-    }
-    LA.ltiles = ws.alloc<uint32_t>(NLEVELS + 2);
-    const uint32_t nt1u = uint32_t(nt1);
-    CR_CUDA(cudaMemcpyAsync(LA.ltiles, &nt1u, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    LA.G = G;
-    LA.overflow = flags + 1;
-    int dev = 0, nsm = 0, per_sm = 0;
-    CR_CUDA(cudaGetDevice(&dev));
-    CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_levels_coop, THREADS, SMEM));
-    if (per_sm < 1) throw Error{CR_EINTERNAL, "k1_levels_coop cannot be resident"};
-    // item levels are small (a random walk leaves < 1 % of basins undecided per tile): one CTA
-    // per SM keeps the grid syncs cheap; CTAs loop over tiles if there are more
-    const int64_t blocks = std::min<int64_t>(int64_t(nsm), std::max<int64_t>(1, tiles[1]));
-    void* args[] = {&LA};
-    CR_CUDA(cudaLaunchCooperativeKernel((void*)k1_levels_coop, dim3(unsigned(blocks)),
-                                        dim3(THREADS), args, SMEM, s));
-    ++g_launch_count;
+  LevelsArgs LA{};
+  for (int l = 1; l <= NLEVELS; ++l) {
+    uint32_t* prefix = nt1 > 1 ? ws.alloc<uint32_t>(tiles[l - 1] + 1) : nullptr;
+    LA.in[l - 1] = LevelIn{L[l - 1].key, L[l - 1].rb, L[l - 1].id, L[l - 1].cnt, L[l - 1].lead,
+                           prefix, int(tiles[l - 1])};
+    LA.out[l - 1] = L[l];
+    LA.cap_tiles[l - 1] = tiles[l];
   }
-  prof_mark(s, "1d_levels");
-  uint32_t* sizes = ws.alloc<uint32_t>(nreg + 1);
-  uint32_t* off = ws.alloc<uint32_t>(nreg + 1);
-  k1_region_sizes<<<grid_for(nreg + 1, 256), 256, 0, s>>>(G.rcnt, G.holes, nreg, sizes);
-  CR_CHECK_LAUNCH();
-  exclusive_sum_u32(sizes, off, nreg + 1, ws);
-  k1_gather<<<grid_for(nreg, GATHER_WARPS), GATHER_WARPS * 32, 0, s>>>(G, nreg, off, cap, out,
-                                                                      out_cells, flags + 2);
-  CR_CHECK_LAUNCH();
-  prof_mark(s, "1d_gather");
+  LA.ltiles = ws.alloc<uint32_t>(NLEVELS + 2);
+  const uint32_t nt1u = uint32_t(nt1);
+  CR_CUDA(cudaMemcpyAsync(LA.ltiles, &nt1u, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  LA.G = G;
+  LA.overflow = flags + 1;
+  LA.levels = nt1 > 1;
+  LA.nreg = nreg;
+  LA.total = meta + 3;
+  LA.gctr = reinterpret_cast<uint32_t*>(meta + 4);
+  LA.done = LA.gctr + 1;  // 2 * NLEVELS words
+  int dev = 0, nsm = 0, per_sm = 0;
+  CR_CUDA(cudaGetDevice(&dev));
+  CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_levels_coop, THREADS, SMEM));
+  if (per_sm < 1) throw Error{CR_EINTERNAL, "k1_levels_coop cannot be resident"};
+  // item levels are small (a random walk leaves ~0.5 % of basins undecided per tile); the gather
+  // streams every bar: a few CTAs per SM keep enough loads in flight
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>(int64_t(nsm) * std::min(per_sm, 2), (nreg + 7) / 8));
+  LA.part = ws.alloc<uint32_t>(blocks);
+  void* args[] = {&LA};
+  CR_CUDA(cudaLaunchCooperativeKernel((void*)k1_levels_coop, dim3(unsigned(blocks)),
+                                      dim3(THREADS), args, SMEM, s));
+  ++g_launch_count;
+  prof_mark(s, "1d_levels_gather");
   CR_CUDA(cudaMemcpyAsync(hs.p, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-  CR_CUDA(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(hs.p) + 4, off + nreg, sizeof(uint32_t),
-                          cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaMemcpyAsync(hs.p + 2, meta, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          s));
   CR_CUDA(cudaStreamSynchronize(s));
   const int* hf = reinterpret_cast<const int*>(hs.p);
+  const unsigned long long exported = hs.p[2], decided = hs.p[3], late_holes = hs.p[4];
+  int64_t total = int64_t(hs.p[5]);
+  if (std::getenv("CR_DEBUG_STATS") && nt1 > 1) {
+    uint32_t lt[NLEVELS + 2];
+    CR_CUDA(cudaMemcpy(lt, LA.ltiles, sizeof(lt), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[cr] 1d tiles per level:");
+    for (int l = 0; l <= NLEVELS; ++l) fprintf(stderr, " %u", lt[l]);
+    fprintf(stderr, " | undecided after level 1: %llu, later holes %llu\n", exported, late_holes);
+  }
   if (hf[0]) throw Error{CR_EINVAL, "NaN in image"};
-  if (hf[1] || hf[2]) return -1;  // contraction did not finish (adversarial input)
-  const int64_t total = reinterpret_cast<const uint32_t*>(hs.p)[4];
+  if (hf[1] || exported != decided) return -1;  // contraction did not finish (adversarial)
+  if (late_holes) {
+    // rare: basins undecided at level 1 that turned out zero-length left holes; compact
+    const int64_t m = std::min<int64_t>(total, cap);
+    cr_pair* tmp = ws.alloc<cr_pair>(m + 1);
+    uint32_t* tcell = out_cells ? ws.alloc<uint32_t>(m + 1) : nullptr;
+    uint32_t* flag = ws.alloc<uint32_t>(m + 1);
+    uint32_t* pos = ws.alloc<uint32_t>(m + 1);
+    CR_CUDA(cudaMemcpyAsync(tmp, out, m * sizeof(cr_pair), cudaMemcpyDeviceToDevice, s));
+    if (tcell)
+      CR_CUDA(cudaMemcpyAsync(tcell, out_cells, m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    k1_hole_flags<<<grid_for(m + 1, 256), 256, 0, s>>>(tmp, m, flag);
+    CR_CHECK_LAUNCH();
+    exclusive_sum_u32(flag, pos, m + 1, ws);
+    k1_hole_compact<<<grid_for(m, 256), 256, 0, s>>>(tmp, tcell, m, flag, pos, out, out_cells);
+    CR_CHECK_LAUNCH();
+    if (total <= cap) total -= int64_t(late_holes);  // else: an upper bound forces a retry
+  }
   st.pairs[0] = total;
   return total;
 }
