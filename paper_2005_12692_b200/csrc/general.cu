@@ -35,32 +35,119 @@ __device__ __forceinline__ void coords_of(const Geom& g, uint32_t k, uint32_t& X
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1: cell births.  One thread per voxel writes the (up to) 8 Khalimsky cells
-// whose lowest vertex is that voxel; birth = max over the cell's vertices of ord(phi).  Since
-// ord(+inf) is the largest ord of any non-NaN float, a cell with a +inf vertex gets ABSENT_ORD.
+// K1: cell births.  birth = max over a cell's vertices of ord(phi); since
+// ord(+inf) = ABSENT_ORD exceeds every finite ord, a cell with a +inf vertex gets ABSENT_ORD
+// (absent from K, reading R5).  A thread owns one (x, y) voxel column and streams
+// K1_ZC planes along z: per plane it loads its voxel and the one at y+1 (the plane z+1 pair is
+// carried to the next step), takes the x+1 neighbours from the next lane, and writes the 8 cells
+// whose lowest vertex is its voxel (the 2x2 cells of the Khalimsky rows (2z|2z+1, 2y|2y+1) at
+// X = 2x, 2x+1: contiguous across the warp).  Finite cells are counted per dimension.
 // ---------------------------------------------------------------------------------------------
-__global__ void k_births(const float* __restrict__ img, Geom g, uint32_t* __restrict__ births,
-                         int* __restrict__ nan_flag) {
-  int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= g.nvox) return;
-  int64_t x = v % g.nx, t = v / g.nx, y = t % g.ny, z = t / g.ny;
-  float f = img[v];
-  if (f != f) atomicOr(nan_flag, 1);
-  const int hx = x + 1 < g.nx, hy = y + 1 < g.ny, hz = z + 1 < g.nz;
-  uint32_t o[2][2][2];
-  for (int dz = 0; dz <= hz; ++dz)
-    for (int dy = 0; dy <= hy; ++dy)
-      for (int dx = 0; dx <= hx; ++dx)
-        o[dz][dy][dx] = ord_of(__ldg(img + v + dz * g.nx * g.ny + dy * g.nx + dx));
-  for (int a = 0; a <= hz; ++a)
-    for (int b = 0; b <= hy; ++b)
-      for (int c = 0; c <= hx; ++c) {
-        uint32_t m = 0;
-        for (int dz = 0; dz <= a; ++dz)
-          for (int dy = 0; dy <= b; ++dy)
-            for (int dx = 0; dx <= c; ++dx) m = max(m, o[dz][dy][dx]);
-        births[((2 * z + a) * g.KY + 2 * y + b) * g.KX + 2 * x + c] = m;
+constexpr int K1_ZC = 8;
+__global__ void __launch_bounds__(256) k_births(const float* __restrict__ img, Geom g,
+                                                uint32_t* __restrict__ births,
+                                                unsigned long long* __restrict__ cnt,
+                                                int* __restrict__ nan_flag) {
+  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny), nz = uint32_t(g.nz);
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const uint32_t XB = (nx + 31) / 32, YB = (ny + 7) / 8;
+  uint32_t blk = blockIdx.x;
+  const uint32_t xb = blk % XB;
+  blk /= XB;
+  const uint32_t yb = blk % YB, zb = blk / YB;
+  const int lane = threadIdx.x & 31;
+  const uint32_t x = xb * 32 + lane, y = yb * 8 + (threadIdx.x >> 5);
+  const uint32_t z0 = zb * K1_ZC, z1 = min(nz, z0 + K1_ZC);
+  const bool vx = x < nx, vy = y < ny, hx = x + 1 < nx, hy = y + 1 < ny;
+  const uint64_t plane = uint64_t(nx) * ny;
+  bool nan = false;
+  auto ld = [&](uint32_t xx, uint32_t yy, uint32_t zz, bool ok) -> uint32_t {
+    if (!ok) return ABSENT_ORD;
+    const float f = __ldg(img + zz * plane + uint64_t(yy) * nx + xx);
+    nan |= f != f;
+    return ord_of(f);
+  };
+  // planes z (a, b), z+1 (an, bn) and z+2 (prefetched); lane 31 also streams the x+1 column
+  const bool l31 = lane == 31;
+  uint32_t a = ld(x, y, z0, vx && vy), b = ld(x, y + 1, z0, vx && hy);
+  uint32_t an = ld(x, y, z0 + 1, vx && vy && z0 + 1 < nz), bn = ld(x, y + 1, z0 + 1, vx && hy && z0 + 1 < nz);
+  uint32_t e = l31 ? ld(x + 1, y, z0, hx && vy) : 0u, f = l31 ? ld(x + 1, y + 1, z0, hx && hy) : 0u;
+  uint32_t en = l31 ? ld(x + 1, y, z0 + 1, hx && vy && z0 + 1 < nz) : 0u;
+  uint32_t fn = l31 ? ld(x + 1, y + 1, z0 + 1, hx && hy && z0 + 1 < nz) : 0u;
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  for (uint32_t z = z0; z < z1; ++z) {
+    const bool hz = z + 1 < nz, hz2 = z + 2 < nz && z + 2 < z1 + 1;
+    const uint32_t an2 = ld(x, y, z + 2, vx && vy && hz2), bn2 = ld(x, y + 1, z + 2, vx && hy && hz2);
+    const uint32_t en2 = l31 ? ld(x + 1, y, z + 2, hx && vy && hz2) : 0u;
+    const uint32_t fn2 = l31 ? ld(x + 1, y + 1, z + 2, hx && hy && hz2) : 0u;
+    uint32_t a1 = __shfl_down_sync(0xFFFFFFFFu, a, 1), b1 = __shfl_down_sync(0xFFFFFFFFu, b, 1);
+    uint32_t an1 = __shfl_down_sync(0xFFFFFFFFu, an, 1), bn1 = __shfl_down_sync(0xFFFFFFFFu, bn, 1);
+    if (l31) {
+      a1 = e;
+      b1 = f;
+      an1 = en;
+      bn1 = fn;
+    }
+    if (vx && vy) {
+      const uint32_t c100 = max(a, a1), c010 = max(a, b), c110 = max(c100, max(b, b1));
+      const uint32_t c001 = max(a, an), c101 = max(c100, max(an, an1));
+      const uint32_t c011 = max(c010, max(an, bn));
+      const uint32_t c111 = max(c110, max(max(an, an1), max(bn, bn1)));
+      uint32_t* r = births + (uint64_t(2 * z) * KY + 2 * y) * KX + 2 * x;
+      r[0] = a;
+      if (hx) r[1] = c100;
+      c0 += a != ABSENT_ORD;
+      c1 += hx && c100 != ABSENT_ORD;
+      if (hy) {
+        r[KX] = c010;
+        if (hx) r[KX + 1] = c110;
+        c1 += c010 != ABSENT_ORD;
+        c2 += hx && c110 != ABSENT_ORD;
       }
+      if (hz) {
+        uint32_t* q = r + uint64_t(KX) * KY;
+        q[0] = c001;
+        if (hx) q[1] = c101;
+        c1 += c001 != ABSENT_ORD;
+        c2 += hx && c101 != ABSENT_ORD;
+        if (hy) {
+          q[KX] = c011;
+          if (hx) q[KX + 1] = c111;
+          c2 += c011 != ABSENT_ORD;
+          c3 += hx && c111 != ABSENT_ORD;
+        }
+      }
+    }
+    a = an;
+    b = bn;
+    an = an2;
+    bn = bn2;
+    e = en;
+    f = fn;
+    en = en2;
+    fn = fn2;
+  }
+  // counts and the NaN flag: warp, then block, then one atomic per counter
+  __shared__ uint32_t s_c[4];
+  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
+  c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
+  c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
+  c3 = __reduce_add_sync(0xFFFFFFFFu, c3);
+  const bool anynan = __any_sync(0xFFFFFFFFu, nan);
+  if (lane == 0) {
+    atomicAdd(s_c + 0, c0);
+    atomicAdd(s_c + 1, c1);
+    atomicAdd(s_c + 2, c2);
+    atomicAdd(s_c + 3, c3);
+    if (anynan) atomicOr(nan_flag, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s_c[threadIdx.x]) atomicAdd(cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
+}
+inline unsigned k_births_grid(const Geom& g) {
+  return unsigned(((g.nx + 31) / 32) * ((g.ny + 7) / 8) * ((g.nz + K1_ZC - 1) / K1_ZC));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -70,16 +157,10 @@ __global__ void k_births(const float* __restrict__ img, Geom g, uint32_t* __rest
 // Keys are (ord(birth), kidx); the pair always has death == birth (birth(t) = max facet birth).
 // Each thread writes only its own tag, so no two threads touch the same byte.
 // ---------------------------------------------------------------------------------------------
-__global__ void k_tags(const uint32_t* __restrict__ births, Geom g, uint8_t* __restrict__ tags,
-                       unsigned long long* __restrict__ app_cnt) {
-  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (kk >= g.ncells) return;
-  const uint32_t k = uint32_t(kk);
+__device__ __forceinline__ uint8_t tag_of(const uint32_t* __restrict__ births, const Geom& g,
+                                          uint32_t k, int& dim_out) {
   const uint32_t bo = births[k];
-  if (bo == ABSENT_ORD) {
-    tags[k] = 0;
-    return;
-  }
+  if (bo == ABSENT_ORD) return 0;
   uint32_t c[3];
   coords_of(g, k, c[0], c[1], c[2]);
   const uint32_t ext[3] = {uint32_t(g.KX), uint32_t(g.KY), uint32_t(g.KZ)};
@@ -148,23 +229,368 @@ __global__ void k_tags(const uint32_t* __restrict__ births, Geom g, uint8_t* __r
     }
     if (is_min) tag = make_tag(KIND_DOWN, bdir);
   }
-  tags[k] = tag;
-  if (tag_kind(tag) == KIND_UP) atomicAdd(app_cnt + dim, 1ull);
+  dim_out = dim;
+  return tag;
 }
 
-__global__ void k_count_cells(const uint32_t* __restrict__ births, Geom g,
-                              unsigned long long* __restrict__ cnt) {
-  __shared__ unsigned long long s[4];
-  if (threadIdx.x < 4) s[threadIdx.x] = 0;
-  __syncthreads();
+__global__ void k_tags(const uint32_t* __restrict__ births, Geom g, uint8_t* __restrict__ tags,
+                       unsigned long long* __restrict__ app_cnt) {
   int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (kk < g.ncells && births[kk] != ABSENT_ORD) {
-    uint32_t X, Y, Z;
-    coords_of(g, uint32_t(kk), X, Y, Z);
-    atomicAdd(&s[(X & 1) + (Y & 1) + (Z & 1)], 1ull);
+  uint8_t tag = 0;
+  int dim = 0;
+  if (kk < g.ncells) {
+    tag = tag_of(births, g, uint32_t(kk), dim);
+    tags[kk] = tag;
+  }
+  // apparent (UP) cells per dimension: warp ballots, then one atomic per warp and dimension
+  const bool up = tag_kind(tag) == KIND_UP;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, up && dim == d);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(app_cnt + d, (unsigned long long)__popc(m));
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// K2 in two streaming passes over the Khalimsky grid (the same apparent pairs as tag_of):
+//   K2a: code[s] = (direction of s's min-key cofacet) | (direction of its max-key facet) << 3,
+//        7 = none; bit 6: s absent.  A cell's 6 grid neighbours s +- e_a are its facets (odd
+//        axis a) or cofacets (even a), and their kidx order is fixed: -Z < -Y < -X < +X < +Y < +Z,
+//        so scanning them in that order, a strict < keeps the smaller kidx among equal births
+//        (min key) and >= the larger (max key).  Absent cofacets are not in K.
+//   K2b: s is UP (paired with its min cofacet t) iff t's max facet is s; else DOWN (paired with
+//        its max facet r) iff r's min cofacet is s.
+// A CTA covers 64 cells of a Khalimsky row x 4 rows of one plane; all index math is 32-bit.
+// ---------------------------------------------------------------------------------------------
+constexpr uint8_t CODE_ABSENT = 0x40;
+struct K2Tile {
+  uint32_t X, Y, Z, k;
+  bool valid;
+};
+__device__ __forceinline__ K2Tile k2_tile(const Geom& g) {
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const uint32_t XB = (KX + 63) / 64, YB = (KY + 3) / 4;
+  uint32_t b = blockIdx.x;
+  const uint32_t xb = b % XB;
+  b /= XB;
+  const uint32_t yb = b % YB, zb = b / YB;
+  K2Tile T;
+  T.X = xb * 64 + (threadIdx.x & 63);
+  T.Y = yb * 4 + (threadIdx.x >> 6);
+  T.Z = zb;
+  T.valid = T.X < KX && T.Y < KY;
+  T.k = (T.Z * KY + T.Y) * KX + T.X;
+  return T;
+}
+inline unsigned k2_grid(const Geom& g) {
+  return unsigned(((g.KX + 63) / 64) * ((g.KY + 3) / 4) * g.KZ);
+}
+
+__global__ void __launch_bounds__(256) k_codes(const uint32_t* __restrict__ births, Geom g,
+                                               uint8_t* __restrict__ code) {
+  const K2Tile T = k2_tile(g);
+  if (!T.valid) return;
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY), KZ = uint32_t(g.KZ);
+  const uint32_t sy = KX, sz = KX * KY;
+  const uint32_t b = births[T.k];
+  if (b == ABSENT_ORD) {
+    code[T.k] = CODE_ABSENT;
+    return;
+  }
+  uint32_t mcb = ABSENT_ORD, mfb = 0, mc = 7, mf = 7;
+  auto visit = [&](bool exists, bool odd, uint32_t kk, uint32_t dir) {
+    if (!exists) return;
+    const uint32_t nb = __ldg(births + kk);
+    if (odd) {
+      if (nb >= mfb) {
+        mfb = nb;
+        mf = dir;
+      }
+    } else if (nb < mcb) {  // absent (ABSENT_ORD) never wins
+      mcb = nb;
+      mc = dir;
+    }
+  };
+  visit(T.Z > 0, T.Z & 1, T.k - sz, 4);
+  visit(T.Y > 0, T.Y & 1, T.k - sy, 2);
+  visit(T.X > 0, T.X & 1, T.k - 1, 0);
+  visit(T.X + 1 < KX, T.X & 1, T.k + 1, 1);
+  visit(T.Y + 1 < KY, T.Y & 1, T.k + sy, 3);
+  visit(T.Z + 1 < KZ, T.Z & 1, T.k + sz, 5);
+  code[T.k] = uint8_t(mc | (mf << 3));
+}
+
+// K2a, streaming along Z: a warp owns 32 cells of one Khalimsky row, a CTA 8 rows, and walks
+// K2_ZC planes.  The +-Z neighbours are the thread's own previous/next values (registers), +-X
+// come from the neighbouring lanes, +-Y from the neighbouring warps through shared memory (the
+// CTA's first and last warps load the rows just outside it).  Each birth is read from DRAM once.
+constexpr int K2_ZC = 16;
+inline unsigned k2z_grid(const Geom& g) {
+  return unsigned(((g.KX + 31) / 32) * ((g.KY + 7) / 8) * ((g.KZ + K2_ZC - 1) / K2_ZC));
+}
+__global__ void __launch_bounds__(256) k_codes_z(const uint32_t* __restrict__ births, Geom g,
+                                                 uint8_t* __restrict__ code) {
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY), KZ = uint32_t(g.KZ);
+  const uint32_t XB = (KX + 31) / 32, YB = (KY + 7) / 8;
+  uint32_t blk = blockIdx.x;
+  const uint32_t xb = blk % XB;
+  blk /= XB;
+  const uint32_t yb = blk % YB, zb = blk / YB;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t X = xb * 32 + lane, Y = yb * 8 + w;
+  const uint32_t Z0 = zb * K2_ZC, Z1 = min(KZ, Z0 + K2_ZC);
+  const bool vx = X < KX, vy = Y < KY;
+  const uint32_t sz = KX * KY;
+  __shared__ uint32_t s_row[10][32];  // rows Y0-1 .. Y0+8 of the current plane
+  auto at = [&](uint32_t xx, uint32_t yy, uint32_t zz, bool ok) -> uint32_t {
+    return ok ? __ldg(births + (zz * KY + yy) * KX + xx) : ABSENT_ORD;
+  };
+  uint32_t prev = Z0 > 0 ? at(X, Y, Z0 - 1, vx && vy) : ABSENT_ORD;
+  uint32_t cur = at(X, Y, Z0, vx && vy);
+  for (uint32_t Z = Z0; Z < Z1; ++Z) {
+    const bool hn = Z + 1 < KZ;
+    const uint32_t next = at(X, Y, Z + 1, vx && vy && hn);
+    // rows above/below the CTA (halo), and the X neighbours outside the warp
+    if (w == 0) s_row[0][lane] = at(X, Y - 1, Z, vx && Y > 0);
+    if (w == 7) s_row[9][lane] = at(X, Y + 1, Z, vx && Y + 1 < KY);
+    s_row[w + 1][lane] = cur;
+    uint32_t xm = __shfl_up_sync(0xFFFFFFFFu, cur, 1), xp = __shfl_down_sync(0xFFFFFFFFu, cur, 1);
+    if (lane == 0) xm = at(X - 1, Y, Z, vy && X > 0);
+    if (lane == 31) xp = at(X + 1, Y, Z, vy && X + 1 < KX);
+    __syncthreads();
+    const uint32_t ym = s_row[w][lane], yp = s_row[w + 2][lane];
+    if (vx && vy) {
+      const uint32_t k = (Z * KY + Y) * KX + X;
+      uint8_t c = CODE_ABSENT;
+      if (cur != ABSENT_ORD) {
+        uint32_t mcb = ABSENT_ORD, mfb = 0, mc = 7, mf = 7;
+        auto visit = [&](bool exists, bool odd, uint32_t nb, uint32_t dir) {
+          if (!exists) return;
+          if (odd) {
+            if (nb >= mfb) {
+              mfb = nb;
+              mf = dir;
+            }
+          } else if (nb < mcb) {
+            mcb = nb;
+            mc = dir;
+          }
+        };
+        visit(Z > 0, Z & 1, prev, 4);
+        visit(Y > 0, Y & 1, ym, 2);
+        visit(X > 0, X & 1, xm, 0);
+        visit(X + 1 < KX, X & 1, xp, 1);
+        visit(Y + 1 < KY, Y & 1, yp, 3);
+        visit(hn, Z & 1, next, 5);
+        c = uint8_t(mc | (mf << 3));
+      }
+      code[k] = c;
+    }
+    __syncthreads();
+    prev = cur;
+    cur = next;
+  }
+}
+
+// K2 fused (births -> tags), streaming along Z.  A warp covers 32 consecutive cells of a
+// Khalimsky row, X = X0-1 .. X0+30, and a CTA 18 rows, Y = Y0-1 .. Y0+16; codes (K2a) are formed
+// for all of them, tags (K2b) for the inner 30 x 16.  Step z forms the codes of plane z from the
+// births of planes z-1, z, z+1 (own column in registers, X neighbours by shuffle, Y neighbours
+// through shared memory) and the tags of plane z-1 from the codes of planes z-2, z-1, z.  Births
+// are prefetched two planes ahead; codes never leave the chip.
+constexpr int K2F_ROWS = 16, K2F_ZC = 32, K2F_THREADS = 32 * (K2F_ROWS + 2);
+inline unsigned k2f_grid(const Geom& g) {
+  return unsigned(((g.KX + 29) / 30) * ((g.KY + K2F_ROWS - 1) / K2F_ROWS) *
+                  ((g.KZ + K2F_ZC - 1) / K2F_ZC));
+}
+// Running max (facets) / min (cofacets) of (birth, position in the kidx order), branch-free.
+// Neighbours are visited in increasing kidx order (rank r = 0..5); a missing neighbour has birth
+// ABSENT_ORD and is skipped for cofacets (never < the initial ABSENT_ORD) and, as a facet of a
+// present cell, never occurs.
+struct CodeAcc {
+  uint32_t mcb, mfb, mc, mf;
+  __device__ __forceinline__ CodeAcc() : mcb(ABSENT_ORD), mfb(0u), mc(7u), mf(7u) {}
+  __device__ __forceinline__ void visit(bool exists, bool odd, uint32_t nb, uint32_t dir) {
+    const bool f = exists && odd && nb >= mfb;   // >=: the later (larger kidx) wins ties
+    const bool c = exists && !odd && nb < mcb;   // <: the earlier (smaller kidx) wins ties
+    mfb = f ? nb : mfb;
+    mf = f ? dir : mf;
+    mcb = c ? nb : mcb;
+    mc = c ? dir : mc;
+  }
+  __device__ __forceinline__ uint8_t code() const { return uint8_t(mc | (mf << 3)); }
+};
+// tag of a cell with code c given its six neighbours' codes packed one byte each by direction
+// (dir = 2 axis + (sign > 0)): UP if its min cofacet's max facet is itself, else DOWN if its max
+// facet's min cofacet is itself
+__device__ __forceinline__ uint8_t code_tag(uint8_t c, uint64_t nbp) {
+  if (c & CODE_ABSENT) return 0;
+  const uint32_t mc = c & 7, mf = (c >> 3) & 7;
+  const uint32_t tmc = uint32_t(nbp >> (8 * (mc & 7))) & 0xFF;  // mc == 7: reads byte 7 (= 0)
+  const uint32_t tmf = uint32_t(nbp >> (8 * (mf & 7))) & 0xFF;
+  if (mc != 7 && ((tmc >> 3) & 7) == (mc ^ 1)) return make_tag(KIND_UP, int(mc));
+  if (mf != 7 && (tmf & 7) == (mf ^ 1)) return make_tag(KIND_DOWN, int(mf));
+  return 0;
+}
+
+__global__ void __launch_bounds__(K2F_THREADS) k_apparent(const uint32_t* __restrict__ births,
+                                                         Geom g, uint8_t* __restrict__ tags,
+                                                         unsigned long long* __restrict__ app_cnt) {
+  const int KX = int(g.KX), KY = int(g.KY), KZ = int(g.KZ);
+  const int XB = (KX + 29) / 30, YB = (KY + K2F_ROWS - 1) / K2F_ROWS;
+  uint32_t blk = blockIdx.x;
+  const int xb = int(blk % XB);
+  blk /= XB;
+  const int yb = int(blk % YB), zb = int(blk / YB);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int X = xb * 30 - 1 + lane, Y = yb * K2F_ROWS - 1 + w;
+  const int Z0 = zb * K2F_ZC, Z1 = min(KZ, Z0 + K2F_ZC);
+  const bool vc = X >= 0 && X < KX && Y >= 0 && Y < KY;
+  const bool out_cell = vc && lane >= 1 && lane <= 30 && w >= 1 && w <= K2F_ROWS;
+  const bool ox = X & 1, oy = Y & 1;
+  const bool hxm = X > 0, hxp = X + 1 < KX, hym = Y > 0, hyp = Y + 1 < KY;
+  const uint32_t plane = uint32_t(KX) * uint32_t(KY);
+  __shared__ uint32_t s_b[K2F_ROWS + 4][32];   // births rows Y0-2 .. Y0+17 of plane z
+  __shared__ uint8_t s_c[2][K2F_ROWS + 2][32];  // codes rows Y0-1 .. Y0+16, planes z-1 | z
+  __shared__ uint32_t s_cnt[3];
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  // streams: own column, and one halo column for the CTA's edge threads (warp 0: row Y-1, the last
+  // warp: row Y+1, lanes 0/31: X-1/X+1; the four corner lanes also stream their X halo)
+  int hx = X, hy = Y;
+  if (w == 0) hy = Y - 1;
+  else if (w == K2F_ROWS + 1) hy = Y + 1;
+  else if (lane == 0) hx = X - 1;
+  else if (lane == 31) hx = X + 1;
+  const bool ewarp = w == 0 || w == K2F_ROWS + 1;
+  const bool has_h = hx != X || hy != Y;
+  const bool vh = has_h && hx >= 0 && hx < KX && hy >= 0 && hy < KY;
+  const bool xh = (lane == 0 || lane == 31) && ewarp;
+  const int cx = lane == 0 ? X - 1 : X + 1;
+  const bool vq = xh && cx >= 0 && cx < KX && Y >= 0 && Y < KY;
+  // stream pointers (advanced by one plane per step) and their validity
+  const uint32_t* po = births + (vc ? uint32_t(Y) * uint32_t(KX) + uint32_t(X) : 0u);
+  const uint32_t* ph = births + (vh ? uint32_t(hy) * uint32_t(KX) + uint32_t(hx) : 0u);
+  const uint32_t* pq = births + (vq ? uint32_t(Y) * uint32_t(KX) + uint32_t(cx) : 0u);
+  auto ld0 = [&](const uint32_t* p, bool ok, int zz) -> uint32_t {
+    return (ok && zz >= 0 && zz < KZ) ? __ldg(p + uint32_t(zz) * plane) : ABSENT_ORD;
+  };
+  uint32_t bzm = ld0(po, vc, Z0 - 2), bz = ld0(po, vc, Z0 - 1), bzp = ld0(po, vc, Z0);
+  uint32_t bzp2 = ld0(po, vc, Z0 + 1);
+  uint32_t hz = ld0(ph, vh, Z0 - 1), hzp = ld0(ph, vh, Z0), hzp2 = ld0(ph, vh, Z0 + 1);
+  uint32_t qz = ld0(pq, vq, Z0 - 1), qzp = ld0(pq, vq, Z0), qzp2 = ld0(pq, vq, Z0 + 1);
+  // next loads: plane z + 3
+  const int zl = Z0 + 2;
+  const uint32_t* no = po + (zl > 0 ? uint32_t(zl) * plane : 0u);
+  const uint32_t* nh = ph + (zl > 0 ? uint32_t(zl) * plane : 0u);
+  const uint32_t* nq = pq + (zl > 0 ? uint32_t(zl) * plane : 0u);
+  uint8_t cprev2 = CODE_ABSENT, cprev = CODE_ABSENT;
+  uint32_t nup = 0;  // UP cells per dimension, one byte each (<= K2F_ZC per thread)
+  uint8_t* tout = tags + (uint32_t(max(Y, 0)) * uint32_t(KX) + uint32_t(max(X, 0))) +
+                  uint64_t(max(Z0, 0)) * plane;
+  for (int z = Z0 - 1; z <= Z1; ++z) {
+    const bool lz = z + 3 < KZ;  // z + 3 >= Z0 + 2 >= 0
+    const uint32_t bnext = (vc && lz) ? __ldg(no) : ABSENT_ORD;
+    const uint32_t hnext = (vh && lz) ? __ldg(nh) : ABSENT_ORD;
+    const uint32_t qnext = (vq && lz) ? __ldg(nq) : ABSENT_ORD;
+    no += plane;
+    nh += plane;
+    nq += plane;
+    s_b[w + 1][lane] = bz;
+    if (w == 0) s_b[0][lane] = hz;
+    if (w == K2F_ROWS + 1) s_b[K2F_ROWS + 3][lane] = hz;
+    uint32_t xm = __shfl_up_sync(0xFFFFFFFFu, bz, 1), xp = __shfl_down_sync(0xFFFFFFFFu, bz, 1);
+    const uint32_t xe = ewarp ? qz : hz;
+    if (lane == 0) xm = xe;
+    if (lane == 31) xp = xe;
+    __syncthreads();
+    uint8_t cz = CODE_ABSENT;
+    if (vc && z >= 0 && z < KZ && bz != ABSENT_ORD) {
+      const bool oz = z & 1;
+      CodeAcc acc;
+      acc.visit(z > 0, oz, bzm, 4);
+      acc.visit(hym, oy, s_b[w][lane], 2);
+      acc.visit(hxm, ox, xm, 0);
+      acc.visit(hxp, ox, xp, 1);
+      acc.visit(hyp, oy, s_b[w + 2][lane], 3);
+      acc.visit(z + 1 < KZ, oz, bzp, 5);
+      cz = acc.code();
+    }
+    s_c[z & 1][w][lane] = cz;
+    __syncthreads();
+    // tags of plane z-1 from the codes of planes z-2, z-1, z
+    const int zt = z - 1;
+    const uint32_t cxm = __shfl_up_sync(0xFFFFFFFFu, uint32_t(cprev), 1);
+    const uint32_t cxp = __shfl_down_sync(0xFFFFFFFFu, uint32_t(cprev), 1);
+    if (zt >= Z0 && zt < Z1 && out_cell) {
+      const uint64_t nbp = uint64_t(cxm) | (uint64_t(cxp) << 8) |
+                           (uint64_t(s_c[zt & 1][w - 1][lane]) << 16) |
+                           (uint64_t(s_c[zt & 1][w + 1][lane]) << 24) |
+                           (uint64_t(cprev2) << 32) | (uint64_t(cz) << 40);
+      const uint8_t t = code_tag(cprev, nbp);
+      *tout = t;
+      nup += uint32_t(tag_kind(t) == KIND_UP) << (8 * (ox + oy + (zt & 1)));
+    }
+    if (zt >= Z0) tout += plane;
+    cprev2 = cprev;
+    cprev = cz;
+    bzm = bz;
+    bz = bzp;
+    bzp = bzp2;
+    bzp2 = bnext;
+    hz = hzp;
+    hzp = hzp2;
+    hzp2 = hnext;
+    qz = qzp;
+    qzp = qzp2;
+    qzp2 = qnext;
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, (nup >> (8 * d)) & 0xFFu);
+    if (lane == 0 && v) atomicAdd(s_cnt + d, v);
   }
   __syncthreads();
-  if (threadIdx.x < 4 && s[threadIdx.x]) atomicAdd(cnt + threadIdx.x, s[threadIdx.x]);
+  if (threadIdx.x < 3 && s_cnt[threadIdx.x])
+    atomicAdd(app_cnt + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_tags2(const uint8_t* __restrict__ code, Geom g,
+                                               uint8_t* __restrict__ tags,
+                                               unsigned long long* __restrict__ app_cnt) {
+  const K2Tile T = k2_tile(g);
+  uint8_t tag = 0;
+  int dim = 0;
+  if (T.valid) {
+    const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+    const uint32_t st[3] = {1u, KX, KX * KY};
+    const uint8_t c = code[T.k];
+    dim = (T.X & 1) + (T.Y & 1) + (T.Z & 1);
+    if (!(c & CODE_ABSENT)) {
+      const uint32_t mc = c & 7, mf = (c >> 3) & 7;
+      if (mc != 7) {
+        const uint32_t t = (mc & 1) ? T.k + st[mc >> 1] : T.k - st[mc >> 1];
+        if (((__ldg(code + t) >> 3) & 7) == (mc ^ 1)) tag = make_tag(KIND_UP, int(mc));
+      }
+      if (!tag && mf != 7) {
+        const uint32_t r = (mf & 1) ? T.k + st[mf >> 1] : T.k - st[mf >> 1];
+        if ((__ldg(code + r) & 7) == (mf ^ 1)) tag = make_tag(KIND_DOWN, int(mf));
+      }
+    }
+    tags[T.k] = tag;
+  }
+  const bool up = tag_kind(tag) == KIND_UP;
+  __shared__ uint32_t s_c[3];
+  if (threadIdx.x < 3) s_c[threadIdx.x] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, up && dim == d);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(s_c + d, uint32_t(__popc(m)));
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 && s_c[threadIdx.x])
+    atomicAdd(app_cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -641,14 +1067,24 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
 
-  k_births<<<grid_for(g.nvox, B), B, 0, s>>>(image, g, S.births, nan_flag);
+  k_births<<<k_births_grid(g), 256, 0, s>>>(image, g, S.births, cnt + 4, nan_flag);
   CR_CHECK_LAUNCH();
   prof_mark(s, "births");
-  k_tags<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, S.tags, cnt + 0);
-  CR_CHECK_LAUNCH();
+  if (std::getenv("CR_K2_ONEPASS")) {  // the one-kernel definition (cross-check in tests)
+    k_tags<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, S.tags, cnt + 0);
+    CR_CHECK_LAUNCH();
+  } else if (std::getenv("CR_K2_TWOPASS")) {  // codes in HBM, then tags (cross-check)
+    uint8_t* code = ws.alloc<uint8_t>(g.ncells);
+    k_codes_z<<<k2z_grid(g), 256, 0, s>>>(S.births, g, code);
+    CR_CHECK_LAUNCH();
+    k_tags2<<<k2_grid(g), 256, 0, s>>>(code, g, S.tags, cnt + 0);
+    CR_CHECK_LAUNCH();
+    ws.release(code);
+  } else {
+    k_apparent<<<k2f_grid(g), K2F_THREADS, 0, s>>>(S.births, g, S.tags, cnt + 0);
+    CR_CHECK_LAUNCH();
+  }
   prof_mark(s, "apparent");
-  k_count_cells<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, cnt + 4);
-  CR_CHECK_LAUNCH();
 
   // ---- H0
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);

@@ -30,6 +30,9 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <vector>
+
 #include "pipeline.cuh"
 
 namespace cg = cooperative_groups;
@@ -70,6 +73,7 @@ struct RP {
                               // debug: [4] pool additions [5] pool lengths [7]/[8] cycles in
                               // pool/apparent additions [9] cycles in pivot + owner lookups
   int debug;
+  unsigned long long* colstat;  // debug: per column (additions, entries touched)
 };
 
 __device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
@@ -238,13 +242,136 @@ __device__ __forceinline__ uint64_t take_pivot(Col& c) {
   }
 }
 
+// C = A xor F for a long A (global) and a short F (shared, b <= FCAP), C in global memory, using
+// X (FCAP u64 of shared scratch).  Warp-collective; returns |C|.
+//  1. positions: P[t] = #{A < F[t]} by a sampled search (<= 256 samples of A in X, then a binary
+//     search inside one sample interval; a lane's <= 8 searches run interleaved), dup[t] = (A[P[t]]
+//     == F[t]); prefix counts of inserted (non-dup) and cancelled (dup) F entries over t;
+//  2. the non-dup F entries go to P[t] + ins_before(t) - dup_before(t);
+//  3. A streams through in windows of 256 (8 independent loads per lane): A[i] moves to
+//     i + #{non-dup t : P[t] <= i} - #{dup t : P[t] < i}, unless a dup lands on it.  A window that
+//     holds no position only shifts (one smem search per window).
+__device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a, const uint64_t* F,
+                                     uint32_t b, uint64_t* __restrict__ C, uint64_t* X, int lane) {
+  constexpr int R = FCAP / 32;  // F entries per lane (t = lane + 32 r)
+  constexpr int G = 4;          // searches run interleaved per group
+  constexpr uint32_t NS = FCAP / 2;
+  const unsigned lt = (1u << lane) - 1;
+  uint32_t* XP = reinterpret_cast<uint32_t*>(X + NS);  // P[t]            (upper half of X)
+  uint32_t* XC = reinterpret_cast<uint32_t*>(X);       // prefix counts   (lower half, later)
+  // ---- 1. <= NS samples of A in X[0, NS)
+  const uint32_t S = a > NS ? (a + NS - 1) / NS : 1u;
+  const uint32_t ns = a ? (a + S - 1) / S : 0u;
+  for (uint32_t sidx = lane; sidx < ns; sidx += 32) X[sidx] = ldcg64(A + uint64_t(sidx) * S);
+  __syncwarp();
+  uint32_t dupm = 0;
+#pragma unroll
+  for (int g0 = 0; g0 < R; g0 += G) {
+    uint32_t lo[G], hi[G];
+    uint64_t f[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const uint32_t t = lane + 32 * (g0 + q);
+      f[q] = t < b ? F[t] : NONE64;
+      uint32_t l = 0, h = ns;  // l = #samples < f; the answer lies in (l-1)*S+1 .. min(a, l*S)
+      while (l < h) {
+        const uint32_t m = (l + h) >> 1;
+        if (X[m] < f[q]) l = m + 1;
+        else h = m;
+      }
+      lo[q] = l ? (l - 1) * S + 1 : 0u;
+      hi[q] = l ? min(a, l * S) : 0u;
+      if (t >= b) lo[q] = hi[q] = 0;
+    }
+    bool busy = true;
+    while (busy) {  // interleaved binary searches: lower_bound of f in A[lo, hi)
+      busy = false;
+      uint64_t v[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+        if (lo[q] < hi[q]) v[q] = ldcg64(A + ((lo[q] + hi[q]) >> 1));
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+        if (lo[q] < hi[q]) {
+          const uint32_t m = (lo[q] + hi[q]) >> 1;
+          if (v[q] < f[q]) lo[q] = m + 1;
+          else hi[q] = m;
+          busy |= lo[q] < hi[q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const uint32_t t = lane + 32 * (g0 + q);
+      if (t < b) {
+        if (lo[q] < a && ldcg64(A + lo[q]) == f[q]) dupm |= 1u << (g0 + q);
+        XP[t] = lo[q];
+      }
+    }
+  }
+  __syncwarp();  // the samples are dead: XC takes the lower half
+  uint32_t totI = 0, totD = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t t = lane + 32 * r;
+    const bool valid = t < b, dup = dupm >> r & 1;
+    const unsigned bi = __ballot_sync(0xFFFFFFFFu, valid && !dup);
+    const unsigned bd = __ballot_sync(0xFFFFFFFFu, valid && dup);
+    const uint32_t ci = totI + __popc(bi & lt), cd = totD + __popc(bd & lt);
+    if (valid) {
+      XC[t] = (uint32_t(dup) << 31) | (cd << 16) | ci;
+      if (!dup) C[XP[t] + ci - cd] = F[t];  // 2. the inserted F entries
+    }
+    totI += __popc(bi);
+    totD += __popc(bd);
+  }
+  __syncwarp();
+  // ---- 3. stream A
+  auto lower_p = [&](uint32_t x) {  // #t with P[t] < x
+    uint32_t l = 0, h = b;
+    while (l < h) {
+      const uint32_t m = (l + h) >> 1;
+      if (XP[m] < x) l = m + 1;
+      else h = m;
+    }
+    return l;
+  };
+  for (uint32_t w0 = 0; w0 < a; w0 += 256) {
+    uint64_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = w0 + lane + 32 * k;
+      v[k] = i < a ? ldcg64(A + i) : 0ull;
+    }
+    const uint32_t tl = lower_p(w0), th = lower_p(w0 + 256);
+    const uint32_t cl = tl < b ? XC[tl] & 0x7FFFFFFFu : ((totD << 16) | totI);
+    const uint32_t baseI = cl & 0xFFFFu, baseD = cl >> 16;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = w0 + lane + 32 * k;
+      if (i >= a) continue;
+      uint32_t ins = baseI, rem = baseD;
+      bool removed = false;
+      for (uint32_t t = tl; t < th; ++t) {
+        const uint32_t pt = XP[t];
+        const bool dup = XC[t] >> 31;
+        if (!dup && pt <= i) ++ins;
+        if (dup && pt < i) ++rem;
+        if (dup && pt == i) removed = true;
+      }
+      if (!removed) C[i + ins - rem] = v[k];
+    }
+  }
+  __syncwarp();
+  return a + totI - totD;
+}
+
 // M <- M[h:] xor F[f0:]   (returns false on capacity overflow)
 __device__ bool flush(Col& c, uint32_t mcap, int lane) {
   const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
   if (nb == 0) return true;
   if (na + nb > mcap) return false;
-  const uint32_t n = merge_chunked<false>(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
-                                          c.M[c.mb ^ 1], c.F[c.fb ^ 1], nullptr, lane);
+  const uint32_t n = merge_long_short(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
+                                      c.M[c.mb ^ 1], c.F[c.fb ^ 1], lane);
   c.mb ^= 1;
   c.nm = n;
   c.h = 0;
@@ -282,7 +409,7 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, uint32_t mcap
   return true;
 }
 
-__global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
+__global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s_F[WPB][2][FCAP];
   __shared__ uint64_t s_small[WPB][8];
@@ -379,6 +506,10 @@ __global__ void __launch_bounds__(THREADS) k_reduce(RP P) {
         atomicAdd(P.stats + 1, adds);
         atomicAdd(P.stats + 2, addlen);
         atomicMax(P.stats + 3, (unsigned long long)c.len());
+        if (P.colstat) {
+          P.colstat[2 * j] += adds;
+          P.colstat[2 * j + 1] += addlen;
+        }
       }
       if (ok && !ready && cval == NONE64) {  // zero column: essential (exact given clearing)
         fin = true;
@@ -590,6 +721,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     unsigned long long pool_cap = std::max<unsigned long long>(8ull * ncols + 4096, 1ull << 20);
     uint64_t* work = nullptr;
     uint64_t* pool = nullptr;
+    unsigned long long* P_colstat = nullptr;
     for (int attempt = 0;; ++attempt) {
       if (!work) work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
@@ -624,6 +756,12 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.max_steps = 256;
       P.stats = stats;
       P.debug = std::getenv("CR_DEBUG_STATS") != nullptr;
+      P.colstat = nullptr;
+      if (P.debug) {
+        if (!P_colstat) P_colstat = ws.alloc<unsigned long long>(2 * int64_t(ncols));
+        P.colstat = P_colstat;
+        CR_CUDA(cudaMemsetAsync(P.colstat, 0, 2 * sizeof(unsigned long long) * ncols, s));
+      }
       void* args[] = {&P};
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, 0, s));
@@ -649,11 +787,35 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     st.additions[d] = int64_t(hs.p[7]);
     st.addlen[d] = int64_t(hs.p[8]);
     st.maxlen[d] = int64_t(hs.p[9]);
-    if (std::getenv("CR_DEBUG_STATS"))
+    if (std::getenv("CR_DEBUG_STATS")) {
+      std::vector<unsigned long long> cs(2 * size_t(ncols));
+      CR_CUDA(cudaMemcpy(cs.data(), P_colstat, cs.size() * 8, cudaMemcpyDeviceToHost));
+      std::vector<std::pair<unsigned long long, uint32_t>> byent(ncols);
+      unsigned long long tot = 0;
+      for (uint32_t j = 0; j < ncols; ++j) {
+        byent[j] = {cs[2 * j + 1], j};
+        tot += cs[2 * j + 1];
+      }
+      std::sort(byent.rbegin(), byent.rend());
+      unsigned long long acc = 0;
+      const uint32_t marks[5] = {1, 10, 100, 1000, 10000};
+      fprintf(stderr, "[cr] dim %d entry work: total %llu;", d, tot);
+      for (uint32_t m : marks) {
+        if (m > ncols) break;
+        acc = 0;
+        for (uint32_t q = 0; q < m; ++q) acc += byent[q].first;
+        fprintf(stderr, " top%u %.3f", m, tot ? double(acc) / tot : 0.0);
+      }
+      fprintf(stderr, "\n[cr] top columns (pos, adds, entries):");
+      for (int q = 0; q < 8 && q < int(ncols); ++q)
+        fprintf(stderr, " (%u,%llu,%llu)", byent[q].second, cs[2 * byent[q].second],
+                byent[q].first);
+      fprintf(stderr, "\n");
       fprintf(stderr,
               "[cr] dim %d: cols %u rounds %llu adds %llu pool_adds %llu pool_len %llu "
               "cyc_pool %llu cyc_app %llu cyc_lookup %llu W %u\n",
               d, ncols, hs.p[6], hs.p[7], hs.p[10], hs.p[11], hs.p[13], hs.p[14], hs.p[15], W);
+    }
     ws.release(work);
     ws.release(pool);
     ws.release(owner);
