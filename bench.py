@@ -245,7 +245,17 @@ def run_ours(args, rank, world, local_rank):
     K_basins = st["columns"][0]
     stage_avg = {k: v / args.steps for k, v in stage_tot.items()}
     dom = max(stage_avg, key=stage_avg.get) if stage_avg else None
-    alg = algorithmic_bytes(args.config, dom, nvox_local, st, n_out)
+    alg = algorithmic_bytes(args.config, dom, nvox_local, st, n_out,
+                            None if batched else tuple(host_img.shape))
+    # the filtration (K1) and apparent-pair (K2) kernels' achieved bandwidth (BASELINE north_star)
+    k1k2 = None
+    if not batched and "births" in stage_avg and "apparent" in stage_avg:
+        k1k2 = {}
+        for name in ("births", "apparent"):
+            b = algorithmic_bytes(args.config, name, nvox_local, st, n_out, tuple(host_img.shape))
+            gbs = b / (stage_avg[name] / 1e3) / 1e9
+            k1k2[name] = {"ms": round(stage_avg[name], 4), "alg_bytes": b,
+                          "achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm, 4)}
     roof = None
     if dom and alg:
         ach = alg / (stage_avg[dom] / 1e3) / 1e9
@@ -265,6 +275,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed before every timed step (256 MiB write, outside the events)",
                    "bars_per_step": n_out},
         "roofline": roof,
+        "k1_k2": k1k2,
         "stages_ms": {k: round(v, 5) for k, v in stage_avg.items()},
         "clocks": clocks,
         "e2e": e2e,
@@ -276,7 +287,7 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def algorithmic_bytes(cfg, stage, nvox, st, n_out):
+def algorithmic_bytes(cfg, stage, nvox, st, n_out, shape=None):
     """Bytes a stage must move once."""
     K = st["columns"][0]
     if stage is None:
@@ -295,13 +306,19 @@ def algorithmic_bytes(cfg, stage, nvox, st, n_out):
         return 28 * K + 12 * n_out                # read keys/death/cells, write bars
     if stage.startswith("1d_tree"):
         return 32 * K                             # read level 0, write levels >= 1 (~K)
-    if stage == "births":
-        cells = sum(st["cells"])
-        return 4 * nvox + 4 * cells
-    if stage == "apparent":
-        cells = sum(st["cells"])
-        return 5 * cells
+    kcells = khalimsky_cells(shape) if shape else sum(st["cells"])
+    if stage == "births":                         # read the image, write every Khalimsky cell
+        return 4 * nvox + 4 * kcells
+    if stage == "apparent":                       # read the births, write a tag per cell
+        return 5 * kcells
     return None
+
+
+def khalimsky_cells(shape):
+    n = 1
+    for v in shape:
+        n *= 2 * int(v) - 1
+    return n
 
 
 def cpu_baseline(cfg, host_img, maxdim):

@@ -222,6 +222,7 @@ struct Stage {
   int64_t cap;
   unsigned long long* cnt;    // [0] undecided basins exported, [1] decided later, [2] of them
                               // zero-persistence (holes in the output)
+  uint32_t* ltiles0;          // level-1 tile count for the item levels (written by tile 0)
 };
 
 constexpr uint32_t BAR_PENDING = 0x7FC00001u;  // NaN payload marking an undecided death
@@ -559,6 +560,7 @@ __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x
   WarpScratch& SC = reinterpret_cast<WarpScratch*>(smem)[w];
   const uint32_t t = blockIdx.x;
   const int64_t a = int64_t(t) * L1_TILE;
+  if (t == 0 && threadIdx.x == 0) *G.ltiles0 = gridDim.x;
   const int64_t b0 = a + int64_t(w) * L1_SPW;                    // region start
   const uint64_t rslot = (uint64_t(t) * L1_WARPS + w) * L1_IPW;  // region's first slot
   const bool left_start = (t == 0 && w == 0);
@@ -1054,15 +1056,22 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     tiles[l] = std::max<int64_t>(1, (items + ITILE - 1) / ITILE);
     items = std::max<int64_t>(ITILE, items / 16);
   }
-  int* flags = ws.alloc<int>(4);  // nan, overflow, bad, total bars
-  CR_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
+  ws.use_arena();
   Stage G;
   const int nreg = nt1 * L1_WARPS;
+  // control block, zeroed by one memset and read back by one copy:
+  //   [0, 2) u64: flags (int nan, int overflow), [2, 6): counters, total bars,
+  //   [6, 7 + NLEVELS): gather chunk counter + level flags (u32), then holes per region (u32)
+  constexpr int CTL_HEAD = 7 + NLEVELS;
+  const size_t ctl_bytes = CTL_HEAD * sizeof(unsigned long long) + (nreg + 1) * sizeof(uint32_t);
+  unsigned long long* ctl = static_cast<unsigned long long*>(ws.alloc_bytes(ctl_bytes));
+  CR_CUDA(cudaMemsetAsync(ctl, 0, ctl_bytes, s));
+  int* flags = reinterpret_cast<int*>(ctl);  // nan, overflow
+  unsigned long long* meta = ctl + 2;
+  G.holes = reinterpret_cast<uint32_t*>(ctl + CTL_HEAD);
   G.st = ws.alloc<uint2>(int64_t(nreg) * L1_IPW);
   G.cell = out_cells ? ws.alloc<uint32_t>(int64_t(nreg) * L1_IPW) : nullptr;
   G.rcnt = ws.alloc<uint32_t>(nreg + 1);
-  G.holes = ws.alloc<uint32_t>(nreg + 1);
-  CR_CUDA(cudaMemsetAsync(G.holes, 0, (nreg + 1) * sizeof(uint32_t), s));
   Items L[NLEVELS + 1];
   for (int l = 0; l <= NLEVELS; ++l) {
     const int64_t cap_items = tiles[l] * int64_t(MAXITEMS);
@@ -1072,10 +1081,24 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     L[l].cnt = ws.alloc<uint32_t>(tiles[l]);
     L[l].lead = ws.alloc<uint64_t>(tiles[l]);
   }
-  CR_CUDA(cudaFuncSetAttribute(k1_level1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(L1_SMEM)));
-  CR_CUDA(cudaFuncSetAttribute(k1_levels_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(SMEM)));
+  // per-device launch facts, cached per host thread
+  struct DevFacts {
+    bool ok = false;
+    int nsm = 0, per_sm = 0;
+  };
+  static thread_local DevFacts facts[64];
+  DevFacts& F = facts[ws.device() & 63];
+  if (!F.ok) {
+    CR_CUDA(cudaFuncSetAttribute(k1_level1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(L1_SMEM)));
+    CR_CUDA(cudaFuncSetAttribute(k1_levels_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(SMEM)));
+    CR_CUDA(cudaDeviceGetAttribute(&F.nsm, cudaDevAttrMultiProcessorCount, ws.device()));
+    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&F.per_sm, k1_levels_coop, THREADS,
+                                                          SMEM));
+    if (F.per_sm < 1) throw Error{CR_EINTERNAL, "k1_levels_coop cannot be resident"};
+    F.ok = true;
+  }
   if (const char* e = std::getenv("CR_1D_ROUNDS")) {  // tuning knob (not part of the ABI)
     const int v = std::atoi(e);
     CR_CUDA(cudaMemcpyToSymbolAsync(g_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
@@ -1087,15 +1110,14 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   G.out = out;
   G.out_cells = out_cells;
   G.cap = cap;
-  // counters, total bars, gather chunk counter + level flags: one memset
-  unsigned long long* meta = ws.alloc<unsigned long long>(4 + NLEVELS + 1);
-  CR_CUDA(cudaMemsetAsync(meta, 0, (4 + NLEVELS + 1) * sizeof(unsigned long long), s));
   G.cnt = meta;
   G.regoff = ws.alloc<uint32_t>(nreg);
+  LevelsArgs LA{};
+  LA.ltiles = ws.alloc<uint32_t>(NLEVELS + 2);  // [0] = nt1, written by k1_level1
+  G.ltiles0 = LA.ltiles;
   k1_level1<<<nt1, THREADS, L1_SMEM, s>>>(x, n, L[0], G, flags + 0, flags + 1);
   CR_CHECK_LAUNCH();
   prof_mark(s, "1d_level1");
-  LevelsArgs LA{};
   for (int l = 1; l <= NLEVELS; ++l) {
     uint32_t* prefix = nt1 > 1 ? ws.alloc<uint32_t>(tiles[l - 1] + 1) : nullptr;
     LA.in[l - 1] = LevelIn{L[l - 1].key, L[l - 1].rb, L[l - 1].id, L[l - 1].cnt, L[l - 1].lead,
@@ -1103,34 +1125,24 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     LA.out[l - 1] = L[l];
     LA.cap_tiles[l - 1] = tiles[l];
   }
-  LA.ltiles = ws.alloc<uint32_t>(NLEVELS + 2);
-  const uint32_t nt1u = uint32_t(nt1);
-  CR_CUDA(cudaMemcpyAsync(LA.ltiles, &nt1u, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   LA.G = G;
   LA.overflow = flags + 1;
   LA.levels = nt1 > 1;
   LA.nreg = nreg;
   LA.total = meta + 3;
-  LA.gctr = reinterpret_cast<uint32_t*>(meta + 4);
-  LA.done = LA.gctr + 1;  // 2 * NLEVELS words
-  int dev = 0, nsm = 0, per_sm = 0;
-  CR_CUDA(cudaGetDevice(&dev));
-  CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_levels_coop, THREADS, SMEM));
-  if (per_sm < 1) throw Error{CR_EINTERNAL, "k1_levels_coop cannot be resident"};
+  LA.gctr = reinterpret_cast<uint32_t*>(ctl + 6);
+  LA.done = LA.gctr + 1;  // 2 * NLEVELS - 1 words up to the holes
   // item levels are small (a random walk leaves ~0.5 % of basins undecided per tile); the gather
   // streams every bar: a few CTAs per SM keep enough loads in flight
   const int64_t blocks = std::max<int64_t>(
-      1, std::min<int64_t>(int64_t(nsm) * std::min(per_sm, 2), (nreg + 7) / 8));
+      1, std::min<int64_t>(int64_t(F.nsm) * std::min(F.per_sm, 2), (nreg + 7) / 8));
   LA.part = ws.alloc<uint32_t>(blocks);
   void* args[] = {&LA};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k1_levels_coop, dim3(unsigned(blocks)),
                                       dim3(THREADS), args, SMEM, s));
   ++g_launch_count;
   prof_mark(s, "1d_levels_gather");
-  CR_CUDA(cudaMemcpyAsync(hs.p, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-  CR_CUDA(cudaMemcpyAsync(hs.p + 2, meta, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          s));
+  CR_CUDA(cudaMemcpyAsync(hs.p, ctl, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
   const int* hf = reinterpret_cast<const int*>(hs.p);
   const unsigned long long exported = hs.p[2], decided = hs.p[3], late_holes = hs.p[4];

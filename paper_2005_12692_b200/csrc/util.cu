@@ -67,23 +67,59 @@ void prof_end(cr_stats& st) {
   }
 }
 
+namespace {
+struct Arena {
+  void* base = nullptr;
+  size_t cap = 0;
+};
+constexpr int MAX_DEV = 64;
+thread_local Arena g_arena[MAX_DEV];
+thread_local bool g_pool_set[MAX_DEV] = {};
+}  // namespace
+
 Workspace::Workspace(cudaStream_t s) : s_(s) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) {
+  if (cudaGetDevice(&dev_) != cudaSuccess || dev_ < 0 || dev_ >= MAX_DEV) dev_ = 0;
+  if (!g_pool_set[dev_]) {  // keep freed blocks in the default pool (once per thread and device)
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, dev_) == cudaSuccess) {
       uint64_t thr = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    g_pool_set[dev_] = true;
   }
 }
 
 Workspace::~Workspace() {
   for (void* p : ptrs_)
     if (p) cudaFreeAsync(p, s_);
+  if (arena_ && need_ > acap_) {  // grow the arena to this call's high-water mark
+    Arena& A = g_arena[dev_];
+    if (A.base) cudaFreeAsync(A.base, s_);
+    A.base = nullptr;
+    A.cap = 0;
+    const size_t cap = need_ + need_ / 4;
+    if (cudaMallocAsync(&A.base, cap, s_) == cudaSuccess) A.cap = cap;
+    else A.base = nullptr, cudaGetLastError();
+  }
+}
+
+void Workspace::use_arena() {
+  arena_ = true;
+  abase_ = static_cast<char*>(g_arena[dev_].base);
+  acap_ = g_arena[dev_].cap;
+  aoff_ = need_ = 0;
 }
 
 void* Workspace::alloc_bytes(size_t bytes) {
+  if (arena_) {
+    const size_t b = (bytes + 255) & ~size_t(255);
+    need_ += b;
+    if (aoff_ + b <= acap_) {
+      void* p = abase_ + aoff_;
+      aoff_ += b;
+      return p;
+    }
+  }
   void* p = nullptr;
   CR_CUDA(cudaMallocAsync(&p, bytes, s_));
   ptrs_.push_back(p);
