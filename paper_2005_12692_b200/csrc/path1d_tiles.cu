@@ -41,7 +41,11 @@ constexpr uint64_t KEY_NONE = 0;  // no barrier / unknown barrier: neutral for m
 
 constexpr int THREADS = 256;
 constexpr int MAXITEMS = 512;           // items per CTA buffer (level-1 residual, level-k tile)
-constexpr int ITILE = MAXITEMS;         // items per level-k tile
+#ifndef CR_1D_ITILE
+#define CR_1D_ITILE 512
+#endif
+constexpr int ITILE = CR_1D_ITILE;      // items per level-k tile (<= MAXITEMS)
+static_assert(ITILE <= MAXITEMS, "level tiles fit the CTA buffers");
 constexpr int L1_WARPS = THREADS / 32;
 constexpr int L1_SPW = 512;             // level-1 samples per warp region
 constexpr int L1_TILE = L1_WARPS * L1_SPW;  // level-1 samples per CTA
@@ -822,15 +826,43 @@ __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, con
   const int P = I.ntiles;
   const uint32_t k0 = t * ITILE;
   const int n = int(total - k0 < uint32_t(ITILE) ? total - k0 : uint32_t(ITILE));
-  // gather items k0..k0+n-1 (and item k0-1's barrier) from the previous level's tile regions
+  // gather items k0..k0+n-1 (and item k0-1's barrier) from the previous level's tile regions;
+  // the source tile of item g is the last i with prefix[i] <= g.  The prefix segment covering the
+  // tile's items is staged in shared memory (two global searches instead of one per item).
+  constexpr int PSEG = 2048;
   __shared__ uint64_t s_lead0;
+  __shared__ uint32_t s_pref[PSEG];
+  __shared__ int s_plo, s_pn;
+  auto src_tile = [&](uint32_t g) {
+    int lo = 0, hi = P - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldcg(I.prefix + mid) <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  if (threadIdx.x == 0) {
+    const int a = src_tile(k0 > 0 ? k0 - 1 : 0), b = src_tile(k0 + uint32_t(n) - 1);
+    s_plo = a;
+    s_pn = b - a + 1 <= PSEG ? b - a + 1 : 0;  // 0: too wide, search globally
+  }
+  __syncthreads();
+  const int plo = s_plo, pn = s_pn;
+  for (int i = threadIdx.x; i < pn; i += THREADS) s_pref[i] = __ldcg(I.prefix + plo + i);
+  __syncthreads();
   for (int j = int(threadIdx.x) - 1; j < n; j += THREADS) {
     if (j < 0 && k0 == 0) continue;
     const uint32_t g = k0 + j;  // j = -1: the item left of the tile
-    int lo = 0, hi = P - 1;     // source tile: last i with prefix[i] <= g
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (I.prefix[mid] <= g) lo = mid; else hi = mid - 1;
+    int lo;
+    if (pn) {
+      int l = 0, h = pn - 1;
+      while (l < h) {
+        const int mid = (l + h + 1) >> 1;
+        if (s_pref[mid] <= g) l = mid; else h = mid - 1;
+      }
+      lo = plo + l;
+    } else {
+      lo = src_tile(g);
     }
     const uint32_t r = g - I.prefix[lo];
     const uint64_t src = uint64_t(lo) * MAXITEMS + r;
