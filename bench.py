@@ -263,6 +263,7 @@ def run_ours(args, rank, world, local_rank):
                 "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
                 "alg_bytes_per_launch": alg, "avg_ms": round(stage_avg[dom], 5),
                 "peak_source": peak_src}
+        roof.update(ncu_traffic(dom))
     out = {
         "metric": METRIC, "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -312,6 +313,28 @@ def algorithmic_bytes(cfg, stage, nvox, st, n_out, shape=None):
     if stage == "apparent":                       # read the births, write a tag per cell
         return 5 * kcells
     return None
+
+
+NCU_KERNEL = {"1d_level1": "k1_level1", "1d_levels_gather": "k1_levels_coop"}
+
+
+def ncu_traffic(stage):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu --set full capture
+    (profiles/), or nothing if there is none for it."""
+    import glob
+    k = NCU_KERNEL.get(stage)
+    if not k:
+        return {}
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "*", "ncu_full_*_summary.json")),
+                    reverse=True):
+        try:
+            with open(p) as f:
+                d = json.load(f)["kernels"][k]
+            return {"traffic": round((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6),
+                    "traffic_source": os.path.relpath(p, ROOT)}
+        except (KeyError, OSError, ValueError):
+            continue
+    return {}
 
 
 def khalimsky_cells(shape):
