@@ -97,6 +97,26 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
 cr_status cr_pairing(const float* image, const int64_t* shape, int ndim, uint32_t* partner,
                      cr_stream_t stream);
 
+/* Death cells of bars (the "location ... where it is killed" option of PAPER.md:326-331, 438-441).
+ *   image, shape, ndim  as for cr_barcodes (the same image the bars were computed from).
+ *   birth_cells         device, n uint32: birth-cell kidx of each bar (cr_barcodes' out_birth_cells).
+ *   out_death_cells     device, n uint32: kidx of the cell that kills each bar, CR_PARTNER_ESSENTIAL
+ *                       for essential bars.  Computed from the cell pairing (cr_pairing), so the
+ *                       call costs about one more barcode computation.  The location is unique
+ *                       given the total order (reading R1, R13). */
+cr_status cr_death_cells(const float* image, const int64_t* shape, int ndim,
+                         const uint32_t* birth_cells, int64_t n, uint32_t* out_death_cells,
+                         cr_stream_t stream);
+
+/* Lifetime-enhanced images of `batch` images of identical shape (back to back).
+ *   out    device float32, batch * C * prod(shape), C = 2 + min(maxdim, ndim-1): for image b,
+ *          channel 0 is the image itself and channel 1+d holds, at each voxel, the largest lifetime
+ *          (death - birth) of the dim-d bars whose birth cell has that voxel as its base corner
+ *          (X/2, Y/2, Z/2) -- 0 where no bar is born.  Essential bars use death = inf_value.
+ *   inf_value  the death assigned to essential bars (e.g. the image maximum); NaN -> CR_EINVAL. */
+cr_status cr_lifetime_image(const float* images, int64_t batch, const int64_t* shape, int ndim,
+                            int maxdim, float inf_value, float* out, cr_stream_t stream);
+
 /* Number of cells of dims 0..min(maxdim, ndim-1): a safe out_capacity (each bar has a distinct
  * birth cell).  Returns -1 on invalid shape. */
 int64_t cr_max_pairs(const int64_t* shape, int ndim, int maxdim);

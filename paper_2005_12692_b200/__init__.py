@@ -57,6 +57,11 @@ _lib.cr_barcodes_host.argtypes = [_vp, _i64p, ctypes.c_int, ctypes.c_int, _vp, _
 _lib.cr_barcodes_batched.restype = ctypes.c_int
 _lib.cr_barcodes_batched.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64,
                                      _vp, _i64p, _vp]
+_lib.cr_death_cells.restype = ctypes.c_int
+_lib.cr_death_cells.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _i64, _vp, _vp]
+_lib.cr_lifetime_image.restype = ctypes.c_int
+_lib.cr_lifetime_image.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                   _vp, _vp]
 _lib.cr_pairing.restype = ctypes.c_int
 _lib.cr_pairing.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _vp]
 _lib.cr_max_pairs.restype = _i64
@@ -71,7 +76,8 @@ _lib.cr_set_profiling.restype = None
 _lib.cr_set_profiling.argtypes = [ctypes.c_int]
 
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
-            "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling"]
+            "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling",
+            "cr_death_cells", "cr_lifetime_image"]
 
 
 class CrError(RuntimeError):
@@ -240,3 +246,49 @@ def pairing(image):
                          _stream_ptr(torch, image.device))
     _check(st)
     return part
+
+
+def death_cells(image, birth_cells):
+    """kidx of the cell that kills each bar (PAPER.md:326-331 location="death"), given the bars'
+    birth cells from ``barcodes(..., cells=True)``; 0xFFFFFFFF (as int32 -1) for essential bars."""
+    import torch
+    image = image.contiguous()
+    shape = tuple(image.shape)
+    birth_cells = birth_cells.contiguous()
+    n = int(birth_cells.numel())
+    out = torch.empty((max(n, 1),), dtype=torch.int32, device=image.device)
+    st = _lib.cr_death_cells(image.data_ptr(), _shape(shape), len(shape), birth_cells.data_ptr(), n,
+                             out.data_ptr(), _stream_ptr(torch, image.device))
+    _check(st)
+    return out[:n]
+
+
+def cell_coords(cells, shape):
+    """Khalimsky (X, Y, Z) of cells and their base voxel (x, y, z) = (X//2, Y//2, Z//2) -- the
+    paper's cell location (x, y, z, m).  cells: int64/uint32 array."""
+    s = [1] * (3 - len(shape)) + [int(v) for v in shape]
+    KX, KY = 2 * s[2] - 1, 2 * s[1] - 1
+    k = np.asarray(cells).astype(np.int64) & 0xFFFFFFFF
+    X, Y, Z = k % KX, (k // KX) % KY, k // (KX * KY)
+    return np.stack([X, Y, Z], -1), np.stack([X // 2, Y // 2, Z // 2], -1)
+
+
+def lifetime_image(images, maxdim: int = 2, inf_value: float | None = None, batched: bool = False):
+    """Lifetime-enhanced image(s): channel 0 the image, channel 1+d the largest
+    dim-d lifetime born at each voxel (0 elsewhere).  Essential bars die at ``inf_value``
+    (default: the largest finite value of the input).  Returns (C, *shape), or (B, C, *shape)
+    with ``batched=True`` (images of shape (B, *shape))."""
+    import torch
+    images = images.contiguous()
+    shape = tuple(images.shape[1:] if batched else images.shape)
+    B = int(images.shape[0]) if batched else 1
+    if inf_value is None:
+        fin = images[torch.isfinite(images)]
+        inf_value = float(fin.max().item()) if fin.numel() else 0.0
+    D = sum(1 for v in shape if v > 1)
+    C = 2 + min(int(maxdim), max(D - 1, 0))
+    out = torch.empty((B, C) + shape, dtype=torch.float32, device=images.device)
+    st = _lib.cr_lifetime_image(images.data_ptr(), B, _shape(shape), len(shape), int(maxdim),
+                                float(inf_value), out.data_ptr(), _stream_ptr(torch, images.device))
+    _check(st)
+    return out if batched else out[0]

@@ -29,6 +29,51 @@ bool force_general() {
   return e && e[0] == '1';
 }
 
+// death cell of each bar: the partner of its birth cell ("or optionally, killed")
+__global__ void k_death_cells(const uint32_t* __restrict__ birth_cells, int64_t n,
+                              const uint32_t* __restrict__ partner, uint32_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = partner[birth_cells[i]];
+}
+
+// lifetime-enhanced image: channel 0 = the image, channel 1 + d = per voxel the
+// largest lifetime of the dim-d bars born at a cell whose base voxel (X/2, Y/2, Z/2) it is.
+// Lifetimes are >= 0, so their float bits order like the values (integer atomicMax).
+__global__ void k_lifetime_scatter(const cr_pair* __restrict__ bars, const uint32_t* __restrict__ cells,
+                                   int64_t n, const int64_t* __restrict__ offsets, int64_t batch,
+                                   Geom g, int nch, float inf_value, float* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t b = 0;
+  if (offsets) {  // image of bar i: last b with offsets[b] <= i
+    int64_t lo = 0, hi = batch - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (offsets[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    b = lo;
+  }
+  const cr_pair p = bars[i];
+  const float death = isinf(p.death) ? inf_value : p.death;
+  float life = death - p.birth;
+  if (!(life > 0.f)) life = 0.f;
+  const uint32_t k = cells[i];
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const uint32_t X = k % KX, Y = (k / KX) % KY, Z = k / (KX * KY);
+  const int64_t v = (int64_t(Z >> 1) * g.ny + (Y >> 1)) * g.nx + (X >> 1);
+  float* ch = out + (b * nch + 1 + p.dim) * g.nvox;
+  atomicMax(reinterpret_cast<int*>(ch + v), __float_as_int(life));
+}
+
+__global__ void k_lifetime_init(const float* __restrict__ img, int64_t nvox, int64_t batch, int nch,
+                                float* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nvox * batch) return;
+  const int64_t b = i / nvox, v = i - b * nvox;
+  out[(b * nch) * nvox + v] = img[i];
+  for (int c = 1; c < nch; ++c) out[(b * nch + c) * nvox + v] = 0.f;
+}
+
 cr_status fail(const Error& e) {
   set_error_text(e.msg);
   return e.st;
@@ -368,6 +413,74 @@ cr_status cr_pairing(const float* image, const int64_t* shape, int ndim, uint32_
     CR_CUDA(cudaStreamSynchronize(s));
     g_last_stats = st;
     return CR_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+cr_status cr_death_cells(const float* image, const int64_t* shape, int ndim,
+                         const uint32_t* birth_cells, int64_t n, uint32_t* out_death_cells,
+                         cr_stream_t stream) {
+  if (!image || n < 0 || (n > 0 && (!birth_cells || !out_death_cells)) || !valid_shape(shape, ndim))
+    return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t nc = cr_num_cells(shape, ndim);
+    uint32_t* partner = nullptr;
+    CR_CUDA(cudaMallocAsync(&partner, size_t(nc) * sizeof(uint32_t), s));
+    cr_status r = cr_pairing(image, shape, ndim, partner, stream);
+    if (r == CR_OK && n > 0) {
+      k_death_cells<<<grid_for(n, 256), 256, 0, s>>>(birth_cells, n, partner, out_death_cells);
+      if (cudaGetLastError() != cudaSuccess) r = CR_ECUDA;
+    }
+    cudaFreeAsync(partner, s);
+    if (r == CR_OK) CR_CUDA(cudaStreamSynchronize(s));
+    return r;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+static cr_status lifetime_common(const float* images, int64_t batch, const int64_t* shape,
+                                 int ndim, int maxdim, float inf_value, float* out,
+                                 cudaStream_t s) {
+  const Geom g = make_geom(shape, ndim);
+  const int nch = 2 + report_dmax(g, maxdim);
+  const int64_t cap = cr_max_pairs(shape, ndim, maxdim) * batch;
+  cr_pair* bars = nullptr;
+  uint32_t* cells = nullptr;
+  int64_t* offs = nullptr;
+  CR_CUDA(cudaMallocAsync(&bars, size_t(cap + 1) * sizeof(cr_pair), s));
+  CR_CUDA(cudaMallocAsync(&cells, size_t(cap + 1) * sizeof(uint32_t), s));
+  if (batch > 1) CR_CUDA(cudaMallocAsync(&offs, size_t(batch + 1) * sizeof(int64_t), s));
+  int64_t n = 0;
+  cr_status r = batch > 1
+                    ? cr_barcodes_batched(images, batch, shape, ndim, maxdim, bars, cells, cap, offs,
+                                          &n, reinterpret_cast<cr_stream_t>(s))
+                    : cr_barcodes(images, shape, ndim, maxdim, bars, cells, cap, &n,
+                                  reinterpret_cast<cr_stream_t>(s));
+  if (r == CR_OK) {
+    k_lifetime_init<<<grid_for(g.nvox * batch, 256), 256, 0, s>>>(images, g.nvox, batch, nch, out);
+    if (n > 0)
+      k_lifetime_scatter<<<grid_for(n, 256), 256, 0, s>>>(bars, cells, n, offs, batch, g, nch,
+                                                          inf_value, out);
+    if (cudaGetLastError() != cudaSuccess) r = CR_ECUDA;
+  }
+  cudaFreeAsync(bars, s);
+  cudaFreeAsync(cells, s);
+  if (offs) cudaFreeAsync(offs, s);
+  if (r == CR_OK) CR_CUDA(cudaStreamSynchronize(s));
+  return r;
+}
+
+cr_status cr_lifetime_image(const float* images, int64_t batch, const int64_t* shape, int ndim,
+                            int maxdim, float inf_value, float* out, cr_stream_t stream) {
+  if (!images || !out || batch < 1 || maxdim < 0 || !valid_shape(shape, ndim) ||
+      inf_value != inf_value)
+    return CR_EINVAL;
+  try {
+    return lifetime_common(images, batch, shape, ndim, maxdim, inf_value, out,
+                           reinterpret_cast<cudaStream_t>(stream));
   } catch (const Error& e) {
     return fail(e);
   }

@@ -74,6 +74,7 @@ struct RP {
                               // pool/apparent additions [9] cycles in pivot + owner lookups
   int debug;
   unsigned long long* colstat;  // debug: per column (additions, entries touched)
+  int prefetch;                 // warm next pivots' lookups (CR_K5_PREFETCH=1; measured no gain)
 };
 
 __device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
@@ -455,6 +456,23 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         const uint64_t piv = take_pivot(c);
         if (piv == NONE64) break;
         const uint32_t pk = key_kidx(piv);
+        if (P.prefetch && lane >= 1 && lane <= 12) {
+          // warm the lookups of the column's next entries (the likely next pivots): their tag and
+          // owner lines, so that the dependent chain of the next additions hits L2
+          uint64_t e = NONE64;
+          if (lane <= 6) {
+            const uint32_t i = c.h + lane;
+            if (i < c.nm) e = ldcg64(c.M[c.mb] + i);
+          } else {
+            const uint32_t i = c.f0 + uint32_t(lane - 6);
+            if (i < c.nf) e = c.F[c.fb][i];
+          }
+          if (e != NONE64) {
+            const uint32_t ek = key_kidx(e);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.tags + ek));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.owner + ek));
+          }
+        }
         const uint8_t t = __ldg(P.tags + pk);
         const uint64_t* add;
         uint32_t alen;
@@ -757,6 +775,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.stats = stats;
       P.debug = std::getenv("CR_DEBUG_STATS") != nullptr;
       P.colstat = nullptr;
+      P.prefetch = std::getenv("CR_K5_PREFETCH") != nullptr;
       if (P.debug) {
         if (!P_colstat) P_colstat = ws.alloc<unsigned long long>(2 * int64_t(ncols));
         P.colstat = P_colstat;

@@ -302,3 +302,51 @@ def test_batched_small_2d_vs_oracle_and_stacked(cr, monkeypatch):
         for i in range(shp[0]):
             s = slice(o3[i], o3[i + 1])
             assert_bars_equal(tuple(y[s] for y in d3), oracle.ph(x[i], 0), ctx=(shp, i))
+
+
+# ---------------------------------------------------------------- NEXT-2 / NEXT-4
+
+def test_death_cells_and_coords(cr):
+    """Death locations (location="death") equal the oracle's partner of each
+    bar's birth cell; cell_coords decodes kidx."""
+    import torch
+    for img, md in [(gen.small_int_image((13, 17), 4, seed=31, inf_frac=0.05), 1),
+                    (gen.masked_grf((12, 14, 16), 2.0, 7.0, 32), 2),
+                    (gen.random_walk(9000, seed=33), 0)]:
+        o = oracle.ph(img, md, partner=True)
+        t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        bc = cr.barcodes(t, md, cells=True)
+        births = bc.cells.cpu().numpy().view(np.uint32)
+        deaths = cr.death_cells(t, bc.cells).cpu().numpy().view(np.uint32)
+        assert np.array_equal(deaths, o.partner[births])
+        ess = deaths == 0xFFFFFFFF
+        assert np.array_equal(ess, np.isinf(bc.numpy()[2]))
+        K, v = cr.cell_coords(births, img.shape)
+        s = [1] * (3 - img.ndim) + list(img.shape)
+        KX, KY = 2 * s[2] - 1, 2 * s[1] - 1
+        assert np.array_equal((K[:, 2] * KY + K[:, 1]) * KX + K[:, 0], births.astype(np.int64))
+        assert np.array_equal(v, K // 2)
+
+
+def test_lifetime_image(cr):
+    """Lifetime-enhanced image equals a numpy scatter-max of the oracle's bars
+    at their birth cells' base voxels; the TTK 3x3 example puts lifetime 9 in channel 2."""
+    import torch
+    g = json.load(open(os.path.join(GOLDEN, "ttk_3x3.json")))
+    img = np.array(g["image"], np.float32)
+    li = cr.lifetime_image(torch.from_numpy(img).cuda(), 1, inf_value=9.0).cpu().numpy()
+    assert li.shape == (3, 3, 3) and np.array_equal(li[0], img)
+    assert li[2].max() == 9.0 and li[1].max() == 9.0  # H1 bar [0, 9); essential H0 [0, inf->9)
+    imgs = np.stack([gen.small_int_image((11, 9), 5, seed=40 + i, inf_frac=0.05) for i in range(6)])
+    out = cr.lifetime_image(torch.from_numpy(imgs).cuda(), 1, inf_value=10.0, batched=True)
+    out = out.cpu().numpy()
+    for b in range(len(imgs)):
+        o = oracle.ph(imgs[b], 1)
+        ref = np.zeros((3,) + imgs[b].shape, np.float32)
+        ref[0] = imgs[b]
+        KX = 2 * imgs[b].shape[1] - 1
+        for d, bi, de, c in zip(o.dim, o.birth, o.death, o.cell):
+            life = (10.0 if np.isinf(de) else de) - bi
+            y, x = (int(c) // KX) // 2, (int(c) % KX) // 2
+            ref[1 + d, y, x] = max(ref[1 + d, y, x], life)
+        assert np.array_equal(out[b], ref), b
