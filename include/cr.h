@@ -73,6 +73,15 @@ cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int ma
                       cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
                       int64_t* n_pairs, cr_stream_t stream);
 
+/* The top dimension alone (dim D-1 for an image with D axes of extent > 1, D >= 2): the paper's
+ * "--top_dim" mode, computed by Alexander duality as a union-find on the dual
+ * graph (top cells and the outside as vertices, (D-1)-cells as edges in decreasing birth) -- no
+ * H0 and no lower-dimensional reduction.  Arguments and output order as for cr_barcodes; the bars
+ * equal cr_barcodes' dim-(D-1) bars.  CR_EINVAL if D < 2.  cr_stats.path = 6. */
+cr_status cr_barcodes_topdim(const float* image, const int64_t* shape, int ndim,
+                             cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
+                             int64_t* n_pairs, cr_stream_t stream);
+
 /* Same as cr_barcodes with HOST image and HOST outputs: the library copies the image in and the
  * bars out on `stream` (end-to-end entry point; pinned host memory is fastest). */
 cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int ndim, int maxdim,
@@ -137,7 +146,7 @@ typedef struct {
   int64_t pairs[4];       /* bars with death > birth per dim                        */
   int64_t essential[4];   /* essential bars per dim                                 */
   int64_t path;           /* 1 = 1D tiles, 2 = general, 3 = batched (stacked), 4 = 1D tree,
-                             5 = batched small 2D (one CTA per image)                    */
+                             5 = batched small 2D (one CTA per image), 6 = top dimension only */
   int32_t nstages;        /* stages timed (only when profiling is enabled)            */
   float stage_ms[16];     /* device time of each stage, CUDA events on the call's stream */
   char stage_name[16][24];

@@ -57,6 +57,8 @@ _lib.cr_barcodes_host.argtypes = [_vp, _i64p, ctypes.c_int, ctypes.c_int, _vp, _
 _lib.cr_barcodes_batched.restype = ctypes.c_int
 _lib.cr_barcodes_batched.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64,
                                      _vp, _i64p, _vp]
+_lib.cr_barcodes_topdim.restype = ctypes.c_int
+_lib.cr_barcodes_topdim.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _vp, _i64, _i64p, _vp]
 _lib.cr_death_cells.restype = ctypes.c_int
 _lib.cr_death_cells.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _i64, _vp, _vp]
 _lib.cr_lifetime_image.restype = ctypes.c_int
@@ -77,7 +79,7 @@ _lib.cr_set_profiling.argtypes = [ctypes.c_int]
 
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
             "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling",
-            "cr_death_cells", "cr_lifetime_image"]
+            "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim"]
 
 
 class CrError(RuntimeError):
@@ -292,3 +294,22 @@ def lifetime_image(images, maxdim: int = 2, inf_value: float | None = None, batc
                                 float(inf_value), out.data_ptr(), _stream_ptr(torch, images.device))
     _check(st)
     return out if batched else out[0]
+
+
+def barcodes_topdim(image, cells: bool = False) -> "Barcode":
+    """Top-dimension bars only (dim D-1; the paper's --top_dim) by Alexander
+    duality.  image: CUDA float32 tensor with >= 2 axes of extent > 1."""
+    import torch
+    image = image.contiguous()
+    shape = tuple(image.shape)
+    D = sum(1 for v in shape if v > 1)
+    cap = max(max_pairs(shape, D - 1) - max_pairs(shape, D - 2), 1)
+    pairs = torch.empty((cap, 3), dtype=torch.int32, device=image.device)
+    cbuf = torch.empty((cap,), dtype=torch.int32, device=image.device) if cells else None
+    n = ctypes.c_int64(0)
+    st = _lib.cr_barcodes_topdim(image.data_ptr(), _shape(shape), len(shape), pairs.data_ptr(),
+                                 cbuf.data_ptr() if cbuf is not None else None, cap,
+                                 ctypes.byref(n), _stream_ptr(torch, image.device))
+    _check(st)
+    m = int(n.value)
+    return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None)

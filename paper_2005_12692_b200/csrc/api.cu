@@ -233,6 +233,36 @@ cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int ma
   }
 }
 
+cr_status cr_barcodes_topdim(const float* image, const int64_t* shape, int ndim,
+                             cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
+                             int64_t* n_pairs, cr_stream_t stream) {
+  if (!image || !n_pairs || !valid_shape(shape, ndim) || out_capacity < 0 ||
+      (out_capacity > 0 && !out_pairs))
+    return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Geom g = make_geom(shape, ndim);
+    if (g.D < 2) return CR_EINVAL;  // the top dimension of a 1D image is H0: use cr_barcodes
+    Workspace ws(s);
+    HostScalars hs;
+    cr_stats st{};
+    prof_begin(s);
+    st.path = 6;
+    GeneralState S;
+    S.top_only = true;
+    run_general(image, g, g.D - 1, ws, hs, S, st);
+    const int64_t n = emit_bars(S, g.D - 1, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
+    CR_CUDA(cudaStreamSynchronize(s));
+    prof_end(st);
+    *n_pairs = n;
+    if (n > out_capacity) return CR_ERANGE;
+    g_last_stats = st;
+    return CR_OK;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
 cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int ndim, int maxdim,
                            cr_pair* host_out_pairs, uint32_t* host_out_birth_cells,
                            int64_t out_capacity, int64_t* n_pairs, cr_stream_t stream) {

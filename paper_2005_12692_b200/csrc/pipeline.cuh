@@ -18,6 +18,7 @@ struct GeneralState {
   uint8_t* tags = nullptr;     // see cr_internal.cuh
   uint32_t seg_cells = 0;      // batched: Khalimsky cells per image period (kidx / seg_cells =
                                // image); 0 for a single image
+  bool top_only = false;       // compute only dimension D-1, by duality (cr_barcodes_topdim)
   Records R;
 };
 

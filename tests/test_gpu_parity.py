@@ -125,6 +125,59 @@ def test_k2_variants_agree(cr, monkeypatch):
             assert np.array_equal(p, o.partner), (k, var, np.flatnonzero(p != o.partner)[:10])
 
 
+def _cavity_cases():
+    rng = np.random.default_rng(50)
+    a = rng.random((20, 22)).astype(np.float32)
+    a[8:12, 9:13] = np.inf                      # enclosed hole: an essential H1 bar
+    b = rng.integers(0, 4, (19, 23)).astype(np.float32)
+    b[3:6, 3:6] = np.inf                        # two holes and one touching the border
+    b[12:15, 15:18] = np.inf
+    b[0:4, 20:23] = np.inf
+    c = gen.grf((12, 13, 14), 1.5, 51)
+    c[5:8, 5:8, 5:9] = np.inf                   # enclosed void: an essential H2 bar
+    d = gen.small_int_image((10, 11, 9), 3, seed=52)
+    d[4:7, 4:7, :] = np.inf                     # a tunnel through the volume: essential H1
+    e = gen.small_int_image((9, 8, 10), 3, seed=53, inf_frac=0.15)
+    f = gen.small_int_image((31, 29), 3, seed=54, inf_frac=0.2)
+    return {"hole2d": a, "holes2d": b, "void3d": c, "tunnel3d": d, "fuzz3d": e, "fuzz2d": f}
+
+
+@pytest.mark.parametrize("name", sorted(_cavity_cases()))
+def test_topdim_duality(cr, monkeypatch, name):
+    """The top dimension by Alexander duality gives the oracle's bars and the
+    same full pairing as the coboundary reduction (CR_TOP_REDUCE=1), incl. essential bars of
+    enclosed +inf cavities."""
+    import torch
+    img = _cavity_cases()[name]
+    md = img.ndim - 1
+    check_image(cr, img, md, ctx=name)
+    t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    p_dual = cr.pairing(t).cpu().numpy()
+    monkeypatch.setenv("CR_TOP_REDUCE", "1")
+    p_red = cr.pairing(t).cpu().numpy()
+    assert np.array_equal(p_dual, p_red)
+
+
+def test_barcodes_topdim(cr):
+    """cr_barcodes_topdim (the paper's --top_dim) returns exactly the oracle's dim-(D-1) bars,
+    birth cells included, with no H0 or lower-dimensional reduction."""
+    import torch
+    cases = dict(_cavity_cases())
+    cases["c1"] = gen.config("c1")[0]
+    cases["c4crop"] = gen.grf((40, 36, 44), 2.0, 4)
+    for name, img in cases.items():
+        D = sum(1 for v in img.shape if v > 1)
+        o = oracle.ph(img, D - 1)
+        sel = o.dim == D - 1
+        bc = cr.barcodes_topdim(torch.from_numpy(np.ascontiguousarray(img)).cuda(), cells=True)
+        d, b, e, c = bc.numpy()
+        assert np.all(d == D - 1), name
+        assert np.array_equal(c, o.cell[sel]), name
+        assert np.array_equal(b.view(np.uint32), o.birth[sel].view(np.uint32)), name
+        assert np.array_equal(e.view(np.uint32), o.death[sel].view(np.uint32)), name
+        assert cr.last_stats()["path"] == 6
+
+
 # ---------------------------------------------------------------- configs (cropped / full)
 
 def test_c1_full(cr):
