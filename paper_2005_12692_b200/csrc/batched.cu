@@ -34,6 +34,7 @@ struct K7Args {
   uint32_t* count;  // bars per image
   int cap;          // bars per image region
   int* flags;       // [0] NaN, [1] overflow
+  int dual;         // dimension 1 by Alexander duality (union-find over squares); else reduction
 };
 
 struct K7Smem {
@@ -259,7 +260,93 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
   const bool do_d1 = A.maxdim >= 1 && nx > 1 && ny > 1;
   if (threadIdx.x == 0) S.nkeys = 0;
   __syncthreads();
-  if (do_d1) {
+  if (do_d1 && A.dual && nvox + 1 <= K7_MAXVOX) {
+    // dimension 1 = the top dimension of a 2D image, by Alexander duality (the
+    // same construction as general.cu's top_dual): squares and the outside OMEGA are the vertices,
+    // residual edges in decreasing key the edges, the root with the larger key survives.  Dual
+    // parents live in S.ord (the voxel ords are dead after step 1).
+    uint32_t* dp = S.ord;
+    const uint32_t OMEGA = uint32_t(nvox);
+    auto sq_of = [&](uint32_t v) -> uint32_t {  // square with base voxel v
+      return (2 * (v / nx) + 1) * KX + 2 * (v % nx) + 1;
+    };
+    auto side = [&](int e, int sg) -> uint32_t {  // dual vertex on side sg of edge e
+      const int X = e % KX, Y = e / KX;
+      int q;
+      if (X & 1) {  // horizontal edge: squares above/below
+        if (sg ? Y + 1 >= KY : Y == 0) return OMEGA;
+        q = e + (sg ? KX : -KX);
+      } else {
+        if (sg ? X + 1 >= KX : X == 0) return OMEGA;
+        q = e + (sg ? 1 : -1);
+      }
+      return uint32_t((q / KX / 2) * nx + (q % KX) / 2);
+    };
+    for (int v = threadIdx.x; v <= nvox; v += K7_THREADS) {
+      uint32_t p = uint32_t(v);
+      if (v < nvox && (v % nx) + 1 < nx && (v / nx) + 1 < ny) {
+        const uint32_t k = sq_of(uint32_t(v));
+        const uint8_t t = S.tags[k];
+        if (S.births[k] != ABSENT_ORD && tag_kind(t) == KIND_DOWN) {
+          const int d = tag_dir(t), off = (d >> 1) == 0 ? 1 : KX;
+          p = side(int(k) + ((d & 1) ? off : -off), d & 1);
+        }
+      }
+      dp[v] = p;
+    }
+    __syncthreads();
+    auto dfind = [&](uint32_t x) {
+      while (true) {
+        const uint32_t q = *(volatile uint32_t*)(dp + x);
+        if (q == x) return x;
+        const uint32_t qq = *(volatile uint32_t*)(dp + q);
+        if (qq != q) atomicCAS(dp + x, q, qq);
+        x = qq;
+      }
+    };
+    for (int k = threadIdx.x; k < N; k += K7_THREADS) {  // absent faces join absent sides
+      const int X = k % KX, Y = k / KX;
+      if (((X & 1) + (Y & 1)) != 1 || S.births[k] != ABSENT_ORD) continue;
+      uint32_t a = side(k, 0), b = side(k, 1);
+      while (true) {
+        a = dfind(a);
+        b = dfind(b);
+        if (a == b) break;
+        if (a > b) { const uint32_t t = a; a = b; b = t; }
+        if (atomicCAS(dp + a, a, b) == a) break;
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < N; k += K7_THREADS) {  // residual edges between components
+      const int X = k % KX, Y = k / KX;
+      if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
+      if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
+      if (dfind(side(k, 0)) != dfind(side(k, 1))) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = cellkey(S, k);
+    }
+    __syncthreads();
+    const uint32_t nc = S.nkeys;
+    k7_sort(S, nc, true);
+    if (threadIdx.x == 0) {
+      auto rkey = [&](uint32_t v) -> uint64_t {
+        return v == OMEGA ? NONE64 : cellkey(S, sq_of(v));
+      };
+      for (uint32_t i = 0; i < nc; ++i) {
+        const uint32_t e = key_kidx(S.tmp.keys[i]);
+        const uint32_t ra = dfind(side(int(e), 0)), rb = dfind(side(int(e), 1));
+        if (ra == rb) continue;  // closes a cycle (a death of dimension 0)
+        const uint64_t ka = rkey(ra), kb = rkey(rb);
+        const uint32_t young = ka < kb ? ra : rb, old = ka < kb ? rb : ra;
+        const uint64_t ky = ka < kb ? ka : kb;
+        dp[young] = old;
+        if (key_ord(ky) == ABSENT_ORD) {
+          S.death[e] = D_ESS;  // two absent regions meet: a hole that never fills
+        } else {
+          const uint32_t by = key_ord(ky);
+          S.death[e] = by > S.births[e] ? by : D_ZERO;
+        }
+      }
+    }
+  } else if (do_d1) {
     for (int k = threadIdx.x; k < N; k += K7_THREADS) {
       const int X = k % KX, Y = k / KX;
       if (((X & 1) + (Y & 1)) == 1 && S.births[k] != ABSENT_ORD &&
@@ -431,6 +518,10 @@ int64_t barcodes_batched_small_2d(const float* images, int64_t batch, int64_t ny
   A.ny = int(ny);
   A.nx = int(nx);
   A.maxdim = maxdim;
+  {
+    const char* e = std::getenv("CR_TOP_REDUCE");
+    A.dual = !(e && e[0] == '1');
+  }
   A.cap = per;
   A.sbar = ws.alloc<uint32_t>(batch * int64_t(per) * 3);
   A.scell = out_cells ? ws.alloc<uint32_t>(batch * int64_t(per)) : nullptr;

@@ -158,6 +158,33 @@ def test_topdim_duality(cr, monkeypatch, name):
     assert np.array_equal(p_dual, p_red)
 
 
+def test_batched_small_2d_dual(cr, monkeypatch):
+    """The one-CTA-per-image path (K7) with dimension 1 by duality equals the oracle and its own
+    reduction variant, on blob images with +inf holes (enclosed and touching the border)."""
+    import torch
+    imgs = gen.blobs(96, 7)
+    rng = np.random.default_rng(8)
+    for i in range(0, 96, 3):
+        y, x = rng.integers(3, 22, 2)
+        imgs[i, y:y + 3, x:x + 4] = np.inf
+    imgs[1, 0:3, 10:14] = np.inf
+    t = torch.from_numpy(imgs).cuda()
+    ba, offa = cr.barcodes_batched(t, 1, cells=True)
+    assert cr.last_stats()["path"] == 5
+    monkeypatch.setenv("CR_TOP_REDUCE", "1")
+    bb, offb = cr.barcodes_batched(t, 1, cells=True)
+    pa, pb = ba.pairs.cpu().numpy(), bb.pairs.cpu().numpy()
+    assert np.array_equal(pa, pb) and np.array_equal(ba.cells.cpu().numpy(), bb.cells.cpu().numpy())
+    off = offa.cpu().numpy()
+    assert np.array_equal(off, offb.cpu().numpy())
+    for i in range(0, 96, 5):
+        o = oracle.ph(imgs[i], 1)
+        seg = pa[off[i]:off[i + 1]]
+        assert np.array_equal(seg[:, 0], o.dim), i
+        assert np.array_equal(seg[:, 1].view(np.uint32), o.birth.view(np.uint32)), i
+        assert np.array_equal(seg[:, 2].view(np.uint32), o.death.view(np.uint32)), i
+
+
 def test_barcodes_topdim(cr):
     """cr_barcodes_topdim (the paper's --top_dim) returns exactly the oracle's dim-(D-1) bars,
     birth cells included, with no H0 or lower-dimensional reduction."""
