@@ -75,6 +75,8 @@ struct RP {
   int debug;
   unsigned long long* colstat;  // debug: per column (additions, entries touched)
   int prefetch;                 // warm next pivots' lookups (CR_K5_PREFETCH=1; measured no gain)
+  int lcache;                   // per-warp lookup cache (CR_K5_CACHE=1; measured no gain: the
+                                // rounds wait on the heaviest column's addition chain)
 };
 
 __device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
@@ -85,8 +87,24 @@ __device__ __forceinline__ uint64_t ld64(const uint64_t* p) {
   return G ? ldcg64(p) : *p;
 }
 
+// Per-warp direct-mapped cache of pivot lookups (tag and owner of a (d+1)-cell), in shared
+// memory.  Owners change only in the commit phase, so the cache is cleared at every round start;
+// tags never change.  Filled by the coboundary enumeration (the cofacets of an apparent partner
+// are the likeliest next pivots) and by the pivot lookups themselves.
+constexpr int LC = 32;
+struct LookupCache {
+  uint32_t key[LC];
+  uint32_t val[LC];  // tag << 24 | owner (0xFFFFFF: none)
+};
+constexpr uint32_t LC_NOOWN = 0xFFFFFFu;
+__device__ __forceinline__ uint32_t lc_pack(uint8_t tag, uint32_t owner) {
+  return (uint32_t(tag) << 24) | (owner == NONE32 ? LC_NOOWN : (owner & LC_NOOWN));
+}
+
 // Finite cofacets of cell s, sorted ascending, written to dst (<= 6 entries).  Warp-collective.
-__device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
+template <bool CACHE = false>
+__device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane,
+                              LookupCache* lc = nullptr) {
   const Geom& g = P.g;
   const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
   const uint32_t c[3] = {s % KX, (s / KX) % KY, s / (KX * KY)};
@@ -98,6 +116,14 @@ __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane)
       const int64_t stv = g.stride(a);
       const uint32_t t = uint32_t(int64_t(s) + (sg ? stv : -stv));
       const uint32_t tb = __ldg(P.births + t);
+      if (CACHE) {  // the cofacet's lookups ride along with its birth (independent loads)
+        const uint8_t tt = __ldg(P.tags + t);
+        const uint32_t to = __ldcg(P.owner + t);
+        if (tb != ABSENT_ORD) {
+          lc->key[t & (LC - 1)] = t;
+          lc->val[t & (LC - 1)] = lc_pack(tt, to);
+        }
+      }
       if (tb != ABSENT_ORD) key = make_key(tb, t);
     }
   }
@@ -366,13 +392,22 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
   return a + totI - totD;
 }
 
+__device__ int g_k5_dbg = 0;                      // CR_DEBUG_STATS: flush counters below
+__device__ unsigned long long g_k5_flush[4];      // flushes, cycles, entries of M, long merges
+
 // M <- M[h:] xor F[f0:]   (returns false on capacity overflow)
 __device__ bool flush(Col& c, uint32_t mcap, int lane) {
   const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
   if (nb == 0) return true;
   if (na + nb > mcap) return false;
+  const long long t0 = g_k5_dbg ? clock64() : 0;
   const uint32_t n = merge_long_short(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
                                       c.M[c.mb ^ 1], c.F[c.fb ^ 1], lane);
+  if (g_k5_dbg && lane == 0) {
+    atomicAdd(g_k5_flush + 0, 1ull);
+    atomicAdd(g_k5_flush + 1, (unsigned long long)(clock64() - t0));
+    atomicAdd(g_k5_flush + 2, (unsigned long long)na);
+  }
   c.mb ^= 1;
   c.nm = n;
   c.h = 0;
@@ -414,6 +449,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s_F[WPB][2][FCAP];
   __shared__ uint64_t s_small[WPB][8];
+  __shared__ LookupCache s_lc[WPB];
   __shared__ uint64_t s_pref[4 * THREADS];
   __shared__ typename SScan::TempStorage s_scan;
   const int lane = threadIdx.x & 31;
@@ -431,7 +467,10 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
   bool started = false, fin = false;
   uint32_t lo = 0;
 
+  LookupCache* lc = &s_lc[wib];
   for (uint32_t round = 0;; ++round) {
+    for (int i = lane; i < LC; i += 32) lc->key[i] = NONE32;  // owners may have changed
+    __syncwarp();
     // ---------------- phase A: advance my column
     if (fin && j < lo) {
       j += W;
@@ -446,7 +485,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         c.mb = c.fb = 0;
         c.h = c.f0 = c.nm = 0;
         c.mstale = true;
-        c.nf = coboundary(P, key_kidx(P.cols[j]), c.F[0], lane);
+        c.nf = coboundary<false>(P, key_kidx(P.cols[j]), c.F[0], lane);
       }
       int steps = 0;
       unsigned long long adds = 0, addlen = 0;
@@ -473,18 +512,31 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
             asm volatile("prefetch.global.L2 [%0];" ::"l"(P.owner + ek));
           }
         }
-        const uint8_t t = __ldg(P.tags + pk);
+        uint8_t t;
+        uint32_t ocached = 0;
+        bool hit = false;
+        if (P.lcache) {
+          const uint32_t ck = lc->key[pk & (LC - 1)];
+          if (ck == pk) {
+            const uint32_t v = lc->val[pk & (LC - 1)];
+            t = uint8_t(v >> 24);
+            ocached = (v & LC_NOOWN) == LC_NOOWN ? NONE32 : (v & LC_NOOWN);
+            hit = true;
+          }
+        }
+        if (!hit) t = __ldg(P.tags + pk);
         const uint64_t* add;
         uint32_t alen;
         bool glob;
         if (tag_kind(t) == KIND_DOWN) {
           // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
           const uint32_t sp = uint32_t(int64_t(pk) + dir_offset(P.g, tag_dir(t)));
-          alen = coboundary(P, sp, s_small[wib], lane);
+          alen = P.lcache ? coboundary<true>(P, sp, s_small[wib], lane, lc)
+                          : coboundary<false>(P, sp, s_small[wib], lane);
           add = s_small[wib];
           glob = false;
         } else {
-          const uint32_t o = __ldcg(P.owner + pk);
+          const uint32_t o = hit ? ocached : __ldcg(P.owner + pk);
           if (o == NONE32) {
             ready = true;
             cval = piv;
@@ -774,8 +826,15 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.max_steps = 256;
       P.stats = stats;
       P.debug = std::getenv("CR_DEBUG_STATS") != nullptr;
+      {
+        const int dbg = P.debug ? 1 : 0;
+        unsigned long long z[4] = {0, 0, 0, 0};
+        CR_CUDA(cudaMemcpyToSymbolAsync(g_k5_dbg, &dbg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+        CR_CUDA(cudaMemcpyToSymbolAsync(g_k5_flush, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+      }
       P.colstat = nullptr;
       P.prefetch = std::getenv("CR_K5_PREFETCH") != nullptr;
+      P.lcache = std::getenv("CR_K5_CACHE") != nullptr;
       if (P.debug) {
         if (!P_colstat) P_colstat = ws.alloc<unsigned long long>(2 * int64_t(ncols));
         P.colstat = P_colstat;
@@ -825,6 +884,9 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
         for (uint32_t q = 0; q < m; ++q) acc += byent[q].first;
         fprintf(stderr, " top%u %.3f", m, tot ? double(acc) / tot : 0.0);
       }
+      unsigned long long fl[4];
+      CR_CUDA(cudaMemcpyFromSymbol(fl, g_k5_flush, sizeof(fl)));
+      fprintf(stderr, " | flushes %llu cycles %llu M-entries %llu", fl[0], fl[1], fl[2]);
       fprintf(stderr, "\n[cr] top columns (pos, adds, entries):");
       for (int q = 0; q < 8 && q < int(ncols); ++q)
         fprintf(stderr, " (%u,%llu,%llu)", byent[q].second, cs[2 * byent[q].second],
