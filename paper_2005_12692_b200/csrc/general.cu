@@ -146,6 +146,234 @@ __global__ void __launch_bounds__(256) k_births(const float* __restrict__ img, G
   __syncthreads();
   if (threadIdx.x < 4 && s_c[threadIdx.x]) atomicAdd(cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
 }
+// ---------------------------------------------------------------------------------------------
+// K1 with K2a fused: births AND the direction codes (min-key cofacet | max-key facet << 3, see
+// K2 below) of every cell, from one read of the image.  Thread = voxel column (x, y), streamed
+// along z; a warp covers x = 30*xb-1 .. 30*xb+30 (lanes 0 and 31 are halo), a CTA covers the voxel
+// rows y = 8*yb-1 .. 8*yb+8 (warps 0 and 9 are halo).  A cell's 6 grid neighbours come from: the
+// same thread (the other half of its voxel's 2x2x2 block), the neighbouring lanes (X), the
+// neighbouring warps through shared memory (Y), and the previous / next z step (Z) -- the codes of
+// the cz=1 layer of plane z are formed one step later, when plane z+1's cz=0 layer exists.
+// Outputs (births, codes) are written by the non-halo threads only.
+// ---------------------------------------------------------------------------------------------
+constexpr uint8_t CODE_ABSENT = 0x40;  // code bit 6: the cell is absent (+inf birth)
+constexpr int K1C_ROWS = 8, K1C_THREADS = 32 * (K1C_ROWS + 2), K1C_ZC = 8;
+inline unsigned k1c_grid(const Geom& g) {
+  return unsigned(((g.nx + 29) / 30) * ((g.ny + K1C_ROWS - 1) / K1C_ROWS) *
+                  ((g.nz + K1C_ZC - 1) / K1C_ZC));
+}
+__device__ __forceinline__ void code_visit(bool exists, bool odd, uint32_t nb, uint32_t dir,
+                                           uint32_t& mcb, uint32_t& mc, uint32_t& mfb,
+                                           uint32_t& mf) {
+  const bool f = exists && odd && nb >= mfb;
+  const bool c = exists && !odd && nb < mcb;
+  mfb = f ? nb : mfb;
+  mf = f ? dir : mf;
+  mcb = c ? nb : mcb;
+  mc = c ? dir : mc;
+}
+// code of a cell with birth b, odd-axis flags, and its neighbours (ABSENT_ORD where missing);
+// neighbours are visited in increasing kidx order: -Z, -Y, -X, +X, +Y, +Z
+__device__ __forceinline__ uint8_t cell_code6(uint32_t b, bool ox, bool oy, bool oz, uint32_t zm,
+                                              bool hzm, uint32_t ym, bool hym, uint32_t xm,
+                                              bool hxm, uint32_t xp, bool hxp, uint32_t yp,
+                                              bool hyp, uint32_t zp, bool hzp) {
+  if (b == ABSENT_ORD) return CODE_ABSENT;
+  uint32_t mcb = ABSENT_ORD, mc = 7, mfb = 0, mf = 7;
+  code_visit(hzm, oz, zm, 4, mcb, mc, mfb, mf);
+  code_visit(hym, oy, ym, 2, mcb, mc, mfb, mf);
+  code_visit(hxm, ox, xm, 0, mcb, mc, mfb, mf);
+  code_visit(hxp, ox, xp, 1, mcb, mc, mfb, mf);
+  code_visit(hyp, oy, yp, 3, mcb, mc, mfb, mf);
+  code_visit(hzp, oz, zp, 5, mcb, mc, mfb, mf);
+  return uint8_t(mc | (mf << 3));
+}
+
+__global__ void __launch_bounds__(K1C_THREADS) k_births_codes(const float* __restrict__ img,
+                                                              Geom g,
+                                                              uint32_t* __restrict__ births,
+                                                              uint8_t* __restrict__ code,
+                                                              unsigned long long* __restrict__ cnt,
+                                                              int* __restrict__ nan_flag) {
+  const int nx = int(g.nx), ny = int(g.ny), nz = int(g.nz);
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const int XB = (nx + 29) / 30, YB = (ny + K1C_ROWS - 1) / K1C_ROWS;
+  uint32_t blk = blockIdx.x;
+  const int xb = int(blk % XB);
+  blk /= XB;
+  const int yb = int(blk % YB), zb = int(blk / YB);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int x = xb * 30 - 1 + lane, y = yb * K1C_ROWS - 1 + w;
+  const int z0 = zb * K1C_ZC, z1 = min(nz, z0 + K1C_ZC);
+  const bool vx = x >= 0 && x < nx, vy = y >= 0 && y < ny, vv = vx && vy;
+  const bool hx = x + 1 < nx, hy = y + 1 < ny;  // the cell spans x+1 / y+1
+  const bool outp = vv && lane >= 1 && lane <= 30 && w >= 1 && w <= K1C_ROWS;
+  const uint64_t plane = uint64_t(nx) * ny;
+  // shared rows: births of the cz=0 layer of plane z and the cz=1 layer of plane z-1,
+  // 2 cells (cy = 0, 1) x 2 (cx) per thread, indexed [w][lane]
+  __shared__ uint32_t s_b0[K1C_ROWS + 2][4][32];
+  __shared__ uint32_t s_b1[K1C_ROWS + 2][4][32];
+  __shared__ uint32_t s_c[4];
+  bool nan = false;
+  auto ld = [&](int xx, int yy, int zz) -> uint32_t {
+    if (xx < 0 || xx >= nx || yy < 0 || yy >= ny || zz < 0 || zz >= nz) return ABSENT_ORD;
+    const float f = __ldg(img + uint64_t(zz) * plane + uint64_t(yy) * nx + xx);
+    nan |= f != f;
+    return ord_of(f);
+  };
+  // voxel values of plane zz: a = (x, y), b = (x, y+1); x+1 by shuffle (lane 31 loads)
+  uint32_t a = ld(x, y, z0 - 1), b = ld(x, y + 1, z0 - 1);
+  uint32_t an = ld(x, y, z0), bn = ld(x, y + 1, z0);
+  uint32_t e = lane == 31 ? ld(x + 1, y, z0 - 1) : 0u, f = lane == 31 ? ld(x + 1, y + 1, z0 - 1) : 0u;
+  uint32_t en = lane == 31 ? ld(x + 1, y, z0) : 0u, fn = lane == 31 ? ld(x + 1, y + 1, z0) : 0u;
+  // previous step's cz=1 layer (plane z-1): births [cy][cx], for the Z- of this step's cz=0 cells
+  // and its own codes one step late; and its Z- layer (plane z-1's cz=0)
+  uint32_t p1[2][2] = {{ABSENT_ORD, ABSENT_ORD}, {ABSENT_ORD, ABSENT_ORD}};
+  uint32_t p0[2][2] = {{ABSENT_ORD, ABSENT_ORD}, {ABSENT_ORD, ABSENT_ORD}};
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  for (int z = z0 - 1; z <= z1; ++z) {
+    const bool pz = z >= 0 && z < nz;     // plane z exists
+    const bool hz = z + 1 < nz;           // cells of plane z span z+1
+    const uint32_t an2 = ld(x, y, z + 2), bn2 = ld(x, y + 1, z + 2);
+    const uint32_t en2 = lane == 31 ? ld(x + 1, y, z + 2) : 0u;
+    const uint32_t fn2 = lane == 31 ? ld(x + 1, y + 1, z + 2) : 0u;
+    uint32_t a1 = __shfl_down_sync(0xFFFFFFFFu, a, 1), b1 = __shfl_down_sync(0xFFFFFFFFu, b, 1);
+    uint32_t an1 = __shfl_down_sync(0xFFFFFFFFu, an, 1), bn1 = __shfl_down_sync(0xFFFFFFFFu, bn, 1);
+    if (lane == 31) {
+      a1 = e;
+      b1 = f;
+      an1 = en;
+      bn1 = fn;
+    }
+    // births of the 8 cells of voxel (x, y, z): q0[cy][cx] (Z = 2z), q1[cy][cx] (Z = 2z+1);
+    // cells that do not exist (beyond the grid) are ABSENT_ORD, i.e. not in K
+    uint32_t q0[2][2], q1[2][2];
+    {
+      const uint32_t A = pz && vv ? a : ABSENT_ORD;
+      const uint32_t c100 = hx ? max(a, a1) : ABSENT_ORD, c010 = hy ? max(a, b) : ABSENT_ORD;
+      const uint32_t c110 = hx && hy ? max(max(a, a1), max(b, b1)) : ABSENT_ORD;
+      q0[0][0] = A;
+      q0[0][1] = pz && vv ? c100 : ABSENT_ORD;
+      q0[1][0] = pz && vv ? c010 : ABSENT_ORD;
+      q0[1][1] = pz && vv ? c110 : ABSENT_ORD;
+      const bool o1 = pz && vv && hz;
+      q1[0][0] = o1 ? max(a, an) : ABSENT_ORD;
+      q1[0][1] = o1 && hx ? max(max(a, a1), max(an, an1)) : ABSENT_ORD;
+      q1[1][0] = o1 && hy ? max(max(a, b), max(an, bn)) : ABSENT_ORD;
+      q1[1][1] = o1 && hx && hy ? max(max(max(a, a1), max(b, b1)), max(max(an, an1), max(bn, bn1)))
+                                : ABSENT_ORD;
+    }
+    // exchange the cz=0 layer of plane z and the cz=1 layer of plane z-1 (X by shuffle, Y by smem)
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        s_b0[w][2 * cy + cx][lane] = q0[cy][cx];
+        s_b1[w][2 * cy + cx][lane] = p1[cy][cx];
+      }
+    uint32_t x0m[2], x0p[2], x1m[2], x1p[2];  // [cy]: X-1 of a cx=0 cell, X+1 of a cx=1 cell
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      x0m[cy] = __shfl_up_sync(0xFFFFFFFFu, q0[cy][1], 1);
+      x0p[cy] = __shfl_down_sync(0xFFFFFFFFu, q0[cy][0], 1);
+      x1m[cy] = __shfl_up_sync(0xFFFFFFFFu, p1[cy][1], 1);
+      x1p[cy] = __shfl_down_sync(0xFFFFFFFFu, p1[cy][0], 1);
+    }
+    __syncthreads();
+    if (outp) {
+      const uint32_t X0 = 2 * uint32_t(x), Y0 = 2 * uint32_t(y);
+      // ---- births of plane z, and the codes of its cz=0 layer (Z = 2z)
+      if (pz && z >= z0 && z < z1) {
+        const uint32_t Z = 2 * uint32_t(z);
+        uint32_t* r = births + (uint64_t(Z) * KY + Y0) * KX + X0;
+        uint8_t* cr = code + (uint64_t(Z) * KY + Y0) * KX + X0;
+#pragma unroll
+        for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < 2; ++cx) {
+            if ((cx && !hx) || (cy && !hy)) continue;
+            const uint32_t bb = q0[cy][cx];
+            const uint32_t xm = cx ? q0[cy][0] : x0m[cy];
+            const uint32_t xp = cx ? x0p[cy] : q0[cy][1];
+            const uint32_t ym = cy ? q0[0][cx] : s_b0[w - 1][2 + cx][lane];
+            const uint32_t yp = cy ? s_b0[w + 1][cx][lane] : q0[1][cx];
+            const uint8_t cd = cell_code6(bb, cx, cy, false, p1[cy][cx], z > 0, ym, Y0 + cy > 0,
+                                          xm, X0 + cx > 0, xp, X0 + cx + 1 < KX, yp,
+                                          Y0 + cy + 1 < KY, q1[cy][cx], hz);
+            r[cy * KX + cx] = bb;
+            cr[cy * KX + cx] = cd;
+            const int dim = cx + cy;
+            const bool fin = bb != ABSENT_ORD;
+            c0 += fin && dim == 0;
+            c1 += fin && dim == 1;
+            c2 += fin && dim == 2;
+            if (hz) {
+              const uint32_t b1v = q1[cy][cx];
+              r[uint64_t(KX) * KY + cy * KX + cx] = b1v;
+              const bool fin1 = b1v != ABSENT_ORD;
+              c1 += fin1 && dim == 0;
+              c2 += fin1 && dim == 1;
+              c3 += fin1 && dim == 2;
+            }
+          }
+      }
+      // ---- codes of plane z-1's cz=1 layer (Z = 2z-1): Z- = plane z-1's cz=0, Z+ = plane z's cz=0
+      const int zq = z - 1;
+      if (zq >= z0 && zq < z1 && zq + 1 < nz) {
+        const uint32_t Z = 2 * uint32_t(zq) + 1;
+        uint8_t* cr = code + (uint64_t(Z) * KY + Y0) * KX + X0;
+#pragma unroll
+        for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < 2; ++cx) {
+            if ((cx && !hx) || (cy && !hy)) continue;
+            const uint32_t bb = p1[cy][cx];
+            const uint32_t xm = cx ? p1[cy][0] : x1m[cy];
+            const uint32_t xp = cx ? x1p[cy] : p1[cy][1];
+            const uint32_t ym = cy ? p1[0][cx] : s_b1[w - 1][2 + cx][lane];
+            const uint32_t yp = cy ? s_b1[w + 1][cx][lane] : p1[1][cx];
+            cr[cy * KX + cx] = cell_code6(bb, cx, cy, true, p0[cy][cx], true, ym, Y0 + cy > 0, xm,
+                                          X0 + cx > 0, xp, X0 + cx + 1 < KX, yp, Y0 + cy + 1 < KY,
+                                          q0[cy][cx], true);
+          }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {
+        p0[cy][cx] = q0[cy][cx];
+        p1[cy][cx] = q1[cy][cx];
+      }
+    a = an;
+    b = bn;
+    an = an2;
+    bn = bn2;
+    e = en;
+    f = fn;
+    en = en2;
+    fn = fn2;
+  }
+  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
+  c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
+  c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
+  c3 = __reduce_add_sync(0xFFFFFFFFu, c3);
+  const bool anynan = __any_sync(0xFFFFFFFFu, nan);
+  if (lane == 0) {
+    atomicAdd(s_c + 0, c0);
+    atomicAdd(s_c + 1, c1);
+    atomicAdd(s_c + 2, c2);
+    atomicAdd(s_c + 3, c3);
+    if (anynan) atomicOr(nan_flag, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && s_c[threadIdx.x])
+    atomicAdd(cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
+}
+
 inline unsigned k_births_grid(const Geom& g) {
   return unsigned(((g.nx + 31) / 32) * ((g.ny + 7) / 8) * ((g.nz + K1_ZC - 1) / K1_ZC));
 }
@@ -263,7 +491,6 @@ __global__ void k_tags(const uint32_t* __restrict__ births, Geom g, uint8_t* __r
 //        its max facet r) iff r's min cofacet is s.
 // A CTA covers 64 cells of a Khalimsky row x 4 rows of one plane; all index math is 32-bit.
 // ---------------------------------------------------------------------------------------------
-constexpr uint8_t CODE_ABSENT = 0x40;
 struct K2Tile {
   uint32_t X, Y, Z, k;
   bool valid;
@@ -587,6 +814,74 @@ __global__ void __launch_bounds__(256) k_tags2(const uint8_t* __restrict__ code,
   for (int d = 0; d < 3; ++d) {
     const unsigned m = __ballot_sync(0xFFFFFFFFu, up && dim == d);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(s_c + d, uint32_t(__popc(m)));
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 && s_c[threadIdx.x])
+    atomicAdd(app_cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
+}
+
+// K2b over the codes formed by k_births_codes: 4 consecutive cells per thread (one 32-bit load of
+// their codes, one 32-bit store of their tags); the partner's code is a byte load (L1/L2).
+__global__ void __launch_bounds__(256) k_tags_codes(const uint8_t* __restrict__ code, Geom g,
+                                                    uint8_t* __restrict__ tags,
+                                                    unsigned long long* __restrict__ app_cnt) {
+  const uint64_t k0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  const uint64_t N = uint64_t(g.ncells);
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  auto stride = [&](uint32_t ax) -> int64_t {
+    return ax == 0 ? 1 : (ax == 1 ? int64_t(KX) : int64_t(KX) * KY);
+  };
+  uint32_t nup = 0;
+  if (k0 < N) {
+    uint32_t w4 = 0;
+    if (k0 + 3 < N) {
+      w4 = __ldg(reinterpret_cast<const uint32_t*>(code + k0));
+    } else {
+      for (uint64_t j = 0; k0 + j < N; ++j) w4 |= uint32_t(code[k0 + j]) << (8 * j);
+    }
+    uint32_t X = uint32_t(k0 % KX), Y = uint32_t((k0 / KX) % KY), Z = uint32_t(k0 / (uint64_t(KX) * KY));
+    uint32_t out = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t k = k0 + j;
+      if (k < N) {
+        const uint8_t c = uint8_t(w4 >> (8 * j));
+        uint8_t tag = 0;
+        if (!(c & CODE_ABSENT)) {
+          const uint32_t mc = c & 7, mf = (c >> 3) & 7;
+          if (mc != 7) {
+            const int64_t t = int64_t(k) + ((mc & 1) ? stride(mc >> 1) : -stride(mc >> 1));
+            if (((__ldg(code + t) >> 3) & 7) == (mc ^ 1)) tag = make_tag(KIND_UP, int(mc));
+          }
+          if (!tag && mf != 7) {
+            const int64_t r = int64_t(k) + ((mf & 1) ? stride(mf >> 1) : -stride(mf >> 1));
+            if ((__ldg(code + r) & 7) == (mf ^ 1)) tag = make_tag(KIND_DOWN, int(mf));
+          }
+          if (tag_kind(tag) == KIND_UP) nup += 1u << (8 * ((X & 1) + (Y & 1) + (Z & 1)));
+        }
+        out |= uint32_t(tag) << (8 * j);
+      }
+      if (++X == KX) {
+        X = 0;
+        if (++Y == KY) {
+          Y = 0;
+          ++Z;
+        }
+      }
+    }
+    if (k0 + 3 < N) {
+      *reinterpret_cast<uint32_t*>(tags + k0) = out;
+    } else {
+      for (uint64_t j = 0; k0 + j < N; ++j) tags[k0 + j] = uint8_t(out >> (8 * j));
+    }
+  }
+  __shared__ uint32_t s_c[3];
+  if (threadIdx.x < 3) s_c[threadIdx.x] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, (nup >> (8 * d)) & 0xFFu);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(s_c + d, v);
   }
   __syncthreads();
   if (threadIdx.x < 3 && s_c[threadIdx.x])
@@ -1382,6 +1677,31 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
 
+  // Default: K1 (k_births) + K2 fused (k_apparent).  Variants for cross-checks and measurement
+  // (profiles/r01/s3: C5 K1+K2 = 0.52 + 3.60 ms default, 1.91 + 1.76 fused births+codes,
+  // 0.52 + 1.66 + 1.76 split): CR_K12_FUSED, CR_K12_SPLIT, CR_K2_TWOPASS, CR_K2_ONEPASS.
+  const bool k12_old = !(std::getenv("CR_K12_FUSED") || std::getenv("CR_K12_SPLIT"));
+  if (!k12_old && std::getenv("CR_K12_SPLIT")) {
+    // K1 (births) alone, then K2 as codes (z-streaming) + tags from codes
+    uint8_t* code = ws.alloc<uint8_t>(g.ncells + 4);
+    k_births<<<k_births_grid(g), 256, 0, s>>>(image, g, S.births, cnt + 4, nan_flag);
+    CR_CHECK_LAUNCH();
+    prof_mark(s, "births");
+    k_codes_z<<<k2z_grid(g), 256, 0, s>>>(S.births, g, code);
+    CR_CHECK_LAUNCH();
+    k_tags_codes<<<grid_for((g.ncells + 3) / 4, 256), 256, 0, s>>>(code, g, S.tags, cnt + 0);
+    CR_CHECK_LAUNCH();
+    ws.release(code);
+  } else if (!k12_old) {
+    // K1 + K2a fused (births and direction codes), then K2b (tags from codes)
+    uint8_t* code = ws.alloc<uint8_t>(g.ncells + 4);
+    k_births_codes<<<k1c_grid(g), K1C_THREADS, 0, s>>>(image, g, S.births, code, cnt + 4, nan_flag);
+    CR_CHECK_LAUNCH();
+    prof_mark(s, "births");
+    k_tags_codes<<<grid_for((g.ncells + 3) / 4, 256), 256, 0, s>>>(code, g, S.tags, cnt + 0);
+    CR_CHECK_LAUNCH();
+    ws.release(code);
+  } else {
   k_births<<<k_births_grid(g), 256, 0, s>>>(image, g, S.births, cnt + 4, nan_flag);
   CR_CHECK_LAUNCH();
   prof_mark(s, "births");
@@ -1398,6 +1718,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   } else {
     k_apparent<<<k2f_grid(g), K2F_THREADS, 0, s>>>(S.births, g, S.tags, cnt + 0);
     CR_CHECK_LAUNCH();
+  }
   }
   prof_mark(s, "apparent");
 

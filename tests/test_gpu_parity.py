@@ -106,9 +106,9 @@ def test_general_path_on_1d(cr, monkeypatch):
 
 
 def test_k2_variants_agree(cr, monkeypatch):
-    """K2 (apparent pairs) as one fused streaming kernel, as codes-then-tags, and as the direct
-    one-kernel definition give the same pairing (and the oracle's), on shapes whose Khalimsky
-    extents are not multiples of the kernels' tiles (30 x 16 x 32, 32 x 8 x 16, 64 x 4)."""
+    """K2 (apparent pairs) as one fused streaming kernel, as codes-then-tags, as the direct
+    one-kernel definition, and with the codes fused into K1 (births) give the same pairing (and
+    the oracle's), on shapes whose Khalimsky extents are not multiples of the kernels' tiles."""
     import torch
     imgs = [gen.masked_grf((33, 37, 41), 2.0, 17.0, 21),
             gen.small_int_image((9, 70, 13), 3, seed=22, inf_frac=0.1),
@@ -116,8 +116,8 @@ def test_k2_variants_agree(cr, monkeypatch):
     for k, img in enumerate(imgs):
         o = oracle.ph(img, img.ndim - 1, partner=True)
         t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
-        for var in ["", "CR_K2_TWOPASS", "CR_K2_ONEPASS"]:
-            for v in ["CR_K2_TWOPASS", "CR_K2_ONEPASS"]:
+        for var in ["", "CR_K2_TWOPASS", "CR_K2_ONEPASS", "CR_K12_FUSED", "CR_K12_SPLIT"]:
+            for v in ["CR_K2_TWOPASS", "CR_K2_ONEPASS", "CR_K12_FUSED", "CR_K12_SPLIT"]:
                 monkeypatch.delenv(v, raising=False)
             if var:
                 monkeypatch.setenv(var, "1")
