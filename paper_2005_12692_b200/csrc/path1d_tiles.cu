@@ -197,6 +197,14 @@ __device__ __forceinline__ uint32_t decide(const STree& T, int j, bool left_star
 }
 
 
+__device__ unsigned long long* g_tl = nullptr;  // debug: level-tile timeline (block 0)
+__device__ __forceinline__ void tl_mark(int slot) {
+  if (g_tl && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tl[slot] = t;
+  }
+}
 __device__ int g_rounds = 1;      // contraction rounds before the tree (tunable: CR_1D_ROUNDS)
 __device__ int g_l1_rounds = 3;   // level-1 warp rounds incl. the register round (CR_1D_L1ROUNDS)
 
@@ -388,8 +396,10 @@ __device__ __forceinline__ int decide_tile(Smem& S, int n, bool left_start, uint
   }
   for (int w = threadIdx.x; w < MAXITEMS / 32; w += THREADS) s_pend[w] = 0;
   __syncthreads();
+  tl_mark(8);
   stree_layout(S.T, n);
   stree_build(S.T);
+  tl_mark(9);
   for (int j = threadIdx.x; j < n; j += THREADS) {
     const uint32_t d = decide(S.T, j, left_start, lead);
     if (d != DEATH_PENDING) sink(S.id[j], S.T.mn[j], d);
@@ -841,8 +851,22 @@ __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, con
     }
     return lo;
   };
+  // source tiles of the first and last item: one parallel pass over the prefix (a thread owns a
+  // run of entries and recognises the boundary i with prefix[i] <= g < prefix[i+1]); no
+  // dependent chain of global loads
+  __shared__ int s_pa, s_pb;
+  {
+    const uint32_t ga = k0 > 0 ? k0 - 1 : 0, gb = k0 + uint32_t(n) - 1;
+    for (int i = threadIdx.x; i < P; i += THREADS) {
+      const uint32_t pi = __ldcg(I.prefix + i);
+      const uint32_t pn = i + 1 < P ? __ldcg(I.prefix + i + 1) : 0xFFFFFFFFu;
+      if (pi <= ga && ga < pn) s_pa = i;
+      if (pi <= gb && gb < pn) s_pb = i;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int a = src_tile(k0 > 0 ? k0 - 1 : 0), b = src_tile(k0 + uint32_t(n) - 1);
+    const int a = s_pa, b = s_pb;
     s_plo = a;
     s_pn = b - a + 1 <= PSEG ? b - a + 1 : 0;  // 0: too wide, search globally
   }
@@ -883,12 +907,15 @@ __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, con
   }
   if (k0 == 0 && threadIdx.x == 0) s_lead0 = KEY_NONE;
   __syncthreads();
+  tl_mark(ntiles > 1 ? 7 : 12);
   uint64_t ld = s_lead0;
   const int nres = decide_tile(S, n, t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
     final_put(G, id, key_ord(key), d);
   });
+  tl_mark(ntiles > 1 ? 10 : 13);
   if (ntiles > 1) {
     export_pending(S, nres, ld, O, t, [](uint32_t id) { return id; });
+    tl_mark(11);
   } else if (threadIdx.x == 0) {
     O.cnt[t] = 0;
     O.lead[t] = KEY_NONE;
@@ -914,8 +941,10 @@ struct LevelsArgs {
   int levels;              // 0: one level-1 tile (every basin decided there)
   int nreg;                // level-1 regions
   uint32_t* part;          // per CTA: bars in its regions
+  uint32_t* part2;         // per CTA: undecided basins in its share of the level-1 tiles
   unsigned long long* total;
   uint32_t* gctr;          // next gather chunk
+  unsigned long long* tl;  // debug timeline (null unless CR_DEBUG_STATS)
   uint32_t* done;          // [l]: level l's count scan done (1); [NLEVELS + l]: its tiles done
 };
 
@@ -951,45 +980,87 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
   __shared__ uint32_t s_red[THREADS / 32];
   __shared__ uint32_t s_bar[THREADS / 32][96];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // ---- (0) region offsets
+  auto stamp = [&](int slot) {  // debug timeline (CR_DEBUG_STATS): block 0's view
+    if (A.tl && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      A.tl[slot] = t;
+    }
+  };
+  stamp(0);
+  // ---- (0) two grid-wide scans at once: the level-1 regions' bar counts (output offsets) and,
+  // when there are item levels, the level-1 tiles' undecided counts (the first item level's
+  // prefix, so that no single CTA scans it later)
   const int per = (A.nreg + int(gridDim.x) - 1) / int(gridDim.x);
   const int r0 = min(A.nreg, int(blockIdx.x) * per), r1 = min(A.nreg, r0 + per);
-  {
-    uint32_t sum = 0;
-    for (int r = r0 + threadIdx.x; r < r1; r += THREADS)
-      sum += __ldcg(A.G.rcnt + r) - __ldcg(A.G.holes + r);
-    sum = __reduce_add_sync(0xFFFFFFFFu, sum);
-    if (lane == 0) s_red[w] = sum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t t = 0;
-      for (int k = 0; k < THREADS / 32; ++k) t += s_red[k];
-      A.part[blockIdx.x] = t;
-    }
-  }
-  grid.sync();
-  {
-    uint32_t v = 0;
-    for (uint32_t k = threadIdx.x; k < blockIdx.x; k += THREADS) v += __ldcg(A.part + k);
+  const int P0 = A.levels ? int(__ldcg(A.ltiles)) : 0;
+  const int per2 = (P0 + int(gridDim.x) - 1) / int(gridDim.x);
+  const int t0 = min(P0, int(blockIdx.x) * per2), t1 = min(P0, t0 + per2);
+  auto rsz = [&](int r) { return __ldcg(A.G.rcnt + r) - __ldcg(A.G.holes + r); };
+  auto tsz = [&](int t) { return __ldcg(A.in[0].cnt + t); };
+  auto block_sum = [&](uint32_t v) {  // block-wide sum, returned to every thread
     v = __reduce_add_sync(0xFFFFFFFFu, v);
     __syncthreads();
     if (lane == 0) s_red[w] = v;
     __syncthreads();
-    uint32_t base = 0;
-    for (int k = 0; k < THREADS / 32; ++k) base += s_red[k];
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
+    uint32_t t = 0;
+    for (int k = 0; k < THREADS / 32; ++k) t += s_red[k];
+    return t;
+  };
+  {
+    uint32_t s1 = 0, s2 = 0;
+    for (int r = r0 + threadIdx.x; r < r1; r += THREADS) s1 += rsz(r);
+    for (int t = t0 + threadIdx.x; t < t1; t += THREADS) s2 += tsz(t);
+    s1 = block_sum(s1);
+    s2 = block_sum(s2);
+    if (threadIdx.x == 0) {
+      A.part[blockIdx.x] = s1;
+      A.part2[blockIdx.x] = s2;
+    }
+  }
+  grid.sync(); stamp(1);
+  {
+    uint32_t v1 = 0, v2 = 0;
+    for (uint32_t k = threadIdx.x; k < blockIdx.x; k += THREADS) {
+      v1 += __ldcg(A.part + k);
+      v2 += __ldcg(A.part2 + k);
+    }
+    uint32_t base = block_sum(v1), base2 = block_sum(v2);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
       *A.total = base + __ldcg(A.part + blockIdx.x);
+      if (A.levels) {  // the first item level's size (what block 0 used to scan)
+        const uint32_t run = base2 + __ldcg(A.part2 + blockIdx.x);
+        const_cast<uint32_t*>(A.in[0].prefix)[P0] = run;
+        const uint32_t nt = (run + ITILE - 1) / ITILE;
+        if (int64_t(nt) > A.cap_tiles[0]) {
+          atomicOr(A.overflow, 1);
+          A.ltiles[1] = 0;
+        } else {
+          A.ltiles[1] = nt > 1 ? nt : 0;
+        }
+      }
+    }
     for (int c = r0; c < r1; c += THREADS) {
       const int r = c + threadIdx.x;
-      const uint32_t sz = r < r1 ? __ldcg(A.G.rcnt + r) - __ldcg(A.G.holes + r) : 0u;
+      const uint32_t sz = r < r1 ? rsz(r) : 0u;
       uint32_t pre, tot;
       __syncthreads();
       BS(s_scan).ExclusiveSum(sz, pre, tot);
       if (r < r1) A.G.regoff[r] = base + pre;
       base += tot;
     }
+    uint32_t* pref0 = const_cast<uint32_t*>(A.in[0].prefix);
+    for (int c = t0; c < t1; c += THREADS) {
+      const int t = c + threadIdx.x;
+      const uint32_t sz = t < t1 ? tsz(t) : 0u;
+      uint32_t pre, tot;
+      __syncthreads();
+      BS(s_scan).ExclusiveSum(sz, pre, tot);
+      if (t < t1) pref0[t] = base2 + pre;
+      base2 += tot;
+    }
   }
-  grid.sync();
+  grid.sync(); stamp(2);
   // ---- (1) item levels, (2) the gather when idle
   __shared__ uint32_t s_chunk;
   bool more = true;  // gather chunks left
@@ -997,45 +1068,48 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
     LevelIn I = A.in[l];
     I.ntiles = int(__ldcg(A.ltiles + l));
     uint32_t* pref = const_cast<uint32_t*>(I.prefix);
-    if (blockIdx.x == 0) {
-      constexpr int PT = 16;  // counts per thread per pass
-      uint32_t run = 0;
-      for (int c = 0; c < I.ntiles; c += THREADS * PT) {
-        const int i0 = c + threadIdx.x * PT;
-        uint32_t v[PT], sum = 0;
+    if (l > 0) {  // (level 0's prefix comes from phase (0))
+      if (blockIdx.x == 0) {
+        constexpr int PT = 16;  // counts per thread per pass
+        uint32_t run = 0;
+        for (int c = 0; c < I.ntiles; c += THREADS * PT) {
+          const int i0 = c + threadIdx.x * PT;
+          uint32_t v[PT], sum = 0;
 #pragma unroll
-        for (int r = 0; r < PT; ++r) {
-          v[r] = i0 + r < I.ntiles ? __ldcg(I.cnt + i0 + r) : 0u;
-          sum += v[r];
-        }
-        uint32_t pre, tot;
-        BS(s_scan).ExclusiveSum(sum, pre, tot);
-        pre += run;
-#pragma unroll
-        for (int r = 0; r < PT; ++r)
-          if (i0 + r < I.ntiles) {
-            pref[i0 + r] = pre;
-            pre += v[r];
+          for (int r = 0; r < PT; ++r) {
+            v[r] = i0 + r < I.ntiles ? __ldcg(I.cnt + i0 + r) : 0u;
+            sum += v[r];
           }
-        run += tot;
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) {
-        pref[I.ntiles] = run;
-        const uint32_t nt = (run + ITILE - 1) / ITILE;
-        if (int64_t(nt) > A.cap_tiles[l] || (l == NLEVELS - 1 && nt > 1)) {
-          atomicOr(A.overflow, 1);
-          A.ltiles[l + 1] = 0;
-        } else {
-          A.ltiles[l + 1] = nt > 1 ? nt : 0;  // a final (single) tile exports nothing
+          uint32_t pre, tot;
+          BS(s_scan).ExclusiveSum(sum, pre, tot);
+          pre += run;
+#pragma unroll
+          for (int r = 0; r < PT; ++r)
+            if (i0 + r < I.ntiles) {
+              pref[i0 + r] = pre;
+              pre += v[r];
+            }
+          run += tot;
+          __syncthreads();
         }
-        __threadfence();
-        atomicExch(A.done + l, 1u);
+        if (threadIdx.x == 0) {
+          pref[I.ntiles] = run;
+          const uint32_t nt = (run + ITILE - 1) / ITILE;
+          if (int64_t(nt) > A.cap_tiles[l] || (l == NLEVELS - 1 && nt > 1)) {
+            atomicOr(A.overflow, 1);
+            A.ltiles[l + 1] = 0;
+          } else {
+            A.ltiles[l + 1] = nt > 1 ? nt : 0;  // a final (single) tile exports nothing
+          }
+          __threadfence();
+          atomicExch(A.done + l, 1u);
+        }
+      } else if (more) {  // block 0 scans; the others gather meanwhile
+        more = gather_until(A, A.done + l, 1u, s_bar, &s_chunk);
       }
-    } else if (more) {  // block 0 scans; the others gather meanwhile
-      more = gather_until(A, A.done + l, 1u, s_bar, &s_chunk);
+      grid.sync();
     }
-    grid.sync();
+    stamp(3 + 3 * l);
     if (__ldcg(A.overflow)) return;
     const uint32_t total = __ldcg(pref + I.ntiles);
     const uint32_t ntiles = (total + ITILE - 1) / ITILE;
@@ -1043,6 +1117,7 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
     if (blockIdx.x < ntiles) {
       for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x)
         level_tile(I, A.out[l], A.G, S, t, total, ntiles);
+      stamp(4 + 3 * l);
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
@@ -1052,9 +1127,11 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
       more = gather_until(A, A.done + NLEVELS + l, min(ntiles, gridDim.x), s_bar, &s_chunk);
     }
     if (ntiles == 1) break;
-    grid.sync();
+    grid.sync(); stamp(5 + 3 * l);
   }
+  stamp(14);
   if (more) gather_until(A, nullptr, 0u, s_bar, &s_chunk);
+  stamp(15);
 }
 
 __global__ void k1_hole_flags(const cr_pair* __restrict__ in, int64_t n, uint32_t* flag) {
@@ -1169,6 +1246,17 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   const int64_t blocks = std::max<int64_t>(
       1, std::min<int64_t>(int64_t(F.nsm) * std::min(F.per_sm, 2), (nreg + 7) / 8));
   LA.part = ws.alloc<uint32_t>(blocks);
+  LA.part2 = ws.alloc<uint32_t>(blocks);
+  LA.tl = nullptr;
+  {
+    unsigned long long* gt = nullptr;
+    if (std::getenv("CR_DEBUG_STATS")) {
+      LA.tl = ws.alloc<unsigned long long>(32);
+      CR_CUDA(cudaMemsetAsync(LA.tl, 0, 32 * sizeof(unsigned long long), s));
+      gt = LA.tl + 16;
+    }
+    CR_CUDA(cudaMemcpyToSymbolAsync(g_tl, &gt, sizeof(gt), 0, cudaMemcpyHostToDevice, s));
+  }
   void* args[] = {&LA};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k1_levels_coop, dim3(unsigned(blocks)),
                                       dim3(THREADS), args, SMEM, s));
@@ -1185,6 +1273,14 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     fprintf(stderr, "[cr] 1d tiles per level:");
     for (int l = 0; l <= NLEVELS; ++l) fprintf(stderr, " %u", lt[l]);
     fprintf(stderr, " | undecided after level 1: %llu, later holes %llu\n", exported, late_holes);
+    unsigned long long tl[32];
+    CR_CUDA(cudaMemcpy(tl, LA.tl, sizeof(tl), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[cr] coop timeline (us since start, block 0):");
+    for (int q = 1; q < 16; ++q)
+      if (tl[q]) fprintf(stderr, " [%d]%.1f", q, (tl[q] - tl[0]) / 1000.0);
+    for (int q = 16; q < 32; ++q)
+      if (tl[q]) fprintf(stderr, " t%d:%.1f", q - 16, (tl[q] - tl[0]) / 1000.0);
+    fprintf(stderr, "\n");
   }
   if (hf[0]) throw Error{CR_EINVAL, "NaN in image"};
   if (hf[1] || exported != decided) return -1;  // contraction did not finish (adversarial)
