@@ -762,19 +762,24 @@ __global__ void __launch_bounds__(THREADS) k1_level1(const float* __restrict__ x
   const int nres = decide_tile(S, int(m), t == 0, ld, [=](uint32_t id, uint64_t key, uint32_t d) {
     stage_put(G, tslot + id, key_ord(key), d);
   });
-  __shared__ uint32_t s_npend;
-  if (threadIdx.x == 0) s_npend = 0;
+  __shared__ uint32_t s_npend, s_nexp;  // undecided basins needing the rank pass; all of them
+  if (threadIdx.x == 0) s_npend = s_nexp = 0;
   __syncthreads();
   for (int j = threadIdx.x; j < nres; j += THREADS)
     if (s_pend[j >> 5] >> (j & 31) & 1) {
-      G.st[tslot + S.id[j]] =
-          make_uint2(__float_as_uint(float_of_ord(key_ord(S.T.mn[j]))), BAR_PENDING);
-      atomicAdd(&s_npend, 1u);
+      // an undecided basin's rank among its region's bars is its index unless the region holds
+      // holes (zero-persistence basins); those regions are ranked by the pass below
+      const uint64_t slot = tslot + S.id[j];
+      const bool holes = __ldcg(G.holes + slot / L1_IPW) != 0;
+      G.st[slot] = make_uint2(__float_as_uint(float_of_ord(key_ord(S.T.mn[j]))),
+                              holes ? BAR_PENDING : (PEND_TAG | uint32_t(slot % L1_IPW)));
+      if (holes) atomicAdd(&s_npend, 1u);
+      atomicAdd(&s_nexp, 1u);
     }
   __syncthreads();
-  if (threadIdx.x == 0 && s_npend) atomicAdd(G.cnt + 0, (unsigned long long)s_npend);
+  if (threadIdx.x == 0 && s_nexp) atomicAdd(G.cnt + 0, (unsigned long long)s_nexp);
   // ---------------- (e) ranks of the undecided basins among the bars of their region
-  if (s_npend) {  // the loads below go out together
+  if (s_npend && __ldcg(G.holes + rslot / L1_IPW)) {  // the loads below go out together
     constexpr int NCH = L1_IPW / 32;
     uint2 v[NCH];
 #pragma unroll
