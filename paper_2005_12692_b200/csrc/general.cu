@@ -1012,11 +1012,19 @@ __global__ void k_mm_commit(const Cand* cand, unsigned n, const uint32_t* __rest
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || !alive[i]) return;
   Cand c = cand[i];
-  if (best[c.a] != c.key || best[c.b] != c.key) return;
+  // Commit when the edge is the minimum at both components (the next Kruskal merge there), or
+  // when it is the minimum at the YOUNGER component alone: that component does not change before
+  // the edge, and the other one can only merge with older roots first, so the younger root dies
+  // at this edge whatever happens on the other side.  (Mutual minima alone degenerate into one
+  // merge per round when a large old component absorbs many young ones.)
+  const bool min_a = best[c.a] == c.key, min_b = best[c.b] == c.key;
+  if (!min_a && !min_b) return;
   uint32_t ka = vox_kidx(g, c.a), kb = vox_kidx(g, c.b);
   uint64_t keya = make_key(births[ka], ka), keyb = make_key(births[kb], kb);
-  uint32_t young = keya > keyb ? c.a : c.b, old = keya > keyb ? c.b : c.a;
-  uint32_t kyoung = keya > keyb ? ka : kb;
+  const bool a_young = keya > keyb;
+  if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) return;
+  uint32_t young = a_young ? c.a : c.b, old = a_young ? c.b : c.a;
+  uint32_t kyoung = a_young ? ka : kb;
   parent[young] = old;  // elder rule: the younger component dies
   tags[key_kidx(c.key)] = make_tag(KIND_CLEARED, 0);  // a death edge: cleared for dim 1
   unsigned long long r = atomicAdd(nrec, 1ull);

@@ -205,6 +205,17 @@ def test_barcodes_topdim(cr):
         assert cr.last_stats()["path"] == 6
 
 
+def test_h0_many_basins(cr):
+    """H0 with more basins than one CTA's shared memory (the device-wide merge rounds, incl. the
+    one-sided commit of a younger component's minimum edge) on iid noise and on integer levels."""
+    rng = np.random.default_rng(60)
+    for img in [rng.random((600, 640), dtype=np.float32),
+                rng.integers(0, 6, (700, 560)).astype(np.float32)]:
+        check_image(cr, img, 1, partner=False, ctx="many basins")
+        st = cr.last_stats()
+        assert st["columns"][0] > 56000, st["columns"][0]
+
+
 # ---------------------------------------------------------------- configs (cropped / full)
 
 def test_c1_full(cr):
