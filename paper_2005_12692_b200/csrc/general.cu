@@ -1079,7 +1079,17 @@ __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
 // phases (a round costs ~1 us instead of a host round trip).  Basins are renumbered by their rank
 // in elder order, so the elder of two roots is simply the smaller id; candidate edges are sorted
 // by key, so a component's minimum edge is the smallest edge index.
-constexpr int SMEM_BASINS = 56000;  // u32 union-find in <= 224 KB of shared memory; ranks < 2^16
+constexpr int SMEM_BASINS = 56000;
+// Up to this many roots the union-find runs in one CTA's shared memory (Boruvka MSF + Kruskal),
+// beyond it as device-wide merge rounds.  Since the rounds also commit a younger component's
+// minimum edge they take ~10-15 rounds on every config and beat the one-CTA path everywhere
+// (profiles/r01: C1 H0 1.38 -> 0.47 ms, C4 top dim 15.8 -> 0.52 ms), so the default is 0;
+// CR_SMEM_BASINS=n (<= SMEM_BASINS) brings the one-CTA path back for cross-checks.
+unsigned smem_basins_max() {
+  const char* e = std::getenv("CR_SMEM_BASINS");
+  const unsigned v = e ? unsigned(std::strtoul(e, nullptr, 10)) : 0u;
+  return v < unsigned(SMEM_BASINS) ? v : unsigned(SMEM_BASINS);
+}  // u32 union-find in <= 224 KB of shared memory; ranks < 2^16
 constexpr int H0_THREADS = 1024;
 
 __global__ void k_collect_roots(const uint32_t* __restrict__ births, Geom g,
@@ -1506,6 +1516,26 @@ __global__ void __launch_bounds__(H0_THREADS) k_dual_kruskal(
   }
 }
 
+// Device-wide dual merge round (mirror of k_mm_commit: the elder is the LARGER key): an edge
+// commits if it is the minimum (in complemented order) at both components, or at the younger one.
+__global__ void k_dual_mm_commit(const Cand* cand, unsigned n, const uint32_t* __restrict__ births,
+                                 DualG G, uint32_t* parent, const unsigned long long* best,
+                                 uint8_t* alive, uint64_t* rec, unsigned long long* nrec) {
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !alive[i]) return;
+  const Cand c = cand[i];
+  const bool min_a = best[c.a] == c.key, min_b = best[c.b] == c.key;
+  if (!min_a && !min_b) return;
+  const uint64_t ka = dual_root_key(births, G, c.a), kb = dual_root_key(births, G, c.b);
+  const bool a_young = ka < kb;
+  if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) return;
+  const uint32_t young = a_young ? c.a : c.b, old = a_young ? c.b : c.a;
+  parent[young] = old;
+  const unsigned long long r = atomicAdd(nrec, 1ull);
+  rec[r] = dual_record(c.key, a_young ? ka : kb);
+  alive[i] = 2;
+}
+
 // Returns false (doing nothing) if the dual graph has more than max_basins roots: its union-find
 // then runs on one CTA's shared memory only up to SMEM_BASINS roots, and the device-wide
 // mutual-minimum rounds degenerate on the dual graph (the outside vertex absorbs components one
@@ -1538,13 +1568,38 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   CR_CUDA(cudaStreamSynchronize(s));
   unsigned n = unsigned(hs.p[0] & 0xFFFFFFFFu);
   const unsigned nb = unsigned(hs.p[1]);
-  if (nb > max_basins || nb > unsigned(SMEM_BASINS)) {
+  if (nb > max_basins) {
     ws.release(cand);
     ws.release(parent);
     return false;
   }
   st.columns[d] = nb;
+
   unsigned long long* nrec = cnt + 2;
+  if (nb > smem_basins_max()) {  // device-wide merge rounds
+    unsigned long long* best = ws.alloc<unsigned long long>(nv);
+    CR_CUDA(cudaMemsetAsync(best, 0xFF, nv * sizeof(unsigned long long), s));
+    uint8_t* alive = ws.alloc<uint8_t>(n + 1);
+    Cand* cand2 = ws.alloc<Cand>(n + 1);
+    unsigned* nnext = reinterpret_cast<unsigned*>(cnt + 6);
+    int64_t rounds = 0;
+    while (n > 0) {
+      k_mm_find<<<grid_for(n, B), B, 0, s>>>(cand, n, parent, best, alive);
+      CR_CHECK_LAUNCH();
+      k_dual_mm_commit<<<grid_for(n, B), B, 0, s>>>(cand, n, S.births, G, parent, best, alive,
+                                                    S.R.rec[d], nrec);
+      CR_CHECK_LAUNCH();
+      CR_CUDA(cudaMemsetAsync(nnext, 0, sizeof(unsigned), s));
+      k_mm_reset<<<grid_for(n, B), B, 0, s>>>(cand, n, best, alive, cand2, nnext);
+      CR_CHECK_LAUNCH();
+      std::swap(cand, cand2);
+      n = read_scalar(nnext, s, hs);
+      ++rounds;
+    }
+    st.rounds[d] = rounds;
+    S.R.n[d] = int64_t(read_scalar(nrec, s, hs));
+    return true;
+  }
   {
     uint64_t* rootkey = ws.alloc<uint64_t>(nb + 1);
     k_dual_roots<<<grid_for(nv, B), B, 0, s>>>(S.births, G, parent, rootkey,
@@ -1605,7 +1660,10 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
 // In a full barcode the reduction of the top dimension is cheap once lower dimensions are cleared;
 // the dual union-find wins while its roots fit a fast single-CTA pass (measured: C1 2.7k roots,
 // 1.1 vs 2.0 ms; C4 50k roots, 15.8 vs 8.7 ms).
-constexpr unsigned DUAL_MAX_BASINS = 16384;
+unsigned dual_max_basins() {  // tuning knob CR_DUAL_MAX (measurement); default: always
+  const char* e = std::getenv("CR_DUAL_MAX");
+  return e ? unsigned(std::strtoul(e, nullptr, 10)) : 0xFFFFFFFFu;
+}
 bool use_dual(const Geom& g, int d) {
   if (d != g.D - 1 || d < 1) return false;
   const char* e = std::getenv("CR_TOP_REDUCE");  // force the coboundary reduction (cross-checks)
@@ -1738,7 +1796,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       st.apparent[d] = int64_t(hs.p[d]);
       st.cells[d] = int64_t(hs.p[4 + d]);
     }
-    if (g.D < 2 || top_dual(S, g.D - 1, ws, hs, st, unsigned(SMEM_BASINS))) {
+    if (g.D < 2 || top_dual(S, g.D - 1, ws, hs, st, 0xFFFFFFFFu)) {
       prof_mark(s, "top_dual");
       return;
     }
@@ -1778,7 +1836,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   S.R.rec[0] = ws.alloc<uint64_t>(st.cells[0]);
   unsigned long long* nrec0 = cnt + 13;
   const unsigned nb = unsigned(st.columns[0]);
-  if (nb <= unsigned(SMEM_BASINS)) {
+  if (nb <= smem_basins_max()) {
     // few basins: shared-memory rounds in one CTA
     uint64_t* rootkey = ws.alloc<uint64_t>(nb + 1);
     unsigned* nroot = reinterpret_cast<unsigned*>(cnt + 15);
@@ -1841,7 +1899,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     ws.release(parent);
     static const char* names1[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
     for (int d = 1; d <= dmax; ++d) {
-      if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, DUAL_MAX_BASINS)))
+      if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, dual_max_basins())))
         reduce_dimension(S, d, ws, hs, st);
       prof_mark(s, names1[d]);
     }
@@ -1882,7 +1940,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
 
   static const char* names[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
   for (int d = 1; d <= dmax; ++d) {
-    if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, DUAL_MAX_BASINS)))
+    if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, dual_max_basins())))
       reduce_dimension(S, d, ws, hs, st);
     prof_mark(s, names[d]);
   }
