@@ -46,6 +46,10 @@ def _load():
                                   vp, vp, vp, vp, ctypes.c_int64, vp, vp]
         lib.oracle_births.restype = ctypes.c_int
         lib.oracle_births.argtypes = [vp, i64p, ctypes.c_int, vp]
+        lib.oracle_ph_f64.restype = ctypes.c_int64
+        lib.oracle_ph_f64.argtypes = lib.oracle_ph.argtypes
+        lib.oracle_births_f64.restype = ctypes.c_int
+        lib.oracle_births_f64.argtypes = lib.oracle_births.argtypes
         _lib = lib
     return _lib
 
@@ -76,8 +80,8 @@ def max_pairs(shape, maxdim: int) -> int:
 @dataclass
 class OracleResult:
     dim: np.ndarray        # int32 (M,)
-    birth: np.ndarray      # float32 (M,)
-    death: np.ndarray      # float32 (M,), +inf for essential classes
+    birth: np.ndarray      # float32 (M,) (float64 for ph(..., dtype=np.float64))
+    death: np.ndarray      # same dtype as birth, +inf for essential classes
     cell: np.ndarray       # uint32 (M,), kidx of the birth cell
     partner: np.ndarray | None  # uint32 Khalimsky-size or None
     stats: np.ndarray      # int64 (4, 3): per dim [positive, zero-length, essential]
@@ -88,21 +92,29 @@ class OracleResult:
                          self.death.astype(np.float64)], axis=1)
 
 
-def ph(image: np.ndarray, maxdim: int, twist: bool = True, partner: bool = False) -> OracleResult:
-    """Persistence of K(image) over Z/2; see cr_oracle.cpp for the algorithm and citations."""
+def ph(image: np.ndarray, maxdim: int, twist: bool = True, partner: bool = False,
+       dtype=np.float32) -> OracleResult:
+    """Persistence of K(image) over Z/2; see cr_oracle.cpp for the algorithm and citations.
+
+    dtype=np.float32 (default) computes in float32 (the image is cast); np.float64 runs the same
+    algorithm in double precision (oracle_ph_f64, the paper's precision PAPER.md:188)."""
     lib = _load()
-    img = np.ascontiguousarray(image, dtype=np.float32)
+    dtype = np.dtype(dtype)
+    if dtype not in (np.float32, np.float64):
+        raise ValueError("dtype must be float32 or float64")
+    img = np.ascontiguousarray(image, dtype=dtype)
     shape = img.shape
     if img.ndim < 1 or img.ndim > 3:
         raise ValueError("ndim must be 1, 2 or 3")
     cap = max_pairs(shape, max(0, min(maxdim, 3)))
     dim = np.empty(cap, np.int32)
-    birth = np.empty(cap, np.float32)
-    death = np.empty(cap, np.float32)
+    birth = np.empty(cap, dtype)
+    death = np.empty(cap, dtype)
     cell = np.empty(cap, np.uint32)
     part = np.empty(int(np.prod(khalimsky_shape(shape))), np.uint32) if partner else None
     stats = np.zeros(12, np.int64)
-    n = lib.oracle_ph(img.ctypes.data, _shape_arg(shape), img.ndim, int(maxdim), int(bool(twist)),
+    fn = lib.oracle_ph if dtype == np.float32 else lib.oracle_ph_f64
+    n = fn(img.ctypes.data, _shape_arg(shape), img.ndim, int(maxdim), int(bool(twist)),
                       dim.ctypes.data, birth.ctypes.data, death.ctypes.data, cell.ctypes.data,
                       cap, part.ctypes.data if part is not None else None, stats.ctypes.data)
     if n < 0:
@@ -111,11 +123,13 @@ def ph(image: np.ndarray, maxdim: int, twist: bool = True, partner: bool = False
     return OracleResult(dim[:n], birth[:n], death[:n], cell[:n], part, stats.reshape(4, 3))
 
 
-def births(image: np.ndarray) -> np.ndarray:
-    """Khalimsky-grid cell births (float32, +inf = absent), shape khalimsky_shape(image.shape)."""
+def births(image: np.ndarray, dtype=np.float32) -> np.ndarray:
+    """Khalimsky-grid cell births (+inf = absent), shape khalimsky_shape(image.shape)."""
     lib = _load()
-    img = np.ascontiguousarray(image, dtype=np.float32)
-    out = np.empty(khalimsky_shape(img.shape), np.float32)
-    if lib.oracle_births(img.ctypes.data, _shape_arg(img.shape), img.ndim, out.ctypes.data) != 0:
+    dtype = np.dtype(dtype)
+    img = np.ascontiguousarray(image, dtype=dtype)
+    out = np.empty(khalimsky_shape(img.shape), dtype)
+    fn = lib.oracle_births if dtype == np.float32 else lib.oracle_births_f64
+    if fn(img.ctypes.data, _shape_arg(img.shape), img.ndim, out.ctypes.data) != 0:
         raise ValueError("oracle: invalid input")
     return out

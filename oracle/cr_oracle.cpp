@@ -1,7 +1,8 @@
 // cr_oracle.cpp -- TEST INFRASTRUCTURE ONLY.
 //
 // A plain, slow, obviously-correct CPU computation of the Z/2 persistence barcode of
-// the weighted cubical complex K(phi) (V-construction) of a 1D/2D/3D float32 image.
+// the weighted cubical complex K(phi) (V-construction) of a 1D/2D/3D float32 image (and, with the
+// same code instantiated for double, of a float64 image: the paper's own precision).
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
 // load this library.  It shares no code, header or table with the CUDA path
 // (paper_2005_12692_b200/csrc); the product never links or imports it.
@@ -45,32 +46,34 @@ struct Grid {
   int64_t kidx(int64_t X, int64_t Y, int64_t Z) const { return (Z * KY + Y) * KX + X; }
 };
 
+template <class T>
 struct Cell {
-  float birth;
+  T birth;
   int dim;
   uint32_t kidx;
 };
 
 // Step 1+2: cell births over the Khalimsky grid; returns false on NaN.
-bool cell_births(const float* image, const Grid& g, std::vector<float>& birth) {
+template <class T>
+bool cell_births(const T* image, const Grid& g, std::vector<T>& birth) {
   const int64_t nvox = g.nx * g.ny * g.nz;
-  std::vector<float> v(nvox);
+  std::vector<T> v(nvox);
   for (int64_t i = 0; i < nvox; ++i) {
-    float f = image[i];
+    T f = image[i];
     if (std::isnan(f)) return false;
-    if (f == 0.0f) f = 0.0f;  // -0.0 -> +0.0 (reading R7)
+    if (f == T(0)) f = T(0);  // -0.0 -> +0.0 (reading R7)
     v[i] = f;
   }
-  birth.assign(g.ncells(), 0.0f);
+  birth.assign(g.ncells(), T(0));
   for (int64_t Z = 0; Z < g.KZ; ++Z)
     for (int64_t Y = 0; Y < g.KY; ++Y)
       for (int64_t X = 0; X < g.KX; ++X) {
         // vertices: floor/ceil of half the Khalimsky coordinate on every odd axis
-        float b = -INFINITY;
+        T b = -T(INFINITY);
         for (int64_t z = Z / 2; z <= (Z + 1) / 2; ++z)
           for (int64_t y = Y / 2; y <= (Y + 1) / 2; ++y)
             for (int64_t x = X / 2; x <= (X + 1) / 2; ++x) {
-              float f = v[(z * g.ny + y) * g.nx + x];
+              T f = v[(z * g.ny + y) * g.nx + x];
               if (f > b) b = f;  // birth = max over the cell's vertices
             }
         birth[g.kidx(X, Y, Z)] = b;
@@ -115,21 +118,7 @@ bool setup_grid(const int64_t* shape, int ndim, Grid& g) {
   return true;
 }
 
-}  // namespace
-
-extern "C" {
-
-// Khalimsky-grid births (float32, +inf for absent cells).  0 on success, -1 on bad input/NaN.
-int oracle_births(const float* image, const int64_t* shape, int ndim, float* out) {
-  Grid g;
-  if (!image || !out || !setup_grid(shape, ndim, g)) return -1;
-  std::vector<float> b;
-  if (!cell_births(image, g, b)) return -1;
-  std::memcpy(out, b.data(), sizeof(float) * b.size());
-  return 0;
-}
-
-// Full persistence computation.
+// Steps 3-6 for either value type (float32 product precision, float64 paper precision).
 //   out_dim/out_birth/out_death/out_cell: capacity `cap` entries (may be NULL if cap == 0);
 //     pairs with death > birth and essential classes (death = +inf), dims <= maxdim,
 //     ordered by (dim, birth-cell kidx) ascending.
@@ -139,21 +128,22 @@ int oracle_births(const float* image, const int64_t* shape, int ndim, float* out
 //     [3d+2] essential classes (all dims, independent of maxdim).
 // Returns the number of output pairs (may exceed cap; nothing beyond cap is written),
 // or -1 on invalid input (NaN, bad shape, maxdim < 0).
-int64_t oracle_ph(const float* image, const int64_t* shape, int ndim, int maxdim, int twist,
-                  int32_t* out_dim, float* out_birth, float* out_death, uint32_t* out_cell,
-                  int64_t cap, uint32_t* partner, int64_t* stats) {
+template <class T>
+int64_t ph_impl(const T* image, const int64_t* shape, int ndim, int maxdim, int twist,
+                int32_t* out_dim, T* out_birth, T* out_death, uint32_t* out_cell,
+                int64_t cap, uint32_t* partner, int64_t* stats) {
   Grid g;
   if (!image || maxdim < 0 || !setup_grid(shape, ndim, g)) return -1;
-  std::vector<float> birth;
+  std::vector<T> birth;
   if (!cell_births(image, g, birth)) return -1;
   const int64_t N = g.ncells();
 
   // Step 3: the present cells in filtration order (birth, dim, kidx).
-  std::vector<Cell> cells;
+  std::vector<Cell<T>> cells;
   cells.reserve(N);
   for (int64_t k = 0; k < N; ++k)
-    if (birth[k] != INFINITY) cells.push_back({birth[k], cell_dim(g, k), uint32_t(k)});
-  std::sort(cells.begin(), cells.end(), [](const Cell& a, const Cell& b) {
+    if (birth[k] != T(INFINITY)) cells.push_back({birth[k], cell_dim(g, k), uint32_t(k)});
+  std::sort(cells.begin(), cells.end(), [](const Cell<T>& a, const Cell<T>& b) {
     if (a.birth != b.birth) return a.birth < b.birth;
     if (a.dim != b.dim) return a.dim < b.dim;
     return a.kidx < b.kidx;
@@ -201,16 +191,16 @@ int64_t oracle_ph(const float* image, const int64_t* shape, int ndim, int maxdim
       partner[cells[r].kidx] =
           paired_with[r] == NONE ? PARTNER_ESSENTIAL : cells[paired_with[r]].kidx;
   }
-  struct Out { int32_t dim; float b, d; uint32_t cell; };
+  struct Out { int32_t dim; T b, d; uint32_t cell; };
   std::vector<Out> outs;
   int64_t st[12] = {0};
   for (uint32_t r = 0; r < M; ++r) {
-    const Cell& c = cells[r];
+    const Cell<T>& c = cells[r];
     if (paired_with[r] == NONE) {
       st[3 * c.dim + 2]++;
-      if (c.dim <= maxdim) outs.push_back({c.dim, c.birth, INFINITY, c.kidx});
+      if (c.dim <= maxdim) outs.push_back({c.dim, c.birth, T(INFINITY), c.kidx});
     } else if (paired_with[r] > r) {  // r is the birth (lower) cell of its pair
-      float death = cells[paired_with[r]].birth;
+      T death = cells[paired_with[r]].birth;
       if (death > c.birth) {
         st[3 * c.dim]++;
         if (c.dim <= maxdim) outs.push_back({c.dim, c.birth, death, c.kidx});
@@ -231,6 +221,56 @@ int64_t oracle_ph(const float* image, const int64_t* shape, int ndim, int maxdim
   }
   if (stats) std::memcpy(stats, st, sizeof(st));
   return int64_t(outs.size());
+}
+
+}  // namespace
+
+extern "C" {
+
+// Khalimsky-grid births (float32, +inf for absent cells).  0 on success, -1 on bad input/NaN.
+int oracle_births(const float* image, const int64_t* shape, int ndim, float* out) {
+  Grid g;
+  if (!image || !out || !setup_grid(shape, ndim, g)) return -1;
+  std::vector<float> b;
+  if (!cell_births(image, g, b)) return -1;
+  std::memcpy(out, b.data(), sizeof(float) * b.size());
+  return 0;
+}
+
+// Full persistence computation (float32 image; births and deaths are float32).
+//   out_dim/out_birth/out_death/out_cell: capacity `cap` entries (may be NULL if cap == 0);
+//     pairs with death > birth and essential classes (death = +inf), dims <= maxdim,
+//     ordered by (dim, birth-cell kidx) ascending.
+//   partner: NULL or Khalimsky-size uint32: paired cell's kidx, 0xFFFFFFFF essential,
+//     0xFFFFFFFE absent (+inf birth).  Always covers all dimensions.
+//   stats: NULL or int64[12]: per dim d in 0..3: [3d] positive pairs, [3d+1] zero pairs,
+//     [3d+2] essential classes (all dims, independent of maxdim).
+// Returns the number of output pairs (may exceed cap; nothing beyond cap is written),
+// or -1 on invalid input (NaN, bad shape, maxdim < 0).
+int64_t oracle_ph(const float* image, const int64_t* shape, int ndim, int maxdim, int twist,
+                  int32_t* out_dim, float* out_birth, float* out_death, uint32_t* out_cell,
+                  int64_t cap, uint32_t* partner, int64_t* stats) {
+  return ph_impl<float>(image, shape, ndim, maxdim, twist, out_dim, out_birth, out_death,
+                        out_cell, cap, partner, stats);
+}
+
+// The same computation on a float64 image (the paper's own precision): the
+// filtration order compares doubles, births and deaths are doubles.  Same contract as oracle_ph.
+int64_t oracle_ph_f64(const double* image, const int64_t* shape, int ndim, int maxdim, int twist,
+                      int32_t* out_dim, double* out_birth, double* out_death, uint32_t* out_cell,
+                      int64_t cap, uint32_t* partner, int64_t* stats) {
+  return ph_impl<double>(image, shape, ndim, maxdim, twist, out_dim, out_birth, out_death,
+                         out_cell, cap, partner, stats);
+}
+
+// Khalimsky-grid births of a float64 image.  0 on success, -1 on bad input/NaN.
+int oracle_births_f64(const double* image, const int64_t* shape, int ndim, double* out) {
+  Grid g;
+  if (!image || !out || !setup_grid(shape, ndim, g)) return -1;
+  std::vector<double> b;
+  if (!cell_births(image, g, b)) return -1;
+  std::memcpy(out, b.data(), sizeof(double) * b.size());
+  return 0;
 }
 
 }  // extern "C"

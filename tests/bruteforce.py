@@ -29,7 +29,9 @@ INF = math.inf
 
 
 def _canon(img):
-    a = np.asarray(img, dtype=np.float32).astype(np.float64)
+    a = np.asarray(img)
+    # float64 images keep their precision; everything else is read as float32
+    a = a.astype(np.float64) if a.dtype == np.float64 else a.astype(np.float32).astype(np.float64)
     a = np.where(a == 0.0, 0.0, a)  # -0.0 -> +0.0
     s = [1] * (3 - a.ndim) + list(a.shape)
     return a.reshape(s)  # (nz, ny, nx)

@@ -269,3 +269,88 @@ def test_contractible_domain_one_essential():
         r = oracle.ph(gen.iid_uniform(shape, seed=3), 2)
         assert int(np.sum(np.isinf(r.death))) == 1
         assert int(r.dim[np.isinf(r.death)][0]) == 0
+
+
+# ---------------------------------------------------------------- float64
+#
+# The paper's implementation stores pixel values as doubles.  oracle_ph_f64 runs
+# the same steps in double precision; these pins use values that differ BELOW float32
+# resolution (1 + k*2^-40 all round to 1.0f), so a float64 path that rounded through float32
+# anywhere would collapse them and fail.
+
+def _tiny(k, base=1.0, step=2.0 ** -40):
+    return base + np.asarray(k, np.float64) * step
+
+
+def test_f64_values_below_f32_resolution():
+    k = np.arange(6, dtype=np.float64)
+    assert np.all(_tiny(k).astype(np.float32) == np.float32(1.0))
+    img = _tiny(np.array([3, 0, 2, 1, 5, 4]))
+    r = oracle.ph(img, 0, dtype=np.float64)
+    assert r.birth.dtype == np.float64
+    # f32 collapses everything to one constant component; f64 sees three minima
+    assert len(oracle.ph(img, 0).dim) == 1
+    exp = Counter([(0, _tiny(0), INF), (0, _tiny(1), _tiny(2)), (0, _tiny(4), _tiny(5))])
+    assert _multiset(r) == exp
+
+
+def test_f64_exhaustive_2x2_levels3():
+    for vals in itertools.product([0, 1, 2], repeat=4):
+        img = _tiny(np.array(vals).reshape(2, 2))
+        r = oracle.ph(img, 1, partner=True, dtype=np.float64)
+        assert _multiset(r) == bf.barcode_by_ranks(img, 1), vals
+
+
+def test_f64_fuzz_against_bruteforce():
+    rng = np.random.default_rng(777)
+    for t in range(150):
+        nd = int(rng.integers(1, 4))
+        shape = {1: (int(rng.integers(1, 12)),),
+                 2: tuple(int(s) for s in rng.integers(1, 5, size=2)),
+                 3: tuple(int(s) for s in rng.integers(1, 4, size=3))}[nd]
+        img = _tiny(rng.integers(0, 5, size=shape))
+        if t % 3 == 0:
+            img[rng.random(shape) < 0.15] = np.inf
+        r = oracle.ph(img, 2, partner=(t % 4 == 0), dtype=np.float64)
+        assert _multiset(r) == bf.barcode_by_ranks(img, 2), (t, img)
+        if t % 4 == 0:
+            for kk, p in bf.cohomology_pairing(img).items():
+                assert r.partner[kk] == (oracle.PARTNER_ESSENTIAL if p is None else p)
+
+
+def test_f64_pairing_equals_integer_levels():
+    """Strictly increasing g: pairing of g(k) in float64 == pairing of k (exact in float32)."""
+    for s, shape in enumerate([(6, 7), (3, 4, 5), (40,)]):
+        k = gen.small_int_image(shape, 9, seed=900 + s, inf_frac=0.1 if s % 2 else 0.0)
+        r32 = oracle.ph(k, 2, partner=True)
+        r64 = oracle.ph(_tiny(k.astype(np.float64)), 2, partner=True, dtype=np.float64)
+        assert np.array_equal(r32.partner, r64.partner)
+        fin = np.isfinite(r32.death)
+        assert np.array_equal(_tiny(r32.birth.astype(np.float64)), r64.birth)
+        assert np.array_equal(_tiny(r32.death[fin].astype(np.float64)), r64.death[fin])
+
+
+def test_f64_elder_1d_and_union_find():
+    x = gen.random_walk(2000, seed=8).astype(np.float64) * 2.0 ** -30 + 1.0
+    r = oracle.ph(x, 0, partner=True, dtype=np.float64)
+    ref = bf.elder_1d(x)
+    for i in range(len(x)):
+        assert r.partner[2 * i] == (oracle.PARTNER_ESSENTIAL if ref[i] is None else 2 * ref[i] + 1)
+    img = _tiny(gen.small_int_image((5, 6), 7, seed=4))
+    r = oracle.ph(img, 0, partner=True, dtype=np.float64)
+    for v, e in bf.union_find_h0(img).items():
+        assert r.partner[v] == (oracle.PARTNER_ESSENTIAL if e is None else e)
+
+
+def test_f64_births_and_invalid():
+    img = _tiny(gen.small_int_image((3, 4, 5), 7, seed=12))
+    B = oracle.births(img, dtype=np.float64)
+    assert B.dtype == np.float64
+    KZ, KY, KX = B.shape
+    for c in bf.enumerate_cells(img):
+        assert B.reshape(-1)[c["kidx"]] == c["birth"]
+    with pytest.raises(ValueError):
+        oracle.ph(np.array([1.0, np.nan]), 0, dtype=np.float64)
+    a = oracle.ph(np.array([-0.0, 1.0, 0.0]), 0, partner=True, dtype=np.float64)
+    b = oracle.ph(np.array([0.0, 1.0, 0.0]), 0, partner=True, dtype=np.float64)
+    assert np.array_equal(a.partner, b.partner)
