@@ -40,7 +40,9 @@ CONFIG_DESC = {
     "c4": "3D 128^3 GRF sigma=2, H0-H2",
     "c5": "3D 384^3 GRF sigma=3, +inf outside ball r=180, H0-H2",
     "c5b": "64 x 128^3 GRF sigma=3 in ball r=60, H0-H2, sharded by volume",
+    "c2f64": "1D Gaussian random walk, 2^24 float64 samples (kept in double), H0",
 }
+F64 = {"c2f64"}
 BATCHED = {"c3", "c5b"}
 
 
@@ -121,6 +123,8 @@ def make_input(cfg: str, rank: int, world: int):
         vols, md = gen.config("c5b")
         a, b = shard_range(len(vols), rank, world)
         return vols[a:b], md, len(vols)
+    if cfg == "c2f64":
+        return gen.random_walk(1 << 24, 2, dtype=np.float64), 0, 1
     img, md = gen.config(cfg)
     return img, md, 1
 
@@ -134,6 +138,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     host_img, maxdim, units_total = make_input(args.config, rank, world)
     batched = args.config in BATCHED
+    f64 = args.config in F64
     nvox_local = int(np.prod(host_img.shape))
     img = torch.from_numpy(np.ascontiguousarray(host_img)).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -162,6 +167,8 @@ def run_ours(args, rank, world, local_rank):
                 p_all, _ = gather_barcodes(pairs[:m], offsets)
                 return int(p_all.shape[0])
             return m
+        if f64:
+            return len(cr.barcodes_f64(img, maxdim, capacity=cap).dim)
         return len(cr.barcodes(img, maxdim, out=(pairs, None)).pairs)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
@@ -209,7 +216,36 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the host entry point (pinned buffers, copies inside the region)
     e2e = None
-    if not batched:
+    if f64:  # public API with host buffers: pinned double in, float64 bars out
+        pin_in = torch.from_numpy(np.ascontiguousarray(host_img)).pin_memory()
+        dev_in = torch.empty_like(pin_in, device=dev)
+
+        def e2e_step():
+            dev_in.copy_(pin_in, non_blocking=True)
+            bc = cr.barcodes_f64(dev_in, maxdim, capacity=cap)
+            res = (bc.dim.cpu(), bc.birth.cpu(), bc.death.cpu())
+            return len(res[0])
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_ev = []
+        for k in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            m_out = e2e_step()
+            b.record(stream)
+            e2e_ev.append((a, b))
+        torch.cuda.synchronize()
+        e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+        if dist.is_initialized():
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": nvox_total / (e2e_ms / args.steps / 1e3), "unit": "voxels/s",
+               "h2d_bytes_per_step": nvox_local * 8, "d2h_bytes_per_step": m_out * 20,
+               "ms_per_step": e2e_ms / args.steps}
+    elif not batched:
         pin_in = torch.from_numpy(np.ascontiguousarray(host_img)).pin_memory()
         pin_out = torch.empty((cap, 3), dtype=torch.int32).pin_memory()
         for _ in range(max(1, args.warmup)):
@@ -267,7 +303,8 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded, workloads/generators.py)",
         "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                    "voxels_per_step": nvox_total, "maxdim": maxdim,
@@ -307,6 +344,10 @@ def algorithmic_bytes(cfg, stage, nvox, st, n_out, shape=None):
         return 28 * K + 12 * n_out                # read keys/death/cells, write bars
     if stage.startswith("1d_tree"):
         return 32 * K                             # read level 0, write levels >= 1 (~K)
+    if stage in ("f64_rank", "f64_cast"):        # read the doubles, write the float32 surrogate
+        return 12 * nvox + (8 * nvox if stage == "f64_rank" else 0)  # + table of distinct values
+    if stage == "f64_map":
+        return 12 * n_out + 24 * n_out            # read float32 bars, write float64 bars
     kcells = khalimsky_cells(shape) if shape else sum(st["cells"])
     if stage == "births":                         # read the image, write every Khalimsky cell
         return 4 * nvox + 4 * kcells
@@ -348,9 +389,9 @@ def cpu_baseline(cfg, host_img, maxdim):
     """The oracle (single-threaded C++), as it stands, on a bounded sample of the workload."""
     import oracle
     oracle.build()
-    if cfg == "c2":
+    if cfg in ("c2", "c2f64"):
         sample = host_img
-        desc = "full C2 series (2^24 samples), one run"
+        desc = f"full {cfg} series (2^24 samples), one run"
     elif cfg in BATCHED:
         sample = host_img[:64]
         desc = f"first 64 images of the {cfg} batch"
@@ -365,7 +406,7 @@ def cpu_baseline(cfg, host_img, maxdim):
         for im in sample:
             oracle.ph(im, maxdim)
     else:
-        oracle.ph(sample, maxdim)
+        oracle.ph(sample, maxdim, dtype=sample.dtype)
     dt = time.perf_counter() - t0
     return {"value": float(np.prod(sample.shape)) / dt, "unit": "voxels/s", "cores": 1,
             "kind": "oracle", "sample": desc, "seconds": dt}
@@ -378,8 +419,8 @@ def run_reference(args, rank, world):
     import oracle
     oracle.build()
     host_img, maxdim, _ = make_input(args.config, 0, 1)
-    if args.config == "c2":
-        sample, desc = host_img[: 1 << 20], "first 2^20 samples of C2 per step"
+    if args.config in ("c2", "c2f64"):
+        sample, desc = host_img[: 1 << 20], f"first 2^20 samples of {args.config} per step"
     elif args.config in BATCHED:
         sample, desc = host_img[:16], f"first 16 images of {args.config} per step"
     elif args.config == "c5":
@@ -392,7 +433,7 @@ def run_reference(args, rank, world):
             for im in sample:
                 oracle.ph(im, maxdim)
         else:
-            oracle.ph(sample, maxdim)
+            oracle.ph(sample, maxdim, dtype=sample.dtype)
 
     for _ in range(args.warmup):
         one()
@@ -403,8 +444,8 @@ def run_reference(args, rank, world):
     v = float(np.prod(sample.shape)) / dt
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "voxels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded, workloads/generators.py)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.config in F64 else "f32", "data": "synthetic (seeded, workloads/generators.py)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "maxdim": maxdim},
             "cpu_baseline": {"value": v, "unit": "voxels/s", "cores": 1, "kind": "oracle",
                              "sample": desc},

@@ -82,6 +82,26 @@ cr_status cr_barcodes_topdim(const float* image, const int64_t* shape, int ndim,
                              cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
                              int64_t* n_pairs, cr_stream_t stream);
 
+/* One bar of a float64 image (cr_barcodes_f64).  24 bytes; pad is 0. */
+typedef struct {
+  int32_t dim;
+  int32_t pad;
+  double birth;
+  double death;
+} cr_pair64;
+
+/* Barcode of a float64 image -- the paper's own value precision ("pixel values ... stored as
+ * double").  Arguments, output order and errors as for cr_barcodes, with a device
+ * float64 image and cr_pair64 bars whose endpoints are the image's own double values.  The
+ * filtration order compares doubles exactly: values that differ only below float32 resolution
+ * stay distinct.  Implementation: an order-isomorphic float32 surrogate (the cast when every value
+ * is a float32 value, else dense ranks from a device radix sort) run through cr_barcodes, bars
+ * mapped back; CR_EINVAL also when ranking is needed and prod(shape) >= 0x7F000000.
+ * cr_last_stats describes the float32 pass. */
+cr_status cr_barcodes_f64(const double* image, const int64_t* shape, int ndim, int maxdim,
+                          cr_pair64* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,
+                          int64_t* n_pairs, cr_stream_t stream);
+
 /* Same as cr_barcodes with HOST image and HOST outputs: the library copies the image in and the
  * bars out on `stream` (end-to-end entry point; pinned host memory is fastest). */
 cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int ndim, int maxdim,

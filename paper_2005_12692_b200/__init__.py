@@ -60,6 +60,8 @@ _lib.cr_barcodes_batched.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_in
 _lib.cr_barcodes_topdim.restype = ctypes.c_int
 _lib.cr_barcodes_topdim.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _vp, _i64, _i64p, _vp]
 _lib.cr_death_cells.restype = ctypes.c_int
+_lib.cr_barcodes_f64.argtypes = [_vp, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, _i64p, _vp]
+_lib.cr_barcodes_f64.restype = ctypes.c_int
 _lib.cr_death_cells.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _i64, _vp, _vp]
 _lib.cr_lifetime_image.restype = ctypes.c_int
 _lib.cr_lifetime_image.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, ctypes.c_float,
@@ -79,7 +81,7 @@ _lib.cr_set_profiling.argtypes = [ctypes.c_int]
 
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
             "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling",
-            "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim"]
+            "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim", "cr_barcodes_f64"]
 
 
 class CrError(RuntimeError):
@@ -313,3 +315,38 @@ def barcodes_topdim(image, cells: bool = False) -> "Barcode":
     _check(st)
     m = int(n.value)
     return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None)
+
+
+@dataclass
+class Barcode64:
+    """Bars of a float64 image (cr_barcodes_f64), ordered by (dim, birth cell kidx)."""
+    dim: "object"             # torch int32 (M,)
+    birth: "object"           # torch float64 (M,)
+    death: "object"           # torch float64 (M,), +inf for essential classes
+    cells: "object | None"    # uint32 (as int32 storage) kidx of birth cells, or None
+
+    def numpy(self):
+        c = self.cells.cpu().numpy().view(np.uint32) if self.cells is not None else None
+        return (self.dim.cpu().numpy(), self.birth.cpu().numpy(), self.death.cpu().numpy(), c)
+
+
+def barcodes_f64(image, maxdim: int = 1, cells: bool = False,
+                 capacity: int | None = None) -> Barcode64:
+    """Barcode of a CUDA float64 tensor in float64 (the paper's precision)."""
+    import torch
+    if not (isinstance(image, torch.Tensor) and image.is_cuda and image.dtype == torch.float64):
+        raise TypeError("image must be a CUDA float64 tensor")
+    image = image.contiguous()
+    shape = tuple(image.shape)
+    cap = max_pairs(shape, maxdim) if capacity is None else int(capacity)
+    raw = torch.empty((max(cap, 1), 3), dtype=torch.float64, device=image.device)  # cr_pair64
+    cbuf = torch.empty((max(cap, 1),), dtype=torch.int32, device=image.device) if cells else None
+    n = ctypes.c_int64(0)
+    st = _lib.cr_barcodes_f64(image.data_ptr(), _shape(shape), len(shape), int(maxdim),
+                              raw.data_ptr(), cbuf.data_ptr() if cbuf is not None else None, cap,
+                              ctypes.byref(n), _stream_ptr(torch, image.device))
+    _check(st)
+    m = int(n.value)
+    raw = raw[:m]
+    dim = raw.view(torch.int32).view(-1, 6)[:, 0]  # int32 dim at byte 0 of each 24-byte pair
+    return Barcode64(dim, raw[:, 1], raw[:, 2], cbuf[:m] if cbuf is not None else None)

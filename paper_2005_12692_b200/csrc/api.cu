@@ -157,6 +157,25 @@ int report_dmax(const Geom& g, int maxdim) {
 }
 
 }  // namespace
+
+// The float32 barcode of one image on the caller's workspace (no profiling brackets, no sync):
+// the body of cr_barcodes, shared with cr_barcodes_f64's surrogate pass.
+int64_t barcodes_core(const float* image, const Geom& g, int maxdim, cr_pair* out_pairs,
+                      uint32_t* out_birth_cells, int64_t out_capacity, Workspace& ws,
+                      HostScalars& hs, cr_stats& st) {
+  if (g.D <= 1 && !force_general()) {
+    st.path = 1;
+    return barcodes_1d(image, g.nvox, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
+  }
+  st.path = 2;
+  GeneralState S;
+  int dm = report_dmax(g, maxdim);
+  run_general(image, g, dm, ws, hs, S, st);
+  return emit_bars(S, dm, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
+}
+
+void set_last_stats(const cr_stats& st) { g_last_stats = st; }
+
 }  // namespace cr
 
 using namespace cr;
@@ -211,17 +230,8 @@ cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int ma
     HostScalars hs;
     cr_stats st{};
     prof_begin(s);
-    int64_t n;
-    if (g.D <= 1 && !force_general()) {
-      st.path = 1;
-      n = barcodes_1d(image, g.nvox, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
-    } else {
-      st.path = 2;
-      GeneralState S;
-      int dm = report_dmax(g, maxdim);
-      run_general(image, g, dm, ws, hs, S, st);
-      n = emit_bars(S, dm, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
-    }
+    const int64_t n = barcodes_core(image, g, maxdim, out_pairs, out_birth_cells, out_capacity, ws,
+                                    hs, st);
     CR_CUDA(cudaStreamSynchronize(s));
     prof_end(st);
     *n_pairs = n;

@@ -67,6 +67,12 @@ int64_t barcodes_batched_small_2d(const float* images, int64_t batch, int64_t ny
                                   int64_t* out_offsets, Workspace& ws, HostScalars& hs,
                                   cr_stats& st);
 
+// The float32 barcode on the caller's workspace, no profiling brackets (api.cu).
+int64_t barcodes_core(const float* image, const Geom& g, int maxdim, cr_pair* out_pairs,
+                      uint32_t* out_birth_cells, int64_t out_capacity, Workspace& ws,
+                      HostScalars& hs, cr_stats& st);
+void set_last_stats(const cr_stats& st);
+
 // Device-wide helpers (util.cu).
 void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws);
 void exclusive_sum_u32(const uint32_t* in, uint32_t* out, int64_t n, Workspace& ws);

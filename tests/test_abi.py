@@ -21,7 +21,7 @@ def cr():
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "cr.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(cr_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(cr_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(cr):

@@ -116,3 +116,27 @@ def test_c5_properties(cr):
         alive = (b <= t) & (t < e)
         rhs = int(np.sum(np.where(d[alive] % 2 == 0, 1, -1)))
         assert lhs == rhs, t
+
+
+def _eq64(cr, img, md, ctx):
+    import torch
+    o = oracle.ph(img, md, dtype=np.float64)
+    d, b, e, c = cr.barcodes_f64(torch.from_numpy(img).cuda(), md, cells=True).numpy()
+    assert len(d) == len(o.dim), ctx
+    assert np.array_equal(d, o.dim), ctx
+    assert np.array_equal(c, o.cell), ctx
+    assert np.array_equal(b.view(np.uint64), o.birth.view(np.uint64)), ctx
+    assert np.array_equal(e.view(np.uint64), o.death.view(np.uint64)), ctx
+
+
+def test_c2_full_f64(cr):
+    """C2's random walk kept in float64 (rank path: 2^24 distinct doubles)."""
+    x = gen.random_walk(1 << 24, 2, dtype=np.float64)
+    _eq64(cr, x, 0, "c2_f64")
+
+
+def test_c1_and_c4_crop_f64(cr):
+    rng = np.random.default_rng(11)
+    _eq64(cr, rng.random((128, 128)), 1, "c1_f64")
+    _eq64(cr, gen.grf((48, 48, 48), 2.0, 4).astype(np.float64) + rng.random((48, 48, 48)) * 1e-12,
+          2, "c4crop_f64")

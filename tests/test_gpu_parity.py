@@ -441,3 +441,55 @@ def test_lifetime_image(cr):
             y, x = (int(c) // KX) // 2, (int(c) % KX) // 2
             ref[1 + d, y, x] = max(ref[1 + d, y, x], life)
         assert np.array_equal(out[b], ref), b
+
+
+# ---------------------------------------------------------------- float64 images
+
+def _check_f64(cr, img, maxdim, ctx=""):
+    import torch
+    img = np.ascontiguousarray(img, np.float64)
+    o = oracle.ph(img, maxdim, dtype=np.float64)
+    bc = cr.barcodes_f64(torch.from_numpy(img).cuda(), maxdim, cells=True)
+    d, b, e, c = bc.numpy()
+    assert len(d) == len(o.dim), (ctx, len(d), len(o.dim))
+    assert np.array_equal(d, o.dim), ctx
+    assert np.array_equal(c, o.cell), ctx
+    assert np.array_equal(b.view(np.uint64), o.birth.view(np.uint64)), ctx
+    assert np.array_equal(e.view(np.uint64), o.death.view(np.uint64)), ctx
+    return o
+
+
+def test_barcodes_f64_rank_path(cr):
+    """Values that differ below float32 resolution (all round to the same float32) -> rank path."""
+    step = 2.0 ** -40
+    cases = [
+        ("1d_small", (257,)), ("1d_tiles", (20011,)), ("2d", (61, 47)), ("2d_wide", (7, 3001)),
+        ("3d", (13, 17, 19)),
+    ]
+    for s, (name, shape) in enumerate(cases):
+        k = gen.small_int_image(shape, 50, seed=1200 + s, inf_frac=0.1 if s % 2 else 0.0)
+        img = 1.0 + k.astype(np.float64) * step
+        o = _check_f64(cr, img, 2, ctx=name)
+        if s % 2 == 0:
+            assert len(o.dim) > 1, name  # the sub-float32 structure is really there
+
+
+def test_barcodes_f64_iid_and_specials(cr):
+    rng = np.random.default_rng(4242)
+    for shape in [(5000,), (90, 110), (16, 18, 20)]:
+        _check_f64(cr, rng.random(shape), 2, ctx=shape)            # distinct doubles
+        _check_f64(cr, rng.standard_normal(shape) * 1e300, 2, ctx=shape)
+    img = rng.random((40, 41))
+    img[3, 4], img[5, 6], img[7, 8] = -np.inf, -0.0, 0.0
+    img[10:14, 10:14] = np.inf
+    _check_f64(cr, img, 1, ctx="specials")
+    # the exact (cast) path: float32-representable values
+    f = gen.iid_uniform((33, 35), seed=3).astype(np.float64)
+    o = _check_f64(cr, f, 1, ctx="exact")
+    g = oracle.ph(f.astype(np.float32), 1)
+    assert np.array_equal(o.birth, g.birth.astype(np.float64))
+    import torch
+    with pytest.raises(cr.CrError):
+        cr.barcodes_f64(torch.tensor([1.0, float("nan")], dtype=torch.float64).cuda(), 0)
+    with pytest.raises(TypeError):
+        cr.barcodes_f64(torch.zeros(4, device="cuda"), 0)

@@ -31,10 +31,11 @@ def iid_uniform(shape, seed: int = 1) -> np.ndarray:
     return np.random.default_rng(seed).random(tuple(shape), dtype=np.float32)
 
 
-def random_walk(n: int = 1 << 24, seed: int = 2) -> np.ndarray:
-    """C2: cumulative sum of N(0,1) steps in float64, cast to float32 (BJ:8)."""
+def random_walk(n: int = 1 << 24, seed: int = 2, dtype=np.float32) -> np.ndarray:
+    """C2: cumulative sum of N(0,1) steps in float64, cast to float32 (BJ:8).
+    dtype=np.float64 keeps the walk in double (the float64 variant)."""
     s = np.random.default_rng(seed).standard_normal(n)
-    return np.cumsum(s).astype(np.float32)
+    return np.cumsum(s).astype(dtype)
 
 
 def blobs(batch: int = 65536, seed: int = 3, size: int = 28, chunk: int = 4096) -> np.ndarray:
