@@ -10,6 +10,11 @@ namespace cr {
 const char* last_error_text();
 void set_profiling(bool on);
 static thread_local cr_stats g_last_stats;
+static thread_local uint64_t g_stats_gen = 0;  // prof_gen() when g_last_stats was committed
+static void commit_stats(const cr_stats& st) {
+  g_last_stats = st;
+  g_stats_gen = prof_gen();
+}
 
 namespace {
 
@@ -174,7 +179,7 @@ int64_t barcodes_core(const float* image, const Geom& g, int maxdim, cr_pair* ou
   return emit_bars(S, dm, out_pairs, out_birth_cells, out_capacity, ws, hs, st);
 }
 
-void set_last_stats(const cr_stats& st) { g_last_stats = st; }
+void set_last_stats(const cr_stats& st) { commit_stats(st); }
 
 }  // namespace cr
 
@@ -212,7 +217,9 @@ const char* cr_status_string(cr_status s) {
 }
 
 void cr_last_stats(cr_stats* out) {
-  if (out) *out = g_last_stats;
+  if (!out) return;
+  *out = g_last_stats;
+  if (g_stats_gen == prof_gen()) prof_fill(*out);
 }
 
 void cr_set_profiling(int enable) { cr::set_profiling(enable != 0); }
@@ -236,7 +243,7 @@ cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int ma
     prof_end(st);
     *n_pairs = n;
     if (n > out_capacity) return CR_ERANGE;
-    g_last_stats = st;
+    commit_stats(st);
     return CR_OK;
   } catch (const Error& e) {
     return fail(e);
@@ -266,7 +273,7 @@ cr_status cr_barcodes_topdim(const float* image, const int64_t* shape, int ndim,
     prof_end(st);
     *n_pairs = n;
     if (n > out_capacity) return CR_ERANGE;
-    g_last_stats = st;
+    commit_stats(st);
     return CR_OK;
   } catch (const Error& e) {
     return fail(e);
@@ -345,7 +352,7 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
         prof_end(st);
         *n_pairs = n;
         if (n > out_capacity) return CR_ERANGE;
-        g_last_stats = st;
+        commit_stats(st);
         return CR_OK;
       }
     }
@@ -425,7 +432,7 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
     prof_end(st);
     *n_pairs = nk;
     if (int64_t(nk) > out_capacity) return CR_ERANGE;
-    g_last_stats = st;
+    commit_stats(st);
     return CR_OK;
   } catch (const Error& e) {
     return fail(e);
@@ -451,7 +458,7 @@ cr_status cr_pairing(const float* image, const int64_t* shape, int ndim, uint32_
       emit_partner(S, partner, ws);
     }
     CR_CUDA(cudaStreamSynchronize(s));
-    g_last_stats = st;
+    commit_stats(st);
     return CR_OK;
   } catch (const Error& e) {
     return fail(e);

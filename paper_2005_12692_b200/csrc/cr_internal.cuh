@@ -84,6 +84,8 @@ void set_error_text(const std::string& s);
 void prof_begin(cudaStream_t s);
 void prof_mark(cudaStream_t s, const char* stage);  // the stage that just ended
 void prof_end(cr_stats& st);                         // after the call's final sync
+uint64_t prof_gen();                                 // profiled calls begun on this thread
+void prof_fill(cr_stats& st);  // stage times of the last call, if no call began since
 
 #define CR_CUDA(call)                                                                       \
   do {                                                                                      \

@@ -951,7 +951,11 @@ struct LevelsArgs {
   uint32_t* gctr;          // next gather chunk
   unsigned long long* tl;  // debug timeline (null unless CR_DEBUG_STATS)
   uint32_t* done;          // [l]: level l's count scan done (1); [NLEVELS + l]: its tiles done
+  uint32_t* exits;         // CTAs that finished (the last one publishes the control head)
+  const unsigned long long* ctl;  // control head (flags, counters, total): CTL_PUB words
+  unsigned long long* host_ctl;   // pinned host words receiving it (no separate D2H copy)
 };
+constexpr int CTL_PUB = 6;
 
 // Gather chunks of THREADS/32 regions (one per warp), taken from a global counter, until the
 // chunks run out or *until reaches goal (goal 0: no stop condition).  Returns false once exhausted.
@@ -976,7 +980,7 @@ __device__ bool gather_until(const LevelsArgs& A, const uint32_t* until, uint32_
   }
 }
 
-__global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
+__device__ __forceinline__ void levels_body(const LevelsArgs& A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
   Smem S = carve(smem);
@@ -1139,6 +1143,22 @@ __global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
   stamp(15);
 }
 
+__global__ void __launch_bounds__(THREADS) k1_levels_coop(LevelsArgs A) {
+  levels_body(A);
+  // the last CTA out writes the control head straight into pinned host memory: the host's
+  // stream sync then reads it without a separate copy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(A.exits, 1u) == gridDim.x - 1) {
+      __threadfence();
+#pragma unroll
+      for (int i = 0; i < CTL_PUB; ++i) A.host_ctl[i] = __ldcg(A.ctl + i);
+      __threadfence_system();
+    }
+  }
+}
+
 __global__ void k1_hole_flags(const cr_pair* __restrict__ in, int64_t n, uint32_t* flag) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) flag[i] = in[i].dim != -1;
@@ -1245,7 +1265,11 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   LA.nreg = nreg;
   LA.total = meta + 3;
   LA.gctr = reinterpret_cast<uint32_t*>(ctl + 6);
-  LA.done = LA.gctr + 1;  // 2 * NLEVELS - 1 words up to the holes
+  LA.done = LA.gctr + 1;  // 2 * NLEVELS words, then the exit counter, up to the holes
+  LA.exits = LA.done + 2 * NLEVELS;
+  static_assert(1 + 2 * NLEVELS + 1 <= 2 * (CTL_HEAD - 6), "control words fit the head");
+  LA.ctl = ctl;
+  LA.host_ctl = hs.p;
   // item levels are small (a random walk leaves ~0.5 % of basins undecided per tile); the gather
   // streams every bar: a few CTAs per SM keep enough loads in flight
   const int64_t blocks = std::max<int64_t>(
@@ -1260,15 +1284,18 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
       CR_CUDA(cudaMemsetAsync(LA.tl, 0, 32 * sizeof(unsigned long long), s));
       gt = LA.tl + 16;
     }
-    CR_CUDA(cudaMemcpyToSymbolAsync(g_tl, &gt, sizeof(gt), 0, cudaMemcpyHostToDevice, s));
+    static thread_local bool tl_set[64] = {};  // g_tl is non-null on this device
+    if (gt || tl_set[ws.device() & 63]) {       // no per-call copy in the common case
+      CR_CUDA(cudaMemcpyToSymbolAsync(g_tl, &gt, sizeof(gt), 0, cudaMemcpyHostToDevice, s));
+      tl_set[ws.device() & 63] = gt != nullptr;
+    }
   }
   void* args[] = {&LA};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k1_levels_coop, dim3(unsigned(blocks)),
                                       dim3(THREADS), args, SMEM, s));
   ++g_launch_count;
   prof_mark(s, "1d_levels_gather");
-  CR_CUDA(cudaMemcpyAsync(hs.p, ctl, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  CR_CUDA(cudaStreamSynchronize(s));
+  CR_CUDA(cudaStreamSynchronize(s));  // k1_levels_coop wrote ctl[0, CTL_PUB) into hs.p
   const int* hf = reinterpret_cast<const int*>(hs.p);
   const unsigned long long exported = hs.p[2], decided = hs.p[3], late_holes = hs.p[4];
   int64_t total = int64_t(hs.p[5]);

@@ -44,19 +44,30 @@ constexpr int WPB = 8;  // warps per block
 constexpr int THREADS = WPB * 32;
 constexpr uint32_t FCAP = 256;  // fresh-array capacity per warp (shared memory, x2 ping-pong)
 
+// n / d for n, d < 2^32 by one 64-bit high multiply: m = ceil(2^64 / d) makes the quotient exact
+// (the error n * (m - 2^64/d) / 2^64 < 2^-32 cannot carry past the fractional part (d-1)/d).
+struct FastDiv {
+  uint64_t m;
+  uint32_t d;
+  static FastDiv make(uint32_t d) { return FastDiv{d <= 1 ? 0ull : (~0ull / d) + 1, d}; }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return d <= 1 ? n : uint32_t(__umul64hi(uint64_t(n), m));
+  }
+};
+
 struct RP {
   Geom g;
+  FastDiv fx, fxy;  // by KX and by KX*KY: Khalimsky coordinates of a kidx
   int d;
   const uint64_t* cols;
   uint32_t ncols;
   const uint32_t* births;
   const uint8_t* tags;
-  uint32_t* owner;
+  uint64_t* owninfo;   // per (d+1)-cell: (pool offset << 24) | length of the column owning it as
+                       // pivot, NONE64 if unowned -- one load instead of owner -> offset, length
   uint64_t* pool;
   unsigned long long* pool_top;
   unsigned long long pool_cap;
-  unsigned long long* pool_off;
-  uint32_t* pool_len;
   uint64_t* work;      // per warp: 2 * mcap main-array entries
   uint32_t mcap;
   uint64_t* cand;      // per window position
@@ -73,11 +84,12 @@ struct RP {
                               // debug: [4] pool additions [5] pool lengths [7]/[8] cycles in
                               // pool/apparent additions [9] cycles in pivot + owner lookups
   int debug;
-  unsigned long long* colstat;  // debug: per column (additions, entries touched)
-  int prefetch;                 // warm next pivots' lookups (CR_K5_PREFETCH=1; measured no gain)
-  int lcache;                   // per-warp lookup cache (CR_K5_CACHE=1; measured no gain: the
-                                // rounds wait on the heaviest column's addition chain)
+  unsigned long long* rdbg;  // debug: per round [max phase-A cycles, max steps, active warps, t]
+  uint32_t rdbg_cap;
+  unsigned long long* colstat;  // debug: per column (additions, entries touched, cycles in
+                                // lookups, apparent adds, pool adds, flushes)
 };
+constexpr int OI_LEN_BITS = 24;  // owninfo: stored column length field
 
 __device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
   return __ldcg((const unsigned long long*)p);
@@ -87,27 +99,12 @@ __device__ __forceinline__ uint64_t ld64(const uint64_t* p) {
   return G ? ldcg64(p) : *p;
 }
 
-// Per-warp direct-mapped cache of pivot lookups (tag and owner of a (d+1)-cell), in shared
-// memory.  Owners change only in the commit phase, so the cache is cleared at every round start;
-// tags never change.  Filled by the coboundary enumeration (the cofacets of an apparent partner
-// are the likeliest next pivots) and by the pivot lookups themselves.
-constexpr int LC = 32;
-struct LookupCache {
-  uint32_t key[LC];
-  uint32_t val[LC];  // tag << 24 | owner (0xFFFFFF: none)
-};
-constexpr uint32_t LC_NOOWN = 0xFFFFFFu;
-__device__ __forceinline__ uint32_t lc_pack(uint8_t tag, uint32_t owner) {
-  return (uint32_t(tag) << 24) | (owner == NONE32 ? LC_NOOWN : (owner & LC_NOOWN));
-}
-
 // Finite cofacets of cell s, sorted ascending, written to dst (<= 6 entries).  Warp-collective.
-template <bool CACHE = false>
-__device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane,
-                              LookupCache* lc = nullptr) {
+__device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
   const Geom& g = P.g;
   const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  const uint32_t c[3] = {s % KX, (s / KX) % KY, s / (KX * KY)};
+  const uint32_t r = P.fx.div(s), z = P.fxy.div(s);
+  const uint32_t c[3] = {s - r * KX, r - z * KY, z};
   const uint32_t ext[3] = {KX, KY, uint32_t(g.KZ)};
   uint64_t key = NONE64;
   if (lane < 6) {
@@ -116,14 +113,6 @@ __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane,
       const int64_t stv = g.stride(a);
       const uint32_t t = uint32_t(int64_t(s) + (sg ? stv : -stv));
       const uint32_t tb = __ldg(P.births + t);
-      if (CACHE) {  // the cofacet's lookups ride along with its birth (independent loads)
-        const uint8_t tt = __ldg(P.tags + t);
-        const uint32_t to = __ldcg(P.owner + t);
-        if (tb != ABSENT_ORD) {
-          lc->key[t & (LC - 1)] = t;
-          lc->val[t & (LC - 1)] = lc_pack(tt, to);
-        }
-      }
       if (tb != ABSENT_ORD) key = make_key(tb, t);
     }
   }
@@ -181,6 +170,46 @@ __device__ uint32_t merge_symdiff(const uint64_t* A, uint32_t a, const uint64_t*
   }
   __syncwarp();
   return a + b - 2 * dups;
+}
+
+// C = A xor B for A in shared memory and a tiny B (nb <= SMALLB, shared memory), C distinct from
+// both.  Lane k < nb places B[k] by one binary search in A; every lane then holds all of B in
+// registers, so an A entry needs only register compares, and the A chunks are independent:
+//   kept A[i] goes to i + #{B < A[i]} - 2 #{common values < A[i]},
+//   kept B[k] goes to k + #{A < B[k]} - 2 #{common values < B[k]}.
+// Warp-collective; returns |C|.
+constexpr uint32_t SMALLB = 8;
+__device__ uint32_t merge_small(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t nb,
+                                uint64_t* C, int lane) {
+  uint64_t y = NONE64;
+  uint32_t la = 0;
+  bool ydup = false;
+  if (lane < int(nb)) {
+    y = B[lane];
+    la = lower_bound<false>(A, a, y);
+    ydup = la < a && A[la] == y;
+  }
+  const uint32_t bdup = __ballot_sync(0xFFFFFFFFu, ydup);
+  uint64_t bv[SMALLB];
+#pragma unroll
+  for (int k = 0; k < int(SMALLB); ++k) bv[k] = __shfl_sync(0xFFFFFFFFu, y, k);  // NONE64 past nb
+#pragma unroll 2
+  for (uint32_t i = lane; i < a; i += 32) {
+    const uint64_t x = A[i];
+    uint32_t lessB = 0, D = 0;
+    bool dup = false;
+#pragma unroll
+    for (int k = 0; k < int(SMALLB); ++k) {
+      const bool lt = bv[k] < x;
+      lessB += lt ? 1u : 0u;
+      D += (lt && (bdup >> k & 1)) ? 1u : 0u;
+      dup |= bv[k] == x;
+    }
+    if (!dup) C[i + lessB - 2 * D] = x;
+  }
+  if (lane < int(nb) && !ydup) C[lane + la - 2 * __popc(bdup & ((1u << lane) - 1))] = y;
+  __syncwarp();
+  return a + nb - 2 * __popc(bdup);
 }
 
 // C = A xor B with A in global memory and B in global (BG) or shared memory, for long inputs:
@@ -246,27 +275,88 @@ struct Col {
   uint64_t* F[2];  // shared fresh arrays
   uint32_t mb, nm, h;
   uint32_t fb, nf, f0;
-  uint64_t mhead;  // cached M[mb][h] (valid unless mstale)
+  uint64_t mwin;   // per lane: M[mb][wb + lane] (valid unless mstale), NONE64 past the end
+  uint32_t wb;     // window base
   bool mstale;
+  long long fcyc;  // debug: cycles spent in flushes
+  uint32_t cap;    // capacity of M[0] and M[1]
+  uint64_t* spare; // the second half of a grown pair, installed after the merge that grew it
   __device__ uint32_t len() const { return (nm - h) + (nf - f0); }
 };
 
 // pivot = min of (M[h:] xor F[f0:]), cancelling equal heads; NONE64 if the column is zero.
-// The head of M is cached in a register (mhead) and reloaded only when h moves or M changes.
-__device__ __forceinline__ uint64_t take_pivot(Col& c) {
+// Warp-collective.  The next 32 entries of M sit in a register window (one per lane), reloaded
+// with one coalesced load when h leaves it or M changes: the head of a long column is not a
+// dependent global load per cancellation.
+__device__ __forceinline__ uint64_t take_pivot(Col& c, int lane) {
   while (true) {
-    if (c.mstale) {
-      c.mhead = c.h < c.nm ? ldcg64(c.M[c.mb] + c.h) : NONE64;
+    if (c.mstale || c.h >= c.wb + 32) {
+      c.wb = c.h;
+      c.mwin = c.h + lane < c.nm ? ldcg64(c.M[c.mb] + c.h + lane) : NONE64;
       c.mstale = false;
     }
-    const uint64_t a = c.mhead;
+    const uint64_t a = __shfl_sync(0xFFFFFFFFu, c.mwin, c.h - c.wb);
     const uint64_t b = c.f0 < c.nf ? c.F[c.fb][c.f0] : NONE64;
     if (a != b) return a < b ? a : b;
     if (a == NONE64) return NONE64;
     ++c.h;
     ++c.f0;
-    c.mstale = true;
   }
+}
+
+// The apparent-partner coboundary, speculated.  A DOWN pivot t (a (d+1)-cell) is the upper cell
+// of an apparent pair (s', t) with s' = t + e_dir, a facet of t; the column then adds delta(s') =
+// {t} + the other cofacets of s'.  Before t's tag is known, lane L < 30 loads the birth of member
+// L % 5 of facet direction L / 5: member 0 is t + 2 e_dir (across the facet), members 1-4 are
+// s' -/+ e_b for the two other axes b (when b is even in t).  The tag, the owner record and these
+// births are independent loads, so an addition waits on one memory latency instead of a chain.
+struct Spec {
+  uint32_t cell;
+  uint32_t birth;  // ABSENT_ORD if the member does not exist
+};
+__device__ __forceinline__ Spec spec_issue(const RP& P, uint32_t t, int lane) {
+  const Geom& g = P.g;
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const uint32_t ty = P.fx.div(t), tz = P.fxy.div(t);
+  const uint32_t c[3] = {t - ty * KX, ty - tz * KY, tz};
+  const uint32_t ext[3] = {KX, KY, uint32_t(g.KZ)};
+  Spec r{0u, ABSENT_ORD};
+  if (lane < 30) {
+    const int f = lane / 5, m = lane % 5;
+    const int a = f >> 1;
+    const int sa = (f & 1) ? 1 : -1;
+    if (c[a] & 1) {  // the facet exists (odd axis of t)
+      int64_t cell = -1;
+      if (m == 0) {
+        const int64_t ca = int64_t(c[a]) + 2 * sa;
+        if (ca >= 0 && ca < int64_t(ext[a])) cell = int64_t(t) + 2 * sa * g.stride(a);
+      } else {
+        const int b = (a + 1 + ((m - 1) >> 1)) % 3;
+        const int sb = (m & 1) ? -1 : 1;  // m = 1, 3: -;  m = 2, 4: +
+        const int64_t cb = int64_t(c[b]) + sb;
+        if (!(c[b] & 1) && cb >= 0 && cb < int64_t(ext[b]))
+          cell = int64_t(t) + sa * g.stride(a) + sb * g.stride(b);
+      }
+      if (cell >= 0) {
+        r.cell = uint32_t(cell);
+        r.birth = __ldg(P.births + r.cell);
+      }
+    }
+  }
+  return r;
+}
+// delta(s') sorted ascending into dst (<= 6 entries) for the partner direction dir; warp-collective.
+__device__ __forceinline__ uint32_t spec_finish(const Spec& sp, int dir, uint64_t piv,
+                                                uint64_t* dst, int lane) {
+  uint64_t key = NONE64;
+  if (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD) key = make_key(sp.birth, sp.cell);
+  if (lane == 31) key = piv;
+  const unsigned vm = __ballot_sync(0xFFFFFFFFu, key != NONE64);
+  int rank = 0;
+  for (unsigned m = vm; m; m &= m - 1) rank += __shfl_sync(0xFFFFFFFFu, key, __ffs(m) - 1) < key;
+  if (key != NONE64) dst[rank] = key;
+  __syncwarp();
+  return __popc(vm);
 }
 
 // C = A xor F for a long A (global) and a short F (shared, b <= FCAP), C in global memory, using
@@ -395,20 +485,49 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
 __device__ int g_k5_dbg = 0;                      // CR_DEBUG_STATS: flush counters below
 __device__ unsigned long long g_k5_flush[4];      // flushes, cycles, entries of M, long merges
 
+// Make room for a merge of `need` entries into M[mb ^ 1]: a column that outgrows its warp's slot
+// moves to a larger pair carved from the pool (bump allocation; the few long columns of a launch
+// leave their old pairs behind).  False (err 2: the caller retries with a larger pool) if the
+// pool is exhausted.
+__device__ bool grow(Col& c, uint32_t need, const RP& P, int lane) {
+  if (need <= c.cap) return true;
+  uint64_t ncap = uint64_t(need) * 2;
+  if (ncap < uint64_t(c.cap) * 4) ncap = uint64_t(c.cap) * 4;
+  unsigned long long off = 0;
+  if (lane == 0) off = atomicAdd(P.pool_top, 2ull * ncap);
+  off = __shfl_sync(0xFFFFFFFFu, off, 0);
+  if (off + 2 * ncap > P.pool_cap || ncap > 0xFFFFFFFFull) {
+    if (lane == 0) atomicOr(P.err, 2);
+    return false;
+  }
+  c.M[c.mb ^ 1] = P.pool + off;  // the merge's destination
+  c.spare = P.pool + off + ncap;  // replaces the old M[mb] once the merge has read it
+  c.cap = uint32_t(ncap);
+  return true;
+}
+__device__ __forceinline__ void swap_main(Col& c) {
+  c.mb ^= 1;
+  if (c.spare) {
+    c.M[c.mb ^ 1] = c.spare;
+    c.spare = nullptr;
+  }
+}
+
 // M <- M[h:] xor F[f0:]   (returns false on capacity overflow)
-__device__ bool flush(Col& c, uint32_t mcap, int lane) {
+__device__ bool flush(Col& c, const RP& P, int lane) {
   const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
   if (nb == 0) return true;
-  if (na + nb > mcap) return false;
+  if (!grow(c, na + nb, P, lane)) return false;
   const long long t0 = g_k5_dbg ? clock64() : 0;
   const uint32_t n = merge_long_short(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
                                       c.M[c.mb ^ 1], c.F[c.fb ^ 1], lane);
   if (g_k5_dbg && lane == 0) {
     atomicAdd(g_k5_flush + 0, 1ull);
     atomicAdd(g_k5_flush + 1, (unsigned long long)(clock64() - t0));
+    c.fcyc += clock64() - t0;
     atomicAdd(g_k5_flush + 2, (unsigned long long)na);
   }
-  c.mb ^= 1;
+  swap_main(c);
   c.nm = n;
   c.h = 0;
   c.nf = c.f0 = 0;
@@ -416,9 +535,33 @@ __device__ bool flush(Col& c, uint32_t mcap, int lane) {
   return true;
 }
 
+constexpr uint32_t STAGE = 64;  // short global addends are staged in shared memory first
+
 // column += B (sorted; BG: B in global memory).  Returns false on capacity overflow.
 template <bool BG>
-__device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, uint32_t mcap, int lane) {
+__device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, int lane,
+                           uint64_t* stage) {
+  if (BG && nb <= STAGE && (c.nf - c.f0) + nb <= FCAP) {
+    // one coalesced load instead of a dependent global binary search per F entry
+    for (uint32_t i = lane; i < nb; i += 32) stage[i] = ldcg64(B + i);
+    __syncwarp();
+    const uint32_t n =
+        nb <= SMALLB
+            ? merge_small(c.F[c.fb] + c.f0, c.nf - c.f0, stage, nb, c.F[c.fb ^ 1], lane)
+            : merge_symdiff<false, false>(c.F[c.fb] + c.f0, c.nf - c.f0, stage, nb,
+                                          c.F[c.fb ^ 1], lane);
+    c.fb ^= 1;
+    c.nf = n;
+    c.f0 = 0;
+    return true;
+  }
+  if (!BG && nb <= SMALLB && (c.nf - c.f0) + nb <= FCAP) {
+    const uint32_t n = merge_small(c.F[c.fb] + c.f0, c.nf - c.f0, B, nb, c.F[c.fb ^ 1], lane);
+    c.fb ^= 1;
+    c.nf = n;
+    c.f0 = 0;
+    return true;
+  }
   if ((c.nf - c.f0) + nb <= FCAP) {
     const uint32_t n =
         merge_symdiff<false, BG>(c.F[c.fb] + c.f0, c.nf - c.f0, B, nb, c.F[c.fb ^ 1], lane);
@@ -427,7 +570,7 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, uint32_t mcap
     c.f0 = 0;
     return true;
   }
-  if (!flush(c, mcap, lane)) return false;
+  if (!flush(c, P, lane)) return false;
   if (nb <= FCAP) {  // F is empty now: B becomes F
     for (uint32_t i = lane; i < nb; i += 32) c.F[c.fb][i] = ld64<BG>(B + i);
     __syncwarp();
@@ -435,10 +578,10 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, uint32_t mcap
     c.f0 = 0;
     return true;
   }
-  if ((c.nm - c.h) + nb > mcap) return false;
+  if (!grow(c, (c.nm - c.h) + nb, P, lane)) return false;
   const uint32_t n = merge_chunked<BG>(c.M[c.mb] + c.h, c.nm - c.h, B, nb, c.M[c.mb ^ 1],
                                        c.F[0], c.F[1], lane);
-  c.mb ^= 1;
+  swap_main(c);
   c.nm = n;
   c.h = 0;
   c.mstale = true;
@@ -449,8 +592,14 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s_F[WPB][2][FCAP];
   __shared__ uint64_t s_small[WPB][8];
-  __shared__ LookupCache s_lc[WPB];
-  __shared__ uint64_t s_pref[4 * THREADS];
+  // phase A stages short addends, phase C scans chunk minima: grid syncs separate them
+  __shared__ union {
+    uint64_t stage[WPB][STAGE];
+    uint64_t pref[4 * THREADS];
+  } s_u;
+  static_assert(sizeof(uint64_t) * WPB * STAGE <= sizeof(uint64_t) * 4 * THREADS, "alias");
+  auto& s_stage = s_u.stage;
+  auto& s_pref = s_u.pref;
   __shared__ typename SScan::TempStorage s_scan;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -459,18 +608,14 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
   const uint32_t nblocks = gridDim.x;
 
   Col c;
-  c.M[0] = P.work + uint64_t(w) * 2 * P.mcap;
-  c.M[1] = c.M[0] + P.mcap;
+  uint64_t* const slot = P.work + uint64_t(w) * 2 * P.mcap;
   c.F[0] = s_F[wib][0];
   c.F[1] = s_F[wib][1];
   uint32_t j = w;
   bool started = false, fin = false;
   uint32_t lo = 0;
 
-  LookupCache* lc = &s_lc[wib];
   for (uint32_t round = 0;; ++round) {
-    for (int i = lane; i < LC; i += 32) lc->key[i] = NONE32;  // owners may have changed
-    __syncwarp();
     // ---------------- phase A: advance my column
     if (fin && j < lo) {
       j += W;
@@ -479,71 +624,49 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
     }
     uint64_t cval = NONE64;
     bool ready = false;
+    const long long pa0 = P.rdbg ? clock64() : 0;
+    int dbg_steps = -1;
     if (j < P.ncols && !fin) {
       if (!started) {
         started = true;
         c.mb = c.fb = 0;
         c.h = c.f0 = c.nm = 0;
+        c.M[0] = slot;  // a column grown into the pool last time starts over in the slot
+        c.M[1] = slot + P.mcap;
+        c.cap = P.mcap;
+        c.spare = nullptr;
         c.mstale = true;
-        c.nf = coboundary<false>(P, key_kidx(P.cols[j]), c.F[0], lane);
+        c.nf = coboundary(P, key_kidx(P.cols[j]), c.F[0], lane);
       }
       int steps = 0;
-      unsigned long long adds = 0, addlen = 0;
+      unsigned long long adds = 0, addlen = 0, cl = 0, ca = 0, cp = 0;
+      c.fcyc = 0;
       bool ok = true;
       while (true) {
         const long long tl0 = P.debug ? clock64() : 0;
-        const uint64_t piv = take_pivot(c);
+        const uint64_t piv = take_pivot(c, lane);
         if (piv == NONE64) break;
         const uint32_t pk = key_kidx(piv);
-        if (P.prefetch && lane >= 1 && lane <= 12) {
-          // warm the lookups of the column's next entries (the likely next pivots): their tag and
-          // owner lines, so that the dependent chain of the next additions hits L2
-          uint64_t e = NONE64;
-          if (lane <= 6) {
-            const uint32_t i = c.h + lane;
-            if (i < c.nm) e = ldcg64(c.M[c.mb] + i);
-          } else {
-            const uint32_t i = c.f0 + uint32_t(lane - 6);
-            if (i < c.nf) e = c.F[c.fb][i];
-          }
-          if (e != NONE64) {
-            const uint32_t ek = key_kidx(e);
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.tags + ek));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.owner + ek));
-          }
-        }
-        uint8_t t;
-        uint32_t ocached = 0;
-        bool hit = false;
-        if (P.lcache) {
-          const uint32_t ck = lc->key[pk & (LC - 1)];
-          if (ck == pk) {
-            const uint32_t v = lc->val[pk & (LC - 1)];
-            t = uint8_t(v >> 24);
-            ocached = (v & LC_NOOWN) == LC_NOOWN ? NONE32 : (v & LC_NOOWN);
-            hit = true;
-          }
-        }
-        if (!hit) t = __ldg(P.tags + pk);
+        // independent loads: the speculated partner coboundary, the tag, the owner record
+        const Spec sp = spec_issue(P, pk, lane);
+        const uint8_t t = __ldg(P.tags + pk);
+        const uint64_t oi = ldcg64(P.owninfo + pk);
         const uint64_t* add;
         uint32_t alen;
         bool glob;
         if (tag_kind(t) == KIND_DOWN) {
           // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
-          const uint32_t sp = uint32_t(int64_t(pk) + dir_offset(P.g, tag_dir(t)));
-          alen = P.lcache ? coboundary<true>(P, sp, s_small[wib], lane, lc)
-                          : coboundary<false>(P, sp, s_small[wib], lane);
+          alen = spec_finish(sp, tag_dir(t), piv, s_small[wib], lane);
           add = s_small[wib];
           glob = false;
         } else {
-          const uint32_t o = hit ? ocached : __ldcg(P.owner + pk);
-          if (o == NONE32) {
+          if (oi == NONE64) {
             ready = true;
             cval = piv;
             break;
           }
-          add = P.pool + __ldcg(P.pool_off + o);
-          alen = __ldcg(P.pool_len + o);
+          add = P.pool + (oi >> OI_LEN_BITS);
+          alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1));
           glob = true;
         }
         if (steps >= P.max_steps) {
@@ -551,34 +674,39 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
           break;
         }
         addlen += c.len() + alen;
-        const long long t0 = clock64();
+        const long long t0 = P.debug ? clock64() : 0;
         if (P.debug && lane == 0) atomicAdd(P.stats + 9, (unsigned long long)(t0 - tl0));
-        ok = glob ? add_column<true>(c, add, alen, P.mcap, lane)
-                  : add_column<false>(c, add, alen, P.mcap, lane);
+        cl += t0 - tl0;
+        ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib])
+                  : add_column<false>(c, add, alen, P, lane, s_stage[wib]);
         if (P.debug && lane == 0) {
           const unsigned long long dt = (unsigned long long)(clock64() - t0);
           if (glob) {
             atomicAdd(P.stats + 4, 1ull);
             atomicAdd(P.stats + 5, (unsigned long long)alen);
             atomicAdd(P.stats + 7, dt);
+            cp += dt;
           } else {
             atomicAdd(P.stats + 8, dt);
+            ca += dt;
           }
         }
-        if (!ok) {
-          if (lane == 0) atomicOr(P.err, 1);
-          break;
-        }
+        if (!ok) break;  // pool exhausted (err 2 set): the launch is retried
         ++steps;
         ++adds;
       }
+      dbg_steps = steps;
       if (lane == 0 && adds) {
         atomicAdd(P.stats + 1, adds);
         atomicAdd(P.stats + 2, addlen);
         atomicMax(P.stats + 3, (unsigned long long)c.len());
         if (P.colstat) {
-          P.colstat[2 * j] += adds;
-          P.colstat[2 * j + 1] += addlen;
+          P.colstat[6 * j] += adds;
+          P.colstat[6 * j + 1] += addlen;
+          P.colstat[6 * j + 2] += cl;
+          P.colstat[6 * j + 3] += ca;
+          P.colstat[6 * j + 4] += cp;
+          P.colstat[6 * j + 5] += (unsigned long long)c.fcyc;
         }
       }
       if (ok && !ready && cval == NONE64) {  // zero column: essential (exact given clearing)
@@ -588,6 +716,17 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
           P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | NONE32;
         }
       }
+    }
+    if (P.rdbg && lane == 0 && round < P.rdbg_cap && dbg_steps >= 0) {
+      unsigned long long* R = P.rdbg + 4ull * round;
+      atomicMax(R + 0, (unsigned long long)(clock64() - pa0));
+      atomicMax(R + 1, (unsigned long long)dbg_steps);
+      atomicAdd(R + 2, 1ull);
+    }
+    if (P.rdbg && blockIdx.x == 0 && threadIdx.x == 0 && round < P.rdbg_cap) {
+      unsigned long long tnow;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+      P.rdbg[4ull * round + 3] = tnow;
     }
     // publish at my window position (every position is owned by exactly one warp), with the
     // segment (image of a batch) of the column: columns of different images never interact, so
@@ -657,10 +796,9 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
                                                   c.nf - c.f0, P.pool + off, c.F[c.fb ^ 1],
                                                   nullptr, lane);
           if (lane == 0) {
-            P.pool_off[j] = off;
-            P.pool_len[j] = n;
+            if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
             __threadfence();
-            P.owner[key_kidx(cval)] = j;
+            P.owninfo[key_kidx(cval)] = (uint64_t(off) << OI_LEN_BITS) | n;
             const unsigned long long r = atomicAdd(P.nrec, 1ull);
             P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | key_kidx(cval);
           }
@@ -774,9 +912,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     if (blocks > int64_t(THREADS) * 4) blocks = THREADS * 4;
     const uint32_t W = uint32_t(blocks * WPB);
 
-    uint32_t* owner = ws.alloc<uint32_t>(g.ncells);
-    unsigned long long* pool_off = ws.alloc<unsigned long long>(ncols);
-    uint32_t* pool_len = ws.alloc<uint32_t>(ncols);
+    uint64_t* owninfo = ws.alloc<uint64_t>(g.ncells);
     uint64_t* cand = ws.alloc<uint64_t>(W + blocks);
     uint64_t* chunkmin = ws.alloc<uint64_t>(blocks);
     uint32_t* chunkflag = ws.alloc<uint32_t>(blocks);
@@ -787,31 +923,38 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     unsigned long long* pool_top = ctr + 5;
     unsigned long long* stats = ctr + 6;  // [6] rounds [7] additions [8] lengths [9] max length
 
-    uint32_t mcap = 4096;
-    unsigned long long pool_cap = std::max<unsigned long long>(8ull * ncols + 4096, 1ull << 20);
+    // main-array slot per warp; longer columns grow into the pool.  The pool (reduced columns +
+    // grown main arrays) is sized so that exhausting it -- which reruns the whole launch with 4x --
+    // does not happen on realistic inputs: 16 entries per column + 32 Mi entries (256 MB)
+    const uint32_t mcap = std::getenv("CR_K5_MCAP")
+                              ? uint32_t(std::atoi(std::getenv("CR_K5_MCAP")))
+                              : 4096u;
+    unsigned long long pool_cap = 16ull * ncols + (1ull << 25);
     uint64_t* work = nullptr;
     uint64_t* pool = nullptr;
     unsigned long long* P_colstat = nullptr;
+    unsigned long long* P_rdbg = nullptr;
+    uint32_t P_rdbg_cap = 0;
     for (int attempt = 0;; ++attempt) {
       if (!work) work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
-      CR_CUDA(cudaMemsetAsync(owner, 0xFF, g.ncells * sizeof(uint32_t), s));
+      CR_CUDA(cudaMemsetAsync(owninfo, 0xFF, g.ncells * sizeof(uint64_t), s));
       CR_CUDA(cudaMemsetAsync(lo_buf, 0xFF, 2 * sizeof(unsigned), s));
       CR_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
       CR_CUDA(cudaMemsetAsync(nrec, 0, 6 * sizeof(unsigned long long), s));
       RP P;
       P.g = g;
+      P.fx = FastDiv::make(uint32_t(g.KX));
+      P.fxy = FastDiv::make(uint32_t(g.KX * g.KY));
       P.d = d;
       P.cols = cols;
       P.ncols = ncols;
       P.births = S.births;
       P.tags = S.tags;
-      P.owner = owner;
+      P.owninfo = owninfo;
       P.pool = pool;
       P.pool_top = pool_top;
       P.pool_cap = pool_cap;
-      P.pool_off = pool_off;
-      P.pool_len = pool_len;
       P.work = work;
       P.mcap = mcap;
       P.cand = cand;
@@ -833,25 +976,31 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
         CR_CUDA(cudaMemcpyToSymbolAsync(g_k5_flush, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
       }
       P.colstat = nullptr;
-      P.prefetch = std::getenv("CR_K5_PREFETCH") != nullptr;
-      P.lcache = std::getenv("CR_K5_CACHE") != nullptr;
+      P.rdbg = nullptr;
+      P.rdbg_cap = 0;
       if (P.debug) {
-        if (!P_colstat) P_colstat = ws.alloc<unsigned long long>(2 * int64_t(ncols));
-        P.colstat = P_colstat;
-        CR_CUDA(cudaMemsetAsync(P.colstat, 0, 2 * sizeof(unsigned long long) * ncols, s));
+        P.rdbg_cap = 16384;
+        P.rdbg = ws.alloc<unsigned long long>(4 * int64_t(P.rdbg_cap));
+        CR_CUDA(cudaMemsetAsync(P.rdbg, 0, 32 * sizeof(unsigned long long) * P.rdbg_cap / 8, s));
       }
+      if (P.debug) {
+        if (!P_colstat) P_colstat = ws.alloc<unsigned long long>(6 * int64_t(ncols));
+        P.colstat = P_colstat;
+        CR_CUDA(cudaMemsetAsync(P.colstat, 0, 6 * sizeof(unsigned long long) * ncols, s));
+      }
+      P_rdbg = P.rdbg;
+      P_rdbg_cap = P.rdbg_cap;
       void* args[] = {&P};
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, 0, s));
       ++g_launch_count;
       const int e = read_scalar(err, s, hs);
+      if (std::getenv("CR_DEBUG_STATS"))
+        fprintf(stderr, "[cr] dim %d attempt %d: err %d (mcap %u, pool %llu)\n", d, attempt, e,
+                mcap, pool_cap);
       if (e == 0) break;
+      if (e & 4) throw Error{CR_EINTERNAL, "reduced column longer than 2^24 entries"};
       if (attempt > 12) throw Error{CR_ENOMEM, "reduction buffers exhausted"};
-      if (e & 1) {
-        ws.release(work);
-        work = nullptr;
-        mcap *= 4;
-      }
       if (e & 2) {
         ws.release(pool);
         pool = nullptr;
@@ -866,13 +1015,13 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     st.addlen[d] = int64_t(hs.p[8]);
     st.maxlen[d] = int64_t(hs.p[9]);
     if (std::getenv("CR_DEBUG_STATS")) {
-      std::vector<unsigned long long> cs(2 * size_t(ncols));
+      std::vector<unsigned long long> cs(6 * size_t(ncols));
       CR_CUDA(cudaMemcpy(cs.data(), P_colstat, cs.size() * 8, cudaMemcpyDeviceToHost));
       std::vector<std::pair<unsigned long long, uint32_t>> byent(ncols);
       unsigned long long tot = 0;
       for (uint32_t j = 0; j < ncols; ++j) {
-        byent[j] = {cs[2 * j + 1], j};
-        tot += cs[2 * j + 1];
+        byent[j] = {cs[6 * j + 1], j};
+        tot += cs[6 * j + 1];
       }
       std::sort(byent.rbegin(), byent.rend());
       unsigned long long acc = 0;
@@ -887,10 +1036,34 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       unsigned long long fl[4];
       CR_CUDA(cudaMemcpyFromSymbol(fl, g_k5_flush, sizeof(fl)));
       fprintf(stderr, " | flushes %llu cycles %llu M-entries %llu", fl[0], fl[1], fl[2]);
+      {
+        const uint32_t nr = uint32_t(std::min<unsigned long long>(hs.p[6], P_rdbg_cap));
+        std::vector<unsigned long long> R(4 * size_t(nr));
+        CR_CUDA(cudaMemcpy(R.data(), P_rdbg, R.size() * 8, cudaMemcpyDeviceToHost));
+        double cyc = 0, steps_full = 0;
+        unsigned long long hist[5] = {0, 0, 0, 0, 0};
+        for (uint32_t r = 0; r < nr; ++r) {
+          cyc += double(R[4 * r]);
+          const unsigned long long ms = R[4 * r + 1];
+          hist[ms >= 256 ? 4 : ms >= 64 ? 3 : ms >= 16 ? 2 : ms >= 1 ? 1 : 0]++;
+          if (ms >= 256) steps_full += 1;
+        }
+        const double wall = nr > 1 ? double(R[4 * (nr - 1) + 3] - R[3]) / 1e6 : 0.0;
+        fprintf(stderr, "[cr] dim %d rounds %u: sum of max phase-A %.1f ms (at 1.9 GHz), wall %.1f ms;"
+                " max-steps hist 0:%llu 1-15:%llu 16-63:%llu 64-255:%llu 256:%llu\n",
+                d, nr, cyc / 1.9e6, wall, hist[0], hist[1], hist[2], hist[3], hist[4]);
+        for (uint32_t r = 0; r < nr; r += nr / 12 + 1)
+          fprintf(stderr, "   round %u: maxA %.1f us steps %llu active %llu\n", r,
+                  R[4 * r] / 1.9e3, R[4 * r + 1], R[4 * r + 2]);
+      }
       fprintf(stderr, "\n[cr] top columns (pos, adds, entries):");
-      for (int q = 0; q < 8 && q < int(ncols); ++q)
-        fprintf(stderr, " (%u,%llu,%llu)", byent[q].second, cs[2 * byent[q].second],
-                byent[q].first);
+      for (int q = 0; q < 8 && q < int(ncols); ++q) {
+        const uint32_t jj = byent[q].second;
+        const double a = double(cs[6 * jj] ? cs[6 * jj] : 1);
+        fprintf(stderr, "\n   col %u adds %llu entries %llu | per add cycles: lookup %.0f app %.0f "
+                "pool %.0f (flush %.0f)", jj, cs[6 * jj], byent[q].first, cs[6 * jj + 2] / a,
+                cs[6 * jj + 3] / a, cs[6 * jj + 4] / a, cs[6 * jj + 5] / a);
+      }
       fprintf(stderr, "\n");
       fprintf(stderr,
               "[cr] dim %d: cols %u rounds %llu adds %llu pool_adds %llu pool_len %llu "
@@ -899,9 +1072,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     }
     ws.release(work);
     ws.release(pool);
-    ws.release(owner);
-    ws.release(pool_off);
-    ws.release(pool_len);
+    ws.release(owninfo);
   }
   if (S.R.n[d] > 0) {
     k_mark_cleared<<<grid_for(S.R.n[d], B), B, 0, s>>>(S.R.rec[d], S.R.n[d], S.tags);

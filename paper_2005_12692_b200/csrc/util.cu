@@ -12,6 +12,7 @@ const char* last_error_text() { return g_err_text.c_str(); }
 namespace {
 struct Prof {
   bool on = false;
+  uint64_t gen = 0, ended = 0;  // calls begun / the last call whose events are complete
   std::vector<cudaEvent_t> pool;
   int used = 0;
   std::vector<const char*> names;
@@ -36,6 +37,7 @@ void set_profiling(bool on) { g_prof.on = on; }
 
 void prof_begin(cudaStream_t s) {
   g_launch_count = 0;
+  ++g_prof.gen;
   g_prof.used = 0;
   g_prof.names.clear();
   if (!g_prof.on) return;
@@ -55,7 +57,14 @@ void prof_mark(cudaStream_t s, const char* stage) {
 void prof_end(cr_stats& st) {
   st.launches = g_launch_count;
   st.nstages = 0;
-  if (!g_prof.on) return;
+  g_prof.ended = g_prof.gen;  // stage times are read lazily (prof_fill), outside the call
+}
+
+uint64_t prof_gen() { return g_prof.gen; }
+
+void prof_fill(cr_stats& st) {
+  if (!g_prof.on || g_prof.ended != g_prof.gen) return;
+  st.nstages = 0;
   int n = int(g_prof.names.size());
   for (int i = 1; i < n && st.nstages < 16; ++i) {
     float ms = 0.f;
