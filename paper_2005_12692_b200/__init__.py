@@ -90,8 +90,11 @@ class CrError(RuntimeError):
         super().__init__(f"cr status {status}: {_lib.cr_status_string(status).decode()}")
 
 
+_SHAPE_T = [ctypes.c_int64 * k for k in range(4)]
+
+
 def _shape(shape):
-    return (ctypes.c_int64 * len(shape))(*[int(s) for s in shape])
+    return _SHAPE_T[len(shape)](*shape) if len(shape) < 4 else (ctypes.c_int64 * len(shape))(*shape)
 
 
 def _check(st):
@@ -160,6 +163,10 @@ def _float_dtype(arr):
 
 
 def _stream_ptr(torch, device):
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # ~10x cheaper than current_stream
+    if raw is not None:
+        return ctypes.c_void_p(raw(device.index if device.index is not None else
+                                   torch.cuda.current_device()))
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
