@@ -281,10 +281,18 @@ struct Col {
   long long fcyc;  // debug: cycles spent in flushes
   uint32_t cap;    // capacity of M[0] and M[1]
   uint64_t* spare; // the second half of a grown pair, installed after the merge that grew it
-  __device__ uint32_t len() const { return (nm - h) + (nf - f0); }
+  uint64_t rv;     // per lane: entry `lane` of the register list R (NONE64 at and past nr)
+  uint32_t nr, r0; // R holds positions [r0, nr) (consumed from the front)
+  __device__ uint32_t len() const { return (nm - h) + (nf - f0) + (nr - r0); }
 };
 
-// pivot = min of (M[h:] xor F[f0:]), cancelling equal heads; NONE64 if the column is zero.
+// The working column is M[h:] xor F[f0:] xor R[r0:nr]: three sorted tiers -- a long main array in
+// global memory, a fresh array in shared memory, and a register list of <= 32 entries (one per
+// lane) that takes the small addends (apparent coboundaries, short stored columns) at a cost of a
+// few shuffles instead of rewriting F.  Equal values in different tiers cancel lazily, when they
+// reach the heads.
+//
+// pivot = min of the three heads, cancelling equal pairs; NONE64 if the column is zero.
 // Warp-collective.  The next 32 entries of M sit in a register window (one per lane), reloaded
 // with one coalesced load when h leaves it or M changes: the head of a long column is not a
 // dependent global load per cancellation.
@@ -297,11 +305,67 @@ __device__ __forceinline__ uint64_t take_pivot(Col& c, int lane) {
     }
     const uint64_t a = __shfl_sync(0xFFFFFFFFu, c.mwin, c.h - c.wb);
     const uint64_t b = c.f0 < c.nf ? c.F[c.fb][c.f0] : NONE64;
-    if (a != b) return a < b ? a : b;
-    if (a == NONE64) return NONE64;
-    ++c.h;
-    ++c.f0;
+    const uint64_t rr = __shfl_sync(0xFFFFFFFFu, c.rv, c.r0 & 31);
+    const uint64_t r = c.r0 < c.nr ? rr : NONE64;
+    if (a == b && a != NONE64) {
+      ++c.h;
+      ++c.f0;
+    } else if (a == r && a != NONE64) {
+      ++c.h;
+      ++c.r0;
+    } else if (b == r && b != NONE64) {
+      ++c.f0;
+      ++c.r0;
+    } else {
+      const uint64_t m = a < b ? a : b;
+      return m < r ? m : r;
+    }
   }
+}
+
+// R <- R[r0:nr] xor B for a sorted B of nb <= SMALLB entries in shared memory, with
+// (nr - r0) + nb <= 32.  Lane k < nb places B[k] by a shuffle binary search over R; every lane
+// holds all of B in registers to place its own R entry; the new list goes through `scratch`
+// (>= 40 entries).  Warp-collective.
+__device__ __forceinline__ void r_insert(Col& c, const uint64_t* B, uint32_t nb, uint64_t* scratch,
+                                         int lane) {
+  const uint32_t live = c.nr - c.r0;
+  const uint64_t y = lane < int(nb) ? B[lane] : NONE64;
+  uint32_t lo = c.r0, hi = c.nr;
+#pragma unroll
+  for (int it = 0; it < 6; ++it) {  // positions [r0, nr] <= 33 values: 6 halvings
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint64_t v = __shfl_sync(0xFFFFFFFFu, c.rv, mid & 31);
+    if (lo < hi) {
+      if (v < y) lo = mid + 1;
+      else hi = mid;
+    }
+  }
+  const uint64_t at = __shfl_sync(0xFFFFFFFFu, c.rv, lo & 31);
+  const bool ydup = lane < int(nb) && lo < c.nr && at == y;
+  const uint32_t bdup = __ballot_sync(0xFFFFFFFFu, ydup);
+  uint64_t bv[SMALLB];
+#pragma unroll
+  for (int k = 0; k < int(SMALLB); ++k) bv[k] = __shfl_sync(0xFFFFFFFFu, y, k);
+  const uint64_t x = c.rv;
+  uint32_t lessB = 0, D = 0;
+  bool dup = false;
+#pragma unroll
+  for (int k = 0; k < int(SMALLB); ++k) {
+    const bool lt = bv[k] < x;
+    lessB += lt ? 1u : 0u;
+    D += (lt && (bdup >> k & 1)) ? 1u : 0u;
+    dup |= bv[k] == x;
+  }
+  if (uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr && !dup)
+    scratch[(lane - c.r0) + lessB - 2 * D] = x;
+  if (lane < int(nb) && !ydup) scratch[lane + (lo - c.r0) - 2 * __popc(bdup & ((1u << lane) - 1))] = y;
+  __syncwarp();
+  const uint32_t n = live + nb - 2 * __popc(bdup);
+  c.rv = uint32_t(lane) < n ? scratch[lane] : NONE64;
+  c.nr = n;
+  c.r0 = 0;
+  __syncwarp();
 }
 
 // The apparent-partner coboundary, speculated.  A DOWN pivot t (a (d+1)-cell) is the upper cell
@@ -314,34 +378,48 @@ struct Spec {
   uint32_t cell;
   uint32_t birth;  // ABSENT_ORD if the member does not exist
 };
-__device__ __forceinline__ Spec spec_issue(const RP& P, uint32_t t, int lane) {
-  const Geom& g = P.g;
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+// The lane's fixed role in spec_issue (depends only on the lane and the grid): member m of facet
+// direction f.  The member exists iff t's axis a is odd, the checked axis `chk` stays inside the
+// grid after moving by `dchk`, and (members 1-4) axis b is even in t.
+struct SpecLane {
+  int a, chk, dchk;
+  bool need_b_even;
+  uint32_t off;  // cell - t (two's complement)
+  bool active;
+};
+__device__ __forceinline__ SpecLane spec_lane(const Geom& g, int lane) {
+  SpecLane L{0, 0, 0, false, 0u, false};
+  if (lane >= 30) return L;
+  const int f = lane / 5, m = lane % 5;
+  L.a = f >> 1;
+  const int sa = (f & 1) ? 1 : -1;
+  L.active = true;
+  if (m == 0) {
+    L.chk = L.a;
+    L.dchk = 2 * sa;
+    L.off = uint32_t(int64_t(2 * sa) * g.stride(L.a));
+  } else {
+    const int b = (L.a + 1 + ((m - 1) >> 1)) % 3;
+    const int sb = (m & 1) ? -1 : 1;  // m = 1, 3: -;  m = 2, 4: +
+    L.chk = b;
+    L.dchk = sb;
+    L.need_b_even = true;
+    L.off = uint32_t(int64_t(sa) * g.stride(L.a) + int64_t(sb) * g.stride(b));
+  }
+  return L;
+}
+__device__ __forceinline__ Spec spec_issue(const RP& P, const SpecLane& L, uint32_t t) {
+  const uint32_t KX = uint32_t(P.g.KX), KY = uint32_t(P.g.KY);
   const uint32_t ty = P.fx.div(t), tz = P.fxy.div(t);
-  const uint32_t c[3] = {t - ty * KX, ty - tz * KY, tz};
-  const uint32_t ext[3] = {KX, KY, uint32_t(g.KZ)};
+  const uint32_t cx = t - ty * KX, cy = ty - tz * KY, cz = tz;
+  const uint32_t ca = L.a == 0 ? cx : (L.a == 1 ? cy : cz);
+  const uint32_t cc = L.chk == 0 ? cx : (L.chk == 1 ? cy : cz);
+  const uint32_t ec = L.chk == 0 ? KX : (L.chk == 1 ? KY : uint32_t(P.g.KZ));
+  const uint32_t moved = cc + uint32_t(L.dchk);  // wraps below 0 to a huge value
   Spec r{0u, ABSENT_ORD};
-  if (lane < 30) {
-    const int f = lane / 5, m = lane % 5;
-    const int a = f >> 1;
-    const int sa = (f & 1) ? 1 : -1;
-    if (c[a] & 1) {  // the facet exists (odd axis of t)
-      int64_t cell = -1;
-      if (m == 0) {
-        const int64_t ca = int64_t(c[a]) + 2 * sa;
-        if (ca >= 0 && ca < int64_t(ext[a])) cell = int64_t(t) + 2 * sa * g.stride(a);
-      } else {
-        const int b = (a + 1 + ((m - 1) >> 1)) % 3;
-        const int sb = (m & 1) ? -1 : 1;  // m = 1, 3: -;  m = 2, 4: +
-        const int64_t cb = int64_t(c[b]) + sb;
-        if (!(c[b] & 1) && cb >= 0 && cb < int64_t(ext[b]))
-          cell = int64_t(t) + sa * g.stride(a) + sb * g.stride(b);
-      }
-      if (cell >= 0) {
-        r.cell = uint32_t(cell);
-        r.birth = __ldg(P.births + r.cell);
-      }
-    }
+  if (L.active && (ca & 1) && moved < ec && !(L.need_b_even && (cc & 1))) {
+    r.cell = t + L.off;
+    r.birth = __ldg(P.births + r.cell);
   }
   return r;
 }
@@ -371,7 +449,7 @@ __device__ __forceinline__ uint32_t spec_finish(const Spec& sp, int dir, uint64_
 __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a, const uint64_t* F,
                                      uint32_t b, uint64_t* __restrict__ C, uint64_t* X, int lane) {
   constexpr int R = FCAP / 32;  // F entries per lane (t = lane + 32 r)
-  constexpr int G = 4;          // searches run interleaved per group
+  constexpr int G = R;          // all of a lane's searches run interleaved
   constexpr uint32_t NS = FCAP / 2;
   const unsigned lt = (1u << lane) - 1;
   uint32_t* XP = reinterpret_cast<uint32_t*>(X + NS);  // P[t]            (upper half of X)
@@ -452,12 +530,21 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
     }
     return l;
   };
+  // windows of 256, software-pipelined: the next window's loads are in flight while this one is
+  // placed
+  uint64_t nv[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t i = lane + 32 * k;
+    nv[k] = i < a ? ldcg64(A + i) : 0ull;
+  }
   for (uint32_t w0 = 0; w0 < a; w0 += 256) {
     uint64_t v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint32_t i = w0 + lane + 32 * k;
-      v[k] = i < a ? ldcg64(A + i) : 0ull;
+      v[k] = nv[k];
+      const uint32_t i = w0 + 256 + lane + 32 * k;
+      nv[k] = i < a ? ldcg64(A + i) : 0ull;
     }
     const uint32_t tl = lower_p(w0), th = lower_p(w0 + 256);
     const uint32_t cl = tl < b ? XC[tl] & 0x7FFFFFFFu : ((totD << 16) | totI);
@@ -537,10 +624,43 @@ __device__ bool flush(Col& c, const RP& P, int lane) {
 
 constexpr uint32_t STAGE = 64;  // short global addends are staged in shared memory first
 
+// F <- F xor R, R emptied (flushing F into M first if it cannot take R).  Warp-collective.
+__device__ bool spill_r(Col& c, const RP& P, uint64_t* scratch, int lane) {
+  const uint32_t live = c.nr - c.r0;
+  if (live > 0) {
+    if ((c.nf - c.f0) + live > FCAP && !flush(c, P, lane)) return false;
+    if (uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr) scratch[lane - c.r0] = c.rv;
+    __syncwarp();
+    if (c.nf == c.f0) {
+      if (uint32_t(lane) < live) c.F[c.fb][lane] = scratch[lane];
+      c.nf = live;
+    } else {
+      c.nf = merge_symdiff<false, false>(c.F[c.fb] + c.f0, c.nf - c.f0, scratch, live,
+                                         c.F[c.fb ^ 1], lane);
+      c.fb ^= 1;
+    }
+    c.f0 = 0;
+    __syncwarp();
+  }
+  c.rv = NONE64;
+  c.nr = c.r0 = 0;
+  return true;
+}
+
 // column += B (sorted; BG: B in global memory).  Returns false on capacity overflow.
 template <bool BG>
 __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, int lane,
-                           uint64_t* stage) {
+                           uint64_t* stage, uint64_t* small) {
+  if (nb <= SMALLB) {  // into the register list
+    if (BG) {
+      if (uint32_t(lane) < nb) small[lane] = ldcg64(B + lane);
+      __syncwarp();
+      B = small;
+    }
+    if ((c.nr - c.r0) + nb > 32 && !spill_r(c, P, stage, lane)) return false;
+    r_insert(c, B, nb, stage, lane);
+    return true;
+  }
   if (BG && nb <= STAGE && (c.nf - c.f0) + nb <= FCAP) {
     // one coalesced load instead of a dependent global binary search per F entry
     for (uint32_t i = lane; i < nb; i += 32) stage[i] = ldcg64(B + i);
@@ -609,6 +729,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
 
   Col c;
   uint64_t* const slot = P.work + uint64_t(w) * 2 * P.mcap;
+  const SpecLane sl = spec_lane(P.g, lane);
   c.F[0] = s_F[wib][0];
   c.F[1] = s_F[wib][1];
   uint32_t j = w;
@@ -635,6 +756,8 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         c.M[1] = slot + P.mcap;
         c.cap = P.mcap;
         c.spare = nullptr;
+        c.rv = NONE64;
+        c.nr = c.r0 = 0;
         c.mstale = true;
         c.nf = coboundary(P, key_kidx(P.cols[j]), c.F[0], lane);
       }
@@ -648,7 +771,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         if (piv == NONE64) break;
         const uint32_t pk = key_kidx(piv);
         // independent loads: the speculated partner coboundary, the tag, the owner record
-        const Spec sp = spec_issue(P, pk, lane);
+        const Spec sp = spec_issue(P, sl, pk);
         const uint8_t t = __ldg(P.tags + pk);
         const uint64_t oi = ldcg64(P.owninfo + pk);
         const uint64_t* add;
@@ -661,7 +784,10 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
           glob = false;
         } else {
           if (oi == NONE64) {
-            ready = true;
+            // ready to commit: fold R into F now (phase C's commit reads M and F, and its shared
+            // scratch is busy there)
+            ok = spill_r(c, P, s_stage[wib], lane);
+            ready = ok;
             cval = piv;
             break;
           }
@@ -677,8 +803,8 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         const long long t0 = P.debug ? clock64() : 0;
         if (P.debug && lane == 0) atomicAdd(P.stats + 9, (unsigned long long)(t0 - tl0));
         cl += t0 - tl0;
-        ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib])
-                  : add_column<false>(c, add, alen, P, lane, s_stage[wib]);
+        ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
+                  : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
         if (P.debug && lane == 0) {
           const unsigned long long dt = (unsigned long long)(clock64() - t0);
           if (glob) {
