@@ -520,24 +520,16 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
     totD += __popc(bd);
   }
   __syncwarp();
-  // ---- 3. stream A
-  auto lower_p = [&](uint32_t x) {  // #t with P[t] < x
-    uint32_t l = 0, h = b;
-    while (l < h) {
-      const uint32_t m = (l + h) >> 1;
-      if (XP[m] < x) l = m + 1;
-      else h = m;
-    }
-    return l;
-  };
-  // windows of 256, software-pipelined: the next window's loads are in flight while this one is
-  // placed
+  // ---- 3. stream A in windows of 256, software-pipelined (the next window's loads are in flight
+  // while this one is placed).  The F entries landing in a window, [tl, th), are walked once per
+  // window (broadcast shared reads) against all 8 of a lane's entries at once.
   uint64_t nv[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t i = lane + 32 * k;
     nv[k] = i < a ? ldcg64(A + i) : 0ull;
   }
+  uint32_t tl = 0;
   for (uint32_t w0 = 0; w0 < a; w0 += 256) {
     uint64_t v[8];
 #pragma unroll
@@ -546,24 +538,33 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
       const uint32_t i = w0 + 256 + lane + 32 * k;
       nv[k] = i < a ? ldcg64(A + i) : 0ull;
     }
-    const uint32_t tl = lower_p(w0), th = lower_p(w0 + 256);
+    uint32_t th = tl;
+    while (th < b && XP[th] < w0 + 256) ++th;
     const uint32_t cl = tl < b ? XC[tl] & 0x7FFFFFFFu : ((totD << 16) | totI);
-    const uint32_t baseI = cl & 0xFFFFu, baseD = cl >> 16;
+    uint32_t ins[8], rem[8];
+    uint32_t removed = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      ins[k] = cl & 0xFFFFu;
+      rem[k] = cl >> 16;
+    }
+    for (uint32_t t = tl; t < th; ++t) {
+      const uint32_t pt = XP[t];
+      const bool dup = XC[t] >> 31;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = w0 + lane + 32 * k;
+        ins[k] += (!dup && pt <= i) ? 1u : 0u;
+        rem[k] += (dup && pt < i) ? 1u : 0u;
+        removed |= (dup && pt == i) ? (1u << k) : 0u;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const uint32_t i = w0 + lane + 32 * k;
-      if (i >= a) continue;
-      uint32_t ins = baseI, rem = baseD;
-      bool removed = false;
-      for (uint32_t t = tl; t < th; ++t) {
-        const uint32_t pt = XP[t];
-        const bool dup = XC[t] >> 31;
-        if (!dup && pt <= i) ++ins;
-        if (dup && pt < i) ++rem;
-        if (dup && pt == i) removed = true;
-      }
-      if (!removed) C[i + ins - rem] = v[k];
+      if (i < a && !(removed >> k & 1)) C[i + ins[k] - rem[k]] = v[k];
     }
+    tl = th;
   }
   __syncwarp();
   return a + totI - totD;
