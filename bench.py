@@ -285,9 +285,12 @@ def run_ours(args, rank, world, local_rank):
                             None if batched else tuple(host_img.shape))
     # the filtration (K1) and apparent-pair (K2) kernels' achieved bandwidth (BASELINE north_star)
     k1k2 = None
-    if not batched and "births" in stage_avg and "apparent" in stage_avg:
+    k12_names = [n for n in ("filtration", "births", "apparent") if n in stage_avg]
+    if not batched and k12_names:
         k1k2 = {}
-        for name in ("births", "apparent"):
+        if "filtration" in stage_avg:
+            k1k2["fused"] = "K1 and K2 are one kernel (k_filtration): the entry covers both"
+        for name in k12_names:
             b = algorithmic_bytes(args.config, name, nvox_local, st, n_out, tuple(host_img.shape))
             gbs = b / (stage_avg[name] / 1e3) / 1e9
             k1k2[name] = {"ms": round(stage_avg[name], 4), "alg_bytes": b,
@@ -353,10 +356,13 @@ def algorithmic_bytes(cfg, stage, nvox, st, n_out, shape=None):
         return 4 * nvox + 4 * kcells
     if stage == "apparent":                       # read the births, write a tag per cell
         return 5 * kcells
+    if stage == "filtration":                     # K1+K2 fused: read the image, write births+tags
+        return 4 * nvox + 5 * kcells
     return None
 
 
-NCU_KERNEL = {"1d_level1": "k1_level1", "1d_levels_gather": "k1_levels_coop"}
+NCU_KERNEL = {"1d_level1": "k1_level1", "1d_levels_gather": "k1_levels_coop",
+              "filtration": "k_filtration"}
 
 
 def ncu_traffic(stage):

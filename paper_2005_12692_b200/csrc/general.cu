@@ -889,6 +889,400 @@ __global__ void __launch_bounds__(256) k_tags_codes(const uint8_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------------------
+// K1 + K2 fused (the default): births AND apparent-pair tags of every cell from one read of the
+// image (PAPER.md:97-108 for the births, PAPER.md:44-45 for the apparent pairs; the same pairs as
+// k_births + k_apparent above).  A thread owns one voxel column (x, y) and walks it along z; its
+// unit of work is the voxel block B(x,y,z) = the 8 cells (2x+i, 2y+j, 2z+k), i,j,k in {0,1},
+// whose births are maxima over the voxels (x..x+i, y..y+j, z..z+k): with the "plane cells"
+// P(z) = {V, Ex, Ey, Sxy} of a block, the k=1 cells are max(P(z), P(z+1)) (4 max per block).
+// A cell's 6 Khalimsky neighbours lie in its own block or in the blocks at x+-1 (neighbouring
+// lanes: shuffles), y+-1 (neighbouring warps: shared memory) and z+-1 (the thread's previous /
+// next step: registers), so codes and tags are formed from registers with one __syncthreads per
+// step.  Lanes 0 and 31 and warps 0 and KF_ROWS+1 are halo (their blocks' codes feed the tags of
+// the inner 30 x KF_ROWS columns); lane 31 also loads the x+1 voxels its i=1 cells need.  Step z
+// completes B(z-1)'s births (writes them), forms B(z-1)'s codes and B(z-2)'s tags (writes them).
+//
+// Codes use equal births only.  A cell's max-key facet has the cell's own birth (a birth is the max
+// over the vertices, and every vertex lies in a facet), so it is the LAST facet in kidx order whose
+// birth equals the cell's.  Cofacets have births >= the cell's; the min-key cofacet matters only
+// when its birth equals the cell's (an apparent pair has death == birth), and then it is the FIRST
+// cofacet in kidx order with that birth; otherwise the code says "none" (7), which gives the same
+// UP / DOWN decisions as the full min-key code.  One compare + select per neighbour.
+// Warps whose births (codes) are all absent skip the code (tag) arithmetic: C5's outside-ball
+// region costs only its stores.
+// Layout in registers: births b[i + 2j + 4k]; codes and tags packed in two words by j, byte i+2k.
+// ---------------------------------------------------------------------------------------------
+constexpr int KF_ROWS = 14, KF_THREADS = 32 * (KF_ROWS + 2);
+struct KfLaunch {
+  unsigned grid;
+  int zc;
+};
+inline KfLaunch kf_launch(const Geom& g) {
+  const int64_t xy = ((g.nx + 29) / 30) * ((g.ny + KF_ROWS - 1) / KF_ROWS);
+  int zc = 64;
+  while (zc > 8 && xy * ((g.nz + zc - 1) / zc) < 4 * 148) zc >>= 1;
+  return {unsigned(xy * ((g.nz + zc - 1) / zc)), zc};
+}
+
+// code of cell (I,J,K) of block B; L/R: births of the x-1 block's i=1 / x+1 block's i=0 cells
+// (index j + 2k), D/U: the y-1 block's j=1 / y+1 block's j=0 cells (index i + 2k), Zm/Zp: the
+// z-1 block's k=1 / z+1 block's k=0 cells (index i + 2j).  kidx order of the neighbours:
+// -Z (dir 4) < -Y (2) < -X (0) < +X (1) < +Y (3) < +Z (5); odd axis -> facet, even -> cofacet.
+template <int I, int J, int K>
+__device__ __forceinline__ uint32_t kf_code(const uint32_t (&B)[8], const uint32_t (&L)[4],
+                                            const uint32_t (&R)[4], const uint32_t (&D)[4],
+                                            const uint32_t (&U)[4], const uint32_t (&Zm)[4],
+                                            const uint32_t (&Zp)[4]) {
+  const uint32_t b = B[I + 2 * J + 4 * K];
+  const uint32_t nb[6] = {K ? B[I + 2 * J] : Zm[I + 2 * J],       // -Z
+                          J ? B[I + 4 * K] : D[I + 2 * K],        // -Y
+                          I ? B[2 * J + 4 * K] : L[J + 2 * K],    // -X
+                          I ? R[J + 2 * K] : B[1 + 2 * J + 4 * K],  // +X
+                          J ? U[I + 2 * K] : B[I + 2 + 4 * K],    // +Y
+                          K ? Zp[I + 2 * J] : B[I + 2 * J + 4]};  // +Z
+  constexpr uint32_t dir[6] = {4, 2, 0, 1, 3, 5};
+  const bool odd[6] = {K != 0, J != 0, I != 0, I != 0, J != 0, K != 0};
+  // facets: the last equal one (the first facet is the default: one of them must be equal)
+  uint32_t mf = 7;
+  bool first = true;
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+    if (odd[q]) {
+      mf = first ? dir[q] : (nb[q] == b ? dir[q] : mf);
+      first = false;
+    }
+  // cofacets: the first equal one (scan backwards); absent cofacets never equal a present birth
+  uint32_t mc = 7;
+#pragma unroll
+  for (int q = 5; q >= 0; --q)
+    if (!odd[q]) mc = nb[q] == b ? dir[q] : mc;
+  return b == ABSENT_ORD ? uint32_t(CODE_ABSENT) : (mc | (mf << 3));
+}
+// Tags of the 4 cells of code word J (bytes p = i + 2k), all at once: byte-wise SIMD on packed
+// codes.  nbw[d] holds, in byte p, the code of that cell's neighbour in direction d (assembled by
+// byte permutes from the block's and the neighbouring blocks' code words).  UP at byte p iff its
+// mc == d and the neighbour's mf == d^1 for some d; DOWN iff its mf == d and the neighbour's
+// mc == d^1 (the pair is apparent iff each is the other's extremal (co)facet).
+// Per direction: a bit-select pairs the two 3-bit fields, a xor+mask compares them with the
+// constant, and (z + 0x7F) has bit 7 clear iff the 6-bit byte z is 0 (no carry leaves a byte).
+// A word holds only j-even (J=0: Y cofacets) or j-odd (J=1: Y facets) cells, so half of the Y
+// tests are dropped.  Absent cells (code 0x40: fields 0) are masked out at the end.
+template <int J>
+__device__ __forceinline__ uint32_t kf_tags_word(uint32_t own, uint32_t xm, uint32_t xp,
+                                                 uint32_t ym, uint32_t yp, uint32_t zm,
+                                                 uint32_t zp) {
+  const uint32_t nbw[6] = {xm, xp, ym, yp, zm, zp};
+  uint32_t upn = 0, dnn = 0;  // bit 7 of each byte: set iff NO direction matched
+  upn = dnn = 0xFFFFFFFFu;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const bool ydir = d == 2 || d == 3;
+    if (!ydir || J == 0) {  // UP: own mc (bits 0-2) with the neighbour's mf (bits 3-5)
+      const uint32_t K = uint32_t(d | ((d ^ 1) << 3)) * 0x01010101u;
+      const uint32_t X = (own & 0x07070707u) | (nbw[d] & 0x38383838u);
+      upn &= ((X ^ K) & 0x3F3F3F3Fu) + 0x7F7F7F7Fu;
+    }
+    if (!ydir || J == 1) {  // DOWN: own mf with the neighbour's mc
+      const uint32_t K = uint32_t((d ^ 1) | (d << 3)) * 0x01010101u;
+      const uint32_t X = (nbw[d] & 0x07070707u) | (own & 0x38383838u);
+      dnn &= ((X ^ K) & 0x3F3F3F3Fu) + 0x7F7F7F7Fu;
+    }
+  }
+  const uint32_t pres = ~(own << 1);                       // bit 7 set iff present
+  const uint32_t upf = ~upn & pres & 0x80808080u;
+  const uint32_t dnf = ~dnn & ~upf & pres & 0x80808080u;   // UP wins (as in tag_of)
+  const uint32_t upm = (upf >> 7) * 0xFFu, dnm = (dnf >> 7) * 0xFFu;
+  return (upm & (0x80808080u | (own & 0x07070707u))) |
+         (dnm & (0x40404040u | ((own >> 3) & 0x07070707u)));
+}
+
+__device__ __forceinline__ uint32_t kf_ord(float f) {
+  const uint32_t u = __float_as_uint(f + 0.0f);  // -0 + 0 = +0 (reading R7); NaN stays NaN
+  return u ^ (uint32_t(int32_t(u) >> 31) | 0x80000000u);
+}
+
+__device__ __forceinline__ void kf_cp4(uint32_t saddr, const float* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void kf_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void kf_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int KF_PF = 3, KF_RING = KF_PF + 1;  // voxel planes in flight, ring slots
+constexpr int KF_VROWS = KF_ROWS + 3, KF_VCOLS = 33;
+struct KfSmem {
+  uint32_t v[KF_RING][KF_VROWS][KF_VCOLS];  // voxel ring (raw float bits)
+  uint4 bj0[2][KF_ROWS + 2][32];            // births of the j=0 cells (i + 2k), double-buffered
+  uint4 bj1[2][KF_ROWS + 2][32];            // births of the j=1 cells
+  uint32_t c0[2][KF_ROWS + 2][32];          // codes word j=0
+  uint32_t c1[2][KF_ROWS + 2][32];          // codes word j=1
+  uint32_t cnt[8];
+};
+
+struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsky grid < 2^32 cells)
+  uint32_t nx, ny, nz, KX, KXY, plane, XB, YB, zc;
+};
+inline KfP kf_params(const Geom& g, int zc) {
+  KfP p;
+  p.nx = uint32_t(g.nx);
+  p.ny = uint32_t(g.ny);
+  p.nz = uint32_t(g.nz);
+  p.KX = uint32_t(g.KX);
+  p.KXY = uint32_t(g.KX * g.KY);
+  p.plane = uint32_t(g.nx * g.ny);
+  p.XB = uint32_t((g.nx + 29) / 30);
+  p.YB = uint32_t((g.ny + KF_ROWS - 1) / KF_ROWS);
+  p.zc = uint32_t(zc);
+  return p;
+}
+
+__global__ void __launch_bounds__(KF_THREADS, 2) k_filtration(const float* __restrict__ img,
+                                                              const KfP P,
+                                                              uint32_t* __restrict__ births,
+                                                              uint8_t* __restrict__ tags,
+                                                              unsigned long long* __restrict__ cnt,
+                                                              int* __restrict__ nan_flag) {
+  extern __shared__ uint4 kf_dyn[];
+  KfSmem& S = *reinterpret_cast<KfSmem*>(kf_dyn);
+  const int nx = int(P.nx), ny = int(P.ny), nz = int(P.nz);
+  uint32_t blk = blockIdx.x;
+  const int xb = int(blk % P.XB);
+  blk /= P.XB;
+  const int yb = int(blk % P.YB), zb = int(blk / P.YB);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int x = xb * 30 - 1 + lane, y = yb * KF_ROWS - 1 + w;
+  const int z0 = zb * int(P.zc), z1 = min(nz, z0 + int(P.zc));
+  const bool vx = x >= 0 && x < nx, vy = y >= 0 && y < ny, vy1 = y + 1 < ny;
+  const bool l31 = lane == 31, vx1 = x + 1 < nx, lastw = w == KF_ROWS + 1;
+  const bool out = vx && vy && lane >= 1 && lane <= 30 && w >= 1 && w <= KF_ROWS;
+  const bool halo_w = w == 0 || lastw;  // warp-uniform: no tags needed
+  if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
+  constexpr uint32_t INF_BITS = 0x7F800000u;
+  // Voxel ring: v[slot][row][col], rows y0-1 .. y0+KF_ROWS+1 (the last copied by the last warp),
+  // cols x0-1 .. x0+31 (col 32 copied by lane 31).  Copies: (x, y); lane 31 also (x+1, y); the
+  // last warp also (x, y+1) and its lane 31 (x+1, y+1) -- all offsets of the (x, y) pointer.
+  // Positions outside the image hold +inf from the start and are never copied.
+  const bool o00 = vx && vy, o10 = l31 && vx1 && vy, o01 = lastw && vx && vy1,
+             o11 = lastw && l31 && vx1 && vy1;
+  uint32_t* const vown = &S.v[0][w][lane];
+  const uint32_t sv0 = uint32_t(__cvta_generic_to_shared(vown));
+  constexpr uint32_t SLOTW = KF_VROWS * KF_VCOLS, SLOT = SLOTW * 4, ROW = KF_VCOLS * 4;
+  const int c32 = 32 - lane;  // own col -> col 32
+#pragma unroll
+  for (int r = 0; r < KF_RING; ++r) {
+    if (!o00) vown[r * SLOTW] = INF_BITS;
+    if (l31 && !o10) vown[r * SLOTW + c32] = INF_BITS;
+    if (lastw && !o01) vown[r * SLOTW + KF_VCOLS] = INF_BITS;
+    if (lastw && l31 && !o11) vown[r * SLOTW + KF_VCOLS + c32] = INF_BITS;
+  }
+  const float* gsrc = img + (o00 ? uint64_t(uint32_t(y) * P.nx + uint32_t(x)) : 0ull);
+  // plane zz into ring slot s (always one commit group, possibly empty)
+  auto issue = [&](int zz, uint32_t s) {
+    if (zz >= 0 && zz < nz) {  // CTA-uniform
+      const uint32_t a = sv0 + s * SLOT;
+      const float* p = gsrc + uint64_t(uint32_t(zz)) * P.plane;
+      if (o00) kf_cp4(a, p);
+      if (o10) kf_cp4(a + 4 * c32, p + 1);
+      if (lastw) {
+        const float* q = p + P.nx;
+        if (o01) kf_cp4(a + ROW, q);
+        if (o11) kf_cp4(a + ROW + 4 * c32, q + 1);
+      }
+    } else {
+      uint32_t* v = vown + s * SLOTW;
+      if (o00) v[0] = INF_BITS;
+      if (o10) v[c32] = INF_BITS;
+      if (o01) v[KF_VCOLS] = INF_BITS;
+      if (o11) v[KF_VCOLS + c32] = INF_BITS;
+    }
+    kf_commit();
+  };
+  // all voxels this thread copies (or prefilled) into slot s are +inf
+  auto own_inf = [&](uint32_t s) -> bool {
+    const uint32_t* v = vown + s * SLOTW;
+    bool r = v[0] == INF_BITS;
+    if (l31) r = r && v[c32] == INF_BITS;
+    if (lastw) r = r && v[KF_VCOLS] == INF_BITS && (!l31 || v[KF_VCOLS + c32] == INF_BITS);
+    return r;
+  };
+  int z = z0 - 2;
+#pragma unroll
+  for (int q = 0; q < KF_PF; ++q) issue(z + q, uint32_t(q));
+  kf_wait<KF_PF - 1>();  // plane z0-2 landed (own copies)
+  // CTA-uniform "plane is +inf over the CTA's footprint" flags of planes z-2, z-1, z; the
+  // fictitious planes before z0-2 count as +inf (the state below is initialised as absent)
+  bool f2 = true, f1 = true, f0 = __syncthreads_and(own_inf(0));
+  const int wm = max(w - 1, 0), wp = min(w + 1, KF_ROWS + 1);
+  bool nan = false;
+  uint32_t P0[4] = {ABSENT_ORD, ABSENT_ORD, ABSENT_ORD, ABSENT_ORD};  // P(z-1)
+  uint32_t Zm[4] = {ABSENT_ORD, ABSENT_ORD, ABSENT_ORD, ABSENT_ORD};  // B(z-2), k=1 cells
+  uint32_t CC[2] = {0x40404040u, 0x40404040u};                     // codes of B(z-2)
+  uint32_t CZm[2] = {0x40404040u, 0x40404040u};                    // codes of B(z-3)
+  // per-byte counters (byte = cell position i + 2k of word j): finite cells, UP cells
+  uint32_t fin0 = 0, fin1 = 0, up0 = 0, up1 = 0;
+  // output: births of B(z-1) / tags of B(z-2) at (2z'+k, 2y+j, 2x+i); offset of (2z0-2, 2y, 2x)
+  // ... advanced by 2 KXY per step (only used when the step's plane is in [z0, z1))
+  const uint32_t rowbase = uint32_t(2 * max(y, 0)) * P.KX + uint32_t(2 * max(x, 0));
+  const bool hx = x + 1 < nx, hy = y + 1 < ny;
+  uint32_t rs = 0;  // ring slot of plane z
+  for (; z <= z1 + 1; ++z) {
+    issue(z + KF_PF, (rs + KF_PF) & (KF_RING - 1));
+    const bool fast = f2 && f1 && f0;  // B(z-1), B(z-2) entirely absent: nothing to compute
+    uint32_t Pn[4] = {ABSENT_ORD, ABSENT_ORD, ABSENT_ORD, ABSENT_ORD};
+    uint32_t Bk[8];
+    const int buf = z & 1;
+    if (!fast) {
+      // P(z): plane cells of block z, from the ring (max over floats, then the order key)
+      const uint32_t* v = vown + rs * SLOTW;
+      const float v00 = __uint_as_float(v[0]), v10 = __uint_as_float(v[1]);
+      const float v01 = __uint_as_float(v[KF_VCOLS]), v11 = __uint_as_float(v[KF_VCOLS + 1]);
+      nan |= v00 != v00;
+      const float ex = fmaxf(v00, v10);
+      Pn[0] = kf_ord(v00);
+      Pn[1] = kf_ord(ex);
+      Pn[2] = kf_ord(fmaxf(v00, v01));
+      Pn[3] = kf_ord(fmaxf(ex, fmaxf(v01, v11)));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Bk[q] = P0[q];
+        Bk[q + 4] = max(P0[q], Pn[q]);
+      }
+      S.bj0[buf][w][lane] = make_uint4(Bk[0], Bk[1], Bk[4], Bk[5]);
+      S.bj1[buf][w][lane] = make_uint4(Bk[2], Bk[3], Bk[6], Bk[7]);
+      S.c0[buf][w][lane] = CC[0];
+      S.c1[buf][w][lane] = CC[1];
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) Bk[q] = ABSENT_ORD;
+    }
+    kf_wait<KF_PF - 1>();  // plane z+1 landed (own copies); visible to all after the barrier
+    const uint32_t rn = (rs + 1) & (KF_RING - 1);
+    const bool fn = __syncthreads_and(own_inf(rn));
+    uint32_t NC[2] = {0x40404040u, 0x40404040u};
+    uint32_t T0 = 0, T1 = 0;  // tag bytes, words by j, bytes i + 2k (like the codes)
+    if (!fast) {
+      // codes of B(z-1)
+      const uint32_t bmin = min(min(min(Bk[0], Bk[1]), min(Bk[2], Bk[3])),
+                                min(min(Bk[4], Bk[5]), min(Bk[6], Bk[7])));
+      if (__any_sync(0xFFFFFFFFu, bmin != ABSENT_ORD)) {
+        const uint4 dq = S.bj1[buf][wm][lane], uq = S.bj0[buf][wp][lane];
+        const uint32_t D[4] = {dq.x, dq.y, dq.z, dq.w}, U[4] = {uq.x, uq.y, uq.z, uq.w};
+        uint32_t L[4], R[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // q = j + 2k: L = x-1's (1,j,k), R = x+1's (0,j,k)
+          L[q] = __shfl_up_sync(0xFFFFFFFFu, Bk[1 + 2 * q], 1);
+          R[q] = __shfl_down_sync(0xFFFFFFFFu, Bk[2 * q], 1);
+        }
+        const uint32_t c000 = kf_code<0, 0, 0>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c100 = kf_code<1, 0, 0>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c010 = kf_code<0, 1, 0>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c110 = kf_code<1, 1, 0>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c001 = kf_code<0, 0, 1>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c101 = kf_code<1, 0, 1>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c011 = kf_code<0, 1, 1>(Bk, L, R, D, U, Zm, Pn);
+        const uint32_t c111 = kf_code<1, 1, 1>(Bk, L, R, D, U, Zm, Pn);
+        NC[0] = c000 | (c100 << 8) | (c001 << 16) | (c101 << 24);
+        NC[1] = c010 | (c110 << 8) | (c011 << 16) | (c111 << 24);
+      }
+      // tags of B(z-2) (not needed in the halo warps)
+      if (!halo_w && __any_sync(0xFFFFFFFFu, (CC[0] & CC[1] & 0x40404040u) != 0x40404040u)) {
+        const uint32_t CD = S.c1[buf][wm][lane], CU = S.c0[buf][wp][lane];
+        uint32_t CL[2], CR[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          CL[q] = __shfl_up_sync(0xFFFFFFFFu, CC[q], 1);
+          CR[q] = __shfl_down_sync(0xFFFFFFFFu, CC[q], 1);
+        }
+        // neighbour codes by direction, byte p = i + 2k (see kf_tags_word)
+        T0 = kf_tags_word<0>(CC[0], __byte_perm(CL[0], CC[0], 0x6341),
+                             __byte_perm(CC[0], CR[0], 0x6341), CD, CC[1],
+                             __byte_perm(CZm[0], CC[0], 0x5432), __byte_perm(CC[0], NC[0], 0x5432));
+        T1 = kf_tags_word<1>(CC[1], __byte_perm(CL[1], CC[1], 0x6341),
+                             __byte_perm(CC[1], CR[1], 0x6341), CC[0], CU,
+                             __byte_perm(CZm[1], CC[1], 0x5432), __byte_perm(CC[1], NC[1], 0x5432));
+      }
+    }
+    // stores: births of B(z-1), tags of B(z-2); counters from the codes (bit 6 = absent) and
+    // the tags (bit 7 = UP).  Cell (i,j,k) exists iff (i=0 or hx), (j=0 or hy), (k=0 or hz).
+    if (out) {
+      const int zb1 = z - 1, zb2 = z - 2;
+      if (zb1 >= z0 && zb1 < z1) {
+        fin0 += (~NC[0] >> 6) & 0x01010101u;
+        fin1 += (~NC[1] >> 6) & 0x01010101u;
+        uint32_t* p0 = births + (uint32_t(zb1) * 2u * P.KXY + rowbase);
+        uint32_t* p1 = p0 + P.KX;
+        const bool hz = zb1 + 1 < nz;
+        p0[0] = Bk[0];
+        if (hx) p0[1] = Bk[1];
+        if (hy) p1[0] = Bk[2];
+        if (hx && hy) p1[1] = Bk[3];
+        if (hz) {
+          uint32_t* p2 = p0 + P.KXY;
+          uint32_t* p3 = p1 + P.KXY;
+          p2[0] = Bk[4];
+          if (hx) p2[1] = Bk[5];
+          if (hy) p3[0] = Bk[6];
+          if (hx && hy) p3[1] = Bk[7];
+        }
+      }
+      if (zb2 >= z0 && zb2 < z1) {
+        up0 += (T0 >> 7) & 0x01010101u;
+        up1 += (T1 >> 7) & 0x01010101u;
+        uint8_t* p0 = tags + (uint32_t(zb2) * 2u * P.KXY + rowbase);
+        uint8_t* p1 = p0 + P.KX;
+        const bool hz = zb2 + 1 < nz;
+        p0[0] = uint8_t(T0);
+        if (hx) p0[1] = uint8_t(T0 >> 8);
+        if (hy) p1[0] = uint8_t(T1);
+        if (hx && hy) p1[1] = uint8_t(T1 >> 8);
+        if (hz) {
+          uint8_t* p2 = p0 + P.KXY;
+          uint8_t* p3 = p1 + P.KXY;
+          p2[0] = uint8_t(T0 >> 16);
+          if (hx) p2[1] = uint8_t(T0 >> 24);
+          if (hy) p3[0] = uint8_t(T1 >> 16);
+          if (hx && hy) p3[1] = uint8_t(T1 >> 24);
+        }
+      }
+    }
+    // shift the pipeline
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      Zm[q] = Bk[q + 4];
+      P0[q] = Pn[q];
+    }
+    CZm[0] = CC[0];
+    CZm[1] = CC[1];
+    CC[0] = NC[0];
+    CC[1] = NC[1];
+    f2 = f1;
+    f1 = f0;
+    f0 = fn;
+    rs = rn;
+  }
+  kf_wait<0>();
+  // counters: byte p of word j is cell (i, j, k) with p = i + 2k, dim = i + j + k
+  auto B8 = [](uint32_t v, int p) { return (v >> (8 * p)) & 0xFFu; };
+  const uint32_t v[7] = {B8(up0, 0),                                      // UP, dim 0
+                         B8(up0, 1) + B8(up0, 2) + B8(up1, 0),             // UP, dim 1
+                         B8(up0, 3) + B8(up1, 1) + B8(up1, 2),             // UP, dim 2
+                         B8(fin0, 0),                                     // finite, dim 0
+                         B8(fin0, 1) + B8(fin0, 2) + B8(fin1, 0),          // dim 1
+                         B8(fin0, 3) + B8(fin1, 1) + B8(fin1, 2),          // dim 2
+                         B8(fin1, 3)};                                    // dim 3
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, v[q]);
+    if (lane == 0 && s) atomicAdd(S.cnt + q, s);
+  }
+  const bool anynan = __any_sync(0xFFFFFFFFu, nan);
+  if (lane == 0 && anynan) atomicOr(nan_flag, 1);
+  __syncthreads();
+  if (threadIdx.x < 7 && S.cnt[threadIdx.x])
+    atomicAdd(cnt + (threadIdx.x < 3 ? threadIdx.x : threadIdx.x + 1),
+              (unsigned long long)S.cnt[threadIdx.x]);
+}
+// ---------------------------------------------------------------------------------------------
 // K4: H0 by union-find with the elder rule.
 //  (1) every apparent vertex v (UP, paired with its earliest edge e_v) hangs under the other
 //      endpoint of e_v, which is older; roots are the non-apparent vertices ("basins").
@@ -1743,11 +2137,26 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
 
-  // Default: K1 (k_births) + K2 fused (k_apparent).  Variants for cross-checks and measurement
-  // (profiles/r01/s3: C5 K1+K2 = 0.52 + 3.60 ms default, 1.91 + 1.76 fused births+codes,
-  // 0.52 + 1.66 + 1.76 split): CR_K12_FUSED, CR_K12_SPLIT, CR_K2_TWOPASS, CR_K2_ONEPASS.
+  // Default: K1 + K2 in one kernel (k_filtration).  Variants for cross-checks and measurement
+  // (profiles/r01/s3: C5 K1+K2 = 0.52 + 3.60 ms as k_births + k_apparent (CR_K12_OLD),
+  // 1.91 + 1.76 fused births+codes, 0.52 + 1.66 + 1.76 split): CR_K12_OLD, CR_K12_FUSED,
+  // CR_K12_SPLIT, CR_K2_TWOPASS, CR_K2_ONEPASS.
   const bool k12_old = !(std::getenv("CR_K12_FUSED") || std::getenv("CR_K12_SPLIT"));
-  if (!k12_old && std::getenv("CR_K12_SPLIT")) {
+  const bool k12_sep = std::getenv("CR_K12_OLD") || std::getenv("CR_K2_ONEPASS") ||
+                       std::getenv("CR_K2_TWOPASS") || !k12_old;
+  if (!k12_sep) {  // default: K1 + K2 in one streaming kernel
+    const KfLaunch L = kf_launch(g);
+    static thread_local int kf_attr_dev = -1;
+    if (kf_attr_dev != ws.device()) {
+      CR_CUDA(cudaFuncSetAttribute(k_filtration, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(KfSmem))));
+      kf_attr_dev = ws.device();
+    }
+    k_filtration<<<L.grid, KF_THREADS, sizeof(KfSmem), s>>>(image, kf_params(g, L.zc), S.births,
+                                                            S.tags, cnt, nan_flag);
+    CR_CHECK_LAUNCH();
+    prof_mark(s, "filtration");
+  } else if (!k12_old && std::getenv("CR_K12_SPLIT")) {
     // K1 (births) alone, then K2 as codes (z-streaming) + tags from codes
     uint8_t* code = ws.alloc<uint8_t>(g.ncells + 4);
     k_births<<<k_births_grid(g), 256, 0, s>>>(image, g, S.births, cnt + 4, nan_flag);
@@ -1786,7 +2195,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     CR_CHECK_LAUNCH();
   }
   }
-  prof_mark(s, "apparent");
+  if (k12_sep) prof_mark(s, "apparent");
 
   if (S.top_only) {  // the top dimension alone (--top_dim): no H0, no clearing
     CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));

@@ -106,23 +106,35 @@ def test_general_path_on_1d(cr, monkeypatch):
 
 
 def test_k2_variants_agree(cr, monkeypatch):
-    """K2 (apparent pairs) as one fused streaming kernel, as codes-then-tags, as the direct
-    one-kernel definition, and with the codes fused into K1 (births) give the same pairing (and
-    the oracle's), on shapes whose Khalimsky extents are not multiples of the kernels' tiles."""
+    """K1+K2 in one kernel (default), K2 as one fused streaming kernel after K1, as
+    codes-then-tags, as the direct one-kernel definition, and with the codes fused into K1 give
+    the same pairing (and the oracle's) and the same cell / apparent-pair counts, on shapes whose
+    extents are not multiples of the kernels' tiles."""
     import torch
     imgs = [gen.masked_grf((33, 37, 41), 2.0, 17.0, 21),
             gen.small_int_image((9, 70, 13), 3, seed=22, inf_frac=0.1),
-            gen.small_int_image((67, 35), 4, seed=23, inf_frac=0.05)]
+            gen.small_int_image((67, 35), 4, seed=23, inf_frac=0.05),
+            gen.small_int_image((20, 45, 61), 3, seed=24, inf_frac=0.05),
+            gen.masked_grf((70, 31, 29), 1.5, 12.0, 25)]
     for k, img in enumerate(imgs):
         o = oracle.ph(img, img.ndim - 1, partner=True)
         t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
-        for var in ["", "CR_K2_TWOPASS", "CR_K2_ONEPASS", "CR_K12_FUSED", "CR_K12_SPLIT"]:
-            for v in ["CR_K2_TWOPASS", "CR_K2_ONEPASS", "CR_K12_FUSED", "CR_K12_SPLIT"]:
+        ref_stats = None
+        variants = ["", "CR_K12_OLD", "CR_K2_TWOPASS", "CR_K2_ONEPASS", "CR_K12_FUSED", "CR_K12_SPLIT"]
+        for var in variants:
+            for v in variants[1:]:
                 monkeypatch.delenv(v, raising=False)
             if var:
                 monkeypatch.setenv(var, "1")
             p = cr.pairing(t).cpu().numpy().view(np.uint32)
             assert np.array_equal(p, o.partner), (k, var, np.flatnonzero(p != o.partner)[:10])
+            # a missed apparent pair would still be paired by the reduction: compare the counts
+            cr.barcodes(t, img.ndim - 1)
+            st = cr.last_stats()
+            got = (list(st["cells"]), list(st["apparent"]))
+            if ref_stats is None:
+                ref_stats = got
+            assert got == ref_stats, (k, var, got, ref_stats)
 
 
 def _cavity_cases():
