@@ -1,6 +1,9 @@
 // util.cu -- workspace, device sort/scan wrappers.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+#include <map>
+
 #include "pipeline.cuh"
 
 namespace cr {
@@ -83,24 +86,50 @@ struct Arena {
 };
 constexpr int MAX_DEV = 64;
 thread_local Arena g_arena[MAX_DEV];
-thread_local bool g_pool_set[MAX_DEV] = {};
+
+// Block cache (per host thread and device): device blocks are kept after a call and handed out
+// again by size, so a steady stream of calls makes no allocator calls at all.  The stream-ordered
+// pool (cudaMallocAsync) was measured to stall the host for 10-1000 ms on some repeated calls
+// (profiles/r01/s5: C5 reduce_d1 1.63 -> 2.72 s, H0 4.5 -> 536 ms) -- fragmentation makes it map
+// fresh memory.  A block is reused for a request of size in [size/2, size]; blocks are only freed
+// when an allocation fails (then everything cached is returned to the driver and it is retried).
+// Calls are blocking and one stream each; a call on another stream first waits on an event
+// recorded at the end of the previous call, so cached blocks are never in use by two streams.
+struct Cache {
+  std::multimap<size_t, void*> free_blocks;  // size -> block
+  std::map<void*, size_t> size_of;           // every block this cache owns
+  cudaEvent_t done = nullptr;                // recorded at the end of the last call
+  cudaStream_t last = nullptr;
+  bool pool_set = false;
+};
+thread_local Cache g_cache[MAX_DEV];
+size_t round_block(size_t b) {
+  if (b <= (size_t(1) << 20)) return (b + 511) & ~size_t(511);
+  return (b + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+}
 }  // namespace
 
 Workspace::Workspace(cudaStream_t s) : s_(s) {
   if (cudaGetDevice(&dev_) != cudaSuccess || dev_ < 0 || dev_ >= MAX_DEV) dev_ = 0;
-  if (!g_pool_set[dev_]) {  // keep freed blocks in the default pool (once per thread and device)
+  Cache& C = g_cache[dev_];
+  if (!C.pool_set) {  // keep freed blocks in the default pool (once per thread and device)
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev_) == cudaSuccess) {
       uint64_t thr = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    g_pool_set[dev_] = true;
+    C.pool_set = true;
   }
+  if (C.done && C.last != s_) cudaStreamWaitEvent(s_, C.done, 0);
 }
 
 Workspace::~Workspace() {
+  Cache& C = g_cache[dev_];
   for (void* p : ptrs_)
-    if (p) cudaFreeAsync(p, s_);
+    if (p) C.free_blocks.emplace(C.size_of[p], p);
+  if (!C.done) cudaEventCreateWithFlags(&C.done, cudaEventDisableTiming);
+  if (C.done) cudaEventRecord(C.done, s_);
+  C.last = s_;
   if (arena_ && need_ > acap_) {  // grow the arena to this call's high-water mark
     Arena& A = g_arena[dev_];
     if (A.base) cudaFreeAsync(A.base, s_);
@@ -129,8 +158,26 @@ void* Workspace::alloc_bytes(size_t bytes) {
       return p;
     }
   }
+  Cache& C = g_cache[dev_];
+  const size_t want = round_block(bytes < 1 ? 1 : bytes);
+  auto it = C.free_blocks.lower_bound(want);
+  if (it != C.free_blocks.end() && it->first <= 2 * want) {
+    void* p = it->second;
+    C.free_blocks.erase(it);
+    ptrs_.push_back(p);
+    return p;
+  }
   void* p = nullptr;
-  CR_CUDA(cudaMallocAsync(&p, bytes, s_));
+  if (cudaMallocAsync(&p, want, s_) != cudaSuccess) {
+    cudaGetLastError();  // out of memory: return the cache to the driver and retry once
+    for (auto& kv : C.free_blocks) {
+      cudaFreeAsync(kv.second, s_);
+      C.size_of.erase(kv.second);
+    }
+    C.free_blocks.clear();
+    CR_CUDA(cudaMallocAsync(&p, want, s_));
+  }
+  C.size_of[p] = want;
   ptrs_.push_back(p);
   return p;
 }
@@ -138,7 +185,8 @@ void* Workspace::alloc_bytes(size_t bytes) {
 void Workspace::release(void* p) {
   for (auto& q : ptrs_)
     if (q == p) {
-      cudaFreeAsync(q, s_);
+      Cache& C = g_cache[dev_];
+      C.free_blocks.emplace(C.size_of[q], q);  // reusable by later allocations on this stream
       q = nullptr;
       return;
     }
