@@ -73,9 +73,14 @@ struct RP {
   uint64_t* cand;      // per window position
   uint64_t* chunkmin;  // per block (positions [WPB*b, WPB*b+WPB))
   uint32_t* chunkflag; // per block: a segment starts inside the chunk
-  uint32_t* segpos;    // per window position: segment (image) of its column
+  uint32_t* segpos;    // per window position: its warp group (positions of a group are contiguous)
   uint32_t seg_cells;  // cells per segment (batched images), 0: one segment
-  unsigned* lo_buf;    // [2]
+  const uint32_t* seg_off;  // nseg + 1 column offsets (columns are grouped by segment)
+  uint32_t nseg;
+  uint32_t G;          // warps per group; group g reduces segments g, g + ngroups, ...
+  uint32_t ngroups;
+  unsigned* lo_buf;    // [2 * ngroups]: next window start of each group (double-buffered)
+  unsigned* done_buf;  // [2]: groups with no segment left (double-buffered)
   uint64_t* rec;
   unsigned long long* nrec;
   int* err;
@@ -733,14 +738,25 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
   const SpecLane sl = spec_lane(P.g, lane);
   c.F[0] = s_F[wib][0];
   c.F[1] = s_F[wib][1];
-  uint32_t j = w;
+  // Warp groups: group grp (G warps, window positions [grp*G, grp*G + G)) reduces the segments
+  // grp, grp + ngroups, ... one after the other; segments (images of a batch) are independent
+  // complexes, so each has its own window and the groups progress concurrently.  One image:
+  // one group of all W warps.  Warps beyond ngroups * G stay idle.
+  const uint32_t G = P.G, grp = w / G, k = w - grp * G;
+  uint32_t seg = grp < P.ngroups ? grp : P.nseg;
+  uint32_t lo = seg < P.nseg ? __ldg(P.seg_off + seg) : P.ncols;
+  uint32_t end = seg < P.nseg ? __ldg(P.seg_off + seg + 1) : P.ncols;
+  uint32_t j = lo + k;
   bool started = false, fin = false;
-  uint32_t lo = 0;
+  if (lane == 0) {
+    P.segpos[w] = grp < P.ngroups ? grp : 0xFFFFFFFFu;  // idle positions: a segment of their own
+    P.cand[w] = NONE64;
+  }
 
   for (uint32_t round = 0;; ++round) {
     // ---------------- phase A: advance my column
     if (fin && j < lo) {
-      j += W;
+      j += G;
       started = false;
       fin = false;
     }
@@ -748,7 +764,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
     bool ready = false;
     const long long pa0 = P.rdbg ? clock64() : 0;
     int dbg_steps = -1;
-    if (j < P.ncols && !fin) {
+    if (j < end && !fin) {
       if (!started) {
         started = true;
         c.mb = c.fb = 0;
@@ -855,14 +871,11 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
       P.rdbg[4ull * round + 3] = tnow;
     }
-    // publish at my window position (every position is owned by exactly one warp), with the
-    // segment (image of a batch) of the column: columns of different images never interact, so
-    // a column is blocked only by unfinished earlier columns of its own segment
+    // publish at my window position (every position of a group's window is owned by exactly one
+    // of its warps); a column is blocked only by unfinished earlier columns of its own window
     const uint32_t q = j - lo;
-    if (lane == 0 && q < W) {
-      P.cand[q] = (j < P.ncols && !fin) ? cval : NONE64;
-      P.segpos[q] = (j < P.ncols && P.seg_cells) ? key_kidx(P.cols[j]) / P.seg_cells : 0xFFFFFFFFu;
-    }
+    const uint32_t qg = grp * G + q;
+    if (lane == 0 && grp < P.ngroups && q < G) P.cand[qg] = (j < end && !fin) ? cval : NONE64;
     grid.sync();
 
     // ---------------- phase B: segmented minima of the window's chunks of WPB positions
@@ -903,12 +916,12 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
       }
     }
     __syncthreads();
-    if (j < P.ncols && !fin && ready && q < W) {
-      const uint32_t chunk = q / WPB;
+    if (j < end && !fin && ready && q < G) {
+      const uint32_t chunk = qg / WPB;
       uint64_t prefix = s_pref[chunk];
-      for (uint32_t k = chunk * WPB; k <= q; ++k) {
-        if (k == 0 || __ldcg(P.segpos + k) != __ldcg(P.segpos + k - 1)) prefix = NONE64;
-        if (k < q) prefix = min(prefix, ldcg64(P.cand + k));
+      for (uint32_t kk = chunk * WPB; kk <= qg; ++kk) {
+        if (kk == 0 || __ldcg(P.segpos + kk) != __ldcg(P.segpos + kk - 1)) prefix = NONE64;
+        if (kk < qg) prefix = min(prefix, ldcg64(P.cand + kk));
       }
       if (cval < prefix) {
         const uint32_t L = c.len();
@@ -933,18 +946,35 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         }
       }
     }
-    // next lo = min(first unfinished window column, lo + W)
-    if (lane == 0 && j < P.ncols && !fin) atomicMin(P.lo_buf + ((round + 1) & 1), j);
+    // next lo of my group = min(first unfinished window column, lo + G, end of the segment)
+    const unsigned nxt = ((round + 1) & 1) * P.ngroups, cur = (round & 1) * P.ngroups;
+    if (grp < P.ngroups) {
+      if (lane == 0 && j < end && !fin) atomicMin(P.lo_buf + nxt + grp, j);
+      if (k == 0 && lane == 0) {
+        const uint64_t nl = uint64_t(lo) + G;
+        atomicMin(P.lo_buf + nxt + grp, unsigned(nl < end ? nl : end));
+        P.lo_buf[cur + grp] = NONE32;
+        if (seg >= P.nseg) atomicAdd(P.done_buf + ((round + 1) & 1), 1u);
+      }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      const uint64_t nl = uint64_t(lo) + W;
-      atomicMin(P.lo_buf + ((round + 1) & 1), unsigned(nl < P.ncols ? nl : P.ncols));
-      P.lo_buf[round & 1] = NONE32;
+      P.done_buf[round & 1] = 0;
       atomicAdd(P.stats, 1ull);
     }
     grid.sync();
-    lo = __ldcg(P.lo_buf + ((round + 1) & 1));
-    if (lo >= P.ncols) break;
+    if (__ldcg(P.done_buf + ((round + 1) & 1)) >= P.ngroups) break;
     if (__ldcg(P.err)) break;
+    if (grp < P.ngroups && seg < P.nseg) {
+      lo = __ldcg(P.lo_buf + nxt + grp);
+      if (lo >= end) {  // segment done: the group moves on to its next one
+        seg += P.ngroups;
+        lo = seg < P.nseg ? __ldg(P.seg_off + seg) : P.ncols;
+        end = seg < P.nseg ? __ldg(P.seg_off + seg + 1) : P.ncols;
+        j = lo + k;
+        started = false;
+        fin = false;
+      }
+    }
   }
 }
 
@@ -980,6 +1010,20 @@ __global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32
   if (i < n) segk[i] = key_kidx(cols[i]) / seg_cells;
 }
 
+// seg_off[t] = first position i with segk[i] >= t (segk sorted ascending), t = 0..nseg
+__global__ void k_seg_offsets(const uint32_t* __restrict__ segk, unsigned n, unsigned nseg,
+                              uint32_t* __restrict__ seg_off) {
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > nseg) return;
+  unsigned a = 0, b = n;
+  while (a < b) {
+    const unsigned m = (a + b) >> 1;
+    if (segk[m] < t) a = m + 1;
+    else b = m;
+  }
+  seg_off[t] = a;
+}
+
 __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint8_t* tags) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1008,6 +1052,8 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
   st.columns[d] = ncols;
   if (ncols > 0) {
     sort_keys_u64(cols, ncols, /*descending=*/true, 64, ws);
+    unsigned nseg = 1;
+    uint32_t* seg_off = nullptr;
     if (S.seg_cells) {
       // batched images: group the columns by image (stable, so each image keeps its decreasing
       // key order); images are independent complexes, so their relative order is immaterial
@@ -1025,6 +1071,15 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       if (dv.Current() != cols)
         CR_CUDA(cudaMemcpyAsync(cols, dv.Current(), ncols * sizeof(uint64_t),
                                 cudaMemcpyDeviceToDevice, s));
+      nseg = unsigned((uint64_t(g.ncells) + S.seg_cells - 1) / S.seg_cells);
+      seg_off = ws.alloc<uint32_t>(nseg + 1);
+      k_seg_offsets<<<grid_for(nseg + 1, B), B, 0, s>>>(dk.Current(), ncols, nseg, seg_off);
+      CR_CHECK_LAUNCH();
+    } else {
+      seg_off = ws.alloc<uint32_t>(2);
+      const uint32_t h[2] = {0u, ncols};
+      CR_CUDA(cudaMemcpyAsync(seg_off, h, sizeof(h), cudaMemcpyHostToDevice, s));
+      CR_CUDA(cudaStreamSynchronize(s));  // h is on the stack
     }
 
     int dev = 0, nsm = 0, per_sm = 0;
@@ -1044,7 +1099,9 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     uint64_t* chunkmin = ws.alloc<uint64_t>(blocks);
     uint32_t* chunkflag = ws.alloc<uint32_t>(blocks);
     uint32_t* segpos = ws.alloc<uint32_t>(W);
-    unsigned* lo_buf = reinterpret_cast<unsigned*>(ctr + 2);
+    const uint32_t ngroups = nseg < W ? nseg : W, G = W / ngroups;
+    unsigned* lo_buf = ws.alloc<unsigned>(2 * int64_t(ngroups));
+    unsigned* done_buf = reinterpret_cast<unsigned*>(ctr + 2);
     int* err = reinterpret_cast<int*>(ctr + 3);
     unsigned long long* nrec = ctr + 4;
     unsigned long long* pool_top = ctr + 5;
@@ -1066,7 +1123,8 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       if (!work) work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
       CR_CUDA(cudaMemsetAsync(owninfo, 0xFF, g.ncells * sizeof(uint64_t), s));
-      CR_CUDA(cudaMemsetAsync(lo_buf, 0xFF, 2 * sizeof(unsigned), s));
+      CR_CUDA(cudaMemsetAsync(lo_buf, 0xFF, 2 * sizeof(unsigned) * ngroups, s));
+      CR_CUDA(cudaMemsetAsync(done_buf, 0, 2 * sizeof(unsigned), s));
       CR_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
       CR_CUDA(cudaMemsetAsync(nrec, 0, 6 * sizeof(unsigned long long), s));
       RP P;
@@ -1090,6 +1148,11 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.segpos = segpos;
       P.seg_cells = S.seg_cells;
       P.lo_buf = lo_buf;
+      P.done_buf = done_buf;
+      P.seg_off = seg_off;
+      P.nseg = nseg;
+      P.G = G;
+      P.ngroups = ngroups;
       P.rec = S.R.rec[d];
       P.nrec = nrec;
       P.err = err;
