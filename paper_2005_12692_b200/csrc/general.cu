@@ -2126,6 +2126,35 @@ __global__ void k_partner_records(const uint64_t* __restrict__ rec, int64_t n,
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
+// Dimensions 1..dmax after H0: dimension 1 by the cohomology reduction, whose
+// pivots clear dimension 2, then the top dimension by duality.  Alternative (CR_K5_HOM=1, 3D):
+// the top dimension 2 by duality first (it needs no clearing), then dimension 1 by the HOMOLOGY
+// reduction of the square columns with the clearing of the squares that create a 2-class (the
+// twist).  Its reduced columns are 1-cycles: on C4 the entry work halves (210 M -> 115 M entries,
+// heaviest column 55 M -> 10.6 M) but the additions grow (423 k -> 545 k) and the critical chain
+// of dependent additions is as long (366 vs 363 rounds): 168 vs 174 ms, C5 1.63 vs 1.76 s, so
+// cohomology stays the default.  Both give the same pairing (unique given reading R1).
+void reduce_dims(GeneralState& S, const Geom& g, int dmax, Workspace& ws, HostScalars& hs,
+                 cr_stats& st) {
+  static const char* names[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
+  cudaStream_t s = ws.stream();
+  const char* e = std::getenv("CR_K5_HOM");
+  const bool hom1 = g.D == 3 && dmax >= 1 && use_dual(g, 2) && e && e[0] == '1';
+  if (hom1) {
+    if (!top_dual(S, 2, ws, hs, st, 0xFFFFFFFFu)) throw Error{CR_EINTERNAL, "top dimension"};
+    prof_mark(s, names[2]);
+    mark_cleared_births(S, 2, ws);
+    reduce_dimension(S, 1, ws, hs, st, /*hom=*/true);
+    prof_mark(s, names[1]);
+    return;
+  }
+  for (int d = 1; d <= dmax; ++d) {
+    if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, dual_max_basins())))
+      reduce_dimension(S, d, ws, hs, st);
+    prof_mark(s, names[d]);
+  }
+}
+
 void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, HostScalars& hs,
                  GeneralState& S, cr_stats& st) {
   cudaStream_t s = ws.stream();
@@ -2306,12 +2335,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     ws.release(cand);
     ws.release(cand2);
     ws.release(parent);
-    static const char* names1[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
-    for (int d = 1; d <= dmax; ++d) {
-      if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, dual_max_basins())))
-        reduce_dimension(S, d, ws, hs, st);
-      prof_mark(s, names1[d]);
-    }
+    reduce_dims(S, g, dmax, ws, hs, st);
     return;
   }
   unsigned long long* best = ws.alloc<unsigned long long>(g.nvox);
@@ -2347,12 +2371,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   ws.release(alive);
   ws.release(parent);
 
-  static const char* names[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
-  for (int d = 1; d <= dmax; ++d) {
-    if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, dual_max_basins())))
-      reduce_dimension(S, d, ws, hs, st);
-    prof_mark(s, names[d]);
-  }
+  reduce_dims(S, g, dmax, ws, hs, st);
 }
 
 int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out_cells,

@@ -29,7 +29,12 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
                  GeneralState& S, cr_stats& st);
 
 // Residual column reduction of dimension d (reduce.cu).  Appends records to R.rec[d].
-void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st);
+// hom = false: cohomology (columns = d-cells, coboundaries, decreasing order; marks the pivots
+// cleared for dimension d+1).  hom = true: homology (columns = (d+1)-cells, boundaries, increasing
+// order), which needs the dimension-(d+1) births cleared first (mark_cleared_births(S, d+1)).
+void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st,
+                      bool hom = false);
+void mark_cleared_births(GeneralState& S, int d, Workspace& ws);
 
 // Records (dims 0..maxdim) -> bars with death > birth plus essentials, ordered (dim, birth kidx).
 // Writes at most cap entries; returns the count needed.

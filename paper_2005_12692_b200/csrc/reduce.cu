@@ -59,6 +59,7 @@ struct RP {
   Geom g;
   FastDiv fx, fxy;  // by KX and by KX*KY: Khalimsky coordinates of a kidx
   int d;
+  int hom;             // 1: homology mode (columns = (d+1)-cells by boundary, keys complemented)
   const uint64_t* cols;
   uint32_t ncols;
   const uint32_t* births;
@@ -104,7 +105,19 @@ __device__ __forceinline__ uint64_t ld64(const uint64_t* p) {
   return G ? ldcg64(p) : *p;
 }
 
-// Finite cofacets of cell s, sorted ascending, written to dst (<= 6 entries).  Warp-collective.
+// Keys of the working columns.  Cohomology: (ord << 32 | kidx), pivot = min.  Homology mode: the
+// complement ~(ord << 32 | kidx), so that the min-pivot machinery below takes the MAX (latest)
+// face as the pivot and processes columns in increasing filtration order (decreasing ~key).
+__device__ __forceinline__ uint64_t rkey(const RP& P, uint32_t b, uint32_t k) {
+  const uint64_t x = make_key(b, k);
+  return P.hom ? ~x : x;
+}
+__device__ __forceinline__ uint32_t rkid(const RP& P, uint64_t key) {
+  return P.hom ? ~uint32_t(key) : uint32_t(key);
+}
+
+// The column of cell s, sorted ascending (by rkey), written to dst (<= 6 entries): its finite
+// cofacets (cohomology), or its facets (homology mode).  Warp-collective.
 __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
   const Geom& g = P.g;
   const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
@@ -114,11 +127,11 @@ __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane)
   uint64_t key = NONE64;
   if (lane < 6) {
     const int a = lane >> 1, sg = lane & 1;
-    if (!(c[a] & 1) && (sg ? c[a] + 1 < ext[a] : c[a] > 0)) {
+    if ((P.hom ? (c[a] & 1) : !(c[a] & 1)) && (sg ? c[a] + 1 < ext[a] : c[a] > 0)) {
       const int64_t stv = g.stride(a);
       const uint32_t t = uint32_t(int64_t(s) + (sg ? stv : -stv));
       const uint32_t tb = __ldg(P.births + t);
-      if (tb != ABSENT_ORD) key = make_key(tb, t);
+      if (tb != ABSENT_ORD) key = rkey(P, tb, t);
     }
   }
   const unsigned valid = __ballot_sync(0xFFFFFFFFu, key != NONE64);
@@ -387,17 +400,22 @@ struct Spec {
 // direction f.  The member exists iff t's axis a is odd, the checked axis `chk` stays inside the
 // grid after moving by `dchk`, and (members 1-4) axis b is even in t.
 struct SpecLane {
-  int a, chk, dchk;
-  bool need_b_even;
-  uint32_t off;  // cell - t (two's complement)
+  int a, chk, dchk, sa;
+  bool need_b_even;  // (homology mode: axis b must be odd in the pivot)
+  uint32_t off;      // cell - t (two's complement)
   bool active;
+  bool hom;
 };
-__device__ __forceinline__ SpecLane spec_lane(const Geom& g, int lane) {
-  SpecLane L{0, 0, 0, false, 0u, false};
+// Homology mode mirrors it: an UP pivot e (a d-cell) is the lower cell of an apparent pair
+// (e, s') with s' = e + e_dir a cofacet; the column adds del(s') = {e} + the other facets of s':
+// member 0 is e + 2 e_dir, members 1-4 are s' -/+ e_b for the other axes b odd in e.
+__device__ __forceinline__ SpecLane spec_lane(const Geom& g, int lane, bool hom) {
+  SpecLane L{0, 0, 0, 0, false, 0u, false, hom};
   if (lane >= 30) return L;
   const int f = lane / 5, m = lane % 5;
   L.a = f >> 1;
   const int sa = (f & 1) ? 1 : -1;
+  L.sa = sa;
   L.active = true;
   if (m == 0) {
     L.chk = L.a;
@@ -422,17 +440,22 @@ __device__ __forceinline__ Spec spec_issue(const RP& P, const SpecLane& L, uint3
   const uint32_t ec = L.chk == 0 ? KX : (L.chk == 1 ? KY : uint32_t(P.g.KZ));
   const uint32_t moved = cc + uint32_t(L.dchk);  // wraps below 0 to a huge value
   Spec r{0u, ABSENT_ORD};
-  if (L.active && (ca & 1) && moved < ec && !(L.need_b_even && (cc & 1))) {
+  const bool up_axis = L.hom ? !(ca & 1) : (ca & 1);  // t on the pivot side of axis a
+  const bool b_bad = L.need_b_even && (L.hom ? !(cc & 1) : (cc & 1));
+  // homology: t is even along a and may sit on the border; the partner t + sa e_a must exist
+  const uint32_t ea = L.a == 0 ? KX : (L.a == 1 ? KY : uint32_t(P.g.KZ));
+  const bool a_ok = !L.hom || ca + uint32_t(L.sa) < ea;
+  if (L.active && up_axis && a_ok && moved < ec && !b_bad) {
     r.cell = t + L.off;
     r.birth = __ldg(P.births + r.cell);
   }
   return r;
 }
 // delta(s') sorted ascending into dst (<= 6 entries) for the partner direction dir; warp-collective.
-__device__ __forceinline__ uint32_t spec_finish(const Spec& sp, int dir, uint64_t piv,
+__device__ __forceinline__ uint32_t spec_finish(const RP& P, const Spec& sp, int dir, uint64_t piv,
                                                 uint64_t* dst, int lane) {
   uint64_t key = NONE64;
-  if (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD) key = make_key(sp.birth, sp.cell);
+  if (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD) key = rkey(P, sp.birth, sp.cell);
   if (lane == 31) key = piv;
   const unsigned vm = __ballot_sync(0xFFFFFFFFu, key != NONE64);
   int rank = 0;
@@ -735,7 +758,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
 
   Col c;
   uint64_t* const slot = P.work + uint64_t(w) * 2 * P.mcap;
-  const SpecLane sl = spec_lane(P.g, lane);
+  const SpecLane sl = spec_lane(P.g, lane, P.hom != 0);
   c.F[0] = s_F[wib][0];
   c.F[1] = s_F[wib][1];
   // Warp groups: group grp (G warps, window positions [grp*G, grp*G + G)) reduces the segments
@@ -776,7 +799,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         c.rv = NONE64;
         c.nr = c.r0 = 0;
         c.mstale = true;
-        c.nf = coboundary(P, key_kidx(P.cols[j]), c.F[0], lane);
+        c.nf = coboundary(P, rkid(P, P.cols[j]), c.F[0], lane);
       }
       int steps = 0;
       unsigned long long adds = 0, addlen = 0, cl = 0, ca = 0, cp = 0;
@@ -786,7 +809,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         const long long tl0 = P.debug ? clock64() : 0;
         const uint64_t piv = take_pivot(c, lane);
         if (piv == NONE64) break;
-        const uint32_t pk = key_kidx(piv);
+        const uint32_t pk = rkid(P, piv);
         // independent loads: the speculated partner coboundary, the tag, the owner record
         const Spec sp = spec_issue(P, sl, pk);
         const uint8_t t = __ldg(P.tags + pk);
@@ -794,9 +817,10 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         const uint64_t* add;
         uint32_t alen;
         bool glob;
-        if (tag_kind(t) == KIND_DOWN) {
+        if (tag_kind(t) == (P.hom ? KIND_UP : KIND_DOWN)) {
           // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
-          alen = spec_finish(sp, tag_dir(t), piv, s_small[wib], lane);
+          // (homology: the lower cell of (pivot, s'): add del(s'))
+          alen = spec_finish(P, sp, tag_dir(t), piv, s_small[wib], lane);
           add = s_small[wib];
           glob = false;
         } else {
@@ -855,8 +879,12 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
       if (ok && !ready && cval == NONE64) {  // zero column: essential (exact given clearing)
         fin = true;
         if (lane == 0) {
-          const unsigned long long r = atomicAdd(P.nrec, 1ull);
-          P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | NONE32;
+          if (P.hom) {
+            atomicOr(P.err, 8);  // homology: every column left after the clearing is nonzero
+          } else {
+            const unsigned long long r = atomicAdd(P.nrec, 1ull);
+            P.rec[r] = (uint64_t(rkid(P, P.cols[j])) << 32) | NONE32;
+          }
         }
       }
     }
@@ -938,9 +966,11 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
           if (lane == 0) {
             if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
             __threadfence();
-            P.owninfo[key_kidx(cval)] = (uint64_t(off) << OI_LEN_BITS) | n;
+            P.owninfo[rkid(P, cval)] = (uint64_t(off) << OI_LEN_BITS) | n;
             const unsigned long long r = atomicAdd(P.nrec, 1ull);
-            P.rec[r] = (uint64_t(key_kidx(P.cols[j])) << 32) | key_kidx(cval);
+            // (birth cell, death cell): cohomology (column, pivot), homology (pivot, column)
+            const uint64_t cc = rkid(P, P.cols[j]), pc = rkid(P, cval);
+            P.rec[r] = P.hom ? ((pc << 32) | cc) : ((cc << 32) | pc);
           }
           fin = true;
         }
@@ -979,7 +1009,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
 }
 
 __global__ void k_collect_columns(const uint32_t* __restrict__ births,
-                                  const uint8_t* __restrict__ tags, Geom g, int d,
+                                  const uint8_t* __restrict__ tags, Geom g, int d, int hom,
                                   uint64_t* __restrict__ cols, unsigned* __restrict__ ncols) {
   int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   bool emit = false;
@@ -992,7 +1022,7 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
     uint32_t b = births[k];
     if (dim == d && b != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
       emit = true;
-      key = make_key(b, k);
+      key = hom ? ~make_key(b, k) : make_key(b, k);
     }
   }
   unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
@@ -1005,9 +1035,33 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
 }
 
 __global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32_t seg_cells,
-                           uint32_t* __restrict__ segk) {
+                           int hom, uint32_t* __restrict__ segk) {
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) segk[i] = key_kidx(cols[i]) / seg_cells;
+  if (i < n) segk[i] = (hom ? ~key_kidx(cols[i]) : key_kidx(cols[i])) / seg_cells;
+}
+
+// Homology mode, after the reduction: a residual d-cell (not apparent, not cleared as a death
+// cell of dimension d-1) that is no column's pivot is an essential class (birth, +inf).
+__global__ void k_hom_essential(const uint32_t* __restrict__ births,
+                                const uint8_t* __restrict__ tags, Geom g, int d,
+                                const uint64_t* __restrict__ owninfo, uint64_t* rec,
+                                unsigned long long* nrec) {
+  const int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (kk >= g.ncells) return;
+  const uint32_t k = uint32_t(kk);
+  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
+  const uint32_t X = k % KX, r = k / KX, Y = r % KY, Z = r / KY;
+  if (int((X & 1) + (Y & 1) + (Z & 1)) != d) return;
+  if (births[k] == ABSENT_ORD || tag_kind(tags[k]) != KIND_RESIDUAL) return;
+  if (owninfo && ldcg64(owninfo + k) != NONE64) return;
+  rec[atomicAdd(nrec, 1ull)] = (uint64_t(k) << 32) | NONE32;
+}
+
+// Clearing for the homology mode: the birth cells of dimension-(d+1) records (cells that create a
+// class, paired with a (d+2)-cell or essential) have zero reduced boundary columns.
+__global__ void k_mark_cleared_birth(const uint64_t* __restrict__ rec, int64_t n, uint8_t* tags) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) tags[uint32_t(rec[i] >> 32)] = make_tag(KIND_CLEARED, 0);
 }
 
 // seg_off[t] = first position i with segk[i] >= t (segk sorted ascending), t = 0..nseg
@@ -1033,20 +1087,23 @@ __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint
 
 }  // namespace
 
-void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st) {
+void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st,
+                      bool hom) {
   cudaStream_t s = ws.stream();
   const Geom& g = S.g;
   const int B = 256;
-  const int64_t nd = st.cells[d];
-  S.R.rec[d] = ws.alloc<uint64_t>(nd);
+  const int dc = hom ? d + 1 : d;  // dimension of the column cells
+  const int64_t nd = st.cells[dc];
+  // records: at most one per column, plus (homology) the essential d-cells
+  S.R.rec[d] = ws.alloc<uint64_t>(nd + (hom ? st.cells[d] : 0) + 1);
   S.R.n[d] = 0;
-  if (nd == 0) return;
+  if (nd == 0 && !hom) return;
 
   unsigned long long* ctr = ws.alloc<unsigned long long>(16);
   CR_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
-  uint64_t* cols = ws.alloc<uint64_t>(nd);
-  k_collect_columns<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, cols,
-                                                        reinterpret_cast<unsigned*>(ctr));
+  uint64_t* cols = ws.alloc<uint64_t>(nd + 1);
+  k_collect_columns<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, dc, hom ? 1 : 0,
+                                                        cols, reinterpret_cast<unsigned*>(ctr));
   CR_CHECK_LAUNCH();
   const unsigned ncols = read_scalar(reinterpret_cast<unsigned*>(ctr), s, hs);
   st.columns[d] = ncols;
@@ -1060,7 +1117,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       uint32_t* segk = ws.alloc<uint32_t>(ncols);
       uint32_t* segk2 = ws.alloc<uint32_t>(ncols);
       uint64_t* cols2 = ws.alloc<uint64_t>(ncols);
-      k_seg_keys<<<grid_for(ncols, B), B, 0, s>>>(cols, ncols, S.seg_cells, segk);
+      k_seg_keys<<<grid_for(ncols, B), B, 0, s>>>(cols, ncols, S.seg_cells, hom ? 1 : 0, segk);
       CR_CHECK_LAUNCH();
       cub::DoubleBuffer<uint32_t> dk(segk, segk2);
       cub::DoubleBuffer<uint64_t> dv(cols, cols2);
@@ -1132,6 +1189,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.fx = FastDiv::make(uint32_t(g.KX));
       P.fxy = FastDiv::make(uint32_t(g.KX * g.KY));
       P.d = d;
+      P.hom = hom ? 1 : 0;
       P.cols = cols;
       P.ncols = ncols;
       P.births = S.births;
@@ -1190,6 +1248,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
                 mcap, pool_cap);
       if (e == 0) break;
       if (e & 4) throw Error{CR_EINTERNAL, "reduced column longer than 2^24 entries"};
+      if (e & 8) throw Error{CR_EINTERNAL, "homology reduction: a column reduced to zero"};
       if (attempt > 12) throw Error{CR_ENOMEM, "reduction buffers exhausted"};
       if (e & 2) {
         ws.release(pool);
@@ -1260,15 +1319,33 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
               "cyc_pool %llu cyc_app %llu cyc_lookup %llu W %u\n",
               d, ncols, hs.p[6], hs.p[7], hs.p[10], hs.p[11], hs.p[13], hs.p[14], hs.p[15], W);
     }
+    if (hom) {
+      k_hom_essential<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, owninfo,
+                                                         S.R.rec[d], ctr + 4);
+      CR_CHECK_LAUNCH();
+      S.R.n[d] = int64_t(read_scalar(ctr + 4, s, hs));
+    }
     ws.release(work);
     ws.release(pool);
     ws.release(owninfo);
+  } else if (hom) {
+    k_hom_essential<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, nullptr,
+                                                       S.R.rec[d], ctr + 4);
+    CR_CHECK_LAUNCH();
+    S.R.n[d] = int64_t(read_scalar(ctr + 4, s, hs));
   }
-  if (S.R.n[d] > 0) {
+  if (S.R.n[d] > 0 && !hom) {
     k_mark_cleared<<<grid_for(S.R.n[d], B), B, 0, s>>>(S.R.rec[d], S.R.n[d], S.tags);
     CR_CHECK_LAUNCH();
   }
   ws.release(cols);
+}
+
+void mark_cleared_births(GeneralState& S, int d, Workspace& ws) {
+  if (S.R.n[d] <= 0) return;
+  k_mark_cleared_birth<<<grid_for(S.R.n[d], 256), 256, 0, ws.stream()>>>(S.R.rec[d], S.R.n[d],
+                                                                          S.tags);
+  CR_CHECK_LAUNCH();
 }
 
 }  // namespace cr

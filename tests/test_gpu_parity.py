@@ -154,6 +154,40 @@ def _cavity_cases():
     return {"hole2d": a, "holes2d": b, "void3d": c, "tunnel3d": d, "fuzz3d": e, "fuzz2d": f}
 
 
+def test_dim1_homology_vs_cohomology(cr, monkeypatch):
+    """3D dimension 1 by the cohomology reduction of edge columns (default) and by the homology
+    reduction of square columns after the top dimension (CR_K5_HOM=1) give the oracle's bars and
+    pairing, incl. essential H1 bars (tunnels through +inf), H1-only requests (maxdim=1) and
+    batches."""
+    import torch
+    cases = _cavity_cases()
+    imgs = [cases["tunnel3d"], cases["void3d"], cases["fuzz3d"],
+            gen.masked_grf((26, 30, 28), 2.0, 13.0, 61),
+            gen.small_int_image((12, 14, 11), 3, seed=62, inf_frac=0.08)]
+    for k, img in enumerate(imgs):
+        t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        p_coh = cr.pairing(t).cpu().numpy()
+        monkeypatch.setenv("CR_K5_HOM", "1")
+        for md in (1, 2):
+            check_image(cr, img, md, partner=(md == 2), ctx=(k, md))
+        p_hom = cr.pairing(t).cpu().numpy()
+        monkeypatch.delenv("CR_K5_HOM")
+        assert np.array_equal(p_hom, p_coh), k
+    vols = np.stack([gen.masked_grf((14, 15, 13), 1.5, 6.5, 70 + i) for i in range(5)])
+    t = torch.from_numpy(vols).cuda()
+    bc2, offs2 = cr.barcodes_batched(t, 2)
+    monkeypatch.setenv("CR_K5_HOM", "1")
+    bc, offs = cr.barcodes_batched(t, 2)
+    assert np.array_equal(np.asarray(bc.pairs.cpu()), np.asarray(bc2.pairs.cpu()))
+    assert np.array_equal(offs.cpu().numpy(), offs2.cpu().numpy())
+    for i in range(len(vols)):  # and each image's bars are the oracle's
+        o = oracle.ph(vols[i], 2)
+        a, b = int(offs[i]), int(offs[i + 1])
+        d, bi, de, _ = bc.numpy()
+        got = sorted(zip(d[a:b].tolist(), bi[a:b].tolist(), de[a:b].tolist()))
+        assert got == sorted(zip(o.dim.tolist(), o.birth.tolist(), o.death.tolist())), i
+
+
 @pytest.mark.parametrize("name", sorted(_cavity_cases()))
 def test_topdim_duality(cr, monkeypatch, name):
     """The top dimension by Alexander duality gives the oracle's bars and the

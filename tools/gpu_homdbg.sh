@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+CR_DEBUG_STATS=1 timeout 900 python tools/gpu_general_stats.py c4 > gpurun_out/homdbg.log 2>&1; echo a=$?
