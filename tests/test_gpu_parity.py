@@ -539,3 +539,31 @@ def test_barcodes_f64_iid_and_specials(cr):
         cr.barcodes_f64(torch.tensor([1.0, float("nan")], dtype=torch.float64).cuda(), 0)
     with pytest.raises(TypeError):
         cr.barcodes_f64(torch.zeros(4, device="cuda"), 0)
+
+
+def test_stats_counters_match_definitions(cr, monkeypatch):
+    """The pairing-determined counters of cr_stats equal their definitions:
+    finite cells and apparent (UP) cells per dimension and the H0 basins from tests/apparent.py,
+    bars per dimension from the oracle -- for the fused K1+K2 kernel and the former pair."""
+    import torch
+    import apparent as ap
+    imgs = [gen.masked_grf((23, 27, 31), 2.0, 11.0, 81),
+            gen.small_int_image((9, 40, 33), 3, seed=82, inf_frac=0.1),
+            gen.iid_uniform((61, 47), seed=83),
+            gen.small_int_image((50, 45), 5, seed=84, inf_frac=0.05)]
+    for k, img in enumerate(imgs):
+        exp = ap.counts(img)
+        o = oracle.ph(img, img.ndim - 1)
+        t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        for var in ("", "CR_K12_OLD"):
+            if var:
+                monkeypatch.setenv(var, "1")
+            cr.barcodes(t, img.ndim - 1)
+            st = cr.last_stats()
+            assert list(st["cells"]) == exp["cells"], (k, var, st["cells"], exp["cells"])
+            assert list(st["apparent"])[:3] == exp["apparent"][:3], (k, var, st["apparent"], exp)
+            assert st["columns"][0] == exp["basins"], (k, var, st["columns"][0], exp["basins"])
+            nb = [int(np.count_nonzero(o.dim == d)) for d in range(img.ndim)]
+            assert list(st["pairs"])[:img.ndim] == nb, (k, var, st["pairs"], nb)
+            if var:
+                monkeypatch.delenv(var)

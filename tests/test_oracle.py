@@ -354,3 +354,33 @@ def test_f64_births_and_invalid():
     a = oracle.ph(np.array([-0.0, 1.0, 0.0]), 0, partner=True, dtype=np.float64)
     b = oracle.ph(np.array([0.0, 1.0, 0.0]), 0, partner=True, dtype=np.float64)
     assert np.array_equal(a.partner, b.partner)
+
+
+# ---------------------------------------------------------------- apparent pairs
+
+def test_apparent_pairs_in_oracle_pairing():
+    """Every apparent pair by its definition (tests/apparent.py) is a pair of the
+    oracle's full pairing with death == birth (App. A.4), on random 1D/2D/3D images with +inf
+    masks and ties; the per-dimension finite-cell counts match the closed-form grid counts."""
+    import apparent as ap
+    rng = np.random.default_rng(4545)
+    for t in range(120):
+        nd = int(rng.integers(1, 4))
+        shape = tuple(int(s) for s in rng.integers(1, 8 if nd < 3 else 5, size=nd))
+        img = gen.small_int_image(shape, 4, seed=int(rng.integers(1 << 30)),
+                                  inf_frac=0.15 if t % 3 == 0 else 0.0)
+        o = oracle.ph(img, 2, partner=True)
+        b = ap.khalimsky_births(img).ravel()
+        for s, u in ap.pairs_up(img):
+            assert o.partner[s] == u and o.partner[u] == s, (t, shape, s, u)
+            assert b[s] == b[u], (t, s, u)
+        if not np.isinf(img).any():
+            c = ap.counts(img)["cells"]
+            full = [1, 1, 1]
+            full[3 - nd:] = shape
+            nz, ny, nx = full
+            exp = [nz * ny * nx,
+                   (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1),
+                   (nx - 1) * (ny - 1) * nz + (nx - 1) * ny * (nz - 1) + nx * (ny - 1) * (nz - 1),
+                   (nx - 1) * (ny - 1) * (nz - 1)]
+            assert c == exp, (shape, c, exp)
