@@ -1,9 +1,13 @@
 // general.cu -- the general (1D/2D/3D, one image) path: K1 filtration, K2 apparent pairs,
 // K4 dimension-0 pairing (union-find with the elder rule), bar/partner emission.
 // The dims >= 1 reduction (K5) is in reduce.cu.
+#include <cooperative_groups.h>
+
 #include <cub/cub.cuh>
 
 #include "pipeline.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace cr {
 
@@ -1930,6 +1934,140 @@ __global__ void k_dual_mm_commit(const Cand* cand, unsigned n, const uint32_t* _
   alive[i] = 2;
 }
 
+// All merge rounds (H0 or the dual) in one cooperative launch: the phases of k_mm_find,
+// k_mm_commit / k_dual_mm_commit and k_mm_reset separated by grid syncs, looping on the device
+// until no candidate is left -- instead of three launches, a memset and a host round trip per
+// round (C1: 14 rounds cost ~35 us each on the host path).  Same per-edge logic, so the same
+// commits in the same rounds.  ctl: [0]/[1] survivor counters (double-buffered), [2] rounds.
+struct MMArgs {
+  Cand* cur;
+  Cand* nxt;
+  unsigned n;
+  uint32_t* parent;
+  unsigned long long* best;
+  uint8_t* alive;
+  const uint32_t* births;
+  Geom g;
+  DualG G;
+  uint8_t* tags;
+  uint64_t* rec;
+  unsigned long long* nrec;
+  unsigned* ctl;
+};
+template <bool DUAL>
+__global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  const unsigned gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  Cand* cur = A.cur;
+  Cand* nxt = A.nxt;
+  unsigned n = A.n, rounds = 0;
+  while (n > 0) {
+    for (unsigned i = gt; i < n; i += gs) {  // find
+      Cand c = cur[i];
+      const uint32_t a = uf_find(A.parent, c.a), b = uf_find(A.parent, c.b);
+      cur[i].a = a;
+      cur[i].b = b;
+      if (a == b) {
+        A.alive[i] = 0;
+        continue;
+      }
+      A.alive[i] = 1;
+      atomicMin(A.best + a, (unsigned long long)c.key);
+      atomicMin(A.best + b, (unsigned long long)c.key);
+    }
+    grid.sync();
+    for (unsigned i = gt; i < n; i += gs) {  // commit (see k_mm_commit / k_dual_mm_commit)
+      if (!A.alive[i]) continue;
+      const Cand c = cur[i];
+      const bool min_a = A.best[c.a] == c.key, min_b = A.best[c.b] == c.key;
+      if (!min_a && !min_b) continue;
+      uint64_t ka, kb;
+      if (DUAL) {
+        ka = dual_root_key(A.births, A.G, c.a);
+        kb = dual_root_key(A.births, A.G, c.b);
+      } else {
+        const uint32_t xa = vox_kidx(A.g, c.a), xb = vox_kidx(A.g, c.b);
+        ka = make_key(A.births[xa], xa);
+        kb = make_key(A.births[xb], xb);
+      }
+      const bool a_young = DUAL ? ka < kb : ka > kb;
+      if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) continue;
+      const uint32_t young = a_young ? c.a : c.b, old = a_young ? c.b : c.a;
+      A.parent[young] = old;
+      const unsigned long long r = atomicAdd(A.nrec, 1ull);
+      if (DUAL) {
+        A.rec[r] = dual_record(c.key, a_young ? ka : kb);
+      } else {
+        A.tags[key_kidx(c.key)] = make_tag(KIND_CLEARED, 0);  // a death edge: cleared for dim 1
+        A.rec[r] = (uint64_t(key_kidx(a_young ? ka : kb)) << 32) | key_kidx(c.key);
+      }
+      A.alive[i] = 2;
+    }
+    grid.sync();
+    unsigned* cnt = A.ctl + (rounds & 1);
+    for (unsigned base = gt - (gt & 31u); base < n; base += gs) {  // reset + compact survivors
+      const unsigned i = base + lane;
+      bool keep = false;
+      Cand c;
+      if (i < n) {
+        c = cur[i];
+        if (A.alive[i]) {
+          A.best[c.a] = NONE64;
+          A.best[c.b] = NONE64;
+        }
+        keep = A.alive[i] == 1;
+      }
+      const unsigned mask = __ballot_sync(0xFFFFFFFFu, keep);
+      if (!mask) continue;
+      unsigned off = 0;
+      if (lane == __ffs(mask) - 1) off = atomicAdd(cnt, __popc(mask));
+      off = __shfl_sync(0xFFFFFFFFu, off, __ffs(mask) - 1);
+      if (keep) nxt[off + __popc(mask & ((1u << lane) - 1))] = c;
+    }
+    if (gt == 0) A.ctl[(rounds + 1) & 1] = 0;  // the next round's counter (read before 2 syncs)
+    grid.sync();
+    n = __ldcg(cnt);
+    Cand* t = cur;
+    cur = nxt;
+    nxt = t;
+    ++rounds;
+  }
+  if (gt == 0) A.ctl[2] = rounds;
+}
+
+// Runs the merge rounds on n candidates (cand, spare buffer cand2); returns the number of rounds.
+template <bool DUAL>
+int64_t mm_rounds(Cand* cand, Cand* cand2, unsigned n, uint32_t* parent, unsigned long long* best,
+                  uint8_t* alive, const uint32_t* births, const Geom& g, const DualG& G,
+                  uint8_t* tags, uint64_t* rec, unsigned long long* nrec, Workspace& ws,
+                  HostScalars& hs) {
+  if (n == 0) return 0;
+  cudaStream_t s = ws.stream();
+  unsigned* ctl = ws.alloc<unsigned>(4);
+  CR_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned), s));
+  static thread_local int occ[2] = {0, 0};
+  static thread_local int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    CR_CUDA(cudaGetDevice(&dev));
+    CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (!occ[DUAL]) {
+    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[DUAL], k_mm_rounds<DUAL>, 256, 0));
+    if (occ[DUAL] < 1) throw Error{CR_EINTERNAL, "k_mm_rounds cannot be resident"};
+  }
+  int64_t blocks = (int64_t(n) + 255) / 256;
+  const int64_t cap = int64_t(nsm) * occ[DUAL];
+  if (blocks > cap) blocks = cap;
+  MMArgs A{cand, cand2, n, parent, best, alive, births, g, G, tags, rec, nrec, ctl};
+  void* args[] = {&A};
+  CR_CUDA(cudaLaunchCooperativeKernel((void*)k_mm_rounds<DUAL>, dim3(unsigned(blocks)), dim3(256),
+                                      args, 0, s));
+  ++g_launch_count;
+  return int64_t(read_scalar(ctl + 2, s, hs));
+}
+
 // Returns false (doing nothing) if the dual graph has more than max_basins roots: its union-find
 // then runs on one CTA's shared memory only up to SMEM_BASINS roots, and the device-wide
 // mutual-minimum rounds degenerate on the dual graph (the outside vertex absorbs components one
@@ -1976,21 +2114,9 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     uint8_t* alive = ws.alloc<uint8_t>(n + 1);
     Cand* cand2 = ws.alloc<Cand>(n + 1);
     unsigned* nnext = reinterpret_cast<unsigned*>(cnt + 6);
-    int64_t rounds = 0;
-    while (n > 0) {
-      k_mm_find<<<grid_for(n, B), B, 0, s>>>(cand, n, parent, best, alive);
-      CR_CHECK_LAUNCH();
-      k_dual_mm_commit<<<grid_for(n, B), B, 0, s>>>(cand, n, S.births, G, parent, best, alive,
-                                                    S.R.rec[d], nrec);
-      CR_CHECK_LAUNCH();
-      CR_CUDA(cudaMemsetAsync(nnext, 0, sizeof(unsigned), s));
-      k_mm_reset<<<grid_for(n, B), B, 0, s>>>(cand, n, best, alive, cand2, nnext);
-      CR_CHECK_LAUNCH();
-      std::swap(cand, cand2);
-      n = read_scalar(nnext, s, hs);
-      ++rounds;
-    }
-    st.rounds[d] = rounds;
+    (void)nnext;
+    st.rounds[d] = mm_rounds<true>(cand, cand2, n, parent, best, alive, S.births, g, G, nullptr,
+                                   S.R.rec[d], nrec, ws, hs);
     S.R.n[d] = int64_t(read_scalar(nrec, s, hs));
     return true;
   }
@@ -2342,21 +2468,9 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   CR_CUDA(cudaMemsetAsync(best, 0xFF, g.nvox * sizeof(unsigned long long), s));
   uint8_t* alive = ws.alloc<uint8_t>(nedges);
   unsigned* nnext = reinterpret_cast<unsigned*>(cnt + 14);
-  int64_t rounds = 0;
-  while (n > 0) {
-    k_mm_find<<<grid_for(n, B), B, 0, s>>>(cand, n, parent, best, alive);
-    CR_CHECK_LAUNCH();
-    k_mm_commit<<<grid_for(n, B), B, 0, s>>>(cand, n, S.births, g, parent, best, alive, S.tags,
-                                             S.R.rec[0], nrec0);
-    CR_CHECK_LAUNCH();
-    CR_CUDA(cudaMemsetAsync(nnext, 0, sizeof(unsigned), s));
-    k_mm_reset<<<grid_for(n, B), B, 0, s>>>(cand, n, best, alive, cand2, nnext);
-    CR_CHECK_LAUNCH();
-    std::swap(cand, cand2);
-    n = read_scalar(nnext, s, hs);
-    ++rounds;
-  }
-  st.rounds[0] = rounds;
+  (void)nnext;
+  st.rounds[0] = mm_rounds<false>(cand, cand2, n, parent, best, alive, S.births, g,
+                                  DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ws, hs);
   // flatten once more so that roots are exact, then essential classes
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
   CR_CHECK_LAUNCH();
