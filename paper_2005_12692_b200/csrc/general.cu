@@ -2205,11 +2205,11 @@ __global__ void k_bar_flags(const uint64_t* __restrict__ rec, int64_t n,
 __global__ void k_bar_scatter(const uint64_t* __restrict__ rec, int64_t n,
                               const uint32_t* __restrict__ births,
                               const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                              int dim, int64_t base, int64_t cap, cr_pair* out,
-                              uint32_t* out_cells) {
+                              int dim, const long long* __restrict__ dbase, int64_t cap,
+                              cr_pair* out, uint32_t* out_cells) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n || !flag[i]) return;
-  int64_t o = base + pos[i];
+  int64_t o = dbase[dim] + pos[i];
   if (o >= cap) return;
   uint64_t r = rec[i];
   uint32_t b = uint32_t(r >> 32), d = uint32_t(r);
@@ -2219,6 +2219,12 @@ __global__ void k_bar_scatter(const uint64_t* __restrict__ rec, int64_t n,
   p.death = d == NONE32 ? __int_as_float(0x7F800000) : float_of_ord(births[d]);
   out[o] = p;
   if (out_cells) out_cells[o] = b;
+}
+
+// running output offsets of emit_bars: dbase[d + 1] = dbase[d] + bars of dimension d
+__global__ void k_bar_advance(const uint32_t* __restrict__ pos, int64_t n, long long* dbase,
+                              int d) {
+  dbase[d + 1] = dbase[d] + (pos ? (long long)pos[n] : 0ll);
 }
 
 __global__ void k_partner_init(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
@@ -2492,28 +2498,39 @@ int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out
                   int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st) {
   cudaStream_t s = ws.stream();
   const int B = 256;
-  int64_t total = 0;
-  for (int d = 0; d <= maxdim && d < 4; ++d) {
+  // one host read at the end: the output offset of each dimension is kept on the device
+  const int dl = maxdim < 3 ? maxdim : 3;
+  long long* dbase = ws.alloc<long long>(5);
+  CR_CUDA(cudaMemsetAsync(dbase, 0, 5 * sizeof(long long), s));
+  int kb = 1;  // significant bits of a kidx: records sort by birth kidx (distinct per dimension)
+  while (kb < 32 && (int64_t(1) << kb) < S.g.ncells) ++kb;
+  for (int d = 0; d <= dl; ++d) {
     int64_t n = S.R.n[d];
-    if (n == 0 || !S.R.rec[d]) continue;
-    sort_keys_u64(S.R.rec[d], n, false, 64, ws);
+    if (n == 0 || !S.R.rec[d]) {
+      k_bar_advance<<<1, 1, 0, s>>>(nullptr, 0, dbase, d);
+      CR_CHECK_LAUNCH();
+      continue;
+    }
+    sort_keys_u64(S.R.rec[d], n, false, 32 + kb, ws, 32);
     uint32_t* flag = ws.alloc<uint32_t>(n + 1);
     uint32_t* pos = ws.alloc<uint32_t>(n + 1);
     k_bar_flags<<<grid_for(n, B), B, 0, s>>>(S.R.rec[d], n, S.births, flag);
     CR_CHECK_LAUNCH();
     CR_CUDA(cudaMemsetAsync(flag + n, 0, sizeof(uint32_t), s));
     exclusive_sum_u32(flag, pos, n + 1, ws);
-    uint32_t cnt = read_scalar(pos + n, s, hs);
-    k_bar_scatter<<<grid_for(n, B), B, 0, s>>>(S.R.rec[d], n, S.births, flag, pos, d, total, cap,
+    k_bar_scatter<<<grid_for(n, B), B, 0, s>>>(S.R.rec[d], n, S.births, flag, pos, d, dbase, cap,
                                                out, out_cells);
     CR_CHECK_LAUNCH();
-    total += cnt;
-    st.pairs[d] = cnt;
+    k_bar_advance<<<1, 1, 0, s>>>(pos, n, dbase, d);
+    CR_CHECK_LAUNCH();
     ws.release(flag);
     ws.release(pos);
   }
+  CR_CUDA(cudaMemcpyAsync(hs.p, dbase, 5 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  for (int d = 0; d <= dl; ++d) st.pairs[d] = int64_t(hs.p[d + 1] - hs.p[d]);
   prof_mark(s, "emit");
-  return total;
+  return int64_t(hs.p[dl + 1]);
 }
 
 void emit_partner(const GeneralState& S, uint32_t* partner, Workspace& ws) {

@@ -79,7 +79,8 @@ int64_t barcodes_core(const float* image, const Geom& g, int maxdim, cr_pair* ou
 void set_last_stats(const cr_stats& st);
 
 // Device-wide helpers (util.cu).
-void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws);
+void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws,
+                   int begin_bit = 0);
 void exclusive_sum_u32(const uint32_t* in, uint32_t* out, int64_t n, Workspace& ws);
 
 }  // namespace cr

@@ -210,20 +210,21 @@ HostScalars::HostScalars() : p(nullptr) {
 }
 HostScalars::~HostScalars() {}
 
-void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws) {
+void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws,
+                   int begin_bit) {
   if (n <= 1) return;
   uint64_t* alt = ws.alloc<uint64_t>(n);
   cub::DoubleBuffer<uint64_t> db(keys, alt);
   size_t tmp = 0;
   if (descending)
-    CR_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp, db, int(n), 0, end_bit, ws.stream()));
+    CR_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
   else
-    CR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, int(n), 0, end_bit, ws.stream()));
+    CR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
   void* t = ws.alloc_bytes(tmp);
   if (descending)
-    CR_CUDA(cub::DeviceRadixSort::SortKeysDescending(t, tmp, db, int(n), 0, end_bit, ws.stream()));
+    CR_CUDA(cub::DeviceRadixSort::SortKeysDescending(t, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
   else
-    CR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, db, int(n), 0, end_bit, ws.stream()));
+    CR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
   if (db.Current() != keys)
     CR_CUDA(cudaMemcpyAsync(keys, db.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
                             ws.stream()));
