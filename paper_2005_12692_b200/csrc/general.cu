@@ -1942,7 +1942,7 @@ __global__ void k_dual_mm_commit(const Cand* cand, unsigned n, const uint32_t* _
 struct MMArgs {
   Cand* cur;
   Cand* nxt;
-  unsigned n;
+  const unsigned* n;  // device: the number of candidates (read by the kernel: no host round trip)
   uint32_t* parent;
   unsigned long long* best;
   uint8_t* alive;
@@ -1961,7 +1961,7 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
   const int lane = threadIdx.x & 31;
   Cand* cur = A.cur;
   Cand* nxt = A.nxt;
-  unsigned n = A.n, rounds = 0;
+  unsigned n = *A.n, rounds = 0;
   while (n > 0) {
     for (unsigned i = gt; i < n; i += gs) {  // find
       Cand c = cur[i];
@@ -2036,16 +2036,15 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
   if (gt == 0) A.ctl[2] = rounds;
 }
 
-// Runs the merge rounds on n candidates (cand, spare buffer cand2); returns the number of rounds.
+// Launches the merge rounds on the *n_dev candidates (cand, spare buffer cand2, both holding
+// n_max); ctl (4 device unsigned, zeroed by the caller) receives the number of rounds in ctl[2].
+// No host synchronisation: the caller reads ctl[2] with its next scalar read.
 template <bool DUAL>
-int64_t mm_rounds(Cand* cand, Cand* cand2, unsigned n, uint32_t* parent, unsigned long long* best,
-                  uint8_t* alive, const uint32_t* births, const Geom& g, const DualG& G,
-                  uint8_t* tags, uint64_t* rec, unsigned long long* nrec, Workspace& ws,
-                  HostScalars& hs) {
-  if (n == 0) return 0;
+void mm_rounds(Cand* cand, Cand* cand2, const unsigned* n_dev, int64_t n_max, uint32_t* parent,
+               unsigned long long* best, uint8_t* alive, const uint32_t* births, const Geom& g,
+               const DualG& G, uint8_t* tags, uint64_t* rec, unsigned long long* nrec,
+               unsigned* ctl, Workspace& ws) {
   cudaStream_t s = ws.stream();
-  unsigned* ctl = ws.alloc<unsigned>(4);
-  CR_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned), s));
   static thread_local int occ[2] = {0, 0};
   static thread_local int nsm = 0;
   if (!nsm) {
@@ -2057,15 +2056,15 @@ int64_t mm_rounds(Cand* cand, Cand* cand2, unsigned n, uint32_t* parent, unsigne
     CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[DUAL], k_mm_rounds<DUAL>, 256, 0));
     if (occ[DUAL] < 1) throw Error{CR_EINTERNAL, "k_mm_rounds cannot be resident"};
   }
-  int64_t blocks = (int64_t(n) + 255) / 256;
+  int64_t blocks = (n_max + 255) / 256;
   const int64_t cap = int64_t(nsm) * occ[DUAL];
   if (blocks > cap) blocks = cap;
-  MMArgs A{cand, cand2, n, parent, best, alive, births, g, G, tags, rec, nrec, ctl};
+  if (blocks < 1) blocks = 1;
+  MMArgs A{cand, cand2, n_dev, parent, best, alive, births, g, G, tags, rec, nrec, ctl};
   void* args[] = {&A};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k_mm_rounds<DUAL>, dim3(unsigned(blocks)), dim3(256),
                                       args, 0, s));
   ++g_launch_count;
-  return int64_t(read_scalar(ctl + 2, s, hs));
 }
 
 // Returns false (doing nothing) if the dual graph has more than max_basins roots: its union-find
@@ -2113,11 +2112,14 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     CR_CUDA(cudaMemsetAsync(best, 0xFF, nv * sizeof(unsigned long long), s));
     uint8_t* alive = ws.alloc<uint8_t>(n + 1);
     Cand* cand2 = ws.alloc<Cand>(n + 1);
-    unsigned* nnext = reinterpret_cast<unsigned*>(cnt + 6);
-    (void)nnext;
-    st.rounds[d] = mm_rounds<true>(cand, cand2, n, parent, best, alive, S.births, g, G, nullptr,
-                                   S.R.rec[d], nrec, ws, hs);
-    S.R.n[d] = int64_t(read_scalar(nrec, s, hs));
+    unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 6);  // cnt[6], cnt[7]: zeroed above
+    mm_rounds<true>(cand, cand2, ncand, n, parent, best, alive, S.births, g, G, nullptr,
+                    S.R.rec[d], nrec, ctl, ws);
+    CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 2, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            s));
+    CR_CUDA(cudaStreamSynchronize(s));
+    S.R.n[d] = int64_t(hs.p[0]);
+    st.rounds[d] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 4)[2]);
     return true;
   }
   {
@@ -2400,7 +2402,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
   k_h0_edges<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
   CR_CHECK_LAUNCH();
-  unsigned n = read_scalar(ncand, s, hs);
 
   // vertex records: at most one per finite vertex
   S.R.rec[0] = ws.alloc<uint64_t>(st.cells[0]);
@@ -2408,6 +2409,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   const unsigned nb = unsigned(st.columns[0]);
   if (nb <= smem_basins_max()) {
     // few basins: shared-memory rounds in one CTA
+    const unsigned n = read_scalar(ncand, s, hs);
     uint64_t* rootkey = ws.alloc<uint64_t>(nb + 1);
     unsigned* nroot = reinterpret_cast<unsigned*>(cnt + 15);
     k_collect_roots<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, rootkey, nroot);
@@ -2473,17 +2475,20 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   unsigned long long* best = ws.alloc<unsigned long long>(g.nvox);
   CR_CUDA(cudaMemsetAsync(best, 0xFF, g.nvox * sizeof(unsigned long long), s));
   uint8_t* alive = ws.alloc<uint8_t>(nedges);
-  unsigned* nnext = reinterpret_cast<unsigned*>(cnt + 14);
-  (void)nnext;
-  st.rounds[0] = mm_rounds<false>(cand, cand2, n, parent, best, alive, S.births, g,
-                                  DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ws, hs);
+  unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 20);  // cnt[20], cnt[21]: zeroed at the start
+  mm_rounds<false>(cand, cand2, ncand, nedges, parent, best, alive, S.births, g,
+                   DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ctl, ws);
   // flatten once more so that roots are exact, then essential classes
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
   CR_CHECK_LAUNCH();
   k_h0_essential<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
                                                     nullptr);
   CR_CHECK_LAUNCH();
-  S.R.n[0] = int64_t(read_scalar(nrec0, s, hs));
+  CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  S.R.n[0] = int64_t(hs.p[0]);
+  st.rounds[0] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 7)[2]);
   prof_mark(s, "h0");
   ws.release(cand);
   ws.release(cand2);
