@@ -10,6 +10,9 @@
 // pool overflow) are flagged and the caller recomputes the batch on the device-wide path.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <type_traits>
+
 #include "pipeline.cuh"
 
 namespace cr {
@@ -37,17 +40,25 @@ struct K7Args {
   int dual;         // dimension 1 by Alexander duality (union-find over squares); else reduction
 };
 
-struct K7Smem {
-  uint32_t ord[K7_MAXVOX];
-  uint32_t births[K7_MAXCELLS];
-  uint32_t death[K7_MAXCELLS];
+// Per-CTA shared memory.  DUAL (dimension 1 by duality, the default): no reduction buffers, so
+// more CTAs fit an SM.  pre: the next image's pixels, prefetched by cp.async while this one runs.
+struct K7Red {
   uint16_t owner[K7_MAXCELLS];
-  uint16_t vpar[K7_MAXVOX];
-  uint8_t tags[K7_MAXCELLS];
   uint64_t pool[K7_POOL];
   uint64_t work[2][K7_WORK];
   uint16_t pool_off[K7_MAXCELLS / 2];
   uint16_t pool_len[K7_MAXCELLS / 2];
+};
+struct K7Empty {};
+template <bool DUAL>
+struct K7Smem {
+  uint32_t pre[K7_MAXVOX];
+  uint32_t ord[K7_MAXVOX];
+  uint32_t births[K7_MAXCELLS];
+  uint32_t death[K7_MAXCELLS];
+  uint16_t vpar[K7_MAXVOX];
+  uint8_t tags[K7_MAXCELLS];
+  typename std::conditional<DUAL, K7Empty, K7Red>::type red;
   union {  // the keys are held in registers while the sort uses its temporary storage
     typename cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT>::TempStorage sort;
     typename cub::BlockScan<uint32_t, K7_THREADS>::TempStorage scan;
@@ -58,22 +69,34 @@ struct K7Smem {
   uint32_t nbars;
 };
 
-__device__ __forceinline__ uint64_t cellkey(const K7Smem& S, uint32_t k) {
+template <class SM>
+__device__ __forceinline__ uint64_t cellkey(const SM& S, uint32_t k) {
   return make_key(S.births[k], k);
 }
+// compact sort key (ord << 12 | kidx): the same order as cellkey on <= 4096 cells, 44 bits
+constexpr int K7_KBITS = 12, K7_SORT_BITS = 32 + K7_KBITS;
+static_assert(K7_MAXCELLS <= (1 << K7_KBITS), "kidx field");
+template <class SM>
+__device__ __forceinline__ uint64_t sortkey(const SM& S, uint32_t k) {
+  return (uint64_t(S.births[k]) << K7_KBITS) | k;
+}
+__device__ __forceinline__ uint32_t sortcell(uint64_t key) {
+  return uint32_t(key & ((1u << K7_KBITS) - 1));
+}
 
-// sort S.tmp.keys[0..n) ascending (descending if desc) in place
-__device__ void k7_sort(K7Smem& S, uint32_t n, bool desc) {
+// sort S.tmp.keys[0..n) ascending (descending if desc) in place, on the compact key's 44 bits
+template <class SM>
+__device__ void k7_sort(SM& S, uint32_t n, bool desc) {
   uint64_t it[K7_IPT];
 #pragma unroll
   for (int r = 0; r < K7_IPT; ++r) {
     const uint32_t i = threadIdx.x * K7_IPT + r;
-    it[r] = i < n ? S.tmp.keys[i] : (desc ? 0ull : NONE64);
+    it[r] = i < n ? S.tmp.keys[i] : (desc ? 0ull : (1ull << K7_SORT_BITS) - 1);
   }
   __syncthreads();
   typedef cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT> BRS;
-  if (desc) BRS(S.tmp.sort).SortDescending(it);
-  else BRS(S.tmp.sort).Sort(it);
+  if (desc) BRS(S.tmp.sort).SortDescending(it, 0, K7_SORT_BITS);
+  else BRS(S.tmp.sort).Sort(it, 0, K7_SORT_BITS);
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < K7_IPT; ++r) {
@@ -106,21 +129,39 @@ __device__ uint32_t k7_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B,
   return n;
 }
 
+__device__ __forceinline__ void k7_cp4(uint32_t* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                   uint32_t(__cvta_generic_to_shared(dst))), "l"(src));
+}
+
+// Persistent CTAs: CTA b takes images b, b + gridDim.x, ...; once an image's pixels are turned
+// into ords, the next image's pixels are copied into S.pre by cp.async while this one is
+// processed (the load latency was a quarter of the stall samples with one image per CTA).
+template <bool DUAL>
 __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K7Smem& S = *reinterpret_cast<K7Smem*>(smem_raw);
-  const int64_t img = blockIdx.x;
+  K7Smem<DUAL>& S = *reinterpret_cast<K7Smem<DUAL>*>(smem_raw);
   const int nx = A.nx, ny = A.ny, nvox = nx * ny;
   const int KX = 2 * nx - 1, KY = 2 * ny - 1, N = KX * KY;
+  auto prefetch = [&](int64_t im) {
+    if (im < A.batch)
+      for (int v = threadIdx.x; v < nvox; v += K7_THREADS) k7_cp4(&S.pre[v], A.images + im * nvox + v);
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  prefetch(blockIdx.x);
+  for (int64_t img = blockIdx.x; img < A.batch; img += gridDim.x) {
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
   // ---- 1. ords, births
   bool nan = false;
   for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
-    const float f = A.images[img * nvox + v];
+    const float f = __uint_as_float(S.pre[v]);
     nan |= f != f;
     S.ord[v] = ord_of(f);
   }
   if (nan) atomicOr(A.flags, 1);
   __syncthreads();
+  prefetch(img + gridDim.x);  // S.pre is free again
   for (int k = threadIdx.x; k < N; k += K7_THREADS) {
     const int X = k % KX, Y = k / KX;
     uint32_t m = 0;
@@ -128,7 +169,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
       for (int x = X >> 1; x <= (X + 1) >> 1; ++x) m = max(m, S.ord[y * nx + x]);
     S.births[k] = m;
     S.death[k] = D_NONE;
-    S.owner[k] = 0xFFFFu;
+    if constexpr (!DUAL) S.red.owner[k] = 0xFFFFu;
   }
   __syncthreads();
   // ---- 2. apparent pairs (same rule as k_tags)
@@ -228,30 +269,76 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
     const int s = (X & 1) ? 1 : KX;
     const int a = k - s, b = k + s;
     const int va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
-    if (S.vpar[va] != S.vpar[vb]) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = cellkey(S, k);
+    if (S.vpar[va] != S.vpar[vb]) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = sortkey(S, k);
   }
   __syncthreads();
   const uint32_t nc = S.nkeys;
   k7_sort(S, nc, false);
-  if (threadIdx.x == 0) {
-    for (uint32_t i = 0; i < nc; ++i) {
-      const uint32_t k = key_kidx(S.tmp.keys[i]);
-      const int X = k % KX;
-      const int s = (X & 1) ? 1 : KX;
-      const int a = k - s, b = k + s;
-      const uint32_t va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
-      const uint32_t ra = k7_find(S.vpar, va), rb = k7_find(S.vpar, vb);
-      if (ra == rb) continue;  // positive edge
-      const uint32_t ka = 2 * (ra / nx) * KX + 2 * (ra % nx), kb = 2 * (rb / nx) * KX + 2 * (rb % nx);
-      const bool a_young = cellkey(S, ka) > cellkey(S, kb);
-      const uint32_t young = a_young ? ra : rb, old = a_young ? rb : ra;
-      const uint32_t ky = a_young ? ka : kb;
-      S.vpar[young] = uint16_t(old);  // elder rule
-      S.death[ky] = S.births[k] > S.births[ky] ? S.births[k] : D_ZERO;
-      S.tags[k] = make_tag(KIND_CLEARED, 0);
+  // Elder-rule Kruskal over the sorted candidates as block-wide merge rounds (the rule of
+  // general.cu's k_mm_rounds: an edge commits when it is the minimum candidate at both of its
+  // components, or at the younger one alone -- the same merges as the sequential loop).  A
+  // candidate's minimum is its index in the sorted list; per-root minima live in S.ord (the ords
+  // are dead once the births exist).  Thread t owns candidates t + 256 r, r < K7_IPT.
+  {
+    uint32_t* best = S.ord;
+    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) best[v] = NONE32;
+    uint32_t alive = 0;  // bit r: candidate t + 256 r undecided
+#pragma unroll
+    for (int r = 0; r < K7_IPT; ++r)
+      if (threadIdx.x + K7_THREADS * r < int(nc)) alive |= 1u << r;
+    uint16_t ra[K7_IPT], rb[K7_IPT];
+    __syncthreads();
+    while (true) {
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < K7_IPT; ++r) {
+        if (!(alive >> r & 1)) continue;
+        const uint32_t i = threadIdx.x + K7_THREADS * r;
+        const uint32_t k = sortcell(S.tmp.keys[i]);
+        const int s1 = ((k % KX) & 1) ? 1 : KX;
+        const int a = int(k) - s1, b = int(k) + s1;
+        const uint32_t va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
+        const uint32_t x = k7_find(S.vpar, va), y = k7_find(S.vpar, vb);
+        if (x == y) {  // positive edge: closes a cycle of older edges
+          alive &= ~(1u << r);
+          continue;
+        }
+        ra[r] = uint16_t(x);
+        rb[r] = uint16_t(y);
+        any = true;
+        atomicMin(best + x, i);
+        atomicMin(best + y, i);
+      }
+      if (!__syncthreads_or(any)) break;
+      uint32_t touched = alive;
+#pragma unroll
+      for (int r = 0; r < K7_IPT; ++r) {
+        if (!(alive >> r & 1)) continue;
+        const uint32_t i = threadIdx.x + K7_THREADS * r;
+        const uint32_t x = ra[r], y = rb[r];
+        const bool min_a = best[x] == i, min_b = best[y] == i;
+        if (!min_a && !min_b) continue;
+        const uint32_t kxa = 2 * (x / nx) * KX + 2 * (x % nx), kxb = 2 * (y / nx) * KX + 2 * (y % nx);
+        const bool a_young = cellkey(S, kxa) > cellkey(S, kxb);
+        if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) continue;
+        const uint32_t young = a_young ? x : y, old = a_young ? y : x;
+        const uint32_t ky = a_young ? kxa : kxb;
+        const uint32_t k = sortcell(S.tmp.keys[i]);
+        S.vpar[young] = uint16_t(old);  // elder rule
+        S.death[ky] = S.births[k] > S.births[ky] ? S.births[k] : D_ZERO;
+        S.tags[k] = make_tag(KIND_CLEARED, 0);
+        alive &= ~(1u << r);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < K7_IPT; ++r)
+        if (touched >> r & 1) {
+          best[ra[r]] = NONE32;
+          best[rb[r]] = NONE32;
+        }
+      __syncthreads();
     }
   }
-  __syncthreads();
   for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
     const int k = 2 * (v / nx) * KX + 2 * (v % nx);
     if (S.vpar[v] == v && S.births[k] != ABSENT_ORD) S.death[k] = D_ESS;
@@ -260,7 +347,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
   const bool do_d1 = A.maxdim >= 1 && nx > 1 && ny > 1;
   if (threadIdx.x == 0) S.nkeys = 0;
   __syncthreads();
-  if (do_d1 && A.dual && nvox + 1 <= K7_MAXVOX) {
+  if (DUAL && do_d1) {
     // dimension 1 = the top dimension of a 2D image, by Alexander duality (the
     // same construction as general.cu's top_dual): squares and the outside OMEGA are the vertices,
     // residual edges in decreasing key the edges, the root with the larger key survives.  Dual
@@ -321,37 +408,90 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
       const int X = k % KX, Y = k / KX;
       if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
       if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
-      if (dfind(side(k, 0)) != dfind(side(k, 1))) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = cellkey(S, k);
+      if (dfind(side(k, 0)) != dfind(side(k, 1))) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = sortkey(S, k);
     }
     __syncthreads();
     const uint32_t nc = S.nkeys;
     k7_sort(S, nc, true);
-    if (threadIdx.x == 0) {
+    // Kruskal over the dual edges (decreasing key) as block-wide merge rounds, the mirror of the
+    // H0 rounds above (the root with the LARGER key survives).  Per-root minima: square roots in
+    // the death slots of their squares (a 2D barcode never reads a square's death), OMEGA in
+    // S.changed.
+    {
       auto rkey = [&](uint32_t v) -> uint64_t {
         return v == OMEGA ? NONE64 : cellkey(S, sq_of(v));
       };
-      for (uint32_t i = 0; i < nc; ++i) {
-        const uint32_t e = key_kidx(S.tmp.keys[i]);
-        const uint32_t ra = dfind(side(int(e), 0)), rb = dfind(side(int(e), 1));
-        if (ra == rb) continue;  // closes a cycle (a death of dimension 0)
-        const uint64_t ka = rkey(ra), kb = rkey(rb);
-        const uint32_t young = ka < kb ? ra : rb, old = ka < kb ? rb : ra;
-        const uint64_t ky = ka < kb ? ka : kb;
-        dp[young] = old;
-        if (key_ord(ky) == ABSENT_ORD) {
-          S.death[e] = D_ESS;  // two absent regions meet: a hole that never fills
-        } else {
-          const uint32_t by = key_ord(ky);
-          S.death[e] = by > S.births[e] ? by : D_ZERO;
+      auto bslot = [&](uint32_t v) -> uint32_t* {
+        return v == OMEGA ? &S.changed : &S.death[sq_of(v)];
+      };
+      for (int v = threadIdx.x; v <= nvox; v += K7_THREADS)
+        if (uint32_t(v) == OMEGA || ((v % nx) + 1 < nx && (v / nx) + 1 < ny)) *bslot(uint32_t(v)) = NONE32;
+      uint32_t alive = 0;
+#pragma unroll
+      for (int r = 0; r < K7_IPT; ++r)
+        if (threadIdx.x + K7_THREADS * r < int(nc)) alive |= 1u << r;
+      uint32_t ra[K7_IPT], rb[K7_IPT];
+      __syncthreads();
+      while (true) {
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < K7_IPT; ++r) {
+          if (!(alive >> r & 1)) continue;
+          const uint32_t i = threadIdx.x + K7_THREADS * r;
+          const uint32_t e = sortcell(S.tmp.keys[i]);
+          const uint32_t x = dfind(side(int(e), 0)), y = dfind(side(int(e), 1));
+          if (x == y) {  // closes a cycle (a death of dimension 0)
+            alive &= ~(1u << r);
+            continue;
+          }
+          ra[r] = x;
+          rb[r] = y;
+          any = true;
+          atomicMin(bslot(x), i);
+          atomicMin(bslot(y), i);
         }
+        if (!__syncthreads_or(any)) break;
+        const uint32_t touched = alive;
+#pragma unroll
+        for (int r = 0; r < K7_IPT; ++r) {
+          if (!(alive >> r & 1)) continue;
+          const uint32_t i = threadIdx.x + K7_THREADS * r;
+          const uint32_t x = ra[r], y = rb[r];
+          const bool min_a = *bslot(x) == i, min_b = *bslot(y) == i;
+          if (!min_a && !min_b) continue;
+          const uint64_t ka = rkey(x), kb = rkey(y);
+          const bool a_young = ka < kb;
+          if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) continue;
+          const uint32_t young = a_young ? x : y, old = a_young ? y : x;
+          const uint64_t ky = a_young ? ka : kb;
+          const uint32_t e = sortcell(S.tmp.keys[i]);
+          dp[young] = old;
+          if (key_ord(ky) == ABSENT_ORD) {
+            S.death[e] = D_ESS;  // two absent regions meet: a hole that never fills
+          } else {
+            const uint32_t by = key_ord(ky);
+            S.death[e] = by > S.births[e] ? by : D_ZERO;
+          }
+          alive &= ~(1u << r);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < K7_IPT; ++r)
+          if (touched >> r & 1) {
+            *bslot(ra[r]) = NONE32;
+            *bslot(rb[r]) = NONE32;
+          }
+        __syncthreads();
       }
     }
   } else if (do_d1) {
+   if constexpr (!DUAL) {
+    auto& R = S.red;
     for (int k = threadIdx.x; k < N; k += K7_THREADS) {
       const int X = k % KX, Y = k / KX;
       if (((X & 1) + (Y & 1)) == 1 && S.births[k] != ABSENT_ORD &&
           tag_kind(S.tags[k]) == KIND_RESIDUAL)
-        S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = cellkey(S, k);
+        S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = sortkey(S, k);
     }
     __syncthreads();
     const uint32_t ncol = S.nkeys;
@@ -360,7 +500,7 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
       uint32_t ptop = 0;
       bool overflow = false;
       for (uint32_t ci = 0; ci < ncol && !overflow; ++ci) {
-        const uint32_t sk = key_kidx(S.tmp.keys[ci]);
+        const uint32_t sk = sortcell(S.tmp.keys[ci]);
         // coboundary: the finite squares on both sides of the edge
         auto cob = [&](uint32_t e, uint64_t* dst) -> uint32_t {
           const int X = e % KX, Y = e / KX;
@@ -379,14 +519,14 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
           return n;
         };
         int cur = 0;
-        uint32_t len = cob(sk, S.work[0]);
+        uint32_t len = cob(sk, R.work[0]);
         uint64_t tmpc[2];
         while (true) {
           if (len == 0) {
             S.death[sk] = D_ESS;
             break;
           }
-          const uint64_t p = S.work[cur][0];
+          const uint64_t p = R.work[cur][0];
           const uint32_t pk = key_kidx(p);
           const uint8_t t = S.tags[pk];
           const uint64_t* add;
@@ -396,20 +536,20 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
             const int off = (d >> 1) == 0 ? 1 : KX;
             alen = cob(uint32_t(int(pk) + ((d & 1) ? off : -off)), tmpc);
             add = tmpc;
-          } else if (S.owner[pk] != 0xFFFFu) {
-            const uint32_t o = S.owner[pk];
-            add = S.pool + S.pool_off[o];
-            alen = S.pool_len[o];
+          } else if (R.owner[pk] != 0xFFFFu) {
+            const uint32_t o = R.owner[pk];
+            add = R.pool + R.pool_off[o];
+            alen = R.pool_len[o];
           } else {  // new pair (edge, square): bar [birth edge, birth square)
             if (ptop + len > K7_POOL || ci >= K7_MAXCELLS / 2) {
               overflow = true;
               break;
             }
-            for (uint32_t i = 0; i < len; ++i) S.pool[ptop + i] = S.work[cur][i];
-            S.pool_off[ci] = uint16_t(ptop);
-            S.pool_len[ci] = uint16_t(len);
+            for (uint32_t i = 0; i < len; ++i) R.pool[ptop + i] = R.work[cur][i];
+            R.pool_off[ci] = uint16_t(ptop);
+            R.pool_len[ci] = uint16_t(len);
             ptop += len;
-            S.owner[pk] = uint16_t(ci);
+            R.owner[pk] = uint16_t(ci);
             S.death[sk] = S.births[pk] > S.births[sk] ? S.births[pk] : D_ZERO;
             break;
           }
@@ -417,50 +557,60 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
             overflow = true;
             break;
           }
-          len = k7_symdiff(S.work[cur], len, add, alen, S.work[cur ^ 1]);
+          len = k7_symdiff(R.work[cur], len, add, alen, R.work[cur ^ 1]);
           cur ^= 1;
         }
       }
       if (overflow) atomicOr(A.flags + 1, 1);
     }
+   }
   }
   __syncthreads();
-  // ---- 5. bars in (dim, birth kidx) order: vertices, then edges
+  // ---- 5. bars in (dim, birth kidx) order: vertices, then edges.  Thread t owns the cells
+  // [CPT t, CPT t + CPT); one block scan of its packed (dim-0 | dim-1 << 16) counts places them.
   typedef cub::BlockScan<uint32_t, K7_THREADS> BS;
-  if (threadIdx.x == 0) S.nbars = 0;
-  __syncthreads();
+  constexpr int CPT = (K7_MAXCELLS + K7_THREADS - 1) / K7_THREADS;
   const int64_t base = img * A.cap;
-  for (int dim = 0; dim <= (do_d1 ? 1 : 0); ++dim) {
-    for (int c0 = 0; c0 < N; c0 += K7_THREADS) {
-      const int k = c0 + threadIdx.x;
-      bool keep = false;
-      if (k < N) {
-        const int X = k % KX, Y = k / KX;
-        const uint32_t d = S.death[k];
-        keep = ((X & 1) + (Y & 1)) == dim && d != D_NONE && d != D_ZERO;
-      }
-      uint32_t pre, tot;
-      BS(S.tmp.scan).ExclusiveSum(uint32_t(keep), pre, tot);
-      if (keep) {
-        const uint32_t o = S.nbars + pre;
-        if (int(o) < A.cap) {
-          const uint32_t d = S.death[k];
-          uint32_t* w = A.sbar + 3 * (base + o);
-          w[0] = uint32_t(dim);
-          w[1] = __float_as_uint(float_of_ord(S.births[k]));
-          w[2] = d == D_ESS ? 0x7F800000u : __float_as_uint(float_of_ord(d));
-          if (A.scell) A.scell[base + o] = uint32_t(k);
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) S.nbars += tot;
-      __syncthreads();
+  const int dmx = do_d1 ? 1 : 0;
+  const int k0 = threadIdx.x * CPT;
+  uint32_t keepm = 0, cnt = 0;
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int k = k0 + q;
+    if (k >= N) break;
+    const int X = k % KX, Y = k / KX, dim = (X & 1) + (Y & 1);
+    const uint32_t d = S.death[k];
+    if (dim <= dmx && d != D_NONE && d != D_ZERO) {
+      keepm |= 1u << q;
+      cnt += 1u << (16 * dim);
+    }
+  }
+  uint32_t pre, tot;
+  BS(S.tmp.scan).ExclusiveSum(cnt, pre, tot);
+  const uint32_t tot0 = tot & 0xFFFFu, nb = (tot & 0xFFFFu) + (tot >> 16);
+  uint32_t o0 = pre & 0xFFFFu, o1 = tot0 + (pre >> 16);
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    if (!(keepm >> q & 1)) continue;
+    const int k = k0 + q;
+    const int dim = ((k % KX) & 1) + ((k / KX) & 1);
+    const uint32_t o = dim ? o1++ : o0++;
+    if (int(o) < A.cap) {
+      const uint32_t d = S.death[k];
+      uint32_t* w = A.sbar + 3 * (base + o);
+      w[0] = uint32_t(dim);
+      w[1] = __float_as_uint(float_of_ord(S.births[k]));
+      w[2] = d == D_ESS ? 0x7F800000u : __float_as_uint(float_of_ord(d));
+      if (A.scell) A.scell[base + o] = uint32_t(k);
     }
   }
   if (threadIdx.x == 0) {
-    if (int(S.nbars) > A.cap) atomicOr(A.flags + 1, 1);
-    A.count[img] = S.nbars;
+    if (int(nb) > A.cap) atomicOr(A.flags + 1, 1);
+    A.count[img] = nb;
   }
+  __syncthreads();  // S is reused by the next image
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 __global__ void k7_gather(const uint32_t* __restrict__ sbar, const uint32_t* __restrict__ scell,
@@ -528,9 +678,19 @@ int64_t barcodes_batched_small_2d(const float* images, int64_t batch, int64_t ny
   A.count = ws.alloc<uint32_t>(batch + 1);
   A.flags = ws.alloc<int>(4);
   CR_CUDA(cudaMemsetAsync(A.flags, 0, 4 * sizeof(int), s));
-  const size_t smem = sizeof(K7Smem);
-  CR_CUDA(cudaFuncSetAttribute(k7_image, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k7_image<<<unsigned(batch), K7_THREADS, smem, s>>>(A);
+  const bool dual = A.dual && nx > 1 && ny > 1 && vox + 1 <= K7_MAXVOX;
+  auto launch = [&](auto kern, size_t smem) {
+    CR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int dev = 0, nsm = 0, per_sm = 0;
+    CR_CUDA(cudaGetDevice(&dev));
+    CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K7_THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid = std::min<int64_t>(batch, int64_t(nsm) * per_sm);
+    kern<<<unsigned(grid), K7_THREADS, smem, s>>>(A);
+  };
+  if (dual) launch(k7_image<true>, sizeof(K7Smem<true>));
+  else launch(k7_image<false>, sizeof(K7Smem<false>));
   CR_CHECK_LAUNCH();
   prof_mark(s, "k7_images");
   k7_offsets<<<1, 1024, 0, s>>>(A.count, batch, out_offsets);
