@@ -172,65 +172,46 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
     if constexpr (!DUAL) S.red.owner[k] = 0xFFFFu;
   }
   __syncthreads();
-  // ---- 2. apparent pairs (same rule as k_tags)
+  // ---- 2. apparent pairs, as in general.cu's k_filtration: a code per cell
+  // (direction of the first equal-birth cofacet, of the last equal-birth facet, in kidx order
+  // -Y(2) < -X(0) < +X(1) < +Y(3); 7 = none; reading R17), then UP iff the min cofacet's max
+  // facet points back, else DOWN iff the max facet's min cofacet points back.  The codes use the
+  // sort buffer (free until the H0 sort).
+  uint8_t* code = reinterpret_cast<uint8_t*>(S.tmp.keys);
   for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+    const uint32_t b = S.births[k];
+    uint32_t c = 0x40;  // absent
+    if (b != ABSENT_ORD) {
+      const int X = k % KX, Y = k / KX;
+      const bool ox = X & 1, oy = Y & 1;
+      const uint32_t ym = Y > 0 ? S.births[k - KX] : ABSENT_ORD;
+      const uint32_t xm = X > 0 ? S.births[k - 1] : ABSENT_ORD;
+      const uint32_t xp = X + 1 < KX ? S.births[k + 1] : ABSENT_ORD;
+      const uint32_t yp = Y + 1 < KY ? S.births[k + KX] : ABSENT_ORD;
+      uint32_t mc = 7, mf = 7;
+      // cofacets (even axes): the first equal one -- scan backwards
+      if (!oy && yp == b) mc = 3;
+      if (!ox && xp == b) mc = 1;
+      if (!ox && xm == b) mc = 0;
+      if (!oy && ym == b) mc = 2;
+      // facets (odd axes; present cells have present facets): the last equal one
+      if (oy && ym == b) mf = 2;
+      if (ox && xm == b) mf = 0;
+      if (ox && xp == b) mf = 1;
+      if (oy && yp == b) mf = 3;
+      c = mc | (mf << 3);
+    }
+    code[k] = uint8_t(c);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+    const uint32_t c = code[k];
     uint8_t tag = 0;
-    const uint32_t bo = S.births[k];
-    if (bo != ABSENT_ORD) {
-      const int c[2] = {k % KX, k / KX};
-      const int ext[2] = {KX, KY};
-      const int st[2] = {1, KX};
-      const uint64_t mykey = make_key(bo, k);
-      const int dim = (c[0] & 1) + (c[1] & 1);
-      uint64_t best = NONE64;
-      int bdir = -1;
-      for (int a = 0; a < 2; ++a) {
-        if (c[a] & 1) continue;
-        for (int s = 0; s < 2; ++s) {
-          if (s == 0 ? c[a] == 0 : c[a] + 1 >= ext[a]) continue;
-          const int t = k + (s ? st[a] : -st[a]);
-          if (S.births[t] == ABSENT_ORD) continue;
-          const uint64_t key = cellkey(S, t);
-          if (key < best) { best = key; bdir = 2 * a + s; }
-        }
-      }
-      if (bdir >= 0) {
-        const int t = int(key_kidx(best)), ta = bdir >> 1;
-        bool is_max = true;
-        for (int a = 0; a < 2 && is_max; ++a) {
-          if (!(a == ta || (c[a] & 1))) continue;
-          for (int s = 0; s < 2; ++s) {
-            const int f = t + (s ? st[a] : -st[a]);
-            if (f != k && cellkey(S, f) > mykey) { is_max = false; break; }
-          }
-        }
-        if (is_max) tag = make_tag(KIND_UP, bdir);
-      }
-      if (!tag && dim >= 1) {
-        uint64_t bestf = 0;
-        int fdir = -1;
-        for (int a = 0; a < 2; ++a) {
-          if (!(c[a] & 1)) continue;
-          for (int s = 0; s < 2; ++s) {
-            const int f = k + (s ? st[a] : -st[a]);
-            const uint64_t key = cellkey(S, f);
-            if (fdir < 0 || key > bestf) { bestf = key; fdir = 2 * a + s; }
-          }
-        }
-        const int r = int(key_kidx(bestf)), ra = fdir >> 1;
-        bool is_min = true;
-        for (int a = 0; a < 2 && is_min; ++a) {
-          if (a != ra && (c[a] & 1)) continue;
-          const int ca = a == ra ? c[a] + ((fdir & 1) ? 1 : -1) : c[a];
-          for (int s = 0; s < 2; ++s) {
-            if (s == 0 ? ca == 0 : ca + 1 >= ext[a]) continue;
-            const int t = r + (s ? st[a] : -st[a]);
-            if (t == k || S.births[t] == ABSENT_ORD) continue;
-            if (cellkey(S, t) < mykey) { is_min = false; break; }
-          }
-        }
-        if (is_min) tag = make_tag(KIND_DOWN, fdir);
-      }
+    if (!(c & 0x40)) {
+      const uint32_t mc = c & 7, mf = (c >> 3) & 7;
+      auto nbk = [&](uint32_t d) { return k + ((d >> 1) ? KX : 1) * ((d & 1) ? 1 : -1); };
+      if (mc != 7 && ((code[nbk(mc)] >> 3) & 7) == (mc ^ 1)) tag = make_tag(KIND_UP, int(mc));
+      else if (mf != 7 && (code[nbk(mf)] & 7) == (mf ^ 1)) tag = make_tag(KIND_DOWN, int(mf));
     }
     S.tags[k] = tag;
   }
