@@ -21,6 +21,8 @@ namespace {
 constexpr int K7_THREADS = 256;
 constexpr int K7_IPT = 8;
 constexpr int K7_SORT = K7_THREADS * K7_IPT;  // 2048 keys
+constexpr int K7_RADIX = 5;  // digit bits of the block radix sort (44-bit keys: 9 passes; 6+ bits
+                              // would not leave room for 4 CTAs per SM)
 constexpr int K7_MAXCELLS = 3072;  // Khalimsky cells per image (28x28 -> 3025)
 constexpr int K7_MAXVOX = 1024;
 constexpr int K7_POOL = 1024;  // stored reduced columns (u64 keys)
@@ -40,8 +42,9 @@ struct K7Args {
   int dual;         // dimension 1 by Alexander duality (union-find over squares); else reduction
 };
 
-// Per-CTA shared memory.  DUAL (dimension 1 by duality, the default): no reduction buffers, so
-// more CTAs fit an SM.  pre: the next image's pixels, prefetched by cp.async while this one runs.
+// Per-CTA shared memory.  DUAL (dimension 1 by duality, the default): no reduction buffers and no
+// sort, so 4 CTAs fit an SM.  The union holds, in turn: the codes (step 2), the union-find
+// candidates with their per-root minima (steps 3, 4), the scan (step 5), the sort (reduction).
 struct K7Red {
   uint16_t owner[K7_MAXCELLS];
   uint64_t pool[K7_POOL];
@@ -51,8 +54,9 @@ struct K7Red {
 };
 struct K7Empty {};
 template <bool DUAL>
+constexpr int k7_cand() { return DUAL ? 1536 : K7_SORT; }  // union-find candidates per image
+template <bool DUAL>
 struct K7Smem {
-  uint32_t pre[K7_MAXVOX];
   uint32_t ord[K7_MAXVOX];
   uint32_t births[K7_MAXCELLS];
   uint32_t death[K7_MAXCELLS];
@@ -60,9 +64,15 @@ struct K7Smem {
   uint8_t tags[K7_MAXCELLS];
   typename std::conditional<DUAL, K7Empty, K7Red>::type red;
   union {  // the keys are held in registers while the sort uses its temporary storage
-    typename cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT>::TempStorage sort;
+    typename std::conditional<
+        DUAL, K7Empty,
+        typename cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT, cub::NullType,
+                                     K7_RADIX>::TempStorage>::type sort;
     typename cub::BlockScan<uint32_t, K7_THREADS>::TempStorage scan;
-    uint64_t keys[K7_SORT];
+    struct {
+      uint64_t keys[k7_cand<DUAL>()];  // candidates (compact keys), unsorted
+      uint64_t best[K7_MAXVOX];        // per root: the minimum (H0) / maximum (dual) candidate
+    };
   } tmp;
   uint32_t nkeys;
   uint32_t changed;
@@ -94,7 +104,7 @@ __device__ void k7_sort(SM& S, uint32_t n, bool desc) {
     it[r] = i < n ? S.tmp.keys[i] : (desc ? 0ull : (1ull << K7_SORT_BITS) - 1);
   }
   __syncthreads();
-  typedef cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT> BRS;
+  typedef cub::BlockRadixSort<uint64_t, K7_THREADS, K7_IPT, cub::NullType, K7_RADIX> BRS;
   if (desc) BRS(S.tmp.sort).SortDescending(it, 0, K7_SORT_BITS);
   else BRS(S.tmp.sort).Sort(it, 0, K7_SORT_BITS);
   __syncthreads();
@@ -129,39 +139,24 @@ __device__ uint32_t k7_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B,
   return n;
 }
 
-__device__ __forceinline__ void k7_cp4(uint32_t* dst, const float* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
-                   uint32_t(__cvta_generic_to_shared(dst))), "l"(src));
-}
 
-// Persistent CTAs: CTA b takes images b, b + gridDim.x, ...; once an image's pixels are turned
-// into ords, the next image's pixels are copied into S.pre by cp.async while this one is
-// processed (the load latency was a quarter of the stall samples with one image per CTA).
+// Persistent CTAs: CTA b takes images b, b + gridDim.x, ...
 template <bool DUAL>
 __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K7Smem<DUAL>& S = *reinterpret_cast<K7Smem<DUAL>*>(smem_raw);
   const int nx = A.nx, ny = A.ny, nvox = nx * ny;
   const int KX = 2 * nx - 1, KY = 2 * ny - 1, N = KX * KY;
-  auto prefetch = [&](int64_t im) {
-    if (im < A.batch)
-      for (int v = threadIdx.x; v < nvox; v += K7_THREADS) k7_cp4(&S.pre[v], A.images + im * nvox + v);
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-  prefetch(blockIdx.x);
   for (int64_t img = blockIdx.x; img < A.batch; img += gridDim.x) {
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
   // ---- 1. ords, births
   bool nan = false;
   for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
-    const float f = __uint_as_float(S.pre[v]);
+    const float f = __ldg(A.images + img * nvox + v);
     nan |= f != f;
     S.ord[v] = ord_of(f);
   }
   if (nan) atomicOr(A.flags, 1);
   __syncthreads();
-  prefetch(img + gridDim.x);  // S.pre is free again
   for (int k = threadIdx.x; k < N; k += K7_THREADS) {
     const int X = k % KX, Y = k / KX;
     uint32_t m = 0;
@@ -250,19 +245,24 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
     const int s = (X & 1) ? 1 : KX;
     const int a = k - s, b = k + s;
     const int va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
-    if (S.vpar[va] != S.vpar[vb]) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = sortkey(S, k);
+    if (S.vpar[va] != S.vpar[vb]) {
+      const uint32_t q = atomicAdd(&S.nkeys, 1u);
+      if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
+    }
   }
   __syncthreads();
   const uint32_t nc = S.nkeys;
-  k7_sort(S, nc, false);
-  // Elder-rule Kruskal over the sorted candidates as block-wide merge rounds (the rule of
-  // general.cu's k_mm_rounds: an edge commits when it is the minimum candidate at both of its
-  // components, or at the younger one alone -- the same merges as the sequential loop).  A
-  // candidate's minimum is its index in the sorted list; per-root minima live in S.ord (the ords
-  // are dead once the births exist).  Thread t owns candidates t + 256 r, r < K7_IPT.
+  if (nc > uint32_t(k7_cand<DUAL>())) {  // adversarial image: the stacked path takes the batch
+    if (threadIdx.x == 0) atomicOr(A.flags + 1, 1);
+    continue;
+  }
+  // Elder-rule Kruskal over the candidates as block-wide merge rounds (the rule of general.cu's
+  // k_mm_rounds: an edge commits when it is the minimum candidate at both of its components, or
+  // at the younger one alone -- the merges of the sequential Kruskal loop, with no sort: the
+  // per-root minima are taken on the compact keys).  Thread t owns candidates t + 256 r.
   {
-    uint32_t* best = S.ord;
-    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) best[v] = NONE32;
+    uint64_t* best = S.tmp.best;
+    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) best[v] = NONE64;
     uint32_t alive = 0;  // bit r: candidate t + 256 r undecided
 #pragma unroll
     for (int r = 0; r < K7_IPT; ++r)
@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
       for (int r = 0; r < K7_IPT; ++r) {
         if (!(alive >> r & 1)) continue;
         const uint32_t i = threadIdx.x + K7_THREADS * r;
-        const uint32_t k = sortcell(S.tmp.keys[i]);
+        const uint64_t key = S.tmp.keys[i];
+        const uint32_t k = sortcell(key);
         const int s1 = ((k % KX) & 1) ? 1 : KX;
         const int a = int(k) - s1, b = int(k) + s1;
         const uint32_t va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
@@ -287,8 +288,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
         ra[r] = uint16_t(x);
         rb[r] = uint16_t(y);
         any = true;
-        atomicMin(best + x, i);
-        atomicMin(best + y, i);
+        atomicMin((unsigned long long*)(best + x), (unsigned long long)key);
+        atomicMin((unsigned long long*)(best + y), (unsigned long long)key);
       }
       if (!__syncthreads_or(any)) break;
       uint32_t touched = alive;
@@ -296,15 +297,16 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
       for (int r = 0; r < K7_IPT; ++r) {
         if (!(alive >> r & 1)) continue;
         const uint32_t i = threadIdx.x + K7_THREADS * r;
+        const uint64_t key = S.tmp.keys[i];
         const uint32_t x = ra[r], y = rb[r];
-        const bool min_a = best[x] == i, min_b = best[y] == i;
+        const bool min_a = best[x] == key, min_b = best[y] == key;
         if (!min_a && !min_b) continue;
         const uint32_t kxa = 2 * (x / nx) * KX + 2 * (x % nx), kxb = 2 * (y / nx) * KX + 2 * (y % nx);
         const bool a_young = cellkey(S, kxa) > cellkey(S, kxb);
         if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) continue;
         const uint32_t young = a_young ? x : y, old = a_young ? y : x;
         const uint32_t ky = a_young ? kxa : kxb;
-        const uint32_t k = sortcell(S.tmp.keys[i]);
+        const uint32_t k = sortcell(key);
         S.vpar[young] = uint16_t(old);  // elder rule
         S.death[ky] = S.births[k] > S.births[ky] ? S.births[k] : D_ZERO;
         S.tags[k] = make_tag(KIND_CLEARED, 0);
@@ -314,8 +316,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
 #pragma unroll
       for (int r = 0; r < K7_IPT; ++r)
         if (touched >> r & 1) {
-          best[ra[r]] = NONE32;
-          best[rb[r]] = NONE32;
+          best[ra[r]] = NONE64;
+          best[rb[r]] = NONE64;
         }
       __syncthreads();
     }
@@ -389,24 +391,26 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
       const int X = k % KX, Y = k / KX;
       if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
       if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
-      if (dfind(side(k, 0)) != dfind(side(k, 1))) S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = sortkey(S, k);
+      if (dfind(side(k, 0)) != dfind(side(k, 1))) {
+        const uint32_t q = atomicAdd(&S.nkeys, 1u);
+        if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
+      }
     }
     __syncthreads();
     const uint32_t nc = S.nkeys;
-    k7_sort(S, nc, true);
-    // Kruskal over the dual edges (decreasing key) as block-wide merge rounds, the mirror of the
-    // H0 rounds above (the root with the LARGER key survives).  Per-root minima: square roots in
-    // the death slots of their squares (a 2D barcode never reads a square's death), OMEGA in
-    // S.changed.
+    if (nc > uint32_t(k7_cand<DUAL>())) {
+      if (threadIdx.x == 0) atomicOr(A.flags + 1, 1);
+      continue;
+    }
+    // Kruskal over the dual edges in decreasing key order as block-wide merge rounds, the mirror
+    // of the H0 rounds above: the per-root extremum is the MAXIMUM candidate key, and the root
+    // with the larger key survives.
     {
       auto rkey = [&](uint32_t v) -> uint64_t {
         return v == OMEGA ? NONE64 : cellkey(S, sq_of(v));
       };
-      auto bslot = [&](uint32_t v) -> uint32_t* {
-        return v == OMEGA ? &S.changed : &S.death[sq_of(v)];
-      };
-      for (int v = threadIdx.x; v <= nvox; v += K7_THREADS)
-        if (uint32_t(v) == OMEGA || ((v % nx) + 1 < nx && (v / nx) + 1 < ny)) *bslot(uint32_t(v)) = NONE32;
+      uint64_t* best = S.tmp.best;  // dual vertices 0..nvox (OMEGA = nvox < K7_MAXVOX)
+      for (int v = threadIdx.x; v <= nvox; v += K7_THREADS) best[v] = 0;
       uint32_t alive = 0;
 #pragma unroll
       for (int r = 0; r < K7_IPT; ++r)
@@ -419,7 +423,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
         for (int r = 0; r < K7_IPT; ++r) {
           if (!(alive >> r & 1)) continue;
           const uint32_t i = threadIdx.x + K7_THREADS * r;
-          const uint32_t e = sortcell(S.tmp.keys[i]);
+          const uint64_t key = S.tmp.keys[i];
+          const uint32_t e = sortcell(key);
           const uint32_t x = dfind(side(int(e), 0)), y = dfind(side(int(e), 1));
           if (x == y) {  // closes a cycle (a death of dimension 0)
             alive &= ~(1u << r);
@@ -428,8 +433,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
           ra[r] = x;
           rb[r] = y;
           any = true;
-          atomicMin(bslot(x), i);
-          atomicMin(bslot(y), i);
+          atomicMax((unsigned long long*)(best + x), (unsigned long long)key);
+          atomicMax((unsigned long long*)(best + y), (unsigned long long)key);
         }
         if (!__syncthreads_or(any)) break;
         const uint32_t touched = alive;
@@ -437,15 +442,16 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
         for (int r = 0; r < K7_IPT; ++r) {
           if (!(alive >> r & 1)) continue;
           const uint32_t i = threadIdx.x + K7_THREADS * r;
+          const uint64_t key = S.tmp.keys[i];
           const uint32_t x = ra[r], y = rb[r];
-          const bool min_a = *bslot(x) == i, min_b = *bslot(y) == i;
+          const bool min_a = best[x] == key, min_b = best[y] == key;
           if (!min_a && !min_b) continue;
           const uint64_t ka = rkey(x), kb = rkey(y);
           const bool a_young = ka < kb;
           if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) continue;
           const uint32_t young = a_young ? x : y, old = a_young ? y : x;
           const uint64_t ky = a_young ? ka : kb;
-          const uint32_t e = sortcell(S.tmp.keys[i]);
+          const uint32_t e = sortcell(key);
           dp[young] = old;
           if (key_ord(ky) == ABSENT_ORD) {
             S.death[e] = D_ESS;  // two absent regions meet: a hole that never fills
@@ -459,8 +465,8 @@ __global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
 #pragma unroll
         for (int r = 0; r < K7_IPT; ++r)
           if (touched >> r & 1) {
-            *bslot(ra[r]) = NONE32;
-            *bslot(rb[r]) = NONE32;
+            best[ra[r]] = 0;
+            best[rb[r]] = 0;
           }
         __syncthreads();
       }
