@@ -142,7 +142,7 @@ __device__ uint32_t k7_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B,
 
 // Persistent CTAs: CTA b takes images b, b + gridDim.x, ...
 template <bool DUAL>
-__global__ void __launch_bounds__(K7_THREADS) k7_image(K7Args A) {
+__global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K7Smem<DUAL>& S = *reinterpret_cast<K7Smem<DUAL>*>(smem_raw);
   const int nx = A.nx, ny = A.ny, nvox = nx * ny;
