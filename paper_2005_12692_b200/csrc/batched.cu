@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   K7Smem<DUAL>& S = *reinterpret_cast<K7Smem<DUAL>*>(smem_raw);
   const int nx = A.nx, ny = A.ny, nvox = nx * ny;
   const int KX = 2 * nx - 1, KY = 2 * ny - 1, N = KX * KY;
+  constexpr int KC = k7_cand<DUAL>() / K7_THREADS;  // candidate slots per thread
   for (int64_t img = blockIdx.x; img < A.batch; img += gridDim.x) {
   // ---- 1. ords, births
   bool nan = false;
@@ -265,14 +266,14 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
     for (int v = threadIdx.x; v < nvox; v += K7_THREADS) best[v] = NONE64;
     uint32_t alive = 0;  // bit r: candidate t + 256 r undecided
 #pragma unroll
-    for (int r = 0; r < K7_IPT; ++r)
+    for (int r = 0; r < KC; ++r)
       if (threadIdx.x + K7_THREADS * r < int(nc)) alive |= 1u << r;
-    uint16_t ra[K7_IPT], rb[K7_IPT];
+    uint16_t ra[KC], rb[KC];
     __syncthreads();
     while (true) {
       bool any = false;
 #pragma unroll
-      for (int r = 0; r < K7_IPT; ++r) {
+      for (int r = 0; r < KC; ++r) {
         if (!(alive >> r & 1)) continue;
         const uint32_t i = threadIdx.x + K7_THREADS * r;
         const uint64_t key = S.tmp.keys[i];
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       if (!__syncthreads_or(any)) break;
       uint32_t touched = alive;
 #pragma unroll
-      for (int r = 0; r < K7_IPT; ++r) {
+      for (int r = 0; r < KC; ++r) {
         if (!(alive >> r & 1)) continue;
         const uint32_t i = threadIdx.x + K7_THREADS * r;
         const uint64_t key = S.tmp.keys[i];
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       }
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < K7_IPT; ++r)
+      for (int r = 0; r < KC; ++r)
         if (touched >> r & 1) {
           best[ra[r]] = NONE64;
           best[rb[r]] = NONE64;
@@ -413,14 +414,14 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       for (int v = threadIdx.x; v <= nvox; v += K7_THREADS) best[v] = 0;
       uint32_t alive = 0;
 #pragma unroll
-      for (int r = 0; r < K7_IPT; ++r)
+      for (int r = 0; r < KC; ++r)
         if (threadIdx.x + K7_THREADS * r < int(nc)) alive |= 1u << r;
-      uint32_t ra[K7_IPT], rb[K7_IPT];
+      uint32_t ra[KC], rb[KC];
       __syncthreads();
       while (true) {
         bool any = false;
 #pragma unroll
-        for (int r = 0; r < K7_IPT; ++r) {
+        for (int r = 0; r < KC; ++r) {
           if (!(alive >> r & 1)) continue;
           const uint32_t i = threadIdx.x + K7_THREADS * r;
           const uint64_t key = S.tmp.keys[i];
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         if (!__syncthreads_or(any)) break;
         const uint32_t touched = alive;
 #pragma unroll
-        for (int r = 0; r < K7_IPT; ++r) {
+        for (int r = 0; r < KC; ++r) {
           if (!(alive >> r & 1)) continue;
           const uint32_t i = threadIdx.x + K7_THREADS * r;
           const uint64_t key = S.tmp.keys[i];
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         }
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < K7_IPT; ++r)
+        for (int r = 0; r < KC; ++r)
           if (touched >> r & 1) {
             best[ra[r]] = 0;
             best[rb[r]] = 0;
