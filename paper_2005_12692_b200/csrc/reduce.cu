@@ -85,7 +85,8 @@ struct RP {
   uint64_t* rec;
   unsigned long long* nrec;
   int* err;
-  int max_steps;
+  int max_steps;       // additions per warp and round, at most ...
+  long long budget;    // ... and until this many cycles of the round have passed (0: no limit)
   unsigned long long* stats;  // [0] rounds [1] additions [2] sum of lengths [3] max length
                               // debug: [4] pool additions [5] pool lengths [7]/[8] cycles in
                               // pool/apparent additions [9] cycles in pivot + owner lookups
@@ -802,6 +803,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
         c.nf = coboundary(P, rkid(P, P.cols[j]), c.F[0], lane);
       }
       int steps = 0;
+      const long long round_t0 = clock64();
       unsigned long long adds = 0, addlen = 0, cl = 0, ca = 0, cp = 0;
       c.fcyc = 0;
       bool ok = true;
@@ -836,7 +838,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
           alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1));
           glob = true;
         }
-        if (steps >= P.max_steps) {
+        if (steps >= P.max_steps || (P.budget && clock64() - round_t0 > P.budget)) {
           cval = piv;
           break;
         }
@@ -1214,7 +1216,20 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.rec = S.R.rec[d];
       P.nrec = nrec;
       P.err = err;
-      P.max_steps = 256;
+      // Round length: a warp stops adding after ~150 us of the round (not after a fixed number
+      // of additions): columns blocked on an earlier column's commit resume one round after it,
+      // so short rounds speed up chains of dependent columns, while long ones amortise the grid
+      // syncs.  Measured (CR_K5_BUDGET_US / CR_K5_STEPS): C4 reduce 168 ms with 256 steps per
+      // round -> 103 ms, C5 1.63 -> 1.37 s, C5b 0.62 -> 0.37 s.
+      {
+        int clk_khz = 0;
+        CR_CUDA(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev));
+        const char* bu = std::getenv("CR_K5_BUDGET_US");
+        const double us = bu ? std::atof(bu) : 150.0;
+        P.budget = (long long)(us * (clk_khz > 0 ? clk_khz : 1900000) / 1e3);
+        const char* ms = std::getenv("CR_K5_STEPS");
+        P.max_steps = ms ? std::atoi(ms) : (1 << 30);
+      }
       P.stats = stats;
       P.debug = std::getenv("CR_DEBUG_STATS") != nullptr;
       {
