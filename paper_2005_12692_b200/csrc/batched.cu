@@ -148,6 +148,9 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   const int nx = A.nx, ny = A.ny, nvox = nx * ny;
   const int KX = 2 * nx - 1, KY = 2 * ny - 1, N = KX * KY;
   constexpr int KC = k7_cand<DUAL>() / K7_THREADS;  // candidate slots per thread
+  // exact quotient by KX (operands < 2^12) with one multiply-high
+  const uint64_t mKX = ((1ull << 32) + KX - 1) / KX;
+  auto dKX = [&](int c) { return int((uint64_t(uint32_t(c)) * mKX) >> 32); };
   for (int64_t img = blockIdx.x; img < A.batch; img += gridDim.x) {
   // ---- 1. ords, births
   bool nan = false;
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   if (nan) atomicOr(A.flags, 1);
   __syncthreads();
   for (int k = threadIdx.x; k < N; k += K7_THREADS) {
-    const int X = k % KX, Y = k / KX;
+    const int Y = dKX(k), X = k - Y * KX;
     uint32_t m = 0;
     for (int y = Y >> 1; y <= (Y + 1) >> 1; ++y)
       for (int x = X >> 1; x <= (X + 1) >> 1; ++x) m = max(m, S.ord[y * nx + x]);
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
     const uint32_t b = S.births[k];
     uint32_t c = 0x40;  // absent
     if (b != ABSENT_ORD) {
-      const int X = k % KX, Y = k / KX;
+      const int Y = dKX(k), X = k - Y * KX;
       const bool ox = X & 1, oy = Y & 1;
       const uint32_t ym = Y > 0 ? S.births[k - KX] : ABSENT_ORD;
       const uint32_t xm = X > 0 ? S.births[k - 1] : ABSENT_ORD;
