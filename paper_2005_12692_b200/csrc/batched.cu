@@ -151,6 +151,10 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   // exact quotient by KX (operands < 2^12) with one multiply-high
   const uint64_t mKX = ((1ull << 32) + KX - 1) / KX;
   auto dKX = [&](int c) { return int((uint64_t(uint32_t(c)) * mKX) >> 32); };
+  auto vox = [&](int c) {  // base voxel of cell c
+    const int Y = dKX(c);
+    return (Y >> 1) * nx + ((c - Y * KX) >> 1);
+  };
   for (int64_t img = blockIdx.x; img < A.batch; img += gridDim.x) {
   // ---- 1. ords, births
   bool nan = false;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
     if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
     const int s = (X & 1) ? 1 : KX;
     const int a = k - s, b = k + s;
-    const int va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
+    const int va = vox(a), vb = vox(b);
     if (S.vpar[va] != S.vpar[vb]) {
       const uint32_t q = atomicAdd(&S.nkeys, 1u);
       if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         const uint32_t k = sortcell(key);
         const int s1 = ((k % KX) & 1) ? 1 : KX;
         const int a = int(k) - s1, b = int(k) + s1;
-        const uint32_t va = (a / KX / 2) * nx + (a % KX) / 2, vb = (b / KX / 2) * nx + (b % KX) / 2;
+        const uint32_t va = vox(a), vb = vox(b);
         const uint32_t x = k7_find(S.vpar, va), y = k7_find(S.vpar, vb);
         if (x == y) {  // positive edge: closes a cycle of older edges
           alive &= ~(1u << r);
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         if (sg ? X + 1 >= KX : X == 0) return OMEGA;
         q = e + (sg ? 1 : -1);
       }
-      return uint32_t((q / KX / 2) * nx + (q % KX) / 2);
+      return uint32_t(vox(q));
     };
     for (int v = threadIdx.x; v <= nvox; v += K7_THREADS) {
       uint32_t p = uint32_t(v);
