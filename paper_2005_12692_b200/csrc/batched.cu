@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
     __syncthreads();
   } while (S.changed);
   for (int k = threadIdx.x; k < N; k += K7_THREADS) {
-    const int X = k % KX, Y = k / KX;
+    const int Y = dKX(k), X = k - Y * KX;
     if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
     if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
     const int s = (X & 1) ? 1 : KX;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         const uint32_t i = threadIdx.x + K7_THREADS * r;
         const uint64_t key = S.tmp.keys[i];
         const uint32_t k = sortcell(key);
-        const int s1 = ((k % KX) & 1) ? 1 : KX;
+        const int s1 = ((int(k) - dKX(int(k)) * KX) & 1) ? 1 : KX;
         const int a = int(k) - s1, b = int(k) + s1;
         const uint32_t va = vox(a), vb = vox(b);
         const uint32_t x = k7_find(S.vpar, va), y = k7_find(S.vpar, vb);
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       return (2 * (v / nx) + 1) * KX + 2 * (v % nx) + 1;
     };
     auto side = [&](int e, int sg) -> uint32_t {  // dual vertex on side sg of edge e
-      const int X = e % KX, Y = e / KX;
+      const int Y = dKX(e), X = e - Y * KX;
       int q;
       if (X & 1) {  // horizontal edge: squares above/below
         if (sg ? Y + 1 >= KY : Y == 0) return OMEGA;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       }
     };
     for (int k = threadIdx.x; k < N; k += K7_THREADS) {  // absent faces join absent sides
-      const int X = k % KX, Y = k / KX;
+      const int Y = dKX(k), X = k - Y * KX;
       if (((X & 1) + (Y & 1)) != 1 || S.births[k] != ABSENT_ORD) continue;
       uint32_t a = side(k, 0), b = side(k, 1);
       while (true) {
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
     }
     __syncthreads();
     for (int k = threadIdx.x; k < N; k += K7_THREADS) {  // residual edges between components
-      const int X = k % KX, Y = k / KX;
+      const int Y = dKX(k), X = k - Y * KX;
       if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
       if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
       if (dfind(side(k, 0)) != dfind(side(k, 1))) {
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
    if constexpr (!DUAL) {
     auto& R = S.red;
     for (int k = threadIdx.x; k < N; k += K7_THREADS) {
-      const int X = k % KX, Y = k / KX;
+      const int Y = dKX(k), X = k - Y * KX;
       if (((X & 1) + (Y & 1)) == 1 && S.births[k] != ABSENT_ORD &&
           tag_kind(S.tags[k]) == KIND_RESIDUAL)
         S.tmp.keys[atomicAdd(&S.nkeys, 1u)] = sortkey(S, k);
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         const uint32_t sk = sortcell(S.tmp.keys[ci]);
         // coboundary: the finite squares on both sides of the edge
         auto cob = [&](uint32_t e, uint64_t* dst) -> uint32_t {
-          const int X = e % KX, Y = e / KX;
+          const int Y = dKX(e), X = e - Y * KX;
           uint32_t n = 0;
           uint64_t c0 = NONE64, c1 = NONE64;
           if (X & 1) {  // horizontal edge: squares above and below
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   for (int q = 0; q < CPT; ++q) {
     const int k = k0 + q;
     if (k >= N) break;
-    const int X = k % KX, Y = k / KX, dim = (X & 1) + (Y & 1);
+    const int Y = dKX(k), X = k - Y * KX, dim = (X & 1) + (Y & 1);
     const uint32_t d = S.death[k];
     if (dim <= dmx && d != D_NONE && d != D_ZERO) {
       keepm |= 1u << q;
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   for (int q = 0; q < CPT; ++q) {
     if (!(keepm >> q & 1)) continue;
     const int k = k0 + q;
-    const int dim = ((k % KX) & 1) + ((k / KX) & 1);
+    const int Yk = dKX(k), dim = ((k - Yk * KX) & 1) + (Yk & 1);
     const uint32_t o = dim ? o1++ : o0++;
     if (int(o) < A.cap) {
       const uint32_t d = S.death[k];
