@@ -165,15 +165,30 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   }
   if (nan) atomicOr(A.flags, 1);
   __syncthreads();
-  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
-    const int Y = dKX(k), X = k - Y * KX;
-    uint32_t m = 0;
-    for (int y = Y >> 1; y <= (Y + 1) >> 1; ++y)
-      for (int x = X >> 1; x <= (X + 1) >> 1; ++x) m = max(m, S.ord[y * nx + x]);
-    S.births[k] = m;
+  // per voxel (x, y): its vertex and the edges / square toward x+1, y+1
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const int y = v / nx, x = v - y * nx;
+    const bool hx = x + 1 < nx, hy = y + 1 < ny;
+    const uint32_t a = S.ord[v], ax = hx ? S.ord[v + 1] : 0u, ay = hy ? S.ord[v + nx] : 0u,
+                   axy = (hx && hy) ? S.ord[v + nx + 1] : 0u;
+    const int k = 2 * y * KX + 2 * x;
+    S.births[k] = a;
     S.death[k] = D_NONE;
-    if constexpr (!DUAL) S.red.owner[k] = 0xFFFFu;
+    if (hx) {
+      S.births[k + 1] = max(a, ax);
+      S.death[k + 1] = D_NONE;
+    }
+    if (hy) {
+      S.births[k + KX] = max(a, ay);
+      S.death[k + KX] = D_NONE;
+      if (hx) {
+        S.births[k + KX + 1] = max(max(a, ax), max(ay, axy));
+        S.death[k + KX + 1] = D_NONE;
+      }
+    }
   }
+  if constexpr (!DUAL)
+    for (int k = threadIdx.x; k < N; k += K7_THREADS) S.red.owner[k] = 0xFFFFu;
   __syncthreads();
   // ---- 2. apparent pairs, as in general.cu's k_filtration: a code per cell
   // (direction of the first equal-birth cofacet, of the last equal-birth facet, in kidx order
