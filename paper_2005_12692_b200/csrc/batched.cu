@@ -151,6 +151,8 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   // exact quotient by KX (operands < 2^12) with one multiply-high
   const uint64_t mKX = ((1ull << 32) + KX - 1) / KX;
   auto dKX = [&](int c) { return int((uint64_t(uint32_t(c)) * mKX) >> 32); };
+  const uint64_t mNX = ((1ull << 32) + nx - 1) / nx;
+  auto dNX = [&](int v) { return int((uint64_t(uint32_t(v)) * mNX) >> 32); };
   auto vox = [&](int c) {  // base voxel of cell c
     const int Y = dKX(c);
     return (Y >> 1) * nx + ((c - Y * KX) >> 1);
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   __syncthreads();
   // per voxel (x, y): its vertex and the edges / square toward x+1, y+1
   for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
-    const int y = v / nx, x = v - y * nx;
+    const int y = dNX(v), x = v - y * nx;
     const bool hx = x + 1 < nx, hy = y + 1 < ny;
     const uint32_t a = S.ord[v], ax = hx ? S.ord[v + 1] : 0u, ay = hy ? S.ord[v + nx] : 0u,
                    axy = (hx && hy) ? S.ord[v + nx + 1] : 0u;
@@ -261,16 +263,18 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
     }
     __syncthreads();
   } while (S.changed);
-  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
-    const int Y = dKX(k), X = k - Y * KX;
-    if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
-    if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
-    const int s = (X & 1) ? 1 : KX;
-    const int a = k - s, b = k + s;
-    const int va = vox(a), vb = vox(b);
-    if (S.vpar[va] != S.vpar[vb]) {
-      const uint32_t q = atomicAdd(&S.nkeys, 1u);
-      if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
+  // residual edges joining different basins, enumerated per voxel: (v, v+1) and (v, v+nx)
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const int y = dNX(v), x = v - y * nx, kv = 2 * y * KX + 2 * x;
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      if (o == 0 ? x + 1 >= nx : y + 1 >= ny) continue;
+      const int k = kv + (o == 0 ? 1 : KX), vb = v + (o == 0 ? 1 : nx);
+      if (S.births[k] == ABSENT_ORD || tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
+      if (S.vpar[v] != S.vpar[vb]) {
+        const uint32_t q = atomicAdd(&S.nkeys, 1u);
+        if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
+      }
     }
   }
   __syncthreads();
@@ -397,26 +401,35 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         x = qq;
       }
     };
-    for (int k = threadIdx.x; k < N; k += K7_THREADS) {  // absent faces join absent sides
-      const int Y = dKX(k), X = k - Y * KX;
-      if (((X & 1) + (Y & 1)) != 1 || S.births[k] != ABSENT_ORD) continue;
-      uint32_t a = side(k, 0), b = side(k, 1);
-      while (true) {
-        a = dfind(a);
-        b = dfind(b);
-        if (a == b) break;
-        if (a > b) { const uint32_t t = a; a = b; b = t; }
-        if (atomicCAS(dp + a, a, b) == a) break;
+    // edges enumerated per voxel: (v, v+1) and (v, v+nx)
+    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {  // absent faces join absent sides
+      const int y = dNX(v), x = v - y * nx, kv = 2 * y * KX + 2 * x;
+      for (int o = 0; o < 2; ++o) {
+        if (o == 0 ? x + 1 >= nx : y + 1 >= ny) continue;
+        const int k = kv + (o == 0 ? 1 : KX);
+        if (S.births[k] != ABSENT_ORD) continue;
+        uint32_t a = side(k, 0), b = side(k, 1);
+        while (true) {
+          a = dfind(a);
+          b = dfind(b);
+          if (a == b) break;
+          if (a > b) { const uint32_t t = a; a = b; b = t; }
+          if (atomicCAS(dp + a, a, b) == a) break;
+        }
       }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < N; k += K7_THREADS) {  // residual edges between components
-      const int Y = dKX(k), X = k - Y * KX;
-      if (((X & 1) + (Y & 1)) != 1 || S.births[k] == ABSENT_ORD) continue;
-      if (tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
-      if (dfind(side(k, 0)) != dfind(side(k, 1))) {
-        const uint32_t q = atomicAdd(&S.nkeys, 1u);
-        if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
+    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {  // residual edges between components
+      const int y = dNX(v), x = v - y * nx, kv = 2 * y * KX + 2 * x;
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        if (o == 0 ? x + 1 >= nx : y + 1 >= ny) continue;
+        const int k = kv + (o == 0 ? 1 : KX);
+        if (S.births[k] == ABSENT_ORD || tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
+        if (dfind(side(k, 0)) != dfind(side(k, 1))) {
+          const uint32_t q = atomicAdd(&S.nkeys, 1u);
+          if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
+        }
       }
     }
     __syncthreads();
