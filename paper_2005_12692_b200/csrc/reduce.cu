@@ -738,7 +738,10 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, 
   return true;
 }
 
-__global__ void __launch_bounds__(THREADS, 4) k_reduce(RP P) {
+#ifndef K5_MINB
+#define K5_MINB 4
+#endif
+__global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s_F[WPB][2][FCAP];
   __shared__ uint64_t s_small[WPB][8];
