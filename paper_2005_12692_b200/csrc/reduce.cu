@@ -42,7 +42,10 @@ namespace {
 
 constexpr int WPB = 8;  // warps per block
 constexpr int THREADS = WPB * 32;
-constexpr uint32_t FCAP = 256;  // fresh-array capacity per warp (shared memory, x2 ping-pong)
+#ifndef K5_FCAP
+#define K5_FCAP 256
+#endif
+constexpr uint32_t FCAP = K5_FCAP;  // fresh-array capacity per warp (shared memory, x2 ping-pong)
 
 // n / d for n, d < 2^32 by one 64-bit high multiply: m = ceil(2^64 / d) makes the quotient exact
 // (the error n * (m - 2^64/d) / 2^64 < 2^-32 cannot carry past the fractional part (d-1)/d).
