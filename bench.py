@@ -343,6 +343,16 @@ def run_ours(args, rank, world, local_rank):
                 "alg_bytes_per_launch": alg, "avg_ms": round(stage_avg[dom], 5),
                 "peak_source": peak_src}
         roof.update(ncu_traffic(dom))
+        # The same kernel against the instruction-issue ceiling: warp instructions
+        # per launch (ncu) / the live launch time, vs 148 SMs x 4 schedulers x 1 warp-instruction
+        # per clock at the sampled SM clock.  The 1D and the fused K1+K2 kernels are issue-bound.
+        wi = roof.pop("warp_instructions", None)
+        if wi:
+            mhz = (clocks or {}).get("sm_mhz") or 1965.0
+            ipeak = 148 * 4 * mhz * 1e6 / 1e9  # G warp-instructions/s
+            iach = wi / (stage_avg[dom] / 1e3) / 1e9
+            roof["issue"] = {"achieved": round(iach, 1), "peak": round(ipeak, 1),
+                             "unit": "G warp-inst/s", "frac": round(iach / ipeak, 4)}
     out = {
         "metric": METRIC, "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -417,8 +427,11 @@ def ncu_traffic(stage):
         try:
             with open(p) as f:
                 d = json.load(f)["kernels"][k]
-            return {"traffic": round((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6),
-                    "traffic_source": os.path.relpath(p, ROOT)}
+            out = {"traffic": round((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6),
+                   "traffic_source": os.path.relpath(p, ROOT)}
+            if "warp_instructions" in d:
+                out["warp_instructions"] = int(float(d["warp_instructions"]))
+            return out
         except (KeyError, OSError, ValueError):
             continue
     return {}
