@@ -553,7 +553,21 @@ def test_stats_counters_match_definitions(cr, monkeypatch):
             gen.small_int_image((50, 45), 5, seed=84, inf_frac=0.05)]
     for k, img in enumerate(imgs):
         exp = ap.counts(img)
-        o = oracle.ph(img, img.ndim - 1)
+        o = oracle.ph(img, img.ndim - 1, partner=True)
+        # K5 columns of dimension d (cohomology, d < D-1): d-cells that are neither apparent nor
+        # the death cell of a (d-1)-pair -- from the oracle's pairing and the definition
+        up, dims, finite = ap.apparent_up(img)
+        part = o.partner.astype(np.int64)
+        flat_dims = dims.ravel()
+        app_any = up.ravel().copy()
+        for s_, t_ in ap.pairs_up(img):
+            app_any[t_] = True
+        is_cell = finite.ravel()
+        paired = (part < len(part))
+        partner_dim = np.where(paired, flat_dims[np.minimum(part, len(part) - 1)], -1)
+        cols_exp = [int(np.count_nonzero(is_cell & (flat_dims == d) & ~app_any &
+                                         ~(paired & (partner_dim == d - 1))))
+                    for d in range(4)]
         t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
         for var in ("", "CR_K12_OLD"):
             if var:
@@ -565,5 +579,7 @@ def test_stats_counters_match_definitions(cr, monkeypatch):
             assert st["columns"][0] == exp["basins"], (k, var, st["columns"][0], exp["basins"])
             nb = [int(np.count_nonzero(o.dim == d)) for d in range(img.ndim)]
             assert list(st["pairs"])[:img.ndim] == nb, (k, var, st["pairs"], nb)
+            for d in range(1, img.ndim - 1):  # the top dimension runs by duality (roots)
+                assert st["columns"][d] == cols_exp[d], (k, var, d, st["columns"], cols_exp)
             if var:
                 monkeypatch.delenv(var)
