@@ -88,6 +88,7 @@ struct RP {
   uint64_t* rec;
   unsigned long long* nrec;
   int* err;
+  int ahead;           // read-ahead of the next column (see phase A)
   int max_steps;       // additions per warp and round, at most ...
   long long budget;    // ... and until this many cycles of the round have passed (0: no limit)
   unsigned long long* stats;  // [0] rounds [1] additions [2] sum of lengths [3] max length
@@ -785,7 +786,10 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
 
   for (uint32_t round = 0;; ++round) {
     // ---------------- phase A: advance my column
-    if (fin && j < lo) {
+    // Read-ahead: a warp whose column is finished takes its next column j + G at once, even if
+    // the window has not reached it yet: it reduces it with the owners committed so far (always
+    // valid) and only publishes / commits once the column is inside the window.
+    if (fin && (j < lo || P.ahead)) {
       j += G;
       started = false;
       fin = false;
@@ -912,6 +916,8 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     const uint32_t q = j - lo;
     const uint32_t qg = grp * G + q;
     if (lane == 0 && grp < P.ngroups && q < G) P.cand[qg] = (j < end && !fin) ? cval : NONE64;
+    // a read-ahead warp still owns its finished previous column's position
+    if (lane == 0 && grp < P.ngroups && q >= G && q - G < G) P.cand[qg - G] = NONE64;
     grid.sync();
 
     // ---------------- phase B: segmented minima of the window's chunks of WPB positions
@@ -1234,6 +1240,8 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
         const char* bu = std::getenv("CR_K5_BUDGET_US");
         const double us = bu ? std::atof(bu) : 150.0;
         P.budget = (long long)(us * (clk_khz > 0 ? clk_khz : 1900000) / 1e3);
+        const char* ah = std::getenv("CR_K5_AHEAD");
+        P.ahead = ah ? std::atoi(ah) : 1;
         const char* ms = std::getenv("CR_K5_STEPS");
         P.max_steps = ms ? std::atoi(ms) : (1 << 30);
       }
