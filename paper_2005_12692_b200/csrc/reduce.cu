@@ -1158,7 +1158,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce, THREADS, 0));
     if (per_sm < 1) throw Error{CR_EINTERNAL, "k_reduce cannot be resident"};
-    per_sm = per_sm > 4 ? 4 : per_sm;
+    per_sm = per_sm > K5_MINB ? K5_MINB : per_sm;
     if (const char* e = std::getenv("CR_K5_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     int64_t blocks = int64_t(nsm) * per_sm;
     const int64_t need_blocks = (int64_t(ncols) + WPB - 1) / WPB;  // small problems
