@@ -1229,16 +1229,17 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.rec = S.R.rec[d];
       P.nrec = nrec;
       P.err = err;
-      // Round length: a warp stops adding after ~150 us of the round (not after a fixed number
+      // Round length: a warp stops adding after ~100 us of the round (not after a fixed number
       // of additions): columns blocked on an earlier column's commit resume one round after it,
       // so short rounds speed up chains of dependent columns, while long ones amortise the grid
       // syncs.  Measured (CR_K5_BUDGET_US / CR_K5_STEPS): C4 reduce 168 ms with 256 steps per
-      // round -> 103 ms, C5 1.63 -> 1.37 s, C5b 0.62 -> 0.37 s.
+      // round -> 103 ms, C5 1.63 -> 1.37 s, C5b 0.62 -> 0.37 s; with read-ahead 100 us is best
+      // on C4 (100 / 106 / 118 ms at 100 / 150 / 250 us; C5, C5b within run-to-run noise).
       {
         int clk_khz = 0;
         CR_CUDA(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev));
         const char* bu = std::getenv("CR_K5_BUDGET_US");
-        const double us = bu ? std::atof(bu) : 150.0;
+        const double us = bu ? std::atof(bu) : 100.0;
         P.budget = (long long)(us * (clk_khz > 0 ? clk_khz : 1900000) / 1e3);
         const char* ah = std::getenv("CR_K5_AHEAD");
         P.ahead = ah ? std::atoi(ah) : 1;
