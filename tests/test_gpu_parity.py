@@ -583,3 +583,26 @@ def test_stats_counters_match_definitions(cr, monkeypatch):
                 assert st["columns"][d] == cols_exp[d], (k, var, d, st["columns"], cols_exp)
             if var:
                 monkeypatch.delenv(var)
+
+
+def test_k5_schedule_independence(cr, monkeypatch):
+    """The dims >= 1 reduction's pairing does not depend on its schedule (the commit rule of
+    DESIGN.md §6): read-ahead on/off, rounds of one addition, tiny and large time budgets, and one
+    resident block per SM all give the oracle's pairing."""
+    import torch
+    imgs = [gen.masked_grf((20, 22, 24), 2.0, 10.0, 91),
+            gen.small_int_image((9, 16, 13), 3, seed=92, inf_frac=0.1),
+            gen.grf((18, 17, 19), 1.5, 93)]
+    knobs = [{}, {"CR_K5_AHEAD": "0"}, {"CR_K5_STEPS": "1"}, {"CR_K5_BUDGET_US": "2"},
+             {"CR_K5_BUDGET_US": "5000", "CR_K5_AHEAD": "0"}, {"CR_K5_PER_SM": "1"},
+             {"CR_K5_HOM": "1", "CR_K5_STEPS": "3"}]
+    for k, img in enumerate(imgs):
+        o = oracle.ph(img, 2, partner=True)
+        t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        for kn in knobs:
+            for v in ("CR_K5_AHEAD", "CR_K5_STEPS", "CR_K5_BUDGET_US", "CR_K5_PER_SM", "CR_K5_HOM"):
+                monkeypatch.delenv(v, raising=False)
+            for a, b in kn.items():
+                monkeypatch.setenv(a, b)
+            p = cr.pairing(t).cpu().numpy().view(np.uint32)
+            assert np.array_equal(p, o.partner), (k, kn, np.flatnonzero(p != o.partner)[:10])
