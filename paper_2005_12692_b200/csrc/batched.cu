@@ -288,8 +288,12 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   // at the younger one alone -- the merges of the sequential Kruskal loop, with no sort: the
   // per-root minima are taken on the compact keys).  Thread t owns candidates t + 256 r.
   {
+    // per-root extremum of round `rnd`, round-tagged so that no reset phase is needed:
+    // (rnd << 44) | (~key & mask44) under atomicMax = the minimum key of the newest round
     uint64_t* best = S.tmp.best;
-    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) best[v] = NONE64;
+    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) best[v] = 0;
+    constexpr uint64_t KM = (1ull << K7_SORT_BITS) - 1;
+    uint64_t rnd = 0;
     uint32_t alive = 0;  // bit r: candidate t + 256 r undecided
 #pragma unroll
     for (int r = 0; r < KC; ++r)
@@ -315,18 +319,19 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         ra[r] = uint16_t(x);
         rb[r] = uint16_t(y);
         any = true;
-        atomicMin((unsigned long long*)(best + x), (unsigned long long)key);
-        atomicMin((unsigned long long*)(best + y), (unsigned long long)key);
+        const unsigned long long tk = (rnd << K7_SORT_BITS) | (~key & KM);
+        atomicMax((unsigned long long*)(best + x), tk);
+        atomicMax((unsigned long long*)(best + y), tk);
       }
       if (!__syncthreads_or(any)) break;
-      uint32_t touched = alive;
 #pragma unroll
       for (int r = 0; r < KC; ++r) {
         if (!(alive >> r & 1)) continue;
         const uint32_t i = threadIdx.x + K7_THREADS * r;
         const uint64_t key = S.tmp.keys[i];
         const uint32_t x = ra[r], y = rb[r];
-        const bool min_a = best[x] == key, min_b = best[y] == key;
+        const uint64_t tk = (rnd << K7_SORT_BITS) | (~key & KM);
+        const bool min_a = best[x] == tk, min_b = best[y] == tk;
         if (!min_a && !min_b) continue;
         const uint32_t kxa = 2 * (x / nx) * KX + 2 * (x % nx), kxb = 2 * (y / nx) * KX + 2 * (y % nx);
         const bool a_young = cellkey(S, kxa) > cellkey(S, kxb);
@@ -339,13 +344,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
         S.tags[k] = make_tag(KIND_CLEARED, 0);
         alive &= ~(1u << r);
       }
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < KC; ++r)
-        if (touched >> r & 1) {
-          best[ra[r]] = NONE64;
-          best[rb[r]] = NONE64;
-        }
+      ++rnd;
       __syncthreads();
     }
   }
@@ -447,6 +446,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       };
       uint64_t* best = S.tmp.best;  // dual vertices 0..nvox (OMEGA = nvox < K7_MAXVOX)
       for (int v = threadIdx.x; v <= nvox; v += K7_THREADS) best[v] = 0;
+      uint64_t rnd = 0;  // round-tagged maxima: (rnd << 44) | key, no reset phase
       uint32_t alive = 0;
 #pragma unroll
       for (int r = 0; r < KC; ++r)
@@ -469,18 +469,19 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
           ra[r] = x;
           rb[r] = y;
           any = true;
-          atomicMax((unsigned long long*)(best + x), (unsigned long long)key);
-          atomicMax((unsigned long long*)(best + y), (unsigned long long)key);
+          const unsigned long long tk = (rnd << K7_SORT_BITS) | key;
+          atomicMax((unsigned long long*)(best + x), tk);
+          atomicMax((unsigned long long*)(best + y), tk);
         }
         if (!__syncthreads_or(any)) break;
-        const uint32_t touched = alive;
 #pragma unroll
         for (int r = 0; r < KC; ++r) {
           if (!(alive >> r & 1)) continue;
           const uint32_t i = threadIdx.x + K7_THREADS * r;
           const uint64_t key = S.tmp.keys[i];
           const uint32_t x = ra[r], y = rb[r];
-          const bool min_a = best[x] == key, min_b = best[y] == key;
+          const uint64_t tk = (rnd << K7_SORT_BITS) | key;
+          const bool min_a = best[x] == tk, min_b = best[y] == tk;
           if (!min_a && !min_b) continue;
           const uint64_t ka = rkey(x), kb = rkey(y);
           const bool a_young = ka < kb;
@@ -497,13 +498,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
           }
           alive &= ~(1u << r);
         }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < KC; ++r)
-          if (touched >> r & 1) {
-            best[ra[r]] = 0;
-            best[rb[r]] = 0;
-          }
+        ++rnd;
         __syncthreads();
       }
     }
