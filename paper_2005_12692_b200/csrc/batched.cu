@@ -250,19 +250,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   }
   if (threadIdx.x == 0) S.nkeys = 0;
   __syncthreads();
-  do {  // pointer jumping
-    __syncthreads();
-    if (threadIdx.x == 0) S.changed = 0;
-    __syncthreads();
-    for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
-      const uint16_t p = S.vpar[v], pp = S.vpar[p];
-      if (p != pp) {
-        S.vpar[v] = pp;
-        S.changed = 1;
-      }
-    }
-    __syncthreads();
-  } while (S.changed);
+  // (no flattening pass: the roots below come from finds with path halving)
   // residual edges joining different basins, enumerated per voxel: (v, v+1) and (v, v+nx)
   for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
     const int y = dNX(v), x = v - y * nx, kv = 2 * y * KX + 2 * x;
@@ -271,7 +259,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       if (o == 0 ? x + 1 >= nx : y + 1 >= ny) continue;
       const int k = kv + (o == 0 ? 1 : KX), vb = v + (o == 0 ? 1 : nx);
       if (S.births[k] == ABSENT_ORD || tag_kind(S.tags[k]) != KIND_RESIDUAL) continue;
-      if (S.vpar[v] != S.vpar[vb]) {
+      if (k7_find(S.vpar, v) != k7_find(S.vpar, vb)) {
         const uint32_t q = atomicAdd(&S.nkeys, 1u);
         if (q < uint32_t(k7_cand<DUAL>())) S.tmp.keys[q] = sortkey(S, k);
       }
