@@ -140,6 +140,30 @@ __device__ uint32_t k7_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B,
 }
 
 
+// Code of a 2D cell k with parities (OX, OY) (the rule of k_filtration): the first equal-birth
+// cofacet in kidx order (-Y < -X < +X < +Y) and the last equal-birth facet; h*: the neighbour in
+// that direction is inside the grid (facets of a present cell always are).
+template <bool OX, bool OY, class SM>
+__device__ __forceinline__ uint32_t k7_code(const SM& S, int k, int KX, bool hxm, bool hxp,
+                                            bool hym, bool hyp) {
+  const uint32_t b = S.births[k];
+  if (b == ABSENT_ORD) return 0x40;
+  const uint32_t ym = hym ? S.births[k - KX] : ABSENT_ORD;
+  const uint32_t xm = hxm ? S.births[k - 1] : ABSENT_ORD;
+  const uint32_t xp = hxp ? S.births[k + 1] : ABSENT_ORD;
+  const uint32_t yp = hyp ? S.births[k + KX] : ABSENT_ORD;
+  uint32_t mc = 7, mf = 7;
+  if (!OY && yp == b) mc = 3;
+  if (!OX && xp == b) mc = 1;
+  if (!OX && xm == b) mc = 0;
+  if (!OY && ym == b) mc = 2;
+  if (OY && ym == b) mf = 2;
+  if (OX && xm == b) mf = 0;
+  if (OX && xp == b) mf = 1;
+  if (OY && yp == b) mf = 3;
+  return mc | (mf << 3);
+}
+
 // Persistent CTAs: CTA b takes images b, b + gridDim.x, ...
 template <bool DUAL>
 __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
@@ -198,33 +222,19 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
   // facet points back, else DOWN iff the max facet's min cofacet points back.  The codes use the
   // sort buffer (free until the H0 sort).
   uint8_t* code = reinterpret_cast<uint8_t*>(S.tmp.keys);
-  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
-    const uint32_t b = S.births[k];
-    uint32_t c = 0x40;  // absent
-    if (b != ABSENT_ORD) {
-      const int Y = dKX(k), X = k - Y * KX;
-      const bool ox = X & 1, oy = Y & 1;
-      const uint32_t ym = Y > 0 ? S.births[k - KX] : ABSENT_ORD;
-      const uint32_t xm = X > 0 ? S.births[k - 1] : ABSENT_ORD;
-      const uint32_t xp = X + 1 < KX ? S.births[k + 1] : ABSENT_ORD;
-      const uint32_t yp = Y + 1 < KY ? S.births[k + KX] : ABSENT_ORD;
-      uint32_t mc = 7, mf = 7;
-      // cofacets (even axes): the first equal one -- scan backwards
-      if (!oy && yp == b) mc = 3;
-      if (!ox && xp == b) mc = 1;
-      if (!ox && xm == b) mc = 0;
-      if (!oy && ym == b) mc = 2;
-      // facets (odd axes; present cells have present facets): the last equal one
-      if (oy && ym == b) mf = 2;
-      if (ox && xm == b) mf = 0;
-      if (ox && xp == b) mf = 1;
-      if (oy && yp == b) mf = 3;
-      c = mc | (mf << 3);
+  // per voxel: its vertex, edges toward x+1 / y+1 and square (static parities, no division)
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const int y = dNX(v), x = v - y * nx, k = 2 * y * KX + 2 * x;
+    const bool hx = x + 1 < nx, hy = y + 1 < ny, lx = x > 0, ly = y > 0;
+    code[k] = uint8_t(k7_code<false, false>(S, k, KX, lx, hx, ly, hy));
+    if (hx) code[k + 1] = uint8_t(k7_code<true, false>(S, k + 1, KX, true, true, ly, hy));
+    if (hy) {
+      code[k + KX] = uint8_t(k7_code<false, true>(S, k + KX, KX, lx, hx, true, true));
+      if (hx) code[k + KX + 1] = uint8_t(k7_code<true, true>(S, k + KX + 1, KX, true, true, true, true));
     }
-    code[k] = uint8_t(c);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < N; k += K7_THREADS) {
+  auto tag_at = [&](int k) {
     const uint32_t c = code[k];
     uint8_t tag = 0;
     if (!(c & 0x40)) {
@@ -234,6 +244,16 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       else if (mf != 7 && (code[nbk(mf)] & 7) == (mf ^ 1)) tag = make_tag(KIND_DOWN, int(mf));
     }
     S.tags[k] = tag;
+  };
+  for (int v = threadIdx.x; v < nvox; v += K7_THREADS) {
+    const int y = dNX(v), x = v - y * nx, k = 2 * y * KX + 2 * x;
+    const bool hx = x + 1 < nx, hy = y + 1 < ny;
+    tag_at(k);
+    if (hx) tag_at(k + 1);
+    if (hy) {
+      tag_at(k + KX);
+      if (hx) tag_at(k + KX + 1);
+    }
   }
   __syncthreads();
   // ---- 3. H0: apparent forest, roots, residual edges in key order, elder-rule union-find
