@@ -606,3 +606,28 @@ def test_k5_schedule_independence(cr, monkeypatch):
                 monkeypatch.setenv(a, b)
             p = cr.pairing(t).cpu().numpy().view(np.uint32)
             assert np.array_equal(p, o.partner), (k, kn, np.flatnonzero(p != o.partner)[:10])
+
+
+def test_k7_fuzz_shapes(cr):
+    """Batches of small 2D images through the one-CTA-per-image path (K7) on random shapes from
+    1-wide to 32 x 32 (the last takes the reduction variant), with and without +inf masks: each
+    image's bars equal the oracle's."""
+    import torch
+    rng = np.random.default_rng(2024)
+    for t in range(40):
+        ny, nx = int(rng.integers(1, 33)), int(rng.integers(1, 33))
+        if t == 0:
+            ny = nx = 32
+        B = int(rng.integers(1, 30))
+        imgs = np.stack([gen.small_int_image((ny, nx), int(rng.integers(2, 9)),
+                                             seed=int(rng.integers(1 << 30)),
+                                             inf_frac=[0.0, 0.05, 0.3][t % 3]) for _ in range(B)])
+        bc, off = cr.barcodes_batched(torch.from_numpy(imgs).cuda(), 1)
+        d, b, e, _ = bc.numpy()
+        off = off.cpu().numpy()
+        for i in range(B):
+            o = oracle.ph(imgs[i], 1)
+            s = slice(off[i], off[i + 1])
+            got = sorted(zip(d[s].tolist(), b[s].tolist(), e[s].tolist()))
+            exp = sorted(zip(o.dim.tolist(), o.birth.tolist(), o.death.tolist()))
+            assert got == exp, (t, (ny, nx), i)
