@@ -1991,8 +1991,9 @@ struct MMArgs {
   Cand* nxt;
   const unsigned* n;  // device: the number of candidates (read by the kernel: no host round trip)
   uint32_t* parent;
-  unsigned long long* best;
-  uint8_t* alive;
+  unsigned long long* best;  // 2 * nbest entries (two buffers, by round parity)
+  unsigned nbest;
+  uint8_t* alive;            // n entries, 1 on entry
   const uint32_t* births;
   Geom g;
   DualG G;
@@ -2003,43 +2004,66 @@ struct MMArgs {
 };
 template <bool DUAL>
 __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
+  // Two grid syncs per round: the candidate list is never compacted (alive bit 0: undecided,
+  // bit 1: did an atomicMin last round), and the per-root minima alternate between two buffers
+  // (A.best, A.best + A.nbest) by round parity, the previous round's buffer being reset by the
+  // candidates that touched it while the current one is filled.
   cg::grid_group grid = cg::this_grid();
   const unsigned gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
   Cand* cur = A.cur;
-  Cand* nxt = A.nxt;
-  unsigned n = *A.n, rounds = 0;
-  while (n > 0) {
-    for (unsigned i = gt; i < n; i += gs) {  // find
+  const unsigned n = *A.n;
+  unsigned rounds = 0;
+  while (true) {
+    unsigned long long* bc = A.best + (rounds & 1) * A.nbest;
+    unsigned long long* bp = A.best + ((rounds + 1) & 1) * A.nbest;
+    for (unsigned i = gt; i < n; i += gs) {  // find (and reset the previous round's minima)
+      uint8_t st = A.alive[i];
+      if (!st) continue;
       Cand c = cur[i];
-      const uint32_t a = uf_find(A.parent, c.a), b = uf_find(A.parent, c.b);
-      cur[i].a = a;
-      cur[i].b = b;
-      if (a == b) {
-        A.alive[i] = 0;
-        continue;
+      if (st & 2) {
+        bp[c.a] = NONE64;
+        bp[c.b] = NONE64;
+        st &= 1;
       }
-      A.alive[i] = 1;
-      atomicMin(A.best + a, (unsigned long long)c.key);
-      atomicMin(A.best + b, (unsigned long long)c.key);
+      if (st & 1) {
+        const uint32_t a = uf_find(A.parent, c.a), b = uf_find(A.parent, c.b);
+        if (a == b) {  // connected through strictly smaller edges: positive
+          st = 0;
+        } else {
+          cur[i].a = a;
+          cur[i].b = b;
+          atomicMin(bc + a, (unsigned long long)c.key);
+          atomicMin(bc + b, (unsigned long long)c.key);
+          st = 3;
+        }
+      }
+      A.alive[i] = st;
     }
     grid.sync();
+    unsigned left = 0;
     for (unsigned i = gt; i < n; i += gs) {  // commit (see k_mm_commit / k_dual_mm_commit)
-      if (!A.alive[i]) continue;
+      if (A.alive[i] != 3) continue;
       const Cand c = cur[i];
-      const bool min_a = A.best[c.a] == c.key, min_b = A.best[c.b] == c.key;
-      if (!min_a && !min_b) continue;
-      uint64_t ka, kb;
-      if (DUAL) {
-        ka = dual_root_key(A.births, A.G, c.a);
-        kb = dual_root_key(A.births, A.G, c.b);
-      } else {
-        const uint32_t xa = vox_kidx(A.g, c.a), xb = vox_kidx(A.g, c.b);
-        ka = make_key(A.births[xa], xa);
-        kb = make_key(A.births[xb], xb);
+      const bool min_a = bc[c.a] == c.key, min_b = bc[c.b] == c.key;
+      bool commit = false;
+      uint64_t ka = 0, kb = 0;
+      bool a_young = false;
+      if (min_a || min_b) {
+        if (DUAL) {
+          ka = dual_root_key(A.births, A.G, c.a);
+          kb = dual_root_key(A.births, A.G, c.b);
+        } else {
+          const uint32_t xa = vox_kidx(A.g, c.a), xb = vox_kidx(A.g, c.b);
+          ka = make_key(A.births[xa], xa);
+          kb = make_key(A.births[xb], xb);
+        }
+        a_young = DUAL ? ka < kb : ka > kb;
+        commit = (min_a && min_b) || (a_young ? min_a : min_b);
       }
-      const bool a_young = DUAL ? ka < kb : ka > kb;
-      if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) continue;
+      if (!commit) {
+        ++left;
+        continue;
+      }
       const uint32_t young = a_young ? c.a : c.b, old = a_young ? c.b : c.a;
       A.parent[young] = old;
       const unsigned long long r = atomicAdd(A.nrec, 1ull);
@@ -2049,36 +2073,15 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
         A.tags[key_kidx(c.key)] = make_tag(KIND_CLEARED, 0);  // a death edge: cleared for dim 1
         A.rec[r] = (uint64_t(key_kidx(a_young ? ka : kb)) << 32) | key_kidx(c.key);
       }
-      A.alive[i] = 2;
+      A.alive[i] = 2;  // decided; its minima are reset next round
     }
-    grid.sync();
     unsigned* cnt = A.ctl + (rounds & 1);
-    for (unsigned base = gt - (gt & 31u); base < n; base += gs) {  // reset + compact survivors
-      const unsigned i = base + lane;
-      bool keep = false;
-      Cand c;
-      if (i < n) {
-        c = cur[i];
-        if (A.alive[i]) {
-          A.best[c.a] = NONE64;
-          A.best[c.b] = NONE64;
-        }
-        keep = A.alive[i] == 1;
-      }
-      const unsigned mask = __ballot_sync(0xFFFFFFFFu, keep);
-      if (!mask) continue;
-      unsigned off = 0;
-      if (lane == __ffs(mask) - 1) off = atomicAdd(cnt, __popc(mask));
-      off = __shfl_sync(0xFFFFFFFFu, off, __ffs(mask) - 1);
-      if (keep) nxt[off + __popc(mask & ((1u << lane) - 1))] = c;
-    }
+    left = __reduce_add_sync(0xFFFFFFFFu, left);
+    if ((threadIdx.x & 31) == 0 && left) atomicAdd(cnt, left);
     if (gt == 0) A.ctl[(rounds + 1) & 1] = 0;  // the next round's counter (read before 2 syncs)
     grid.sync();
-    n = __ldcg(cnt);
-    Cand* t = cur;
-    cur = nxt;
-    nxt = t;
     ++rounds;
+    if (__ldcg(cnt) == 0) break;
   }
   if (gt == 0) A.ctl[2] = rounds;
 }
@@ -2088,7 +2091,8 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
 // No host synchronisation: the caller reads ctl[2] with its next scalar read.
 template <bool DUAL>
 void mm_rounds(Cand* cand, Cand* cand2, const unsigned* n_dev, int64_t n_max, uint32_t* parent,
-               unsigned long long* best, uint8_t* alive, const uint32_t* births, const Geom& g,
+               unsigned long long* best, unsigned nbest, uint8_t* alive, const uint32_t* births,
+               const Geom& g,
                const DualG& G, uint8_t* tags, uint64_t* rec, unsigned long long* nrec,
                unsigned* ctl, Workspace& ws) {
   cudaStream_t s = ws.stream();
@@ -2107,7 +2111,8 @@ void mm_rounds(Cand* cand, Cand* cand2, const unsigned* n_dev, int64_t n_max, ui
   const int64_t cap = int64_t(nsm) * occ[DUAL];
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  MMArgs A{cand, cand2, n_dev, parent, best, alive, births, g, G, tags, rec, nrec, ctl};
+  CR_CUDA(cudaMemsetAsync(alive, 1, size_t(n_max > 0 ? n_max : 1), s));
+  MMArgs A{cand, cand2, n_dev, parent, best, nbest, alive, births, g, G, tags, rec, nrec, ctl};
   void* args[] = {&A};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k_mm_rounds<DUAL>, dim3(unsigned(blocks)), dim3(256),
                                       args, 0, s));
@@ -2158,13 +2163,13 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
 
   unsigned long long* nrec = cnt + 2;
   if (nb > smem_basins_max()) {  // device-wide merge rounds
-    unsigned long long* best = ws.alloc<unsigned long long>(nv);
-    CR_CUDA(cudaMemsetAsync(best, 0xFF, nv * sizeof(unsigned long long), s));
+    unsigned long long* best = ws.alloc<unsigned long long>(2 * nv);
+    CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * nv * sizeof(unsigned long long), s));
     uint8_t* alive = ws.alloc<uint8_t>(n + 1);
     Cand* cand2 = ws.alloc<Cand>(n + 1);
     unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 6);  // cnt[6], cnt[7]: zeroed above
-    mm_rounds<true>(cand, cand2, ncand, n, parent, best, alive, S.births, g, G, nullptr,
-                    S.R.rec[d], nrec, ctl, ws);
+    mm_rounds<true>(cand, cand2, ncand, n, parent, best, unsigned(nv), alive, S.births, g, G,
+                    nullptr, S.R.rec[d], nrec, ctl, ws);
     CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 2, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                             s));
     CR_CUDA(cudaStreamSynchronize(s));
@@ -2522,11 +2527,11 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     reduce_dims(S, g, dmax, ws, hs, st);
     return;
   }
-  unsigned long long* best = ws.alloc<unsigned long long>(g.nvox);
-  CR_CUDA(cudaMemsetAsync(best, 0xFF, g.nvox * sizeof(unsigned long long), s));
+  unsigned long long* best = ws.alloc<unsigned long long>(2 * g.nvox);
+  CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * g.nvox * sizeof(unsigned long long), s));
   uint8_t* alive = ws.alloc<uint8_t>(nedges);
   unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 20);  // cnt[20], cnt[21]: zeroed at the start
-  mm_rounds<false>(cand, cand2, ncand, nedges, parent, best, alive, S.births, g,
+  mm_rounds<false>(cand, cand2, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
                    DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ctl, ws);
   // flatten once more so that roots are exact, then essential classes
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
