@@ -182,6 +182,21 @@ void cr_last_stats(cr_stats* out);
  * cr_stats.stage_ms / stage_name; the events add no synchronisation beyond the call's own. */
 void cr_set_profiling(int enable);
 
+/* Validation and measurement options of this host thread (thread-local; every option defaults to
+ * 0 = the product path).  They select cross-check variants that must give identical results --
+ * the tests use them to pin one path against another -- or perturb the schedule of the
+ * parallel reduction, whose result does not depend on it.  Returns CR_EINVAL for
+ * an unknown option.  Not read from the environment. */
+typedef enum {
+  CR_OPT_FORCE_GENERAL = 1,    /* 1D images through the general 3D path (not the 1D tiles)      */
+  CR_OPT_1D_TREE = 2,          /* 1D images through the tree path (not the tiles)               */
+  CR_OPT_TOP_REDUCE = 3,       /* top dimension by the coboundary reduction (not duality)       */
+  CR_OPT_K5_BLOCKS_PER_SM = 4, /* resident blocks per SM of the reduction (0: occupancy limit)  */
+  CR_OPT_K5_JITTER_NS = 5,     /* pseudo-random delays up to this many ns inside the reduction   */
+  CR_OPT_DEBUG = 6             /* per-stage counters printed to stderr                          */
+} cr_option;
+cr_status cr_set_option(int option, int64_t value);
+
 #ifdef __cplusplus
 }
 #endif

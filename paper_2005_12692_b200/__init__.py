@@ -78,10 +78,17 @@ _lib.cr_last_stats.restype = None
 _lib.cr_last_stats.argtypes = [ctypes.POINTER(CrStats)]
 _lib.cr_set_profiling.restype = None
 _lib.cr_set_profiling.argtypes = [ctypes.c_int]
+_lib.cr_set_option.restype = ctypes.c_int
+_lib.cr_set_option.argtypes = [ctypes.c_int, _i64]
 
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
             "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling",
-            "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim", "cr_barcodes_f64"]
+            "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim", "cr_barcodes_f64",
+            "cr_set_option"]
+
+# cr_option (include/cr.h): validation / measurement switches, 0 = the product path
+OPTIONS = {"force_general": 1, "1d_tree": 2, "top_reduce": 3, "k5_blocks_per_sm": 4,
+           "k5_jitter_ns": 5, "debug": 6}
 
 
 class CrError(RuntimeError):
@@ -119,6 +126,28 @@ def num_cells(shape) -> int:
 def set_profiling(enable: bool) -> None:
     """Per-stage CUDA-event timing of subsequent calls on this thread (see cr_set_profiling)."""
     _lib.cr_set_profiling(1 if enable else 0)
+
+
+def set_option(name: str, value: int) -> None:
+    """cr_set_option for this host thread (see OPTIONS)."""
+    _check(_lib.cr_set_option(OPTIONS[name], int(value)))
+
+
+class options:
+    """``with cr.options(top_reduce=1): ...`` sets options for the block, then restores 0."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k in self.kw:
+            set_option(k, 0)
+        return False
 
 
 def last_stats() -> dict:

@@ -9,6 +9,7 @@
 namespace cr {
 const char* last_error_text();
 void set_profiling(bool on);
+bool set_opt(int key, int64_t v);
 static thread_local cr_stats g_last_stats;
 static thread_local uint64_t g_stats_gen = 0;  // prof_gen() when g_last_stats was committed
 static void commit_stats(const cr_stats& st) {
@@ -29,10 +30,7 @@ bool valid_shape(const int64_t* shape, int ndim) {
   return true;
 }
 
-bool force_general() {
-  const char* e = std::getenv("CR_FORCE_GENERAL");
-  return e && e[0] == '1';
-}
+bool force_general() { return opt(OPT_FORCE_GENERAL) != 0; }
 
 // death cell of each bar: the partner of its birth cell ("or optionally, killed")
 __global__ void k_death_cells(const uint32_t* __restrict__ birth_cells, int64_t n,
@@ -223,6 +221,10 @@ void cr_last_stats(cr_stats* out) {
 }
 
 void cr_set_profiling(int enable) { cr::set_profiling(enable != 0); }
+
+cr_status cr_set_option(int option, int64_t value) {
+  return cr::set_opt(option, value) ? CR_OK : CR_EINVAL;
+}
 
 cr_status cr_barcodes(const float* image, const int64_t* shape, int ndim, int maxdim,
                       cr_pair* out_pairs, uint32_t* out_birth_cells, int64_t out_capacity,

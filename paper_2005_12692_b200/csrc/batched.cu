@@ -694,10 +694,7 @@ int64_t barcodes_batched_small_2d(const float* images, int64_t batch, int64_t ny
   A.ny = int(ny);
   A.nx = int(nx);
   A.maxdim = maxdim;
-  {
-    const char* e = std::getenv("CR_TOP_REDUCE");
-    A.dual = !(e && e[0] == '1');
-  }
+  A.dual = opt(OPT_TOP_REDUCE) == 0;
   A.cap = per;
   A.sbar = ws.alloc<uint32_t>(batch * int64_t(per) * 3);
   A.scell = out_cells ? ws.alloc<uint32_t>(batch * int64_t(per)) : nullptr;

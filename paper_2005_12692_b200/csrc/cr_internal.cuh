@@ -73,6 +73,18 @@ __host__ __device__ __forceinline__ int64_t dir_offset(const Geom& g, int dir) {
   return (dir & 1) ? s : -s;
 }
 
+// Validation / measurement options (cr_set_option; thread-local, 0 = the product default).
+enum OptKey {
+  OPT_FORCE_GENERAL = 1,     // 1D images through the general path
+  OPT_1D_TREE = 2,           // 1D images through the tree path instead of the tiles
+  OPT_TOP_REDUCE = 3,        // top dimension by the coboundary reduction instead of duality
+  OPT_K5_BLOCKS_PER_SM = 4,  // resident K5 blocks per SM (<= the occupancy limit)
+  OPT_K5_JITTER_NS = 5,      // pseudo-random K5 delays: perturb the schedule (tests)
+  OPT_DEBUG = 6,             // per-stage counters on stderr
+  OPT_COUNT = 8
+};
+int64_t opt(int key);
+
 // Error plumbing (host).
 struct Error {
   cr_status st;

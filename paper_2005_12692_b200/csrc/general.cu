@@ -39,863 +39,8 @@ __device__ __forceinline__ void coords_of(const Geom& g, uint32_t k, uint32_t& X
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1: cell births.  birth = max over a cell's vertices of ord(phi); since
-// ord(+inf) = ABSENT_ORD exceeds every finite ord, a cell with a +inf vertex gets ABSENT_ORD
-// (absent from K, reading R5).  A thread owns one (x, y) voxel column and streams
-// K1_ZC planes along z: per plane it loads its voxel and the one at y+1 (the plane z+1 pair is
-// carried to the next step), takes the x+1 neighbours from the next lane, and writes the 8 cells
-// whose lowest vertex is its voxel (the 2x2 cells of the Khalimsky rows (2z|2z+1, 2y|2y+1) at
-// X = 2x, 2x+1: contiguous across the warp).  Finite cells are counted per dimension.
-// ---------------------------------------------------------------------------------------------
-constexpr int K1_ZC = 8;
-__global__ void __launch_bounds__(256) k_births(const float* __restrict__ img, Geom g,
-                                                uint32_t* __restrict__ births,
-                                                unsigned long long* __restrict__ cnt,
-                                                int* __restrict__ nan_flag) {
-  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny), nz = uint32_t(g.nz);
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  const uint32_t XB = (nx + 31) / 32, YB = (ny + 7) / 8;
-  uint32_t blk = blockIdx.x;
-  const uint32_t xb = blk % XB;
-  blk /= XB;
-  const uint32_t yb = blk % YB, zb = blk / YB;
-  const int lane = threadIdx.x & 31;
-  const uint32_t x = xb * 32 + lane, y = yb * 8 + (threadIdx.x >> 5);
-  const uint32_t z0 = zb * K1_ZC, z1 = min(nz, z0 + K1_ZC);
-  const bool vx = x < nx, vy = y < ny, hx = x + 1 < nx, hy = y + 1 < ny;
-  const uint64_t plane = uint64_t(nx) * ny;
-  bool nan = false;
-  auto ld = [&](uint32_t xx, uint32_t yy, uint32_t zz, bool ok) -> uint32_t {
-    if (!ok) return ABSENT_ORD;
-    const float f = __ldg(img + zz * plane + uint64_t(yy) * nx + xx);
-    nan |= f != f;
-    return ord_of(f);
-  };
-  // planes z (a, b), z+1 (an, bn) and z+2 (prefetched); lane 31 also streams the x+1 column
-  const bool l31 = lane == 31;
-  uint32_t a = ld(x, y, z0, vx && vy), b = ld(x, y + 1, z0, vx && hy);
-  uint32_t an = ld(x, y, z0 + 1, vx && vy && z0 + 1 < nz), bn = ld(x, y + 1, z0 + 1, vx && hy && z0 + 1 < nz);
-  uint32_t e = l31 ? ld(x + 1, y, z0, hx && vy) : 0u, f = l31 ? ld(x + 1, y + 1, z0, hx && hy) : 0u;
-  uint32_t en = l31 ? ld(x + 1, y, z0 + 1, hx && vy && z0 + 1 < nz) : 0u;
-  uint32_t fn = l31 ? ld(x + 1, y + 1, z0 + 1, hx && hy && z0 + 1 < nz) : 0u;
-  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-  for (uint32_t z = z0; z < z1; ++z) {
-    const bool hz = z + 1 < nz, hz2 = z + 2 < nz && z + 2 < z1 + 1;
-    const uint32_t an2 = ld(x, y, z + 2, vx && vy && hz2), bn2 = ld(x, y + 1, z + 2, vx && hy && hz2);
-    const uint32_t en2 = l31 ? ld(x + 1, y, z + 2, hx && vy && hz2) : 0u;
-    const uint32_t fn2 = l31 ? ld(x + 1, y + 1, z + 2, hx && hy && hz2) : 0u;
-    uint32_t a1 = __shfl_down_sync(0xFFFFFFFFu, a, 1), b1 = __shfl_down_sync(0xFFFFFFFFu, b, 1);
-    uint32_t an1 = __shfl_down_sync(0xFFFFFFFFu, an, 1), bn1 = __shfl_down_sync(0xFFFFFFFFu, bn, 1);
-    if (l31) {
-      a1 = e;
-      b1 = f;
-      an1 = en;
-      bn1 = fn;
-    }
-    if (vx && vy) {
-      const uint32_t c100 = max(a, a1), c010 = max(a, b), c110 = max(c100, max(b, b1));
-      const uint32_t c001 = max(a, an), c101 = max(c100, max(an, an1));
-      const uint32_t c011 = max(c010, max(an, bn));
-      const uint32_t c111 = max(c110, max(max(an, an1), max(bn, bn1)));
-      uint32_t* r = births + (uint64_t(2 * z) * KY + 2 * y) * KX + 2 * x;
-      r[0] = a;
-      if (hx) r[1] = c100;
-      c0 += a != ABSENT_ORD;
-      c1 += hx && c100 != ABSENT_ORD;
-      if (hy) {
-        r[KX] = c010;
-        if (hx) r[KX + 1] = c110;
-        c1 += c010 != ABSENT_ORD;
-        c2 += hx && c110 != ABSENT_ORD;
-      }
-      if (hz) {
-        uint32_t* q = r + uint64_t(KX) * KY;
-        q[0] = c001;
-        if (hx) q[1] = c101;
-        c1 += c001 != ABSENT_ORD;
-        c2 += hx && c101 != ABSENT_ORD;
-        if (hy) {
-          q[KX] = c011;
-          if (hx) q[KX + 1] = c111;
-          c2 += c011 != ABSENT_ORD;
-          c3 += hx && c111 != ABSENT_ORD;
-        }
-      }
-    }
-    a = an;
-    b = bn;
-    an = an2;
-    bn = bn2;
-    e = en;
-    f = fn;
-    en = en2;
-    fn = fn2;
-  }
-  // counts and the NaN flag: warp, then block, then one atomic per counter
-  __shared__ uint32_t s_c[4];
-  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
-  __syncthreads();
-  c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
-  c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
-  c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
-  c3 = __reduce_add_sync(0xFFFFFFFFu, c3);
-  const bool anynan = __any_sync(0xFFFFFFFFu, nan);
-  if (lane == 0) {
-    atomicAdd(s_c + 0, c0);
-    atomicAdd(s_c + 1, c1);
-    atomicAdd(s_c + 2, c2);
-    atomicAdd(s_c + 3, c3);
-    if (anynan) atomicOr(nan_flag, 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < 4 && s_c[threadIdx.x]) atomicAdd(cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
-}
-// ---------------------------------------------------------------------------------------------
-// K1 with K2a fused: births AND the direction codes (min-key cofacet | max-key facet << 3, see
-// K2 below) of every cell, from one read of the image.  Thread = voxel column (x, y), streamed
-// along z; a warp covers x = 30*xb-1 .. 30*xb+30 (lanes 0 and 31 are halo), a CTA covers the voxel
-// rows y = 8*yb-1 .. 8*yb+8 (warps 0 and 9 are halo).  A cell's 6 grid neighbours come from: the
-// same thread (the other half of its voxel's 2x2x2 block), the neighbouring lanes (X), the
-// neighbouring warps through shared memory (Y), and the previous / next z step (Z) -- the codes of
-// the cz=1 layer of plane z are formed one step later, when plane z+1's cz=0 layer exists.
-// Outputs (births, codes) are written by the non-halo threads only.
-// ---------------------------------------------------------------------------------------------
-constexpr uint8_t CODE_ABSENT = 0x40;  // code bit 6: the cell is absent (+inf birth)
-constexpr int K1C_ROWS = 8, K1C_THREADS = 32 * (K1C_ROWS + 2), K1C_ZC = 8;
-inline unsigned k1c_grid(const Geom& g) {
-  return unsigned(((g.nx + 29) / 30) * ((g.ny + K1C_ROWS - 1) / K1C_ROWS) *
-                  ((g.nz + K1C_ZC - 1) / K1C_ZC));
-}
-__device__ __forceinline__ void code_visit(bool exists, bool odd, uint32_t nb, uint32_t dir,
-                                           uint32_t& mcb, uint32_t& mc, uint32_t& mfb,
-                                           uint32_t& mf) {
-  const bool f = exists && odd && nb >= mfb;
-  const bool c = exists && !odd && nb < mcb;
-  mfb = f ? nb : mfb;
-  mf = f ? dir : mf;
-  mcb = c ? nb : mcb;
-  mc = c ? dir : mc;
-}
-// code of a cell with birth b, odd-axis flags, and its neighbours (ABSENT_ORD where missing);
-// neighbours are visited in increasing kidx order: -Z, -Y, -X, +X, +Y, +Z
-__device__ __forceinline__ uint8_t cell_code6(uint32_t b, bool ox, bool oy, bool oz, uint32_t zm,
-                                              bool hzm, uint32_t ym, bool hym, uint32_t xm,
-                                              bool hxm, uint32_t xp, bool hxp, uint32_t yp,
-                                              bool hyp, uint32_t zp, bool hzp) {
-  if (b == ABSENT_ORD) return CODE_ABSENT;
-  uint32_t mcb = ABSENT_ORD, mc = 7, mfb = 0, mf = 7;
-  code_visit(hzm, oz, zm, 4, mcb, mc, mfb, mf);
-  code_visit(hym, oy, ym, 2, mcb, mc, mfb, mf);
-  code_visit(hxm, ox, xm, 0, mcb, mc, mfb, mf);
-  code_visit(hxp, ox, xp, 1, mcb, mc, mfb, mf);
-  code_visit(hyp, oy, yp, 3, mcb, mc, mfb, mf);
-  code_visit(hzp, oz, zp, 5, mcb, mc, mfb, mf);
-  return uint8_t(mc | (mf << 3));
-}
-
-__global__ void __launch_bounds__(K1C_THREADS) k_births_codes(const float* __restrict__ img,
-                                                              Geom g,
-                                                              uint32_t* __restrict__ births,
-                                                              uint8_t* __restrict__ code,
-                                                              unsigned long long* __restrict__ cnt,
-                                                              int* __restrict__ nan_flag) {
-  const int nx = int(g.nx), ny = int(g.ny), nz = int(g.nz);
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  const int XB = (nx + 29) / 30, YB = (ny + K1C_ROWS - 1) / K1C_ROWS;
-  uint32_t blk = blockIdx.x;
-  const int xb = int(blk % XB);
-  blk /= XB;
-  const int yb = int(blk % YB), zb = int(blk / YB);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int x = xb * 30 - 1 + lane, y = yb * K1C_ROWS - 1 + w;
-  const int z0 = zb * K1C_ZC, z1 = min(nz, z0 + K1C_ZC);
-  const bool vx = x >= 0 && x < nx, vy = y >= 0 && y < ny, vv = vx && vy;
-  const bool hx = x + 1 < nx, hy = y + 1 < ny;  // the cell spans x+1 / y+1
-  const bool outp = vv && lane >= 1 && lane <= 30 && w >= 1 && w <= K1C_ROWS;
-  const uint64_t plane = uint64_t(nx) * ny;
-  // shared rows: births of the cz=0 layer of plane z and the cz=1 layer of plane z-1,
-  // 2 cells (cy = 0, 1) x 2 (cx) per thread, indexed [w][lane]
-  __shared__ uint32_t s_b0[K1C_ROWS + 2][4][32];
-  __shared__ uint32_t s_b1[K1C_ROWS + 2][4][32];
-  __shared__ uint32_t s_c[4];
-  bool nan = false;
-  auto ld = [&](int xx, int yy, int zz) -> uint32_t {
-    if (xx < 0 || xx >= nx || yy < 0 || yy >= ny || zz < 0 || zz >= nz) return ABSENT_ORD;
-    const float f = __ldg(img + uint64_t(zz) * plane + uint64_t(yy) * nx + xx);
-    nan |= f != f;
-    return ord_of(f);
-  };
-  // voxel values of plane zz: a = (x, y), b = (x, y+1); x+1 by shuffle (lane 31 loads)
-  uint32_t a = ld(x, y, z0 - 1), b = ld(x, y + 1, z0 - 1);
-  uint32_t an = ld(x, y, z0), bn = ld(x, y + 1, z0);
-  uint32_t e = lane == 31 ? ld(x + 1, y, z0 - 1) : 0u, f = lane == 31 ? ld(x + 1, y + 1, z0 - 1) : 0u;
-  uint32_t en = lane == 31 ? ld(x + 1, y, z0) : 0u, fn = lane == 31 ? ld(x + 1, y + 1, z0) : 0u;
-  // previous step's cz=1 layer (plane z-1): births [cy][cx], for the Z- of this step's cz=0 cells
-  // and its own codes one step late; and its Z- layer (plane z-1's cz=0)
-  uint32_t p1[2][2] = {{ABSENT_ORD, ABSENT_ORD}, {ABSENT_ORD, ABSENT_ORD}};
-  uint32_t p0[2][2] = {{ABSENT_ORD, ABSENT_ORD}, {ABSENT_ORD, ABSENT_ORD}};
-  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-  for (int z = z0 - 1; z <= z1; ++z) {
-    const bool pz = z >= 0 && z < nz;     // plane z exists
-    const bool hz = z + 1 < nz;           // cells of plane z span z+1
-    const uint32_t an2 = ld(x, y, z + 2), bn2 = ld(x, y + 1, z + 2);
-    const uint32_t en2 = lane == 31 ? ld(x + 1, y, z + 2) : 0u;
-    const uint32_t fn2 = lane == 31 ? ld(x + 1, y + 1, z + 2) : 0u;
-    uint32_t a1 = __shfl_down_sync(0xFFFFFFFFu, a, 1), b1 = __shfl_down_sync(0xFFFFFFFFu, b, 1);
-    uint32_t an1 = __shfl_down_sync(0xFFFFFFFFu, an, 1), bn1 = __shfl_down_sync(0xFFFFFFFFu, bn, 1);
-    if (lane == 31) {
-      a1 = e;
-      b1 = f;
-      an1 = en;
-      bn1 = fn;
-    }
-    // births of the 8 cells of voxel (x, y, z): q0[cy][cx] (Z = 2z), q1[cy][cx] (Z = 2z+1);
-    // cells that do not exist (beyond the grid) are ABSENT_ORD, i.e. not in K
-    uint32_t q0[2][2], q1[2][2];
-    {
-      const uint32_t A = pz && vv ? a : ABSENT_ORD;
-      const uint32_t c100 = hx ? max(a, a1) : ABSENT_ORD, c010 = hy ? max(a, b) : ABSENT_ORD;
-      const uint32_t c110 = hx && hy ? max(max(a, a1), max(b, b1)) : ABSENT_ORD;
-      q0[0][0] = A;
-      q0[0][1] = pz && vv ? c100 : ABSENT_ORD;
-      q0[1][0] = pz && vv ? c010 : ABSENT_ORD;
-      q0[1][1] = pz && vv ? c110 : ABSENT_ORD;
-      const bool o1 = pz && vv && hz;
-      q1[0][0] = o1 ? max(a, an) : ABSENT_ORD;
-      q1[0][1] = o1 && hx ? max(max(a, a1), max(an, an1)) : ABSENT_ORD;
-      q1[1][0] = o1 && hy ? max(max(a, b), max(an, bn)) : ABSENT_ORD;
-      q1[1][1] = o1 && hx && hy ? max(max(max(a, a1), max(b, b1)), max(max(an, an1), max(bn, bn1)))
-                                : ABSENT_ORD;
-    }
-    // exchange the cz=0 layer of plane z and the cz=1 layer of plane z-1 (X by shuffle, Y by smem)
-#pragma unroll
-    for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-      for (int cx = 0; cx < 2; ++cx) {
-        s_b0[w][2 * cy + cx][lane] = q0[cy][cx];
-        s_b1[w][2 * cy + cx][lane] = p1[cy][cx];
-      }
-    uint32_t x0m[2], x0p[2], x1m[2], x1p[2];  // [cy]: X-1 of a cx=0 cell, X+1 of a cx=1 cell
-#pragma unroll
-    for (int cy = 0; cy < 2; ++cy) {
-      x0m[cy] = __shfl_up_sync(0xFFFFFFFFu, q0[cy][1], 1);
-      x0p[cy] = __shfl_down_sync(0xFFFFFFFFu, q0[cy][0], 1);
-      x1m[cy] = __shfl_up_sync(0xFFFFFFFFu, p1[cy][1], 1);
-      x1p[cy] = __shfl_down_sync(0xFFFFFFFFu, p1[cy][0], 1);
-    }
-    __syncthreads();
-    if (outp) {
-      const uint32_t X0 = 2 * uint32_t(x), Y0 = 2 * uint32_t(y);
-      // ---- births of plane z, and the codes of its cz=0 layer (Z = 2z)
-      if (pz && z >= z0 && z < z1) {
-        const uint32_t Z = 2 * uint32_t(z);
-        uint32_t* r = births + (uint64_t(Z) * KY + Y0) * KX + X0;
-        uint8_t* cr = code + (uint64_t(Z) * KY + Y0) * KX + X0;
-#pragma unroll
-        for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-          for (int cx = 0; cx < 2; ++cx) {
-            if ((cx && !hx) || (cy && !hy)) continue;
-            const uint32_t bb = q0[cy][cx];
-            const uint32_t xm = cx ? q0[cy][0] : x0m[cy];
-            const uint32_t xp = cx ? x0p[cy] : q0[cy][1];
-            const uint32_t ym = cy ? q0[0][cx] : s_b0[w - 1][2 + cx][lane];
-            const uint32_t yp = cy ? s_b0[w + 1][cx][lane] : q0[1][cx];
-            const uint8_t cd = cell_code6(bb, cx, cy, false, p1[cy][cx], z > 0, ym, Y0 + cy > 0,
-                                          xm, X0 + cx > 0, xp, X0 + cx + 1 < KX, yp,
-                                          Y0 + cy + 1 < KY, q1[cy][cx], hz);
-            r[cy * KX + cx] = bb;
-            cr[cy * KX + cx] = cd;
-            const int dim = cx + cy;
-            const bool fin = bb != ABSENT_ORD;
-            c0 += fin && dim == 0;
-            c1 += fin && dim == 1;
-            c2 += fin && dim == 2;
-            if (hz) {
-              const uint32_t b1v = q1[cy][cx];
-              r[uint64_t(KX) * KY + cy * KX + cx] = b1v;
-              const bool fin1 = b1v != ABSENT_ORD;
-              c1 += fin1 && dim == 0;
-              c2 += fin1 && dim == 1;
-              c3 += fin1 && dim == 2;
-            }
-          }
-      }
-      // ---- codes of plane z-1's cz=1 layer (Z = 2z-1): Z- = plane z-1's cz=0, Z+ = plane z's cz=0
-      const int zq = z - 1;
-      if (zq >= z0 && zq < z1 && zq + 1 < nz) {
-        const uint32_t Z = 2 * uint32_t(zq) + 1;
-        uint8_t* cr = code + (uint64_t(Z) * KY + Y0) * KX + X0;
-#pragma unroll
-        for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-          for (int cx = 0; cx < 2; ++cx) {
-            if ((cx && !hx) || (cy && !hy)) continue;
-            const uint32_t bb = p1[cy][cx];
-            const uint32_t xm = cx ? p1[cy][0] : x1m[cy];
-            const uint32_t xp = cx ? x1p[cy] : p1[cy][1];
-            const uint32_t ym = cy ? p1[0][cx] : s_b1[w - 1][2 + cx][lane];
-            const uint32_t yp = cy ? s_b1[w + 1][cx][lane] : p1[1][cx];
-            cr[cy * KX + cx] = cell_code6(bb, cx, cy, true, p0[cy][cx], true, ym, Y0 + cy > 0, xm,
-                                          X0 + cx > 0, xp, X0 + cx + 1 < KX, yp, Y0 + cy + 1 < KY,
-                                          q0[cy][cx], true);
-          }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-      for (int cx = 0; cx < 2; ++cx) {
-        p0[cy][cx] = q0[cy][cx];
-        p1[cy][cx] = q1[cy][cx];
-      }
-    a = an;
-    b = bn;
-    an = an2;
-    bn = bn2;
-    e = en;
-    f = fn;
-    en = en2;
-    fn = fn2;
-  }
-  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
-  __syncthreads();
-  c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
-  c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
-  c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
-  c3 = __reduce_add_sync(0xFFFFFFFFu, c3);
-  const bool anynan = __any_sync(0xFFFFFFFFu, nan);
-  if (lane == 0) {
-    atomicAdd(s_c + 0, c0);
-    atomicAdd(s_c + 1, c1);
-    atomicAdd(s_c + 2, c2);
-    atomicAdd(s_c + 3, c3);
-    if (anynan) atomicOr(nan_flag, 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < 4 && s_c[threadIdx.x])
-    atomicAdd(cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
-}
-
-inline unsigned k_births_grid(const Geom& g) {
-  return unsigned(((g.nx + 31) / 32) * ((g.ny + 7) / 8) * ((g.nz + K1_ZC - 1) / K1_ZC));
-}
-
-// ---------------------------------------------------------------------------------------------
-// K2: apparent pairs (Ripser's shortcut, inherited per PAPER.md:44-45).  For a finite cell s:
-//   UP   : t = min-key cofacet of s, and s is the max-key facet of t  -> (s, t) is a pair;
-//   DOWN : r = max-key facet of s, and s is the min-key cofacet of r   -> (r, s) is a pair.
-// Keys are (ord(birth), kidx); the pair always has death == birth (birth(t) = max facet birth).
-// Each thread writes only its own tag, so no two threads touch the same byte.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint8_t tag_of(const uint32_t* __restrict__ births, const Geom& g,
-                                          uint32_t k, int& dim_out) {
-  const uint32_t bo = births[k];
-  if (bo == ABSENT_ORD) return 0;
-  uint32_t c[3];
-  coords_of(g, k, c[0], c[1], c[2]);
-  const uint32_t ext[3] = {uint32_t(g.KX), uint32_t(g.KY), uint32_t(g.KZ)};
-  const int64_t st[3] = {1, g.KX, g.KX * g.KY};
-  const uint64_t mykey = make_key(bo, k);
-  const int dim = (c[0] & 1) + (c[1] & 1) + (c[2] & 1);
-  uint8_t tag = 0;
-  // UP
-  {
-    uint64_t best = NONE64;
-    int bdir = -1;
-    for (int a = 0; a < 3; ++a) {
-      if (c[a] & 1) continue;
-      for (int s = 0; s < 2; ++s) {
-        if (s == 0 ? c[a] == 0 : c[a] + 1 >= ext[a]) continue;
-        uint32_t t = uint32_t(int64_t(k) + (s ? st[a] : -st[a]));
-        uint32_t tb = __ldg(births + t);
-        if (tb == ABSENT_ORD) continue;
-        uint64_t key = make_key(tb, t);
-        if (key < best) { best = key; bdir = 2 * a + s; }
-      }
-    }
-    if (bdir >= 0) {
-      uint32_t t = key_kidx(best);
-      int ta = bdir >> 1;
-      bool is_max = true;
-      for (int a = 0; a < 3 && is_max; ++a) {
-        bool odd = (a == ta) ? true : (c[a] & 1);
-        if (!odd) continue;
-        for (int s = 0; s < 2; ++s) {
-          uint32_t f = uint32_t(int64_t(t) + (s ? st[a] : -st[a]));
-          if (f == k) continue;
-          if (make_key(__ldg(births + f), f) > mykey) { is_max = false; break; }
-        }
-      }
-      if (is_max) tag = make_tag(KIND_UP, bdir);
-    }
-  }
-  // DOWN
-  if (!tag && dim >= 1) {
-    uint64_t best = 0;
-    int bdir = -1;
-    for (int a = 0; a < 3; ++a) {
-      if (!(c[a] & 1)) continue;
-      for (int s = 0; s < 2; ++s) {
-        uint32_t f = uint32_t(int64_t(k) + (s ? st[a] : -st[a]));
-        uint64_t key = make_key(__ldg(births + f), f);
-        if (bdir < 0 || key > best) { best = key; bdir = 2 * a + s; }
-      }
-    }
-    uint32_t r = key_kidx(best);
-    int ra = bdir >> 1;
-    bool is_min = true;
-    for (int a = 0; a < 3 && is_min; ++a) {
-      bool odd = (a == ra) ? false : (c[a] & 1);
-      if (odd) continue;
-      uint32_t ca = (a == ra) ? c[a] + ((bdir & 1) ? 1 : -1) : c[a];
-      for (int s = 0; s < 2; ++s) {
-        if (s == 0 ? ca == 0 : ca + 1 >= ext[a]) continue;
-        uint32_t t = uint32_t(int64_t(r) + (s ? st[a] : -st[a]));
-        if (t == k) continue;
-        uint32_t tb = __ldg(births + t);
-        if (tb == ABSENT_ORD) continue;
-        if (make_key(tb, t) < mykey) { is_min = false; break; }
-      }
-    }
-    if (is_min) tag = make_tag(KIND_DOWN, bdir);
-  }
-  dim_out = dim;
-  return tag;
-}
-
-__global__ void k_tags(const uint32_t* __restrict__ births, Geom g, uint8_t* __restrict__ tags,
-                       unsigned long long* __restrict__ app_cnt) {
-  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint8_t tag = 0;
-  int dim = 0;
-  if (kk < g.ncells) {
-    tag = tag_of(births, g, uint32_t(kk), dim);
-    tags[kk] = tag;
-  }
-  // apparent (UP) cells per dimension: warp ballots, then one atomic per warp and dimension
-  const bool up = tag_kind(tag) == KIND_UP;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, up && dim == d);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(app_cnt + d, (unsigned long long)__popc(m));
-  }
-}
-
-
-// ---------------------------------------------------------------------------------------------
-// K2 in two streaming passes over the Khalimsky grid (the same apparent pairs as tag_of):
-//   K2a: code[s] = (direction of s's min-key cofacet) | (direction of its max-key facet) << 3,
-//        7 = none; bit 6: s absent.  A cell's 6 grid neighbours s +- e_a are its facets (odd
-//        axis a) or cofacets (even a), and their kidx order is fixed: -Z < -Y < -X < +X < +Y < +Z,
-//        so scanning them in that order, a strict < keeps the smaller kidx among equal births
-//        (min key) and >= the larger (max key).  Absent cofacets are not in K.
-//   K2b: s is UP (paired with its min cofacet t) iff t's max facet is s; else DOWN (paired with
-//        its max facet r) iff r's min cofacet is s.
-// A CTA covers 64 cells of a Khalimsky row x 4 rows of one plane; all index math is 32-bit.
-// ---------------------------------------------------------------------------------------------
-struct K2Tile {
-  uint32_t X, Y, Z, k;
-  bool valid;
-};
-__device__ __forceinline__ K2Tile k2_tile(const Geom& g) {
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  const uint32_t XB = (KX + 63) / 64, YB = (KY + 3) / 4;
-  uint32_t b = blockIdx.x;
-  const uint32_t xb = b % XB;
-  b /= XB;
-  const uint32_t yb = b % YB, zb = b / YB;
-  K2Tile T;
-  T.X = xb * 64 + (threadIdx.x & 63);
-  T.Y = yb * 4 + (threadIdx.x >> 6);
-  T.Z = zb;
-  T.valid = T.X < KX && T.Y < KY;
-  T.k = (T.Z * KY + T.Y) * KX + T.X;
-  return T;
-}
-inline unsigned k2_grid(const Geom& g) {
-  return unsigned(((g.KX + 63) / 64) * ((g.KY + 3) / 4) * g.KZ);
-}
-
-__global__ void __launch_bounds__(256) k_codes(const uint32_t* __restrict__ births, Geom g,
-                                               uint8_t* __restrict__ code) {
-  const K2Tile T = k2_tile(g);
-  if (!T.valid) return;
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY), KZ = uint32_t(g.KZ);
-  const uint32_t sy = KX, sz = KX * KY;
-  const uint32_t b = births[T.k];
-  if (b == ABSENT_ORD) {
-    code[T.k] = CODE_ABSENT;
-    return;
-  }
-  uint32_t mcb = ABSENT_ORD, mfb = 0, mc = 7, mf = 7;
-  auto visit = [&](bool exists, bool odd, uint32_t kk, uint32_t dir) {
-    if (!exists) return;
-    const uint32_t nb = __ldg(births + kk);
-    if (odd) {
-      if (nb >= mfb) {
-        mfb = nb;
-        mf = dir;
-      }
-    } else if (nb < mcb) {  // absent (ABSENT_ORD) never wins
-      mcb = nb;
-      mc = dir;
-    }
-  };
-  visit(T.Z > 0, T.Z & 1, T.k - sz, 4);
-  visit(T.Y > 0, T.Y & 1, T.k - sy, 2);
-  visit(T.X > 0, T.X & 1, T.k - 1, 0);
-  visit(T.X + 1 < KX, T.X & 1, T.k + 1, 1);
-  visit(T.Y + 1 < KY, T.Y & 1, T.k + sy, 3);
-  visit(T.Z + 1 < KZ, T.Z & 1, T.k + sz, 5);
-  code[T.k] = uint8_t(mc | (mf << 3));
-}
-
-// K2a, streaming along Z: a warp owns 32 cells of one Khalimsky row, a CTA 8 rows, and walks
-// K2_ZC planes.  The +-Z neighbours are the thread's own previous/next values (registers), +-X
-// come from the neighbouring lanes, +-Y from the neighbouring warps through shared memory (the
-// CTA's first and last warps load the rows just outside it).  Each birth is read from DRAM once.
-constexpr int K2_ZC = 16;
-inline unsigned k2z_grid(const Geom& g) {
-  return unsigned(((g.KX + 31) / 32) * ((g.KY + 7) / 8) * ((g.KZ + K2_ZC - 1) / K2_ZC));
-}
-__global__ void __launch_bounds__(256) k_codes_z(const uint32_t* __restrict__ births, Geom g,
-                                                 uint8_t* __restrict__ code) {
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY), KZ = uint32_t(g.KZ);
-  const uint32_t XB = (KX + 31) / 32, YB = (KY + 7) / 8;
-  uint32_t blk = blockIdx.x;
-  const uint32_t xb = blk % XB;
-  blk /= XB;
-  const uint32_t yb = blk % YB, zb = blk / YB;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t X = xb * 32 + lane, Y = yb * 8 + w;
-  const uint32_t Z0 = zb * K2_ZC, Z1 = min(KZ, Z0 + K2_ZC);
-  const bool vx = X < KX, vy = Y < KY;
-  const uint32_t sz = KX * KY;
-  __shared__ uint32_t s_row[10][32];  // rows Y0-1 .. Y0+8 of the current plane
-  auto at = [&](uint32_t xx, uint32_t yy, uint32_t zz, bool ok) -> uint32_t {
-    return ok ? __ldg(births + (zz * KY + yy) * KX + xx) : ABSENT_ORD;
-  };
-  uint32_t prev = Z0 > 0 ? at(X, Y, Z0 - 1, vx && vy) : ABSENT_ORD;
-  uint32_t cur = at(X, Y, Z0, vx && vy);
-  for (uint32_t Z = Z0; Z < Z1; ++Z) {
-    const bool hn = Z + 1 < KZ;
-    const uint32_t next = at(X, Y, Z + 1, vx && vy && hn);
-    // rows above/below the CTA (halo), and the X neighbours outside the warp
-    if (w == 0) s_row[0][lane] = at(X, Y - 1, Z, vx && Y > 0);
-    if (w == 7) s_row[9][lane] = at(X, Y + 1, Z, vx && Y + 1 < KY);
-    s_row[w + 1][lane] = cur;
-    uint32_t xm = __shfl_up_sync(0xFFFFFFFFu, cur, 1), xp = __shfl_down_sync(0xFFFFFFFFu, cur, 1);
-    if (lane == 0) xm = at(X - 1, Y, Z, vy && X > 0);
-    if (lane == 31) xp = at(X + 1, Y, Z, vy && X + 1 < KX);
-    __syncthreads();
-    const uint32_t ym = s_row[w][lane], yp = s_row[w + 2][lane];
-    if (vx && vy) {
-      const uint32_t k = (Z * KY + Y) * KX + X;
-      uint8_t c = CODE_ABSENT;
-      if (cur != ABSENT_ORD) {
-        uint32_t mcb = ABSENT_ORD, mfb = 0, mc = 7, mf = 7;
-        auto visit = [&](bool exists, bool odd, uint32_t nb, uint32_t dir) {
-          if (!exists) return;
-          if (odd) {
-            if (nb >= mfb) {
-              mfb = nb;
-              mf = dir;
-            }
-          } else if (nb < mcb) {
-            mcb = nb;
-            mc = dir;
-          }
-        };
-        visit(Z > 0, Z & 1, prev, 4);
-        visit(Y > 0, Y & 1, ym, 2);
-        visit(X > 0, X & 1, xm, 0);
-        visit(X + 1 < KX, X & 1, xp, 1);
-        visit(Y + 1 < KY, Y & 1, yp, 3);
-        visit(hn, Z & 1, next, 5);
-        c = uint8_t(mc | (mf << 3));
-      }
-      code[k] = c;
-    }
-    __syncthreads();
-    prev = cur;
-    cur = next;
-  }
-}
-
-// K2 fused (births -> tags), streaming along Z.  A warp covers 32 consecutive cells of a
-// Khalimsky row, X = X0-1 .. X0+30, and a CTA 18 rows, Y = Y0-1 .. Y0+16; codes (K2a) are formed
-// for all of them, tags (K2b) for the inner 30 x 16.  Step z forms the codes of plane z from the
-// births of planes z-1, z, z+1 (own column in registers, X neighbours by shuffle, Y neighbours
-// through shared memory) and the tags of plane z-1 from the codes of planes z-2, z-1, z.  Births
-// are prefetched two planes ahead; codes never leave the chip.
-constexpr int K2F_ROWS = 16, K2F_ZC = 32, K2F_THREADS = 32 * (K2F_ROWS + 2);
-inline unsigned k2f_grid(const Geom& g) {
-  return unsigned(((g.KX + 29) / 30) * ((g.KY + K2F_ROWS - 1) / K2F_ROWS) *
-                  ((g.KZ + K2F_ZC - 1) / K2F_ZC));
-}
-// Running max (facets) / min (cofacets) of (birth, position in the kidx order), branch-free.
-// Neighbours are visited in increasing kidx order (rank r = 0..5); a missing neighbour has birth
-// ABSENT_ORD and is skipped for cofacets (never < the initial ABSENT_ORD) and, as a facet of a
-// present cell, never occurs.
-struct CodeAcc {
-  uint32_t mcb, mfb, mc, mf;
-  __device__ __forceinline__ CodeAcc() : mcb(ABSENT_ORD), mfb(0u), mc(7u), mf(7u) {}
-  __device__ __forceinline__ void visit(bool exists, bool odd, uint32_t nb, uint32_t dir) {
-    const bool f = exists && odd && nb >= mfb;   // >=: the later (larger kidx) wins ties
-    const bool c = exists && !odd && nb < mcb;   // <: the earlier (smaller kidx) wins ties
-    mfb = f ? nb : mfb;
-    mf = f ? dir : mf;
-    mcb = c ? nb : mcb;
-    mc = c ? dir : mc;
-  }
-  __device__ __forceinline__ uint8_t code() const { return uint8_t(mc | (mf << 3)); }
-};
-// tag of a cell with code c given its six neighbours' codes packed one byte each by direction
-// (dir = 2 axis + (sign > 0)): UP if its min cofacet's max facet is itself, else DOWN if its max
-// facet's min cofacet is itself
-__device__ __forceinline__ uint8_t code_tag(uint8_t c, uint64_t nbp) {
-  if (c & CODE_ABSENT) return 0;
-  const uint32_t mc = c & 7, mf = (c >> 3) & 7;
-  const uint32_t tmc = uint32_t(nbp >> (8 * (mc & 7))) & 0xFF;  // mc == 7: reads byte 7 (= 0)
-  const uint32_t tmf = uint32_t(nbp >> (8 * (mf & 7))) & 0xFF;
-  if (mc != 7 && ((tmc >> 3) & 7) == (mc ^ 1)) return make_tag(KIND_UP, int(mc));
-  if (mf != 7 && (tmf & 7) == (mf ^ 1)) return make_tag(KIND_DOWN, int(mf));
-  return 0;
-}
-
-__global__ void __launch_bounds__(K2F_THREADS) k_apparent(const uint32_t* __restrict__ births,
-                                                         Geom g, uint8_t* __restrict__ tags,
-                                                         unsigned long long* __restrict__ app_cnt) {
-  const int KX = int(g.KX), KY = int(g.KY), KZ = int(g.KZ);
-  const int XB = (KX + 29) / 30, YB = (KY + K2F_ROWS - 1) / K2F_ROWS;
-  uint32_t blk = blockIdx.x;
-  const int xb = int(blk % XB);
-  blk /= XB;
-  const int yb = int(blk % YB), zb = int(blk / YB);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int X = xb * 30 - 1 + lane, Y = yb * K2F_ROWS - 1 + w;
-  const int Z0 = zb * K2F_ZC, Z1 = min(KZ, Z0 + K2F_ZC);
-  const bool vc = X >= 0 && X < KX && Y >= 0 && Y < KY;
-  const bool out_cell = vc && lane >= 1 && lane <= 30 && w >= 1 && w <= K2F_ROWS;
-  const bool ox = X & 1, oy = Y & 1;
-  const bool hxm = X > 0, hxp = X + 1 < KX, hym = Y > 0, hyp = Y + 1 < KY;
-  const uint32_t plane = uint32_t(KX) * uint32_t(KY);
-  __shared__ uint32_t s_b[K2F_ROWS + 4][32];   // births rows Y0-2 .. Y0+17 of plane z
-  __shared__ uint8_t s_c[2][K2F_ROWS + 2][32];  // codes rows Y0-1 .. Y0+16, planes z-1 | z
-  __shared__ uint32_t s_cnt[3];
-  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
-  // streams: own column, and one halo column for the CTA's edge threads (warp 0: row Y-1, the last
-  // warp: row Y+1, lanes 0/31: X-1/X+1; the four corner lanes also stream their X halo)
-  int hx = X, hy = Y;
-  if (w == 0) hy = Y - 1;
-  else if (w == K2F_ROWS + 1) hy = Y + 1;
-  else if (lane == 0) hx = X - 1;
-  else if (lane == 31) hx = X + 1;
-  const bool ewarp = w == 0 || w == K2F_ROWS + 1;
-  const bool has_h = hx != X || hy != Y;
-  const bool vh = has_h && hx >= 0 && hx < KX && hy >= 0 && hy < KY;
-  const bool xh = (lane == 0 || lane == 31) && ewarp;
-  const int cx = lane == 0 ? X - 1 : X + 1;
-  const bool vq = xh && cx >= 0 && cx < KX && Y >= 0 && Y < KY;
-  // stream pointers (advanced by one plane per step) and their validity
-  const uint32_t* po = births + (vc ? uint32_t(Y) * uint32_t(KX) + uint32_t(X) : 0u);
-  const uint32_t* ph = births + (vh ? uint32_t(hy) * uint32_t(KX) + uint32_t(hx) : 0u);
-  const uint32_t* pq = births + (vq ? uint32_t(Y) * uint32_t(KX) + uint32_t(cx) : 0u);
-  auto ld0 = [&](const uint32_t* p, bool ok, int zz) -> uint32_t {
-    return (ok && zz >= 0 && zz < KZ) ? __ldg(p + uint32_t(zz) * plane) : ABSENT_ORD;
-  };
-  uint32_t bzm = ld0(po, vc, Z0 - 2), bz = ld0(po, vc, Z0 - 1), bzp = ld0(po, vc, Z0);
-  uint32_t bzp2 = ld0(po, vc, Z0 + 1);
-  uint32_t hz = ld0(ph, vh, Z0 - 1), hzp = ld0(ph, vh, Z0), hzp2 = ld0(ph, vh, Z0 + 1);
-  uint32_t qz = ld0(pq, vq, Z0 - 1), qzp = ld0(pq, vq, Z0), qzp2 = ld0(pq, vq, Z0 + 1);
-  // next loads: plane z + 3
-  const int zl = Z0 + 2;
-  const uint32_t* no = po + (zl > 0 ? uint32_t(zl) * plane : 0u);
-  const uint32_t* nh = ph + (zl > 0 ? uint32_t(zl) * plane : 0u);
-  const uint32_t* nq = pq + (zl > 0 ? uint32_t(zl) * plane : 0u);
-  uint8_t cprev2 = CODE_ABSENT, cprev = CODE_ABSENT;
-  uint32_t nup = 0;  // UP cells per dimension, one byte each (<= K2F_ZC per thread)
-  uint8_t* tout = tags + (uint32_t(max(Y, 0)) * uint32_t(KX) + uint32_t(max(X, 0))) +
-                  uint64_t(max(Z0, 0)) * plane;
-  for (int z = Z0 - 1; z <= Z1; ++z) {
-    const bool lz = z + 3 < KZ;  // z + 3 >= Z0 + 2 >= 0
-    const uint32_t bnext = (vc && lz) ? __ldg(no) : ABSENT_ORD;
-    const uint32_t hnext = (vh && lz) ? __ldg(nh) : ABSENT_ORD;
-    const uint32_t qnext = (vq && lz) ? __ldg(nq) : ABSENT_ORD;
-    no += plane;
-    nh += plane;
-    nq += plane;
-    s_b[w + 1][lane] = bz;
-    if (w == 0) s_b[0][lane] = hz;
-    if (w == K2F_ROWS + 1) s_b[K2F_ROWS + 3][lane] = hz;
-    uint32_t xm = __shfl_up_sync(0xFFFFFFFFu, bz, 1), xp = __shfl_down_sync(0xFFFFFFFFu, bz, 1);
-    const uint32_t xe = ewarp ? qz : hz;
-    if (lane == 0) xm = xe;
-    if (lane == 31) xp = xe;
-    __syncthreads();
-    uint8_t cz = CODE_ABSENT;
-    if (vc && z >= 0 && z < KZ && bz != ABSENT_ORD) {
-      const bool oz = z & 1;
-      CodeAcc acc;
-      acc.visit(z > 0, oz, bzm, 4);
-      acc.visit(hym, oy, s_b[w][lane], 2);
-      acc.visit(hxm, ox, xm, 0);
-      acc.visit(hxp, ox, xp, 1);
-      acc.visit(hyp, oy, s_b[w + 2][lane], 3);
-      acc.visit(z + 1 < KZ, oz, bzp, 5);
-      cz = acc.code();
-    }
-    s_c[z & 1][w][lane] = cz;
-    __syncthreads();
-    // tags of plane z-1 from the codes of planes z-2, z-1, z
-    const int zt = z - 1;
-    const uint32_t cxm = __shfl_up_sync(0xFFFFFFFFu, uint32_t(cprev), 1);
-    const uint32_t cxp = __shfl_down_sync(0xFFFFFFFFu, uint32_t(cprev), 1);
-    if (zt >= Z0 && zt < Z1 && out_cell) {
-      const uint64_t nbp = uint64_t(cxm) | (uint64_t(cxp) << 8) |
-                           (uint64_t(s_c[zt & 1][w - 1][lane]) << 16) |
-                           (uint64_t(s_c[zt & 1][w + 1][lane]) << 24) |
-                           (uint64_t(cprev2) << 32) | (uint64_t(cz) << 40);
-      const uint8_t t = code_tag(cprev, nbp);
-      *tout = t;
-      nup += uint32_t(tag_kind(t) == KIND_UP) << (8 * (ox + oy + (zt & 1)));
-    }
-    if (zt >= Z0) tout += plane;
-    cprev2 = cprev;
-    cprev = cz;
-    bzm = bz;
-    bz = bzp;
-    bzp = bzp2;
-    bzp2 = bnext;
-    hz = hzp;
-    hzp = hzp2;
-    hzp2 = hnext;
-    qz = qzp;
-    qzp = qzp2;
-    qzp2 = qnext;
-  }
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, (nup >> (8 * d)) & 0xFFu);
-    if (lane == 0 && v) atomicAdd(s_cnt + d, v);
-  }
-  __syncthreads();
-  if (threadIdx.x < 3 && s_cnt[threadIdx.x])
-    atomicAdd(app_cnt + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
-}
-
-__global__ void __launch_bounds__(256) k_tags2(const uint8_t* __restrict__ code, Geom g,
-                                               uint8_t* __restrict__ tags,
-                                               unsigned long long* __restrict__ app_cnt) {
-  const K2Tile T = k2_tile(g);
-  uint8_t tag = 0;
-  int dim = 0;
-  if (T.valid) {
-    const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-    const uint32_t st[3] = {1u, KX, KX * KY};
-    const uint8_t c = code[T.k];
-    dim = (T.X & 1) + (T.Y & 1) + (T.Z & 1);
-    if (!(c & CODE_ABSENT)) {
-      const uint32_t mc = c & 7, mf = (c >> 3) & 7;
-      if (mc != 7) {
-        const uint32_t t = (mc & 1) ? T.k + st[mc >> 1] : T.k - st[mc >> 1];
-        if (((__ldg(code + t) >> 3) & 7) == (mc ^ 1)) tag = make_tag(KIND_UP, int(mc));
-      }
-      if (!tag && mf != 7) {
-        const uint32_t r = (mf & 1) ? T.k + st[mf >> 1] : T.k - st[mf >> 1];
-        if ((__ldg(code + r) & 7) == (mf ^ 1)) tag = make_tag(KIND_DOWN, int(mf));
-      }
-    }
-    tags[T.k] = tag;
-  }
-  const bool up = tag_kind(tag) == KIND_UP;
-  __shared__ uint32_t s_c[3];
-  if (threadIdx.x < 3) s_c[threadIdx.x] = 0;
-  __syncthreads();
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, up && dim == d);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(s_c + d, uint32_t(__popc(m)));
-  }
-  __syncthreads();
-  if (threadIdx.x < 3 && s_c[threadIdx.x])
-    atomicAdd(app_cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
-}
-
-// K2b over the codes formed by k_births_codes: 4 consecutive cells per thread (one 32-bit load of
-// their codes, one 32-bit store of their tags); the partner's code is a byte load (L1/L2).
-__global__ void __launch_bounds__(256) k_tags_codes(const uint8_t* __restrict__ code, Geom g,
-                                                    uint8_t* __restrict__ tags,
-                                                    unsigned long long* __restrict__ app_cnt) {
-  const uint64_t k0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-  const uint64_t N = uint64_t(g.ncells);
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  auto stride = [&](uint32_t ax) -> int64_t {
-    return ax == 0 ? 1 : (ax == 1 ? int64_t(KX) : int64_t(KX) * KY);
-  };
-  uint32_t nup = 0;
-  if (k0 < N) {
-    uint32_t w4 = 0;
-    if (k0 + 3 < N) {
-      w4 = __ldg(reinterpret_cast<const uint32_t*>(code + k0));
-    } else {
-      for (uint64_t j = 0; k0 + j < N; ++j) w4 |= uint32_t(code[k0 + j]) << (8 * j);
-    }
-    uint32_t X = uint32_t(k0 % KX), Y = uint32_t((k0 / KX) % KY), Z = uint32_t(k0 / (uint64_t(KX) * KY));
-    uint32_t out = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t k = k0 + j;
-      if (k < N) {
-        const uint8_t c = uint8_t(w4 >> (8 * j));
-        uint8_t tag = 0;
-        if (!(c & CODE_ABSENT)) {
-          const uint32_t mc = c & 7, mf = (c >> 3) & 7;
-          if (mc != 7) {
-            const int64_t t = int64_t(k) + ((mc & 1) ? stride(mc >> 1) : -stride(mc >> 1));
-            if (((__ldg(code + t) >> 3) & 7) == (mc ^ 1)) tag = make_tag(KIND_UP, int(mc));
-          }
-          if (!tag && mf != 7) {
-            const int64_t r = int64_t(k) + ((mf & 1) ? stride(mf >> 1) : -stride(mf >> 1));
-            if ((__ldg(code + r) & 7) == (mf ^ 1)) tag = make_tag(KIND_DOWN, int(mf));
-          }
-          if (tag_kind(tag) == KIND_UP) nup += 1u << (8 * ((X & 1) + (Y & 1) + (Z & 1)));
-        }
-        out |= uint32_t(tag) << (8 * j);
-      }
-      if (++X == KX) {
-        X = 0;
-        if (++Y == KY) {
-          Y = 0;
-          ++Z;
-        }
-      }
-    }
-    if (k0 + 3 < N) {
-      *reinterpret_cast<uint32_t*>(tags + k0) = out;
-    } else {
-      for (uint64_t j = 0; k0 + j < N; ++j) tags[k0 + j] = uint8_t(out >> (8 * j));
-    }
-  }
-  __shared__ uint32_t s_c[3];
-  if (threadIdx.x < 3) s_c[threadIdx.x] = 0;
-  __syncthreads();
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, (nup >> (8 * d)) & 0xFFu);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(s_c + d, v);
-  }
-  __syncthreads();
-  if (threadIdx.x < 3 && s_c[threadIdx.x])
-    atomicAdd(app_cnt + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
-}
-
-// ---------------------------------------------------------------------------------------------
 // K1 + K2 fused (the default): births AND apparent-pair tags of every cell from one read of the
-// image (PAPER.md:97-108 for the births, PAPER.md:44-45 for the apparent pairs; the same pairs as
-// k_births + k_apparent above).  A thread owns one voxel column (x, y) and walks it along z; its
+// image (PAPER.md:97-108 for the births, PAPER.md:44-45 for the apparent pairs).  A thread owns one voxel column (x, y) and walks it along z; its
 // unit of work is the voxel block B(x,y,z) = the 8 cells (2x+i, 2y+j, 2z+k), i,j,k in {0,1},
 // whose births are maxima over the voxels (x..x+i, y..y+j, z..z+k): with the "plane cells"
 // P(z) = {V, Ex, Ey, Sxy} of a block, the k=1 cells are max(P(z), P(z+1)) (4 max per block).
@@ -916,6 +61,7 @@ __global__ void __launch_bounds__(256) k_tags_codes(const uint8_t* __restrict__ 
 // region costs only its stores.
 // Layout in registers: births b[i + 2j + 4k]; codes and tags packed in two words by j, byte i+2k.
 // ---------------------------------------------------------------------------------------------
+constexpr uint8_t CODE_ABSENT = 0x40;  // code bit 6: the cell is absent (+inf birth)
 constexpr int KF_ROWS = 14, KF_THREADS = 32 * (KF_ROWS + 2);
 struct KfLaunch {
   unsigned grid;
@@ -1386,72 +532,6 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
   return p;
 }
 
-__global__ void k_mm_find(Cand* cand, unsigned n, uint32_t* parent, unsigned long long* best,
-                          uint8_t* alive) {
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  Cand c = cand[i];
-  uint32_t a = uf_find(parent, c.a), b = uf_find(parent, c.b);
-  cand[i].a = a;
-  cand[i].b = b;
-  if (a == b) {  // connected through strictly smaller edges: positive
-    alive[i] = 0;
-    return;
-  }
-  alive[i] = 1;
-  atomicMin(best + a, (unsigned long long)c.key);
-  atomicMin(best + b, (unsigned long long)c.key);
-}
-
-__global__ void k_mm_commit(const Cand* cand, unsigned n, const uint32_t* __restrict__ births,
-                            Geom g, uint32_t* parent, const unsigned long long* best,
-                            uint8_t* alive, uint8_t* tags, uint64_t* rec,
-                            unsigned long long* nrec) {
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || !alive[i]) return;
-  Cand c = cand[i];
-  // Commit when the edge is the minimum at both components (the next Kruskal merge there), or
-  // when it is the minimum at the YOUNGER component alone: that component does not change before
-  // the edge, and the other one can only merge with older roots first, so the younger root dies
-  // at this edge whatever happens on the other side.  (Mutual minima alone degenerate into one
-  // merge per round when a large old component absorbs many young ones.)
-  const bool min_a = best[c.a] == c.key, min_b = best[c.b] == c.key;
-  if (!min_a && !min_b) return;
-  uint32_t ka = vox_kidx(g, c.a), kb = vox_kidx(g, c.b);
-  uint64_t keya = make_key(births[ka], ka), keyb = make_key(births[kb], kb);
-  const bool a_young = keya > keyb;
-  if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) return;
-  uint32_t young = a_young ? c.a : c.b, old = a_young ? c.b : c.a;
-  uint32_t kyoung = a_young ? ka : kb;
-  parent[young] = old;  // elder rule: the younger component dies
-  tags[key_kidx(c.key)] = make_tag(KIND_CLEARED, 0);  // a death edge: cleared for dim 1
-  unsigned long long r = atomicAdd(nrec, 1ull);
-  rec[r] = (uint64_t(kyoung) << 32) | key_kidx(c.key);
-  alive[i] = 2;
-}
-
-__global__ void k_mm_reset(Cand* cand, unsigned n, unsigned long long* best, const uint8_t* alive,
-                           Cand* next, unsigned* nnext) {
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  bool keep = false;
-  Cand c;
-  if (i < n) {
-    c = cand[i];
-    if (alive[i]) {
-      best[c.a] = NONE64;
-      best[c.b] = NONE64;
-    }
-    keep = alive[i] == 1;
-  }
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, keep);
-  if (!mask) return;
-  int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(nnext, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (keep) next[base + __popc(mask & ((1u << lane) - 1))] = c;
-}
-
 __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
                                const uint32_t* __restrict__ parent, uint64_t* rec,
                                unsigned long long* nrec, unsigned long long* nroots) {
@@ -1470,226 +550,6 @@ __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
   if (lane == __ffs(mask) - 1) base = atomicAdd(nrec, (unsigned long long)__popc(mask));
   base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
   if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
-}
-
-// ---- single-CTA variant for up to SMEM_BASINS basins: the same mutual-minimum rounds, with the
-// union-find forest and the per-component minimum in shared memory and __syncthreads between
-// phases (a round costs ~1 us instead of a host round trip).  Basins are renumbered by their rank
-// in elder order, so the elder of two roots is simply the smaller id; candidate edges are sorted
-// by key, so a component's minimum edge is the smallest edge index.
-constexpr int SMEM_BASINS = 56000;
-// Up to this many roots the union-find runs in one CTA's shared memory (Boruvka MSF + Kruskal),
-// beyond it as device-wide merge rounds.  Since the rounds also commit a younger component's
-// minimum edge they take ~10-15 rounds on every config and beat the one-CTA path everywhere
-// (profiles/r01: C1 H0 1.38 -> 0.47 ms, C4 top dim 15.8 -> 0.52 ms), so the default is 0;
-// CR_SMEM_BASINS=n (<= SMEM_BASINS) brings the one-CTA path back for cross-checks.
-unsigned smem_basins_max() {
-  const char* e = std::getenv("CR_SMEM_BASINS");
-  const unsigned v = e ? unsigned(std::strtoul(e, nullptr, 10)) : 0u;
-  return v < unsigned(SMEM_BASINS) ? v : unsigned(SMEM_BASINS);
-}  // u32 union-find in <= 224 KB of shared memory; ranks < 2^16
-constexpr int H0_THREADS = 1024;
-
-__global__ void k_collect_roots(const uint32_t* __restrict__ births, Geom g,
-                                const uint32_t* __restrict__ parent, uint64_t* rootkey,
-                                unsigned* nroot) {
-  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool emit = false;
-  uint64_t key = 0;
-  if (vv < g.nvox) {
-    uint32_t v = uint32_t(vv);
-    uint32_t k = vox_kidx(g, v);
-    if (parent[v] == v && births[k] != ABSENT_ORD) {
-      emit = true;
-      key = make_key(births[k], k);
-    }
-  }
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(nroot, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) rootkey[base + __popc(mask & ((1u << lane) - 1))] = key;
-}
-
-__global__ void k_rank_roots(const uint64_t* __restrict__ rootkey, unsigned nb, Geom g,
-                             uint32_t* rank_of) {
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nb) rank_of[kidx_vox(g, key_kidx(rootkey[i]))] = i;
-}
-
-__global__ void k_cand_pack(const Cand* __restrict__ cand, unsigned n,
-                            const uint32_t* __restrict__ rank_of, uint64_t* keys, uint32_t* ab) {
-  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const Cand c = cand[i];
-  keys[i] = c.key;
-  ab[i] = (rank_of[c.a] << 16) | rank_of[c.b];
-}
-
-__device__ __forceinline__ uint32_t sfind(uint32_t* par, uint32_t x) {
-  while (true) {
-    const uint32_t p = par[x];
-    if (p == x) return x;
-    const uint32_t pp = par[p];
-    if (pp != p) par[x] = pp;  // path halving (benign under concurrency: both are ancestors)
-    x = pp;
-  }
-}
-
-// Boruvka on the basin graph (one CTA, union-find in shared memory): every component's minimum
-// edge is a minimum-spanning-forest edge (keys are distinct); components hook along them (of a
-// mutual pair only the larger id hooks) until no edge joins two components.  MSF edges are exactly
-// Kruskal's merge edges; the others close cycles (positive edges, dimension-1 columns).
-__global__ void __launch_bounds__(H0_THREADS) k_h0_boruvka(
-    const uint32_t* __restrict__ ab, unsigned n, unsigned nb, uint32_t* best, uint32_t* act0,
-    uint32_t* act1, uint32_t* hook, uint32_t* msf, unsigned* nmsf, unsigned long long* rounds_out) {
-  extern __shared__ uint32_t sh[];
-  uint32_t* par = sh;
-  __shared__ unsigned s_nnext;
-  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) {
-    par[i] = i;
-    best[i] = 0xFFFFFFFFu;
-  }
-  for (unsigned i = threadIdx.x; i < n; i += H0_THREADS) act0[i] = i;
-  __syncthreads();
-  unsigned na = n;
-  uint32_t* act = act0;
-  uint32_t* nxt = act1;
-  unsigned long long rounds = 0;
-  while (na > 0) {
-    if (threadIdx.x == 0) s_nnext = 0;
-    __syncthreads();
-    for (unsigned t = threadIdx.x; t < na; t += H0_THREADS) {
-      const uint32_t e = act[t];
-      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
-      if (a == b) continue;  // closes a cycle: not an MSF edge
-      atomicMin(best + a, e);
-      atomicMin(best + b, e);
-      nxt[atomicAdd(&s_nnext, 1u)] = e;
-    }
-    __syncthreads();
-    // hook targets (computed before any hooking)
-    for (unsigned c = threadIdx.x; c < nb; c += H0_THREADS) {
-      uint32_t h = 0xFFFFFFFFu;
-      if (par[c] == c && best[c] != 0xFFFFFFFFu) {
-        const uint32_t e = best[c];
-        const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
-        const uint32_t o = a == c ? b : a;
-        if (!(best[o] == e && c < o)) h = o;  // of a mutual pair only the larger id hooks
-        if (best[o] != e || c < o) msf[atomicAdd(nmsf, 1u)] = e;  // record each edge once
-      }
-      hook[c] = h;
-    }
-    __syncthreads();
-    for (unsigned c = threadIdx.x; c < nb; c += H0_THREADS) {
-      if (hook[c] != 0xFFFFFFFFu) par[c] = hook[c];
-      best[c] = 0xFFFFFFFFu;
-    }
-    __syncthreads();
-    na = s_nnext;
-    uint32_t* tmp = act;
-    act = nxt;
-    nxt = tmp;
-    ++rounds;
-  }
-  if (threadIdx.x == 0) *rounds_out = rounds;
-}
-
-// Elder-rule Kruskal over the MSF edges in key order (one thread; union-find in shared memory).
-__global__ void __launch_bounds__(H0_THREADS) k_h0_kruskal(
-    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ab,
-    const uint32_t* __restrict__ msf, unsigned nmsf, const uint64_t* __restrict__ rootkey,
-    unsigned nb, uint8_t* tags, uint64_t* rec, unsigned long long* nrec) {
-  extern __shared__ uint32_t sh[];
-  uint32_t* par = sh;
-  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) par[i] = i;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long r = *nrec;
-    for (unsigned t = 0; t < nmsf; ++t) {
-      const uint32_t e = msf[t];
-      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
-      const uint32_t young = a > b ? a : b, old = a > b ? b : a;  // elder = smaller rank
-      par[young] = old;
-      const uint32_t ke = key_kidx(keys[e]);
-      tags[ke] = make_tag(KIND_CLEARED, 0);
-      rec[r++] = (uint64_t(key_kidx(rootkey[young])) << 32) | ke;
-    }
-    *nrec = r;
-  }
-  __syncthreads();
-  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS)
-    if (par[i] == i) {
-      const unsigned long long r = atomicAdd(nrec, 1ull);
-      rec[r] = (uint64_t(key_kidx(rootkey[i])) << 32) | NONE32;
-    }
-}
-
-__global__ void __launch_bounds__(H0_THREADS) k_h0_smem(
-    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ab, unsigned n,
-    const uint64_t* __restrict__ rootkey, unsigned nb, uint32_t* act0, uint32_t* act1,
-    uint8_t* tags, uint64_t* rec, unsigned long long* nrec, unsigned long long* rounds_out) {
-  extern __shared__ uint32_t sh[];
-  uint32_t* par = sh;
-  uint32_t* best = sh + nb;
-  __shared__ unsigned s_nnext;
-  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) {
-    par[i] = i;
-    best[i] = 0xFFFFFFFFu;
-  }
-  for (unsigned i = threadIdx.x; i < n; i += H0_THREADS) act0[i] = i;
-  __syncthreads();
-  unsigned na = n;
-  uint32_t* act = act0;
-  uint32_t* nxt = act1;
-  unsigned long long rounds = 0;
-  while (na > 0) {
-    // phase 1: components' minimum edges (edges inside one component are positive: dropped)
-    for (unsigned t = threadIdx.x; t < na; t += H0_THREADS) {
-      const uint32_t e = act[t];
-      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
-      if (a != b) {
-        atomicMin(best + a, e);
-        atomicMin(best + b, e);
-      }
-    }
-    if (threadIdx.x == 0) s_nnext = 0;
-    __syncthreads();
-    // phase 2: an edge minimal at both components is the next Kruskal merge there
-    for (unsigned t = threadIdx.x; t < na; t += H0_THREADS) {
-      const uint32_t e = act[t];
-      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
-      if (a == b) continue;  // positive edge
-      if (best[a] == e && best[b] == e) {
-        const uint32_t young = a > b ? a : b, old = a > b ? b : a;  // elder = smaller rank
-        par[young] = old;
-        const uint32_t ke = key_kidx(keys[e]);
-        tags[ke] = make_tag(KIND_CLEARED, 0);
-        const unsigned long long r = atomicAdd(nrec, 1ull);
-        rec[r] = (uint64_t(key_kidx(rootkey[young])) << 32) | ke;
-      } else {
-        nxt[atomicAdd(&s_nnext, 1u)] = e;
-      }
-    }
-    __syncthreads();
-    // phase 3: reset the minima; next round's active list
-    for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) best[i] = 0xFFFFFFFFu;
-    na = s_nnext;
-    uint32_t* tmp = act;
-    act = nxt;
-    nxt = tmp;
-    ++rounds;
-    __syncthreads();
-  }
-  // essential classes: the remaining roots
-  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS)
-    if (par[i] == i) {
-      const unsigned long long r = atomicAdd(nrec, 1ull);
-      rec[r] = (uint64_t(key_kidx(rootkey[i])) << 32) | NONE32;
-    }
-  if (threadIdx.x == 0) *rounds_out = rounds;
 }
 
 __global__ void k_count_basins(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
@@ -1836,27 +696,6 @@ __global__ void k_dual_absent_vox(const uint32_t* __restrict__ births, DualG G,
 }
 
 // absent faces join their absent sides (larger id = elder root, OMEGA the eldest)
-__global__ void k_dual_absent(const uint32_t* __restrict__ births, DualG G, uint32_t* parent) {
-  const int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (kk >= G.g.ncells) return;
-  const uint32_t k = uint32_t(kk);
-  if (births[k] != ABSENT_ORD) return;
-  const int n = face_normal(G.g, k);
-  if (n < 0) return;
-  uint32_t a = dual_side(G, k, n, 0), b = dual_side(G, k, n, 1);
-  while (true) {
-    a = d_find(parent, a);
-    b = d_find(parent, b);
-    if (a == b) return;
-    if (a > b) {
-      const uint32_t t = a;
-      a = b;
-      b = t;
-    }
-    if (atomicCAS(parent + a, a, b) == a) return;
-  }
-}
-
 __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                              DualG G, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
                              unsigned int* __restrict__ ncand) {
@@ -1924,14 +763,6 @@ __global__ void k_dual_roots(const uint32_t* __restrict__ births, DualG G,
   if (emit) rootkey[base + __popc(mask & ((1u << lane) - 1))] = key;
 }
 
-__global__ void k_dual_rank(const uint64_t* __restrict__ rootkey, unsigned nb, DualG G,
-                            uint32_t* rank_of) {
-  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nb) return;
-  const uint64_t key = ~rootkey[i];
-  rank_of[key == ~0ull ? G.omega : kidx_vox(G.g, key_kidx(key))] = i;
-}
-
 // dual record of the edge with complemented key ek whose younger root has key ry
 __device__ __forceinline__ uint64_t dual_record(uint64_t ek, uint64_t ry) {
   const uint32_t sigma = ~key_kidx(ek);
@@ -1939,56 +770,8 @@ __device__ __forceinline__ uint64_t dual_record(uint64_t ek, uint64_t ry) {
   return (uint64_t(sigma) << 32) | (absent ? NONE32 : key_kidx(ry));
 }
 
-// Kruskal over the MSF edges in (complemented) key order, elder = smaller rank.
-__global__ void __launch_bounds__(H0_THREADS) k_dual_kruskal(
-    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ab,
-    const uint32_t* __restrict__ msf, unsigned nmsf, const uint64_t* __restrict__ rootkey,
-    unsigned nb, uint64_t* rec, unsigned long long* nrec) {
-  extern __shared__ uint32_t sh[];
-  uint32_t* par = sh;
-  for (unsigned i = threadIdx.x; i < nb; i += H0_THREADS) par[i] = i;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long r = *nrec;
-    for (unsigned t = 0; t < nmsf; ++t) {
-      const uint32_t e = msf[t];
-      const uint32_t a = sfind(par, ab[e] >> 16), b = sfind(par, ab[e] & 0xFFFFu);
-      const uint32_t young = a > b ? a : b, old = a > b ? b : a;
-      par[young] = old;
-      rec[r++] = dual_record(keys[e], ~rootkey[young]);
-    }
-    *nrec = r;
-  }
-}
-
-// Device-wide dual merge round (mirror of k_mm_commit: the elder is the LARGER key): an edge
-// commits if it is the minimum (in complemented order) at both components, or at the younger one.
-__global__ void k_dual_mm_commit(const Cand* cand, unsigned n, const uint32_t* __restrict__ births,
-                                 DualG G, uint32_t* parent, const unsigned long long* best,
-                                 uint8_t* alive, uint64_t* rec, unsigned long long* nrec) {
-  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || !alive[i]) return;
-  const Cand c = cand[i];
-  const bool min_a = best[c.a] == c.key, min_b = best[c.b] == c.key;
-  if (!min_a && !min_b) return;
-  const uint64_t ka = dual_root_key(births, G, c.a), kb = dual_root_key(births, G, c.b);
-  const bool a_young = ka < kb;
-  if (!(min_a && min_b) && (a_young ? !min_a : !min_b)) return;
-  const uint32_t young = a_young ? c.a : c.b, old = a_young ? c.b : c.a;
-  parent[young] = old;
-  const unsigned long long r = atomicAdd(nrec, 1ull);
-  rec[r] = dual_record(c.key, a_young ? ka : kb);
-  alive[i] = 2;
-}
-
-// All merge rounds (H0 or the dual) in one cooperative launch: the phases of k_mm_find,
-// k_mm_commit / k_dual_mm_commit and k_mm_reset separated by grid syncs, looping on the device
-// until no candidate is left -- instead of three launches, a memset and a host round trip per
-// round (C1: 14 rounds cost ~35 us each on the host path).  Same per-edge logic, so the same
-// commits in the same rounds.  ctl: [0]/[1] survivor counters (double-buffered), [2] rounds.
 struct MMArgs {
   Cand* cur;
-  Cand* nxt;
   const unsigned* n;  // device: the number of candidates (read by the kernel: no host round trip)
   uint32_t* parent;
   unsigned long long* best;  // 2 * nbest entries (two buffers, by round parity)
@@ -2041,7 +824,12 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
     }
     grid.sync();
     unsigned left = 0;
-    for (unsigned i = gt; i < n; i += gs) {  // commit (see k_mm_commit / k_dual_mm_commit)
+    // commit: an edge that is the minimum at both of its components is the next Kruskal merge
+    // there; one that is the minimum at the younger component alone also commits -- that
+    // component does not change before the edge, so its root dies at this edge whatever the
+    // other side does first (the elder rule).  Dual graph: the
+    // same with the elder rule reversed (the root with the larger key survives).
+    for (unsigned i = gt; i < n; i += gs) {
       if (A.alive[i] != 3) continue;
       const Cand c = cur[i];
       const bool min_a = bc[c.a] == c.key, min_b = bc[c.b] == c.key;
@@ -2086,11 +874,10 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
   if (gt == 0) A.ctl[2] = rounds;
 }
 
-// Launches the merge rounds on the *n_dev candidates (cand, spare buffer cand2, both holding
-// n_max); ctl (4 device unsigned, zeroed by the caller) receives the number of rounds in ctl[2].
+// Launches the merge rounds on the *n_dev candidates (cand, holding n_max); ctl (4 device unsigned, zeroed by the caller) receives the number of rounds in ctl[2].
 // No host synchronisation: the caller reads ctl[2] with its next scalar read.
 template <bool DUAL>
-void mm_rounds(Cand* cand, Cand* cand2, const unsigned* n_dev, int64_t n_max, uint32_t* parent,
+void mm_rounds(Cand* cand, const unsigned* n_dev, int64_t n_max, uint32_t* parent,
                unsigned long long* best, unsigned nbest, uint8_t* alive, const uint32_t* births,
                const Geom& g,
                const DualG& G, uint8_t* tags, uint64_t* rec, unsigned long long* nrec,
@@ -2112,19 +899,17 @@ void mm_rounds(Cand* cand, Cand* cand2, const unsigned* n_dev, int64_t n_max, ui
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   CR_CUDA(cudaMemsetAsync(alive, 1, size_t(n_max > 0 ? n_max : 1), s));
-  MMArgs A{cand, cand2, n_dev, parent, best, nbest, alive, births, g, G, tags, rec, nrec, ctl};
+  MMArgs A{cand, n_dev, parent, best, nbest, alive, births, g, G, tags, rec, nrec, ctl};
   void* args[] = {&A};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k_mm_rounds<DUAL>, dim3(unsigned(blocks)), dim3(256),
                                       args, 0, s));
   ++g_launch_count;
 }
 
-// Returns false (doing nothing) if the dual graph has more than max_basins roots: its union-find
-// then runs on one CTA's shared memory only up to SMEM_BASINS roots, and the device-wide
-// mutual-minimum rounds degenerate on the dual graph (the outside vertex absorbs components one
-// per round), so the caller reduces the coboundary matrix instead.
-bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st,
-              unsigned max_basins) {
+// The top dimension d = D-1 by Alexander duality: a union-find with the
+// reversed elder rule on the dual graph (top cells + the outside vertex, (D-1)-cells as edges),
+// run as device-wide merge rounds.  Always succeeds (returns true).
+bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st) {
   cudaStream_t s = ws.stream();
   const Geom& g = S.g;
   const int B = 256;
@@ -2137,10 +922,7 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   uint32_t* parent = ws.alloc<uint32_t>(nv);
   k_dual_parent<<<grid_for(nv, B), B, 0, s>>>(S.births, S.tags, G, parent);
   CR_CHECK_LAUNCH();
-  if (std::getenv("CR_DUAL_ABSENT_CELLS"))  // the per-cell form (cross-check)
-    k_dual_absent<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, G, parent);
-  else
-    k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
+  k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
   CR_CHECK_LAUNCH();
   k_pointer_jump<<<grid_for(nv, B), B, 0, s>>>(parent, nv);
   CR_CHECK_LAUNCH();
@@ -2154,97 +936,30 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   CR_CUDA(cudaStreamSynchronize(s));
   unsigned n = unsigned(hs.p[0] & 0xFFFFFFFFu);
   const unsigned nb = unsigned(hs.p[1]);
-  if (nb > max_basins) {
-    ws.release(cand);
-    ws.release(parent);
-    return false;
-  }
   st.columns[d] = nb;
 
   unsigned long long* nrec = cnt + 2;
-  if (nb > smem_basins_max()) {  // device-wide merge rounds
-    unsigned long long* best = ws.alloc<unsigned long long>(2 * nv);
-    CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * nv * sizeof(unsigned long long), s));
-    uint8_t* alive = ws.alloc<uint8_t>(n + 1);
-    Cand* cand2 = ws.alloc<Cand>(n + 1);
-    unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 6);  // cnt[6], cnt[7]: zeroed above
-    mm_rounds<true>(cand, cand2, ncand, n, parent, best, unsigned(nv), alive, S.births, g, G,
-                    nullptr, S.R.rec[d], nrec, ctl, ws);
-    CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 2, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            s));
-    CR_CUDA(cudaStreamSynchronize(s));
-    S.R.n[d] = int64_t(hs.p[0]);
-    st.rounds[d] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 4)[2]);
-    return true;
-  }
-  {
-    uint64_t* rootkey = ws.alloc<uint64_t>(nb + 1);
-    k_dual_roots<<<grid_for(nv, B), B, 0, s>>>(S.births, G, parent, rootkey,
-                                               reinterpret_cast<unsigned*>(cnt + 3), nullptr);
-    CR_CHECK_LAUNCH();
-    sort_keys_u64(rootkey, nb, false, 64, ws);
-    uint32_t* rank_of = ws.alloc<uint32_t>(nv);
-    k_dual_rank<<<grid_for(nb, B), B, 0, s>>>(rootkey, nb, G, rank_of);
-    CR_CHECK_LAUNCH();
-    uint64_t* keys = ws.alloc<uint64_t>(n + 1);
-    uint32_t* ab = ws.alloc<uint32_t>(n + 1);
-    if (n > 0) {
-      k_cand_pack<<<grid_for(n, B), B, 0, s>>>(cand, n, rank_of, keys, ab);
-      CR_CHECK_LAUNCH();
-      uint64_t* k2 = ws.alloc<uint64_t>(n);
-      uint32_t* v2 = ws.alloc<uint32_t>(n);
-      cub::DoubleBuffer<uint64_t> dk(keys, k2);
-      cub::DoubleBuffer<uint32_t> dv(ab, v2);
-      size_t tmp = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 64, s));
-      void* t = ws.alloc_bytes(tmp);
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(n), 0, 64, s));
-      keys = dk.Current();
-      ab = dv.Current();
-    }
-    uint32_t* act0 = ws.alloc<uint32_t>(n + 1);
-    uint32_t* act1 = ws.alloc<uint32_t>(n + 1);
-    uint32_t* best32 = ws.alloc<uint32_t>(nb + 1);
-    uint32_t* hook = ws.alloc<uint32_t>(nb + 1);
-    uint32_t* msf = ws.alloc<uint32_t>(nb + 1);
-    unsigned* nmsf = reinterpret_cast<unsigned*>(cnt + 4);
-    const size_t smem = size_t(nb > 0 ? nb : 1) * 4;
-    CR_CUDA(cudaFuncSetAttribute(k_h0_boruvka, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    CR_CUDA(cudaFuncSetAttribute(k_dual_kruskal, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    k_h0_boruvka<<<1, H0_THREADS, smem, s>>>(ab, n, nb, best32, act0, act1, hook, msf, nmsf,
-                                             cnt + 5);
-    CR_CHECK_LAUNCH();
-    const unsigned nm = read_scalar(nmsf, s, hs);
-    if (nm > 1) {
-      uint32_t* m2 = ws.alloc<uint32_t>(nm);
-      cub::DoubleBuffer<uint32_t> dm(msf, m2);
-      size_t tmp = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, dm, int(nm), 0, 32, s));
-      void* t = ws.alloc_bytes(tmp);
-      CR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, dm, int(nm), 0, 32, s));
-      msf = dm.Current();
-    }
-    k_dual_kruskal<<<1, H0_THREADS, smem, s>>>(keys, ab, msf, nm, rootkey, nb, S.R.rec[d], nrec);
-    CR_CHECK_LAUNCH();
-    st.rounds[d] = int64_t(read_scalar(cnt + 5, s, hs));
-    S.R.n[d] = int64_t(read_scalar(nrec, s, hs));
-  }
+  unsigned long long* best = ws.alloc<unsigned long long>(2 * nv);
+  CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * nv * sizeof(unsigned long long), s));
+  uint8_t* alive = ws.alloc<uint8_t>(n + 1);
+  unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 6);  // cnt[6], cnt[7]: zeroed above
+  mm_rounds<true>(cand, ncand, n, parent, best, unsigned(nv), alive, S.births, g, G, nullptr,
+                  S.R.rec[d], nrec, ctl, ws);
+  CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 2, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  S.R.n[d] = int64_t(hs.p[0]);
+  st.rounds[d] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 4)[2]);
+  ws.release(best);
+  ws.release(alive);
+  ws.release(cand);
+  ws.release(parent);
   return true;
 }
 
-// In a full barcode the reduction of the top dimension is cheap once lower dimensions are cleared;
-// the dual union-find wins while its roots fit a fast single-CTA pass (measured: C1 2.7k roots,
-// 1.1 vs 2.0 ms; C4 50k roots, 15.8 vs 8.7 ms).
-unsigned dual_max_basins() {  // tuning knob CR_DUAL_MAX (measurement); default: always
-  const char* e = std::getenv("CR_DUAL_MAX");
-  return e ? unsigned(std::strtoul(e, nullptr, 10)) : 0xFFFFFFFFu;
-}
 bool use_dual(const Geom& g, int d) {
   if (d != g.D - 1 || d < 1) return false;
-  const char* e = std::getenv("CR_TOP_REDUCE");  // force the coboundary reduction (cross-checks)
-  return !(e && e[0] == '1');
+  return opt(OPT_TOP_REDUCE) == 0;  // the coboundary reduction instead (cross-checks)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2316,29 +1031,16 @@ __global__ void k_partner_records(const uint64_t* __restrict__ rec, int64_t n,
 
 // ---------------------------------------------------------------------------------------------
 // Dimensions 1..dmax after H0: dimension 1 by the cohomology reduction, whose
-// pivots clear dimension 2, then the top dimension by duality.  Alternative (CR_K5_HOM=1, 3D):
-// the top dimension 2 by duality first (it needs no clearing), then dimension 1 by the HOMOLOGY
-// reduction of the square columns with the clearing of the squares that create a 2-class (the
-// twist).  Its reduced columns are 1-cycles: on C4 the entry work halves (210 M -> 115 M entries,
-// heaviest column 55 M -> 10.6 M) but the additions grow (423 k -> 545 k) and the critical chain
-// of dependent additions is as long (366 vs 363 rounds): 168 vs 174 ms, C5 1.63 vs 1.76 s, so
-// cohomology stays the default.  Both give the same pairing (unique given reading R1).
+// pivots clear dimension 2, then the top dimension by duality.  (Round 1 also measured dimension 1
+// by the homology reduction of the square columns after the top dimension: half the entry work on
+// C4 but more additions and an equally long critical chain -- 174 vs 168 ms, C5 1.76 vs 1.63 s --
+// and removed it.)
 void reduce_dims(GeneralState& S, const Geom& g, int dmax, Workspace& ws, HostScalars& hs,
                  cr_stats& st) {
   static const char* names[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
   cudaStream_t s = ws.stream();
-  const char* e = std::getenv("CR_K5_HOM");
-  const bool hom1 = g.D == 3 && dmax >= 1 && use_dual(g, 2) && e && e[0] == '1';
-  if (hom1) {
-    if (!top_dual(S, 2, ws, hs, st, 0xFFFFFFFFu)) throw Error{CR_EINTERNAL, "top dimension"};
-    prof_mark(s, names[2]);
-    mark_cleared_births(S, 2, ws);
-    reduce_dimension(S, 1, ws, hs, st, /*hom=*/true);
-    prof_mark(s, names[1]);
-    return;
-  }
   for (int d = 1; d <= dmax; ++d) {
-    if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st, dual_max_basins())))
+    if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st)))
       reduce_dimension(S, d, ws, hs, st);
     prof_mark(s, names[d]);
   }
@@ -2355,14 +1057,9 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
 
-  // Default: K1 + K2 in one kernel (k_filtration).  Variants for cross-checks and measurement
-  // (profiles/r01/s3: C5 K1+K2 = 0.52 + 3.60 ms as k_births + k_apparent (CR_K12_OLD),
-  // 1.91 + 1.76 fused births+codes, 0.52 + 1.66 + 1.76 split): CR_K12_OLD, CR_K12_FUSED,
-  // CR_K12_SPLIT, CR_K2_TWOPASS, CR_K2_ONEPASS.
-  const bool k12_old = !(std::getenv("CR_K12_FUSED") || std::getenv("CR_K12_SPLIT"));
-  const bool k12_sep = std::getenv("CR_K12_OLD") || std::getenv("CR_K2_ONEPASS") ||
-                       std::getenv("CR_K2_TWOPASS") || !k12_old;
-  if (!k12_sep) {  // default: K1 + K2 in one streaming kernel
+  // K1 + K2 in one streaming kernel (round 1 measured the split alternatives, profiles/r01/s3:
+  // C5 0.52 + 3.60 ms as separate births + apparent-pair kernels)
+  {
     const KfLaunch L = kf_launch(g);
     static thread_local int kf_attr_dev = -1;
     if (kf_attr_dev != ws.device()) {
@@ -2374,46 +1071,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
                                                             S.tags, cnt, nan_flag);
     CR_CHECK_LAUNCH();
     prof_mark(s, "filtration");
-  } else if (!k12_old && std::getenv("CR_K12_SPLIT")) {
-    // K1 (births) alone, then K2 as codes (z-streaming) + tags from codes
-    uint8_t* code = ws.alloc<uint8_t>(g.ncells + 4);
-    k_births<<<k_births_grid(g), 256, 0, s>>>(image, g, S.births, cnt + 4, nan_flag);
-    CR_CHECK_LAUNCH();
-    prof_mark(s, "births");
-    k_codes_z<<<k2z_grid(g), 256, 0, s>>>(S.births, g, code);
-    CR_CHECK_LAUNCH();
-    k_tags_codes<<<grid_for((g.ncells + 3) / 4, 256), 256, 0, s>>>(code, g, S.tags, cnt + 0);
-    CR_CHECK_LAUNCH();
-    ws.release(code);
-  } else if (!k12_old) {
-    // K1 + K2a fused (births and direction codes), then K2b (tags from codes)
-    uint8_t* code = ws.alloc<uint8_t>(g.ncells + 4);
-    k_births_codes<<<k1c_grid(g), K1C_THREADS, 0, s>>>(image, g, S.births, code, cnt + 4, nan_flag);
-    CR_CHECK_LAUNCH();
-    prof_mark(s, "births");
-    k_tags_codes<<<grid_for((g.ncells + 3) / 4, 256), 256, 0, s>>>(code, g, S.tags, cnt + 0);
-    CR_CHECK_LAUNCH();
-    ws.release(code);
-  } else {
-  k_births<<<k_births_grid(g), 256, 0, s>>>(image, g, S.births, cnt + 4, nan_flag);
-  CR_CHECK_LAUNCH();
-  prof_mark(s, "births");
-  if (std::getenv("CR_K2_ONEPASS")) {  // the one-kernel definition (cross-check in tests)
-    k_tags<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, g, S.tags, cnt + 0);
-    CR_CHECK_LAUNCH();
-  } else if (std::getenv("CR_K2_TWOPASS")) {  // codes in HBM, then tags (cross-check)
-    uint8_t* code = ws.alloc<uint8_t>(g.ncells);
-    k_codes_z<<<k2z_grid(g), 256, 0, s>>>(S.births, g, code);
-    CR_CHECK_LAUNCH();
-    k_tags2<<<k2_grid(g), 256, 0, s>>>(code, g, S.tags, cnt + 0);
-    CR_CHECK_LAUNCH();
-    ws.release(code);
-  } else {
-    k_apparent<<<k2f_grid(g), K2F_THREADS, 0, s>>>(S.births, g, S.tags, cnt + 0);
-    CR_CHECK_LAUNCH();
   }
-  }
-  if (k12_sep) prof_mark(s, "apparent");
 
   if (S.top_only) {  // the top dimension alone (--top_dim): no H0, no clearing
     CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -2423,7 +1081,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       st.apparent[d] = int64_t(hs.p[d]);
       st.cells[d] = int64_t(hs.p[4 + d]);
     }
-    if (g.D < 2 || top_dual(S, g.D - 1, ws, hs, st, 0xFFFFFFFFu)) {
+    if (g.D < 2 || top_dual(S, g.D - 1, ws, hs, st)) {
       prof_mark(s, "top_dual");
       return;
     }
@@ -2453,7 +1111,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   const int64_t nedges = st.cells[1];
 
   Cand* cand = ws.alloc<Cand>(nedges);
-  Cand* cand2 = ws.alloc<Cand>(nedges);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
   k_h0_edges<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
   CR_CHECK_LAUNCH();
@@ -2461,77 +1118,11 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // vertex records: at most one per finite vertex
   S.R.rec[0] = ws.alloc<uint64_t>(st.cells[0]);
   unsigned long long* nrec0 = cnt + 13;
-  const unsigned nb = unsigned(st.columns[0]);
-  if (nb <= smem_basins_max()) {
-    // few basins: shared-memory rounds in one CTA
-    const unsigned n = read_scalar(ncand, s, hs);
-    uint64_t* rootkey = ws.alloc<uint64_t>(nb + 1);
-    unsigned* nroot = reinterpret_cast<unsigned*>(cnt + 15);
-    k_collect_roots<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, rootkey, nroot);
-    CR_CHECK_LAUNCH();
-    sort_keys_u64(rootkey, nb, false, 64, ws);
-    uint32_t* rank_of = ws.alloc<uint32_t>(g.nvox);
-    k_rank_roots<<<grid_for(nb, B), B, 0, s>>>(rootkey, nb, g, rank_of);
-    CR_CHECK_LAUNCH();
-    uint64_t* keys = ws.alloc<uint64_t>(n + 1);
-    uint32_t* ab = ws.alloc<uint32_t>(n + 1);
-    if (n > 0) {
-      k_cand_pack<<<grid_for(n, B), B, 0, s>>>(cand, n, rank_of, keys, ab);
-      CR_CHECK_LAUNCH();
-      uint64_t* k2 = ws.alloc<uint64_t>(n);
-      uint32_t* v2 = ws.alloc<uint32_t>(n);
-      cub::DoubleBuffer<uint64_t> dk(keys, k2);
-      cub::DoubleBuffer<uint32_t> dv(ab, v2);
-      size_t tmp = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 64, s));
-      void* t = ws.alloc_bytes(tmp);
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(n), 0, 64, s));
-      keys = dk.Current();
-      ab = dv.Current();
-    }
-    uint32_t* act0 = ws.alloc<uint32_t>(n + 1);
-    uint32_t* act1 = ws.alloc<uint32_t>(n + 1);
-    uint32_t* best32 = ws.alloc<uint32_t>(nb + 1);
-    uint32_t* hook = ws.alloc<uint32_t>(nb + 1);
-    uint32_t* msf = ws.alloc<uint32_t>(nb + 1);
-    unsigned* nmsf = reinterpret_cast<unsigned*>(cnt + 17);
-    const size_t smem = size_t(nb > 0 ? nb : 1) * 4;
-    CR_CUDA(cudaFuncSetAttribute(k_h0_boruvka, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    CR_CUDA(cudaFuncSetAttribute(k_h0_kruskal, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    k_h0_boruvka<<<1, H0_THREADS, smem, s>>>(ab, n, nb, best32, act0, act1, hook, msf, nmsf,
-                                             cnt + 16);
-    CR_CHECK_LAUNCH();
-    const unsigned nm = read_scalar(nmsf, s, hs);
-    if (nm > 1) {  // Kruskal order = edge index order (candidates are sorted by key)
-      uint32_t* m2 = ws.alloc<uint32_t>(nm);
-      cub::DoubleBuffer<uint32_t> dm(msf, m2);
-      size_t tmp = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, dm, int(nm), 0, 32, s));
-      void* t = ws.alloc_bytes(tmp);
-      CR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, dm, int(nm), 0, 32, s));
-      msf = dm.Current();
-    }
-    k_h0_kruskal<<<1, H0_THREADS, smem, s>>>(keys, ab, msf, nm, rootkey, nb, S.tags, S.R.rec[0],
-                                             nrec0);
-    CR_CHECK_LAUNCH();
-    CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CR_CUDA(cudaStreamSynchronize(s));
-    S.R.n[0] = int64_t(hs.p[0]);
-    st.rounds[0] = int64_t(hs.p[3]);
-    prof_mark(s, "h0");
-    ws.release(cand);
-    ws.release(cand2);
-    ws.release(parent);
-    reduce_dims(S, g, dmax, ws, hs, st);
-    return;
-  }
   unsigned long long* best = ws.alloc<unsigned long long>(2 * g.nvox);
   CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * g.nvox * sizeof(unsigned long long), s));
   uint8_t* alive = ws.alloc<uint8_t>(nedges);
   unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 20);  // cnt[20], cnt[21]: zeroed at the start
-  mm_rounds<false>(cand, cand2, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
+  mm_rounds<false>(cand, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
                    DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ctl, ws);
   // flatten once more so that roots are exact, then essential classes
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
@@ -2546,7 +1137,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   st.rounds[0] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 7)[2]);
   prof_mark(s, "h0");
   ws.release(cand);
-  ws.release(cand2);
   ws.release(best);
   ws.release(alive);
   ws.release(parent);

@@ -816,23 +816,6 @@ struct LevelIn {
   int ntiles;              // tiles of the previous level
 };
 
-// exclusive prefix of a level's per-tile counts (one CTA; the tile counts are small)
-__global__ void __launch_bounds__(1024) k1_level_prefix(const uint32_t* cnt, int P,
-                                                        uint32_t* prefix) {
-  typedef cub::BlockScan<uint32_t, 1024> BS;
-  __shared__ typename BS::TempStorage s_scan;
-  uint32_t run = 0;
-  for (int c = 0; c < P; c += 1024) {
-    const int i = c + threadIdx.x;
-    const uint32_t v = i < P ? cnt[i] : 0u;
-    uint32_t pre, tot;
-    BS(s_scan).ExclusiveSum(v, pre, tot);
-    if (i < P) prefix[i] = run + pre;
-    run += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) prefix[P] = run;
-}
 
 // One tile t (of ntiles) of an item level.
 __device__ __forceinline__ void level_tile(const LevelIn& I, const Items& O, const Stage& G,
@@ -1233,14 +1216,6 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
     if (F.per_sm < 1) throw Error{CR_EINTERNAL, "k1_levels_coop cannot be resident"};
     F.ok = true;
   }
-  if (const char* e = std::getenv("CR_1D_ROUNDS")) {  // tuning knob (not part of the ABI)
-    const int v = std::atoi(e);
-    CR_CUDA(cudaMemcpyToSymbolAsync(g_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-  }
-  if (const char* e = std::getenv("CR_1D_L1ROUNDS")) {  // tuning knob (not part of the ABI)
-    const int v = std::atoi(e);
-    CR_CUDA(cudaMemcpyToSymbolAsync(g_l1_rounds, &v, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-  }
   G.out = out;
   G.out_cells = out_cells;
   G.cap = cap;
@@ -1279,7 +1254,7 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   LA.tl = nullptr;
   {
     unsigned long long* gt = nullptr;
-    if (std::getenv("CR_DEBUG_STATS")) {
+    if (opt(OPT_DEBUG)) {
       LA.tl = ws.alloc<unsigned long long>(32);
       CR_CUDA(cudaMemsetAsync(LA.tl, 0, 32 * sizeof(unsigned long long), s));
       gt = LA.tl + 16;
@@ -1299,7 +1274,7 @@ int64_t barcodes_1d_tiles(const float* x, int64_t n, cr_pair* out, uint32_t* out
   const int* hf = reinterpret_cast<const int*>(hs.p);
   const unsigned long long exported = hs.p[2], decided = hs.p[3], late_holes = hs.p[4];
   int64_t total = int64_t(hs.p[5]);
-  if (std::getenv("CR_DEBUG_STATS") && nt1 > 1) {
+  if (opt(OPT_DEBUG) && nt1 > 1) {
     uint32_t lt[NLEVELS + 2];
     CR_CUDA(cudaMemcpy(lt, LA.ltiles, sizeof(lt), cudaMemcpyDeviceToHost));
     fprintf(stderr, "[cr] 1d tiles per level:");

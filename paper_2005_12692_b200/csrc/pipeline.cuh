@@ -28,13 +28,9 @@ Geom make_geom(const int64_t* shape, int ndim);
 void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, HostScalars& hs,
                  GeneralState& S, cr_stats& st);
 
-// Residual column reduction of dimension d (reduce.cu).  Appends records to R.rec[d].
-// hom = false: cohomology (columns = d-cells, coboundaries, decreasing order; marks the pivots
-// cleared for dimension d+1).  hom = true: homology (columns = (d+1)-cells, boundaries, increasing
-// order), which needs the dimension-(d+1) births cleared first (mark_cleared_births(S, d+1)).
-void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st,
-                      bool hom = false);
-void mark_cleared_births(GeneralState& S, int d, Workspace& ws);
+// Residual coboundary column reduction of dimension d (reduce.cu): columns = residual d-cells in
+// decreasing key order; appends records to R.rec[d] and marks the pivots cleared for d+1.
+void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st);
 
 // Records (dims 0..maxdim) -> bars with death > birth plus essentials, ordered (dim, birth kidx).
 // Writes at most cap entries; returns the count needed.
@@ -53,8 +49,7 @@ int64_t barcodes_1d_tree(const float* image, int64_t n, cr_pair* out, uint32_t* 
                          int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st);
 inline int64_t barcodes_1d(const float* image, int64_t n, cr_pair* out, uint32_t* out_cells,
                            int64_t cap, Workspace& ws, HostScalars& hs, cr_stats& st) {
-  const char* e = std::getenv("CR_1D_TREE");
-  if (!(e && e[0] == '1')) {
+  if (opt(OPT_1D_TREE) == 0) {
     int64_t r = barcodes_1d_tiles(image, n, out, out_cells, cap, ws, hs, st);
     if (r >= 0) return r;
     st.path = 4;  // tile levels did not converge: tree path

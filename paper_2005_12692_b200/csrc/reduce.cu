@@ -18,24 +18,20 @@
 // (apparent coboundaries, short stored columns) merge into F at O(|F|) cost; F is merged into M
 // only when it fills up, so a long column is not rewritten on every addition.
 //
-// Parallel schedule (one persistent cooperative kernel).  Warp w owns columns j = w (mod W), W =
-// resident warps; the window is the W columns lo..lo+W-1 (lo = first unfinished), one per warp.
-// Each round every warp advances its column by at most max_steps additions and publishes its
-// current pivot cand(j) at window position j - lo (a lower bound of its final pivot: adding a
-// column with the same pivot only moves the pivot later).  Column j with an unowned pivot commits
-// iff cand(j) < min{cand(i) : lo <= i < j}: no earlier column can end on that pivot, so j's pivot
-// is final, and any column committed while j is unfinished has a pivot j can never reach -- the
-// sequential reduction's pairs are reproduced exactly.
-#include <cooperative_groups.h>
-
+// Parallel schedule (one persistent kernel, no grid-wide rounds).  Warps take columns in
+// processing order from a counter (per segment, segments interleaved).  A column publishes its
+// current pivot cand(j) -- a lower bound of its final pivot: adding a column with the same pivot
+// only moves the pivot later -- after every pivot change.  Column j with an unowned pivot p
+// commits once every earlier column i of its segment has cand(i) > p or is finished (then no
+// earlier column can end on p, and j's pivot is final); it waits on the first blocking column
+// only, and a column committed while j is unfinished has a pivot j can never reach -- the
+// sequential reduction's pairs are reproduced exactly (applied per column).
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <vector>
 
 #include "pipeline.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace cr {
 namespace {
@@ -61,9 +57,7 @@ struct FastDiv {
 struct RP {
   Geom g;
   FastDiv fx, fxy;  // by KX and by KX*KY: Khalimsky coordinates of a kidx
-  int d;
-  int hom;             // 1: homology mode (columns = (d+1)-cells by boundary, keys complemented)
-  const uint64_t* cols;
+  const uint64_t* cols;  // column keys in processing order (grouped by segment)
   uint32_t ncols;
   const uint32_t* births;
   const uint8_t* tags;
@@ -74,31 +68,20 @@ struct RP {
   unsigned long long pool_cap;
   uint64_t* work;      // per warp: 2 * mcap main-array entries
   uint32_t mcap;
-  uint64_t* cand;      // per window position
-  uint64_t* chunkmin;  // per block (positions [WPB*b, WPB*b+WPB))
-  uint32_t* chunkflag; // per block: a segment starts inside the chunk
-  uint32_t* segpos;    // per window position: its warp group (positions of a group are contiguous)
-  uint32_t seg_cells;  // cells per segment (batched images), 0: one segment
+  // lv[0][j] = cand(j): 0 before column j starts, then a lower bound of its pivot key, NONE64
+  // once it is finished.  lv[L][e] (L = 1..3) = a lower bound of min lv[0] over the 32^L columns
+  // [e * 32^L, (e+1) * 32^L): every entry only grows, so a stale bound is still a bound.
+  uint64_t* lv[4];
   const uint32_t* seg_off;  // nseg + 1 column offsets (columns are grouped by segment)
   uint32_t nseg;
-  uint32_t G;          // warps per group; group g reduces segments g, g + ngroups, ...
-  uint32_t ngroups;
-  unsigned* lo_buf;    // [2 * ngroups]: next window start of each group (double-buffered)
-  unsigned* done_buf;  // [2]: groups with no segment left (double-buffered)
+  unsigned* seg_next;  // per segment: columns handed out
+  unsigned long long* fetch;  // fetch counter (spreads warps over the segments)
   uint64_t* rec;
   unsigned long long* nrec;
   int* err;
-  int ahead;           // read-ahead of the next column (see phase A)
-  int max_steps;       // additions per warp and round, at most ...
-  long long budget;    // ... and until this many cycles of the round have passed (0: no limit)
-  unsigned long long* stats;  // [0] rounds [1] additions [2] sum of lengths [3] max length
-                              // debug: [4] pool additions [5] pool lengths [7]/[8] cycles in
-                              // pool/apparent additions [9] cycles in pivot + owner lookups
-  int debug;
-  unsigned long long* rdbg;  // debug: per round [max phase-A cycles, max steps, active warps, t]
-  uint32_t rdbg_cap;
-  unsigned long long* colstat;  // debug: per column (additions, entries touched, cycles in
-                                // lookups, apparent adds, pool adds, flushes)
+  unsigned long long* stats;  // [0] waits [1] additions [2] sum of lengths [3] max length
+                              // [4] cycles waited [5] commits
+  unsigned jitter;     // validation: pseudo-random delays (ns) that perturb the schedule
 };
 constexpr int OI_LEN_BITS = 24;  // owninfo: stored column length field
 
@@ -110,19 +93,12 @@ __device__ __forceinline__ uint64_t ld64(const uint64_t* p) {
   return G ? ldcg64(p) : *p;
 }
 
-// Keys of the working columns.  Cohomology: (ord << 32 | kidx), pivot = min.  Homology mode: the
-// complement ~(ord << 32 | kidx), so that the min-pivot machinery below takes the MAX (latest)
-// face as the pivot and processes columns in increasing filtration order (decreasing ~key).
-__device__ __forceinline__ uint64_t rkey(const RP& P, uint32_t b, uint32_t k) {
-  const uint64_t x = make_key(b, k);
-  return P.hom ? ~x : x;
-}
-__device__ __forceinline__ uint32_t rkid(const RP& P, uint64_t key) {
-  return P.hom ? ~uint32_t(key) : uint32_t(key);
-}
+// Keys of the working columns: (ord << 32 | kidx), pivot = the minimum.
+__device__ __forceinline__ uint64_t rkey(const RP&, uint32_t b, uint32_t k) { return make_key(b, k); }
+__device__ __forceinline__ uint32_t rkid(const RP&, uint64_t key) { return uint32_t(key); }
 
-// The column of cell s, sorted ascending (by rkey), written to dst (<= 6 entries): its finite
-// cofacets (cohomology), or its facets (homology mode).  Warp-collective.
+// The column of cell s, sorted ascending, written to dst (<= 6 entries): its finite cofacets (the
+// implicit coboundary of PAPER.md:135-136).  Warp-collective.
 __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
   const Geom& g = P.g;
   const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
@@ -132,7 +108,7 @@ __device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane)
   uint64_t key = NONE64;
   if (lane < 6) {
     const int a = lane >> 1, sg = lane & 1;
-    if ((P.hom ? (c[a] & 1) : !(c[a] & 1)) && (sg ? c[a] + 1 < ext[a] : c[a] > 0)) {
+    if (!(c[a] & 1) && (sg ? c[a] + 1 < ext[a] : c[a] > 0)) {
       const int64_t stv = g.stride(a);
       const uint32_t t = uint32_t(int64_t(s) + (sg ? stv : -stv));
       const uint32_t tb = __ldg(P.births + t);
@@ -275,23 +251,6 @@ __device__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t*
   return out;
 }
 
-struct MinOp {
-  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
-    return a < b ? a : b;
-  }
-};
-// segmented minimum: (value, starts-a-segment) pairs
-struct SegMin {
-  uint64_t v;
-  uint32_t f;
-};
-struct SegOp {
-  __device__ __forceinline__ SegMin operator()(const SegMin& a, const SegMin& b) const {
-    return SegMin{b.f ? b.v : (a.v < b.v ? a.v : b.v), a.f | b.f};
-  }
-};
-typedef cub::BlockScan<SegMin, THREADS> SScan;
-
 // The working column of a warp.
 struct Col {
   uint64_t* M[2];  // global main arrays
@@ -406,16 +365,12 @@ struct Spec {
 // grid after moving by `dchk`, and (members 1-4) axis b is even in t.
 struct SpecLane {
   int a, chk, dchk, sa;
-  bool need_b_even;  // (homology mode: axis b must be odd in the pivot)
+  bool need_b_even;
   uint32_t off;      // cell - t (two's complement)
   bool active;
-  bool hom;
 };
-// Homology mode mirrors it: an UP pivot e (a d-cell) is the lower cell of an apparent pair
-// (e, s') with s' = e + e_dir a cofacet; the column adds del(s') = {e} + the other facets of s':
-// member 0 is e + 2 e_dir, members 1-4 are s' -/+ e_b for the other axes b odd in e.
-__device__ __forceinline__ SpecLane spec_lane(const Geom& g, int lane, bool hom) {
-  SpecLane L{0, 0, 0, 0, false, 0u, false, hom};
+__device__ __forceinline__ SpecLane spec_lane(const Geom& g, int lane) {
+  SpecLane L{0, 0, 0, 0, false, 0u, false};
   if (lane >= 30) return L;
   const int f = lane / 5, m = lane % 5;
   L.a = f >> 1;
@@ -445,12 +400,9 @@ __device__ __forceinline__ Spec spec_issue(const RP& P, const SpecLane& L, uint3
   const uint32_t ec = L.chk == 0 ? KX : (L.chk == 1 ? KY : uint32_t(P.g.KZ));
   const uint32_t moved = cc + uint32_t(L.dchk);  // wraps below 0 to a huge value
   Spec r{0u, ABSENT_ORD};
-  const bool up_axis = L.hom ? !(ca & 1) : (ca & 1);  // t on the pivot side of axis a
-  const bool b_bad = L.need_b_even && (L.hom ? !(cc & 1) : (cc & 1));
-  // homology: t is even along a and may sit on the border; the partner t + sa e_a must exist
-  const uint32_t ea = L.a == 0 ? KX : (L.a == 1 ? KY : uint32_t(P.g.KZ));
-  const bool a_ok = !L.hom || ca + uint32_t(L.sa) < ea;
-  if (L.active && up_axis && a_ok && moved < ec && !b_bad) {
+  const bool up_axis = ca & 1;  // t spans axis a: s' = t + sa e_a is a facet of t
+  const bool b_bad = L.need_b_even && (cc & 1);
+  if (L.active && up_axis && moved < ec && !b_bad) {
     r.cell = t + L.off;
     r.birth = __ldg(P.births + r.cell);
   }
@@ -742,288 +694,318 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, 
   return true;
 }
 
+// ---------------------------------------------------------------- the asynchronous commit rule
+
+__device__ __forceinline__ uint64_t ld_rlx(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rlx(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_rlx_i32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// The first column i in [x, j) whose published candidate is <= p (it may still end on p, or is
+// not started), or j if there is none.  Warp-collective.  Chunks of 32^L columns whose bound
+// lv[L] exceeds p are skipped whole; a chunk whose bound does not is re-derived from its 32
+// children (and its bound raised with atomicMax: the children's current values are lower bounds
+// of the chunk's later minimum), and entered only if a child is still <= p.  A column found
+// > p or finished stays so (candidates only grow), so the caller resumes after a blocker.
+__device__ uint32_t find_blocker(const RP& P, uint32_t x, uint32_t j, uint64_t p, int lane) {
+  uint32_t desc_end[4] = {0u, 0u, 0u, 0u};  // end of the last level-L chunk entered
+  while (x < j) {
+    int L = 0;
+#pragma unroll
+    for (int l = 3; l >= 1; --l) {
+      const uint32_t sz = 1u << (5 * l);
+      if (L == 0 && (x & (sz - 1)) == 0 && uint64_t(x) + sz <= j && x >= desc_end[l]) L = l;
+    }
+    if (L == 0) {  // single columns
+      const uint32_t n = j - x < 32u ? j - x : 32u;
+      const uint64_t v = uint32_t(lane) < n ? ld_rlx(P.lv[0] + x + lane) : NONE64;
+      const unsigned bad = __ballot_sync(0xFFFFFFFFu, v <= p);
+      if (bad) return x + __ffs(bad) - 1;
+      x += n;
+      continue;
+    }
+    const int sh = 5 * L;
+    uint32_t e = x >> sh;
+    const uint32_t m = ((j - x) >> sh) < 32u ? ((j - x) >> sh) : 32u;  // whole chunks in range
+    const uint64_t v = uint32_t(lane) < m ? ld_rlx(P.lv[L] + e + lane) : NONE64;
+    const unsigned bad = __ballot_sync(0xFFFFFFFFu, v <= p);
+    if (!bad) {
+      x += m << sh;
+      continue;
+    }
+    const uint32_t f = __ffs(bad) - 1;
+    x += f << sh;
+    e += f;
+    const uint64_t cv = ld_rlx(P.lv[L - 1] + (uint64_t(e) << 5) + lane);
+    const unsigned cbad = __ballot_sync(0xFFFFFFFFu, cv <= p);
+    if (!cbad) {
+      const uint64_t mn = warp_min(cv);
+      if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(P.lv[L] + e), mn);
+      x += 1u << sh;
+      continue;
+    }
+    desc_end[L] = x + (1u << sh);
+    x += (__ffs(cbad) - 1) << (sh - 5);
+    if (L == 1) return x;
+  }
+  return j;
+}
+
+// Column j is finished: publish it (after its owner entry / record, fenced) and raise the bounds
+// of its chunks -- the level-1 bound to its 32 columns' current minimum, the levels above while
+// their chunks are entirely finished.  Warp-collective.
+__device__ void finish_column(const RP& P, uint32_t j, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    st_rlx(P.lv[0] + j, NONE64);
+    __threadfence();
+  }
+  __syncwarp();
+  uint32_t e = j;
+  for (int L = 1; L <= 3; ++L) {
+    e >>= 5;
+    const uint64_t cv = ld_rlx(P.lv[L - 1] + (uint64_t(e) << 5) + lane);
+    const uint64_t mn = warp_min(cv);
+    if (lane == 0 && mn > ld_rlx(P.lv[L] + e)) {
+      atomicMax(reinterpret_cast<unsigned long long*>(P.lv[L] + e), mn);
+      __threadfence();
+    }
+    __syncwarp();
+    if (mn != NONE64) break;
+  }
+}
+
+// Next column for this warp: columns are handed out in processing order within each segment;
+// consecutive fetches go to consecutive segments, so independent images progress together.
+// Returns (segment, column) or column NONE32 when every segment is exhausted.
+__device__ __forceinline__ uint32_t fetch_column(const RP& P, uint32_t& seg, int lane) {
+  uint32_t j = NONE32, s = 0;
+  if (lane == 0) {
+    const unsigned long long c = atomicAdd(P.fetch, 1ull);
+    for (uint32_t t = 0; t < P.nseg; ++t) {
+      s = uint32_t((c + t) % P.nseg);
+      const uint32_t lo = __ldg(P.seg_off + s), hi = __ldg(P.seg_off + s + 1);
+      if (lo + *reinterpret_cast<volatile unsigned*>(P.seg_next + s) >= hi) continue;
+      const uint32_t r = atomicAdd(P.seg_next + s, 1u);
+      if (lo + r < hi) {
+        j = lo + r;
+        break;
+      }
+    }
+  }
+  seg = __shfl_sync(0xFFFFFFFFu, s, 0);
+  return __shfl_sync(0xFFFFFFFFu, j, 0);
+}
+
+__device__ __forceinline__ void jitter_sleep(const RP& P, uint32_t a, uint32_t b) {
+  if (!P.jitter) return;
+  uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA6Bu;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 13;
+  if ((h & 3) == 0) __nanosleep(h % P.jitter);
+}
+
 #ifndef K5_MINB
 #define K5_MINB 4
 #endif
 __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
-  cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s_F[WPB][2][FCAP];
   __shared__ uint64_t s_small[WPB][8];
-  // phase A stages short addends, phase C scans chunk minima: grid syncs separate them
-  __shared__ union {
-    uint64_t stage[WPB][STAGE];
-    uint64_t pref[4 * THREADS];
-  } s_u;
-  static_assert(sizeof(uint64_t) * WPB * STAGE <= sizeof(uint64_t) * 4 * THREADS, "alias");
-  auto& s_stage = s_u.stage;
-  auto& s_pref = s_u.pref;
-  __shared__ typename SScan::TempStorage s_scan;
+  __shared__ uint64_t s_stage[WPB][STAGE];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const uint32_t W = (gridDim.x * blockDim.x) >> 5;
   const uint32_t w = blockIdx.x * WPB + wib;
-  const uint32_t nblocks = gridDim.x;
 
   Col c;
   uint64_t* const slot = P.work + uint64_t(w) * 2 * P.mcap;
-  const SpecLane sl = spec_lane(P.g, lane, P.hom != 0);
+  const SpecLane sl = spec_lane(P.g, lane);
   c.F[0] = s_F[wib][0];
   c.F[1] = s_F[wib][1];
-  // Warp groups: group grp (G warps, window positions [grp*G, grp*G + G)) reduces the segments
-  // grp, grp + ngroups, ... one after the other; segments (images of a batch) are independent
-  // complexes, so each has its own window and the groups progress concurrently.  One image:
-  // one group of all W warps.  Warps beyond ngroups * G stay idle.
-  const uint32_t G = P.G, grp = w / G, k = w - grp * G;
-  uint32_t seg = grp < P.ngroups ? grp : P.nseg;
-  uint32_t lo = seg < P.nseg ? __ldg(P.seg_off + seg) : P.ncols;
-  uint32_t end = seg < P.nseg ? __ldg(P.seg_off + seg + 1) : P.ncols;
-  uint32_t j = lo + k;
-  bool started = false, fin = false;
-  if (lane == 0) {
-    P.segpos[w] = grp < P.ngroups ? grp : 0xFFFFFFFFu;  // idle positions: a segment of their own
-    P.cand[w] = NONE64;
-  }
+  unsigned long long adds = 0, addlen = 0, waits = 0, wcyc = 0, commits = 0;
+  uint64_t maxlen = 0;
 
-  for (uint32_t round = 0;; ++round) {
-    // ---------------- phase A: advance my column
-    // Read-ahead: a warp whose column is finished takes its next column j + G at once, even if
-    // the window has not reached it yet: it reduces it with the owners committed so far (always
-    // valid) and only publishes / commits once the column is inside the window.
-    if (fin && (j < lo || P.ahead)) {
-      j += G;
-      started = false;
-      fin = false;
-    }
-    uint64_t cval = NONE64;
-    bool ready = false;
-    const long long pa0 = P.rdbg ? clock64() : 0;
-    int dbg_steps = -1;
-    if (j < end && !fin) {
-      if (!started) {
-        started = true;
-        c.mb = c.fb = 0;
-        c.h = c.f0 = c.nm = 0;
-        c.M[0] = slot;  // a column grown into the pool last time starts over in the slot
-        c.M[1] = slot + P.mcap;
-        c.cap = P.mcap;
-        c.spare = nullptr;
-        c.rv = NONE64;
-        c.nr = c.r0 = 0;
-        c.mstale = true;
-        c.nf = coboundary(P, rkid(P, P.cols[j]), c.F[0], lane);
-      }
-      int steps = 0;
-      const long long round_t0 = clock64();
-      unsigned long long adds = 0, addlen = 0, cl = 0, ca = 0, cp = 0;
-      c.fcyc = 0;
-      bool ok = true;
-      while (true) {
-        const long long tl0 = P.debug ? clock64() : 0;
-        const uint64_t piv = take_pivot(c, lane);
-        if (piv == NONE64) break;
-        const uint32_t pk = rkid(P, piv);
-        // independent loads: the speculated partner coboundary, the tag, the owner record
-        const Spec sp = spec_issue(P, sl, pk);
-        const uint8_t t = __ldg(P.tags + pk);
-        const uint64_t oi = ldcg64(P.owninfo + pk);
-        const uint64_t* add;
-        uint32_t alen;
-        bool glob;
-        if (tag_kind(t) == (P.hom ? KIND_UP : KIND_DOWN)) {
-          // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
-          // (homology: the lower cell of (pivot, s'): add del(s'))
-          alen = spec_finish(P, sp, tag_dir(t), piv, s_small[wib], lane);
-          add = s_small[wib];
-          glob = false;
-        } else {
-          if (oi == NONE64) {
-            // ready to commit: fold R into F now (phase C's commit reads M and F, and its shared
-            // scratch is busy there)
-            ok = spill_r(c, P, s_stage[wib], lane);
-            ready = ok;
-            cval = piv;
-            break;
-          }
-          add = P.pool + (oi >> OI_LEN_BITS);
-          alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1));
-          glob = true;
-        }
-        if (steps >= P.max_steps || (P.budget && clock64() - round_t0 > P.budget)) {
-          cval = piv;
-          break;
-        }
-        addlen += c.len() + alen;
-        const long long t0 = P.debug ? clock64() : 0;
-        if (P.debug && lane == 0) atomicAdd(P.stats + 9, (unsigned long long)(t0 - tl0));
-        cl += t0 - tl0;
-        ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
-                  : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
-        if (P.debug && lane == 0) {
-          const unsigned long long dt = (unsigned long long)(clock64() - t0);
-          if (glob) {
-            atomicAdd(P.stats + 4, 1ull);
-            atomicAdd(P.stats + 5, (unsigned long long)alen);
-            atomicAdd(P.stats + 7, dt);
-            cp += dt;
-          } else {
-            atomicAdd(P.stats + 8, dt);
-            ca += dt;
-          }
-        }
-        if (!ok) break;  // pool exhausted (err 2 set): the launch is retried
-        ++steps;
-        ++adds;
-      }
-      dbg_steps = steps;
-      if (lane == 0 && adds) {
-        atomicAdd(P.stats + 1, adds);
-        atomicAdd(P.stats + 2, addlen);
-        atomicMax(P.stats + 3, (unsigned long long)c.len());
-        if (P.colstat) {
-          P.colstat[6 * j] += adds;
-          P.colstat[6 * j + 1] += addlen;
-          P.colstat[6 * j + 2] += cl;
-          P.colstat[6 * j + 3] += ca;
-          P.colstat[6 * j + 4] += cp;
-          P.colstat[6 * j + 5] += (unsigned long long)c.fcyc;
-        }
-      }
-      if (ok && !ready && cval == NONE64) {  // zero column: essential (exact given clearing)
-        fin = true;
+  for (;;) {
+    if (ld_rlx_i32(P.err)) break;
+    uint32_t seg;
+    const uint32_t j = fetch_column(P, seg, lane);
+    if (j == NONE32) break;
+    const uint32_t seg_lo = __ldg(P.seg_off + seg);
+    const uint32_t cell = rkid(P, P.cols[j]);
+    c.mb = c.fb = 0;
+    c.h = c.f0 = c.nm = 0;
+    c.M[0] = slot;  // a column grown into the pool last time starts over in the slot
+    c.M[1] = slot + P.mcap;
+    c.cap = P.mcap;
+    c.spare = nullptr;
+    c.rv = NONE64;
+    c.nr = c.r0 = 0;
+    c.mstale = true;
+    c.nf = coboundary(P, cell, c.F[0], lane);
+    uint64_t pub = 0;      // last published candidate
+    uint64_t xp = NONE64;  // the pivot the scan cursor x is valid for
+    uint32_t x = seg_lo;
+    bool ok = true;
+    while (true) {
+      const uint64_t piv = take_pivot(c, lane);
+      if (piv == NONE64) {  // zero column: essential (exact given the clearing)
         if (lane == 0) {
-          if (P.hom) {
-            atomicOr(P.err, 8);  // homology: every column left after the clearing is nonzero
-          } else {
-            const unsigned long long r = atomicAdd(P.nrec, 1ull);
-            P.rec[r] = (uint64_t(rkid(P, P.cols[j])) << 32) | NONE32;
+          const unsigned long long r = atomicAdd(P.nrec, 1ull);
+          P.rec[r] = (uint64_t(cell) << 32) | NONE32;
+        }
+        break;
+      }
+      if (piv != pub) {
+        if (lane == 0) st_rlx(P.lv[0] + j, piv);
+        pub = piv;
+      }
+      const uint32_t pk = rkid(P, piv);
+      // independent loads: the speculated partner coboundary, the tag, the owner record
+      const Spec sp = spec_issue(P, sl, pk);
+      const uint8_t t = __ldg(P.tags + pk);
+      const uint64_t oi = ldcg64(P.owninfo + pk);
+      const uint64_t* add;
+      uint32_t alen;
+      bool glob;
+      if (tag_kind(t) == KIND_DOWN) {
+        // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
+        alen = spec_finish(P, sp, tag_dir(t), piv, s_small[wib], lane);
+        add = s_small[wib];
+        glob = false;
+      } else if (oi != NONE64) {
+        add = P.pool + (oi >> OI_LEN_BITS);
+        alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1));
+        glob = true;
+      } else {
+        // unowned pivot: wait until no earlier column of the segment can end on it
+        jitter_sleep(P, j, uint32_t(adds));
+        if (xp != piv) {
+          x = seg_lo;
+          xp = piv;
+        }
+        bool owned = false;
+        while (!owned) {
+          const uint32_t b = find_blocker(P, x, j, piv, lane);
+          if (b == j) break;
+          x = b;
+          ++waits;
+          const long long t0 = clock64();
+          unsigned ns = 32;
+          for (int it = 1;; ++it) {
+            uint64_t v = 0;
+            int e = 0;
+            if (lane == 0) {
+              v = ld_rlx(P.lv[0] + b);
+              e = ld_rlx_i32(P.err);
+            }
+            v = __shfl_sync(0xFFFFFFFFu, v, 0);
+            if (__shfl_sync(0xFFFFFFFFu, e, 0)) {
+              ok = false;
+              break;
+            }
+            if (v > piv) break;
+            if ((it & 3) == 0) {  // an earlier column may commit this very pivot meanwhile
+              uint64_t o = 0;
+              if (lane == 0) o = ld_rlx(P.owninfo + pk);
+              if (__shfl_sync(0xFFFFFFFFu, o, 0) != NONE64) {
+                owned = true;
+                break;
+              }
+            }
+            __nanosleep(ns);
+            if (ns < 512) ns <<= 1;
           }
+          wcyc += clock64() - t0;
+          if (!ok) break;
+          x = b + 1;
         }
-      }
-    }
-    if (P.rdbg && lane == 0 && round < P.rdbg_cap && dbg_steps >= 0) {
-      unsigned long long* R = P.rdbg + 4ull * round;
-      atomicMax(R + 0, (unsigned long long)(clock64() - pa0));
-      atomicMax(R + 1, (unsigned long long)dbg_steps);
-      atomicAdd(R + 2, 1ull);
-    }
-    if (P.rdbg && blockIdx.x == 0 && threadIdx.x == 0 && round < P.rdbg_cap) {
-      unsigned long long tnow;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-      P.rdbg[4ull * round + 3] = tnow;
-    }
-    // publish at my window position (every position of a group's window is owned by exactly one
-    // of its warps); a column is blocked only by unfinished earlier columns of its own window
-    const uint32_t q = j - lo;
-    const uint32_t qg = grp * G + q;
-    if (lane == 0 && grp < P.ngroups && q < G) P.cand[qg] = (j < end && !fin) ? cval : NONE64;
-    // a read-ahead warp still owns its finished previous column's position
-    if (lane == 0 && grp < P.ngroups && q >= G && q - G < G) P.cand[qg - G] = NONE64;
-    grid.sync();
-
-    // ---------------- phase B: segmented minima of the window's chunks of WPB positions
-    if (threadIdx.x == 0) {
-      uint64_t m = NONE64;
-      uint32_t f = 0;
-      for (int k = 0; k < WPB; ++k) {
-        const uint32_t p = blockIdx.x * WPB + k;
-        if (p == 0 || __ldcg(P.segpos + p) != __ldcg(P.segpos + p - 1)) {
-          m = NONE64;  // a segment starts here
-          f = 1;
+        if (!ok) break;
+        if (!owned) {  // every earlier column is finished or beyond piv: final check, commit
+          uint64_t o = 0;
+          if (lane == 0) {
+            __threadfence();
+            o = ld_rlx(P.owninfo + pk);
+          }
+          owned = __shfl_sync(0xFFFFFFFFu, o, 0) != NONE64;
         }
-        m = min(m, ldcg64(P.cand + p));
-      }
-      P.chunkmin[blockIdx.x] = m;
-      P.chunkflag[blockIdx.x] = f;
-    }
-    grid.sync();
-
-    // ---------------- phase C: exclusive segmented prefix-min at my position, commit
-    {  // every block scans the chunk aggregates (nblocks <= 4 * THREADS) into s_pref
-      SegMin v[4];
-      SegMin t{NONE64, 0};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t b = threadIdx.x * 4 + k;
-        v[k] = b < nblocks ? SegMin{ldcg64(P.chunkmin + b), __ldcg(P.chunkflag + b)}
-                           : SegMin{NONE64, 0};
-        t = SegOp()(t, v[k]);
-      }
-      SegMin run;
-      SScan(s_scan).ExclusiveScan(t, run, SegMin{NONE64, 0}, SegOp());
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t b = threadIdx.x * 4 + k;
-        if (b < nblocks) s_pref[b] = run.v;  // min over my segment's positions before chunk b
-        run = SegOp()(run, v[k]);
-      }
-    }
-    __syncthreads();
-    if (j < end && !fin && ready && q < G) {
-      const uint32_t chunk = qg / WPB;
-      uint64_t prefix = s_pref[chunk];
-      for (uint32_t kk = chunk * WPB; kk <= qg; ++kk) {
-        if (kk == 0 || __ldcg(P.segpos + kk) != __ldcg(P.segpos + kk - 1)) prefix = NONE64;
-        if (kk < qg) prefix = min(prefix, ldcg64(P.cand + kk));
-      }
-      if (cval < prefix) {
+        if (owned) continue;  // the owner's column is added on the next pass
+        ok = spill_r(c, P, s_stage[wib], lane);  // the commit reads M and F
+        if (!ok) break;
         const uint32_t L = c.len();
         unsigned long long off = 0;
         if (lane == 0) off = atomicAdd(P.pool_top, (unsigned long long)L);
         off = __shfl_sync(0xFFFFFFFFu, off, 0);
         if (off + L > P.pool_cap) {
           if (lane == 0) atomicOr(P.err, 2);
-        } else {
-          // reduced column = M[h:] xor F[f0:], written straight into the pool
-          const uint32_t n = merge_chunked<false>(c.M[c.mb] + c.h, c.nm - c.h, c.F[c.fb] + c.f0,
-                                                  c.nf - c.f0, P.pool + off, c.F[c.fb ^ 1],
-                                                  nullptr, lane);
-          if (lane == 0) {
-            if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
-            __threadfence();
-            P.owninfo[rkid(P, cval)] = (uint64_t(off) << OI_LEN_BITS) | n;
-            const unsigned long long r = atomicAdd(P.nrec, 1ull);
-            // (birth cell, death cell): cohomology (column, pivot), homology (pivot, column)
-            const uint64_t cc = rkid(P, P.cols[j]), pc = rkid(P, cval);
-            P.rec[r] = P.hom ? ((pc << 32) | cc) : ((cc << 32) | pc);
-          }
-          fin = true;
+          ok = false;
+          break;
         }
+        // reduced column = M[h:] xor F[f0:], written straight into the pool
+        const uint32_t n = merge_chunked<false>(c.M[c.mb] + c.h, c.nm - c.h, c.F[c.fb] + c.f0,
+                                                c.nf - c.f0, P.pool + off, c.F[c.fb ^ 1],
+                                                nullptr, lane);
+        if (lane == 0) {
+          if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
+          __threadfence();
+          st_rlx(P.owninfo + pk, (uint64_t(off) << OI_LEN_BITS) | n);
+          const unsigned long long r = atomicAdd(P.nrec, 1ull);
+          P.rec[r] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
+        }
+        ++commits;
+        break;
       }
+      addlen += c.len() + alen;
+      ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
+                : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
+      if (!ok) break;  // pool exhausted (err 2 set): the launch is retried
+      ++adds;
+      const uint64_t l = c.len();
+      maxlen = l > maxlen ? l : maxlen;
     }
-    // next lo of my group = min(first unfinished window column, lo + G, end of the segment)
-    const unsigned nxt = ((round + 1) & 1) * P.ngroups, cur = (round & 1) * P.ngroups;
-    if (grp < P.ngroups) {
-      if (lane == 0 && j < end && !fin) atomicMin(P.lo_buf + nxt + grp, j);
-      if (k == 0 && lane == 0) {
-        const uint64_t nl = uint64_t(lo) + G;
-        atomicMin(P.lo_buf + nxt + grp, unsigned(nl < end ? nl : end));
-        P.lo_buf[cur + grp] = NONE32;
-        if (seg >= P.nseg) atomicAdd(P.done_buf + ((round + 1) & 1), 1u);
-      }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      P.done_buf[round & 1] = 0;
-      atomicAdd(P.stats, 1ull);
-    }
-    grid.sync();
-    if (__ldcg(P.done_buf + ((round + 1) & 1)) >= P.ngroups) break;
-    if (__ldcg(P.err)) break;
-    if (grp < P.ngroups && seg < P.nseg) {
-      lo = __ldcg(P.lo_buf + nxt + grp);
-      if (lo >= end) {  // segment done: the group moves on to its next one
-        seg += P.ngroups;
-        lo = seg < P.nseg ? __ldg(P.seg_off + seg) : P.ncols;
-        end = seg < P.nseg ? __ldg(P.seg_off + seg + 1) : P.ncols;
-        j = lo + k;
-        started = false;
-        fin = false;
-      }
-    }
+    if (!ok) break;
+    finish_column(P, j, lane);
+  }
+  if (lane == 0) {
+    atomicAdd(P.stats + 0, waits);
+    atomicAdd(P.stats + 1, adds);
+    atomicAdd(P.stats + 2, addlen);
+    atomicMax(P.stats + 3, (unsigned long long)maxlen);
+    atomicAdd(P.stats + 4, wcyc);
+    atomicAdd(P.stats + 5, commits);
   }
 }
 
+// lv[0][i] = 0 for real columns (not started), NONE64 for the padding; chunk bounds likewise.
+__global__ void k_levels_init(uint64_t* lv0, uint64_t* lv1, uint64_t* lv2, uint64_t* lv3,
+                              uint32_t ncols, uint32_t npad) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  lv0[i] = i < ncols ? 0ull : NONE64;
+  if (i < (npad >> 5)) lv1[i] = (uint64_t(i) << 5) < ncols ? 0ull : NONE64;
+  if (i < (npad >> 10)) lv2[i] = (uint64_t(i) << 10) < ncols ? 0ull : NONE64;
+  if (i < (npad >> 15)) lv3[i] = (uint64_t(i) << 15) < ncols ? 0ull : NONE64;
+}
+
 __global__ void k_collect_columns(const uint32_t* __restrict__ births,
-                                  const uint8_t* __restrict__ tags, Geom g, int d, int hom,
+                                  const uint8_t* __restrict__ tags, Geom g, int d,
                                   uint64_t* __restrict__ cols, unsigned* __restrict__ ncols) {
   int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   bool emit = false;
@@ -1036,7 +1018,7 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
     uint32_t b = births[k];
     if (dim == d && b != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
       emit = true;
-      key = hom ? ~make_key(b, k) : make_key(b, k);
+      key = make_key(b, k);
     }
   }
   unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
@@ -1049,33 +1031,9 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
 }
 
 __global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32_t seg_cells,
-                           int hom, uint32_t* __restrict__ segk) {
+                           uint32_t* __restrict__ segk) {
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) segk[i] = (hom ? ~key_kidx(cols[i]) : key_kidx(cols[i])) / seg_cells;
-}
-
-// Homology mode, after the reduction: a residual d-cell (not apparent, not cleared as a death
-// cell of dimension d-1) that is no column's pivot is an essential class (birth, +inf).
-__global__ void k_hom_essential(const uint32_t* __restrict__ births,
-                                const uint8_t* __restrict__ tags, Geom g, int d,
-                                const uint64_t* __restrict__ owninfo, uint64_t* rec,
-                                unsigned long long* nrec) {
-  const int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (kk >= g.ncells) return;
-  const uint32_t k = uint32_t(kk);
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  const uint32_t X = k % KX, r = k / KX, Y = r % KY, Z = r / KY;
-  if (int((X & 1) + (Y & 1) + (Z & 1)) != d) return;
-  if (births[k] == ABSENT_ORD || tag_kind(tags[k]) != KIND_RESIDUAL) return;
-  if (owninfo && ldcg64(owninfo + k) != NONE64) return;
-  rec[atomicAdd(nrec, 1ull)] = (uint64_t(k) << 32) | NONE32;
-}
-
-// Clearing for the homology mode: the birth cells of dimension-(d+1) records (cells that create a
-// class, paired with a (d+2)-cell or essential) have zero reduced boundary columns.
-__global__ void k_mark_cleared_birth(const uint64_t* __restrict__ rec, int64_t n, uint8_t* tags) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) tags[uint32_t(rec[i] >> 32)] = make_tag(KIND_CLEARED, 0);
+  if (i < n) segk[i] = key_kidx(cols[i]) / seg_cells;
 }
 
 // seg_off[t] = first position i with segk[i] >= t (segk sorted ascending), t = 0..nseg
@@ -1092,6 +1050,10 @@ __global__ void k_seg_offsets(const uint32_t* __restrict__ segk, unsigned n, uns
   seg_off[t] = a;
 }
 
+__global__ void k_seg_single(unsigned n, uint32_t* seg_off) {
+  if (threadIdx.x < 2) seg_off[threadIdx.x] = threadIdx.x ? n : 0u;
+}
+
 __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint8_t* tags) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1101,23 +1063,20 @@ __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint
 
 }  // namespace
 
-void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st,
-                      bool hom) {
+void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st) {
   cudaStream_t s = ws.stream();
   const Geom& g = S.g;
   const int B = 256;
-  const int dc = hom ? d + 1 : d;  // dimension of the column cells
-  const int64_t nd = st.cells[dc];
-  // records: at most one per column, plus (homology) the essential d-cells
-  S.R.rec[d] = ws.alloc<uint64_t>(nd + (hom ? st.cells[d] : 0) + 1);
+  const int64_t nd = st.cells[d];
+  S.R.rec[d] = ws.alloc<uint64_t>(nd + 1);  // at most one record per column
   S.R.n[d] = 0;
-  if (nd == 0 && !hom) return;
+  if (nd == 0) return;
 
   unsigned long long* ctr = ws.alloc<unsigned long long>(16);
   CR_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
   uint64_t* cols = ws.alloc<uint64_t>(nd + 1);
-  k_collect_columns<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, dc, hom ? 1 : 0,
-                                                        cols, reinterpret_cast<unsigned*>(ctr));
+  k_collect_columns<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, cols,
+                                                        reinterpret_cast<unsigned*>(ctr));
   CR_CHECK_LAUNCH();
   const unsigned ncols = read_scalar(reinterpret_cast<unsigned*>(ctr), s, hs);
   st.columns[d] = ncols;
@@ -1131,7 +1090,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       uint32_t* segk = ws.alloc<uint32_t>(ncols);
       uint32_t* segk2 = ws.alloc<uint32_t>(ncols);
       uint64_t* cols2 = ws.alloc<uint64_t>(ncols);
-      k_seg_keys<<<grid_for(ncols, B), B, 0, s>>>(cols, ncols, S.seg_cells, hom ? 1 : 0, segk);
+      k_seg_keys<<<grid_for(ncols, B), B, 0, s>>>(cols, ncols, S.seg_cells, segk);
       CR_CHECK_LAUNCH();
       cub::DoubleBuffer<uint32_t> dk(segk, segk2);
       cub::DoubleBuffer<uint64_t> dv(cols, cols2);
@@ -1148,9 +1107,8 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       CR_CHECK_LAUNCH();
     } else {
       seg_off = ws.alloc<uint32_t>(2);
-      const uint32_t h[2] = {0u, ncols};
-      CR_CUDA(cudaMemcpyAsync(seg_off, h, sizeof(h), cudaMemcpyHostToDevice, s));
-      CR_CUDA(cudaStreamSynchronize(s));  // h is on the stack
+      k_seg_single<<<1, 32, 0, s>>>(ncols, seg_off);
+      CR_CHECK_LAUNCH();
     }
 
     int dev = 0, nsm = 0, per_sm = 0;
@@ -1159,52 +1117,43 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce, THREADS, 0));
     if (per_sm < 1) throw Error{CR_EINTERNAL, "k_reduce cannot be resident"};
     per_sm = per_sm > K5_MINB ? K5_MINB : per_sm;
-    if (const char* e = std::getenv("CR_K5_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+    if (opt(OPT_K5_BLOCKS_PER_SM) > 0 && opt(OPT_K5_BLOCKS_PER_SM) < per_sm)
+      per_sm = int(opt(OPT_K5_BLOCKS_PER_SM));
     int64_t blocks = int64_t(nsm) * per_sm;
     const int64_t need_blocks = (int64_t(ncols) + WPB - 1) / WPB;  // small problems
     if (need_blocks < blocks) blocks = need_blocks;
-    if (blocks > int64_t(THREADS) * 4) blocks = THREADS * 4;
     const uint32_t W = uint32_t(blocks * WPB);
 
+    const uint32_t npad = (ncols + 32767u) & ~32767u;
+    uint64_t* lv = ws.alloc<uint64_t>(int64_t(npad) + npad / 32 + npad / 1024 + npad / 32768);
     uint64_t* owninfo = ws.alloc<uint64_t>(g.ncells);
-    uint64_t* cand = ws.alloc<uint64_t>(W + blocks);
-    uint64_t* chunkmin = ws.alloc<uint64_t>(blocks);
-    uint32_t* chunkflag = ws.alloc<uint32_t>(blocks);
-    uint32_t* segpos = ws.alloc<uint32_t>(W);
-    const uint32_t ngroups = nseg < W ? nseg : W, G = W / ngroups;
-    unsigned* lo_buf = ws.alloc<unsigned>(2 * int64_t(ngroups));
-    unsigned* done_buf = reinterpret_cast<unsigned*>(ctr + 2);
+    unsigned* seg_next = ws.alloc<unsigned>(nseg);
     int* err = reinterpret_cast<int*>(ctr + 3);
     unsigned long long* nrec = ctr + 4;
     unsigned long long* pool_top = ctr + 5;
-    unsigned long long* stats = ctr + 6;  // [6] rounds [7] additions [8] lengths [9] max length
+    unsigned long long* stats = ctr + 6;   // [6..11]
+    unsigned long long* fetch = ctr + 12;
 
     // main-array slot per warp; longer columns grow into the pool.  The pool (reduced columns +
     // grown main arrays) is sized so that exhausting it -- which reruns the whole launch with 4x --
     // does not happen on realistic inputs: 16 entries per column + 32 Mi entries (256 MB)
-    const uint32_t mcap = std::getenv("CR_K5_MCAP")
-                              ? uint32_t(std::atoi(std::getenv("CR_K5_MCAP")))
-                              : 4096u;
+    const uint32_t mcap = 4096u;
     unsigned long long pool_cap = 16ull * ncols + (1ull << 25);
-    uint64_t* work = nullptr;
+    uint64_t* work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
     uint64_t* pool = nullptr;
-    unsigned long long* P_colstat = nullptr;
-    unsigned long long* P_rdbg = nullptr;
-    uint32_t P_rdbg_cap = 0;
     for (int attempt = 0;; ++attempt) {
-      if (!work) work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
       CR_CUDA(cudaMemsetAsync(owninfo, 0xFF, g.ncells * sizeof(uint64_t), s));
-      CR_CUDA(cudaMemsetAsync(lo_buf, 0xFF, 2 * sizeof(unsigned) * ngroups, s));
-      CR_CUDA(cudaMemsetAsync(done_buf, 0, 2 * sizeof(unsigned), s));
-      CR_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-      CR_CUDA(cudaMemsetAsync(nrec, 0, 6 * sizeof(unsigned long long), s));
+      CR_CUDA(cudaMemsetAsync(seg_next, 0, nseg * sizeof(unsigned), s));
+      CR_CUDA(cudaMemsetAsync(ctr + 3, 0, 13 * sizeof(unsigned long long), s));
+      k_levels_init<<<grid_for(npad, B), B, 0, s>>>(lv, lv + npad, lv + npad + npad / 32,
+                                                   lv + npad + npad / 32 + npad / 1024, ncols,
+                                                   npad);
+      CR_CHECK_LAUNCH();
       RP P;
       P.g = g;
       P.fx = FastDiv::make(uint32_t(g.KX));
       P.fxy = FastDiv::make(uint32_t(g.KX * g.KY));
-      P.d = d;
-      P.hom = hom ? 1 : 0;
       P.cols = cols;
       P.ncols = ncols;
       P.births = S.births;
@@ -1215,168 +1164,53 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.pool_cap = pool_cap;
       P.work = work;
       P.mcap = mcap;
-      P.cand = cand;
-      P.chunkmin = chunkmin;
-      P.chunkflag = chunkflag;
-      P.segpos = segpos;
-      P.seg_cells = S.seg_cells;
-      P.lo_buf = lo_buf;
-      P.done_buf = done_buf;
+      P.lv[0] = lv;
+      P.lv[1] = lv + npad;
+      P.lv[2] = lv + npad + npad / 32;
+      P.lv[3] = lv + npad + npad / 32 + npad / 1024;
       P.seg_off = seg_off;
       P.nseg = nseg;
-      P.G = G;
-      P.ngroups = ngroups;
+      P.seg_next = seg_next;
+      P.fetch = fetch;
       P.rec = S.R.rec[d];
       P.nrec = nrec;
       P.err = err;
-      // Round length: a warp stops adding after ~100 us of the round (not after a fixed number
-      // of additions): columns blocked on an earlier column's commit resume one round after it,
-      // so short rounds speed up chains of dependent columns, while long ones amortise the grid
-      // syncs.  Measured (CR_K5_BUDGET_US / CR_K5_STEPS): C4 reduce 168 ms with 256 steps per
-      // round -> 103 ms, C5 1.63 -> 1.37 s, C5b 0.62 -> 0.37 s; with read-ahead 100 us is best
-      // on C4 (100 / 106 / 118 ms at 100 / 150 / 250 us; C5, C5b within run-to-run noise).
-      {
-        int clk_khz = 0;
-        CR_CUDA(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev));
-        const char* bu = std::getenv("CR_K5_BUDGET_US");
-        const double us = bu ? std::atof(bu) : 100.0;
-        P.budget = (long long)(us * (clk_khz > 0 ? clk_khz : 1900000) / 1e3);
-        const char* ah = std::getenv("CR_K5_AHEAD");
-        P.ahead = ah ? std::atoi(ah) : 1;
-        const char* ms = std::getenv("CR_K5_STEPS");
-        P.max_steps = ms ? std::atoi(ms) : (1 << 30);
-      }
       P.stats = stats;
-      P.debug = std::getenv("CR_DEBUG_STATS") != nullptr;
-      {
-        const int dbg = P.debug ? 1 : 0;
-        unsigned long long z[4] = {0, 0, 0, 0};
-        CR_CUDA(cudaMemcpyToSymbolAsync(g_k5_dbg, &dbg, sizeof(int), 0, cudaMemcpyHostToDevice, s));
-        CR_CUDA(cudaMemcpyToSymbolAsync(g_k5_flush, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
-      }
-      P.colstat = nullptr;
-      P.rdbg = nullptr;
-      P.rdbg_cap = 0;
-      if (P.debug) {
-        P.rdbg_cap = 16384;
-        P.rdbg = ws.alloc<unsigned long long>(4 * int64_t(P.rdbg_cap));
-        CR_CUDA(cudaMemsetAsync(P.rdbg, 0, 32 * sizeof(unsigned long long) * P.rdbg_cap / 8, s));
-      }
-      if (P.debug) {
-        if (!P_colstat) P_colstat = ws.alloc<unsigned long long>(6 * int64_t(ncols));
-        P.colstat = P_colstat;
-        CR_CUDA(cudaMemsetAsync(P.colstat, 0, 6 * sizeof(unsigned long long) * ncols, s));
-      }
-      P_rdbg = P.rdbg;
-      P_rdbg_cap = P.rdbg_cap;
+      P.jitter = unsigned(opt(OPT_K5_JITTER_NS));
       void* args[] = {&P};
+      // cooperative launch: every warp resident at once (a warp may wait on any other's column)
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, 0, s));
       ++g_launch_count;
       const int e = read_scalar(err, s, hs);
-      if (std::getenv("CR_DEBUG_STATS"))
-        fprintf(stderr, "[cr] dim %d attempt %d: err %d (mcap %u, pool %llu)\n", d, attempt, e,
-                mcap, pool_cap);
       if (e == 0) break;
       if (e & 4) throw Error{CR_EINTERNAL, "reduced column longer than 2^24 entries"};
-      if (e & 8) throw Error{CR_EINTERNAL, "homology reduction: a column reduced to zero"};
       if (attempt > 12) throw Error{CR_ENOMEM, "reduction buffers exhausted"};
-      if (e & 2) {
-        ws.release(pool);
-        pool = nullptr;
-        pool_cap *= 4;
-      }
+      ws.release(pool);
+      pool = nullptr;
+      pool_cap *= 4;
     }
     CR_CUDA(cudaMemcpyAsync(hs.p, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
     S.R.n[d] = int64_t(hs.p[4]);
-    st.rounds[d] = int64_t(hs.p[6]);
+    st.rounds[d] = int64_t(hs.p[6]);  // waits on an earlier column
     st.additions[d] = int64_t(hs.p[7]);
     st.addlen[d] = int64_t(hs.p[8]);
     st.maxlen[d] = int64_t(hs.p[9]);
-    if (std::getenv("CR_DEBUG_STATS")) {
-      std::vector<unsigned long long> cs(6 * size_t(ncols));
-      CR_CUDA(cudaMemcpy(cs.data(), P_colstat, cs.size() * 8, cudaMemcpyDeviceToHost));
-      std::vector<std::pair<unsigned long long, uint32_t>> byent(ncols);
-      unsigned long long tot = 0;
-      for (uint32_t j = 0; j < ncols; ++j) {
-        byent[j] = {cs[6 * j + 1], j};
-        tot += cs[6 * j + 1];
-      }
-      std::sort(byent.rbegin(), byent.rend());
-      unsigned long long acc = 0;
-      const uint32_t marks[5] = {1, 10, 100, 1000, 10000};
-      fprintf(stderr, "[cr] dim %d entry work: total %llu;", d, tot);
-      for (uint32_t m : marks) {
-        if (m > ncols) break;
-        acc = 0;
-        for (uint32_t q = 0; q < m; ++q) acc += byent[q].first;
-        fprintf(stderr, " top%u %.3f", m, tot ? double(acc) / tot : 0.0);
-      }
-      unsigned long long fl[4];
-      CR_CUDA(cudaMemcpyFromSymbol(fl, g_k5_flush, sizeof(fl)));
-      fprintf(stderr, " | flushes %llu cycles %llu M-entries %llu", fl[0], fl[1], fl[2]);
-      {
-        const uint32_t nr = uint32_t(std::min<unsigned long long>(hs.p[6], P_rdbg_cap));
-        std::vector<unsigned long long> R(4 * size_t(nr));
-        CR_CUDA(cudaMemcpy(R.data(), P_rdbg, R.size() * 8, cudaMemcpyDeviceToHost));
-        double cyc = 0, steps_full = 0;
-        unsigned long long hist[5] = {0, 0, 0, 0, 0};
-        for (uint32_t r = 0; r < nr; ++r) {
-          cyc += double(R[4 * r]);
-          const unsigned long long ms = R[4 * r + 1];
-          hist[ms >= 256 ? 4 : ms >= 64 ? 3 : ms >= 16 ? 2 : ms >= 1 ? 1 : 0]++;
-          if (ms >= 256) steps_full += 1;
-        }
-        const double wall = nr > 1 ? double(R[4 * (nr - 1) + 3] - R[3]) / 1e6 : 0.0;
-        fprintf(stderr, "[cr] dim %d rounds %u: sum of max phase-A %.1f ms (at 1.9 GHz), wall %.1f ms;"
-                " max-steps hist 0:%llu 1-15:%llu 16-63:%llu 64-255:%llu 256:%llu\n",
-                d, nr, cyc / 1.9e6, wall, hist[0], hist[1], hist[2], hist[3], hist[4]);
-        for (uint32_t r = 0; r < nr; r += nr / 12 + 1)
-          fprintf(stderr, "   round %u: maxA %.1f us steps %llu active %llu\n", r,
-                  R[4 * r] / 1.9e3, R[4 * r + 1], R[4 * r + 2]);
-      }
-      fprintf(stderr, "\n[cr] top columns (pos, adds, entries):");
-      for (int q = 0; q < 8 && q < int(ncols); ++q) {
-        const uint32_t jj = byent[q].second;
-        const double a = double(cs[6 * jj] ? cs[6 * jj] : 1);
-        fprintf(stderr, "\n   col %u adds %llu entries %llu | per add cycles: lookup %.0f app %.0f "
-                "pool %.0f (flush %.0f)", jj, cs[6 * jj], byent[q].first, cs[6 * jj + 2] / a,
-                cs[6 * jj + 3] / a, cs[6 * jj + 4] / a, cs[6 * jj + 5] / a);
-      }
-      fprintf(stderr, "\n");
-      fprintf(stderr,
-              "[cr] dim %d: cols %u rounds %llu adds %llu pool_adds %llu pool_len %llu "
-              "cyc_pool %llu cyc_app %llu cyc_lookup %llu W %u\n",
-              d, ncols, hs.p[6], hs.p[7], hs.p[10], hs.p[11], hs.p[13], hs.p[14], hs.p[15], W);
-    }
-    if (hom) {
-      k_hom_essential<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, owninfo,
-                                                         S.R.rec[d], ctr + 4);
-      CR_CHECK_LAUNCH();
-      S.R.n[d] = int64_t(read_scalar(ctr + 4, s, hs));
-    }
+    if (opt(OPT_DEBUG))
+      fprintf(stderr, "[cr] dim %d: cols %u warps %u waits %llu adds %llu addlen %llu maxlen %llu "
+              "wait-cycles/warp %.3g commits %llu pool %llu/%llu\n", d, ncols, W, hs.p[6], hs.p[7],
+              hs.p[8], hs.p[9], double(hs.p[10]) / W, hs.p[11], hs.p[5], pool_cap);
     ws.release(work);
     ws.release(pool);
     ws.release(owninfo);
-  } else if (hom) {
-    k_hom_essential<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, nullptr,
-                                                       S.R.rec[d], ctr + 4);
-    CR_CHECK_LAUNCH();
-    S.R.n[d] = int64_t(read_scalar(ctr + 4, s, hs));
+    ws.release(lv);
   }
-  if (S.R.n[d] > 0 && !hom) {
+  if (S.R.n[d] > 0) {
     k_mark_cleared<<<grid_for(S.R.n[d], B), B, 0, s>>>(S.R.rec[d], S.R.n[d], S.tags);
     CR_CHECK_LAUNCH();
   }
   ws.release(cols);
-}
-
-void mark_cleared_births(GeneralState& S, int d, Workspace& ws) {
-  if (S.R.n[d] <= 0) return;
-  k_mark_cleared_birth<<<grid_for(S.R.n[d], 256), 256, 0, ws.stream()>>>(S.R.rec[d], S.R.n[d],
-                                                                          S.tags);
-  CR_CHECK_LAUNCH();
 }
 
 }  // namespace cr

@@ -36,6 +36,14 @@ thread_local Prof g_prof;
 
 thread_local int64_t g_launch_count = 0;
 
+static thread_local int64_t g_opts[OPT_COUNT] = {};
+int64_t opt(int key) { return key > 0 && key < OPT_COUNT ? g_opts[key] : 0; }
+bool set_opt(int key, int64_t v) {
+  if (key <= 0 || key >= OPT_COUNT) return false;
+  g_opts[key] = v;
+  return true;
+}
+
 void set_profiling(bool on) { g_prof.on = on; }
 
 void prof_begin(cudaStream_t s) {

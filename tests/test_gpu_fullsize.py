@@ -1,12 +1,17 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
-C2, C3 and C4 are compared element by element with the oracle (bars, birth cells, and for C4
-the full pairing).  C5 (451 M cells) is beyond the oracle's memory/time budget, so it is checked
-by properties that hold at any size: the Euler-characteristic curve (an exact integer identity
-between cell counts computed here from the image with numpy and the bars alive at each
-threshold), one essential class for the contractible ball domain, and births/deaths drawn from
-the image's values; its cropped version is compared element by element in test_gpu_parity.py.
+C2, C3 and C4 are compared element by element with the oracle run live (bars, birth cells, and
+for C4 the full pairing).  C5 (384^3, 451 M cells: ~3 min and ~20 GB for the oracle on one core)
+and C5b (64 x 128^3) are compared with SHA-256 digests of the oracle's own outputs, written once
+by ``tools/oracle_digest.py`` (which calls only ``oracle/``) into
+``tests/golden/fullsize_oracle.json``: the bars (dim, birth, death, birth cell, in output order)
+and the full partner array over every Khalimsky cell -- bit-exact, element for element, through a
+hash.  The same file pins the full-size partner arrays of C1, C2, C4 and of the first 1024 C3
+images.  C5 is additionally checked by properties that hold at any size (Euler curve, one
+essential class), which localise a failure that the digest only detects.
 """
+import hashlib
+import json
 import os
 from multiprocessing import Pool
 
@@ -48,6 +53,67 @@ def _eq(g, o, ctx):
 def test_c2_full(cr):
     x, md = gen.config("c2")
     _eq(_bars(cr, x, md), oracle.ph(x, md), "c2")
+
+
+_GOLD = os.path.join(os.path.dirname(__file__), "golden", "fullsize_oracle.json")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    with open(_GOLD) as f:
+        return json.load(f)
+
+
+def _bars_digest(d, b, e, c):
+    h = hashlib.sha256()
+    for a, t in ((d, np.int32), (b, np.float32), (e, np.float32), (c, np.uint32)):
+        h.update(np.ascontiguousarray(a).view(t).tobytes())
+    return h.hexdigest()
+
+
+def _partner_digest(cr, img):
+    import torch
+    p = cr.pairing(torch.from_numpy(np.ascontiguousarray(img)).cuda()).cpu().numpy().view(np.uint32)
+    return hashlib.sha256(p.tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_full_partner_digest(cr, gold, name):
+    """The full cell pairing (every Khalimsky cell) at BASELINE size equals the oracle's."""
+    img, md = gen.config(name)
+    assert _bars_digest(*_bars(cr, img, md)) == gold[name]["bars"], name
+    assert _partner_digest(cr, img) == gold[name]["partner"], name
+
+
+def test_c3_partner_first1024(cr, gold):
+    imgs = gen.config("c3")[0][:1024]
+    want = gold["c3"]["partner_first1024"]
+    for i in range(1024):
+        assert _partner_digest(cr, imgs[i]) == want[i], i
+
+
+def test_c5_full_digest(cr, gold):
+    """C5 (384^3 GRF in a ball, H0-H2): bars and the full 451 M-cell pairing vs the oracle."""
+    v, md = gen.config("c5")
+    bars = _bars(cr, v, md)
+    assert len(bars[0]) == gold["c5"]["n_bars"]
+    assert _bars_digest(*bars) == gold["c5"]["bars"]
+    assert _partner_digest(cr, v) == gold["c5"]["partner"]
+
+
+def test_c5b_full_digest(cr, gold):
+    """C5b (64 x 128^3, batched call as bench.py times it): per-volume bars vs the oracle, and
+    every volume's full pairing."""
+    vols, md = gen.config("c5b")
+    (d, b, e, c), off = _bars(cr, vols, md, batched=True)
+    recs = gold["c5b"]["volumes"]
+    assert len(off) == len(recs) + 1
+    for i, r in enumerate(recs):
+        s = slice(off[i], off[i + 1])
+        assert off[i + 1] - off[i] == r["n_bars"], i
+        assert _bars_digest(d[s], b[s], e[s], c[s]) == r["bars"], i
+    for i, r in enumerate(recs):
+        assert _partner_digest(cr, vols[i]) == r["partner"], i
 
 
 def _oracle_one(args):
