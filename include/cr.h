@@ -118,6 +118,17 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
                               int64_t out_capacity, int64_t* out_offsets, int64_t* n_pairs,
                               cr_stream_t stream);
 
+/* cr_barcodes_batched with HOST buffers (the end-to-end batch entry point, BASELINE config 5's
+ * batch): host_images (batch*prod(shape) float32, pinned memory is fastest) are copied in on
+ * `stream`, the bars (and birth cells, if host_out_birth_cells is non-NULL) and the batch+1 CSR
+ * offsets are copied back to the host buffers before return.  Arguments, output order and errors
+ * as for cr_barcodes_batched; device staging is allocated stream-ordered and freed before return. */
+cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, const int64_t* shape,
+                                   int ndim, int maxdim, cr_pair* host_out_pairs,
+                                   uint32_t* host_out_birth_cells, int64_t out_capacity,
+                                   int64_t* host_out_offsets, int64_t* n_pairs,
+                                   cr_stream_t stream);
+
 /* Full cell pairing, all dimensions (validation).  partner: device, Khalimsky-size uint32:
  * partner[k] = kidx of the cell paired with cell k (zero-length pairs included),
  * CR_PARTNER_ESSENTIAL if k never dies / is never killed, CR_PARTNER_ABSENT if k has a +inf vertex. */

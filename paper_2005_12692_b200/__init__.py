@@ -57,6 +57,9 @@ _lib.cr_barcodes_host.argtypes = [_vp, _i64p, ctypes.c_int, ctypes.c_int, _vp, _
 _lib.cr_barcodes_batched.restype = ctypes.c_int
 _lib.cr_barcodes_batched.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64,
                                      _vp, _i64p, _vp]
+_lib.cr_barcodes_batched_host.restype = ctypes.c_int
+_lib.cr_barcodes_batched_host.argtypes = [_vp, _i64, _i64p, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                          _i64, _vp, _i64p, _vp]
 _lib.cr_barcodes_topdim.restype = ctypes.c_int
 _lib.cr_barcodes_topdim.argtypes = [_vp, _i64p, ctypes.c_int, _vp, _vp, _i64, _i64p, _vp]
 _lib.cr_death_cells.restype = ctypes.c_int
@@ -84,7 +87,7 @@ _lib.cr_set_option.argtypes = [ctypes.c_int, _i64]
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
             "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling",
             "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim", "cr_barcodes_f64",
-            "cr_set_option"]
+            "cr_set_option", "cr_barcodes_batched_host"]
 
 # cr_option (include/cr.h): validation / measurement switches, 0 = the product path
 OPTIONS = {"force_general": 1, "1d_tree": 2, "top_reduce": 3, "k5_blocks_per_sm": 4,
@@ -274,6 +277,36 @@ def barcodes_batched(images, maxdim: int = 1, cells: bool = False, capacity: int
     _check(st)
     m = int(n.value)
     return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None), offsets
+
+
+def barcodes_batched_host(images, maxdim: int = 1, cells: bool = False, out=None, stream=None):
+    """End-to-end batch entry: host images (numpy or pinned CPU tensor, shape (B, *shape)) in,
+    host bars + CSR offsets out (cr_barcodes_batched_host).  ``out``: optional preallocated host
+    (pairs int32 (cap,3), offsets int64 (B+1,), cells uint32 (cap,) or None).  Returns
+    (Barcode, offsets) as host arrays/tensors."""
+    import torch
+    img = np.ascontiguousarray(images, dtype=np.float32) if isinstance(images, np.ndarray) else images
+    B = int(img.shape[0])
+    shape = tuple(img.shape[1:])
+    if out is None:
+        cap = max(max_pairs(shape, maxdim) * B, 1)
+        pairs = np.empty((cap, 3), np.int32)
+        offs = np.empty((B + 1,), np.int64)
+        cbuf = np.empty((cap,), np.uint32) if cells else None
+    else:
+        pairs, offs, cbuf = out
+    cap = int(pairs.shape[0])
+
+    def ptr(a):
+        return None if a is None else (a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr())
+    n = ctypes.c_int64(0)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    st = _lib.cr_barcodes_batched_host(ptr(img), B, _shape(shape), len(shape), int(maxdim),
+                                       ptr(pairs), ptr(cbuf), cap, ptr(offs), ctypes.byref(n),
+                                       ctypes.c_void_p(s.cuda_stream))
+    _check(st)
+    m = int(n.value)
+    return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None), offs
 
 
 def pairing(image):

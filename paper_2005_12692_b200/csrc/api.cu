@@ -441,6 +441,58 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
   }
 }
 
+cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, const int64_t* shape,
+                                   int ndim, int maxdim, cr_pair* host_out_pairs,
+                                   uint32_t* host_out_birth_cells, int64_t out_capacity,
+                                   int64_t* host_out_offsets, int64_t* n_pairs,
+                                   cr_stream_t stream) {
+  if (!n_pairs || !host_out_offsets || batch < 0 || !valid_shape(shape, ndim) || maxdim < 0 ||
+      out_capacity < 0 || (out_capacity > 0 && !host_out_pairs) || (batch > 0 && !host_images))
+    return CR_EINVAL;
+  try {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const Geom g = make_geom(shape, ndim);
+    const size_t in_bytes = size_t(batch) * size_t(g.nvox) * sizeof(float);
+    const int64_t cap = out_capacity > 0 ? out_capacity : 1;
+    float* dimg = nullptr;
+    cr_pair* dout = nullptr;
+    uint32_t* dcells = nullptr;
+    int64_t* doff = nullptr;
+    cr_status rs = CR_OK;
+    if (cudaMallocAsync(&dimg, in_bytes > 0 ? in_bytes : 4, s) != cudaSuccess ||
+        cudaMallocAsync(&dout, size_t(cap) * sizeof(cr_pair), s) != cudaSuccess ||
+        cudaMallocAsync(&doff, size_t(batch + 1) * sizeof(int64_t), s) != cudaSuccess ||
+        (host_out_birth_cells &&
+         cudaMallocAsync(&dcells, size_t(cap) * sizeof(uint32_t), s) != cudaSuccess)) {
+      cudaGetLastError();
+      rs = CR_ENOMEM;
+    } else {
+      if (in_bytes) CR_CUDA(cudaMemcpyAsync(dimg, host_images, in_bytes, cudaMemcpyHostToDevice, s));
+      rs = cr_barcodes_batched(dimg, batch, shape, ndim, maxdim, dout, dcells, out_capacity, doff,
+                               n_pairs, stream);
+      if (rs == CR_OK) {
+        CR_CUDA(cudaMemcpyAsync(host_out_offsets, doff, size_t(batch + 1) * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost, s));
+        if (*n_pairs > 0) {
+          CR_CUDA(cudaMemcpyAsync(host_out_pairs, dout, size_t(*n_pairs) * sizeof(cr_pair),
+                                  cudaMemcpyDeviceToHost, s));
+          if (host_out_birth_cells)
+            CR_CUDA(cudaMemcpyAsync(host_out_birth_cells, dcells, size_t(*n_pairs) * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, s));
+        }
+      }
+    }
+    if (dimg) cudaFreeAsync(dimg, s);
+    if (dout) cudaFreeAsync(dout, s);
+    if (doff) cudaFreeAsync(doff, s);
+    if (dcells) cudaFreeAsync(dcells, s);
+    CR_CUDA(cudaStreamSynchronize(s));
+    return rs;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
 cr_status cr_pairing(const float* image, const int64_t* shape, int ndim, uint32_t* partner,
                      cr_stream_t stream) {
   if (!image || !partner || !valid_shape(shape, ndim)) return CR_EINVAL;

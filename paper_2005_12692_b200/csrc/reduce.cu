@@ -82,6 +82,8 @@ struct RP {
   unsigned long long* stats;  // [0] waits [1] additions [2] sum of lengths [3] max length
                               // [4] cycles waited [5] commits
   unsigned jitter;     // validation: pseudo-random delays (ns) that perturb the schedule
+  unsigned long long* colrec;  // debug (option debug >= 2): per column 16 words, see k_reduce
+  bool detail;                 // debug >= 3: per-column cycle breakdown
 };
 constexpr int OI_LEN_BITS = 24;  // owninfo: stored column length field
 
@@ -261,6 +263,9 @@ struct Col {
   uint32_t wb;     // window base
   bool mstale;
   long long fcyc;  // debug: cycles spent in flushes
+  unsigned long long fent;  // debug: flushes, entries of M flushed
+  unsigned fn;
+  bool dbg;
   uint32_t cap;    // capacity of M[0] and M[1]
   uint64_t* spare; // the second half of a grown pair, installed after the merge that grew it
   uint64_t rv;     // per lane: entry `lane` of the register list R (NONE64 at and past nr)
@@ -555,8 +560,6 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
   return a + totI - totD;
 }
 
-__device__ int g_k5_dbg = 0;                      // CR_DEBUG_STATS: flush counters below
-__device__ unsigned long long g_k5_flush[4];      // flushes, cycles, entries of M, long merges
 
 // Make room for a merge of `need` entries into M[mb ^ 1]: a column that outgrows its warp's slot
 // moves to a larger pair carved from the pool (bump allocation; the few long columns of a launch
@@ -591,14 +594,13 @@ __device__ bool flush(Col& c, const RP& P, int lane) {
   const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
   if (nb == 0) return true;
   if (!grow(c, na + nb, P, lane)) return false;
-  const long long t0 = g_k5_dbg ? clock64() : 0;
+  const long long t0 = c.dbg ? clock64() : 0;
   const uint32_t n = merge_long_short(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
                                       c.M[c.mb ^ 1], c.F[c.fb ^ 1], lane);
-  if (g_k5_dbg && lane == 0) {
-    atomicAdd(g_k5_flush + 0, 1ull);
-    atomicAdd(g_k5_flush + 1, (unsigned long long)(clock64() - t0));
+  if (c.dbg) {
     c.fcyc += clock64() - t0;
-    atomicAdd(g_k5_flush + 2, (unsigned long long)na);
+    c.fent += na;
+    ++c.fn;
   }
   swap_main(c);
   c.nm = n;
@@ -827,10 +829,18 @@ __device__ __forceinline__ void jitter_sleep(const RP& P, uint32_t a, uint32_t b
 #ifndef K5_MINB
 #define K5_MINB 4
 #endif
+constexpr size_t K5_SMEM = sizeof(uint64_t) * WPB * (2 * FCAP + 8 + STAGE);
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
-  __shared__ uint64_t s_F[WPB][2][FCAP];
-  __shared__ uint64_t s_small[WPB][8];
-  __shared__ uint64_t s_stage[WPB][STAGE];
+  extern __shared__ uint64_t k5_smem[];  // K5Smem
+  uint64_t(*s_F)[2][FCAP] = reinterpret_cast<uint64_t(*)[2][FCAP]>(k5_smem);
+  uint64_t(*s_small)[8] = reinterpret_cast<uint64_t(*)[8]>(k5_smem + WPB * 2 * FCAP);
+  uint64_t(*s_stage)[STAGE] = reinterpret_cast<uint64_t(*)[STAGE]>(k5_smem + WPB * (2 * FCAP + 8));
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t w = blockIdx.x * WPB + wib;
@@ -860,12 +870,23 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     c.nr = c.r0 = 0;
     c.mstale = true;
     c.nf = coboundary(P, cell, c.F[0], lane);
+    const unsigned long long c_t0 = P.colrec ? gtimer() : 0;
+    c.dbg = P.detail;
+    c.fcyc = 0;
+    c.fent = 0;
+    c.fn = 0;
+    unsigned long long d_tp = 0, d_lk = 0, d_app = 0, d_pool = 0, d_napp = 0, d_plen = 0;
+    unsigned long long c_adds = adds, c_wait = 0, c_waits = waits;
+    uint32_t c_blk = NONE32;
     uint64_t pub = 0;      // last published candidate
     uint64_t xp = NONE64;  // the pivot the scan cursor x is valid for
     uint32_t x = seg_lo;
     bool ok = true;
     while (true) {
+      const long long q0 = c.dbg ? clock64() : 0;
       const uint64_t piv = take_pivot(c, lane);
+      const long long q1 = c.dbg ? clock64() : 0;
+      d_tp += q1 - q0;
       if (piv == NONE64) {  // zero column: essential (exact given the clearing)
         if (lane == 0) {
           const unsigned long long r = atomicAdd(P.nrec, 1ull);
@@ -885,6 +906,8 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       const uint64_t* add;
       uint32_t alen;
       bool glob;
+      const long long q2 = c.dbg ? clock64() : 0;
+      d_lk += q2 - q1;
       if (tag_kind(t) == KIND_DOWN) {
         // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
         alen = spec_finish(P, sp, tag_dir(t), piv, s_small[wib], lane);
@@ -907,6 +930,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           if (b == j) break;
           x = b;
           ++waits;
+          c_blk = b;
           const long long t0 = clock64();
           unsigned ns = 32;
           for (int it = 1;; ++it) {
@@ -934,6 +958,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
             if (ns < 512) ns <<= 1;
           }
           wcyc += clock64() - t0;
+          c_wait += clock64() - t0;
           if (!ok) break;
           x = b + 1;
         }
@@ -975,6 +1000,16 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       addlen += c.len() + alen;
       ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
                 : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
+      if (c.dbg) {
+        const long long q3 = clock64();
+        if (glob) {
+          d_pool += q3 - q2;
+          d_plen += alen;
+        } else {
+          d_app += q3 - q2;
+          ++d_napp;
+        }
+      }
       if (!ok) break;  // pool exhausted (err 2 set): the launch is retried
       ++adds;
       const uint64_t l = c.len();
@@ -982,6 +1017,26 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     }
     if (!ok) break;
     finish_column(P, j, lane);
+    if (P.colrec && lane == 0) {
+      unsigned long long* R = P.colrec + 16ull * j;
+      R[0] = c_t0;
+      R[1] = gtimer();
+      R[2] = adds - c_adds;
+      R[3] = c_wait;
+      R[4] = waits - c_waits;
+      R[5] = c_blk;
+      R[6] = w;
+      if (P.detail) {
+        R[8] = d_tp;
+        R[9] = d_lk;
+        R[10] = d_app;
+        R[11] = d_pool;
+        R[12] = d_napp;
+        R[13] = d_plen;
+        R[14] = (unsigned long long)c.fcyc;
+        R[15] = ((unsigned long long)c.fn << 40) | c.fent;
+      }
+    }
   }
   if (lane == 0) {
     atomicAdd(P.stats + 0, waits);
@@ -1063,6 +1118,60 @@ __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint
 
 }  // namespace
 
+// Debug (option debug >= 2): the chain that ends the launch -- from the last column to finish,
+// follow each column's last blocker -- and the busiest columns.
+static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, cudaStream_t s) {
+  constexpr int RW = 16;
+  std::vector<unsigned long long> R(RW * size_t(ncols));
+  CR_CUDA(cudaMemcpyAsync(R.data(), dcol, R.size() * 8, cudaMemcpyDeviceToHost, s));
+  CR_CUDA(cudaStreamSynchronize(s));
+  unsigned long long t0 = ~0ull, t1 = 0;
+  uint32_t last = 0;
+  for (uint32_t j = 0; j < ncols; ++j) {
+    t0 = std::min(t0, R[RW * j]);
+    if (R[RW * j + 1] > t1) t1 = R[RW * j + 1], last = j;
+  }
+  fprintf(stderr, "[cr] K5 span %.3f ms; chain from the last column (col: start..end us, adds, "
+          "wait us, waits, blocker):\n", (t1 - t0) / 1e6);
+  uint32_t cur = last;
+  for (int k = 0; k < 40 && cur != NONE32 && cur < ncols; ++k) {
+    const unsigned long long* r = &R[RW * size_t(cur)];
+    fprintf(stderr, "   %u: %.1f..%.1f adds %llu wait %.1f waits %llu blk %lld\n", cur,
+            (r[0] - t0) / 1e3, (r[1] - t0) / 1e3, r[2], r[3] / 1.9e3, r[4],
+            r[5] == NONE32 ? -1ll : (long long)r[5]);
+    cur = uint32_t(r[5]);
+  }
+  std::vector<std::pair<unsigned long long, uint32_t>> busy(ncols);
+  for (uint32_t j = 0; j < ncols; ++j) busy[j] = {R[RW * j + 1] - R[RW * j], j};
+  std::sort(busy.rbegin(), busy.rend());
+  fprintf(stderr, "[cr] longest columns (col: start..end us, adds, wait us):\n");
+  for (int k = 0; k < 12 && k < int(ncols); ++k) {
+    const uint32_t j = busy[k].second;
+    const unsigned long long* r = &R[RW * size_t(j)];
+    fprintf(stderr, "   %u: %.1f..%.1f adds %llu wait %.1f\n", j, (r[0] - t0) / 1e3,
+            (r[1] - t0) / 1e3, r[2], r[3] / 1.9e3);
+    if (r[8] + r[9] + r[10] + r[11]) {
+      const double a = r[2] ? double(r[2]) : 1.0, pa = double(r[2] - r[12]);
+      fprintf(stderr, "      per add cycles: pivot %.0f lookup %.0f | apparent adds %llu at %.0f, "
+              "pool adds %.0f at %.0f (avg len %.0f) | flushes %llu: %.0f cycles each, avg M %.0f\n",
+              r[8] / a, r[9] / a, r[12], r[12] ? r[10] / double(r[12]) : 0.0, pa,
+              pa ? r[11] / pa : 0.0, pa ? r[13] / pa : 0.0, r[15] >> 40,
+              (r[15] >> 40) ? r[14] / double(r[15] >> 40) : 0.0,
+              (r[15] >> 40) ? double(r[15] & ((1ull << 40) - 1)) / double(r[15] >> 40) : 0.0);
+    }
+  }
+  // in-flight profile: columns started but unfinished, sampled at 20 instants
+  for (int q = 1; q < 20; ++q) {
+    const unsigned long long tq = t0 + (t1 - t0) * q / 20;
+    uint32_t inflight = 0, done = 0;
+    for (uint32_t j = 0; j < ncols; ++j) {
+      inflight += R[RW * j] <= tq && R[RW * j + 1] > tq;
+      done += R[RW * j + 1] <= tq;
+    }
+    fprintf(stderr, "   t=%.1f ms: in flight %u, done %u\n", (tq - t0) / 1e6, inflight, done);
+  }
+}
+
 void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& st) {
   cudaStream_t s = ws.stream();
   const Geom& g = S.g;
@@ -1114,7 +1223,13 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     int dev = 0, nsm = 0, per_sm = 0;
     CR_CUDA(cudaGetDevice(&dev));
     CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce, THREADS, 0));
+    static thread_local int attr_dev = -1;
+    if (attr_dev != dev) {
+      CR_CUDA(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(K5_SMEM)));
+      attr_dev = dev;
+    }
+    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce, THREADS, K5_SMEM));
     if (per_sm < 1) throw Error{CR_EINTERNAL, "k_reduce cannot be resident"};
     per_sm = per_sm > K5_MINB ? K5_MINB : per_sm;
     if (opt(OPT_K5_BLOCKS_PER_SM) > 0 && opt(OPT_K5_BLOCKS_PER_SM) < per_sm)
@@ -1141,6 +1256,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     unsigned long long pool_cap = 16ull * ncols + (1ull << 25);
     uint64_t* work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
     uint64_t* pool = nullptr;
+    unsigned long long* colrec = nullptr;
     for (int attempt = 0;; ++attempt) {
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
       CR_CUDA(cudaMemsetAsync(owninfo, 0xFF, g.ncells * sizeof(uint64_t), s));
@@ -1177,10 +1293,16 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.err = err;
       P.stats = stats;
       P.jitter = unsigned(opt(OPT_K5_JITTER_NS));
+      P.colrec = nullptr;
+      P.detail = opt(OPT_DEBUG) >= 3;
+      if (opt(OPT_DEBUG) >= 2) {
+        if (!colrec) colrec = ws.alloc<unsigned long long>(16 * int64_t(ncols));
+        P.colrec = colrec;
+      }
       void* args[] = {&P};
       // cooperative launch: every warp resident at once (a warp may wait on any other's column)
       CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
-                                          args, 0, s));
+                                          args, K5_SMEM, s));
       ++g_launch_count;
       const int e = read_scalar(err, s, hs);
       if (e == 0) break;
@@ -1201,6 +1323,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       fprintf(stderr, "[cr] dim %d: cols %u warps %u waits %llu adds %llu addlen %llu maxlen %llu "
               "wait-cycles/warp %.3g commits %llu pool %llu/%llu\n", d, ncols, W, hs.p[6], hs.p[7],
               hs.p[8], hs.p[9], double(hs.p[10]) / W, hs.p[11], hs.p[5], pool_cap);
+    if (colrec) debug_critical_path(colrec, ncols, s);
     ws.release(work);
     ws.release(pool);
     ws.release(owninfo);

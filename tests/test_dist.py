@@ -29,42 +29,52 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, nimg=7):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        # rank r owns images [start, stop) of a batch of 7; image i has i % 3 + 1 bars
-        start, stop = shard_range(7, rank, world)
+        # rank r owns images [start, stop) of a batch of nimg; image i has i % 3 bars (some none)
+        start, stop = shard_range(nimg, rank, world)
         rows, offs = [], [0]
         for i in range(start, stop):
-            for k in range(i % 3 + 1):
+            for k in range(i % 3):
                 rows.append([k % 2, 100 * i + k, 100 * i + k + 1])
             offs.append(len(rows))
         pairs = torch.tensor(rows, dtype=torch.int32).reshape(-1, 3)
         offsets = torch.tensor(offs, dtype=torch.int64)
-        p_all, o_all = gather_barcodes(pairs, offsets)
-        q.put((rank, p_all.tolist(), o_all.tolist()))
+        got = gather_barcodes(pairs, offsets)
+        q.put((rank, None if got is None else (got[0].tolist(), got[1].tolist())))
     finally:
         dist.destroy_process_group()
 
 
-def test_gather_world2_gloo():
+def _run(world, nimg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, nimg)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in procs]
+    res = dict(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world,nimg", [(2, 7), (3, 2)])
+def test_gather_to_rank0_gloo(world, nimg):
+    """Rank 0 receives every shard's bars and CSR offsets in input order (a rank may own no
+    image); the other ranks get None."""
+    res = _run(world, nimg)
     exp_rows, exp_offs = [], [0]
-    for i in range(7):
-        for k in range(i % 3 + 1):
+    for i in range(nimg):
+        for k in range(i % 3):
             exp_rows.append([k % 2, 100 * i + k, 100 * i + k + 1])
         exp_offs.append(len(exp_rows))
-    for rank, rows, offs in res:
-        assert rows == exp_rows, rank
-        assert offs == exp_offs, rank
+    rows, offs = res[0]
+    assert rows == exp_rows
+    assert offs == exp_offs
+    for r in range(1, world):
+        assert res[r] is None

@@ -36,6 +36,10 @@ def main():
     gold = json.load(open(os.path.join(ROOT, "tests", "golden", "fullsize_oracle.json")))
     if "--debug" in sys.argv:
         cr.set_option("debug", 1)
+    if "--debug2" in sys.argv:
+        cr.set_option("debug", 2)
+    if "--debug3" in sys.argv:
+        cr.set_option("debug", 3)
     cr.set_profiling(True)
     for name in args:
         img, md = gen.config(name)
