@@ -252,7 +252,7 @@ def cpu_baseline(cfg, host_img, maxdim):
     hi = host_info()
     if cfg in BATCHED:
         one = host_img[0]
-        dt1, rss1 = _oracle_one((one, maxdim))
+        dt1, rss1 = oracle_pool([one], maxdim, 1)  # one worker process: its own peak RSS
         P = max(1, min(os.cpu_count() or 1, 64, len(host_img)))
         sample = host_img[:P] if len(host_img) >= P else host_img
         wall, rss = oracle_pool(list(sample), maxdim, P)

@@ -20,11 +20,19 @@
  * Conventions for every call:
  *   - pointers documented "device" are CUDA device pointers on the current device; "host" are
  *     ordinary (pageable or pinned) host pointers.  The library never frees or retains them.
- *   - work is enqueued on `stream` (a cudaStream_t; NULL means the legacy default stream).
- *     Workspace is allocated stream-ordered on that stream and released before return.
- *     Calls are blocking: they return after the result is complete.
- *   - no global mutable state; calls on different streams/devices from different host threads
- *     are safe.  cr_status_string's CUDA error text and cr_last_stats are thread-local.
+ *   - work is enqueued on `stream` (a cudaStream_t; NULL means the legacy default stream) on the
+ *     current device.  Calls are blocking: they return after the result is complete.
+ *   - workspace: device scratch comes from a per-host-thread, per-device block cache.  Blocks
+ *     are handed out again to later calls of the same thread (a steady stream of calls makes no
+ *     allocator calls) and are KEPT after a call returns -- a C5-size call leaves a few GB
+ *     cached.  cr_release_workspace() returns this thread's blocks to the driver (also done
+ *     automatically when the thread exits); cr_workspace_bytes() reports what is held.  If an
+ *     allocation fails, the thread's free blocks are released and the allocation retried once.
+ *   - synchronisation: a call synchronises with `stream` a few times to size its buffers from
+ *     device-side counts (e.g. residual columns), and once at the end to learn n_pairs.
+ *   - no state shared between host threads; calls on different streams/devices from different
+ *     host threads are safe.  cr_status_string's CUDA error text, cr_last_stats, the options
+ *     of cr_set_option and the workspace cache are thread-local.
  *   - on any error, outputs are unspecified; nothing is thrown across the ABI.
  */
 #ifndef CR_H_
@@ -108,7 +116,9 @@ cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int nd
                            cr_pair* host_out_pairs, uint32_t* host_out_birth_cells,
                            int64_t out_capacity, int64_t* n_pairs, cr_stream_t stream);
 
-/* Barcodes of `batch` independent images of identical shape stored back to back
+/* Barcodes of `batch` independent images of identical shape stored back to back -- a batch of
+ * images as in the paper's CNN application to (Reduced) MNIST; each image's
+ * bars are exactly cr_barcodes' for that image (the complexes are disjoint, reading R16)
  * (images: device, batch*prod(shape) float32).  Bars of image b occupy
  * out_pairs[out_offsets[b] .. out_offsets[b+1]) in the per-image order of cr_barcodes;
  * out_birth_cells (optional) holds kidx within the image.
@@ -129,7 +139,10 @@ cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, cons
                                    int64_t* host_out_offsets, int64_t* n_pairs,
                                    cr_stream_t stream);
 
-/* Full cell pairing, all dimensions (validation).  partner: device, Khalimsky-size uint32:
+/* Full cell pairing, all dimensions (validation): the pairs (birth cell, death cell) of the
+ * reduction PAPER.md:130-142 (plus the H0 union-find pairs, and the
+ * zero-persistence apparent pairs), unique given the total order R1.
+ * partner: device, Khalimsky-size uint32:
  * partner[k] = kidx of the cell paired with cell k (zero-length pairs included),
  * CR_PARTNER_ESSENTIAL if k never dies / is never killed, CR_PARTNER_ABSENT if k has a +inf vertex. */
 #define CR_PARTNER_ESSENTIAL 0xFFFFFFFFu
@@ -157,11 +170,12 @@ cr_status cr_death_cells(const float* image, const int64_t* shape, int ndim,
 cr_status cr_lifetime_image(const float* images, int64_t batch, const int64_t* shape, int ndim,
                             int maxdim, float inf_value, float* out, cr_stream_t stream);
 
-/* Number of cells of dims 0..min(maxdim, ndim-1): a safe out_capacity (each bar has a distinct
- * birth cell).  Returns -1 on invalid shape. */
+/* Number of cells of dims 0..min(maxdim, ndim-1) of the V-construction grid:
+ * a safe out_capacity (each bar has a distinct birth cell).  Returns -1 on invalid shape. */
 int64_t cr_max_pairs(const int64_t* shape, int ndim, int maxdim);
 
-/* Number of Khalimsky cells prod(2*shape[i]-1), the partner array length; -1 on invalid shape. */
+/* Number of Khalimsky cells prod(2*shape[i]-1) -- every cube of the grid --
+ * the partner array length; -1 on invalid shape. */
 int64_t cr_num_cells(const int64_t* shape, int ndim);
 
 /* Static description of a status code, or (for CR_ECUDA / CR_EINTERNAL) the thread-local text of
@@ -192,6 +206,12 @@ void cr_last_stats(cr_stats* out);
  * When on, each call records an event after every pipeline stage on its stream and fills
  * cr_stats.stage_ms / stage_name; the events add no synchronisation beyond the call's own. */
 void cr_set_profiling(int enable);
+
+/* Return this host thread's cached device workspace (every device) to the driver and trim the
+ * device memory pools; the next call allocates afresh.  Never fails. */
+void cr_release_workspace(void);
+/* Device bytes held by this host thread's workspace cache (all devices). */
+int64_t cr_workspace_bytes(void);
 
 /* Validation and measurement options of this host thread (thread-local; every option defaults to
  * 0 = the product path).  They select cross-check variants that must give identical results --

@@ -81,13 +81,18 @@ _lib.cr_last_stats.restype = None
 _lib.cr_last_stats.argtypes = [ctypes.POINTER(CrStats)]
 _lib.cr_set_profiling.restype = None
 _lib.cr_set_profiling.argtypes = [ctypes.c_int]
+_lib.cr_release_workspace.restype = None
+_lib.cr_release_workspace.argtypes = []
+_lib.cr_workspace_bytes.restype = _i64
+_lib.cr_workspace_bytes.argtypes = []
 _lib.cr_set_option.restype = ctypes.c_int
 _lib.cr_set_option.argtypes = [ctypes.c_int, _i64]
 
 EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairing", "cr_max_pairs",
             "cr_num_cells", "cr_status_string", "cr_last_stats", "cr_set_profiling",
             "cr_death_cells", "cr_lifetime_image", "cr_barcodes_topdim", "cr_barcodes_f64",
-            "cr_set_option", "cr_barcodes_batched_host"]
+            "cr_set_option", "cr_barcodes_batched_host", "cr_release_workspace",
+            "cr_workspace_bytes"]
 
 # cr_option (include/cr.h): validation / measurement switches, 0 = the product path
 OPTIONS = {"force_general": 1, "1d_tree": 2, "top_reduce": 3, "k5_blocks_per_sm": 4,
@@ -129,6 +134,16 @@ def num_cells(shape) -> int:
 def set_profiling(enable: bool) -> None:
     """Per-stage CUDA-event timing of subsequent calls on this thread (see cr_set_profiling)."""
     _lib.cr_set_profiling(1 if enable else 0)
+
+
+def release_workspace() -> None:
+    """Return this thread's cached device workspace to the driver (cr_release_workspace)."""
+    _lib.cr_release_workspace()
+
+
+def workspace_bytes() -> int:
+    """Device bytes held by this thread's workspace cache (cr_workspace_bytes)."""
+    return int(_lib.cr_workspace_bytes())
 
 
 def set_option(name: str, value: int) -> None:

@@ -10,6 +10,8 @@ namespace cr {
 const char* last_error_text();
 void set_profiling(bool on);
 bool set_opt(int key, int64_t v);
+void release_workspace();
+size_t workspace_bytes();
 static thread_local cr_stats g_last_stats;
 static thread_local uint64_t g_stats_gen = 0;  // prof_gen() when g_last_stats was committed
 static void commit_stats(const cr_stats& st) {
@@ -221,6 +223,10 @@ void cr_last_stats(cr_stats* out) {
 }
 
 void cr_set_profiling(int enable) { cr::set_profiling(enable != 0); }
+
+void cr_release_workspace(void) { cr::release_workspace(); }
+
+int64_t cr_workspace_bytes(void) { return int64_t(cr::workspace_bytes()); }
 
 cr_status cr_set_option(int option, int64_t value) {
   return cr::set_opt(option, value) ? CR_OK : CR_EINVAL;

@@ -109,13 +109,60 @@ struct Cache {
   cudaEvent_t done = nullptr;                // recorded at the end of the last call
   cudaStream_t last = nullptr;
   bool pool_set = false;
+  size_t bytes = 0;                          // held by this cache (in use or free)
 };
-thread_local Cache g_cache[MAX_DEV];
+struct Caches {
+  Cache c[MAX_DEV];
+  // A host thread that exits returns its blocks (errors are ignored: at process exit the CUDA
+  // runtime may already be gone, and then the driver reclaims everything anyway).
+  ~Caches() { release_all(); }
+  void release_all();
+};
+thread_local Caches g_caches;
+#define g_cache (g_caches.c)
 size_t round_block(size_t b) {
   if (b <= (size_t(1) << 20)) return (b + 511) & ~size_t(511);
   return (b + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
 }
 }  // namespace
+
+void Caches::release_all() {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  for (int d = 0; d < MAX_DEV; ++d) {
+    Cache& C = c[d];
+    Arena& A = g_arena[d];
+    if (C.size_of.empty() && !A.base) continue;
+    if (cudaSetDevice(d) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (C.done) cudaEventSynchronize(C.done);  // the last call's work is complete
+    for (auto& kv : C.size_of) cudaFree(kv.first);
+    if (A.base) cudaFree(A.base);
+    A.base = nullptr;
+    A.cap = 0;
+    C.free_blocks.clear();
+    C.size_of.clear();
+    C.bytes = 0;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    cudaGetLastError();
+  }
+  cudaSetDevice(cur);
+  cudaGetLastError();
+}
+
+void release_workspace() { g_caches.release_all(); }
+
+size_t workspace_bytes() {
+  size_t n = 0;
+  for (int d = 0; d < MAX_DEV; ++d) n += g_cache[d].bytes + g_arena[d].cap;
+  return n;
+}
 
 Workspace::Workspace(cudaStream_t s) : s_(s) {
   if (cudaGetDevice(&dev_) != cudaSuccess || dev_ < 0 || dev_ >= MAX_DEV) dev_ = 0;
@@ -180,12 +227,14 @@ void* Workspace::alloc_bytes(size_t bytes) {
     cudaGetLastError();  // out of memory: return the cache to the driver and retry once
     for (auto& kv : C.free_blocks) {
       cudaFreeAsync(kv.second, s_);
+      C.bytes -= C.size_of[kv.second];
       C.size_of.erase(kv.second);
     }
     C.free_blocks.clear();
     CR_CUDA(cudaMallocAsync(&p, want, s_));
   }
   C.size_of[p] = want;
+  C.bytes += want;
   ptrs_.push_back(p);
   return p;
 }
