@@ -547,7 +547,10 @@ __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
   if (!mask) return;
   int lane = threadIdx.x & 31;
   unsigned long long base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(nrec, (unsigned long long)__popc(mask));
+  if (lane == __ffs(mask) - 1) {
+    base = atomicAdd(nrec, (unsigned long long)__popc(mask));
+    if (nroots) atomicAdd(nroots, (unsigned long long)__popc(mask));
+  }
   base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
   if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
 }
@@ -608,13 +611,17 @@ __device__ __forceinline__ uint32_t dual_side(const DualG& G, uint32_t k, int a,
   return kidx_vox(G.g, uint32_t(int64_t(k) + (sg ? st : -st)));
 }
 
+// absent_to_omega: no +inf cavity is enclosed (Euler count, see top_dual), so every absent top
+// cell lies in the outside vertex's component and hangs under it directly.
 __global__ void k_dual_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                              DualG G, uint32_t* __restrict__ parent) {
+                              DualG G, uint32_t* __restrict__ parent, int absent_to_omega) {
   const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vv > G.omega) return;
   const uint32_t v = uint32_t(vv);
   uint32_t p = v, k;
-  if (v < G.omega && top_of_voxel(G.g, v, k) && births[k] != ABSENT_ORD) {
+  if (v < G.omega && top_of_voxel(G.g, v, k) && births[k] == ABSENT_ORD) {
+    if (absent_to_omega) p = G.omega;
+  } else if (v < G.omega && top_of_voxel(G.g, v, k)) {
     const uint8_t t = tags[k];
     if (tag_kind(t) == KIND_DOWN) {  // dual apparent pair: hangs under its face's other coface
       const int dir = tag_dir(t);
@@ -920,10 +927,25 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   unsigned long long* cnt = ws.alloc<unsigned long long>(8);
   CR_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), s));
   uint32_t* parent = ws.alloc<uint32_t>(nv);
-  k_dual_parent<<<grid_for(nv, B), B, 0, s>>>(S.births, S.tags, G, parent);
+  // Enclosed +inf cavities (absent components that do not reach the outside) give the essential
+  // classes of the top dimension d = D-1, and by the Euler-Poincare relation their number is
+  //   ess[d] = (-1)^d (chi - sum_{e<d} (-1)^e ess[e]),  chi = sum_e (-1)^e #(finite e-cells),
+  // known here when the dimensions below were computed in this call.  With none, every absent
+  // top cell belongs to the outside vertex's component: no union-find over the absent cells.
+  bool no_cavity = false;
+  if (S.lower_essential_known) {
+    int64_t chi = 0, low = 0;
+    for (int e = 0; e <= g.D; ++e) chi += (e & 1) ? -st.cells[e] : st.cells[e];
+    for (int e = 0; e < d; ++e) low += (e & 1) ? -st.essential[e] : st.essential[e];
+    const int64_t ess_top = (d & 1) ? low - chi : chi - low;
+    no_cavity = ess_top == 0;
+  }
+  k_dual_parent<<<grid_for(nv, B), B, 0, s>>>(S.births, S.tags, G, parent, no_cavity ? 1 : 0);
   CR_CHECK_LAUNCH();
-  k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
-  CR_CHECK_LAUNCH();
+  if (!no_cavity) {
+    k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
+    CR_CHECK_LAUNCH();
+  }
   k_pointer_jump<<<grid_for(nv, B), B, 0, s>>>(parent, nv);
   CR_CHECK_LAUNCH();
   Cand* cand = ws.alloc<Cand>(st.cells[d] + 1);
@@ -1039,6 +1061,7 @@ void reduce_dims(GeneralState& S, const Geom& g, int dmax, Workspace& ws, HostSc
                  cr_stats& st) {
   static const char* names[4] = {"", "reduce_d1", "reduce_d2", "reduce_d3"};
   cudaStream_t s = ws.stream();
+  S.lower_essential_known = true;  // H0 and each reduced dimension count their essential classes
   for (int d = 1; d <= dmax; ++d) {
     if (!(use_dual(g, d) && top_dual(S, d, ws, hs, st)))
       reduce_dimension(S, d, ws, hs, st);
@@ -1128,12 +1151,13 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
   CR_CHECK_LAUNCH();
   k_h0_essential<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
-                                                    nullptr);
+                                                    cnt + 22);
   CR_CHECK_LAUNCH();
-  CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           s));
   CR_CUDA(cudaStreamSynchronize(s));
   S.R.n[0] = int64_t(hs.p[0]);
+  st.essential[0] = int64_t(hs.p[9]);
   st.rounds[0] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 7)[2]);
   prof_mark(s, "h0");
   ws.release(cand);

@@ -19,6 +19,7 @@ struct GeneralState {
   uint32_t seg_cells = 0;      // batched: Khalimsky cells per image period (kidx / seg_cells =
                                // image); 0 for a single image
   bool top_only = false;       // compute only dimension D-1, by duality (cr_barcodes_topdim)
+  bool lower_essential_known = false;  // cr_stats.essential[e] holds every e < current dim
   Records R;
 };
 

@@ -68,6 +68,7 @@ struct RP {
   unsigned long long pool_cap;
   uint64_t* work;      // per warp: 2 * mcap main-array entries
   uint32_t mcap;
+  uint64_t* gwork;     // per warp: 2 * (GCAP + FCAP) middle-tier entries
   // lv[0][j] = cand(j): 0 before column j starts, then a lower bound of its pivot key, NONE64
   // once it is finished.  lv[L][e] (L = 1..3) = a lower bound of min lv[0] over the 32^L columns
   // [e * 32^L, (e+1) * 32^L): every entry only grows, so a stale bound is still a bound.
@@ -81,9 +82,9 @@ struct RP {
   int* err;
   unsigned long long* stats;  // [0] waits [1] additions [2] sum of lengths [3] max length
                               // [4] cycles waited [5] commits
+  unsigned long long* ness;  // essential classes (zero columns)
   unsigned jitter;     // validation: pseudo-random delays (ns) that perturb the schedule
   unsigned long long* colrec;  // debug (option debug >= 2): per column 16 words, see k_reduce
-  bool detail;                 // debug >= 3: per-column cycle breakdown
 };
 constexpr int OI_LEN_BITS = 24;  // owninfo: stored column length field
 
@@ -101,7 +102,7 @@ __device__ __forceinline__ uint32_t rkid(const RP&, uint64_t key) { return uint3
 
 // The column of cell s, sorted ascending, written to dst (<= 6 entries): its finite cofacets (the
 // implicit coboundary of PAPER.md:135-136).  Warp-collective.
-__device__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
+__device__ __forceinline__ uint32_t coboundary(const RP& P, uint32_t s, uint64_t* dst, int lane) {
   const Geom& g = P.g;
   const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
   const uint32_t r = P.fx.div(s), z = P.fxy.div(s);
@@ -218,25 +219,27 @@ __device__ uint32_t merge_small(const uint64_t* A, uint32_t a, const uint64_t* B
 // merged there, so a long array is read once, coalesced, instead of one global binary search per
 // element.  Chunks split by the merge path with ties taken from A first; an equal pair split by a
 // chunk boundary is kept together by taking B's copy into the chunk too.
-template <bool BG>
-__device__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
+template <bool BG, uint32_t CH = FCAP - 1>
+__device__ __noinline__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
                                   uint64_t* C, uint64_t* SA, uint64_t* SB, int lane) {
-  constexpr uint32_t CH = FCAP - 1;
   uint32_t i0 = 0, j0 = 0, out = 0;
   while (i0 < a || j0 < b) {
     const uint32_t ra = a - i0, rb = b - j0;
     const uint32_t k = ra + rb < CH ? ra + rb : CH;
-    uint32_t i = 0;
-    if (lane == 0) {
-      uint32_t lo = k > rb ? k - rb : 0, hi = k < ra ? k : ra;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (ldcg64(A + i0 + mid) <= ld64<BG>(B + j0 + k - mid - 1)) lo = mid + 1;
-        else hi = mid;
-      }
-      i = lo;
+    // merge path: the smallest i in [lo, hi) with A[i0+i] > B[j0+k-i-1] (else hi), by a 32-way
+    // search -- every lane tests one split, the ballot narrows the range 32x per round
+    uint32_t lo = k > rb ? k - rb : 0, hi = k < ra ? k : ra;
+    while (lo < hi) {
+      const uint32_t step = (hi - lo + 31) >> 5;
+      const uint32_t m = lo + uint32_t(lane) * step;
+      const bool p = m < hi && ldcg64(A + i0 + m) <= ld64<BG>(B + j0 + k - m - 1);
+      const uint32_t nt = __popc(__ballot_sync(0xFFFFFFFFu, p));  // the true lanes: a prefix
+      const uint32_t nlo = nt ? lo + (nt - 1) * step + 1 : lo;
+      const uint32_t cand = lo + nt * step;
+      hi = cand < hi ? cand : hi;
+      lo = nlo;
     }
-    i = __shfl_sync(0xFFFFFFFFu, i, 0);
+    const uint32_t i = lo;
     uint32_t j = k - i;
     if (i > 0 && j < rb && ldcg64(A + i0 + i - 1) == ld64<BG>(B + j0 + j)) ++j;
     for (uint32_t t = lane; t < i; t += 32) SA[t] = ldcg64(A + i0 + t);
@@ -253,25 +256,37 @@ __device__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t*
   return out;
 }
 
-// The working column of a warp.
-struct Col {
-  uint64_t* M[2];  // global main arrays
-  uint64_t* F[2];  // shared fresh arrays
-  uint32_t mb, nm, h;
-  uint32_t fb, nf, f0;
+// The working column of a warp (DBG: with the debug counters of option debug >= 2).
+template <bool DBG>
+struct ColT {
+  static constexpr bool dbg = DBG;
+  // tiers as (current, alternate) buffer pairs -- pointers, never indexed arrays, so that the
+  // whole struct stays in registers
+  uint64_t *Mc, *Ma;  // global main arrays
+  uint64_t *Gc, *Ga;  // global middle arrays (GCAP + FCAP entries each)
+  uint32_t ng, g0;
+  uint64_t gwin;   // per lane: G[gb][gwb + lane] (valid unless gstale)
+  uint32_t gwb;
+  bool gstale;
+  uint64_t *Fc, *Fa;  // shared fresh arrays
+  uint32_t nm, h;
+  uint32_t nf, f0;
   uint64_t mwin;   // per lane: M[mb][wb + lane] (valid unless mstale), NONE64 past the end
   uint32_t wb;     // window base
   bool mstale;
   long long fcyc;  // debug: cycles spent in flushes
   unsigned long long fent;  // debug: flushes, entries of M flushed
   unsigned fn;
-  bool dbg;
+  unsigned tpi, tpm, tpg;  // debug: take_pivot iterations, M / G window reloads
+  unsigned nsp;            // debug: R spills
+  long long rcyc, scyc;    // debug: cycles in r_insert, in spills (incl. their flushes)
   uint32_t cap;    // capacity of M[0] and M[1]
   uint64_t* spare; // the second half of a grown pair, installed after the merge that grew it
   uint64_t rv;     // per lane: entry `lane` of the register list R (NONE64 at and past nr)
   uint32_t nr, r0; // R holds positions [r0, nr) (consumed from the front)
-  __device__ uint32_t len() const { return (nm - h) + (nf - f0) + (nr - r0); }
+  __device__ uint32_t len() const { return (nm - h) + (ng - g0) + (nf - f0) + (nr - r0); }
 };
+constexpr uint32_t GCAP = 8192;  // the middle tier: F merges into G, G into M when it exceeds GCAP
 
 // The working column is M[h:] xor F[f0:] xor R[r0:nr]: three sorted tiers -- a long main array in
 // global memory, a fresh array in shared memory, and a register list of <= 32 entries (one per
@@ -283,30 +298,41 @@ struct Col {
 // Warp-collective.  The next 32 entries of M sit in a register window (one per lane), reloaded
 // with one coalesced load when h leaves it or M changes: the head of a long column is not a
 // dependent global load per cancellation.
-__device__ __forceinline__ uint64_t take_pivot(Col& c, int lane) {
+template <class CT>
+__device__ __forceinline__ uint64_t take_pivot(CT& c, int lane) {
   while (true) {
+    if (CT::dbg) ++c.tpi;
     if (c.mstale || c.h >= c.wb + 32) {
       c.wb = c.h;
-      c.mwin = c.h + lane < c.nm ? ldcg64(c.M[c.mb] + c.h + lane) : NONE64;
+      c.mwin = c.h + lane < c.nm ? ldcg64(c.Mc + c.h + lane) : NONE64;
       c.mstale = false;
+      if (CT::dbg) ++c.tpm;
+    }
+    if (c.gstale || c.g0 >= c.gwb + 32) {
+      c.gwb = c.g0;
+      c.gwin = c.g0 + lane < c.ng ? ldcg64(c.Gc + c.g0 + lane) : NONE64;
+      c.gstale = false;
+      if (CT::dbg) ++c.tpg;
     }
     const uint64_t a = __shfl_sync(0xFFFFFFFFu, c.mwin, c.h - c.wb);
-    const uint64_t b = c.f0 < c.nf ? c.F[c.fb][c.f0] : NONE64;
+    const uint64_t g = __shfl_sync(0xFFFFFFFFu, c.gwin, c.g0 - c.gwb);
+    const uint64_t b = c.f0 < c.nf ? c.Fc[c.f0] : NONE64;
     const uint64_t rr = __shfl_sync(0xFFFFFFFFu, c.rv, c.r0 & 31);
     const uint64_t r = c.r0 < c.nr ? rr : NONE64;
-    if (a == b && a != NONE64) {
-      ++c.h;
-      ++c.f0;
-    } else if (a == r && a != NONE64) {
-      ++c.h;
-      ++c.r0;
-    } else if (b == r && b != NONE64) {
-      ++c.f0;
-      ++c.r0;
-    } else {
-      const uint64_t m = a < b ? a : b;
-      return m < r ? m : r;
-    }
+    const uint64_t m1 = a < g ? a : g, m2 = b < r ? b : r;
+    const uint64_t m = m1 < m2 ? m1 : m2;
+    if (m == NONE64) return NONE64;
+    const bool ea = a == m, eg = g == m, eb = b == m, er = r == m;
+    const int k = int(ea) + int(eg) + int(eb) + int(er);
+    if (k == 1) return m;
+    // equal values in several tiers cancel in pairs: an even count removes the value, an odd
+    // count (3) leaves one copy, which is the pivot
+    int drop = k == 3 ? 2 : k;
+    if (ea && drop) ++c.h, --drop;
+    if (eg && drop) ++c.g0, --drop;
+    if (eb && drop) ++c.f0, --drop;
+    if (er && drop) ++c.r0, --drop;
+    if (k == 3) return m;
   }
 }
 
@@ -314,7 +340,8 @@ __device__ __forceinline__ uint64_t take_pivot(Col& c, int lane) {
 // (nr - r0) + nb <= 32.  Lane k < nb places B[k] by a shuffle binary search over R; every lane
 // holds all of B in registers to place its own R entry; the new list goes through `scratch`
 // (>= 40 entries).  Warp-collective.
-__device__ __forceinline__ void r_insert(Col& c, const uint64_t* B, uint32_t nb, uint64_t* scratch,
+template <class CT>
+__device__ __forceinline__ void r_insert(CT& c, const uint64_t* B, uint32_t nb, uint64_t* scratch,
                                          int lane) {
   const uint32_t live = c.nr - c.r0;
   const uint64_t y = lane < int(nb) ? B[lane] : NONE64;
@@ -436,7 +463,7 @@ __device__ __forceinline__ uint32_t spec_finish(const RP& P, const Spec& sp, int
 //  3. A streams through in windows of 256 (8 independent loads per lane): A[i] moves to
 //     i + #{non-dup t : P[t] <= i} - #{dup t : P[t] < i}, unless a dup lands on it.  A window that
 //     holds no position only shifts (one smem search per window).
-__device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a, const uint64_t* F,
+__device__ __noinline__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a, const uint64_t* F,
                                      uint32_t b, uint64_t* __restrict__ C, uint64_t* X, int lane) {
   constexpr int R = FCAP / 32;  // F entries per lane (t = lane + 32 r)
   constexpr int G = R;          // all of a lane's searches run interleaved
@@ -565,7 +592,8 @@ __device__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a,
 // moves to a larger pair carved from the pool (bump allocation; the few long columns of a launch
 // leave their old pairs behind).  False (err 2: the caller retries with a larger pool) if the
 // pool is exhausted.
-__device__ bool grow(Col& c, uint32_t need, const RP& P, int lane) {
+template <class CT>
+__device__ __forceinline__ bool grow(CT& c, uint32_t need, const RP& P, int lane) {
   if (need <= c.cap) return true;
   uint64_t ncap = uint64_t(need) * 2;
   if (ncap < uint64_t(c.cap) * 4) ncap = uint64_t(c.cap) * 4;
@@ -576,56 +604,80 @@ __device__ bool grow(Col& c, uint32_t need, const RP& P, int lane) {
     if (lane == 0) atomicOr(P.err, 2);
     return false;
   }
-  c.M[c.mb ^ 1] = P.pool + off;  // the merge's destination
+  c.Ma = P.pool + off;  // the merge's destination
   c.spare = P.pool + off + ncap;  // replaces the old M[mb] once the merge has read it
   c.cap = uint32_t(ncap);
   return true;
 }
-__device__ __forceinline__ void swap_main(Col& c) {
-  c.mb ^= 1;
-  if (c.spare) {
-    c.M[c.mb ^ 1] = c.spare;
+template <class CT>
+__device__ __forceinline__ void swap_main(CT& c) {
+  {
+    uint64_t* t = c.Mc;
+    c.Mc = c.Ma;
+    c.Ma = c.spare ? c.spare : t;
     c.spare = nullptr;
   }
 }
 
-// M <- M[h:] xor F[f0:]   (returns false on capacity overflow)
-__device__ bool flush(Col& c, const RP& P, int lane) {
-  const uint32_t na = c.nm - c.h, nb = c.nf - c.f0;
+// G <- G[g0:] xor F[f0:]; then, if G holds more than GCAP entries, M <- M[h:] xor G (F is empty
+// then, so both of its buffers are merge scratch).  Returns false on capacity overflow.
+// (The log-structured tiers keep the cost of a flush at O(|G|) -- round 1 merged F straight into
+// M, O(|M|) per flush, which dominated the longest columns: 48k-entry M, ~420k cycles a flush.)
+template <class CT>
+__device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
+  const uint32_t na = c.ng - c.g0, nb = c.nf - c.f0;
   if (nb == 0) return true;
-  if (!grow(c, na + nb, P, lane)) return false;
-  const long long t0 = c.dbg ? clock64() : 0;
-  const uint32_t n = merge_long_short(c.M[c.mb] + c.h, na, c.F[c.fb] + c.f0, nb,
-                                      c.M[c.mb ^ 1], c.F[c.fb ^ 1], lane);
-  if (c.dbg) {
+  const long long t0 = CT::dbg ? clock64() : 0;
+  uint32_t n;
+  if (na == 0) {
+    for (uint32_t i = lane; i < nb; i += 32) c.Ga[i] = c.Fc[c.f0 + i];
+    __syncwarp();
+    n = nb;
+  } else {
+    n = merge_long_short(c.Gc + c.g0, na, c.Fc + c.f0, nb, c.Ga,
+                         c.Fa, lane);
+  }
+  { uint64_t* t = c.Gc; c.Gc = c.Ga; c.Ga = t; }
+  c.ng = n;
+  c.g0 = 0;
+  c.gstale = true;
+  c.nf = c.f0 = 0;
+  if (c.ng > GCAP) {
+    const uint32_t nm = c.nm - c.h;
+    if (!grow(c, nm + c.ng, P, lane)) return false;
+    const uint32_t n2 = merge_chunked<true>(c.Mc + c.h, nm, c.Gc, c.ng, c.Ma,
+                                            c.Fc, c.Fa, lane);
+    swap_main(c);
+    c.nm = n2;
+    c.h = 0;
+    c.mstale = true;
+    c.ng = c.g0 = 0;
+    if (CT::dbg) c.fent += nm;
+  }
+  if (CT::dbg) {
     c.fcyc += clock64() - t0;
-    c.fent += na;
     ++c.fn;
   }
-  swap_main(c);
-  c.nm = n;
-  c.h = 0;
-  c.nf = c.f0 = 0;
-  c.mstale = true;
   return true;
 }
 
 constexpr uint32_t STAGE = 64;  // short global addends are staged in shared memory first
 
 // F <- F xor R, R emptied (flushing F into M first if it cannot take R).  Warp-collective.
-__device__ bool spill_r(Col& c, const RP& P, uint64_t* scratch, int lane) {
+template <class CT>
+__device__ __forceinline__ bool spill_r(CT& c, const RP& P, uint64_t* scratch, int lane) {
   const uint32_t live = c.nr - c.r0;
   if (live > 0) {
     if ((c.nf - c.f0) + live > FCAP && !flush(c, P, lane)) return false;
     if (uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr) scratch[lane - c.r0] = c.rv;
     __syncwarp();
     if (c.nf == c.f0) {
-      if (uint32_t(lane) < live) c.F[c.fb][lane] = scratch[lane];
+      if (uint32_t(lane) < live) c.Fc[lane] = scratch[lane];
       c.nf = live;
     } else {
-      c.nf = merge_symdiff<false, false>(c.F[c.fb] + c.f0, c.nf - c.f0, scratch, live,
-                                         c.F[c.fb ^ 1], lane);
-      c.fb ^= 1;
+      c.nf = merge_symdiff<false, false>(c.Fc + c.f0, c.nf - c.f0, scratch, live,
+                                         c.Fa, lane);
+      { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     }
     c.f0 = 0;
     __syncwarp();
@@ -636,8 +688,8 @@ __device__ bool spill_r(Col& c, const RP& P, uint64_t* scratch, int lane) {
 }
 
 // column += B (sorted; BG: B in global memory).  Returns false on capacity overflow.
-template <bool BG>
-__device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, int lane,
+template <bool BG, class CT>
+__device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb, const RP& P, int lane,
                            uint64_t* stage, uint64_t* small) {
   if (nb <= SMALLB) {  // into the register list
     if (BG) {
@@ -645,8 +697,17 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, 
       __syncwarp();
       B = small;
     }
-    if ((c.nr - c.r0) + nb > 32 && !spill_r(c, P, stage, lane)) return false;
+    const long long t0 = CT::dbg ? clock64() : 0;
+    if ((c.nr - c.r0) + nb > 32) {
+      if (!spill_r(c, P, stage, lane)) return false;
+      if (CT::dbg) ++c.nsp;
+    }
+    const long long t1 = CT::dbg ? clock64() : 0;
     r_insert(c, B, nb, stage, lane);
+    if (CT::dbg) {
+      c.scyc += t1 - t0;
+      c.rcyc += clock64() - t1;
+    }
     return true;
   }
   if (BG && nb <= STAGE && (c.nf - c.f0) + nb <= FCAP) {
@@ -655,40 +716,40 @@ __device__ bool add_column(Col& c, const uint64_t* B, uint32_t nb, const RP& P, 
     __syncwarp();
     const uint32_t n =
         nb <= SMALLB
-            ? merge_small(c.F[c.fb] + c.f0, c.nf - c.f0, stage, nb, c.F[c.fb ^ 1], lane)
-            : merge_symdiff<false, false>(c.F[c.fb] + c.f0, c.nf - c.f0, stage, nb,
-                                          c.F[c.fb ^ 1], lane);
-    c.fb ^= 1;
+            ? merge_small(c.Fc + c.f0, c.nf - c.f0, stage, nb, c.Fa, lane)
+            : merge_symdiff<false, false>(c.Fc + c.f0, c.nf - c.f0, stage, nb,
+                                          c.Fa, lane);
+    { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     c.nf = n;
     c.f0 = 0;
     return true;
   }
   if (!BG && nb <= SMALLB && (c.nf - c.f0) + nb <= FCAP) {
-    const uint32_t n = merge_small(c.F[c.fb] + c.f0, c.nf - c.f0, B, nb, c.F[c.fb ^ 1], lane);
-    c.fb ^= 1;
+    const uint32_t n = merge_small(c.Fc + c.f0, c.nf - c.f0, B, nb, c.Fa, lane);
+    { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     c.nf = n;
     c.f0 = 0;
     return true;
   }
   if ((c.nf - c.f0) + nb <= FCAP) {
     const uint32_t n =
-        merge_symdiff<false, BG>(c.F[c.fb] + c.f0, c.nf - c.f0, B, nb, c.F[c.fb ^ 1], lane);
-    c.fb ^= 1;
+        merge_symdiff<false, BG>(c.Fc + c.f0, c.nf - c.f0, B, nb, c.Fa, lane);
+    { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     c.nf = n;
     c.f0 = 0;
     return true;
   }
   if (!flush(c, P, lane)) return false;
   if (nb <= FCAP) {  // F is empty now: B becomes F
-    for (uint32_t i = lane; i < nb; i += 32) c.F[c.fb][i] = ld64<BG>(B + i);
+    for (uint32_t i = lane; i < nb; i += 32) c.Fc[i] = ld64<BG>(B + i);
     __syncwarp();
     c.nf = nb;
     c.f0 = 0;
     return true;
   }
   if (!grow(c, (c.nm - c.h) + nb, P, lane)) return false;
-  const uint32_t n = merge_chunked<BG>(c.M[c.mb] + c.h, c.nm - c.h, B, nb, c.M[c.mb ^ 1],
-                                       c.F[0], c.F[1], lane);
+  const uint32_t n = merge_chunked<BG>(c.Mc + c.h, c.nm - c.h, B, nb, c.Ma,
+                                       c.Fc, c.Fa, lane);
   swap_main(c);
   c.nm = n;
   c.h = 0;
@@ -726,7 +787,7 @@ __device__ __forceinline__ uint64_t warp_min(uint64_t v) {
 // children (and its bound raised with atomicMax: the children's current values are lower bounds
 // of the chunk's later minimum), and entered only if a child is still <= p.  A column found
 // > p or finished stays so (candidates only grow), so the caller resumes after a blocker.
-__device__ uint32_t find_blocker(const RP& P, uint32_t x, uint32_t j, uint64_t p, int lane) {
+__device__ __forceinline__ uint32_t find_blocker(const RP& P, uint32_t x, uint32_t j, uint64_t p, int lane) {
   uint32_t desc_end[4] = {0u, 0u, 0u, 0u};  // end of the last level-L chunk entered
   while (x < j) {
     int L = 0;
@@ -773,7 +834,7 @@ __device__ uint32_t find_blocker(const RP& P, uint32_t x, uint32_t j, uint64_t p
 // Column j is finished: publish it (after its owner entry / record, fenced) and raise the bounds
 // of its chunks -- the level-1 bound to its 32 columns' current minimum, the levels above while
 // their chunks are entirely finished.  Warp-collective.
-__device__ void finish_column(const RP& P, uint32_t j, int lane) {
+__device__ __forceinline__ void finish_column(const RP& P, uint32_t j, int lane) {
   __syncwarp();
   if (lane == 0) {
     __threadfence();
@@ -836,6 +897,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+template <bool DBG>
 __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
   extern __shared__ uint64_t k5_smem[];  // K5Smem
   uint64_t(*s_F)[2][FCAP] = reinterpret_cast<uint64_t(*)[2][FCAP]>(k5_smem);
@@ -845,13 +907,15 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
   const int wib = threadIdx.x >> 5;
   const uint32_t w = blockIdx.x * WPB + wib;
 
-  Col c;
+  ColT<DBG> c;
+  using CT = ColT<DBG>;
   uint64_t* const slot = P.work + uint64_t(w) * 2 * P.mcap;
+  uint64_t* const gslot = P.gwork + uint64_t(w) * 2 * (GCAP + FCAP);
   const SpecLane sl = spec_lane(P.g, lane);
-  c.F[0] = s_F[wib][0];
-  c.F[1] = s_F[wib][1];
-  unsigned long long adds = 0, addlen = 0, waits = 0, wcyc = 0, commits = 0;
-  uint64_t maxlen = 0;
+  c.Fc = s_F[wib][0];
+  c.Fa = s_F[wib][1];
+  unsigned adds = 0, waits = 0, maxlen = 0;
+  unsigned long long addlen = 0, wcyc = 0, commits = 0;
 
   for (;;) {
     if (ld_rlx_i32(P.err)) break;
@@ -860,21 +924,27 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     if (j == NONE32) break;
     const uint32_t seg_lo = __ldg(P.seg_off + seg);
     const uint32_t cell = rkid(P, P.cols[j]);
-    c.mb = c.fb = 0;
+
     c.h = c.f0 = c.nm = 0;
-    c.M[0] = slot;  // a column grown into the pool last time starts over in the slot
-    c.M[1] = slot + P.mcap;
+    c.Mc = slot;  // a column grown into the pool last time starts over in the slot
+    c.Ma = slot + P.mcap;
+    c.Gc = gslot;
+    c.Ga = gslot + (GCAP + FCAP);
+    c.ng = c.g0 = 0;
+    c.gstale = true;
     c.cap = P.mcap;
     c.spare = nullptr;
     c.rv = NONE64;
     c.nr = c.r0 = 0;
     c.mstale = true;
-    c.nf = coboundary(P, cell, c.F[0], lane);
-    const unsigned long long c_t0 = P.colrec ? gtimer() : 0;
-    c.dbg = P.detail;
+    c.nf = coboundary(P, cell, c.Fc, lane);
+    const unsigned long long c_t0 = DBG ? gtimer() : 0;
     c.fcyc = 0;
     c.fent = 0;
     c.fn = 0;
+    c.tpi = c.tpm = c.tpg = 0;
+    c.nsp = 0;
+    c.rcyc = c.scyc = 0;
     unsigned long long d_tp = 0, d_lk = 0, d_app = 0, d_pool = 0, d_napp = 0, d_plen = 0;
     unsigned long long c_adds = adds, c_wait = 0, c_waits = waits;
     uint32_t c_blk = NONE32;
@@ -883,14 +953,15 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     uint32_t x = seg_lo;
     bool ok = true;
     while (true) {
-      const long long q0 = c.dbg ? clock64() : 0;
+      const long long q0 = DBG ? clock64() : 0;
       const uint64_t piv = take_pivot(c, lane);
-      const long long q1 = c.dbg ? clock64() : 0;
+      const long long q1 = CT::dbg ? clock64() : 0;
       d_tp += q1 - q0;
       if (piv == NONE64) {  // zero column: essential (exact given the clearing)
         if (lane == 0) {
           const unsigned long long r = atomicAdd(P.nrec, 1ull);
           P.rec[r] = (uint64_t(cell) << 32) | NONE32;
+          atomicAdd(P.ness, 1ull);
         }
         break;
       }
@@ -906,7 +977,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       const uint64_t* add;
       uint32_t alen;
       bool glob;
-      const long long q2 = c.dbg ? clock64() : 0;
+      const long long q2 = CT::dbg ? clock64() : 0;
       d_lk += q2 - q1;
       if (tag_kind(t) == KIND_DOWN) {
         // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
@@ -931,7 +1002,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           x = b;
           ++waits;
           c_blk = b;
-          const long long t0 = clock64();
+          const long long t0 = DBG ? clock64() : 0;
           unsigned ns = 32;
           for (int it = 1;; ++it) {
             uint64_t v = 0;
@@ -957,8 +1028,10 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
             __nanosleep(ns);
             if (ns < 512) ns <<= 1;
           }
-          wcyc += clock64() - t0;
-          c_wait += clock64() - t0;
+          if (DBG) {
+            wcyc += clock64() - t0;
+            c_wait += clock64() - t0;
+          }
           if (!ok) break;
           x = b + 1;
         }
@@ -983,10 +1056,22 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           ok = false;
           break;
         }
-        // reduced column = M[h:] xor F[f0:], written straight into the pool
-        const uint32_t n = merge_chunked<false>(c.M[c.mb] + c.h, c.nm - c.h, c.F[c.fb] + c.f0,
-                                                c.nf - c.f0, P.pool + off, c.F[c.fb ^ 1],
-                                                nullptr, lane);
+        // reduced column = M[h:] xor G[g0:] xor F[f0:], written straight into the pool
+        uint32_t n;
+        if (c.ng > c.g0) {
+          if (c.nf > c.f0) {
+            ok = flush(c, P, lane);  // F into G (G may move into M)
+            if (!ok) break;
+          }
+          n = c.ng > c.g0
+                  ? merge_chunked<true>(c.Mc + c.h, c.nm - c.h, c.Gc + c.g0,
+                                        c.ng - c.g0, P.pool + off, c.Fc, c.Fa, lane)
+                  : merge_chunked<false>(c.Mc + c.h, c.nm - c.h, c.Fc + c.f0,
+                                         c.nf - c.f0, P.pool + off, c.Fa, nullptr, lane);
+        } else {
+          n = merge_chunked<false>(c.Mc + c.h, c.nm - c.h, c.Fc + c.f0, c.nf - c.f0,
+                                   P.pool + off, c.Fa, nullptr, lane);
+        }
         if (lane == 0) {
           if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
           __threadfence();
@@ -994,13 +1079,13 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           const unsigned long long r = atomicAdd(P.nrec, 1ull);
           P.rec[r] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
         }
-        ++commits;
+        if (DBG) ++commits;
         break;
       }
       addlen += c.len() + alen;
       ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
                 : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
-      if (c.dbg) {
+      if (CT::dbg) {
         const long long q3 = clock64();
         if (glob) {
           d_pool += q3 - q2;
@@ -1012,13 +1097,13 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       }
       if (!ok) break;  // pool exhausted (err 2 set): the launch is retried
       ++adds;
-      const uint64_t l = c.len();
+      const unsigned l = c.len();
       maxlen = l > maxlen ? l : maxlen;
     }
     if (!ok) break;
     finish_column(P, j, lane);
-    if (P.colrec && lane == 0) {
-      unsigned long long* R = P.colrec + 16ull * j;
+    if (DBG && lane == 0) {
+      unsigned long long* R = P.colrec + 24ull * j;
       R[0] = c_t0;
       R[1] = gtimer();
       R[2] = adds - c_adds;
@@ -1026,7 +1111,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       R[4] = waits - c_waits;
       R[5] = c_blk;
       R[6] = w;
-      if (P.detail) {
+      {
         R[8] = d_tp;
         R[9] = d_lk;
         R[10] = d_app;
@@ -1035,12 +1120,16 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         R[13] = d_plen;
         R[14] = (unsigned long long)c.fcyc;
         R[15] = ((unsigned long long)c.fn << 40) | c.fent;
+        R[7] = ((unsigned long long)c.tpi << 40) | ((unsigned long long)c.tpm << 20) | c.tpg;
+        R[16] = (unsigned long long)c.rcyc;
+        R[17] = (unsigned long long)c.scyc;
+        R[18] = c.nsp;
       }
     }
   }
   if (lane == 0) {
-    atomicAdd(P.stats + 0, waits);
-    atomicAdd(P.stats + 1, adds);
+    atomicAdd(P.stats + 0, (unsigned long long)waits);
+    atomicAdd(P.stats + 1, (unsigned long long)adds);
     atomicAdd(P.stats + 2, addlen);
     atomicMax(P.stats + 3, (unsigned long long)maxlen);
     atomicAdd(P.stats + 4, wcyc);
@@ -1121,7 +1210,7 @@ __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint
 // Debug (option debug >= 2): the chain that ends the launch -- from the last column to finish,
 // follow each column's last blocker -- and the busiest columns.
 static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, cudaStream_t s) {
-  constexpr int RW = 16;
+  constexpr int RW = 24;
   std::vector<unsigned long long> R(RW * size_t(ncols));
   CR_CUDA(cudaMemcpyAsync(R.data(), dcol, R.size() * 8, cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
@@ -1152,6 +1241,11 @@ static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, 
             (r[1] - t0) / 1e3, r[2], r[3] / 1.9e3);
     if (r[8] + r[9] + r[10] + r[11]) {
       const double a = r[2] ? double(r[2]) : 1.0, pa = double(r[2] - r[12]);
+      fprintf(stderr, "      take_pivot: %.2f iterations, %.3f M and %.3f G window reloads per call;"
+              " r_insert %.0f cycles per apparent add, spills %llu at %.0f cycles (incl. flushes)\n",
+              double(r[7] >> 40) / (a + 1), double((r[7] >> 20) & 0xFFFFF) / (a + 1),
+              double(r[7] & 0xFFFFF) / (a + 1), r[12] ? r[16] / double(r[12]) : 0.0, r[18],
+              r[18] ? r[17] / double(r[18]) : 0.0);
       fprintf(stderr, "      per add cycles: pivot %.0f lookup %.0f | apparent adds %llu at %.0f, "
               "pool adds %.0f at %.0f (avg len %.0f) | flushes %llu: %.0f cycles each, avg M %.0f\n",
               r[8] / a, r[9] / a, r[12], r[12] ? r[10] / double(r[12]) : 0.0, pa,
@@ -1223,13 +1317,14 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     int dev = 0, nsm = 0, per_sm = 0;
     CR_CUDA(cudaGetDevice(&dev));
     CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    static thread_local int attr_dev = -1;
-    if (attr_dev != dev) {
-      CR_CUDA(cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(K5_SMEM)));
-      attr_dev = dev;
+    const bool dbg = opt(OPT_DEBUG) >= 2;
+    void* const kfn = dbg ? (void*)k_reduce<true> : (void*)k_reduce<false>;
+    static thread_local int attr_dev[2] = {-1, -1};
+    if (attr_dev[dbg] != dev) {
+      CR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(K5_SMEM)));
+      attr_dev[dbg] = dev;
     }
-    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce, THREADS, K5_SMEM));
+    CR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, THREADS, K5_SMEM));
     if (per_sm < 1) throw Error{CR_EINTERNAL, "k_reduce cannot be resident"};
     per_sm = per_sm > K5_MINB ? K5_MINB : per_sm;
     if (opt(OPT_K5_BLOCKS_PER_SM) > 0 && opt(OPT_K5_BLOCKS_PER_SM) < per_sm)
@@ -1255,6 +1350,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     const uint32_t mcap = 4096u;
     unsigned long long pool_cap = 16ull * ncols + (1ull << 25);
     uint64_t* work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
+    uint64_t* gwork = ws.alloc<uint64_t>(int64_t(W) * 2 * (GCAP + FCAP));
     uint64_t* pool = nullptr;
     unsigned long long* colrec = nullptr;
     for (int attempt = 0;; ++attempt) {
@@ -1280,6 +1376,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.pool_cap = pool_cap;
       P.work = work;
       P.mcap = mcap;
+      P.gwork = gwork;
       P.lv[0] = lv;
       P.lv[1] = lv + npad;
       P.lv[2] = lv + npad + npad / 32;
@@ -1292,16 +1389,16 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.nrec = nrec;
       P.err = err;
       P.stats = stats;
+      P.ness = ctr + 13;
       P.jitter = unsigned(opt(OPT_K5_JITTER_NS));
       P.colrec = nullptr;
-      P.detail = opt(OPT_DEBUG) >= 3;
-      if (opt(OPT_DEBUG) >= 2) {
-        if (!colrec) colrec = ws.alloc<unsigned long long>(16 * int64_t(ncols));
+      if (dbg) {
+        if (!colrec) colrec = ws.alloc<unsigned long long>(24 * int64_t(ncols));
         P.colrec = colrec;
       }
       void* args[] = {&P};
       // cooperative launch: every warp resident at once (a warp may wait on any other's column)
-      CR_CUDA(cudaLaunchCooperativeKernel((void*)k_reduce, dim3(unsigned(blocks)), dim3(THREADS),
+      CR_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(unsigned(blocks)), dim3(THREADS),
                                           args, K5_SMEM, s));
       ++g_launch_count;
       const int e = read_scalar(err, s, hs);
@@ -1319,12 +1416,14 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     st.additions[d] = int64_t(hs.p[7]);
     st.addlen[d] = int64_t(hs.p[8]);
     st.maxlen[d] = int64_t(hs.p[9]);
+    st.essential[d] = int64_t(hs.p[13]);
     if (opt(OPT_DEBUG))
       fprintf(stderr, "[cr] dim %d: cols %u warps %u waits %llu adds %llu addlen %llu maxlen %llu "
               "wait-cycles/warp %.3g commits %llu pool %llu/%llu\n", d, ncols, W, hs.p[6], hs.p[7],
               hs.p[8], hs.p[9], double(hs.p[10]) / W, hs.p[11], hs.p[5], pool_cap);
     if (colrec) debug_critical_path(colrec, ncols, s);
     ws.release(work);
+    ws.release(gwork);
     ws.release(pool);
     ws.release(owninfo);
     ws.release(lv);

@@ -16,6 +16,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if "--pkgroot" in sys.argv:  # a copy of the package with a variant libcr.so (measurement only)
+    sys.path.insert(0, sys.argv[sys.argv.index("--pkgroot") + 1])
 import paper_2005_12692_b200 as cr  # noqa: E402
 from workloads import generators as gen  # noqa: E402
 
@@ -28,7 +30,7 @@ def digest(d, b, e, c):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    args = [a for a in sys.argv[1:] if not a.startswith("--") and not a.startswith("/")]
     reps = 3
     if "--reps" in sys.argv:
         reps = int(sys.argv[sys.argv.index("--reps") + 1])
