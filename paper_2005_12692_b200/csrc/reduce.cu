@@ -783,12 +783,16 @@ __device__ __forceinline__ uint64_t warp_min(uint64_t v) {
 
 // The first column i in [x, j) whose published candidate is <= p (it may still end on p, or is
 // not started), or j if there is none.  Warp-collective.  Chunks of 32^L columns whose bound
-// lv[L] exceeds p are skipped whole; a chunk whose bound does not is re-derived from its 32
-// children (and its bound raised with atomicMax: the children's current values are lower bounds
-// of the chunk's later minimum), and entered only if a child is still <= p.  A column found
+// lv[L] exceeds p are skipped whole, 32 chunks per load.  The chunks whose bound does not are
+// re-derived from their 32 children in parallel (lane = chunk, 32 independent loads each) and
+// their bounds raised with atomicMax -- the children's current values are lower bounds of the
+// chunk's later minimum -- and only the first chunk that still fails is entered.  A column found
 // > p or finished stays so (candidates only grow), so the caller resumes after a blocker.
-__device__ __forceinline__ uint32_t find_blocker(const RP& P, uint32_t x, uint32_t j, uint64_t p, int lane) {
+// *xfin: every column in [seg_lo, *xfin) is known finished; advanced while the scan starts there.
+__device__ __forceinline__ uint32_t find_blocker(const RP& P, uint32_t x, uint32_t j, uint64_t p,
+                                                 uint32_t* xfin, int lane) {
   uint32_t desc_end[4] = {0u, 0u, 0u, 0u};  // end of the last level-L chunk entered
+  bool fin_run = x == *xfin;                // the scan has seen only finished columns so far
   while (x < j) {
     int L = 0;
 #pragma unroll
@@ -796,37 +800,54 @@ __device__ __forceinline__ uint32_t find_blocker(const RP& P, uint32_t x, uint32
       const uint32_t sz = 1u << (5 * l);
       if (L == 0 && (x & (sz - 1)) == 0 && uint64_t(x) + sz <= j && x >= desc_end[l]) L = l;
     }
-    if (L == 0) {  // single columns
-      const uint32_t n = j - x < 32u ? j - x : 32u;
+    if (L == 0) {  // single columns, up to the next 32-aligned position (where chunks resume)
+      const uint32_t to_edge = 32u - (x & 31u);
+      const uint32_t n = j - x < to_edge ? j - x : to_edge;
       const uint64_t v = uint32_t(lane) < n ? ld_rlx(P.lv[0] + x + lane) : NONE64;
       const unsigned bad = __ballot_sync(0xFFFFFFFFu, v <= p);
+      const unsigned notfin = __ballot_sync(0xFFFFFFFFu, v != NONE64);
+      if (fin_run) {
+        const uint32_t nf = notfin ? uint32_t(__ffs(notfin) - 1) : n;
+        *xfin = x + (nf < n ? nf : n);
+        fin_run = !notfin;
+      }
       if (bad) return x + __ffs(bad) - 1;
       x += n;
       continue;
     }
     const int sh = 5 * L;
-    uint32_t e = x >> sh;
-    const uint32_t m = ((j - x) >> sh) < 32u ? ((j - x) >> sh) : 32u;  // whole chunks in range
-    const uint64_t v = uint32_t(lane) < m ? ld_rlx(P.lv[L] + e + lane) : NONE64;
+    const uint32_t e = x >> sh;
+    // whole chunks in range, up to the next level-(L+1) boundary (so the next step can use it)
+    const uint32_t to_edge = 32u - (e & 31u);
+    const uint32_t m = ((j - x) >> sh) < to_edge ? ((j - x) >> sh) : to_edge;
+    uint64_t v = uint32_t(lane) < m ? ld_rlx(P.lv[L] + e + lane) : NONE64;
+    if (__any_sync(0xFFFFFFFFu, v <= p)) {
+      if (v <= p) {  // re-derive this lane's chunk from its children
+        const uint64_t* ch = P.lv[L - 1] + (uint64_t(e + lane) << 5);
+        uint64_t mn = NONE64;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+          const uint64_t cv = ld_rlx(ch + k);
+          mn = cv < mn ? cv : mn;
+        }
+        if (mn > v) atomicMax(reinterpret_cast<unsigned long long*>(P.lv[L] + e + lane), mn);
+        v = mn;
+      }
+    }
     const unsigned bad = __ballot_sync(0xFFFFFFFFu, v <= p);
+    if (fin_run) {
+      const unsigned notfin = __ballot_sync(0xFFFFFFFFu, uint32_t(lane) < m && v != NONE64);
+      const uint32_t nf = notfin ? uint32_t(__ffs(notfin) - 1) : m;
+      *xfin = x + (nf << sh);
+      fin_run = !notfin;
+    }
     if (!bad) {
       x += m << sh;
       continue;
     }
     const uint32_t f = __ffs(bad) - 1;
     x += f << sh;
-    e += f;
-    const uint64_t cv = ld_rlx(P.lv[L - 1] + (uint64_t(e) << 5) + lane);
-    const unsigned cbad = __ballot_sync(0xFFFFFFFFu, cv <= p);
-    if (!cbad) {
-      const uint64_t mn = warp_min(cv);
-      if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(P.lv[L] + e), mn);
-      x += 1u << sh;
-      continue;
-    }
-    desc_end[L] = x + (1u << sh);
-    x += (__ffs(cbad) - 1) << (sh - 5);
-    if (L == 1) return x;
+    desc_end[L] = x + (1u << sh);  // enter chunk f: its 32 children are examined next
   }
   return j;
 }
@@ -920,8 +941,11 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
   for (;;) {
     if (ld_rlx_i32(P.err)) break;
     uint32_t seg;
+    const long long tf0 = DBG ? clock64() : 0;
     const uint32_t j = fetch_column(P, seg, lane);
     if (j == NONE32) break;
+    const long long tf1 = DBG ? clock64() : 0;
+    long long t_scan = 0, t_commit = 0;
     const uint32_t seg_lo = __ldg(P.seg_off + seg);
     const uint32_t cell = rkid(P, P.cols[j]);
 
@@ -951,6 +975,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     uint64_t pub = 0;      // last published candidate
     uint64_t xp = NONE64;  // the pivot the scan cursor x is valid for
     uint32_t x = seg_lo;
+    uint32_t xfin = seg_lo;  // [seg_lo, xfin): known finished
     bool ok = true;
     while (true) {
       const long long q0 = DBG ? clock64() : 0;
@@ -991,13 +1016,15 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       } else {
         // unowned pivot: wait until no earlier column of the segment can end on it
         jitter_sleep(P, j, uint32_t(adds));
-        if (xp != piv) {
-          x = seg_lo;
+        if (xp != piv) {  // a new pivot: earlier columns are checked again, past the finished ones
+          x = xfin;
           xp = piv;
         }
         bool owned = false;
         while (!owned) {
-          const uint32_t b = find_blocker(P, x, j, piv, lane);
+          const long long ts0 = DBG ? clock64() : 0;
+          const uint32_t b = find_blocker(P, x, j, piv, &xfin, lane);
+          if (DBG) t_scan += clock64() - ts0;
           if (b == j) break;
           x = b;
           ++waits;
@@ -1045,6 +1072,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           owned = __shfl_sync(0xFFFFFFFFu, o, 0) != NONE64;
         }
         if (owned) continue;  // the owner's column is added on the next pass
+        const long long tc0 = DBG ? clock64() : 0;
         ok = spill_r(c, P, s_stage[wib], lane);  // the commit reads M and F
         if (!ok) break;
         const uint32_t L = c.len();
@@ -1079,7 +1107,10 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           const unsigned long long r = atomicAdd(P.nrec, 1ull);
           P.rec[r] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
         }
-        if (DBG) ++commits;
+        if (DBG) {
+          ++commits;
+          t_commit += clock64() - tc0;
+        }
         break;
       }
       addlen += c.len() + alen;
@@ -1101,9 +1132,14 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       maxlen = l > maxlen ? l : maxlen;
     }
     if (!ok) break;
+    const long long tfin0 = DBG ? clock64() : 0;
     finish_column(P, j, lane);
     if (DBG && lane == 0) {
       unsigned long long* R = P.colrec + 24ull * j;
+      R[19] = tf1 - tf0;
+      R[20] = t_scan;
+      R[21] = t_commit;
+      R[22] = clock64() - tfin0;
       R[0] = c_t0;
       R[1] = gtimer();
       R[2] = adds - c_adds;
@@ -1253,6 +1289,23 @@ static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, 
               (r[15] >> 40) ? r[14] / double(r[15] >> 40) : 0.0,
               (r[15] >> 40) ? double(r[15] & ((1ull << 40) - 1)) / double(r[15] >> 40) : 0.0);
     }
+  }
+  {  // where the warps' time goes, summed over all columns (cycles -> ms of warp time)
+    double tot = 0, add = 0, wait = 0, fetch = 0, scan = 0, commit = 0, fin = 0;
+    for (uint32_t j = 0; j < ncols; ++j) {
+      const unsigned long long* r = &R[RW * size_t(j)];
+      tot += double(r[1] - r[0]) * 1.9;  // ns -> cycles at ~1.9 GHz
+      wait += double(r[3]);
+      fetch += double(r[19]);
+      scan += double(r[20]);
+      commit += double(r[21]);
+      fin += double(r[22]);
+      add += double(r[8] + r[9] + r[10] + r[11]);
+    }
+    fprintf(stderr, "[cr] column time (sum over columns, %% of column lifetimes): pivot+lookup+adds "
+            "%.1f%%, waits %.1f%%, scans %.1f%%, commits %.1f%%, finish %.1f%%, fetch %.3g cycles "
+            "total\n", 100 * add / tot, 100 * wait / tot, 100 * scan / tot, 100 * commit / tot,
+            100 * fin / tot, fetch);
   }
   // in-flight profile: columns started but unfinished, sampled at 20 instants
   for (int q = 1; q < 20; ++q) {
