@@ -454,20 +454,28 @@ __device__ __forceinline__ uint32_t kidx_vox(const Geom& g, uint32_t k) {
   return ((Z >> 1) * uint32_t(g.ny) + (Y >> 1)) * uint32_t(g.nx) + (X >> 1);
 }
 
+// parent of every voxel in the apparent-pair forest, and the number of basins (present vertices
+// that are not the lower cell of an apparent pair) into *nbasins
 __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                            Geom g, uint32_t* __restrict__ parent) {
-  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (vv >= g.nvox) return;
-  uint32_t v = uint32_t(vv);
-  uint32_t k = vox_kidx(g, v);
-  uint8_t t = tags[k];
-  uint32_t p = v;
-  if (births[k] != ABSENT_ORD && tag_kind(t) == KIND_UP) {
-    int d = tag_dir(t);
-    int64_t vs = (d >> 1) == 0 ? 1 : ((d >> 1) == 1 ? g.nx : g.nx * g.ny);
-    p = uint32_t(int64_t(v) + ((d & 1) ? vs : -vs));
+                            Geom g, uint32_t* __restrict__ parent, unsigned long long* nbasins) {
+  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool basin = false;
+  if (vv < g.nvox) {
+    const uint32_t v = uint32_t(vv);
+    const uint32_t k = vox_kidx(g, v);
+    const uint8_t t = tags[k];
+    const bool present = births[k] != ABSENT_ORD;
+    uint32_t p = v;
+    if (present && tag_kind(t) == KIND_UP) {
+      const int d = tag_dir(t);
+      const int64_t vs = (d >> 1) == 0 ? 1 : ((d >> 1) == 1 ? g.nx : g.nx * g.ny);
+      p = uint32_t(int64_t(v) + ((d & 1) ? vs : -vs));
+    }
+    basin = present && tag_kind(t) != KIND_UP;
+    parent[v] = p;
   }
-  parent[v] = p;
+  const unsigned mask = __ballot_sync(0xFFFFFFFFu, basin);
+  if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nbasins, (unsigned long long)__popc(mask));
 }
 
 __global__ void k_pointer_jump(uint32_t* parent, int64_t n) {
@@ -488,37 +496,63 @@ struct Cand {
   uint32_t a, b; // current component roots (voxel ids)
 };
 
+// voxel v's coordinates (one pair of divisions per voxel, not per Khalimsky cell)
+__device__ __forceinline__ void vox_xyz(const Geom& g, uint32_t v, uint32_t& x, uint32_t& y,
+                                        uint32_t& z) {
+  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
+  const uint32_t r = v / nx;
+  x = v - r * nx;
+  z = r / ny;
+  y = r - z * ny;
+}
+
+// Append up to one item per lane (warp-aggregated atomic); returns nothing.
+template <class T>
+__device__ __forceinline__ void warp_append(bool emit, const T& item, T* __restrict__ out,
+                                            unsigned* __restrict__ n) {
+  const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(n, __popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (emit) out[base + __popc(mask & ((1u << lane) - 1))] = item;
+}
+
+// Inter-basin candidate edges: residual edges whose endpoints have different roots (after
+// pointer jumping).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
 __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                            Geom g, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
                            unsigned int* __restrict__ ncand) {
-  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool emit = false;
-  Cand c;
-  if (kk < g.ncells) {
-    uint32_t k = uint32_t(kk);
-    uint32_t X, Y, Z;
-    coords_of(g, k, X, Y, Z);
-    int dim = (X & 1) + (Y & 1) + (Z & 1);
-    uint32_t bo = births[k];
-    if (dim == 1 && bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-      int64_t s = (X & 1) ? 1 : ((Y & 1) ? g.KX : g.KX * g.KY);
-      uint32_t va = kidx_vox(g, uint32_t(k - s)), vb = kidx_vox(g, uint32_t(k + s));
-      uint32_t ra = parent[va], rb = parent[vb];
-      if (ra != rb) {
-        emit = true;
-        c.key = make_key(bo, k);
-        c.a = ra;
-        c.b = rb;
+  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in = vv < g.nvox;
+  const uint32_t v = in ? uint32_t(vv) : 0u;
+  uint32_t x = 0, y = 0, z = 0;
+  if (in) vox_xyz(g, v, x, y, z);
+  const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
+  const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
+  const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
+  const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
+  const uint32_t ra = in ? parent[v] : 0u;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    bool emit = false;
+    Cand cd;
+    if (in && c[a] + 1 < n[a]) {
+      const uint32_t k = kb + ks[a];
+      const uint32_t bo = births[k];
+      if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+        const uint32_t rb = parent[v + vs[a]];
+        if (ra != rb) {
+          emit = true;
+          cd.key = make_key(bo, k);
+          cd.a = ra;
+          cd.b = rb;
+        }
       }
     }
+    warp_append(emit, cd, cand, ncand);
   }
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(ncand, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) cand[base + __popc(mask & ((1u << lane) - 1))] = c;
 }
 
 __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
@@ -553,19 +587,6 @@ __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
   }
   base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
   if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
-}
-
-__global__ void k_count_basins(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                               Geom g, const uint32_t* __restrict__ parent,
-                               unsigned long long* cnt) {
-  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool b = false;
-  if (vv < g.nvox) {
-    uint32_t k = vox_kidx(g, uint32_t(vv));
-    b = births[k] != ABSENT_ORD && tag_kind(tags[k]) != KIND_UP;
-  }
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, b);
-  if ((threadIdx.x & 31) == 0 && mask) atomicAdd(cnt, (unsigned long long)__popc(mask));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -642,18 +663,6 @@ __device__ __forceinline__ uint32_t d_find(uint32_t* parent, uint32_t v) {
   }
 }
 
-// faces of dimension D-1: the active axes all odd but one (the normal axis, returned)
-__device__ __forceinline__ int face_normal(const Geom& g, uint32_t k) {
-  int even = -1, neven = 0;
-  for (int a = 0; a < 3; ++a) {
-    if (extent_of(g, a) <= 1) continue;
-    if (!(coord_of(g, k, a) & 1)) {
-      even = a;
-      ++neven;
-    }
-  }
-  return neven == 1 ? even : -1;
-}
 
 // The same unions enumerated per voxel v (one thread): the face with normal a whose lower corner
 // is v (Khalimsky 2v_a on axis a, 2v_b + 1 on the other active axes) joins the cubes with base
@@ -703,35 +712,68 @@ __global__ void k_dual_absent_vox(const uint32_t* __restrict__ births, DualG G,
 }
 
 // absent faces join their absent sides (larger id = elder root, OMEGA the eldest)
+// Dual candidate edges: residual (D-1)-cells whose two cofaces (top cells, OMEGA past the border)
+// have different roots.  One thread per voxel v enumerates the (D-1)-cells with base voxel v (one
+// per active normal axis a: even on a, odd on the other active axes), whose cofaces are the top
+// cells with base voxels v - e_a and v.  The same threads count the dual roots into *nroots.
 __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                              DualG G, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
-                             unsigned int* __restrict__ ncand) {
-  const int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool emit = false;
-  Cand c;
-  if (kk < G.g.ncells) {
-    const uint32_t k = uint32_t(kk);
-    const uint32_t bo = births[k];
-    if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-      const int n = face_normal(G.g, k);
-      if (n >= 0) {
-        const uint32_t ra = parent[dual_side(G, k, n, 0)], rb = parent[dual_side(G, k, n, 1)];
-        if (ra != rb) {
-          emit = true;
-          c.key = ~make_key(bo, k);  // ascending ~key = decreasing key
-          c.a = ra;
-          c.b = rb;
+                             unsigned int* __restrict__ ncand, unsigned long long* nroots) {
+  const Geom& g = G.g;
+  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in = vv < g.nvox;
+  const uint32_t v = in ? uint32_t(vv) : 0u;
+  uint32_t x = 0, y = 0, z = 0;
+  if (in) vox_xyz(g, v, x, y, z);
+  const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
+  const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
+  const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
+  const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
+  // the top cell with base voxel v exists iff c_b + 1 < n_b on every active axis b
+  bool has_top = in;
+  uint32_t kt = kb;
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+    if (n[b] > 1) {
+      has_top = has_top && c[b] + 1 < n[b];
+      kt += ks[b];
+    }
+  const uint32_t rv = in ? parent[v] : 0u;  // root of the top cell at v (if it exists)
+  {
+    const bool root = has_top && rv == v;
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, root);
+    if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nroots, (unsigned long long)__popc(mask));
+    if (vv == 0 && parent[G.omega] == G.omega) atomicAdd(nroots, 1ull);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    bool emit = false;
+    Cand cd;
+    if (in && n[a] > 1) {
+      bool ok = true;
+      uint32_t k = kb;
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b != a && n[b] > 1) {
+          ok = ok && c[b] + 1 < n[b];
+          k += ks[b];
+        }
+      if (ok) {
+        const uint32_t bo = births[k];
+        if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+          const uint32_t ra = c[a] > 0 ? parent[v - vs[a]] : G.omega;
+          const uint32_t rb = c[a] + 1 < n[a] ? rv : G.omega;
+          if (ra != rb) {
+            emit = true;
+            cd.key = ~make_key(bo, k);  // ascending ~key = decreasing key
+            cd.a = ra;
+            cd.b = rb;
+          }
         }
       }
     }
+    warp_append(emit, cd, cand, ncand);
   }
-  const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  const int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(ncand, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) cand[base + __popc(mask & ((1u << lane) - 1))] = c;
 }
 
 // key of a dual root (larger = elder): OMEGA the largest, absent top cells next
@@ -743,32 +785,6 @@ __device__ __forceinline__ uint64_t dual_root_key(const uint32_t* __restrict__ b
   return make_key(births[k], k);
 }
 
-__global__ void k_dual_roots(const uint32_t* __restrict__ births, DualG G,
-                             const uint32_t* __restrict__ parent, uint64_t* rootkey, unsigned* nroot,
-                             unsigned long long* count) {
-  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool emit = false;
-  uint64_t key = 0;
-  if (vv <= G.omega) {
-    const uint32_t v = uint32_t(vv);
-    uint32_t k;
-    if (parent[v] == v && (v == G.omega || top_of_voxel(G.g, v, k))) {
-      emit = true;
-      key = ~dual_root_key(births, G, v);  // ascending = elder first
-    }
-  }
-  const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  const int lane = threadIdx.x & 31;
-  if (count) {
-    if (lane == __ffs(mask) - 1) atomicAdd(count, (unsigned long long)__popc(mask));
-    return;
-  }
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(nroot, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) rootkey[base + __popc(mask & ((1u << lane) - 1))] = key;
-}
 
 // dual record of the edge with complemented key ek whose younger root has key ry
 __device__ __forceinline__ uint64_t dual_record(uint64_t ek, uint64_t ry) {
@@ -950,9 +966,8 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   CR_CHECK_LAUNCH();
   Cand* cand = ws.alloc<Cand>(st.cells[d] + 1);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt);
-  k_dual_edges<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, G, parent, cand, ncand);
-  CR_CHECK_LAUNCH();
-  k_dual_roots<<<grid_for(nv, B), B, 0, s>>>(S.births, G, parent, nullptr, nullptr, cnt + 1);
+  k_dual_edges<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
+                                                  cnt + 1);
   CR_CHECK_LAUNCH();
   CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
@@ -1115,11 +1130,9 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
 
   // ---- H0
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);
-  k_h0_parent<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent);
+  k_h0_parent<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
   CR_CHECK_LAUNCH();
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
-  CR_CHECK_LAUNCH();
-  k_count_basins<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
   CR_CHECK_LAUNCH();
 
   // NaN check + counts (one sync)
@@ -1135,7 +1148,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
 
   Cand* cand = ws.alloc<Cand>(nedges);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
-  k_h0_edges<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
+  k_h0_edges<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
   CR_CHECK_LAUNCH();
 
   // vertex records: at most one per finite vertex
@@ -1147,9 +1160,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 20);  // cnt[20], cnt[21]: zeroed at the start
   mm_rounds<false>(cand, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
                    DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ctl, ws);
-  // flatten once more so that roots are exact, then essential classes
-  k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
-  CR_CHECK_LAUNCH();
+  // essential classes: the final roots (parent[v] == v holds exactly for them; no flattening)
   k_h0_essential<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
                                                     cnt + 22);
   CR_CHECK_LAUNCH();

@@ -1184,30 +1184,54 @@ __global__ void k_levels_init(uint64_t* lv0, uint64_t* lv1, uint64_t* lv2, uint6
   if (i < (npad >> 15)) lv3[i] = (uint64_t(i) << 15) < ncols ? 0ull : NONE64;
 }
 
+// Columns of dimension d: finite residual d-cells (not apparent, not cleared), as keys.  One thread
+// per voxel v enumerates the d-cells with base voxel v (odd Khalimsky offsets on d of the axes).
 __global__ void k_collect_columns(const uint32_t* __restrict__ births,
                                   const uint8_t* __restrict__ tags, Geom g, int d,
                                   uint64_t* __restrict__ cols, unsigned* __restrict__ ncols) {
-  int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool emit = false;
-  uint64_t key = 0;
-  if (kk < g.ncells) {
-    uint32_t k = uint32_t(kk);
-    uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-    uint32_t X = k % KX, r = k / KX, Y = r % KY, Z = r / KY;
-    int dim = (X & 1) + (Y & 1) + (Z & 1);
-    uint32_t b = births[k];
-    if (dim == d && b != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-      emit = true;
-      key = make_key(b, k);
-    }
+  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in = vv < g.nvox;
+  uint32_t c[3] = {0u, 0u, 0u};
+  if (in) {
+    const uint32_t v = uint32_t(vv), nx = uint32_t(g.nx), ny = uint32_t(g.ny);
+    const uint32_t r = v / nx;
+    c[0] = v - r * nx;
+    c[2] = r / ny;
+    c[1] = r - c[2] * ny;
   }
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(ncols, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) cols[base + __popc(mask & ((1u << lane) - 1))] = key;
+  const uint32_t n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
+  const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
+  const uint32_t kb = (2 * c[2] * uint32_t(g.KY) + 2 * c[1]) * uint32_t(g.KX) + 2 * c[0];
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int t = 1; t < 8; ++t) {  // cell type: bit a set = odd along axis a
+    if (__popc(t) != d) continue;
+    bool emit = false;
+    uint64_t key = 0;
+    if (in) {
+      bool ok = true;
+      uint32_t k = kb;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (t >> a & 1) {
+          ok = ok && c[a] + 1 < n[a];
+          k += ks[a];
+        }
+      if (ok) {
+        const uint32_t b = births[k];
+        if (b != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+          emit = true;
+          key = make_key(b, k);
+        }
+      }
+    }
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
+    if (!mask) continue;
+    unsigned base = 0;
+    if (lane == __ffs(mask) - 1) base = atomicAdd(ncols, __popc(mask));
+    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+    if (emit) cols[base + __popc(mask & ((1u << lane) - 1))] = key;
+  }
 }
 
 __global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32_t seg_cells,
@@ -1331,7 +1355,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
   unsigned long long* ctr = ws.alloc<unsigned long long>(16);
   CR_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
   uint64_t* cols = ws.alloc<uint64_t>(nd + 1);
-  k_collect_columns<<<grid_for(g.ncells, B), B, 0, s>>>(S.births, S.tags, g, d, cols,
+  k_collect_columns<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, d, cols,
                                                         reinterpret_cast<unsigned*>(ctr));
   CR_CHECK_LAUNCH();
   const unsigned ncols = read_scalar(reinterpret_cast<unsigned*>(ctr), s, hs);
