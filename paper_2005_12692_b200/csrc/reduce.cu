@@ -858,11 +858,12 @@ __device__ __forceinline__ uint32_t find_blocker(const RP& P, uint32_t x, uint32
 __device__ __forceinline__ void finish_column(const RP& P, uint32_t j, int lane) {
   __syncwarp();
   if (lane == 0) {
-    __threadfence();
+    __threadfence();  // the owner entry and the record are visible before "finished"
     st_rlx(P.lv[0] + j, NONE64);
-    __threadfence();
   }
   __syncwarp();
+  // (no fence before reading the siblings: a bound left stale by two columns finishing at once
+  // only costs a later scanner one re-derivation, never correctness)
   uint32_t e = j;
   for (int L = 1; L <= 3; ++L) {
     e >>= 5;
@@ -883,7 +884,7 @@ __device__ __forceinline__ void finish_column(const RP& P, uint32_t j, int lane)
 __device__ __forceinline__ uint32_t fetch_column(const RP& P, uint32_t& seg, int lane) {
   uint32_t j = NONE32, s = 0;
   if (lane == 0) {
-    const unsigned long long c = atomicAdd(P.fetch, 1ull);
+    const unsigned long long c = P.nseg > 1 ? atomicAdd(P.fetch, 1ull) : 0ull;
     for (uint32_t t = 0; t < P.nseg; ++t) {
       s = uint32_t((c + t) % P.nseg);
       const uint32_t lo = __ldg(P.seg_off + s), hi = __ldg(P.seg_off + s + 1);
@@ -1086,7 +1087,11 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         }
         // reduced column = M[h:] xor G[g0:] xor F[f0:], written straight into the pool
         uint32_t n;
-        if (c.ng > c.g0) {
+        if (c.nm == c.h && c.ng == c.g0) {  // held in F alone (most columns): a copy
+          n = c.nf - c.f0;
+          for (uint32_t i = lane; i < n; i += 32) P.pool[off + i] = c.Fc[c.f0 + i];
+          __syncwarp();
+        } else if (c.ng > c.g0) {
           if (c.nf > c.f0) {
             ok = flush(c, P, lane);  // F into G (G may move into M)
             if (!ok) break;
