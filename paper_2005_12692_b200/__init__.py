@@ -236,9 +236,10 @@ def barcodes(image, maxdim: int = 1, cells: bool = False, capacity: int | None =
         pairs, cbuf = out
         cap = pairs.shape[0]
     n = ctypes.c_int64(0)
-    st = _lib.cr_barcodes(image.data_ptr(), _shape(shape), len(shape), int(maxdim), pairs.data_ptr(),
-                          cbuf.data_ptr() if cbuf is not None else None, cap, ctypes.byref(n),
-                          _stream_ptr(torch, image.device))
+    with torch.cuda.device(image.device):  # the library runs on the current device
+        st = _lib.cr_barcodes(image.data_ptr(), _shape(shape), len(shape), int(maxdim), pairs.data_ptr(),
+                              cbuf.data_ptr() if cbuf is not None else None, cap, ctypes.byref(n),
+                              _stream_ptr(torch, image.device))
     _check(st)
     m = int(n.value)
     return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None)
@@ -285,10 +286,11 @@ def barcodes_batched(images, maxdim: int = 1, cells: bool = False, capacity: int
     cbuf = torch.empty((max(cap, 1),), dtype=torch.int32, device=images.device) if cells else None
     offsets = torch.empty((B + 1,), dtype=torch.int64, device=images.device)
     n = ctypes.c_int64(0)
-    st = _lib.cr_barcodes_batched(images.data_ptr(), B, _shape(shape), len(shape), int(maxdim),
-                                  pairs.data_ptr(), cbuf.data_ptr() if cbuf is not None else None,
-                                  cap, offsets.data_ptr(), ctypes.byref(n),
-                                  _stream_ptr(torch, images.device))
+    with torch.cuda.device(images.device):  # the library runs on the current device
+        st = _lib.cr_barcodes_batched(images.data_ptr(), B, _shape(shape), len(shape), int(maxdim),
+                                      pairs.data_ptr(), cbuf.data_ptr() if cbuf is not None else None,
+                                      cap, offsets.data_ptr(), ctypes.byref(n),
+                                      _stream_ptr(torch, images.device))
     _check(st)
     m = int(n.value)
     return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None), offsets
@@ -330,8 +332,9 @@ def pairing(image):
     image = image.contiguous()
     shape = tuple(image.shape)
     part = torch.empty((num_cells(shape),), dtype=torch.int32, device=image.device)
-    st = _lib.cr_pairing(image.data_ptr(), _shape(shape), len(shape), part.data_ptr(),
-                         _stream_ptr(torch, image.device))
+    with torch.cuda.device(image.device):  # the library runs on the current device
+        st = _lib.cr_pairing(image.data_ptr(), _shape(shape), len(shape), part.data_ptr(),
+                             _stream_ptr(torch, image.device))
     _check(st)
     return part
 
@@ -345,8 +348,9 @@ def death_cells(image, birth_cells):
     birth_cells = birth_cells.contiguous()
     n = int(birth_cells.numel())
     out = torch.empty((max(n, 1),), dtype=torch.int32, device=image.device)
-    st = _lib.cr_death_cells(image.data_ptr(), _shape(shape), len(shape), birth_cells.data_ptr(), n,
-                             out.data_ptr(), _stream_ptr(torch, image.device))
+    with torch.cuda.device(image.device):  # the library runs on the current device
+        st = _lib.cr_death_cells(image.data_ptr(), _shape(shape), len(shape), birth_cells.data_ptr(), n,
+                                 out.data_ptr(), _stream_ptr(torch, image.device))
     _check(st)
     return out[:n]
 
@@ -376,8 +380,9 @@ def lifetime_image(images, maxdim: int = 2, inf_value: float | None = None, batc
     D = sum(1 for v in shape if v > 1)
     C = 2 + min(int(maxdim), max(D - 1, 0))
     out = torch.empty((B, C) + shape, dtype=torch.float32, device=images.device)
-    st = _lib.cr_lifetime_image(images.data_ptr(), B, _shape(shape), len(shape), int(maxdim),
-                                float(inf_value), out.data_ptr(), _stream_ptr(torch, images.device))
+    with torch.cuda.device(images.device):  # the library runs on the current device
+        st = _lib.cr_lifetime_image(images.data_ptr(), B, _shape(shape), len(shape), int(maxdim),
+                                    float(inf_value), out.data_ptr(), _stream_ptr(torch, images.device))
     _check(st)
     return out if batched else out[0]
 
@@ -393,9 +398,10 @@ def barcodes_topdim(image, cells: bool = False) -> "Barcode":
     pairs = torch.empty((cap, 3), dtype=torch.int32, device=image.device)
     cbuf = torch.empty((cap,), dtype=torch.int32, device=image.device) if cells else None
     n = ctypes.c_int64(0)
-    st = _lib.cr_barcodes_topdim(image.data_ptr(), _shape(shape), len(shape), pairs.data_ptr(),
-                                 cbuf.data_ptr() if cbuf is not None else None, cap,
-                                 ctypes.byref(n), _stream_ptr(torch, image.device))
+    with torch.cuda.device(image.device):  # the library runs on the current device
+        st = _lib.cr_barcodes_topdim(image.data_ptr(), _shape(shape), len(shape), pairs.data_ptr(),
+                                     cbuf.data_ptr() if cbuf is not None else None, cap,
+                                     ctypes.byref(n), _stream_ptr(torch, image.device))
     _check(st)
     m = int(n.value)
     return Barcode(pairs[:m], cbuf[:m] if cbuf is not None else None)
@@ -426,9 +432,10 @@ def barcodes_f64(image, maxdim: int = 1, cells: bool = False,
     raw = torch.empty((max(cap, 1), 3), dtype=torch.float64, device=image.device)  # cr_pair64
     cbuf = torch.empty((max(cap, 1),), dtype=torch.int32, device=image.device) if cells else None
     n = ctypes.c_int64(0)
-    st = _lib.cr_barcodes_f64(image.data_ptr(), _shape(shape), len(shape), int(maxdim),
-                              raw.data_ptr(), cbuf.data_ptr() if cbuf is not None else None, cap,
-                              ctypes.byref(n), _stream_ptr(torch, image.device))
+    with torch.cuda.device(image.device):  # the library runs on the current device
+        st = _lib.cr_barcodes_f64(image.data_ptr(), _shape(shape), len(shape), int(maxdim),
+                                  raw.data_ptr(), cbuf.data_ptr() if cbuf is not None else None, cap,
+                                  ctypes.byref(n), _stream_ptr(torch, image.device))
     _check(st)
     m = int(n.value)
     raw = raw[:m]

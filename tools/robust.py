@@ -7,19 +7,13 @@ import paper_2005_12692_b200 as cr
 import oracle
 from workloads import generators as gen
 
-def gpu(img, md, **env):
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
+def gpu(img, md, **opts):
+    with cr.options(**opts):
         t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
         t0 = time.time()
         d, b, e, c = cr.barcodes(t, md, cells=True).numpy()
         torch.cuda.synchronize()
         return (d, b, e, c), time.time() - t0, cr.last_stats()
-    finally:
-        for k, v in old.items():
-            if v is None: os.environ.pop(k, None)
-            else: os.environ[k] = v
 
 def same(a, b):
     return all(np.array_equal(np.asarray(x).view(np.uint32) if np.asarray(x).dtype == np.float32 else x,
@@ -46,9 +40,9 @@ for name, img, md, ref in cases:
         ok = same(g, (o.dim, o.birth, o.death, o.cell))
         msg += f" | oracle {time.time()-t0:.1f} s equal={ok}"
     elif ref == "tree":
-        h, _, st2 = gpu(img, md, CR_1D_TREE="1")
+        h, _, st2 = gpu(img, md, **{"1d_tree": 1})
         msg += f" | tree path {st2['path']} equal={same(g, h)}"
     elif ref == "reduce":
-        h, dt2, _ = gpu(img, md, CR_TOP_REDUCE="1")
+        h, dt2, _ = gpu(img, md, top_reduce=1)
         msg += f" | top by reduction ({dt2*1e3:.1f} ms) equal={same(g, h)}"
     print(msg, flush=True)
