@@ -413,17 +413,8 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
       }
     unsigned nk = read_scalar(nkeep, s, hs);
     // sort (image, dim, local kidx) with values
-    if (nk > 1) {
-      uint64_t* k2 = ws.alloc<uint64_t>(nk);
-      uint64_t* v2 = ws.alloc<uint64_t>(nk);
-      cub::DoubleBuffer<uint64_t> dk(keys, k2), dv(vals, v2);
-      size_t tmp = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(nk), 0, 64, s));
-      void* t = ws.alloc_bytes(tmp);
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(nk), 0, 64, s));
-      keys = dk.Current();
-      vals = dv.Current();
-    }
+    if (nk > 1)  // key = (image << 34) | (dim << 32) | local kidx: 34 + bits(batch) significant bits
+      radix_sort<uint64_t, uint64_t>(keys, vals, nk, 0, 34 + bits_for(uint64_t(batch)), false, ws);
     unsigned* count = ws.alloc<unsigned>(batch + 1);
     unsigned* scan = ws.alloc<unsigned>(batch + 1);
     CR_CUDA(cudaMemsetAsync(count, 0, (batch + 1) * sizeof(unsigned), s));

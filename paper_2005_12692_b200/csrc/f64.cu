@@ -144,25 +144,20 @@ extern "C" cr_status cr_barcodes_f64(const double* image, const int64_t* shape, 
     if (hf[1]) {  // rank case
       if (n > MAX_RANKS) return CR_EINVAL;
       uint64_t* k0 = ws.alloc<uint64_t>(n);
-      uint64_t* k1 = ws.alloc<uint64_t>(n);
       uint32_t* i0 = ws.alloc<uint32_t>(n);
-      uint32_t* i1 = ws.alloc<uint32_t>(n);
       uint32_t* flag = ws.alloc<uint32_t>(n);
       uint32_t* incl = ws.alloc<uint32_t>(n);
       uniq = ws.alloc<double>(n);
       k_f64_keys<<<grid_for(n, T), T, 0, s>>>(image, n, k0, i0);
       CR_CHECK_LAUNCH();
-      cub::DoubleBuffer<uint64_t> kb(k0, k1);
-      cub::DoubleBuffer<uint32_t> vb(i0, i1);
-      size_t tmp_bytes = 0, scan_bytes = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, n, 0, 64, s));
+      radix_sort<uint64_t, uint32_t>(k0, i0, n, 0, 64, false, ws);
+      size_t scan_bytes = 0;
       CR_CUDA(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, flag, incl, n, s));
-      void* tmp = ws.alloc_bytes(tmp_bytes > scan_bytes ? tmp_bytes : scan_bytes);
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, n, 0, 64, s));
-      k_f64_runs<<<grid_for(n, T), T, 0, s>>>(kb.Current(), n, flag);
+      void* tmp = ws.alloc_bytes(scan_bytes);
+      k_f64_runs<<<grid_for(n, T), T, 0, s>>>(k0, n, flag);
       CR_CHECK_LAUNCH();
       CR_CUDA(cub::DeviceScan::InclusiveSum(tmp, scan_bytes, flag, incl, n, s));
-      k_f64_scatter<<<grid_for(n, T), T, 0, s>>>(kb.Current(), vb.Current(), flag, incl, n, surr,
+      k_f64_scatter<<<grid_for(n, T), T, 0, s>>>(k0, i0, flag, incl, n, surr,
                                                  uniq);
       CR_CHECK_LAUNCH();
     }

@@ -74,9 +74,19 @@ int64_t barcodes_core(const float* image, const Geom& g, int maxdim, cr_pair* ou
                       HostScalars& hs, cr_stats& st);
 void set_last_stats(const cr_stats& st);
 
-// Device-wide helpers (util.cu).
+// Hand-written stable LSD radix sort (sort.cu) over key bits [begin_bit, end_bit), values optional
+// (vals == nullptr); instantiated for (u64, u64), (u64, u32), (u32, u64).
+template <class K, class V>
+void radix_sort(K* keys, V* vals, int64_t n, int begin_bit, int end_bit, bool descending,
+                Workspace& ws);
 void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws,
                    int begin_bit = 0);
+inline int bits_for(uint64_t v) {  // significant bits of values < v (v >= 1)
+  int b = 0;
+  while (b < 64 && (uint64_t(1) << b) < v) ++b;
+  return b;
+}
+// Device-wide helpers (util.cu).
 void exclusive_sum_u32(const uint32_t* in, uint32_t* out, int64_t n, Workspace& ws);
 
 }  // namespace cr

@@ -1366,29 +1366,26 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
   const unsigned ncols = read_scalar(reinterpret_cast<unsigned*>(ctr), s, hs);
   st.columns[d] = ncols;
   if (ncols > 0) {
-    sort_keys_u64(cols, ncols, /*descending=*/true, 64, ws);
+    // decreasing (ord << 32 | kidx): kidx has bits_for(ncells) significant bits, ord all 32 --
+    // two stable passes over [0, kb) then [32, 64) skip the zero bits in between
+    {
+      const int kb = bits_for(uint64_t(g.ncells));
+      radix_sort<uint64_t, uint32_t>(cols, nullptr, ncols, 0, kb, /*descending=*/true, ws);
+      radix_sort<uint64_t, uint32_t>(cols, nullptr, ncols, 32, 64, /*descending=*/true, ws);
+    }
     unsigned nseg = 1;
     uint32_t* seg_off = nullptr;
     if (S.seg_cells) {
       // batched images: group the columns by image (stable, so each image keeps its decreasing
       // key order); images are independent complexes, so their relative order is immaterial
       uint32_t* segk = ws.alloc<uint32_t>(ncols);
-      uint32_t* segk2 = ws.alloc<uint32_t>(ncols);
-      uint64_t* cols2 = ws.alloc<uint64_t>(ncols);
       k_seg_keys<<<grid_for(ncols, B), B, 0, s>>>(cols, ncols, S.seg_cells, segk);
       CR_CHECK_LAUNCH();
-      cub::DoubleBuffer<uint32_t> dk(segk, segk2);
-      cub::DoubleBuffer<uint64_t> dv(cols, cols2);
-      size_t tmp = 0;
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(ncols), 0, 32, s));
-      void* t = ws.alloc_bytes(tmp);
-      CR_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, int(ncols), 0, 32, s));
-      if (dv.Current() != cols)
-        CR_CUDA(cudaMemcpyAsync(cols, dv.Current(), ncols * sizeof(uint64_t),
-                                cudaMemcpyDeviceToDevice, s));
+      const uint64_t nimg = (uint64_t(g.ncells) + S.seg_cells - 1) / S.seg_cells;
+      radix_sort<uint32_t, uint64_t>(segk, cols, ncols, 0, bits_for(nimg), false, ws);
       nseg = unsigned((uint64_t(g.ncells) + S.seg_cells - 1) / S.seg_cells);
       seg_off = ws.alloc<uint32_t>(nseg + 1);
-      k_seg_offsets<<<grid_for(nseg + 1, B), B, 0, s>>>(dk.Current(), ncols, nseg, seg_off);
+      k_seg_offsets<<<grid_for(nseg + 1, B), B, 0, s>>>(segk, ncols, nseg, seg_off);
       CR_CHECK_LAUNCH();
     } else {
       seg_off = ws.alloc<uint32_t>(2);
@@ -1396,6 +1393,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       CR_CHECK_LAUNCH();
     }
 
+    prof_mark(s, d == 1 ? "sort_d1" : (d == 2 ? "sort_d2" : "sort_d3"));  // collect + sort
     int dev = 0, nsm = 0, per_sm = 0;
     CR_CUDA(cudaGetDevice(&dev));
     CR_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

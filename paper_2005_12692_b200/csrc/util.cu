@@ -267,28 +267,6 @@ HostScalars::HostScalars() : p(nullptr) {
 }
 HostScalars::~HostScalars() {}
 
-void sort_keys_u64(uint64_t* keys, int64_t n, bool descending, int end_bit, Workspace& ws,
-                   int begin_bit) {
-  if (n <= 1) return;
-  uint64_t* alt = ws.alloc<uint64_t>(n);
-  cub::DoubleBuffer<uint64_t> db(keys, alt);
-  size_t tmp = 0;
-  if (descending)
-    CR_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
-  else
-    CR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
-  void* t = ws.alloc_bytes(tmp);
-  if (descending)
-    CR_CUDA(cub::DeviceRadixSort::SortKeysDescending(t, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
-  else
-    CR_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, db, int(n), begin_bit, end_bit, ws.stream()));
-  if (db.Current() != keys)
-    CR_CUDA(cudaMemcpyAsync(keys, db.Current(), n * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
-                            ws.stream()));
-  ws.release(t);
-  ws.release(alt);
-}
-
 void exclusive_sum_u32(const uint32_t* in, uint32_t* out, int64_t n, Workspace& ws) {
   if (n <= 0) return;
   size_t tmp = 0;
