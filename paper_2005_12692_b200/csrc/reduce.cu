@@ -282,6 +282,7 @@ struct ColT {
   long long rcyc, scyc;    // debug: cycles in r_insert, in spills (incl. their flushes)
   uint32_t cap;    // capacity of M[0] and M[1]
   uint64_t* spare; // the second half of a grown pair, installed after the merge that grew it
+  uint32_t pt;     // tier of the pivot take_pivot returned: 0 M, 1 G, 2 F, 3 R
   uint64_t rv;     // per lane: entry `lane` of the register list R (NONE64 at and past nr)
   uint32_t nr, r0; // R holds positions [r0, nr) (consumed from the front)
   __device__ uint32_t len() const { return (nm - h) + (ng - g0) + (nf - f0) + (nr - r0); }
@@ -324,9 +325,10 @@ __device__ __forceinline__ uint64_t take_pivot(CT& c, int lane) {
     if (m == NONE64) return NONE64;
     const bool ea = a == m, eg = g == m, eb = b == m, er = r == m;
     const int k = int(ea) + int(eg) + int(eb) + int(er);
-    if (k == 1) return m;
     // equal values in several tiers cancel in pairs: an even count removes the value, an odd
-    // count (3) leaves one copy, which is the pivot
+    // count (3) leaves one copy, which is the pivot (c.pt: its tier, the last one matching)
+    c.pt = er ? 3u : (eb ? 2u : (eg ? 1u : 0u));
+    if (k == 1) return m;
     int drop = k == 3 ? 2 : k;
     if (ea && drop) ++c.h, --drop;
     if (eg && drop) ++c.g0, --drop;
@@ -334,6 +336,17 @@ __device__ __forceinline__ uint64_t take_pivot(CT& c, int lane) {
     if (er && drop) ++c.r0, --drop;
     if (k == 3) return m;
   }
+}
+
+// Remove the pivot take_pivot returned (it is the head of tier c.pt): adding a column whose first
+// entry is the pivot then adds only the rest of it -- one take_pivot iteration and one insertion
+// fewer per addition than letting the two copies cancel at the heads.
+template <class CT>
+__device__ __forceinline__ void consume_pivot(CT& c) {
+  if (c.pt == 0) ++c.h;
+  else if (c.pt == 1) ++c.g0;
+  else if (c.pt == 2) ++c.f0;
+  else ++c.r0;
 }
 
 // R <- R[r0:nr] xor B for a sorted B of nb <= SMALLB entries in shared memory, with
@@ -440,12 +453,12 @@ __device__ __forceinline__ Spec spec_issue(const RP& P, const SpecLane& L, uint3
   }
   return r;
 }
-// delta(s') sorted ascending into dst (<= 6 entries) for the partner direction dir; warp-collective.
+// delta(s') minus the pivot, sorted ascending into dst (<= 5 entries) for the partner direction
+// dir; warp-collective.
 __device__ __forceinline__ uint32_t spec_finish(const RP& P, const Spec& sp, int dir, uint64_t piv,
                                                 uint64_t* dst, int lane) {
   uint64_t key = NONE64;
   if (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD) key = rkey(P, sp.birth, sp.cell);
-  if (lane == 31) key = piv;
   const unsigned vm = __ballot_sync(0xFFFFFFFFu, key != NONE64);
   int rank = 0;
   for (unsigned m = vm; m; m &= m - 1) rank += __shfl_sync(0xFFFFFFFFu, key, __ffs(m) - 1) < key;
@@ -1010,10 +1023,13 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         alen = spec_finish(P, sp, tag_dir(t), piv, s_small[wib], lane);
         add = s_small[wib];
         glob = false;
+        consume_pivot(c);
       } else if (oi != NONE64) {
-        add = P.pool + (oi >> OI_LEN_BITS);
-        alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1));
+        // the owner's reduced column starts with the pivot itself
+        add = P.pool + (oi >> OI_LEN_BITS) + 1;
+        alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1)) - 1;
         glob = true;
+        consume_pivot(c);
       } else {
         // unowned pivot: wait until no earlier column of the segment can end on it
         jitter_sleep(P, j, uint32_t(adds));
@@ -1119,8 +1135,9 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         break;
       }
       addlen += c.len() + alen;
-      ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
-                : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
+      if (alen)
+        ok = glob ? add_column<true>(c, add, alen, P, lane, s_stage[wib], s_small[wib])
+                  : add_column<false>(c, add, alen, P, lane, s_stage[wib], s_small[wib]);
       if (CT::dbg) {
         const long long q3 = clock64();
         if (glob) {
