@@ -674,7 +674,7 @@ __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
   return true;
 }
 
-constexpr uint32_t STAGE = 64;  // short global addends are staged in shared memory first
+constexpr uint32_t STAGE = 64;  // global addends are staged in shared memory, STAGE entries at a time
 
 // F <- F xor R, R emptied (flushing F into M first if it cannot take R).  Warp-collective.
 template <class CT>
@@ -723,18 +723,21 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
     }
     return true;
   }
-  if (BG && nb <= STAGE && (c.nf - c.f0) + nb <= FCAP) {
-    // one coalesced load instead of a dependent global binary search per F entry
-    for (uint32_t i = lane; i < nb; i += 32) stage[i] = ldcg64(B + i);
-    __syncwarp();
-    const uint32_t n =
-        nb <= SMALLB
-            ? merge_small(c.Fc + c.f0, c.nf - c.f0, stage, nb, c.Fa, lane)
-            : merge_symdiff<false, false>(c.Fc + c.f0, c.nf - c.f0, stage, nb,
-                                          c.Fa, lane);
-    { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
-    c.nf = n;
-    c.f0 = 0;
+  if (BG && (c.nf - c.f0) + nb <= FCAP) {
+    // STAGE entries at a time: one coalesced load each instead of a dependent global binary
+    // search per F entry (F xor B = F xor B[0:64] xor B[64:128] ...)
+    for (uint32_t b0 = 0; b0 < nb; b0 += STAGE) {
+      const uint32_t m = nb - b0 < STAGE ? nb - b0 : STAGE;
+      for (uint32_t i = lane; i < m; i += 32) stage[i] = ldcg64(B + b0 + i);
+      __syncwarp();
+      const uint32_t n =
+          m <= SMALLB
+              ? merge_small(c.Fc + c.f0, c.nf - c.f0, stage, m, c.Fa, lane)
+              : merge_symdiff<false, false>(c.Fc + c.f0, c.nf - c.f0, stage, m, c.Fa, lane);
+      { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
+      c.nf = n;
+      c.f0 = 0;
+    }
     return true;
   }
   if (!BG && nb <= SMALLB && (c.nf - c.f0) + nb <= FCAP) {
