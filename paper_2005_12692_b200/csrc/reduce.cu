@@ -1050,30 +1050,25 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           ++waits;
           c_blk = b;
           const long long t0 = DBG ? clock64() : 0;
-          unsigned ns = 32;
+          // Waiting must stay cheap: 32 warps share an SM's issue slots with the working ones.
+          // All lanes read the same word (one transaction, the same value in every lane: no
+          // shuffles); the owner entry and the error flag are looked at every 8th try; the
+          // back-off grows to 2 us.
+          unsigned ns = 64;
           for (int it = 1;; ++it) {
-            uint64_t v = 0;
-            int e = 0;
-            if (lane == 0) {
-              v = ld_rlx(P.lv[0] + b);
-              e = ld_rlx_i32(P.err);
-            }
-            v = __shfl_sync(0xFFFFFFFFu, v, 0);
-            if (__shfl_sync(0xFFFFFFFFu, e, 0)) {
-              ok = false;
-              break;
-            }
-            if (v > piv) break;
-            if ((it & 3) == 0) {  // an earlier column may commit this very pivot meanwhile
-              uint64_t o = 0;
-              if (lane == 0) o = ld_rlx(P.owninfo + pk);
-              if (__shfl_sync(0xFFFFFFFFu, o, 0) != NONE64) {
+            if (ld_rlx(P.lv[0] + b) > piv) break;
+            if ((it & 7) == 0) {
+              if (ld_rlx_i32(P.err)) {
+                ok = false;
+                break;
+              }
+              if (ld_rlx(P.owninfo + pk) != NONE64) {  // an earlier column committed this pivot
                 owned = true;
                 break;
               }
             }
             __nanosleep(ns);
-            if (ns < 512) ns <<= 1;
+            if (ns < 2048) ns <<= 1;
           }
           if (DBG) {
             wcyc += clock64() - t0;
