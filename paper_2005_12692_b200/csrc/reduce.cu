@@ -925,8 +925,13 @@ __device__ __forceinline__ void jitter_sleep(const RP& P, uint32_t a, uint32_t b
   if ((h & 3) == 0) __nanosleep(h % P.jitter);
 }
 
+// 2 resident blocks (16 warps) per SM: 128 registers a thread keep the working column out of
+// local memory; measured against 4 / 3 / 1 blocks and F of 256 / 512 / 768 / 1024 entries
+// (profiles/r02/s4): C5b 62.5 / 60.3 / 65.0 ms, C5 227 / 223 / 180 ms, C4 31.1 / 30.6 / 26.3 ms
+// vs 56.1 / 198 / 26.3 ms here -- the chains of dependent additions, not the number of columns
+// in flight, bound the reduction.
 #ifndef K5_MINB
-#define K5_MINB 4
+#define K5_MINB 2
 #endif
 constexpr size_t K5_SMEM = sizeof(uint64_t) * WPB * (2 * FCAP + 8 + STAGE);
 __device__ __forceinline__ unsigned long long gtimer() {
