@@ -116,6 +116,35 @@ extern thread_local int64_t g_launch_count;
     ++::cr::g_launch_count;              \
   } while (0)
 
+// One thread per voxel: x within a block row, (y, z) from the grid -- no division per voxel.
+// Images whose y or z extent exceeds the grid limit fall back to a linear launch with division.
+constexpr int VOX_THREADS = 256;
+inline bool vox_grid_ok(const Geom& g) { return g.ny <= 65535 && g.nz <= 65535; }
+inline dim3 vox_grid(const Geom& g) {
+  // (measured: a (row, y, z) grid of 128-thread rows was slower on C5b than the linear launch --
+  // a million small blocks -- so the linear form with one division pair per voxel is used)
+  return dim3(unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), 1, 1);
+}
+// this thread's voxel (v, x, y, z); false past the row end / the grid
+__device__ __forceinline__ bool vox_of_thread(const Geom& g, uint32_t& v, uint32_t& x, uint32_t& y,
+                                              uint32_t& z) {
+  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
+  if (gridDim.y > 1 || gridDim.z > 1) {
+    x = blockIdx.x * VOX_THREADS + threadIdx.x;
+    y = blockIdx.y;
+    z = blockIdx.z;
+    v = (z * ny + y) * nx + x;
+    return x < nx;
+  }
+  const uint64_t vv = uint64_t(blockIdx.x) * VOX_THREADS + threadIdx.x;
+  v = uint32_t(vv);
+  const uint32_t r = v / nx;
+  x = v - r * nx;
+  z = r / ny;
+  y = r - z * ny;
+  return vv < uint64_t(g.nvox);
+}
+
 inline unsigned grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;

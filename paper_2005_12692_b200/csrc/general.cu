@@ -458,20 +458,23 @@ __device__ __forceinline__ uint32_t kidx_vox(const Geom& g, uint32_t k) {
 // that are not the lower cell of an apparent pair) into *nbasins
 __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                             Geom g, uint32_t* __restrict__ parent, unsigned long long* nbasins) {
-  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t v, x, y, z;
+  const bool in = vox_of_thread(g, v, x, y, z);
   bool basin = false;
-  if (vv < g.nvox) {
-    const uint32_t v = uint32_t(vv);
-    const uint32_t k = vox_kidx(g, v);
-    const uint8_t t = tags[k];
+  if (in) {
+    const uint32_t k = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
     const bool present = births[k] != ABSENT_ORD;
     uint32_t p = v;
-    if (present && tag_kind(t) == KIND_UP) {
-      const int d = tag_dir(t);
-      const int64_t vs = (d >> 1) == 0 ? 1 : ((d >> 1) == 1 ? g.nx : g.nx * g.ny);
-      p = uint32_t(int64_t(v) + ((d & 1) ? vs : -vs));
+    if (present) {
+      const uint8_t t = tags[k];
+      if (tag_kind(t) == KIND_UP) {
+        const int d = tag_dir(t);
+        const int64_t vs = (d >> 1) == 0 ? 1 : ((d >> 1) == 1 ? g.nx : g.nx * g.ny);
+        p = uint32_t(int64_t(v) + ((d & 1) ? vs : -vs));
+      } else {
+        basin = true;
+      }
     }
-    basin = present && tag_kind(t) != KIND_UP;
     parent[v] = p;
   }
   const unsigned mask = __ballot_sync(0xFFFFFFFFu, basin);
@@ -496,15 +499,6 @@ struct Cand {
   uint32_t a, b; // current component roots (voxel ids)
 };
 
-// voxel v's coordinates (one pair of divisions per voxel, not per Khalimsky cell)
-__device__ __forceinline__ void vox_xyz(const Geom& g, uint32_t v, uint32_t& x, uint32_t& y,
-                                        uint32_t& z) {
-  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
-  const uint32_t r = v / nx;
-  x = v - r * nx;
-  z = r / ny;
-  y = r - z * ny;
-}
 
 // Append up to one item per lane (warp-aggregated atomic); returns nothing.
 template <class T>
@@ -524,12 +518,11 @@ __device__ __forceinline__ void warp_append(bool emit, const T& item, T* __restr
 __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                            Geom g, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
                            unsigned int* __restrict__ ncand) {
-  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool in = vv < g.nvox;
-  const uint32_t v = in ? uint32_t(vv) : 0u;
-  uint32_t x = 0, y = 0, z = 0;
-  if (in) vox_xyz(g, v, x, y, z);
+  uint32_t v, x, y, z;
+  const bool in0 = vox_of_thread(g, v, x, y, z);
   const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
+  // every edge with base voxel v contains v: an absent v skips them all
+  const bool in = in0 && births[kb] != ABSENT_ORD;
   const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
@@ -569,12 +562,11 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
 __global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
                                const uint32_t* __restrict__ parent, uint64_t* rec,
                                unsigned long long* nrec, unsigned long long* nroots) {
-  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t v, x, y, z;
   bool emit = false;
   uint32_t k = 0;
-  if (vv < g.nvox) {
-    uint32_t v = uint32_t(vv);
-    k = vox_kidx(g, v);
+  if (vox_of_thread(g, v, x, y, z)) {
+    k = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
     emit = parent[v] == v && births[k] != ABSENT_ORD;
   }
   unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
@@ -636,18 +628,21 @@ __device__ __forceinline__ uint32_t dual_side(const DualG& G, uint32_t k, int a,
 // cell lies in the outside vertex's component and hangs under it directly.
 __global__ void k_dual_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                               DualG G, uint32_t* __restrict__ parent, int absent_to_omega) {
-  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (vv > G.omega) return;
-  const uint32_t v = uint32_t(vv);
+  uint32_t v, x, y, z;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
+    parent[G.omega] = G.omega;
+  if (!vox_of_thread(G.g, v, x, y, z)) return;
   uint32_t p = v, k;
-  if (v < G.omega && top_of_voxel(G.g, v, k) && births[k] == ABSENT_ORD) {
-    if (absent_to_omega) p = G.omega;
-  } else if (v < G.omega && top_of_voxel(G.g, v, k)) {
-    const uint8_t t = tags[k];
-    if (tag_kind(t) == KIND_DOWN) {  // dual apparent pair: hangs under its face's other coface
-      const int dir = tag_dir(t);
-      const uint32_t f = uint32_t(int64_t(k) + dir_offset(G.g, dir));
-      p = dual_side(G, f, dir >> 1, dir & 1);
+  if (top_of_voxel(G.g, v, k)) {
+    if (births[k] == ABSENT_ORD) {
+      if (absent_to_omega) p = G.omega;
+    } else {
+      const uint8_t t = tags[k];
+      if (tag_kind(t) == KIND_DOWN) {  // dual apparent pair: hangs under its face's other coface
+        const int dir = tag_dir(t);
+        const uint32_t f = uint32_t(int64_t(k) + dir_offset(G.g, dir));
+        p = dual_side(G, f, dir >> 1, dir & 1);
+      }
     }
   }
   parent[v] = p;
@@ -720,12 +715,11 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
                              DualG G, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
                              unsigned int* __restrict__ ncand, unsigned long long* nroots) {
   const Geom& g = G.g;
-  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool in = vv < g.nvox;
-  const uint32_t v = in ? uint32_t(vv) : 0u;
-  uint32_t x = 0, y = 0, z = 0;
-  if (in) vox_xyz(g, v, x, y, z);
+  uint32_t v, x, y, z;
+  const bool in = vox_of_thread(g, v, x, y, z);
   const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
+  // every face with base voxel v contains v: an absent v has no face to emit (roots still count)
+  const bool vpres = in && births[kb] != ABSENT_ORD;
   const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
@@ -743,13 +737,15 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
     const bool root = has_top && rv == v;
     const unsigned mask = __ballot_sync(0xFFFFFFFFu, root);
     if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nroots, (unsigned long long)__popc(mask));
-    if (vv == 0 && parent[G.omega] == G.omega) atomicAdd(nroots, 1ull);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&
+        parent[G.omega] == G.omega)
+      atomicAdd(nroots, 1ull);
   }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     bool emit = false;
     Cand cd;
-    if (in && n[a] > 1) {
+    if (vpres && n[a] > 1) {
       bool ok = true;
       uint32_t k = kb;
 #pragma unroll
@@ -956,7 +952,8 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     const int64_t ess_top = (d & 1) ? low - chi : chi - low;
     no_cavity = ess_top == 0;
   }
-  k_dual_parent<<<grid_for(nv, B), B, 0, s>>>(S.births, S.tags, G, parent, no_cavity ? 1 : 0);
+  k_dual_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent,
+                                                    no_cavity ? 1 : 0);
   CR_CHECK_LAUNCH();
   if (!no_cavity) {
     k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
@@ -966,7 +963,7 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   CR_CHECK_LAUNCH();
   Cand* cand = ws.alloc<Cand>(st.cells[d] + 1);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt);
-  k_dual_edges<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
+  k_dual_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
                                                   cnt + 1);
   CR_CHECK_LAUNCH();
   CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1130,7 +1127,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
 
   // ---- H0
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);
-  k_h0_parent<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
+  k_h0_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
   CR_CHECK_LAUNCH();
   k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
   CR_CHECK_LAUNCH();
@@ -1148,7 +1145,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
 
   Cand* cand = ws.alloc<Cand>(nedges);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
-  k_h0_edges<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
+  k_h0_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
   CR_CHECK_LAUNCH();
 
   // vertex records: at most one per finite vertex
@@ -1161,7 +1158,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   mm_rounds<false>(cand, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
                    DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ctl, ws);
   // essential classes: the final roots (parent[v] == v holds exactly for them; no flattening)
-  k_h0_essential<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
+  k_h0_essential<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
                                                     cnt + 22);
   CR_CHECK_LAUNCH();
   CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,

@@ -1214,19 +1214,12 @@ __global__ void k_levels_init(uint64_t* lv0, uint64_t* lv1, uint64_t* lv2, uint6
 __global__ void k_collect_columns(const uint32_t* __restrict__ births,
                                   const uint8_t* __restrict__ tags, Geom g, int d,
                                   uint64_t* __restrict__ cols, unsigned* __restrict__ ncols) {
-  const int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool in = vv < g.nvox;
-  uint32_t c[3] = {0u, 0u, 0u};
-  if (in) {
-    const uint32_t v = uint32_t(vv), nx = uint32_t(g.nx), ny = uint32_t(g.ny);
-    const uint32_t r = v / nx;
-    c[0] = v - r * nx;
-    c[2] = r / ny;
-    c[1] = r - c[2] * ny;
-  }
+  uint32_t v, c[3];
+  const bool in0 = vox_of_thread(g, v, c[0], c[1], c[2]);
   const uint32_t n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t kb = (2 * c[2] * uint32_t(g.KY) + 2 * c[1]) * uint32_t(g.KX) + 2 * c[0];
+  const bool in = in0 && births[kb] != ABSENT_ORD;  // every cell with base v contains v
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int t = 1; t < 8; ++t) {  // cell type: bit a set = odd along axis a
@@ -1380,7 +1373,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
   unsigned long long* ctr = ws.alloc<unsigned long long>(16);
   CR_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
   uint64_t* cols = ws.alloc<uint64_t>(nd + 1);
-  k_collect_columns<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, S.tags, g, d, cols,
+  k_collect_columns<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, d, cols,
                                                         reinterpret_cast<unsigned*>(ctr));
   CR_CHECK_LAUNCH();
   const unsigned ncols = read_scalar(reinterpret_cast<unsigned*>(ctr), s, hs);
