@@ -57,7 +57,7 @@ template <bool DUAL>
 constexpr int k7_cand() { return DUAL ? 1536 : K7_SORT; }  // union-find candidates per image
 template <bool DUAL>
 struct K7Smem {
-  uint32_t ord[K7_MAXVOX];
+  uint32_t ord[K7_MAXVOX + 1];  // voxel ords; later the dual parents (OMEGA = nvox <= MAXVOX)
   uint32_t births[K7_MAXCELLS];
   uint32_t death[K7_MAXCELLS];
   uint16_t vpar[K7_MAXVOX];
@@ -71,7 +71,7 @@ struct K7Smem {
     typename cub::BlockScan<uint32_t, K7_THREADS>::TempStorage scan;
     struct {
       uint64_t keys[k7_cand<DUAL>()];  // candidates (compact keys), unsorted
-      uint64_t best[K7_MAXVOX];        // per root: the minimum (H0) / maximum (dual) candidate
+      uint64_t best[K7_MAXVOX + 1];    // per root: the minimum (H0) / maximum (dual) candidate
     };
   } tmp;
   uint32_t nkeys;
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(K7_THREADS, 4) k7_image(K7Args A) {
       auto rkey = [&](uint32_t v) -> uint64_t {
         return v == OMEGA ? NONE64 : cellkey(S, sq_of(v));
       };
-      uint64_t* best = S.tmp.best;  // dual vertices 0..nvox (OMEGA = nvox < K7_MAXVOX)
+      uint64_t* best = S.tmp.best;  // dual vertices 0..nvox (OMEGA = nvox <= K7_MAXVOX)
       for (int v = threadIdx.x; v <= nvox; v += K7_THREADS) best[v] = 0;
       uint64_t rnd = 0;  // round-tagged maxima: (rnd << 44) | key, no reset phase
       uint32_t alive = 0;
