@@ -985,6 +985,8 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     c.mstale = true;
     c.nf = coboundary(P, cell, c.Fc, lane);
     const unsigned long long c_t0 = DBG ? gtimer() : 0;
+    unsigned c_pre = 0;     // debug: apparent additions before the first non-apparent pivot
+    bool c_inpre = true;
     c.fcyc = 0;
     c.fent = 0;
     c.fn = 0;
@@ -1032,13 +1034,16 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         add = s_small[wib];
         glob = false;
         consume_pivot(c);
+        if (DBG && c_inpre) ++c_pre;
       } else if (oi != NONE64) {
+        if (DBG) c_inpre = false;
         // the owner's reduced column starts with the pivot itself
         add = P.pool + (oi >> OI_LEN_BITS) + 1;
         alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1)) - 1;
         glob = true;
         consume_pivot(c);
       } else {
+        if (DBG) c_inpre = false;
         // unowned pivot: wait until no earlier column of the segment can end on it
         jitter_sleep(P, j, uint32_t(adds));
         if (xp != piv) {  // a new pivot: earlier columns are checked again, past the finished ones
@@ -1160,7 +1165,9 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     const long long tfin0 = DBG ? clock64() : 0;
     finish_column(P, j, lane);
     if (DBG && lane == 0) {
-      unsigned long long* R = P.colrec + 24ull * j;
+      unsigned long long* R = P.colrec + 32ull * j;
+      R[23] = (uint64_t(seg) << 32) | (j - seg_lo);  // segment, position in it
+      R[24] = c_pre;
       R[19] = tf1 - tf0;
       R[20] = t_scan;
       R[21] = t_commit;
@@ -1288,7 +1295,7 @@ __global__ void k_mark_cleared(const uint64_t* __restrict__ rec, int64_t n, uint
 // Debug (option debug >= 2): the chain that ends the launch -- from the last column to finish,
 // follow each column's last blocker -- and the busiest columns.
 static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, cudaStream_t s) {
-  constexpr int RW = 24;
+  constexpr int RW = 32;
   std::vector<unsigned long long> R(RW * size_t(ncols));
   CR_CUDA(cudaMemcpyAsync(R.data(), dcol, R.size() * 8, cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
@@ -1303,9 +1310,9 @@ static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, 
   uint32_t cur = last;
   for (int k = 0; k < 40 && cur != NONE32 && cur < ncols; ++k) {
     const unsigned long long* r = &R[RW * size_t(cur)];
-    fprintf(stderr, "   %u: %.1f..%.1f adds %llu wait %.1f waits %llu blk %lld\n", cur,
-            (r[0] - t0) / 1e3, (r[1] - t0) / 1e3, r[2], r[3] / 1.9e3, r[4],
-            r[5] == NONE32 ? -1ll : (long long)r[5]);
+    fprintf(stderr, "   %u (seg %llu pos %llu): %.1f..%.1f adds %llu wait %.1f waits %llu blk %lld\n",
+            cur, r[23] >> 32, r[23] & 0xFFFFFFFFull, (r[0] - t0) / 1e3, (r[1] - t0) / 1e3, r[2],
+            r[3] / 1.9e3, r[4], r[5] == NONE32 ? -1ll : (long long)r[5]);
     cur = uint32_t(r[5]);
   }
   std::vector<std::pair<unsigned long long, uint32_t>> busy(ncols);
@@ -1315,8 +1322,8 @@ static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, 
   for (int k = 0; k < 12 && k < int(ncols); ++k) {
     const uint32_t j = busy[k].second;
     const unsigned long long* r = &R[RW * size_t(j)];
-    fprintf(stderr, "   %u: %.1f..%.1f adds %llu wait %.1f\n", j, (r[0] - t0) / 1e3,
-            (r[1] - t0) / 1e3, r[2], r[3] / 1.9e3);
+    fprintf(stderr, "   %u: %.1f..%.1f adds %llu (apparent before the first other pivot: %llu) "
+            "wait %.1f\n", j, (r[0] - t0) / 1e3, (r[1] - t0) / 1e3, r[2], r[24], r[3] / 1.9e3);
     if (r[8] + r[9] + r[10] + r[11]) {
       const double a = r[2] ? double(r[2]) : 1.0, pa = double(r[2] - r[12]);
       fprintf(stderr, "      take_pivot: %.2f iterations, %.3f M and %.3f G window reloads per call;"
@@ -1331,6 +1338,15 @@ static void debug_critical_path(const unsigned long long* dcol, uint32_t ncols, 
               (r[15] >> 40) ? r[14] / double(r[15] >> 40) : 0.0,
               (r[15] >> 40) ? double(r[15] & ((1ull << 40) - 1)) / double(r[15] >> 40) : 0.0);
     }
+  }
+  {
+    unsigned long long pre = 0, all = 0;
+    for (uint32_t j = 0; j < ncols; ++j) {
+      pre += R[RW * size_t(j) + 24];
+      all += R[RW * size_t(j) + 2];
+    }
+    fprintf(stderr, "[cr] additions %llu, apparent ones before a column's first other pivot %llu\n",
+            all, pre);
   }
   {  // where the warps' time goes, summed over all columns (cycles -> ms of warp time)
     double tot = 0, add = 0, wait = 0, fetch = 0, scan = 0, commit = 0, fin = 0;
@@ -1486,7 +1502,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.jitter = unsigned(opt(OPT_K5_JITTER_NS));
       P.colrec = nullptr;
       if (dbg) {
-        if (!colrec) colrec = ws.alloc<unsigned long long>(24 * int64_t(ncols));
+        if (!colrec) colrec = ws.alloc<unsigned long long>(32 * int64_t(ncols));
         P.colrec = colrec;
       }
       void* args[] = {&P};
