@@ -395,6 +395,55 @@ __device__ __forceinline__ void r_insert(CT& c, const uint64_t* B, uint32_t nb, 
   __syncwarp();
 }
 
+// R <- R[r0:nr] xor Y for the (unsorted, pairwise distinct) keys y held by the lanes in vm --
+// the apparent partner's coboundary, straight from spec_issue's registers: no sort through
+// shared memory and no binary search.  Each y is broadcast once; two ballots give its rank in R
+// and whether it cancels an R entry; an R entry moves by the kept y below it minus the cancelled
+// entries before it.  Requires (nr - r0) + popc(vm) <= 32.  Warp-collective.
+template <class CT>
+__device__ __forceinline__ void r_insert_lanes(CT& c, uint64_t y, unsigned vm, uint64_t* scratch,
+                                               int lane) {
+  const bool mine = uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr;  // lane holds a live R entry
+  const uint64_t x = c.rv;
+  const unsigned lt = (1u << lane) - 1;
+  unsigned rem = 0;       // live R entries cancelled by some y
+  uint32_t keptb = 0;     // (R lanes) kept y below x
+  uint32_t yrank = 0;     // (y lanes) live R entries below y
+  uint32_t ybelow = 0;    // (y lanes) kept y' below y
+  bool ydup = false;      // (y lanes) y cancels an R entry
+  unsigned ymask = 0;     // lanes of the y's that cancel
+  for (unsigned m = vm; m; m &= m - 1) {
+    const int src = __ffs(m) - 1;
+    const uint64_t v = __shfl_sync(0xFFFFFFFFu, y, src);
+    const unsigned ltv = __ballot_sync(0xFFFFFFFFu, mine && x < v);
+    const unsigned eqv = __ballot_sync(0xFFFFFFFFu, mine && x == v);
+    rem |= eqv;
+    if (eqv) ymask |= 1u << src;
+    if (lane == src) {
+      yrank = __popc(ltv);
+      ydup = eqv != 0;
+    }
+    if (!eqv) {
+      if (mine && v < x) ++keptb;
+      if ((vm >> lane & 1) && v < y) ++ybelow;
+    }
+  }
+  const unsigned livem = __ballot_sync(0xFFFFFFFFu, mine);
+  if (mine && !(rem >> lane & 1))
+    scratch[(lane - c.r0) - __popc(rem & lt & livem) + keptb] = x;
+  if ((vm >> lane & 1) && !ydup) {
+    // removed R entries below y: the cancelled lanes among the first yrank live ones
+    const unsigned below = livem & ((yrank + c.r0) >= 32 ? 0xFFFFFFFFu : ((1u << (yrank + c.r0)) - 1));
+    scratch[yrank - __popc(rem & below) + ybelow] = y;
+  }
+  __syncwarp();
+  const uint32_t n = (c.nr - c.r0) - __popc(rem) + (__popc(vm) - __popc(ymask));
+  c.rv = uint32_t(lane) < n ? scratch[lane] : NONE64;
+  c.nr = n;
+  c.r0 = 0;
+  __syncwarp();
+}
+
 // The apparent-partner coboundary, speculated.  A DOWN pivot t (a (d+1)-cell) is the upper cell
 // of an apparent pair (s', t) with s' = t + e_dir, a facet of t; the column then adds delta(s') =
 // {t} + the other cofacets of s'.  Before t's tag is known, lane L < 30 loads the birth of member
@@ -452,19 +501,6 @@ __device__ __forceinline__ Spec spec_issue(const RP& P, const SpecLane& L, uint3
     r.birth = __ldg(P.births + r.cell);
   }
   return r;
-}
-// delta(s') minus the pivot, sorted ascending into dst (<= 5 entries) for the partner direction
-// dir; warp-collective.
-__device__ __forceinline__ uint32_t spec_finish(const RP& P, const Spec& sp, int dir, uint64_t piv,
-                                                uint64_t* dst, int lane) {
-  uint64_t key = NONE64;
-  if (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD) key = rkey(P, sp.birth, sp.cell);
-  const unsigned vm = __ballot_sync(0xFFFFFFFFu, key != NONE64);
-  int rank = 0;
-  for (unsigned m = vm; m; m &= m - 1) rank += __shfl_sync(0xFFFFFFFFu, key, __ffs(m) - 1) < key;
-  if (key != NONE64) dst[rank] = key;
-  __syncwarp();
-  return __popc(vm);
 }
 
 // C = A xor F for a long A (global) and a short F (shared, b <= FCAP), C in global memory, using
@@ -1029,12 +1065,29 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       const long long q2 = CT::dbg ? clock64() : 0;
       d_lk += q2 - q1;
       if (tag_kind(t) == KIND_DOWN) {
-        // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s')
-        alen = spec_finish(P, sp, tag_dir(t), piv, s_small[wib], lane);
-        add = s_small[wib];
-        glob = false;
+        // the pivot is the upper cell of an apparent pair (s', pivot): add delta(s') minus the
+        // pivot, straight from the speculated births into the register list R
+        const int dir = tag_dir(t);
+        const uint64_t y = (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD)
+                               ? rkey(P, sp.birth, sp.cell) : NONE64;
+        const unsigned vm = __ballot_sync(0xFFFFFFFFu, y != NONE64);
         consume_pivot(c);
         if (DBG && c_inpre) ++c_pre;
+        const uint32_t ny = __popc(vm);
+        addlen += c.len() + ny;
+        if (ny) {
+          if ((c.nr - c.r0) + ny > 32) ok = spill_r(c, P, s_stage[wib], lane);
+          if (!ok) break;
+          r_insert_lanes(c, y, vm, s_stage[wib], lane);
+        }
+        ++adds;
+        if (DBG) {
+          d_app += clock64() - q2;
+          ++d_napp;
+        }
+        const unsigned l = c.len();
+        maxlen = l > maxlen ? l : maxlen;
+        continue;
       } else if (oi != NONE64) {
         if (DBG) c_inpre = false;
         // the owner's reduced column starts with the pivot itself
