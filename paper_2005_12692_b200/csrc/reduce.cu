@@ -61,8 +61,12 @@ struct RP {
   uint32_t ncols;
   const uint32_t* births;
   const uint8_t* tags;
-  uint64_t* owninfo;   // per (d+1)-cell: (pool offset << 24) | length of the column owning it as
-                       // pivot, NONE64 if unowned -- one load instead of owner -> offset, length
+  // pivot hash table (open addressing, linear probing, 2^k slots of {key = pivot kidx, val}):
+  // val = (pool offset << 24) | length of the committed column owning that pivot, NONE64 until
+  // written.  ~2x the columns in slots: L2-resident (C5b 64 MB), where round 1's dense table
+  // over every cell took 8.6 GB, a memset per call and a DRAM miss per lookup.
+  ulonglong2* otab;
+  uint32_t omask;
   uint64_t* pool;
   unsigned long long* pool_top;
   unsigned long long pool_cap;
@@ -86,7 +90,46 @@ struct RP {
   unsigned jitter;     // validation: pseudo-random delays (ns) that perturb the schedule
   unsigned long long* colrec;  // debug (option debug >= 2): per column 16 words, see k_reduce
 };
-constexpr int OI_LEN_BITS = 24;  // owninfo: stored column length field
+constexpr int OI_LEN_BITS = 24;  // owner value: stored column length field
+
+__device__ __forceinline__ uint32_t ohash(uint32_t k, uint32_t mask) {
+  return uint32_t((uint64_t(k) * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+}
+// The owner value of pivot k (NONE64: no committed owner -- or one whose value is not written
+// yet, which callers treat as "not yet", re-checking after the owner is published finished).
+// All lanes read the same slot (one transaction); warp-uniform.
+__device__ __forceinline__ uint64_t owner_of(const ulonglong2* otab, uint32_t mask, uint32_t k) {
+  for (uint32_t i = ohash(k, mask);; i = (i + 1) & mask) {
+    const ulonglong2 sl = __ldcg(otab + i);
+    if (sl.x == k) return sl.y;
+    if (sl.x == NONE64) return NONE64;
+  }
+}
+// the same with relaxed (coherent) loads, for the re-checks that order after a fence
+__device__ __forceinline__ uint64_t owner_of_rlx(const ulonglong2* otab, uint32_t mask, uint32_t k) {
+  for (uint32_t i = ohash(k, mask);; i = (i + 1) & mask) {
+    const uint64_t* sl = reinterpret_cast<const uint64_t*>(otab + i);
+    uint64_t key, val;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(key) : "l"(sl) : "memory");
+    if (key == NONE64) return NONE64;
+    if (key == k) {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(val) : "l"(sl + 1) : "memory");
+      return val;
+    }
+  }
+}
+// one thread: claim k's slot and write its value (every pivot is committed once)
+__device__ __forceinline__ void owner_insert(ulonglong2* otab, uint32_t mask, uint32_t k,
+                                             uint64_t val) {
+  for (uint32_t i = ohash(k, mask);; i = (i + 1) & mask) {
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(otab + i);
+    const unsigned long long old = atomicCAS(key, NONE64, (unsigned long long)k);
+    if (old == NONE64 || old == k) {
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(key + 1), "l"(val) : "memory");
+      return;
+    }
+  }
+}
 
 __device__ __forceinline__ uint64_t ldcg64(const uint64_t* p) {
   return __ldcg((const unsigned long long*)p);
@@ -1058,7 +1101,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       // independent loads: the speculated partner coboundary, the tag, the owner record
       const Spec sp = spec_issue(P, sl, pk);
       const uint8_t t = __ldg(P.tags + pk);
-      const uint64_t oi = ldcg64(P.owninfo + pk);
+
       const uint64_t* add;
       uint32_t alen;
       bool glob;
@@ -1088,7 +1131,11 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         const unsigned l = c.len();
         maxlen = l > maxlen ? l : maxlen;
         continue;
-      } else if (oi != NONE64) {
+      }
+      // not apparent: is the pivot owned by a committed column? (probed only now -- apparent
+      // pivots, 93 % of them, never touch the table)
+      const uint64_t oi = owner_of(P.otab, P.omask, pk);
+      if (oi != NONE64) {
         if (DBG) c_inpre = false;
         // the owner's reduced column starts with the pivot itself
         add = P.pool + (oi >> OI_LEN_BITS) + 1;
@@ -1125,7 +1172,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
                 ok = false;
                 break;
               }
-              if (ld_rlx(P.owninfo + pk) != NONE64) {  // an earlier column committed this pivot
+              if (owner_of_rlx(P.otab, P.omask, pk) != NONE64) {  // an earlier column committed it
                 owned = true;
                 break;
               }
@@ -1145,7 +1192,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           uint64_t o = 0;
           if (lane == 0) {
             __threadfence();
-            o = ld_rlx(P.owninfo + pk);
+            o = owner_of_rlx(P.otab, P.omask, pk);
           }
           owned = __shfl_sync(0xFFFFFFFFu, o, 0) != NONE64;
         }
@@ -1185,7 +1232,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         if (lane == 0) {
           if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
           __threadfence();
-          st_rlx(P.owninfo + pk, (uint64_t(off) << OI_LEN_BITS) | n);
+          owner_insert(P.otab, P.omask, pk, (uint64_t(off) << OI_LEN_BITS) | n);
           const unsigned long long r = atomicAdd(P.nrec, 1ull);
           P.rec[r] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
         }
@@ -1498,7 +1545,10 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
 
     const uint32_t npad = (ncols + 32767u) & ~32767u;
     uint64_t* lv = ws.alloc<uint64_t>(int64_t(npad) + npad / 32 + npad / 1024 + npad / 32768);
-    uint64_t* owninfo = ws.alloc<uint64_t>(g.ncells);
+    uint32_t obits = 10;
+    while ((uint64_t(1) << obits) < 4ull * ncols + 1024) ++obits;  // load <= 1/4: short probes
+    const uint32_t oslots = 1u << obits;
+    ulonglong2* otab = static_cast<ulonglong2*>(ws.alloc_bytes(size_t(oslots) * sizeof(ulonglong2)));
     unsigned* seg_next = ws.alloc<unsigned>(nseg);
     int* err = reinterpret_cast<int*>(ctr + 3);
     unsigned long long* nrec = ctr + 4;
@@ -1517,7 +1567,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     unsigned long long* colrec = nullptr;
     for (int attempt = 0;; ++attempt) {
       if (!pool) pool = ws.alloc<uint64_t>(int64_t(pool_cap));
-      CR_CUDA(cudaMemsetAsync(owninfo, 0xFF, g.ncells * sizeof(uint64_t), s));
+      CR_CUDA(cudaMemsetAsync(otab, 0xFF, size_t(oslots) * sizeof(ulonglong2), s));
       CR_CUDA(cudaMemsetAsync(seg_next, 0, nseg * sizeof(unsigned), s));
       CR_CUDA(cudaMemsetAsync(ctr + 3, 0, 13 * sizeof(unsigned long long), s));
       k_levels_init<<<grid_for(npad, B), B, 0, s>>>(lv, lv + npad, lv + npad + npad / 32,
@@ -1532,7 +1582,8 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.ncols = ncols;
       P.births = S.births;
       P.tags = S.tags;
-      P.owninfo = owninfo;
+      P.otab = otab;
+      P.omask = oslots - 1;
       P.pool = pool;
       P.pool_top = pool_top;
       P.pool_cap = pool_cap;
@@ -1587,7 +1638,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     ws.release(work);
     ws.release(gwork);
     ws.release(pool);
-    ws.release(owninfo);
+    ws.release(otab);
     ws.release(lv);
   }
   if (S.R.n[d] > 0) {
