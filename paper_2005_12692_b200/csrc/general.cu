@@ -500,18 +500,6 @@ struct Cand {
 };
 
 
-// Append up to one item per lane (warp-aggregated atomic); returns nothing.
-template <class T>
-__device__ __forceinline__ void warp_append(bool emit, const T& item, T* __restrict__ out,
-                                            unsigned* __restrict__ n) {
-  const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  const int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(n, __popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) out[base + __popc(mask & ((1u << lane) - 1))] = item;
-}
 
 // Inter-basin candidate edges: residual edges whose endpoints have different roots (after
 // pointer jumping).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
@@ -527,25 +515,26 @@ __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* _
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
   const uint32_t ra = in ? parent[v] : 0u;
+  bool emit[3];
+  Cand cd[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    bool emit = false;
-    Cand cd;
+    emit[a] = false;
     if (in && c[a] + 1 < n[a]) {
       const uint32_t k = kb + ks[a];
       const uint32_t bo = births[k];
       if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
         const uint32_t rb = parent[v + vs[a]];
         if (ra != rb) {
-          emit = true;
-          cd.key = make_key(bo, k);
-          cd.a = ra;
-          cd.b = rb;
+          emit[a] = true;
+          cd[a].key = make_key(bo, k);
+          cd[a].a = ra;
+          cd[a].b = rb;
         }
       }
     }
-    warp_append(emit, cd, cand, ncand);
   }
+  warp_append(emit, cd, cand, ncand);
 }
 
 __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
@@ -741,10 +730,11 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
         parent[G.omega] == G.omega)
       atomicAdd(nroots, 1ull);
   }
+  bool emit[3];
+  Cand cd[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    bool emit = false;
-    Cand cd;
+    emit[a] = false;
     if (vpres && n[a] > 1) {
       bool ok = true;
       uint32_t k = kb;
@@ -760,16 +750,16 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
           const uint32_t ra = c[a] > 0 ? parent[v - vs[a]] : G.omega;
           const uint32_t rb = c[a] + 1 < n[a] ? rv : G.omega;
           if (ra != rb) {
-            emit = true;
-            cd.key = ~make_key(bo, k);  // ascending ~key = decreasing key
-            cd.a = ra;
-            cd.b = rb;
+            emit[a] = true;
+            cd[a].key = ~make_key(bo, k);  // ascending ~key = decreasing key
+            cd[a].a = ra;
+            cd[a].b = rb;
           }
         }
       }
     }
-    warp_append(emit, cd, cand, ncand);
   }
+  block_append(emit, cd, cand, ncand);
 }
 
 // key of a dual root (larger = elder): OMEGA the largest, absent top cells next

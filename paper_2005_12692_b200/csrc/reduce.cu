@@ -1327,12 +1327,12 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t kb = (2 * c[2] * uint32_t(g.KY) + 2 * c[1]) * uint32_t(g.KX) + 2 * c[0];
   const bool in = in0 && births[kb] != ABSENT_ORD;  // every cell with base v contains v
-  const int lane = threadIdx.x & 31;
+  bool emit[3] = {false, false, false};
+  uint64_t key[3] = {0, 0, 0};
+  int q = 0;
 #pragma unroll
   for (int t = 1; t < 8; ++t) {  // cell type: bit a set = odd along axis a
-    if (__popc(t) != d) continue;
-    bool emit = false;
-    uint64_t key = 0;
+    if (__popc(t) != d || q >= 3) continue;
     if (in) {
       bool ok = true;
       uint32_t k = kb;
@@ -1345,18 +1345,14 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
       if (ok) {
         const uint32_t b = births[k];
         if (b != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-          emit = true;
-          key = make_key(b, k);
+          emit[q] = true;
+          key[q] = make_key(b, k);
         }
       }
     }
-    const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-    if (!mask) continue;
-    unsigned base = 0;
-    if (lane == __ffs(mask) - 1) base = atomicAdd(ncols, __popc(mask));
-    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-    if (emit) cols[base + __popc(mask & ((1u << lane) - 1))] = key;
+    ++q;
   }
+  warp_append(emit, key, cols, ncols);
 }
 
 __global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32_t seg_cells,
