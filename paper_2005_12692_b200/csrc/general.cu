@@ -481,6 +481,7 @@ __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* 
   if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nbasins, (unsigned long long)__popc(mask));
 }
 
+
 __global__ void k_pointer_jump(uint32_t* parent, int64_t n) {
   int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vv >= n) return;
@@ -494,6 +495,21 @@ __global__ void k_pointer_jump(uint32_t* parent, int64_t n) {
   }
 }
 
+// Root of x in a forest whose links only ever point to ancestors, with path halving (plain
+// stores: a racing writer also stores an ancestor).  Used instead of flattening the whole forest:
+// only the endpoints of the few residual edges need roots (C5b: ~2 M of 172 M edges).
+__device__ __forceinline__ uint32_t find_halve(uint32_t* parent, uint32_t x) {
+  uint32_t p = *(volatile uint32_t*)(parent + x);
+  while (p != x) {
+    const uint32_t pp = *(volatile uint32_t*)(parent + p);
+    if (pp == p) return p;
+    *(volatile uint32_t*)(parent + x) = pp;
+    x = pp;
+    p = *(volatile uint32_t*)(parent + x);
+  }
+  return x;
+}
+
 struct Cand {
   uint64_t key;  // edge key
   uint32_t a, b; // current component roots (voxel ids)
@@ -504,7 +520,7 @@ struct Cand {
 // Inter-basin candidate edges: residual edges whose endpoints have different roots (after
 // pointer jumping).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
 __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                           Geom g, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
+                           Geom g, uint32_t* parent, Cand* __restrict__ cand,
                            unsigned int* __restrict__ ncand) {
   uint32_t v, x, y, z;
   const bool in0 = vox_of_thread(g, v, x, y, z);
@@ -514,7 +530,7 @@ __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* _
   const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
-  const uint32_t ra = in ? parent[v] : 0u;
+  uint32_t ra = NONE32;  // v's root
   bool emit[3];
   Cand cd[3];
 #pragma unroll
@@ -524,6 +540,7 @@ __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* _
       const uint32_t k = kb + ks[a];
       const uint32_t bo = births[k];
       if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+        if (ra == NONE32) ra = parent[v];  // flattened: roots
         const uint32_t rb = parent[v + vs[a]];
         if (ra != rb) {
           emit[a] = true;
@@ -701,7 +718,7 @@ __global__ void k_dual_absent_vox(const uint32_t* __restrict__ births, DualG G,
 // per active normal axis a: even on a, odd on the other active axes), whose cofaces are the top
 // cells with base voxels v - e_a and v.  The same threads count the dual roots into *nroots.
 __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                             DualG G, const uint32_t* __restrict__ parent, Cand* __restrict__ cand,
+                             DualG G, uint32_t* parent, Cand* __restrict__ cand,
                              unsigned int* __restrict__ ncand, unsigned long long* nroots) {
   const Geom& g = G.g;
   uint32_t v, x, y, z;
@@ -721,9 +738,10 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
       has_top = has_top && c[b] + 1 < n[b];
       kt += ks[b];
     }
-  const uint32_t rv = in ? parent[v] : 0u;  // root of the top cell at v (if it exists)
+  const uint32_t pv = in ? parent[v] : 0u;  // the top cell at v is a root iff pv == v
+  uint32_t rv = NONE32;                      // its root, found on the first residual face
   {
-    const bool root = has_top && rv == v;
+    const bool root = has_top && pv == v;
     const unsigned mask = __ballot_sync(0xFFFFFFFFu, root);
     if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nroots, (unsigned long long)__popc(mask));
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&
@@ -747,7 +765,8 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
       if (ok) {
         const uint32_t bo = births[k];
         if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-          const uint32_t ra = c[a] > 0 ? parent[v - vs[a]] : G.omega;
+          const uint32_t ra = c[a] > 0 ? find_halve(parent, v - vs[a]) : G.omega;
+          if (rv == NONE32 && c[a] + 1 < n[a]) rv = find_halve(parent, v);
           const uint32_t rb = c[a] + 1 < n[a] ? rv : G.omega;
           if (ra != rb) {
             emit[a] = true;
@@ -949,8 +968,7 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
     CR_CHECK_LAUNCH();
   }
-  k_pointer_jump<<<grid_for(nv, B), B, 0, s>>>(parent, nv);
-  CR_CHECK_LAUNCH();
+  // (no flattening: k_dual_edges finds the roots of the residual faces' sides on demand)
   Cand* cand = ws.alloc<Cand>(st.cells[d] + 1);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt);
   k_dual_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
@@ -1119,7 +1137,9 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);
   k_h0_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
   CR_CHECK_LAUNCH();
-  k_pointer_jump<<<grid_for(g.nvox, B), B, 0, s>>>(parent, g.nvox);
+  // flatten the apparent forest (H0 chains are long: flattening once beats finds per edge end,
+  // measured; the dual forest is shallow and takes on-demand finds in k_dual_edges instead)
+  k_pointer_jump<<<grid_for(g.nvox, 256), 256, 0, s>>>(parent, g.nvox);
   CR_CHECK_LAUNCH();
 
   // NaN check + counts (one sync)
