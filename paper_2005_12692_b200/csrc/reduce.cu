@@ -184,9 +184,81 @@ __device__ __forceinline__ uint32_t lower_bound(const uint64_t* B, uint32_t n, u
 // C = A xor B (sorted, distinct entries each), C distinct from A and B.  Warp-collective.
 // Output position of a kept A[i]: (#kept A before i) + (#kept B below A[i]); the number of common
 // values below A[i] equals the number of A's duplicates before i.
+// C = A xor B for A, B in shared memory (sorted, distinct entries each), C anywhere: merge path.
+// Lane l takes the merged positions [l*per, (l+1)*per) (ties A first: an equal pair is adjacent,
+// A's copy first); a start falling between an equal pair moves past it, so both copies are in
+// one lane and cancel there.  Each lane merges its ranges sequentially twice -- to count, then
+// (after a warp scan of the counts) to write.  O(1) shared-memory steps per entry instead of a
+// binary search per entry on both sides.  Warp-collective; returns |C|.
+__device__ uint32_t merge_xor_path(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
+                                   uint64_t* C, int lane) {
+  const uint32_t n = a + b;
+  if (n == 0) return 0;
+  const uint32_t per = (n + 31) >> 5;
+  const uint32_t d = min(uint32_t(lane) * per, n);
+  uint32_t lo = d > b ? d - b : 0, hi = d < a ? d : a;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (A[mid] <= B[d - mid - 1]) lo = mid + 1;
+    else hi = mid;
+  }
+  uint32_t is = lo, js = d - lo;
+  if (is > 0 && js < b && A[is - 1] == B[js]) ++js;  // keep an equal pair in one lane
+  uint32_t ie = __shfl_down_sync(0xFFFFFFFFu, is, 1), je = __shfl_down_sync(0xFFFFFFFFu, js, 1);
+  if (lane == 31 || d + per >= n) {
+    ie = a;
+    je = b;
+  }
+  if (d >= n) ie = is = a, je = js = b;  // lanes past the end take nothing
+  uint32_t cnt = 0;
+  {
+    uint32_t i = is, j = js;
+    while (i < ie || j < je) {
+      const uint64_t x = i < ie ? A[i] : NONE64, y = j < je ? B[j] : NONE64;
+      if (x == y) {
+        ++i;
+        ++j;
+      } else if (x < y) {
+        ++cnt;
+        ++i;
+      } else {
+        ++cnt;
+        ++j;
+      }
+    }
+  }
+  uint32_t pos = cnt;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pos, o);
+    if (lane >= o) pos += v;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, pos, 31);
+  pos -= cnt;
+  {
+    uint32_t i = is, j = js;
+    while (i < ie || j < je) {
+      const uint64_t x = i < ie ? A[i] : NONE64, y = j < je ? B[j] : NONE64;
+      if (x == y) {
+        ++i;
+        ++j;
+      } else if (x < y) {
+        C[pos++] = x;
+        ++i;
+      } else {
+        C[pos++] = y;
+        ++j;
+      }
+    }
+  }
+  __syncwarp();
+  return total;
+}
+
 template <bool AG, bool BG>
 __device__ uint32_t merge_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
                                   uint64_t* C, int lane) {
+  if (!AG && !BG) return merge_xor_path(A, a, B, b, C, lane);
   const unsigned lt = (1u << lane) - 1;
   uint32_t carry = 0;
   for (uint32_t base = 0; base < a; base += 32) {
@@ -330,7 +402,10 @@ struct ColT {
   uint32_t nr, r0; // R holds positions [r0, nr) (consumed from the front)
   __device__ uint32_t len() const { return (nm - h) + (ng - g0) + (nf - f0) + (nr - r0); }
 };
-constexpr uint32_t GCAP = 8192;  // the middle tier: F merges into G, G into M when it exceeds GCAP
+#ifndef K5_GCAP
+#define K5_GCAP 8192
+#endif
+constexpr uint32_t GCAP = K5_GCAP;  // the middle tier: F merges into G, G into M when it exceeds GCAP
 
 // The working column is M[h:] xor F[f0:] xor R[r0:nr]: three sorted tiers -- a long main array in
 // global memory, a fresh array in shared memory, and a register list of <= 32 entries (one per
