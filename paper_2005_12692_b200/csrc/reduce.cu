@@ -255,6 +255,90 @@ __device__ uint32_t merge_xor_path(const uint64_t* A, uint32_t a, const uint64_t
   return total;
 }
 
+// L1-cached load of a warp-private buffer (G, M): coherent with this SM's own stores (never the
+// non-coherent read-only path: the buffers are rewritten in ping-pong by the same warp)
+__device__ __forceinline__ uint64_t ld_ca(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.ca.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// C = A xor F for A in global memory, F in shared memory, C in global memory: merge path with
+// each lane merging one contiguous diagonal segment (its reads of A are sequential per lane and
+// hit L1 after the first), twice -- count, warp scan, write.  Warp-collective; returns |C|.
+__device__ uint32_t merge_xor_path_g(const uint64_t* A, uint32_t a, const uint64_t* F,
+                                     uint32_t b, uint64_t* __restrict__ C, int lane) {
+  const uint32_t n = a + b;
+  if (n == 0) return 0;
+  const uint32_t per = (n + 31) >> 5;
+  const uint32_t d = min(uint32_t(lane) * per, n);
+  uint32_t lo = d > b ? d - b : 0, hi = d < a ? d : a;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ld_ca(A + mid) <= F[d - mid - 1]) lo = mid + 1;
+    else hi = mid;
+  }
+  uint32_t is = lo, js = d - lo;
+  if (is > 0 && js < b && ld_ca(A + is - 1) == F[js]) ++js;
+  uint32_t ie = __shfl_down_sync(0xFFFFFFFFu, is, 1), je = __shfl_down_sync(0xFFFFFFFFu, js, 1);
+  if (lane == 31 || d + per >= n) {
+    ie = a;
+    je = b;
+  }
+  if (d >= n) ie = is = a, je = js = b;
+  uint32_t cnt = 0;
+  {
+    uint32_t i = is, j = js;
+    uint64_t x = i < ie ? ld_ca(A + i) : NONE64, y = j < je ? F[j] : NONE64;
+    while (i < ie || j < je) {
+      if (x == y) {
+        ++i;
+        ++j;
+        x = i < ie ? ld_ca(A + i) : NONE64;
+        y = j < je ? F[j] : NONE64;
+      } else if (x < y) {
+        ++cnt;
+        ++i;
+        x = i < ie ? ld_ca(A + i) : NONE64;
+      } else {
+        ++cnt;
+        ++j;
+        y = j < je ? F[j] : NONE64;
+      }
+    }
+  }
+  uint32_t pos = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pos, o);
+    if (lane >= o) pos += v;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, pos, 31);
+  pos -= cnt;
+  {
+    uint32_t i = is, j = js;
+    uint64_t x = i < ie ? ld_ca(A + i) : NONE64, y = j < je ? F[j] : NONE64;
+    while (i < ie || j < je) {
+      if (x == y) {
+        ++i;
+        ++j;
+        x = i < ie ? ld_ca(A + i) : NONE64;
+        y = j < je ? F[j] : NONE64;
+      } else if (x < y) {
+        C[pos++] = x;
+        ++i;
+        x = i < ie ? ld_ca(A + i) : NONE64;
+      } else {
+        C[pos++] = y;
+        ++j;
+        y = j < je ? F[j] : NONE64;
+      }
+    }
+  }
+  __syncwarp();
+  return total;
+}
+
 template <bool AG, bool BG>
 __device__ uint32_t merge_symdiff(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
                                   uint64_t* C, int lane) {
@@ -801,8 +885,7 @@ __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
     __syncwarp();
     n = nb;
   } else {
-    n = merge_long_short(c.Gc + c.g0, na, c.Fc + c.f0, nb, c.Ga,
-                         c.Fa, lane);
+    n = merge_xor_path_g(c.Gc + c.g0, na, c.Fc + c.f0, nb, c.Ga, lane);
   }
   { uint64_t* t = c.Gc; c.Gc = c.Ga; c.Ga = t; }
   c.ng = n;
