@@ -39,9 +39,11 @@ namespace {
 constexpr int WPB = 8;  // warps per block
 constexpr int THREADS = WPB * 32;
 #ifndef K5_FCAP
-#define K5_FCAP 256
+#define K5_FCAP 512
 #endif
-constexpr uint32_t FCAP = K5_FCAP;  // fresh-array capacity per warp (shared memory, x2 ping-pong)
+// fresh-array capacity per warp (shared memory, x2 ping-pong): 512 since the merges went to merge
+// path (profiles/r02/s7: F 256 / 512 / 768 -> C5 169 / 144 / 138 ms, C5b 45.6 / 45.1 / 45.4 ms)
+constexpr uint32_t FCAP = K5_FCAP;
 
 // n / d for n, d < 2^32 by one 64-bit high multiply: m = ceil(2^64 / d) makes the quotient exact
 // (the error n * (m - 2^64/d) / 2^64 < 2^-32 cannot carry past the fractional part (d-1)/d).
