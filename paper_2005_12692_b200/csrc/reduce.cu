@@ -83,8 +83,7 @@ struct RP {
   uint32_t nseg;
   unsigned* seg_next;  // per segment: columns handed out
   unsigned long long* fetch;  // fetch counter (spreads warps over the segments)
-  uint64_t* rec;
-  unsigned long long* nrec;
+  uint64_t* rec;  // one record per column, at the column's index
   int* err;
   unsigned long long* stats;  // [0] waits [1] additions [2] sum of lengths [3] max length
                               // [4] cycles waited [5] commits
@@ -913,7 +912,8 @@ __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
   return true;
 }
 
-constexpr uint32_t STAGE = 64;  // global addends are staged in shared memory, STAGE entries at a time
+constexpr uint32_t STAGE = 64;
+constexpr unsigned long long POOL_CHUNK = 4096;  // pool entries a warp reserves at a time  // global addends are staged in shared memory, STAGE entries at a time
 
 // F <- F xor R, R emptied (flushing F into M first if it cannot take R).  Warp-collective.
 template <class CT>
@@ -1196,6 +1196,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
   const SpecLane sl = spec_lane(P.g, lane);
   c.Fc = s_F[wib][0];
   c.Fa = s_F[wib][1];
+  unsigned long long pool_cur = 0, pool_end = 0;  // this warp's current pool chunk
   unsigned adds = 0, waits = 0, maxlen = 0;
   unsigned long long addlen = 0, wcyc = 0, commits = 0;
 
@@ -1247,8 +1248,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       d_tp += q1 - q0;
       if (piv == NONE64) {  // zero column: essential (exact given the clearing)
         if (lane == 0) {
-          const unsigned long long r = atomicAdd(P.nrec, 1ull);
-          P.rec[r] = (uint64_t(cell) << 32) | NONE32;
+          P.rec[j] = (uint64_t(cell) << 32) | NONE32;  // one record per column: no counter
           atomicAdd(P.ness, 1ull);
         }
         break;
@@ -1361,9 +1361,17 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         ok = spill_r(c, P, s_stage[wib], lane);  // the commit reads M and F
         if (!ok) break;
         const uint32_t L = c.len();
-        unsigned long long off = 0;
-        if (lane == 0) off = atomicAdd(P.pool_top, (unsigned long long)L);
-        off = __shfl_sync(0xFFFFFFFFu, off, 0);
+        // pool space from the warp's own chunk (one global atomic per POOL_CHUNK entries, not
+        // one per committed column: 2k warps committing 1.5 M columns share the counter)
+        if (pool_cur + L > pool_end) {
+          const unsigned long long want = L > POOL_CHUNK ? L : POOL_CHUNK;
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(P.pool_top, want);
+          pool_cur = __shfl_sync(0xFFFFFFFFu, base, 0);
+          pool_end = pool_cur + want;
+        }
+        const unsigned long long off = pool_cur;
+        pool_cur += L;
         if (off + L > P.pool_cap) {
           if (lane == 0) atomicOr(P.err, 2);
           ok = false;
@@ -1393,8 +1401,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
           __threadfence();
           owner_insert(P.otab, P.omask, pk, (uint64_t(off) << OI_LEN_BITS) | n);
-          const unsigned long long r = atomicAdd(P.nrec, 1ull);
-          P.rec[r] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
+          P.rec[j] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
         }
         if (DBG) {
           ++commits;
@@ -1707,7 +1714,6 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     ulonglong2* otab = static_cast<ulonglong2*>(ws.alloc_bytes(size_t(oslots) * sizeof(ulonglong2)));
     unsigned* seg_next = ws.alloc<unsigned>(nseg);
     int* err = reinterpret_cast<int*>(ctr + 3);
-    unsigned long long* nrec = ctr + 4;
     unsigned long long* pool_top = ctr + 5;
     unsigned long long* stats = ctr + 6;   // [6..11]
     unsigned long long* fetch = ctr + 12;
@@ -1716,7 +1722,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     // grown main arrays) is sized so that exhausting it -- which reruns the whole launch with 4x --
     // does not happen on realistic inputs: 16 entries per column + 32 Mi entries (256 MB)
     const uint32_t mcap = 4096u;
-    unsigned long long pool_cap = 16ull * ncols + (1ull << 25);
+    unsigned long long pool_cap = 16ull * ncols + (1ull << 25) + uint64_t(W) * POOL_CHUNK;
     uint64_t* work = ws.alloc<uint64_t>(int64_t(W) * 2 * mcap);
     uint64_t* gwork = ws.alloc<uint64_t>(int64_t(W) * 2 * (GCAP + FCAP));
     uint64_t* pool = nullptr;
@@ -1755,7 +1761,6 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
       P.seg_next = seg_next;
       P.fetch = fetch;
       P.rec = S.R.rec[d];
-      P.nrec = nrec;
       P.err = err;
       P.stats = stats;
       P.ness = ctr + 13;
@@ -1780,7 +1785,7 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
     }
     CR_CUDA(cudaMemcpyAsync(hs.p, ctr, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CR_CUDA(cudaStreamSynchronize(s));
-    S.R.n[d] = int64_t(hs.p[4]);
+    S.R.n[d] = int64_t(ncols);  // one record per column (a pair or an essential class)
     st.rounds[d] = int64_t(hs.p[6]);  // waits on an earlier column
     st.additions[d] = int64_t(hs.p[7]);
     st.addlen[d] = int64_t(hs.p[8]);
