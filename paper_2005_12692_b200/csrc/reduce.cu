@@ -483,46 +483,116 @@ struct ColT {
   uint32_t cap;    // capacity of M[0] and M[1]
   uint64_t* spare; // the second half of a grown pair, installed after the merge that grew it
   uint32_t pt;     // tier of the pivot take_pivot returned: 0 M, 1 G, 2 F, 3 R
-  uint64_t rv;     // per lane: entry `lane` of the register list R (NONE64 at and past nr)
-  uint32_t nr, r0; // R holds positions [r0, nr) (consumed from the front)
-  __device__ uint32_t len() const { return (nm - h) + (ng - g0) + (nf - f0) + (nr - r0); }
+  uint64_t rv;     // per lane: one entry of the register bag R (unsorted; NONE64 = empty lane)
+  uint32_t nr;     // entries in R
+  uint64_t rmin;   // min of R (NONE64 if empty), kept exact
+  uint64_t ha, hg, hb;  // cached heads of M[h:], G[g0:], F[f0:] (valid unless hstale)
+  bool hstale;
+  __device__ uint32_t len() const { return (nm - h) + (ng - g0) + (nf - f0) + nr; }
 };
 #ifndef K5_GCAP
 #define K5_GCAP 8192
 #endif
 constexpr uint32_t GCAP = K5_GCAP;  // the middle tier: F merges into G, G into M when it exceeds GCAP
 
-// The working column is M[h:] xor F[f0:] xor R[r0:nr]: three sorted tiers -- a long main array in
-// global memory, a fresh array in shared memory, and a register list of <= 32 entries (one per
-// lane) that takes the small addends (apparent coboundaries, short stored columns) at a cost of a
-// few shuffles instead of rewriting F.  Equal values in different tiers cancel lazily, when they
-// reach the heads.
-//
-// pivot = min of the three heads, cancelling equal pairs; NONE64 if the column is zero.
-// Warp-collective.  The next 32 entries of M sit in a register window (one per lane), reloaded
-// with one coalesced load when h leaves it or M changes: the head of a long column is not a
-// dependent global load per cancellation.
+// The working column is M[h:] xor G[g0:] xor F[f0:] xor R: three sorted tiers -- a long main
+// array and a middle array in global memory, a fresh array in shared memory -- and a register
+// bag R of <= 32 entries (one per lane, unsorted) that takes the small addends (apparent
+// coboundaries, short stored columns): an insertion is a push through shared memory and a
+// __match_any_sync for the cancellations, its minimum two __reduce_min_sync, instead of a sorted
+// insertion.  Equal values in different tiers cancel lazily, when they reach the heads.  The
+// heads of M, G and F are cached in registers and refreshed only for the tier that moved.
+
+// head of M[h:] / G[g0:] from the register windows (the next 32 entries, one per lane, reloaded
+// with one coalesced load when the head leaves the window or the tier is rewritten)
+template <class CT>
+__device__ __forceinline__ uint64_t head_m(CT& c, int lane) {
+  if (c.mstale || c.h >= c.wb + 32) {
+    c.wb = c.h;
+    c.mwin = c.h + lane < c.nm ? ldcg64(c.Mc + c.h + lane) : NONE64;
+    c.mstale = false;
+    if (CT::dbg) ++c.tpm;
+  }
+  return __shfl_sync(0xFFFFFFFFu, c.mwin, c.h - c.wb);
+}
+template <class CT>
+__device__ __forceinline__ uint64_t head_g(CT& c, int lane) {
+  if (c.gstale || c.g0 >= c.gwb + 32) {
+    c.gwb = c.g0;
+    c.gwin = c.g0 + lane < c.ng ? ldcg64(c.Gc + c.g0 + lane) : NONE64;
+    c.gstale = false;
+    if (CT::dbg) ++c.tpg;
+  }
+  return __shfl_sync(0xFFFFFFFFu, c.gwin, c.g0 - c.gwb);
+}
+template <class CT>
+__device__ __forceinline__ uint64_t head_f(CT& c) {
+  return c.f0 < c.nf ? c.Fc[c.f0] : NONE64;
+}
+template <class CT>
+__device__ __forceinline__ void refresh_heads(CT& c, int lane) {
+  c.ha = head_m(c, lane);
+  c.hg = head_g(c, lane);
+  c.hb = head_f(c);
+  c.hstale = false;
+}
+
+// min over the lanes of a 64-bit key (NONE64 if every lane holds NONE64): two 32-bit reductions
+__device__ __forceinline__ uint64_t bag_min(uint64_t v) {
+  const uint32_t hi = __reduce_min_sync(0xFFFFFFFFu, uint32_t(v >> 32));
+  const uint32_t lo = __reduce_min_sync(0xFFFFFFFFu, uint32_t(v >> 32) == hi ? uint32_t(v) : ~0u);
+  return (uint64_t(hi) << 32) | lo;
+}
+// remove R's minimum
+template <class CT>
+__device__ __forceinline__ void bag_pop(CT& c) {
+  if (c.rv == c.rmin) c.rv = NONE64;
+  --c.nr;
+  c.rmin = bag_min(c.rv);
+}
+// R <- R xor Y for the pairwise distinct keys y held by the lanes in vm (requires nr + |vm| <=
+// 32): the y's go to the free lanes in order (through `scratch`), then a key present twice (a y
+// equal to an R entry) leaves both lanes.  Warp-collective.
+template <class CT>
+__device__ __forceinline__ void bag_insert(CT& c, uint64_t y, unsigned vm, uint64_t* scratch,
+                                           int lane) {
+  const unsigned lt = (1u << lane) - 1;
+  const unsigned fm = __ballot_sync(0xFFFFFFFFu, c.rv == NONE64);
+  if ((vm >> lane) & 1u) scratch[__popc(vm & lt)] = y;
+  __syncwarp();
+  const uint32_t ny = __popc(vm);
+  const uint32_t j = __popc(fm & lt);
+  if (((fm >> lane) & 1u) && j < ny) c.rv = scratch[j];
+  __syncwarp();
+  const unsigned peers = __match_any_sync(0xFFFFFFFFu, c.rv);
+  const bool dup = c.rv != NONE64 && (peers & (peers - 1)) != 0;
+  const unsigned dm = __ballot_sync(0xFFFFFFFFu, dup);
+  if (dup) c.rv = NONE64;
+  c.nr = c.nr + ny - __popc(dm);
+  c.rmin = bag_min(c.rv);
+}
+// the bag sorted ascending across the lanes (empty lanes, NONE64, last): bitonic network
+__device__ __forceinline__ uint64_t bag_sorted(uint64_t v, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+      const bool takemin = ((lane & j) == 0) == ((lane & k) == 0);
+      v = takemin ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  }
+  return v;
+}
+
+// pivot = min of the tier heads, cancelling equal pairs; NONE64 if the column is zero.
+// c.pt: the tier it heads (3 = R).  Warp-collective.
 template <class CT>
 __device__ __forceinline__ uint64_t take_pivot(CT& c, int lane) {
+  if (c.hstale) refresh_heads(c, lane);
   while (true) {
     if (CT::dbg) ++c.tpi;
-    if (c.mstale || c.h >= c.wb + 32) {
-      c.wb = c.h;
-      c.mwin = c.h + lane < c.nm ? ldcg64(c.Mc + c.h + lane) : NONE64;
-      c.mstale = false;
-      if (CT::dbg) ++c.tpm;
-    }
-    if (c.gstale || c.g0 >= c.gwb + 32) {
-      c.gwb = c.g0;
-      c.gwin = c.g0 + lane < c.ng ? ldcg64(c.Gc + c.g0 + lane) : NONE64;
-      c.gstale = false;
-      if (CT::dbg) ++c.tpg;
-    }
-    const uint64_t a = __shfl_sync(0xFFFFFFFFu, c.mwin, c.h - c.wb);
-    const uint64_t g = __shfl_sync(0xFFFFFFFFu, c.gwin, c.g0 - c.gwb);
-    const uint64_t b = c.f0 < c.nf ? c.Fc[c.f0] : NONE64;
-    const uint64_t rr = __shfl_sync(0xFFFFFFFFu, c.rv, c.r0 & 31);
-    const uint64_t r = c.r0 < c.nr ? rr : NONE64;
+    const uint64_t a = c.ha, g = c.hg, b = c.hb, r = c.rmin;
     const uint64_t m1 = a < g ? a : g, m2 = b < r ? b : r;
     const uint64_t m = m1 < m2 ? m1 : m2;
     if (m == NONE64) return NONE64;
@@ -533,10 +603,25 @@ __device__ __forceinline__ uint64_t take_pivot(CT& c, int lane) {
     c.pt = er ? 3u : (eb ? 2u : (eg ? 1u : 0u));
     if (k == 1) return m;
     int drop = k == 3 ? 2 : k;
-    if (ea && drop) ++c.h, --drop;
-    if (eg && drop) ++c.g0, --drop;
-    if (eb && drop) ++c.f0, --drop;
-    if (er && drop) ++c.r0, --drop;
+    if (ea && drop) {
+      ++c.h;
+      c.ha = head_m(c, lane);
+      --drop;
+    }
+    if (eg && drop) {
+      ++c.g0;
+      c.hg = head_g(c, lane);
+      --drop;
+    }
+    if (eb && drop) {
+      ++c.f0;
+      c.hb = head_f(c);
+      --drop;
+    }
+    if (er && drop) {
+      bag_pop(c);
+      --drop;
+    }
     if (k == 3) return m;
   }
 }
@@ -545,106 +630,28 @@ __device__ __forceinline__ uint64_t take_pivot(CT& c, int lane) {
 // entry is the pivot then adds only the rest of it -- one take_pivot iteration and one insertion
 // fewer per addition than letting the two copies cancel at the heads.
 template <class CT>
-__device__ __forceinline__ void consume_pivot(CT& c) {
-  if (c.pt == 0) ++c.h;
-  else if (c.pt == 1) ++c.g0;
-  else if (c.pt == 2) ++c.f0;
-  else ++c.r0;
+__device__ __forceinline__ void consume_pivot(CT& c, int lane) {
+  if (c.pt == 0) {
+    ++c.h;
+    c.ha = head_m(c, lane);
+  } else if (c.pt == 1) {
+    ++c.g0;
+    c.hg = head_g(c, lane);
+  } else if (c.pt == 2) {
+    ++c.f0;
+    c.hb = head_f(c);
+  } else {
+    bag_pop(c);
+  }
 }
 
-// R <- R[r0:nr] xor B for a sorted B of nb <= SMALLB entries in shared memory, with
-// (nr - r0) + nb <= 32.  Lane k < nb places B[k] by a shuffle binary search over R; every lane
-// holds all of B in registers to place its own R entry; the new list goes through `scratch`
-// (>= 40 entries).  Warp-collective.
+// R <- R xor B for a sorted B of nb <= SMALLB entries in shared memory (nr + nb <= 32).
 template <class CT>
 __device__ __forceinline__ void r_insert(CT& c, const uint64_t* B, uint32_t nb, uint64_t* scratch,
                                          int lane) {
-  const uint32_t live = c.nr - c.r0;
   const uint64_t y = lane < int(nb) ? B[lane] : NONE64;
-  uint32_t lo = c.r0, hi = c.nr;
-#pragma unroll
-  for (int it = 0; it < 6; ++it) {  // positions [r0, nr] <= 33 values: 6 halvings
-    const uint32_t mid = (lo + hi) >> 1;
-    const uint64_t v = __shfl_sync(0xFFFFFFFFu, c.rv, mid & 31);
-    if (lo < hi) {
-      if (v < y) lo = mid + 1;
-      else hi = mid;
-    }
-  }
-  const uint64_t at = __shfl_sync(0xFFFFFFFFu, c.rv, lo & 31);
-  const bool ydup = lane < int(nb) && lo < c.nr && at == y;
-  const uint32_t bdup = __ballot_sync(0xFFFFFFFFu, ydup);
-  uint64_t bv[SMALLB];
-#pragma unroll
-  for (int k = 0; k < int(SMALLB); ++k) bv[k] = __shfl_sync(0xFFFFFFFFu, y, k);
-  const uint64_t x = c.rv;
-  uint32_t lessB = 0, D = 0;
-  bool dup = false;
-#pragma unroll
-  for (int k = 0; k < int(SMALLB); ++k) {
-    const bool lt = bv[k] < x;
-    lessB += lt ? 1u : 0u;
-    D += (lt && (bdup >> k & 1)) ? 1u : 0u;
-    dup |= bv[k] == x;
-  }
-  if (uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr && !dup)
-    scratch[(lane - c.r0) + lessB - 2 * D] = x;
-  if (lane < int(nb) && !ydup) scratch[lane + (lo - c.r0) - 2 * __popc(bdup & ((1u << lane) - 1))] = y;
-  __syncwarp();
-  const uint32_t n = live + nb - 2 * __popc(bdup);
-  c.rv = uint32_t(lane) < n ? scratch[lane] : NONE64;
-  c.nr = n;
-  c.r0 = 0;
-  __syncwarp();
-}
-
-// R <- R[r0:nr] xor Y for the (unsorted, pairwise distinct) keys y held by the lanes in vm --
-// the apparent partner's coboundary, straight from spec_issue's registers: no sort through
-// shared memory and no binary search.  Each y is broadcast once; two ballots give its rank in R
-// and whether it cancels an R entry; an R entry moves by the kept y below it minus the cancelled
-// entries before it.  Requires (nr - r0) + popc(vm) <= 32.  Warp-collective.
-template <class CT>
-__device__ __forceinline__ void r_insert_lanes(CT& c, uint64_t y, unsigned vm, uint64_t* scratch,
-                                               int lane) {
-  const bool mine = uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr;  // lane holds a live R entry
-  const uint64_t x = c.rv;
-  const unsigned lt = (1u << lane) - 1;
-  unsigned rem = 0;       // live R entries cancelled by some y
-  uint32_t keptb = 0;     // (R lanes) kept y below x
-  uint32_t yrank = 0;     // (y lanes) live R entries below y
-  uint32_t ybelow = 0;    // (y lanes) kept y' below y
-  bool ydup = false;      // (y lanes) y cancels an R entry
-  unsigned ymask = 0;     // lanes of the y's that cancel
-  for (unsigned m = vm; m; m &= m - 1) {
-    const int src = __ffs(m) - 1;
-    const uint64_t v = __shfl_sync(0xFFFFFFFFu, y, src);
-    const unsigned ltv = __ballot_sync(0xFFFFFFFFu, mine && x < v);
-    const unsigned eqv = __ballot_sync(0xFFFFFFFFu, mine && x == v);
-    rem |= eqv;
-    if (eqv) ymask |= 1u << src;
-    if (lane == src) {
-      yrank = __popc(ltv);
-      ydup = eqv != 0;
-    }
-    if (!eqv) {
-      if (mine && v < x) ++keptb;
-      if ((vm >> lane & 1) && v < y) ++ybelow;
-    }
-  }
-  const unsigned livem = __ballot_sync(0xFFFFFFFFu, mine);
-  if (mine && !(rem >> lane & 1))
-    scratch[(lane - c.r0) - __popc(rem & lt & livem) + keptb] = x;
-  if ((vm >> lane & 1) && !ydup) {
-    // removed R entries below y: the cancelled lanes among the first yrank live ones
-    const unsigned below = livem & ((yrank + c.r0) >= 32 ? 0xFFFFFFFFu : ((1u << (yrank + c.r0)) - 1));
-    scratch[yrank - __popc(rem & below) + ybelow] = y;
-  }
-  __syncwarp();
-  const uint32_t n = (c.nr - c.r0) - __popc(rem) + (__popc(vm) - __popc(ymask));
-  c.rv = uint32_t(lane) < n ? scratch[lane] : NONE64;
-  c.nr = n;
-  c.r0 = 0;
-  __syncwarp();
+  __syncwarp();  // B may be `scratch`'s neighbour: read before the pushes
+  bag_insert(c, y, nb >= 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u), scratch, lane);
 }
 
 // The apparent-partner coboundary, speculated.  A DOWN pivot t (a (d+1)-cell) is the upper cell
@@ -879,6 +886,7 @@ template <class CT>
 __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
   const uint32_t na = c.ng - c.g0, nb = c.nf - c.f0;
   if (nb == 0) return true;
+  c.hstale = true;
   const long long t0 = CT::dbg ? clock64() : 0;
   uint32_t n;
   if (na == 0) {
@@ -918,10 +926,11 @@ constexpr unsigned long long POOL_CHUNK = 4096;  // pool entries a warp reserves
 // F <- F xor R, R emptied (flushing F into M first if it cannot take R).  Warp-collective.
 template <class CT>
 __device__ __forceinline__ bool spill_r(CT& c, const RP& P, uint64_t* scratch, int lane) {
-  const uint32_t live = c.nr - c.r0;
+  const uint32_t live = c.nr;
   if (live > 0) {
     if ((c.nf - c.f0) + live > FCAP && !flush(c, P, lane)) return false;
-    if (uint32_t(lane) >= c.r0 && uint32_t(lane) < c.nr) scratch[lane - c.r0] = c.rv;
+    const uint64_t v = bag_sorted(c.rv, lane);  // R's entries ascending in lanes [0, live)
+    if (uint32_t(lane) < live) scratch[lane] = v;
     __syncwarp();
     if (c.nf == c.f0) {
       if (uint32_t(lane) < live) c.Fc[lane] = scratch[lane];
@@ -933,9 +942,11 @@ __device__ __forceinline__ bool spill_r(CT& c, const RP& P, uint64_t* scratch, i
     }
     c.f0 = 0;
     __syncwarp();
+    c.hstale = true;
   }
   c.rv = NONE64;
-  c.nr = c.r0 = 0;
+  c.nr = 0;
+  c.rmin = NONE64;
   return true;
 }
 
@@ -950,7 +961,7 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
       B = small;
     }
     const long long t0 = CT::dbg ? clock64() : 0;
-    if ((c.nr - c.r0) + nb > 32) {
+    if (c.nr + nb > 32) {
       if (!spill_r(c, P, stage, lane)) return false;
       if (CT::dbg) ++c.nsp;
     }
@@ -962,6 +973,7 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
     }
     return true;
   }
+  c.hstale = true;  // F or M is rewritten below
   if (BG && (c.nf - c.f0) + nb <= FCAP) {
     // STAGE entries at a time: one coalesced load each instead of a dependent global binary
     // search per F entry (F xor B = F xor B[0:64] xor B[64:128] ...)
@@ -1221,8 +1233,10 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     c.cap = P.mcap;
     c.spare = nullptr;
     c.rv = NONE64;
-    c.nr = c.r0 = 0;
+    c.nr = 0;
+    c.rmin = NONE64;
     c.mstale = true;
+    c.hstale = true;
     c.nf = coboundary(P, cell, c.Fc, lane);
     const unsigned long long c_t0 = DBG ? gtimer() : 0;
     unsigned c_pre = 0;     // debug: apparent additions before the first non-apparent pivot
@@ -1274,14 +1288,14 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         const uint64_t y = (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD)
                                ? rkey(P, sp.birth, sp.cell) : NONE64;
         const unsigned vm = __ballot_sync(0xFFFFFFFFu, y != NONE64);
-        consume_pivot(c);
+        consume_pivot(c, lane);
         if (DBG && c_inpre) ++c_pre;
         const uint32_t ny = __popc(vm);
         addlen += c.len() + ny;
         if (ny) {
-          if ((c.nr - c.r0) + ny > 32) ok = spill_r(c, P, s_stage[wib], lane);
+          if (c.nr + ny > 32) ok = spill_r(c, P, s_stage[wib], lane);
           if (!ok) break;
-          r_insert_lanes(c, y, vm, s_stage[wib], lane);
+          bag_insert(c, y, vm, s_stage[wib], lane);
         }
         ++adds;
         if (DBG) {
@@ -1301,7 +1315,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         add = P.pool + (oi >> OI_LEN_BITS) + 1;
         alen = uint32_t(oi & ((1u << OI_LEN_BITS) - 1)) - 1;
         glob = true;
-        consume_pivot(c);
+        consume_pivot(c, lane);
       } else {
         if (DBG) c_inpre = false;
         // unowned pivot: wait until no earlier column of the segment can end on it
