@@ -87,13 +87,28 @@ cr_status fail(const Error& e) {
 // Stack `batch` images along the slowest axis with one +inf separator layer between them, so the
 // complexes are disjoint (cells touching a separator are absent, reading R5).
 __global__ void k_stack(const float* __restrict__ src, int64_t per_img, int64_t layer,
-                        int64_t layers_per_img, int64_t total, float* __restrict__ dst) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  int64_t L = i / layer;  // layer index in the stacked image
-  int64_t b = L / (layers_per_img + 1), l = L % (layers_per_img + 1);
-  dst[i] = (l == layers_per_img) ? __int_as_float(0x7F800000)
-                                 : src[b * per_img + l * layer + (i % layer)];
+                        int64_t layers_per_img, int64_t nlayers, float* __restrict__ dst) {
+  // one stacked layer per blockIdx.y step (its image and slot computed once per block, not per
+  // element), 16-byte copies when the layer allows them
+  const bool v4 = (layer & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) |
+                                        reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  for (int64_t L = blockIdx.y; L < nlayers; L += gridDim.y) {
+    const int64_t b = L / (layers_per_img + 1), l = L % (layers_per_img + 1);
+    float* d = dst + L * layer;
+    const float* sp = src + b * per_img + l * layer;
+    const bool sep = l == layers_per_img;
+    const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t st = int64_t(gridDim.x) * blockDim.x;
+    if (v4) {
+      const float inf = __int_as_float(0x7F800000);
+      float4* d4 = reinterpret_cast<float4*>(d);
+      const float4* s4 = reinterpret_cast<const float4*>(sp);
+      for (int64_t i = t0; i < (layer >> 2); i += st)
+        d4[i] = sep ? make_float4(inf, inf, inf, inf) : __ldg(s4 + i);
+    } else {
+      for (int64_t i = t0; i < layer; i += st) d[i] = sep ? __int_as_float(0x7F800000) : __ldg(sp + i);
+    }
+  }
 }
 
 // Batched emission: keep bars, sort by (image, dim, local kidx), write CSR offsets.
@@ -382,8 +397,15 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
     st.path = 3;
     prof_begin(s);
     float* simg = ws.alloc<float>(g.nvox);
-    k_stack<<<grid_for(g.nvox, 256), 256, 0, s>>>(images, layers * layer, layer, layers, g.nvox,
-                                                   simg);
+    {
+      const int64_t nlayers = g.nvox / layer;
+      int64_t bx = (layer / 4 + 255) / 256;
+      if (bx < 1) bx = 1;
+      if (bx > 64) bx = 64;
+      const unsigned by = unsigned(nlayers < 65535 ? nlayers : 65535);
+      k_stack<<<dim3(unsigned(bx), by), 256, 0, s>>>(images, layers * layer, layer, layers,
+                                                     nlayers, simg);
+    }
     CR_CHECK_LAUNCH();
     GeneralState S;
     {  // Khalimsky cells per image period along the stacking axis: kidx / seg_cells = image

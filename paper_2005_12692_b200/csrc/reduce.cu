@@ -1039,15 +1039,6 @@ __device__ __forceinline__ int ld_rlx_i32(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint64_t warp_min(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    v = w < v ? w : v;
-  }
-  return v;
-}
-
 // The first column i in [x, j) whose published candidate is <= p (it may still end on p, or is
 // not started), or j if there is none.  Warp-collective.  Chunks of 32^L columns whose bound
 // lv[L] exceeds p are skipped whole, 32 chunks per load.  The chunks whose bound does not are
@@ -1135,7 +1126,7 @@ __device__ __forceinline__ void finish_column(const RP& P, uint32_t j, int lane)
   for (int L = 1; L <= 3; ++L) {
     e >>= 5;
     const uint64_t cv = ld_rlx(P.lv[L - 1] + (uint64_t(e) << 5) + lane);
-    const uint64_t mn = warp_min(cv);
+    const uint64_t mn = bag_min(cv);  // two 32-bit reductions instead of five 64-bit shuffles
     if (lane == 0 && mn > ld_rlx(P.lv[L] + e)) {
       atomicMax(reinterpret_cast<unsigned long long*>(P.lv[L] + e), mn);
       __threadfence();
