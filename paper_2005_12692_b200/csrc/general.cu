@@ -1093,7 +1093,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
                  GeneralState& S, cr_stats& st) {
   cudaStream_t s = ws.stream();
   S.g = g;
-  const int B = 256;
   S.births = ws.alloc<uint32_t>(g.ncells);
   S.tags = ws.alloc<uint8_t>(g.ncells);
   unsigned long long* cnt = ws.alloc<unsigned long long>(32);

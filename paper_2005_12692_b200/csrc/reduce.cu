@@ -713,138 +713,6 @@ __device__ __forceinline__ Spec spec_issue(const RP& P, const SpecLane& L, uint3
   return r;
 }
 
-// C = A xor F for a long A (global) and a short F (shared, b <= FCAP), C in global memory, using
-// X (FCAP u64 of shared scratch).  Warp-collective; returns |C|.
-//  1. positions: P[t] = #{A < F[t]} by a sampled search (<= 256 samples of A in X, then a binary
-//     search inside one sample interval; a lane's <= 8 searches run interleaved), dup[t] = (A[P[t]]
-//     == F[t]); prefix counts of inserted (non-dup) and cancelled (dup) F entries over t;
-//  2. the non-dup F entries go to P[t] + ins_before(t) - dup_before(t);
-//  3. A streams through in windows of 256 (8 independent loads per lane): A[i] moves to
-//     i + #{non-dup t : P[t] <= i} - #{dup t : P[t] < i}, unless a dup lands on it.  A window that
-//     holds no position only shifts (one smem search per window).
-__device__ __noinline__ uint32_t merge_long_short(const uint64_t* __restrict__ A, uint32_t a, const uint64_t* F,
-                                     uint32_t b, uint64_t* __restrict__ C, uint64_t* X, int lane) {
-  constexpr int R = FCAP / 32;  // F entries per lane (t = lane + 32 r)
-  constexpr int G = R;          // all of a lane's searches run interleaved
-  constexpr uint32_t NS = FCAP / 2;
-  const unsigned lt = (1u << lane) - 1;
-  uint32_t* XP = reinterpret_cast<uint32_t*>(X + NS);  // P[t]            (upper half of X)
-  uint32_t* XC = reinterpret_cast<uint32_t*>(X);       // prefix counts   (lower half, later)
-  // ---- 1. <= NS samples of A in X[0, NS)
-  const uint32_t S = a > NS ? (a + NS - 1) / NS : 1u;
-  const uint32_t ns = a ? (a + S - 1) / S : 0u;
-  for (uint32_t sidx = lane; sidx < ns; sidx += 32) X[sidx] = ldcg64(A + uint64_t(sidx) * S);
-  __syncwarp();
-  uint32_t dupm = 0;
-#pragma unroll
-  for (int g0 = 0; g0 < R; g0 += G) {
-    uint32_t lo[G], hi[G];
-    uint64_t f[G];
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      const uint32_t t = lane + 32 * (g0 + q);
-      f[q] = t < b ? F[t] : NONE64;
-      uint32_t l = 0, h = ns;  // l = #samples < f; the answer lies in (l-1)*S+1 .. min(a, l*S)
-      while (l < h) {
-        const uint32_t m = (l + h) >> 1;
-        if (X[m] < f[q]) l = m + 1;
-        else h = m;
-      }
-      lo[q] = l ? (l - 1) * S + 1 : 0u;
-      hi[q] = l ? min(a, l * S) : 0u;
-      if (t >= b) lo[q] = hi[q] = 0;
-    }
-    bool busy = true;
-    while (busy) {  // interleaved binary searches: lower_bound of f in A[lo, hi)
-      busy = false;
-      uint64_t v[G];
-#pragma unroll
-      for (int q = 0; q < G; ++q)
-        if (lo[q] < hi[q]) v[q] = ldcg64(A + ((lo[q] + hi[q]) >> 1));
-#pragma unroll
-      for (int q = 0; q < G; ++q)
-        if (lo[q] < hi[q]) {
-          const uint32_t m = (lo[q] + hi[q]) >> 1;
-          if (v[q] < f[q]) lo[q] = m + 1;
-          else hi[q] = m;
-          busy |= lo[q] < hi[q];
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      const uint32_t t = lane + 32 * (g0 + q);
-      if (t < b) {
-        if (lo[q] < a && ldcg64(A + lo[q]) == f[q]) dupm |= 1u << (g0 + q);
-        XP[t] = lo[q];
-      }
-    }
-  }
-  __syncwarp();  // the samples are dead: XC takes the lower half
-  uint32_t totI = 0, totD = 0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t t = lane + 32 * r;
-    const bool valid = t < b, dup = dupm >> r & 1;
-    const unsigned bi = __ballot_sync(0xFFFFFFFFu, valid && !dup);
-    const unsigned bd = __ballot_sync(0xFFFFFFFFu, valid && dup);
-    const uint32_t ci = totI + __popc(bi & lt), cd = totD + __popc(bd & lt);
-    if (valid) {
-      XC[t] = (uint32_t(dup) << 31) | (cd << 16) | ci;
-      if (!dup) C[XP[t] + ci - cd] = F[t];  // 2. the inserted F entries
-    }
-    totI += __popc(bi);
-    totD += __popc(bd);
-  }
-  __syncwarp();
-  // ---- 3. stream A in windows of 256, software-pipelined (the next window's loads are in flight
-  // while this one is placed).  The F entries landing in a window, [tl, th), are walked once per
-  // window (broadcast shared reads) against all 8 of a lane's entries at once.
-  uint64_t nv[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t i = lane + 32 * k;
-    nv[k] = i < a ? ldcg64(A + i) : 0ull;
-  }
-  uint32_t tl = 0;
-  for (uint32_t w0 = 0; w0 < a; w0 += 256) {
-    uint64_t v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      v[k] = nv[k];
-      const uint32_t i = w0 + 256 + lane + 32 * k;
-      nv[k] = i < a ? ldcg64(A + i) : 0ull;
-    }
-    uint32_t th = tl;
-    while (th < b && XP[th] < w0 + 256) ++th;
-    const uint32_t cl = tl < b ? XC[tl] & 0x7FFFFFFFu : ((totD << 16) | totI);
-    uint32_t ins[8], rem[8];
-    uint32_t removed = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      ins[k] = cl & 0xFFFFu;
-      rem[k] = cl >> 16;
-    }
-    for (uint32_t t = tl; t < th; ++t) {
-      const uint32_t pt = XP[t];
-      const bool dup = XC[t] >> 31;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t i = w0 + lane + 32 * k;
-        ins[k] += (!dup && pt <= i) ? 1u : 0u;
-        rem[k] += (dup && pt < i) ? 1u : 0u;
-        removed |= (dup && pt == i) ? (1u << k) : 0u;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t i = w0 + lane + 32 * k;
-      if (i < a && !(removed >> k & 1)) C[i + ins[k] - rem[k]] = v[k];
-    }
-    tl = th;
-  }
-  __syncwarp();
-  return a + totI - totD;
-}
 
 
 // Make room for a merge of `need` entries into M[mb ^ 1]: a column that outgrows its warp's slot
