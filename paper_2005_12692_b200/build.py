@@ -17,7 +17,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O2", "-shared",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v" if os.environ.get("CR_PTXAS_VERBOSE") else "-O3",
-]
+] + (["-DCR_DEVICE_ASSERTS"] if os.environ.get("CR_DEVICE_ASSERTS") else [])
 
 
 def sources():

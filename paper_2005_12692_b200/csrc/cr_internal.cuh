@@ -109,6 +109,24 @@ void prof_fill(cr_stats& st);  // stage times of the last call, if no call began
     }                                                                                       \
   } while (0)
 
+// Device-side bounds assertions (build with CR_DEVICE_ASSERTS=1, see build.py): compiled out of
+// the normal build.  The pool's compute-sanitizer is closed (profiles/r02/sanitizer), so the
+// capacity invariants of the working-column tiers, merges, sort and stores are checked by these
+// instead; a failure prints the site and traps (the call fails with CR_ECUDA).
+#ifdef CR_DEVICE_ASSERTS
+#define CR_DASSERT(c)                                                                  \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("CR_DASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);                  \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define CR_DASSERT(c) \
+  do {                \
+  } while (0)
+#endif
+
 extern thread_local int64_t g_launch_count;
 #define CR_CHECK_LAUNCH()                \
   do {                                   \

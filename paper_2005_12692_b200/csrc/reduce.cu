@@ -513,6 +513,7 @@ __device__ __forceinline__ uint64_t head_m(CT& c, int lane) {
     c.mstale = false;
     if (CT::dbg) ++c.tpm;
   }
+  CR_DASSERT(c.h - c.wb < 32);
   return __shfl_sync(0xFFFFFFFFu, c.mwin, c.h - c.wb);
 }
 template <class CT>
@@ -523,6 +524,7 @@ __device__ __forceinline__ uint64_t head_g(CT& c, int lane) {
     c.gstale = false;
     if (CT::dbg) ++c.tpg;
   }
+  CR_DASSERT(c.g0 - c.gwb < 32);
   return __shfl_sync(0xFFFFFFFFu, c.gwin, c.g0 - c.gwb);
 }
 template <class CT>
@@ -557,6 +559,7 @@ template <class CT>
 __device__ __forceinline__ void bag_insert(CT& c, uint64_t y, unsigned vm, uint64_t* scratch,
                                            int lane) {
   const unsigned lt = (1u << lane) - 1;
+  CR_DASSERT(c.nr + __popc(vm) <= 32);
   const unsigned fm = __ballot_sync(0xFFFFFFFFu, c.rv == NONE64);
   if ((vm >> lane) & 1u) scratch[__popc(vm & lt)] = y;
   __syncwarp();
@@ -764,6 +767,7 @@ __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
   } else {
     n = merge_xor_path_g(c.Gc + c.g0, na, c.Fc + c.f0, nb, c.Ga, lane);
   }
+  CR_DASSERT(n <= GCAP + FCAP);
   { uint64_t* t = c.Gc; c.Gc = c.Ga; c.Ga = t; }
   c.ng = n;
   c.g0 = 0;
@@ -774,6 +778,7 @@ __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
     if (!grow(c, nm + c.ng, P, lane)) return false;
     const uint32_t n2 = merge_chunked<true>(c.Mc + c.h, nm, c.Gc, c.ng, c.Ma,
                                             c.Fc, c.Fa, lane);
+    CR_DASSERT(n2 <= c.cap);
     swap_main(c);
     c.nm = n2;
     c.h = 0;
@@ -809,6 +814,7 @@ __device__ __forceinline__ bool spill_r(CT& c, const RP& P, uint64_t* scratch, i
       { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     }
     c.f0 = 0;
+    CR_DASSERT(c.nf <= FCAP);
     __syncwarp();
     c.hstale = true;
   }
@@ -856,6 +862,7 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
       { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
       c.nf = n;
       c.f0 = 0;
+      CR_DASSERT(c.nf <= FCAP);
     }
     return true;
   }
@@ -864,6 +871,7 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
     { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     c.nf = n;
     c.f0 = 0;
+    CR_DASSERT(c.nf <= FCAP);
     return true;
   }
   if ((c.nf - c.f0) + nb <= FCAP) {
@@ -872,6 +880,7 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
     { uint64_t* t = c.Fc; c.Fc = c.Fa; c.Fa = t; }
     c.nf = n;
     c.f0 = 0;
+    CR_DASSERT(c.nf <= FCAP);
     return true;
   }
   if (!flush(c, P, lane)) return false;
@@ -885,6 +894,7 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
   if (!grow(c, (c.nm - c.h) + nb, P, lane)) return false;
   const uint32_t n = merge_chunked<BG>(c.Mc + c.h, c.nm - c.h, B, nb, c.Ma,
                                        c.Fc, c.Fa, lane);
+  CR_DASSERT(n <= c.cap);
   swap_main(c);
   c.nm = n;
   c.h = 0;
@@ -1254,6 +1264,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         uint32_t n;
         if (c.nm == c.h && c.ng == c.g0) {  // held in F alone (most columns): a copy
           n = c.nf - c.f0;
+          CR_DASSERT(off + n <= P.pool_cap);
           for (uint32_t i = lane; i < n; i += 32) P.pool[off + i] = c.Fc[c.f0 + i];
           __syncwarp();
         } else if (c.ng > c.g0) {

@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_os_pass(
     const unsigned d = OS_DG(r);
     if (d < OS_RADIX) {
       const unsigned pos = S.toff[d] + S.wcnt[w][d] + rk[r];
+      CR_DASSERT(pos < unsigned(OS_TILE));
       S.k[pos] = k[r];
       if (HASV) S.v[pos] = v[r];
     }
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_os_pass(
     const K kk = S.k[i];
     const unsigned d = os_digit(kk, shift, desc);
     const unsigned long long o = S.gbase[d] + unsigned(i - S.toff[d]);
+    CR_DASSERT(o < (unsigned long long)n);
     kout[o] = kk;
     if (HASV) vout[o] = S.v[i];
   }
