@@ -36,6 +36,11 @@
 namespace cr {
 namespace {
 
+#ifdef K5_TIMING  // measurement builds only: per-phase cycles of the heavy columns, printed
+#define KT(...) __VA_ARGS__
+#else
+#define KT(...)
+#endif
 constexpr int WPB = 8;  // warps per block
 constexpr int THREADS = WPB * 32;
 #ifndef K5_FCAP
@@ -1119,6 +1124,8 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     unsigned long long d_tp = 0, d_lk = 0, d_app = 0, d_pool = 0, d_napp = 0, d_plen = 0;
     unsigned long long c_adds = adds, c_wait = 0, c_waits = waits;
     uint32_t c_blk = NONE32;
+    KT(unsigned long long kt_piv = 0, kt_mem = 0, kt_cons = 0, kt_spill = 0, kt_ins = 0, kt_app = 0;
+       const long long kt_c0 = clock64();)
     uint64_t pub = 0;      // last published candidate
     uint64_t xp = NONE64;  // the pivot the scan cursor x is valid for
     uint32_t x = seg_lo;
@@ -1126,7 +1133,9 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
     bool ok = true;
     while (true) {
       const long long q0 = DBG ? clock64() : 0;
+      KT(const long long k0 = clock64();)
       const uint64_t piv = take_pivot(c, lane);
+      KT(const long long k1 = clock64(); kt_piv += k1 - k0;)
       const long long q1 = CT::dbg ? clock64() : 0;
       d_tp += q1 - q0;
       if (piv == NONE64) {  // zero column: essential (exact given the clearing)
@@ -1157,15 +1166,20 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         const uint64_t y = (lane < 30 && lane / 5 == dir && sp.birth != ABSENT_ORD)
                                ? rkey(P, sp.birth, sp.cell) : NONE64;
         const unsigned vm = __ballot_sync(0xFFFFFFFFu, y != NONE64);
+        KT(const long long k2 = clock64(); kt_mem += k2 - k1;)
         consume_pivot(c, lane);
+        KT(const long long k3 = clock64(); kt_cons += k3 - k2;)
         if (DBG && c_inpre) ++c_pre;
         const uint32_t ny = __popc(vm);
         addlen += c.len() + ny;
         if (ny) {
           if (c.nr + ny > 32) ok = spill_r(c, P, s_stage[wib], lane);
           if (!ok) break;
+          KT(const long long k4 = clock64(); kt_spill += k4 - k3;)
           bag_insert(c, y, vm, s_stage[wib], lane);
+          KT(kt_ins += clock64() - k4;)
         }
+        KT(++kt_app;)
         ++adds;
         if (DBG) {
           d_app += clock64() - q2;
@@ -1313,6 +1327,11 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
       maxlen = l > maxlen ? l : maxlen;
     }
     if (!ok) break;
+    KT(if (lane == 0 && kt_app > 2000)
+         printf("K5T col %u: %llu cycles, %llu apparent adds; per add: pivot %.0f mem %.0f consume %.0f "
+                "spill %.0f insert %.0f\n", j, (unsigned long long)(clock64() - kt_c0), kt_app,
+                double(kt_piv) / kt_app, double(kt_mem) / kt_app, double(kt_cons) / kt_app,
+                double(kt_spill) / kt_app, double(kt_ins) / kt_app);)
     const long long tfin0 = DBG ? clock64() : 0;
     finish_column(P, j, lane);
     if (DBG && lane == 0) {
