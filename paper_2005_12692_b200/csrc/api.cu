@@ -407,6 +407,7 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
                                                      nlayers, simg);
     }
     CR_CHECK_LAUNCH();
+    prof_mark(s, "stack");  // its own stage: "filtration" then times k_filtration alone
     GeneralState S;
     {  // Khalimsky cells per image period along the stacking axis: kidx / seg_cells = image
       uint64_t cl = 1;
