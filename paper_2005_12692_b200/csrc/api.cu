@@ -111,6 +111,18 @@ __global__ void k_stack(const float* __restrict__ src, int64_t per_img, int64_t 
   }
 }
 
+// +inf in the separator layers of a stacked batch (layer L of image b: stacked layer
+// (b + 1)(L + 1) - 1, for b < batch - 1)
+__global__ void k_separators(float* __restrict__ dst, int64_t layer, int64_t layers_per_img,
+                             int64_t nsep) {
+  for (int64_t b = blockIdx.y; b < nsep; b += gridDim.y) {
+    float* d = dst + ((b + 1) * (layers_per_img + 1) - 1) * layer;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < layer;
+         i += int64_t(gridDim.x) * blockDim.x)
+      d[i] = __int_as_float(0x7F800000);
+  }
+}
+
 // Batched emission: keep bars, sort by (image, dim, local kidx), write CSR offsets.
 __global__ void k_batch_keys(const uint64_t* __restrict__ rec, int64_t n, int dim,
                              const uint32_t* __restrict__ births, uint32_t cells_per_layer_k,
@@ -195,6 +207,46 @@ int64_t barcodes_core(const float* image, const Geom& g, int maxdim, cr_pair* ou
 }
 
 void set_last_stats(const cr_stats& st) { commit_stats(st); }
+
+// cr_barcodes_batched_host: copy the host batch straight into the stacked layout on a second
+// stream, in up to 8 pieces, each piece's event telling run_general's filtration which z-planes
+// have arrived (the filtration of the first pieces overlaps the copy of the later ones).
+static void stage_host_batch(const float* host, int64_t batch, int64_t L, int64_t layer,
+                             float* simg, GeneralState& S, cudaStream_t s) {
+  int dev = 0;
+  CR_CUDA(cudaGetDevice(&dev));
+  static thread_local int cs_dev = -1;
+  static thread_local cudaStream_t cs = nullptr;
+  static thread_local cudaEvent_t ev[17];
+  if (cs_dev != dev) {
+    CR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (auto& e : ev) CR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cs_dev = dev;
+  }
+  CR_CUDA(cudaEventRecord(ev[16], s));  // the buffer's previous users on s come first
+  CR_CUDA(cudaStreamWaitEvent(cs, ev[16], 0));
+  if (batch > 1) {
+    int64_t bx = (layer + 255) / 256;
+    if (bx > 64) bx = 64;
+    const unsigned by = unsigned(batch - 1 < 65535 ? batch - 1 : 65535);
+    k_separators<<<dim3(unsigned(bx), by), 256, 0, s>>>(simg, layer, L, batch - 1);
+    CR_CHECK_LAUNCH();
+  }
+  const int G = int(batch < 8 ? batch : 8);
+  const int64_t per = (batch + G - 1) / G;
+  S.nready = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += per) {
+    const int64_t b1 = b0 + per < batch ? b0 + per : batch;
+    CR_CUDA(cudaMemcpy2DAsync(simg + b0 * (L + 1) * layer, size_t((L + 1) * layer) * sizeof(float),
+                              host + b0 * L * layer, size_t(L * layer) * sizeof(float),
+                              size_t(L * layer) * sizeof(float), size_t(b1 - b0),
+                              cudaMemcpyHostToDevice, cs));
+    const int i = S.nready++;
+    CR_CUDA(cudaEventRecord(ev[i], cs));
+    S.ready_ev[i] = ev[i];
+    S.ready_z[i] = b1 * (L + 1);  // its volumes and the separator after them (written on s)
+  }
+}
 
 }  // namespace cr
 
@@ -344,12 +396,15 @@ cr_status cr_barcodes_host(const float* host_image, const int64_t* shape, int nd
   }
 }
 
-cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t* shape, int ndim,
-                              int maxdim, cr_pair* out_pairs, uint32_t* out_birth_cells,
-                              int64_t out_capacity, int64_t* out_offsets, int64_t* n_pairs,
-                              cr_stream_t stream) {
+// cr_barcodes_batched with the batch on the device (images) or, for the stacked general path,
+// in host memory (host_images: copied in pieces straight into the stacked layout).
+static cr_status batched_impl(const float* images, const float* host_images, int64_t batch,
+                              const int64_t* shape, int ndim, int maxdim, cr_pair* out_pairs,
+                              uint32_t* out_birth_cells, int64_t out_capacity,
+                              int64_t* out_offsets, int64_t* n_pairs, cr_stream_t stream) {
   if (!n_pairs || !out_offsets || batch < 0 || !valid_shape(shape, ndim) || maxdim < 0 ||
-      out_capacity < 0 || (out_capacity > 0 && !out_pairs) || (batch > 0 && !images))
+      out_capacity < 0 || (out_capacity > 0 && !out_pairs) ||
+      (batch > 0 && !images && !host_images))
     return CR_EINVAL;
   try {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -360,7 +415,7 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
       *n_pairs = 0;
       return CR_OK;
     }
-    if (g1.nz == 1 && batched_small_2d_fits(g1.ny, g1.nx) && !force_general()) {
+    if (images && g1.nz == 1 && batched_small_2d_fits(g1.ny, g1.nx) && !force_general()) {
       // small 2D images: one CTA per image, everything in shared memory
       Workspace ws(s);
       HostScalars hs;
@@ -397,7 +452,10 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
     st.path = 3;
     prof_begin(s);
     float* simg = ws.alloc<float>(g.nvox);
-    {
+    GeneralState S;
+    if (host_images) {
+      stage_host_batch(host_images, batch, L, layer, simg, S, s);
+    } else {
       const int64_t nlayers = g.nvox / layer;
       int64_t bx = (layer / 4 + 255) / 256;
       if (bx < 1) bx = 1;
@@ -408,7 +466,6 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
     }
     CR_CHECK_LAUNCH();
     prof_mark(s, "stack");  // its own stage: "filtration" then times k_filtration alone
-    GeneralState S;
     {  // Khalimsky cells per image period along the stacking axis: kidx / seg_cells = image
       uint64_t cl = 1;
       for (int i = 1; i < ndim; ++i) cl *= uint64_t(2 * shape[i] - 1);
@@ -461,6 +518,15 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
   }
 }
 
+cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t* shape, int ndim,
+                              int maxdim, cr_pair* out_pairs, uint32_t* out_birth_cells,
+                              int64_t out_capacity, int64_t* out_offsets, int64_t* n_pairs,
+                              cr_stream_t stream) {
+  if (batch > 0 && !images) return CR_EINVAL;
+  return batched_impl(images, nullptr, batch, shape, ndim, maxdim, out_pairs, out_birth_cells,
+                      out_capacity, out_offsets, n_pairs, stream);
+}
+
 cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, const int64_t* shape,
                                    int ndim, int maxdim, cr_pair* host_out_pairs,
                                    uint32_t* host_out_birth_cells, int64_t out_capacity,
@@ -479,7 +545,11 @@ cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, cons
     uint32_t* dcells = nullptr;
     int64_t* doff = nullptr;
     cr_status rs = CR_OK;
-    if (cudaMallocAsync(&dimg, in_bytes > 0 ? in_bytes : 4, s) != cudaSuccess ||
+    // the stacked general path takes the host batch in pieces (overlapping the copy with the
+    // filtration); the one-CTA-per-image 2D path and 1D batches take it whole
+    const bool staged = batch > 1 && ndim >= 2 &&
+                        !(g.nz == 1 && batched_small_2d_fits(g.ny, g.nx) && !force_general());
+    if ((!staged && cudaMallocAsync(&dimg, in_bytes > 0 ? in_bytes : 4, s) != cudaSuccess) ||
         cudaMallocAsync(&dout, size_t(cap) * sizeof(cr_pair), s) != cudaSuccess ||
         cudaMallocAsync(&doff, size_t(batch + 1) * sizeof(int64_t), s) != cudaSuccess ||
         (host_out_birth_cells &&
@@ -487,9 +557,15 @@ cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, cons
       cudaGetLastError();
       rs = CR_ENOMEM;
     } else {
-      if (in_bytes) CR_CUDA(cudaMemcpyAsync(dimg, host_images, in_bytes, cudaMemcpyHostToDevice, s));
-      rs = cr_barcodes_batched(dimg, batch, shape, ndim, maxdim, dout, dcells, out_capacity, doff,
-                               n_pairs, stream);
+      if (staged) {
+        rs = batched_impl(nullptr, host_images, batch, shape, ndim, maxdim, dout, dcells,
+                          out_capacity, doff, n_pairs, stream);
+      } else {
+        if (in_bytes)
+          CR_CUDA(cudaMemcpyAsync(dimg, host_images, in_bytes, cudaMemcpyHostToDevice, s));
+        rs = cr_barcodes_batched(dimg, batch, shape, ndim, maxdim, dout, dcells, out_capacity,
+                                 doff, n_pairs, stream);
+      }
       if (rs == CR_OK) {
         CR_CUDA(cudaMemcpyAsync(host_out_offsets, doff, size_t(batch + 1) * sizeof(int64_t),
                                 cudaMemcpyDeviceToHost, s));

@@ -171,6 +171,7 @@ struct KfSmem {
 
 struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsky grid < 2^32 cells)
   uint32_t nx, ny, nz, KX, KXY, plane, XB, YB, zc;
+  uint32_t zb0;  // first z-chunk of this launch
 };
 inline KfP kf_params(const Geom& g, int zc) {
   KfP p;
@@ -183,6 +184,7 @@ inline KfP kf_params(const Geom& g, int zc) {
   p.XB = uint32_t((g.nx + 29) / 30);
   p.YB = uint32_t((g.ny + KF_ROWS - 1) / KF_ROWS);
   p.zc = uint32_t(zc);
+  p.zb0 = 0;
   return p;
 }
 
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(KF_THREADS, 2) k_filtration(const float* __res
   uint32_t blk = blockIdx.x;
   const int xb = int(blk % P.XB);
   blk /= P.XB;
-  const int yb = int(blk % P.YB), zb = int(blk / P.YB);
+  const int yb = int(blk % P.YB), zb = int(P.zb0 + blk / P.YB);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int x = xb * 30 - 1 + lane, y = yb * KF_ROWS - 1 + w;
   const int z0 = zb * int(P.zc), z1 = min(nz, z0 + int(P.zc));
@@ -1109,9 +1111,30 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
                                    int(sizeof(KfSmem))));
       kf_attr_dev = ws.device();
     }
-    k_filtration<<<L.grid, KF_THREADS, sizeof(KfSmem), s>>>(image, kf_params(g, L.zc), S.births,
-                                                            S.tags, cnt, nan_flag);
-    CR_CHECK_LAUNCH();
+    KfP kp = kf_params(g, L.zc);
+    const uint32_t nzc = uint32_t((g.nz + L.zc - 1) / L.zc), xy = kp.XB * kp.YB;
+    if (S.nready == 0) {
+      k_filtration<<<L.grid, KF_THREADS, sizeof(KfSmem), s>>>(image, kp, S.births, S.tags, cnt,
+                                                              nan_flag);
+      CR_CHECK_LAUNCH();
+    } else {
+      // input arriving in pieces: z-chunk c reads planes up to (c + 1) zc + 4; launch the chunks
+      // whose planes are in as each piece lands (the copies run on another stream)
+      uint32_t c0 = 0;
+      for (int i = 0; i < S.nready && c0 < nzc; ++i) {
+        uint32_t c1 = c0;
+        while (c1 < nzc && (i == S.nready - 1 ||
+                            int64_t(c1 + 1) * L.zc + 4 < S.ready_z[i]))
+          ++c1;
+        if (c1 == c0) continue;
+        CR_CUDA(cudaStreamWaitEvent(s, S.ready_ev[i], 0));
+        kp.zb0 = c0;
+        k_filtration<<<(c1 - c0) * xy, KF_THREADS, sizeof(KfSmem), s>>>(image, kp, S.births,
+                                                                        S.tags, cnt, nan_flag);
+        CR_CHECK_LAUNCH();
+        c0 = c1;
+      }
+    }
     prof_mark(s, "filtration");
   }
 

@@ -20,6 +20,12 @@ struct GeneralState {
                                // image); 0 for a single image
   bool top_only = false;       // compute only dimension D-1, by duality (cr_barcodes_topdim)
   bool lower_essential_known = false;  // cr_stats.essential[e] holds every e < current dim
+  // Input arriving in pieces (cr_barcodes_batched_host): planes [0, ready_z[i]) of the image are
+  // on the device once event ready_ev[i] has fired; the filtration launches its z-chunks as their
+  // planes (and the 4 after them it reads) arrive instead of waiting for the whole copy.
+  int nready = 0;
+  int64_t ready_z[16];
+  cudaEvent_t ready_ev[16];
   Records R;
 };
 
