@@ -459,9 +459,14 @@ __device__ __forceinline__ uint32_t kidx_vox(const Geom& g, uint32_t k) {
 // parent of every voxel in the apparent-pair forest, and the number of basins (present vertices
 // that are not the lower cell of an apparent pair) into *nbasins
 __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                            Geom g, uint32_t* __restrict__ parent, unsigned long long* nbasins) {
-  uint32_t v, x, y, z;
-  const bool in = vox_of_thread(g, v, x, y, z);
+                            Geom g, uint32_t* __restrict__ parent, unsigned long long* nbasins,
+                            uint32_t vbase, uint32_t vend) {
+  // voxels [vbase, vend) (a piece of the image: see run_general)
+  const uint64_t vv = uint64_t(vbase) + uint64_t(blockIdx.x) * VOX_THREADS + threadIdx.x;
+  const uint32_t v = uint32_t(vv);
+  const bool in = vv < vend;
+  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
+  const uint32_t r = v / nx, x = v - r * nx, z = r / ny, y = r - z * ny;
   bool basin = false;
   if (in) {
     const uint32_t k = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
@@ -484,8 +489,8 @@ __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* 
 }
 
 
-__global__ void k_pointer_jump(uint32_t* parent, int64_t n) {
-  int64_t vv = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void k_pointer_jump(uint32_t* parent, int64_t vbase, int64_t n) {
+  int64_t vv = vbase + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vv >= n) return;
   uint32_t v = uint32_t(vv);
   uint32_t p = parent[v];
@@ -1100,6 +1105,8 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   unsigned long long* cnt = ws.alloc<unsigned long long>(32);
   CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
+  uint32_t* parent = ws.alloc<uint32_t>(g.nvox);  // H0 basin forest
+  bool h0_forest_done = false;
 
   // K1 + K2 in one streaming kernel (round 1 measured the split alternatives, profiles/r01/s3:
   // C5 0.52 + 3.60 ms as separate births + apparent-pair kernels)
@@ -1113,6 +1120,21 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     }
     KfP kp = kf_params(g, L.zc);
     const uint32_t nzc = uint32_t((g.nz + L.zc - 1) / L.zc), xy = kp.XB * kp.YB;
+    const int64_t plane = g.nx * g.ny;
+    int64_t forest_z = 0;  // planes [0, forest_z) have their basin forest
+    // the basin forest of planes [forest_z, zt): pieces are whole images plus separators, and
+    // apparent vertex-edge pairs never cross a separator (its cells are absent), so the forest
+    // of a piece is closed
+    auto forest_upto = [&](int64_t zt) {
+      if (zt <= forest_z) return;
+      const int64_t v0 = forest_z * plane, v1 = zt * plane;
+      k_h0_parent<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
+          S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1));
+      CR_CHECK_LAUNCH();
+      k_pointer_jump<<<grid_for(v1 - v0, 256), 256, 0, s>>>(parent, v0, v1);
+      CR_CHECK_LAUNCH();
+      forest_z = zt;
+    };
     if (S.nready == 0) {
       k_filtration<<<L.grid, KF_THREADS, sizeof(KfSmem), s>>>(image, kp, S.births, S.tags, cnt,
                                                               nan_flag);
@@ -1133,7 +1155,16 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
                                                                         S.tags, cnt, nan_flag);
         CR_CHECK_LAUNCH();
         c0 = c1;
+        // births and tags are final for the planes below c0 zc - 1 (the last output plane's
+        // tags need the next block's codes): the forest of the pieces entirely below it
+        const int64_t zdone = c0 >= nzc ? g.nz : int64_t(c0) * L.zc - 1;
+        int64_t zt = forest_z;
+        for (int k = 0; k < S.nready; ++k)
+          if (S.ready_z[k] <= zdone) zt = S.ready_z[k] > zt ? S.ready_z[k] : zt;
+        if (c0 >= nzc) zt = g.nz;
+        forest_upto(zt);
       }
+      h0_forest_done = true;
     }
     prof_mark(s, "filtration");
   }
@@ -1156,13 +1187,16 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   }
 
   // ---- H0
-  uint32_t* parent = ws.alloc<uint32_t>(g.nvox);
-  k_h0_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, parent, cnt + 8);
-  CR_CHECK_LAUNCH();
-  // flatten the apparent forest (H0 chains are long: flattening once beats finds per edge end,
-  // measured; the dual forest is shallow and takes on-demand finds in k_dual_edges instead)
-  k_pointer_jump<<<grid_for(g.nvox, 256), 256, 0, s>>>(parent, g.nvox);
-  CR_CHECK_LAUNCH();
+  // basin forest, flattened (H0 chains are long: flattening once beats finds per edge end,
+  // measured; the dual forest is shallow and takes on-demand finds in k_dual_edges instead).
+  // Pieces of a batch arriving from the host were done in the filtration loop above.
+  if (!h0_forest_done) {
+    k_h0_parent<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
+        S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox));
+    CR_CHECK_LAUNCH();
+    k_pointer_jump<<<grid_for(g.nvox, 256), 256, 0, s>>>(parent, 0, g.nvox);
+    CR_CHECK_LAUNCH();
+  }
 
   // NaN check + counts (one sync)
   CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
