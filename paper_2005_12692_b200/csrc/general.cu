@@ -528,9 +528,13 @@ struct Cand {
 // pointer jumping).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
 __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                            Geom g, uint32_t* parent, Cand* __restrict__ cand,
-                           unsigned int* __restrict__ ncand) {
-  uint32_t v, x, y, z;
-  const bool in0 = vox_of_thread(g, v, x, y, z);
+                           unsigned int* __restrict__ ncand, uint32_t vbase, uint32_t vend) {
+  // voxels [vbase, vend) (a piece of the image: see run_general)
+  const uint64_t vv = uint64_t(vbase) + uint64_t(blockIdx.x) * VOX_THREADS + threadIdx.x;
+  const uint32_t v = uint32_t(vv);
+  const bool in0 = vv < vend;
+  const uint32_t nxx = uint32_t(g.nx), nyy = uint32_t(g.ny);
+  const uint32_t rr = v / nxx, x = v - rr * nxx, z = rr / nyy, y = rr - z * nyy;
   const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
   // every edge with base voxel v contains v: an absent v skips them all
   const bool in = in0 && births[kb] != ABSENT_ORD;
@@ -1107,6 +1111,17 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);  // H0 basin forest
   bool h0_forest_done = false;
+  // H0 candidate edges, room for every edge of the grid (a bound known without reading the
+  // finite-cell counts back: no host sync before the merge rounds, and pieces of a host batch
+  // enumerate their candidates as they arrive)
+  int64_t nedges_max = 0;
+  {
+    const int64_t n3[3] = {g.nx, g.ny, g.nz};
+    for (int a = 0; a < 3; ++a)
+      if (n3[a] > 1) nedges_max += (n3[a] - 1) * (g.nvox / n3[a]);
+  }
+  Cand* cand = S.nready ? ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1) : nullptr;
+  unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
 
   // K1 + K2 in one streaming kernel (round 1 measured the split alternatives, profiles/r01/s3:
   // C5 0.52 + 3.60 ms as separate births + apparent-pair kernels)
@@ -1132,6 +1147,9 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
           S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1));
       CR_CHECK_LAUNCH();
       k_pointer_jump<<<grid_for(v1 - v0, 256), 256, 0, s>>>(parent, v0, v1);
+      CR_CHECK_LAUNCH();
+      k_h0_edges<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
+          S.births, S.tags, g, parent, cand, ncand, uint32_t(v0), uint32_t(v1));
       CR_CHECK_LAUNCH();
       forest_z = zt;
     };
@@ -1190,32 +1208,21 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // basin forest, flattened (H0 chains are long: flattening once beats finds per edge end,
   // measured; the dual forest is shallow and takes on-demand finds in k_dual_edges instead).
   // Pieces of a batch arriving from the host were done in the filtration loop above.
+  if (!cand) cand = ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1);
   if (!h0_forest_done) {
     k_h0_parent<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
         S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox));
     CR_CHECK_LAUNCH();
     k_pointer_jump<<<grid_for(g.nvox, 256), 256, 0, s>>>(parent, 0, g.nvox);
     CR_CHECK_LAUNCH();
+    k_h0_edges<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
+        S.births, S.tags, g, parent, cand, ncand, 0u, uint32_t(g.nvox));
+    CR_CHECK_LAUNCH();
   }
+  const int64_t nedges = nedges_max;
 
-  // NaN check + counts (one sync)
-  CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  CR_CUDA(cudaStreamSynchronize(s));
-  if (*reinterpret_cast<int*>(hs.p + 31)) throw Error{CR_EINVAL, "NaN in image"};
-  for (int d = 0; d < 4; ++d) {
-    st.apparent[d] = int64_t(hs.p[d]);
-    st.cells[d] = int64_t(hs.p[4 + d]);
-  }
-  st.columns[0] = int64_t(hs.p[8]);
-  const int64_t nedges = st.cells[1];
-
-  Cand* cand = ws.alloc<Cand>(nedges);
-  unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
-  k_h0_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, parent, cand, ncand);
-  CR_CHECK_LAUNCH();
-
-  // vertex records: at most one per finite vertex
-  S.R.rec[0] = ws.alloc<uint64_t>(st.cells[0]);
+  // vertex records: at most one per vertex
+  S.R.rec[0] = ws.alloc<uint64_t>(g.nvox);
   unsigned long long* nrec0 = cnt + 13;
   unsigned long long* best = ws.alloc<unsigned long long>(2 * g.nvox);
   CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * g.nvox * sizeof(unsigned long long), s));
@@ -1227,12 +1234,18 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   k_h0_essential<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
                                                     cnt + 22);
   CR_CHECK_LAUNCH();
-  CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 13, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          s));
+  // the one read of H0: NaN flag, cell / apparent / basin counts, records, roots, rounds
+  CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
-  S.R.n[0] = int64_t(hs.p[0]);
-  st.essential[0] = int64_t(hs.p[9]);
-  st.rounds[0] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 7)[2]);
+  if (*reinterpret_cast<int*>(hs.p + 31)) throw Error{CR_EINVAL, "NaN in image"};
+  for (int d = 0; d < 4; ++d) {
+    st.apparent[d] = int64_t(hs.p[d]);
+    st.cells[d] = int64_t(hs.p[4 + d]);
+  }
+  st.columns[0] = int64_t(hs.p[8]);
+  S.R.n[0] = int64_t(hs.p[13]);
+  st.essential[0] = int64_t(hs.p[22]);
+  st.rounds[0] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 20)[2]);
   prof_mark(s, "h0");
   ws.release(cand);
   ws.release(best);
