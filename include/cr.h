@@ -129,10 +129,14 @@ cr_status cr_barcodes_batched(const float* images, int64_t batch, const int64_t*
                               cr_stream_t stream);
 
 /* cr_barcodes_batched with HOST buffers (the end-to-end batch entry point, BASELINE config 5's
- * batch): host_images (batch*prod(shape) float32, pinned memory is fastest) are copied in on
- * `stream`, the bars (and birth cells, if host_out_birth_cells is non-NULL) and the batch+1 CSR
- * offsets are copied back to the host buffers before return.  Arguments, output order and errors
- * as for cr_barcodes_batched; device staging is allocated stream-ordered and freed before return. */
+ * batch): host_images (batch*prod(shape) float32, pinned memory is fastest) are copied in, the
+ * bars (and birth cells, if host_out_birth_cells is non-NULL) and the batch+1 CSR offsets are
+ * copied back to the host buffers before return.  Batches of 2D/3D images on the stacked path
+ * are copied in up to 8 pieces, straight into the stacked layout, on a library-owned stream;
+ * `stream` waits on each piece before the filtration and H0 forest of its planes run, so the copy
+ * overlaps them.  host_images must stay unchanged until return.  Arguments,
+ * output order and errors as for cr_barcodes_batched; device staging is allocated stream-ordered
+ * and freed before return. */
 cr_status cr_barcodes_batched_host(const float* host_images, int64_t batch, const int64_t* shape,
                                    int ndim, int maxdim, cr_pair* host_out_pairs,
                                    uint32_t* host_out_birth_cells, int64_t out_capacity,
