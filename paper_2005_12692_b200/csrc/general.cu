@@ -985,12 +985,8 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   k_dual_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
                                                   cnt + 1);
   CR_CHECK_LAUNCH();
-  CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-  CR_CUDA(cudaStreamSynchronize(s));
-  unsigned n = unsigned(hs.p[0] & 0xFFFFFFFFu);
-  const unsigned nb = unsigned(hs.p[1]);
-  st.columns[d] = nb;
-
+  // candidates <= the finite d-cells (known since H0's read): no host read before the rounds
+  const int64_t n = st.cells[d] + 1;
   unsigned long long* nrec = cnt + 2;
   unsigned long long* best = ws.alloc<unsigned long long>(2 * nv);
   CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * nv * sizeof(unsigned long long), s));
@@ -998,11 +994,11 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 6);  // cnt[6], cnt[7]: zeroed above
   mm_rounds<true>(cand, ncand, n, parent, best, unsigned(nv), alive, S.births, g, G, nullptr,
                   S.R.rec[d], nrec, ctl, ws);
-  CR_CUDA(cudaMemcpyAsync(hs.p, cnt + 2, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          s));
+  CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
-  S.R.n[d] = int64_t(hs.p[0]);
-  st.rounds[d] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 4)[2]);
+  st.columns[d] = int64_t(hs.p[1]);  // dual roots
+  S.R.n[d] = int64_t(hs.p[2]);
+  st.rounds[d] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 6)[2]);
   ws.release(best);
   ws.release(alive);
   ws.release(cand);
