@@ -1048,6 +1048,49 @@ __global__ void k_bar_advance(const uint32_t* __restrict__ pos, int64_t n, long 
   dbase[d + 1] = dbase[d] + (pos ? (long long)pos[n] : 0ll);
 }
 
+// emit_bars for a dimension with n <= BAR1_MAX records, in ONE block: keep-flags, block-wide
+// exclusive scan, scatter and the output-offset advance (instead of five launches)
+constexpr int BAR1_THREADS = 1024, BAR1_IPT = 8, BAR1_MAX = BAR1_THREADS * BAR1_IPT;
+__global__ void __launch_bounds__(BAR1_THREADS) k_bar_one_block(
+    const uint64_t* __restrict__ rec, int n, const uint32_t* __restrict__ births, int dim,
+    long long* dbase, int64_t cap, cr_pair* out, uint32_t* out_cells) {
+  typedef cub::BlockScan<unsigned, BAR1_THREADS> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const int t = threadIdx.x;
+  uint64_t r[BAR1_IPT];
+  unsigned keep = 0, cnt = 0;
+#pragma unroll
+  for (int q = 0; q < BAR1_IPT; ++q) {  // blocked: thread t holds records [t IPT, (t + 1) IPT)
+    const int i = t * BAR1_IPT + q;
+    r[q] = i < n ? rec[i] : 0ull;
+    if (i < n) {
+      const uint32_t b = uint32_t(r[q] >> 32), d = uint32_t(r[q]);
+      if (d == NONE32 || births[d] > births[b]) {
+        keep |= 1u << q;
+        ++cnt;
+      }
+    }
+  }
+  unsigned pos, total;
+  BS(tmp).ExclusiveSum(cnt, pos, total);
+  const long long base = dbase[dim];
+#pragma unroll
+  for (int q = 0; q < BAR1_IPT; ++q)
+    if (keep >> q & 1u) {
+      const int64_t o = base + pos++;
+      if (o < cap) {
+        const uint32_t b = uint32_t(r[q] >> 32), d = uint32_t(r[q]);
+        cr_pair p;
+        p.dim = dim;
+        p.birth = float_of_ord(births[b]);
+        p.death = d == NONE32 ? __int_as_float(0x7F800000) : float_of_ord(births[d]);
+        out[o] = p;
+        if (out_cells) out_cells[o] = b;
+      }
+    }
+  if (t == 0) dbase[dim + 1] = base + total;
+}
+
 __global__ void k_partner_init(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                                Geom g, uint32_t* __restrict__ partner) {
   int64_t kk = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1269,6 +1312,12 @@ int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out
       continue;
     }
     sort_keys_u64(S.R.rec[d], n, false, 32 + kb, ws, 32);
+    if (n <= BAR1_MAX) {  // small: one block does the flags, the scan and the scatter
+      k_bar_one_block<<<1, BAR1_THREADS, 0, s>>>(S.R.rec[d], int(n), S.births, d, dbase, cap, out,
+                                                 out_cells);
+      CR_CHECK_LAUNCH();
+      continue;
+    }
     uint32_t* flag = ws.alloc<uint32_t>(n + 1);
     uint32_t* pos = ws.alloc<uint32_t>(n + 1);
     k_bar_flags<<<grid_for(n, B), B, 0, s>>>(S.R.rec[d], n, S.births, flag);
