@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_os_pass(
   typedef cub::BlockScan<unsigned, OS_THREADS> BS;
   __shared__ typename BS::TempStorage s_scan;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  if (t == 0) S.tile = atomicAdd(tile_ctr, 1u);
+  const bool single = gstart == nullptr;  // one tile: its own counts are the global ones
+  if (t == 0) S.tile = single ? 0u : atomicAdd(tile_ctr, 1u);
   for (int i = t; i < OS_WARPS * OS_RADIX; i += OS_THREADS) (&S.wcnt[0][0])[i] = 0;
   S.hist[t] = 0;
   __syncthreads();
@@ -120,8 +121,8 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_os_pass(
   __syncthreads();
   const unsigned cnt = S.hist[t];
   const unsigned long long tag = uint64_t(pass + 1) << 56;
-  unsigned long long* st = status + uint64_t(tile) * OS_RADIX + t;
-  __stcg(st, tag | (tile == 0 ? OS_INC : OS_AGG) | cnt);
+  unsigned long long* st = single ? nullptr : status + uint64_t(tile) * OS_RADIX + t;
+  if (!single) __stcg(st, tag | (tile == 0 ? OS_INC : OS_AGG) | cnt);
 #pragma unroll
   for (int r = 0; r < OS_IPT; ++r) {
     const unsigned d = OS_DG(r);
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_os_pass(
   BS(s_scan).ExclusiveSum(cnt, toff);
   S.toff[t] = toff;
   unsigned long long excl = 0;
-  for (int64_t j = int64_t(tile) - 1; j >= 0; --j) {
+  for (int64_t j = single ? -1 : int64_t(tile) - 1; j >= 0; --j) {
     const unsigned long long* p = status + uint64_t(j) * OS_RADIX + t;
     unsigned long long s;
     do {
@@ -156,8 +157,8 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_os_pass(
     excl += s & OS_CNT;
     if (s & OS_INC) break;
   }
-  if (tile != 0) __stcg(st, tag | OS_INC | (excl + cnt));
-  S.gbase[t] = gstart[t] + excl;
+  if (!single && tile != 0) __stcg(st, tag | OS_INC | (excl + cnt));
+  S.gbase[t] = single ? toff : gstart[t] + excl;
   __syncthreads();
   // 3. stage the tile sorted by digit
 #pragma unroll
@@ -203,6 +204,30 @@ void os_sort(K* keys, V* vals, int64_t n, int begin_bit, int end_bit, bool desce
   const int64_t ntiles = (n + OS_TILE - 1) / OS_TILE;
   K* kalt = ws.alloc<K>(n);
   V* valt = HASV ? ws.alloc<V>(n) : nullptr;
+  if (ntiles == 1) {  // one tile: no histogram pass, no status words, no look-back
+    os_set_smem<K, V, HASV>(ws.device());
+    K *ki = keys, *ko = kalt;
+    V *vi = vals, *vo = valt;
+    for (int p = 0; p < npass; ++p) {
+      k_os_pass<K, V, HASV><<<1, OS_THREADS, sizeof(OsSmem<K, V>), s>>>(
+          ki, vi, ko, vo, n, begin_bit + 8 * p, descending, p, nullptr, nullptr, nullptr);
+      CR_CHECK_LAUNCH();
+      K* tk = ki;
+      ki = ko;
+      ko = tk;
+      V* tv = vi;
+      vi = vo;
+      vo = tv;
+    }
+    if (ki != keys) {
+      CR_CUDA(cudaMemcpyAsync(keys, ki, size_t(n) * sizeof(K), cudaMemcpyDeviceToDevice, s));
+      if (HASV)
+        CR_CUDA(cudaMemcpyAsync(vals, vi, size_t(n) * sizeof(V), cudaMemcpyDeviceToDevice, s));
+    }
+    if (valt) ws.release(valt);
+    ws.release(kalt);
+    return;
+  }
   // counters: ghist [npass][256], tile counters [npass]; status [ntiles][256]
   unsigned* ghist = ws.alloc<unsigned>(OS_MAXPASS * OS_RADIX + OS_MAXPASS);
   unsigned* tctr = ghist + OS_MAXPASS * OS_RADIX;
