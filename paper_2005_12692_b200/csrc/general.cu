@@ -815,7 +815,7 @@ struct MMArgs {
   uint32_t* parent;
   unsigned long long* best;  // 2 * nbest entries (two buffers, by round parity)
   unsigned nbest;
-  uint8_t* alive;            // n entries, 1 on entry
+  uint8_t* alive;            // n entries (set to 1 by the kernel)
   const uint32_t* births;
   Geom g;
   DualG G;
@@ -835,6 +835,18 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
   Cand* cur = A.cur;
   const unsigned n = *A.n;
   unsigned rounds = 0;
+  // Initialise the two minima buffers at the roots the candidates touch, and the alive flags,
+  // instead of memsetting 2 x nbest words (2.2 GB on C5b): every root a later find returns is
+  // an endpoint root of some candidate (links only join two candidates' endpoint roots).
+  for (unsigned i = gt; i < n; i += gs) {
+    const Cand c = cur[i];
+    A.best[c.a] = NONE64;
+    A.best[c.b] = NONE64;
+    A.best[A.nbest + c.a] = NONE64;
+    A.best[A.nbest + c.b] = NONE64;
+    A.alive[i] = 1;
+  }
+  grid.sync();
   while (true) {
     unsigned long long* bc = A.best + (rounds & 1) * A.nbest;
     unsigned long long* bp = A.best + ((rounds + 1) & 1) * A.nbest;
@@ -937,7 +949,6 @@ void mm_rounds(Cand* cand, const unsigned* n_dev, int64_t n_max, uint32_t* paren
   const int64_t cap = int64_t(nsm) * occ[DUAL];
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  CR_CUDA(cudaMemsetAsync(alive, 1, size_t(n_max > 0 ? n_max : 1), s));
   MMArgs A{cand, n_dev, parent, best, nbest, alive, births, g, G, tags, rec, nrec, ctl};
   void* args[] = {&A};
   CR_CUDA(cudaLaunchCooperativeKernel((void*)k_mm_rounds<DUAL>, dim3(unsigned(blocks)), dim3(256),
@@ -988,8 +999,7 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   // candidates <= the finite d-cells (known since H0's read): no host read before the rounds
   const int64_t n = st.cells[d] + 1;
   unsigned long long* nrec = cnt + 2;
-  unsigned long long* best = ws.alloc<unsigned long long>(2 * nv);
-  CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * nv * sizeof(unsigned long long), s));
+  unsigned long long* best = ws.alloc<unsigned long long>(2 * nv);  // set in k_mm_rounds
   uint8_t* alive = ws.alloc<uint8_t>(n + 1);
   unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 6);  // cnt[6], cnt[7]: zeroed above
   mm_rounds<true>(cand, ncand, n, parent, best, unsigned(nv), alive, S.births, g, G, nullptr,
@@ -1263,8 +1273,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // vertex records: at most one per vertex
   S.R.rec[0] = ws.alloc<uint64_t>(g.nvox);
   unsigned long long* nrec0 = cnt + 13;
-  unsigned long long* best = ws.alloc<unsigned long long>(2 * g.nvox);
-  CR_CUDA(cudaMemsetAsync(best, 0xFF, 2 * g.nvox * sizeof(unsigned long long), s));
+  unsigned long long* best = ws.alloc<unsigned long long>(2 * g.nvox);  // set in k_mm_rounds
   uint8_t* alive = ws.alloc<uint8_t>(nedges);
   unsigned* ctl = reinterpret_cast<unsigned*>(cnt + 20);  // cnt[20], cnt[21]: zeroed at the start
   mm_rounds<false>(cand, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
