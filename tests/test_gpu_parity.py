@@ -501,11 +501,12 @@ def test_barcodes_f64_rank_path(cr):
 
 
 def test_f64_rank_sort_tile_boundaries(cr):
-    """The ranking's radix sort (64-bit keys, 32-bit indices, 8 passes; tiles of 4096 keys, see
-    DESIGN.md §K3) at tile boundaries and with long runs of equal values: sub-float32 distinct
-    doubles with ties, 1D (the tiles path) and 2D, against the oracle."""
+    """The ranking's radix sort (64-bit keys, 32-bit indices, 8 passes; tiles of 3072 keys, see
+    DESIGN.md §K3; one tile takes the single-tile path) at tile boundaries and with long runs of
+    equal values: sub-float32 distinct doubles with ties, 1D (the tiles path) and 2D, against the
+    oracle."""
     step = 2.0 ** -38
-    for s, n in enumerate([4095, 4096, 4097, 8193, 3 * 4096 + 17]):
+    for s, n in enumerate([3071, 3072, 3073, 6145, 3 * 3072 + 17, 4097]):
         k = gen.small_int_image((n,), 700, seed=1300 + s, inf_frac=0.05 if s % 2 else 0.0)
         _check_f64(cr, 1.0 + k.astype(np.float64) * step, 1, ctx=("1d", n))
     k = gen.small_int_image((67, 129), 3000, seed=1310)
