@@ -215,14 +215,34 @@ static void stage_host_batch(const float* host, int64_t batch, int64_t L, int64_
                              float* simg, GeneralState& S, cudaStream_t s) {
   int dev = 0;
   CR_CUDA(cudaGetDevice(&dev));
-  static thread_local int cs_dev = -1;
-  static thread_local cudaStream_t cs = nullptr;
-  static thread_local cudaEvent_t ev[17];
-  if (cs_dev != dev) {
-    CR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    for (auto& e : ev) CR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cs_dev = dev;
+  // the copy stream and its events: one set per host thread, re-made on a device change and
+  // destroyed when the thread exits
+  struct CopyStream {
+    int dev = -1;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[17] = {};
+    void destroy() {
+      if (dev < 0) return;
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(dev);
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+      for (auto& e : ev) cudaEventDestroy(e);
+      cudaSetDevice(cur);
+      dev = -1;
+    }
+    ~CopyStream() { destroy(); }
+  };
+  static thread_local CopyStream C;
+  if (C.dev != dev) {
+    C.destroy();
+    CR_CUDA(cudaStreamCreateWithFlags(&C.cs, cudaStreamNonBlocking));
+    for (auto& e : C.ev) CR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    C.dev = dev;
   }
+  cudaStream_t cs = C.cs;
+  cudaEvent_t* ev = C.ev;
   CR_CUDA(cudaEventRecord(ev[16], s));  // the buffer's previous users on s come first
   CR_CUDA(cudaStreamWaitEvent(cs, ev[16], 0));
   if (batch > 1) {
