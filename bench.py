@@ -5,12 +5,13 @@
 
 Workload.  BASELINE.json's metric names no config, so the headline is the largest workload:
 configs[4]'s batch C5b -- 64 volumes of 128^3 (Gaussian random field, sigma = 3, +inf outside a
-centred ball of radius 60), full barcode H0-H2 -- sharded volume by volume across the GPUs
-(weak scaling in the sense that each rank's shard is 64/N volumes of the fixed batch: the job's
-work is fixed, so `scaling` is "strong").  A step is one full barcode computation of the whole
-batch: every SURVEY §8(a) row runs (filtration + apparent pairs, H0 union-find, the dimension-1
-coboundary reduction, the top dimension by duality, output), then (N > 1) the bars are gathered
-onto rank 0.  The same run also times configs[4]'s single 384^3 volume (C5) on rank 0 at N = 1
+centred ball of radius 60), full barcode H0-H2.  Batches are independent problems, so at N GPUs
+the job is N such batches, one per rank (rank 0: the config's own batch, seed 6; rank r > 0: the
+same recipe from seed (6, r)), with no exchange during compute: weak scaling, `scaling` "weak",
+value = all ranks' voxels / the max-over-ranks time.  A step is one full barcode computation of
+every rank's batch: every SURVEY §8(a) row runs (filtration + apparent pairs, H0 union-find, the
+dimension-1 coboundary reduction, the top dimension by duality, output), then (N > 1) the bars
+are gathered onto rank 0.  The same run also times configs[4]'s single 384^3 volume (C5) on rank 0 at N = 1
 (key "c5_single").  Other configs (--config c1..c5, c2f64) remain available as parity cases.
 
 Timing: W >= 3 untimed warm-up steps; then K steps bracketed by CUDA events on the launching
@@ -43,10 +44,10 @@ METRIC = "voxels/sec full barcode (dims 0..d), HBM GB/s vs peak; bit-exact vs or
 CONFIG_DESC = {
     "c1": "2D 128x128 iid U[0,1) float32, H0+H1",
     "c2": "1D Gaussian random walk, 2^24 float32 samples, H0",
-    "c3": "65536 x 28x28 blob images (0..255 levels), H0+H1, sharded by image",
+    "c3": "65536 x 28x28 blob images (0..255 levels), H0+H1 (one such batch per rank)",
     "c4": "3D 128^3 GRF sigma=2, H0-H2",
     "c5": "3D 384^3 GRF sigma=3, +inf outside ball r=180, H0-H2",
-    "c5b": "64 x 128^3 GRF sigma=3, +inf outside ball r=60, H0-H2, sharded by volume",
+    "c5b": "64 x 128^3 GRF sigma=3, +inf outside ball r=60, H0-H2 (one such batch per rank)",
     "c2f64": "1D Gaussian random walk, 2^24 float64 samples (kept in double), H0",
 }
 F64 = {"c2f64"}
@@ -128,24 +129,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
 
 
-def c5b_volumes(k: int = 64):
-    """The first k volumes of the C5b batch (the generator draws them in sequence)."""
+def c5b_volumes(k: int = 64, rank: int = 0):
+    """The first k volumes of the C5b batch (the generator draws them in sequence); rank r > 0 of
+    a multi-GPU job draws its own batch from seed (6, r)."""
     from workloads import generators as gen
-    g = np.random.default_rng(6)
+    g = np.random.default_rng(6 if rank == 0 else (6, rank))
     return np.stack([gen.masked_grf((128, 128, 128), 3.0, 60.0, g) for _ in range(k)]), 2
 
 
 def make_input(cfg: str, rank: int, world: int):
-    """(this rank's input, maxdim, units in the whole job)."""
+    """(this rank's input, maxdim, units in the whole job).  Batches: one whole batch per rank
+    (weak scaling, see the module docstring)."""
     from workloads import generators as gen
     if cfg == "c3":
-        imgs = gen.blobs(65536, 3)
-        a, b = shard_range(len(imgs), rank, world)
-        return imgs[a:b], 1, len(imgs)
+        imgs = gen.blobs(65536, 3 if rank == 0 else (3, rank))
+        return imgs, 1, len(imgs) * world
     if cfg == "c5b":
-        vols, md = c5b_volumes(64)
-        a, b = shard_range(len(vols), rank, world)
-        return vols[a:b], md, len(vols)
+        vols, md = c5b_volumes(64, rank)
+        return vols, md, len(vols) * world
     if cfg == "c2f64":
         return gen.random_walk(1 << 24, 2, dtype=np.float64), 0, 1
     img, md = gen.config(cfg)
@@ -501,12 +502,12 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if batched else "weak",
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64" if f64 else "f32",
         "data": "synthetic (seeded, workloads/generators.py)",
         "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                    "voxels_per_step": nvox_total, "maxdim": maxdim,
-                   "parallelism": (f"dp{world} (volume/image shards, gather to rank 0)" if batched
+                   "parallelism": (f"dp{world} (one batch per rank, gather to rank 0)" if batched
                                    else f"replicas x{world} (one image per rank)"),
                    "l2": ("flushed before every timed step (256 MiB write, outside the events)"
                           if flush is not None else
@@ -568,7 +569,7 @@ def run_reference(args, rank, world):
     cores = P if args.config in BATCHED else 1
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "voxels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-            "higher_is_better": True, "scaling": "strong" if args.config in BATCHED else "weak",
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if args.config in F64 else "f32",
             "data": "synthetic (seeded, workloads/generators.py)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "maxdim": maxdim},
