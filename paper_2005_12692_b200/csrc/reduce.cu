@@ -292,20 +292,24 @@ __device__ uint32_t merge_xor_path_g(const uint64_t* A, uint32_t a, const uint64
     je = b;
   }
   if (d >= n) ie = is = a, je = js = b;
+  // Each lane streams its A segment through a 4-deep register queue (the load of A[i + 4] is
+  // issued when A[i] is consumed), so a step waits on a compare, not on an L1 round trip.
+  auto lda = [&](uint32_t k, uint32_t end) -> uint64_t { return k < end ? ld_ca(A + k) : NONE64; };
   uint32_t cnt = 0;
   {
     uint32_t i = is, j = js;
-    uint64_t x = i < ie ? ld_ca(A + i) : NONE64, y = j < je ? F[j] : NONE64;
+    uint64_t x0 = lda(i, ie), x1 = lda(i + 1, ie), x2 = lda(i + 2, ie), x3 = lda(i + 3, ie);
+    uint64_t y = j < je ? F[j] : NONE64;
     while (i < ie || j < je) {
-      if (x == y) {
+      if (x0 == y) {
         ++i;
         ++j;
-        x = i < ie ? ld_ca(A + i) : NONE64;
+        x0 = x1; x1 = x2; x2 = x3; x3 = lda(i + 3, ie);
         y = j < je ? F[j] : NONE64;
-      } else if (x < y) {
+      } else if (x0 < y) {
         ++cnt;
         ++i;
-        x = i < ie ? ld_ca(A + i) : NONE64;
+        x0 = x1; x1 = x2; x2 = x3; x3 = lda(i + 3, ie);
       } else {
         ++cnt;
         ++j;
@@ -323,17 +327,18 @@ __device__ uint32_t merge_xor_path_g(const uint64_t* A, uint32_t a, const uint64
   pos -= cnt;
   {
     uint32_t i = is, j = js;
-    uint64_t x = i < ie ? ld_ca(A + i) : NONE64, y = j < je ? F[j] : NONE64;
+    uint64_t x0 = lda(i, ie), x1 = lda(i + 1, ie), x2 = lda(i + 2, ie), x3 = lda(i + 3, ie);
+    uint64_t y = j < je ? F[j] : NONE64;
     while (i < ie || j < je) {
-      if (x == y) {
+      if (x0 == y) {
         ++i;
         ++j;
-        x = i < ie ? ld_ca(A + i) : NONE64;
+        x0 = x1; x1 = x2; x2 = x3; x3 = lda(i + 3, ie);
         y = j < je ? F[j] : NONE64;
-      } else if (x < y) {
-        C[pos++] = x;
+      } else if (x0 < y) {
+        C[pos++] = x0;
         ++i;
-        x = i < ie ? ld_ca(A + i) : NONE64;
+        x0 = x1; x1 = x2; x2 = x3; x3 = lda(i + 3, ie);
       } else {
         C[pos++] = y;
         ++j;
