@@ -503,7 +503,10 @@ struct ColT {
 #ifndef K5_GCAP
 #define K5_GCAP 8192
 #endif
-constexpr uint32_t GCAP = K5_GCAP;  // the middle tier: F merges into G, G into M when it exceeds GCAP
+constexpr uint32_t GCAP = K5_GCAP;
+#ifndef K5_GK
+#define K5_GK 24
+#endif  // the middle tier: F merges into G, G into M when it exceeds GCAP
 
 // The working column is M[h:] xor G[g0:] xor F[f0:] xor R: three sorted tiers -- a long main
 // array and a middle array in global memory, a fresh array in shared memory -- and a register
@@ -783,7 +786,11 @@ __device__ __forceinline__ bool flush(CT& c, const RP& P, int lane) {
   c.g0 = 0;
   c.gstale = true;
   c.nf = c.f0 = 0;
-  if (c.ng > GCAP) {
+  // G moves into M once it outgrows ~K5_GK sqrt(|M|) (at least 2048, at most GCAP): the cost of a
+  // flush grows with |G| and that of a G -> M merge with |M|, so the balance point moves with |M|
+  uint32_t glim = uint32_t(float(K5_GK) * __fsqrt_rn(float(c.nm - c.h)));
+  glim = glim < 2048u ? 2048u : (glim > GCAP ? GCAP : glim);
+  if (c.ng > glim) {
     const uint32_t nm = c.nm - c.h;
     if (!grow(c, nm + c.ng, P, lane)) return false;
     const uint32_t n2 = merge_chunked<true>(c.Mc + c.h, nm, c.Gc, c.ng, c.Ma,
