@@ -424,44 +424,77 @@ __device__ uint32_t merge_small(const uint64_t* A, uint32_t a, const uint64_t* B
   return a + nb - 2 * __popc(bdup);
 }
 
-// C = A xor B with A in global memory and B in global (BG) or shared memory, for long inputs:
-// merge-path chunks of <= CH elements are staged in shared memory (SA, SB: CH+1 entries each) and
-// merged there, so a long array is read once, coalesced, instead of one global binary search per
-// element.  Chunks split by the merge path with ties taken from A first; an equal pair split by a
-// chunk boundary is kept together by taking B's copy into the chunk too.
-template <bool BG, uint32_t CH = FCAP - 1>
-__device__ __noinline__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t* B, uint32_t b,
-                                  uint64_t* C, uint64_t* SA, uint64_t* SB, int lane) {
-  uint32_t i0 = 0, j0 = 0, out = 0;
-  while (i0 < a || j0 < b) {
-    const uint32_t ra = a - i0, rb = b - j0;
-    const uint32_t k = ra + rb < CH ? ra + rb : CH;
-    // merge path: the smallest i in [lo, hi) with A[i0+i] > B[j0+k-i-1] (else hi), by a 32-way
-    // search -- every lane tests one split, the ballot narrows the range 32x per round
-    uint32_t lo = k > rb ? k - rb : 0, hi = k < ra ? k : ra;
-    while (lo < hi) {
-      const uint32_t step = (hi - lo + 31) >> 5;
-      const uint32_t m = lo + uint32_t(lane) * step;
-      const bool p = m < hi && ldcg64(A + i0 + m) <= ld64<BG>(B + j0 + k - m - 1);
-      const uint32_t nt = __popc(__ballot_sync(0xFFFFFFFFu, p));  // the true lanes: a prefix
-      const uint32_t nlo = nt ? lo + (nt - 1) * step + 1 : lo;
-      const uint32_t cand = lo + nt * step;
-      hi = cand < hi ? cand : hi;
-      lo = nlo;
-    }
-    const uint32_t i = lo;
-    uint32_t j = k - i;
-    if (i > 0 && j < rb && ldcg64(A + i0 + i - 1) == ld64<BG>(B + j0 + j)) ++j;
-    for (uint32_t t = lane; t < i; t += 32) SA[t] = ldcg64(A + i0 + t);
-    const uint64_t* Bc = B + j0;
+// C = A xor B with A in global memory and B in global (BG) or shared memory (!BG: all of B,
+// b <= FCAP), for long inputs: windows of up to FCAP entries of A (and of B) are staged in shared
+// memory (SA, SB: FCAP entries each) with coalesced loads, and the entries up to
+// min(last staged A, last staged B) -- all of one window -- are merged there (merge path, output
+// straight to C); the rest of the windows is shifted to their fronts and topped up.  No global
+// search per chunk: the cut is found in shared memory.  (Round 2's first form split fixed-size
+// chunks by a 32-way merge-path search over global memory: two dependent global round trips per
+// chunk before its loads.)  Keys within A and within B are distinct, so an equal pair never
+// straddles a cut.
+__device__ __forceinline__ uint32_t upper_bound_smem(const uint64_t* S, uint32_t n, uint64_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (S[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ void shift_front(uint64_t* S, uint32_t from, uint32_t n, int lane) {
+  // S[0, n) <- S[from, from + n), chunk by chunk (a chunk's reads before its writes)
+  for (uint32_t t0 = 0; t0 < n; t0 += 32) {
+    const uint32_t t = t0 + lane;
+    const uint64_t v = t < n ? S[from + t] : 0;
+    __syncwarp();
+    if (t < n) S[t] = v;
+    __syncwarp();
+  }
+}
+template <bool BG>
+__device__ __noinline__ uint32_t merge_chunked(const uint64_t* A, uint32_t a, const uint64_t* B,
+                                               uint32_t b, uint64_t* C, uint64_t* SA, uint64_t* SB,
+                                               int lane) {
+  constexpr uint32_t W = FCAP;
+  uint32_t ia = 0, na = 0;  // A[ia, ia + na) sits in SA[0, na)
+  uint32_t ib = 0, nb = 0;  // BG: B[ib, ib + nb) in SB[0, nb); !BG: B[ib, b) in place
+  uint32_t out = 0;
+  while (true) {
+    const uint32_t fa = (W - na) < (a - ia - na) ? (W - na) : (a - ia - na);
+    for (uint32_t t = lane; t < fa; t += 32) SA[na + t] = ldcg64(A + ia + na + t);
+    na += fa;
+    const uint64_t* WB;
+    uint32_t wnb;
+    bool bmore;
     if (BG) {
-      for (uint32_t t = lane; t < j; t += 32) SB[t] = ldcg64(B + j0 + t);
-      Bc = SB;
+      const uint32_t fb = (W - nb) < (b - ib - nb) ? (W - nb) : (b - ib - nb);
+      for (uint32_t t = lane; t < fb; t += 32) SB[nb + t] = ldcg64(B + ib + nb + t);
+      nb += fb;
+      WB = SB;
+      wnb = nb;
+      bmore = ib + nb < b;
+    } else {
+      WB = B + ib;
+      wnb = b - ib;
+      bmore = false;
     }
     __syncwarp();
-    out += merge_symdiff<false, false>(SA, i, Bc, j, C + out, lane);
-    i0 += i;
-    j0 += j;
+    if (na == 0 && wnb == 0) break;
+    const bool amore = ia + na < a;
+    const uint64_t la = amore ? SA[na - 1] : NONE64, lb = bmore ? WB[wnb - 1] : NONE64;
+    const uint64_t bound = la < lb ? la : lb;
+    const uint32_t ca = bound == NONE64 ? na : upper_bound_smem(SA, na, bound);
+    const uint32_t cb = bound == NONE64 ? wnb : upper_bound_smem(WB, wnb, bound);
+    out += merge_xor_path(SA, ca, WB, cb, C + out, lane);
+    shift_front(SA, ca, na - ca, lane);
+    ia += ca;
+    na -= ca;
+    if (BG) {
+      shift_front(SB, cb, nb - cb, lane);
+      nb -= cb;
+    }
+    ib += cb;
   }
   return out;
 }
