@@ -40,16 +40,18 @@ __device__ __forceinline__ void coords_of(const Geom& g, uint32_t k, uint32_t& X
 
 // ---------------------------------------------------------------------------------------------
 // K1 + K2 fused (the default): births AND apparent-pair tags of every cell from one read of the
-// image (PAPER.md:97-108 for the births, PAPER.md:44-45 for the apparent pairs).  A thread owns one voxel column (x, y) and walks it along z; its
-// unit of work is the voxel block B(x,y,z) = the 8 cells (2x+i, 2y+j, 2z+k), i,j,k in {0,1},
+// image (PAPER.md:97-108 for the births, PAPER.md:44-45 for the apparent pairs).  A thread owns
+// two voxel columns (x, y) and (x, y+1) and walks them along z; its unit of work is the voxel
+// block B(x,y,z) = the 8 cells (2x+i, 2y+j, 2z+k), i,j,k in {0,1},
 // whose births are maxima over the voxels (x..x+i, y..y+j, z..z+k): with the "plane cells"
 // P(z) = {V, Ex, Ey, Sxy} of a block, the k=1 cells are max(P(z), P(z+1)) (4 max per block).
 // A cell's 6 Khalimsky neighbours lie in its own block or in the blocks at x+-1 (neighbouring
-// lanes: shuffles), y+-1 (neighbouring warps: shared memory) and z+-1 (the thread's previous /
-// next step: registers), so codes and tags are formed from registers with one __syncthreads per
-// step.  Lanes 0 and 31 and warps 0 and KF_ROWS+1 are halo (their blocks' codes feed the tags of
-// the inner 30 x KF_ROWS columns); lane 31 also loads the x+1 voxels its i=1 cells need.  Step z
-// completes B(z-1)'s births (writes them), forms B(z-1)'s codes and B(z-2)'s tags (writes them).
+// lanes: shuffles), y+-1 (the thread's other row, or the neighbouring warp's: shared memory) and
+// z+-1 (the thread's previous / next step: registers), so codes and tags are formed from
+// registers with one __syncthreads per step.  Lanes 0 and 31, warp 0's first row and the last
+// warp's second row are halo (their blocks' codes feed the tags of the inner 30 x K2_ROWS
+// columns); lane 31 also loads the x+1 voxels its i=1 cells need.  Step z completes B(z-1)'s
+// births (writes them), forms B(z-1)'s codes and B(z-2)'s tags (writes them).
 //
 // Codes use equal births only.  A cell's max-key facet has the cell's own birth (a birth is the max
 // over the vertices, and every vertex lies in a facet), so it is the LAST facet in kidx order whose
@@ -62,13 +64,12 @@ __device__ __forceinline__ void coords_of(const Geom& g, uint32_t k, uint32_t& X
 // Layout in registers: births b[i + 2j + 4k]; codes and tags packed in two words by j, byte i+2k.
 // ---------------------------------------------------------------------------------------------
 constexpr uint8_t CODE_ABSENT = 0x40;  // code bit 6: the cell is absent (+inf birth)
-constexpr int KF_ROWS = 14, KF_THREADS = 32 * (KF_ROWS + 2);
 struct KfLaunch {
   unsigned grid;
   int zc;
 };
-inline KfLaunch kf_launch(const Geom& g) {
-  const int64_t xy = ((g.nx + 29) / 30) * ((g.ny + KF_ROWS - 1) / KF_ROWS);
+inline KfLaunch kf_launch(const Geom& g, int rows) {
+  const int64_t xy = ((g.nx + 29) / 30) * ((g.ny + rows - 1) / rows);
   int zc = 64;
   while (zc > 8 && xy * ((g.nz + zc - 1) / zc) < 4 * 148) zc >>= 1;
   return {unsigned(xy * ((g.nz + zc - 1) / zc)), zc};
@@ -159,15 +160,7 @@ template <int N>
 __device__ __forceinline__ void kf_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 constexpr int KF_PF = 3, KF_RING = KF_PF + 1;  // voxel planes in flight, ring slots
-constexpr int KF_VROWS = KF_ROWS + 3, KF_VCOLS = 33;
-struct KfSmem {
-  uint32_t v[KF_RING][KF_VROWS][KF_VCOLS];  // voxel ring (raw float bits)
-  uint4 bj0[2][KF_ROWS + 2][32];            // births of the j=0 cells (i + 2k), double-buffered
-  uint4 bj1[2][KF_ROWS + 2][32];            // births of the j=1 cells
-  uint32_t c0[2][KF_ROWS + 2][32];          // codes word j=0
-  uint32_t c1[2][KF_ROWS + 2][32];          // codes word j=1
-  uint32_t cnt[8];
-};
+constexpr int KF_VCOLS = 33;
 
 struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsky grid < 2^32 cells)
   uint32_t nx, ny, nz, KX, KXY, plane, XB, YB, zc;
@@ -182,250 +175,319 @@ inline KfP kf_params(const Geom& g, int zc) {
   p.KXY = uint32_t(g.KX * g.KY);
   p.plane = uint32_t(g.nx * g.ny);
   p.XB = uint32_t((g.nx + 29) / 30);
-  p.YB = uint32_t((g.ny + KF_ROWS - 1) / KF_ROWS);
+  p.YB = 1;  // set by the launcher (rows per CTA)
   p.zc = uint32_t(zc);
   p.zb0 = 0;
   return p;
 }
 
-__global__ void __launch_bounds__(KF_THREADS, 2) k_filtration(const float* __restrict__ img,
-                                                              const KfP P,
-                                                              uint32_t* __restrict__ births,
-                                                              uint8_t* __restrict__ tags,
-                                                              unsigned long long* __restrict__ cnt,
-                                                              int* __restrict__ nan_flag) {
+// The kernel: TWO voxel rows per warp (rows y0-1+2w and y0+2w of warp w): the y-neighbour of a
+// warp's second row is its first row (registers), so shared memory carries only the rows at warp
+// boundaries, and a step's barrier covers twice the voxels.  Small CTAs measured fastest: NW = 4
+// warps, 8 rows (6 output rows) x 30 columns per CTA, 128 registers, many CTAs per SM to cover
+// each other's barrier waits (round 2's first form: one row per warp, 16 warps, 14 output rows:
+// C5b 3.20 ms, C5 1.21 ms -> 2.70 ms, 1.05 ms).
+#ifndef K2_NWARPS
+#define K2_NWARPS 4  // measured (C5b filtration): 3: 2.98 ms, 4: 2.70, 5: 2.82, 6: 2.93, 8: 2.85, 12: 3.16
+#endif
+constexpr int K2_NW = K2_NWARPS, K2_THREADS = 32 * K2_NW, K2_ROWS = 2 * K2_NW - 2;
+constexpr int K2_VROWS = 2 * K2_NW + 1;
+struct Kf2Smem {
+  uint32_t v[KF_RING][K2_VROWS][KF_VCOLS];  // voxel ring (raw float bits)
+  uint4 b0[2][K2_NW][32];    // row 0's j=0 births (i + 2k), for the warp below's row 1 (its U)
+  uint4 b1[2][K2_NW][32];    // row 1's j=1 births, for the warp above's row 0 (its D)
+  uint32_t c0[2][K2_NW][32];  // row 0's j=0 code word
+  uint32_t c1[2][K2_NW][32];  // row 1's j=1 code word
+  uint32_t cnt[8];
+};
+inline KfP kf2_params(const Geom& g, int zc) {
+  KfP p = kf_params(g, zc);
+  p.YB = uint32_t((g.ny + K2_ROWS - 1) / K2_ROWS);
+  return p;
+}
+
+__global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __restrict__ img,
+                                                               const KfP P,
+                                                               uint32_t* __restrict__ births,
+                                                               uint8_t* __restrict__ tags,
+                                                               unsigned long long* __restrict__ cnt,
+                                                               int* __restrict__ nan_flag) {
   extern __shared__ uint4 kf_dyn[];
-  KfSmem& S = *reinterpret_cast<KfSmem*>(kf_dyn);
+  Kf2Smem& S = *reinterpret_cast<Kf2Smem*>(kf_dyn);
   const int nx = int(P.nx), ny = int(P.ny), nz = int(P.nz);
   uint32_t blk = blockIdx.x;
   const int xb = int(blk % P.XB);
   blk /= P.XB;
   const int yb = int(blk % P.YB), zb = int(P.zb0 + blk / P.YB);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int x = xb * 30 - 1 + lane, y = yb * KF_ROWS - 1 + w;
+  const int x = xb * 30 - 1 + lane;
+  const int y0 = yb * K2_ROWS - 1 + 2 * w;  // row 0 of this warp; row 1 is y0 + 1
   const int z0 = zb * int(P.zc), z1 = min(nz, z0 + int(P.zc));
-  const bool vx = x >= 0 && x < nx, vy = y >= 0 && y < ny, vy1 = y + 1 < ny;
-  const bool l31 = lane == 31, vx1 = x + 1 < nx, lastw = w == KF_ROWS + 1;
-  const bool out = vx && vy && lane >= 1 && lane <= 30 && w >= 1 && w <= KF_ROWS;
-  const bool halo_w = w == 0 || lastw;  // warp-uniform: no tags needed
+  const bool vx = x >= 0 && x < nx, vx1 = x + 1 < nx, l31 = lane == 31;
+  const bool lastw = w == K2_NW - 1;
+  bool vy[2], out[2], halo[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int yr = y0 + r;
+    vy[r] = yr >= 0 && yr < ny;
+    halo[r] = (w == 0 && r == 0) || (lastw && r == 1);  // warp-uniform
+    out[r] = vx && vy[r] && lane >= 1 && lane <= 30 && !halo[r];
+  }
+  const bool vy2 = y0 + 2 < ny;  // the extra ring row (last warp)
   if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
   constexpr uint32_t INF_BITS = 0x7F800000u;
-  // Voxel ring: v[slot][row][col], rows y0-1 .. y0+KF_ROWS+1 (the last copied by the last warp),
-  // cols x0-1 .. x0+31 (col 32 copied by lane 31).  Copies: (x, y); lane 31 also (x+1, y); the
-  // last warp also (x, y+1) and its lane 31 (x+1, y+1) -- all offsets of the (x, y) pointer.
-  // Positions outside the image hold +inf from the start and are never copied.
-  const bool o00 = vx && vy, o10 = l31 && vx1 && vy, o01 = lastw && vx && vy1,
-             o11 = lastw && l31 && vx1 && vy1;
-  uint32_t* const vown = &S.v[0][w][lane];
+  // Voxel ring: rows y0(w=0) .. y0(w=0) + 2 NW (the last copied by the last warp), cols x0-1 ..
+  // x0+31 (col 32 copied by lane 31).  A thread copies (x, y0 + r), lane 31 also (x+1, y0 + r);
+  // the last warp also the row after its row 1.  Outside the image: +inf, never copied.
+  const bool o0 = vx && vy[0], o1 = vx && vy[1], o0x = l31 && vx1 && vy[0],
+             o1x = l31 && vx1 && vy[1], o2 = lastw && vx && vy2, o2x = lastw && l31 && vx1 && vy2;
+  uint32_t* const vown = &S.v[0][2 * w][lane];
   const uint32_t sv0 = uint32_t(__cvta_generic_to_shared(vown));
-  constexpr uint32_t SLOTW = KF_VROWS * KF_VCOLS, SLOT = SLOTW * 4, ROW = KF_VCOLS * 4;
-  const int c32 = 32 - lane;  // own col -> col 32
+  constexpr uint32_t SLOTW = K2_VROWS * KF_VCOLS, SLOT = SLOTW * 4, ROW = KF_VCOLS * 4;
+  const int c32 = 32 - lane;
 #pragma unroll
-  for (int r = 0; r < KF_RING; ++r) {
-    if (!o00) vown[r * SLOTW] = INF_BITS;
-    if (l31 && !o10) vown[r * SLOTW + c32] = INF_BITS;
-    if (lastw && !o01) vown[r * SLOTW + KF_VCOLS] = INF_BITS;
-    if (lastw && l31 && !o11) vown[r * SLOTW + KF_VCOLS + c32] = INF_BITS;
+  for (int q = 0; q < KF_RING; ++q) {
+    uint32_t* v = vown + q * SLOTW;
+    if (!o0) v[0] = INF_BITS;
+    if (!o1) v[KF_VCOLS] = INF_BITS;
+    if (l31 && !o0x) v[c32] = INF_BITS;
+    if (l31 && !o1x) v[KF_VCOLS + c32] = INF_BITS;
+    if (lastw && !o2) v[2 * KF_VCOLS] = INF_BITS;
+    if (lastw && l31 && !o2x) v[2 * KF_VCOLS + c32] = INF_BITS;
   }
-  const float* gsrc = img + (o00 ? uint64_t(uint32_t(y) * P.nx + uint32_t(x)) : 0ull);
-  // plane zz into ring slot s (always one commit group, possibly empty)
-  auto issue = [&](int zz, uint32_t s) {
+  const int ys = y0 >= 0 ? y0 : 0;  // copies of row 0 / 1 are offsets of (x, ys) when valid
+  const float* gsrc = img + (vx ? uint64_t(uint32_t(ys) * P.nx + uint32_t(x)) : 0ull);
+  const int d0 = y0 >= 0 ? 0 : 1;   // y0 = -1 only for warp 0's halo row 0 (never copied)
+  auto issue = [&](int zz, uint32_t sl) {
     if (zz >= 0 && zz < nz) {  // CTA-uniform
-      const uint32_t a = sv0 + s * SLOT;
-      const float* p = gsrc + uint64_t(uint32_t(zz)) * P.plane;
-      if (o00) kf_cp4(a, p);
-      if (o10) kf_cp4(a + 4 * c32, p + 1);
+      const uint32_t a = sv0 + sl * SLOT;
+      const float* p = gsrc + uint64_t(uint32_t(zz)) * P.plane - (d0 ? P.nx : 0u);
+      if (o0) kf_cp4(a, p);
+      if (o0x) kf_cp4(a + 4 * c32, p + 1);
+      if (o1) kf_cp4(a + ROW, p + P.nx);
+      if (o1x) kf_cp4(a + ROW + 4 * c32, p + P.nx + 1);
       if (lastw) {
-        const float* q = p + P.nx;
-        if (o01) kf_cp4(a + ROW, q);
-        if (o11) kf_cp4(a + ROW + 4 * c32, q + 1);
+        if (o2) kf_cp4(a + 2 * ROW, p + 2 * P.nx);
+        if (o2x) kf_cp4(a + 2 * ROW + 4 * c32, p + 2 * P.nx + 1);
       }
     } else {
-      uint32_t* v = vown + s * SLOTW;
-      if (o00) v[0] = INF_BITS;
-      if (o10) v[c32] = INF_BITS;
-      if (o01) v[KF_VCOLS] = INF_BITS;
-      if (o11) v[KF_VCOLS + c32] = INF_BITS;
+      uint32_t* v = vown + sl * SLOTW;
+      if (o0) v[0] = INF_BITS;
+      if (o1) v[KF_VCOLS] = INF_BITS;
+      if (o0x) v[c32] = INF_BITS;
+      if (o1x) v[KF_VCOLS + c32] = INF_BITS;
+      if (o2) v[2 * KF_VCOLS] = INF_BITS;
+      if (o2x) v[2 * KF_VCOLS + c32] = INF_BITS;
     }
     kf_commit();
   };
-  // all voxels this thread copies (or prefilled) into slot s are +inf
-  auto own_inf = [&](uint32_t s) -> bool {
-    const uint32_t* v = vown + s * SLOTW;
-    bool r = v[0] == INF_BITS;
-    if (l31) r = r && v[c32] == INF_BITS;
-    if (lastw) r = r && v[KF_VCOLS] == INF_BITS && (!l31 || v[KF_VCOLS + c32] == INF_BITS);
+  auto own_inf = [&](uint32_t sl) -> bool {
+    const uint32_t* v = vown + sl * SLOTW;
+    bool r = v[0] == INF_BITS && v[KF_VCOLS] == INF_BITS;
+    if (l31) r = r && v[c32] == INF_BITS && v[KF_VCOLS + c32] == INF_BITS;
+    if (lastw) r = r && v[2 * KF_VCOLS] == INF_BITS && (!l31 || v[2 * KF_VCOLS + c32] == INF_BITS);
     return r;
   };
   int z = z0 - 2;
 #pragma unroll
   for (int q = 0; q < KF_PF; ++q) issue(z + q, uint32_t(q));
-  kf_wait<KF_PF - 1>();  // plane z0-2 landed (own copies)
-  // CTA-uniform "plane is +inf over the CTA's footprint" flags of planes z-2, z-1, z; the
-  // fictitious planes before z0-2 count as +inf (the state below is initialised as absent)
+  kf_wait<KF_PF - 1>();
   bool f2 = true, f1 = true, f0 = __syncthreads_and(own_inf(0));
-  const int wm = max(w - 1, 0), wp = min(w + 1, KF_ROWS + 1);
+  const int wm = max(w - 1, 0), wp = min(w + 1, K2_NW - 1);
   bool nan = false;
-  uint32_t P0[4] = {ABSENT_ORD, ABSENT_ORD, ABSENT_ORD, ABSENT_ORD};  // P(z-1)
-  uint32_t Zm[4] = {ABSENT_ORD, ABSENT_ORD, ABSENT_ORD, ABSENT_ORD};  // B(z-2), k=1 cells
-  uint32_t CC[2] = {0x40404040u, 0x40404040u};                     // codes of B(z-2)
-  uint32_t CZm[2] = {0x40404040u, 0x40404040u};                    // codes of B(z-3)
-  // per-byte counters (byte = cell position i + 2k of word j): finite cells, UP cells
+  uint32_t P0[2][4], Zm[2][4], CC[2][2], CZm[2][2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) P0[r][q] = Zm[r][q] = ABSENT_ORD;
+    CC[r][0] = CC[r][1] = CZm[r][0] = CZm[r][1] = 0x40404040u;
+  }
   uint32_t fin0 = 0, fin1 = 0, up0 = 0, up1 = 0;
-  // output: births of B(z-1) / tags of B(z-2) at (2z'+k, 2y+j, 2x+i); offset of (2z0-2, 2y, 2x)
-  // ... advanced by 2 KXY per step (only used when the step's plane is in [z0, z1))
-  const uint32_t rowbase = uint32_t(2 * max(y, 0)) * P.KX + uint32_t(2 * max(x, 0));
-  const bool hx = x + 1 < nx, hy = y + 1 < ny;
-  uint32_t rs = 0;  // ring slot of plane z
+  uint32_t rowbase[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    rowbase[r] = uint32_t(2 * max(y0 + r, 0)) * P.KX + uint32_t(2 * max(x, 0));
+  const bool hx = x + 1 < nx;
+  const bool hy[2] = {y0 + 1 < ny, y0 + 2 < ny};
+  uint32_t rs = 0;
   for (; z <= z1 + 1; ++z) {
     issue(z + KF_PF, (rs + KF_PF) & (KF_RING - 1));
-    const bool fast = f2 && f1 && f0;  // B(z-1), B(z-2) entirely absent: nothing to compute
-    uint32_t Pn[4] = {ABSENT_ORD, ABSENT_ORD, ABSENT_ORD, ABSENT_ORD};
-    uint32_t Bk[8];
+    const bool fast = f2 && f1 && f0;
+    uint32_t Pn[2][4], Bk[2][8];
     const int buf = z & 1;
     if (!fast) {
-      // P(z): plane cells of block z, from the ring (max over floats, then the order key)
       const uint32_t* v = vown + rs * SLOTW;
-      const float v00 = __uint_as_float(v[0]), v10 = __uint_as_float(v[1]);
-      const float v01 = __uint_as_float(v[KF_VCOLS]), v11 = __uint_as_float(v[KF_VCOLS + 1]);
-      nan |= v00 != v00;
-      const float ex = fmaxf(v00, v10);
-      Pn[0] = kf_ord(v00);
-      Pn[1] = kf_ord(ex);
-      Pn[2] = kf_ord(fmaxf(v00, v01));
-      Pn[3] = kf_ord(fmaxf(ex, fmaxf(v01, v11)));
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        Bk[q] = P0[q];
-        Bk[q + 4] = max(P0[q], Pn[q]);
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t* vr = v + r * KF_VCOLS;
+        const float v00 = __uint_as_float(vr[0]), v10 = __uint_as_float(vr[1]);
+        const float v01 = __uint_as_float(vr[KF_VCOLS]), v11 = __uint_as_float(vr[KF_VCOLS + 1]);
+        nan |= v00 != v00;
+        const float ex = fmaxf(v00, v10);
+        Pn[r][0] = kf_ord(v00);
+        Pn[r][1] = kf_ord(ex);
+        Pn[r][2] = kf_ord(fmaxf(v00, v01));
+        Pn[r][3] = kf_ord(fmaxf(ex, fmaxf(v01, v11)));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          Bk[r][q] = P0[r][q];
+          Bk[r][q + 4] = max(P0[r][q], Pn[r][q]);
+        }
       }
-      S.bj0[buf][w][lane] = make_uint4(Bk[0], Bk[1], Bk[4], Bk[5]);
-      S.bj1[buf][w][lane] = make_uint4(Bk[2], Bk[3], Bk[6], Bk[7]);
-      S.c0[buf][w][lane] = CC[0];
-      S.c1[buf][w][lane] = CC[1];
+      S.b0[buf][w][lane] = make_uint4(Bk[0][0], Bk[0][1], Bk[0][4], Bk[0][5]);
+      S.b1[buf][w][lane] = make_uint4(Bk[1][2], Bk[1][3], Bk[1][6], Bk[1][7]);
+      S.c0[buf][w][lane] = CC[0][0];
+      S.c1[buf][w][lane] = CC[1][1];
     } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) Bk[q] = ABSENT_ORD;
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          Pn[r][q] = ABSENT_ORD;
+          Bk[r][q] = Bk[r][q + 4] = ABSENT_ORD;
+        }
     }
-    kf_wait<KF_PF - 1>();  // plane z+1 landed (own copies); visible to all after the barrier
+    kf_wait<KF_PF - 1>();
     const uint32_t rn = (rs + 1) & (KF_RING - 1);
     const bool fn = __syncthreads_and(own_inf(rn));
-    uint32_t NC[2] = {0x40404040u, 0x40404040u};
-    uint32_t T0 = 0, T1 = 0;  // tag bytes, words by j, bytes i + 2k (like the codes)
-    if (!fast) {
-      // codes of B(z-1)
-      const uint32_t bmin = min(min(min(Bk[0], Bk[1]), min(Bk[2], Bk[3])),
-                                min(min(Bk[4], Bk[5]), min(Bk[6], Bk[7])));
-      if (__any_sync(0xFFFFFFFFu, bmin != ABSENT_ORD)) {
-        const uint4 dq = S.bj1[buf][wm][lane], uq = S.bj0[buf][wp][lane];
-        const uint32_t D[4] = {dq.x, dq.y, dq.z, dq.w}, U[4] = {uq.x, uq.y, uq.z, uq.w};
-        uint32_t L[4], R[4];
+    uint32_t NC[2][2], T[2][2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // q = j + 2k: L = x-1's (1,j,k), R = x+1's (0,j,k)
-          L[q] = __shfl_up_sync(0xFFFFFFFFu, Bk[1 + 2 * q], 1);
-          R[q] = __shfl_down_sync(0xFFFFFFFFu, Bk[2 * q], 1);
+    for (int r = 0; r < 2; ++r) NC[r][0] = NC[r][1] = 0x40404040u, T[r][0] = T[r][1] = 0u;
+    if (!fast) {
+      // codes of B(z-1), both rows
+      uint32_t bmin = ABSENT_ORD;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) bmin = min(bmin, Bk[r][q]);
+      if (__any_sync(0xFFFFFFFFu, bmin != ABSENT_ORD)) {
+        const uint4 dq = S.b1[buf][wm][lane], uq = S.b0[buf][wp][lane];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          uint32_t D[4], U[4];
+          if (r == 0) {  // below: the warp below's row 1; above: own row 1
+            D[0] = dq.x; D[1] = dq.y; D[2] = dq.z; D[3] = dq.w;
+            U[0] = Bk[1][0]; U[1] = Bk[1][1]; U[2] = Bk[1][4]; U[3] = Bk[1][5];
+          } else {       // below: own row 0; above: the warp above's row 0
+            D[0] = Bk[0][2]; D[1] = Bk[0][3]; D[2] = Bk[0][6]; D[3] = Bk[0][7];
+            U[0] = uq.x; U[1] = uq.y; U[2] = uq.z; U[3] = uq.w;
+          }
+          uint32_t L[4], R[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            L[q] = __shfl_up_sync(0xFFFFFFFFu, Bk[r][1 + 2 * q], 1);
+            R[q] = __shfl_down_sync(0xFFFFFFFFu, Bk[r][2 * q], 1);
+          }
+          const uint32_t c000 = kf_code<0, 0, 0>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c100 = kf_code<1, 0, 0>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c010 = kf_code<0, 1, 0>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c110 = kf_code<1, 1, 0>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c001 = kf_code<0, 0, 1>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c101 = kf_code<1, 0, 1>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c011 = kf_code<0, 1, 1>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          const uint32_t c111 = kf_code<1, 1, 1>(Bk[r], L, R, D, U, Zm[r], Pn[r]);
+          NC[r][0] = c000 | (c100 << 8) | (c001 << 16) | (c101 << 24);
+          NC[r][1] = c010 | (c110 << 8) | (c011 << 16) | (c111 << 24);
         }
-        const uint32_t c000 = kf_code<0, 0, 0>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c100 = kf_code<1, 0, 0>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c010 = kf_code<0, 1, 0>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c110 = kf_code<1, 1, 0>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c001 = kf_code<0, 0, 1>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c101 = kf_code<1, 0, 1>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c011 = kf_code<0, 1, 1>(Bk, L, R, D, U, Zm, Pn);
-        const uint32_t c111 = kf_code<1, 1, 1>(Bk, L, R, D, U, Zm, Pn);
-        NC[0] = c000 | (c100 << 8) | (c001 << 16) | (c101 << 24);
-        NC[1] = c010 | (c110 << 8) | (c011 << 16) | (c111 << 24);
       }
-      // tags of B(z-2) (not needed in the halo warps)
-      if (!halo_w && __any_sync(0xFFFFFFFFu, (CC[0] & CC[1] & 0x40404040u) != 0x40404040u)) {
-        const uint32_t CD = S.c1[buf][wm][lane], CU = S.c0[buf][wp][lane];
+      // tags of B(z-2), rows that are not halo
+      const uint32_t CDw = S.c1[buf][wm][lane], CUw = S.c0[buf][wp][lane];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (halo[r] ||
+            !__any_sync(0xFFFFFFFFu, (CC[r][0] & CC[r][1] & 0x40404040u) != 0x40404040u))
+          continue;
+        const uint32_t CD = r == 0 ? CDw : CC[0][1], CU = r == 0 ? CC[1][0] : CUw;
         uint32_t CL[2], CR[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          CL[q] = __shfl_up_sync(0xFFFFFFFFu, CC[q], 1);
-          CR[q] = __shfl_down_sync(0xFFFFFFFFu, CC[q], 1);
+          CL[q] = __shfl_up_sync(0xFFFFFFFFu, CC[r][q], 1);
+          CR[q] = __shfl_down_sync(0xFFFFFFFFu, CC[r][q], 1);
         }
-        // neighbour codes by direction, byte p = i + 2k (see kf_tags_word)
-        T0 = kf_tags_word<0>(CC[0], __byte_perm(CL[0], CC[0], 0x6341),
-                             __byte_perm(CC[0], CR[0], 0x6341), CD, CC[1],
-                             __byte_perm(CZm[0], CC[0], 0x5432), __byte_perm(CC[0], NC[0], 0x5432));
-        T1 = kf_tags_word<1>(CC[1], __byte_perm(CL[1], CC[1], 0x6341),
-                             __byte_perm(CC[1], CR[1], 0x6341), CC[0], CU,
-                             __byte_perm(CZm[1], CC[1], 0x5432), __byte_perm(CC[1], NC[1], 0x5432));
+        T[r][0] = kf_tags_word<0>(CC[r][0], __byte_perm(CL[0], CC[r][0], 0x6341),
+                                  __byte_perm(CC[r][0], CR[0], 0x6341), CD, CC[r][1],
+                                  __byte_perm(CZm[r][0], CC[r][0], 0x5432),
+                                  __byte_perm(CC[r][0], NC[r][0], 0x5432));
+        T[r][1] = kf_tags_word<1>(CC[r][1], __byte_perm(CL[1], CC[r][1], 0x6341),
+                                  __byte_perm(CC[r][1], CR[1], 0x6341), CC[r][0], CU,
+                                  __byte_perm(CZm[r][1], CC[r][1], 0x5432),
+                                  __byte_perm(CC[r][1], NC[r][1], 0x5432));
       }
     }
-    // stores: births of B(z-1), tags of B(z-2); counters from the codes (bit 6 = absent) and
-    // the tags (bit 7 = UP).  Cell (i,j,k) exists iff (i=0 or hx), (j=0 or hy), (k=0 or hz).
-    if (out) {
+    // stores (as in k_filtration), per row
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (!out[r]) continue;
       const int zb1 = z - 1, zb2 = z - 2;
       if (zb1 >= z0 && zb1 < z1) {
-        fin0 += (~NC[0] >> 6) & 0x01010101u;
-        fin1 += (~NC[1] >> 6) & 0x01010101u;
-        uint32_t* p0 = births + (uint32_t(zb1) * 2u * P.KXY + rowbase);
+        fin0 += (~NC[r][0] >> 6) & 0x01010101u;
+        fin1 += (~NC[r][1] >> 6) & 0x01010101u;
+        uint32_t* p0 = births + (uint32_t(zb1) * 2u * P.KXY + rowbase[r]);
         uint32_t* p1 = p0 + P.KX;
         const bool hz = zb1 + 1 < nz;
-        p0[0] = Bk[0];
-        if (hx) p0[1] = Bk[1];
-        if (hy) p1[0] = Bk[2];
-        if (hx && hy) p1[1] = Bk[3];
+        p0[0] = Bk[r][0];
+        if (hx) p0[1] = Bk[r][1];
+        if (hy[r]) p1[0] = Bk[r][2];
+        if (hx && hy[r]) p1[1] = Bk[r][3];
         if (hz) {
           uint32_t* p2 = p0 + P.KXY;
           uint32_t* p3 = p1 + P.KXY;
-          p2[0] = Bk[4];
-          if (hx) p2[1] = Bk[5];
-          if (hy) p3[0] = Bk[6];
-          if (hx && hy) p3[1] = Bk[7];
+          p2[0] = Bk[r][4];
+          if (hx) p2[1] = Bk[r][5];
+          if (hy[r]) p3[0] = Bk[r][6];
+          if (hx && hy[r]) p3[1] = Bk[r][7];
         }
       }
       if (zb2 >= z0 && zb2 < z1) {
-        up0 += (T0 >> 7) & 0x01010101u;
-        up1 += (T1 >> 7) & 0x01010101u;
-        uint8_t* p0 = tags + (uint32_t(zb2) * 2u * P.KXY + rowbase);
+        up0 += (T[r][0] >> 7) & 0x01010101u;
+        up1 += (T[r][1] >> 7) & 0x01010101u;
+        uint8_t* p0 = tags + (uint32_t(zb2) * 2u * P.KXY + rowbase[r]);
         uint8_t* p1 = p0 + P.KX;
         const bool hz = zb2 + 1 < nz;
-        p0[0] = uint8_t(T0);
-        if (hx) p0[1] = uint8_t(T0 >> 8);
-        if (hy) p1[0] = uint8_t(T1);
-        if (hx && hy) p1[1] = uint8_t(T1 >> 8);
+        p0[0] = uint8_t(T[r][0]);
+        if (hx) p0[1] = uint8_t(T[r][0] >> 8);
+        if (hy[r]) p1[0] = uint8_t(T[r][1]);
+        if (hx && hy[r]) p1[1] = uint8_t(T[r][1] >> 8);
         if (hz) {
           uint8_t* p2 = p0 + P.KXY;
           uint8_t* p3 = p1 + P.KXY;
-          p2[0] = uint8_t(T0 >> 16);
-          if (hx) p2[1] = uint8_t(T0 >> 24);
-          if (hy) p3[0] = uint8_t(T1 >> 16);
-          if (hx && hy) p3[1] = uint8_t(T1 >> 24);
+          p2[0] = uint8_t(T[r][0] >> 16);
+          if (hx) p2[1] = uint8_t(T[r][0] >> 24);
+          if (hy[r]) p3[0] = uint8_t(T[r][1] >> 16);
+          if (hx && hy[r]) p3[1] = uint8_t(T[r][1] >> 24);
         }
       }
     }
-    // shift the pipeline
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      Zm[q] = Bk[q + 4];
-      P0[q] = Pn[q];
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Zm[r][q] = Bk[r][q + 4];
+        P0[r][q] = Pn[r][q];
+      }
+      CZm[r][0] = CC[r][0];
+      CZm[r][1] = CC[r][1];
+      CC[r][0] = NC[r][0];
+      CC[r][1] = NC[r][1];
     }
-    CZm[0] = CC[0];
-    CZm[1] = CC[1];
-    CC[0] = NC[0];
-    CC[1] = NC[1];
     f2 = f1;
     f1 = f0;
     f0 = fn;
     rs = rn;
   }
   kf_wait<0>();
-  // counters: byte p of word j is cell (i, j, k) with p = i + 2k, dim = i + j + k
   auto B8 = [](uint32_t v, int p) { return (v >> (8 * p)) & 0xFFu; };
-  const uint32_t v[7] = {B8(up0, 0),                                      // UP, dim 0
-                         B8(up0, 1) + B8(up0, 2) + B8(up1, 0),             // UP, dim 1
-                         B8(up0, 3) + B8(up1, 1) + B8(up1, 2),             // UP, dim 2
-                         B8(fin0, 0),                                     // finite, dim 0
-                         B8(fin0, 1) + B8(fin0, 2) + B8(fin1, 0),          // dim 1
-                         B8(fin0, 3) + B8(fin1, 1) + B8(fin1, 2),          // dim 2
-                         B8(fin1, 3)};                                    // dim 3
+  const uint32_t vv[7] = {B8(up0, 0),
+                          B8(up0, 1) + B8(up0, 2) + B8(up1, 0),
+                          B8(up0, 3) + B8(up1, 1) + B8(up1, 2),
+                          B8(fin0, 0),
+                          B8(fin0, 1) + B8(fin0, 2) + B8(fin1, 0),
+                          B8(fin0, 3) + B8(fin1, 1) + B8(fin1, 2),
+                          B8(fin1, 3)};
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
-    const uint32_t s = __reduce_add_sync(0xFFFFFFFFu, v[q]);
-    if (lane == 0 && s) atomicAdd(S.cnt + q, s);
+    const uint32_t sm = __reduce_add_sync(0xFFFFFFFFu, vv[q]);
+    if (lane == 0 && sm) atomicAdd(S.cnt + q, sm);
   }
   const bool anynan = __any_sync(0xFFFFFFFFu, nan);
   if (lane == 0 && anynan) atomicOr(nan_flag, 1);
@@ -1175,14 +1237,18 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // K1 + K2 in one streaming kernel (round 1 measured the split alternatives, profiles/r01/s3:
   // C5 0.52 + 3.60 ms as separate births + apparent-pair kernels)
   {
-    const KfLaunch L = kf_launch(g);
+    const KfLaunch L = kf_launch(g, K2_ROWS);
     static thread_local int kf_attr_dev = -1;
     if (kf_attr_dev != ws.device()) {
       CR_CUDA(cudaFuncSetAttribute(k_filtration, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sizeof(KfSmem))));
+                                   int(sizeof(Kf2Smem))));
       kf_attr_dev = ws.device();
     }
-    KfP kp = kf_params(g, L.zc);
+    KfP kp = kf2_params(g, L.zc);
+    auto launch_kf = [&](unsigned grid) {
+      k_filtration<<<grid, K2_THREADS, sizeof(Kf2Smem), s>>>(image, kp, S.births, S.tags, cnt,
+                                                            nan_flag);
+    };
     const uint32_t nzc = uint32_t((g.nz + L.zc - 1) / L.zc), xy = kp.XB * kp.YB;
     const int64_t plane = g.nx * g.ny;
     int64_t forest_z = 0;  // planes [0, forest_z) have their basin forest
@@ -1203,8 +1269,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       forest_z = zt;
     };
     if (S.nready == 0) {
-      k_filtration<<<L.grid, KF_THREADS, sizeof(KfSmem), s>>>(image, kp, S.births, S.tags, cnt,
-                                                              nan_flag);
+      launch_kf(L.grid);
       CR_CHECK_LAUNCH();
     } else {
       // input arriving in pieces: z-chunk c reads planes up to (c + 1) zc + 4; launch the chunks
@@ -1218,8 +1283,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
         if (c1 == c0) continue;
         CR_CUDA(cudaStreamWaitEvent(s, S.ready_ev[i], 0));
         kp.zb0 = c0;
-        k_filtration<<<(c1 - c0) * xy, KF_THREADS, sizeof(KfSmem), s>>>(image, kp, S.births,
-                                                                        S.tags, cnt, nan_flag);
+        launch_kf((c1 - c0) * xy);
         CR_CHECK_LAUNCH();
         c0 = c1;
         // births and tags are final for the planes below c0 zc - 1 (the last output plane's

@@ -106,7 +106,8 @@ def test_general_path_on_1d(cr):
 
 
 def test_filtration_tiles_ragged(cr):
-    """K1+K2 (one fused kernel) on shapes whose extents are not multiples of its tiles: the
+    """K1+K2 (one fused kernel) on shapes whose extents are not multiples of its tiles (30
+    columns x 6 rows x z-chunks; two rows per warp, so odd row counts leave a half-used warp): the
     pairing is the oracle's and the cell / apparent-pair counts equal their numpy definitions
     (tests/apparent.py) -- a missed apparent pair would still be paired by the reduction, so the
     counts are compared too."""
@@ -116,7 +117,11 @@ def test_filtration_tiles_ragged(cr):
             gen.small_int_image((9, 70, 13), 3, seed=22, inf_frac=0.1),
             gen.small_int_image((67, 35), 4, seed=23, inf_frac=0.05),
             gen.small_int_image((20, 45, 61), 3, seed=24, inf_frac=0.05),
-            gen.masked_grf((70, 31, 29), 1.5, 12.0, 25)]
+            gen.masked_grf((70, 31, 29), 1.5, 12.0, 25),
+            gen.small_int_image((11, 7, 31), 3, seed=26, inf_frac=0.05),   # 7 rows: 6 + 1
+            gen.small_int_image((5, 12, 60), 4, seed=27),                 # 12 rows: 2 tiles exactly
+            gen.small_int_image((13, 1, 17), 3, seed=28),                 # a single row
+            gen.small_int_image((6, 5), 3, seed=29)]                      # 2D, 5 rows
     for k, img in enumerate(imgs):
         o = oracle.ph(img, img.ndim - 1, partner=True)
         t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
