@@ -512,11 +512,6 @@ __device__ __forceinline__ uint32_t vox_kidx(const Geom& g, uint32_t v) {
   uint32_t x = v % nx, r = v / nx, y = r % ny, z = r / ny;
   return (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
 }
-__device__ __forceinline__ uint32_t kidx_vox(const Geom& g, uint32_t k) {
-  uint32_t X, Y, Z;
-  coords_of(g, k, X, Y, Z);
-  return ((Z >> 1) * uint32_t(g.ny) + (Y >> 1)) * uint32_t(g.nx) + (X >> 1);
-}
 
 // parent of every voxel in the apparent-pair forest, and the number of basins (present vertices
 // that are not the lower cell of an apparent pair) into *nbasins
@@ -688,21 +683,6 @@ __device__ __forceinline__ bool top_of_voxel(const Geom& g, uint32_t v, uint32_t
   k = (Z * uint32_t(g.KY) + Y) * uint32_t(g.KX) + X;
   return true;
 }
-__device__ __forceinline__ uint32_t coord_of(const Geom& g, uint32_t k, int a) {
-  const uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  return a == 0 ? k % KX : (a == 1 ? (k / KX) % KY : k / (KX * KY));
-}
-__device__ __forceinline__ uint32_t extent_of(const Geom& g, int a) {
-  return uint32_t(a == 0 ? g.KX : (a == 1 ? g.KY : g.KZ));
-}
-// dual vertex of the top cell on side sg (0: -, 1: +) of face k along axis a (OMEGA if outside)
-__device__ __forceinline__ uint32_t dual_side(const DualG& G, uint32_t k, int a, int sg) {
-  const uint32_t c = coord_of(G.g, k, a);
-  if (sg ? c + 1 >= extent_of(G.g, a) : c == 0) return G.omega;
-  const int64_t st = G.g.stride(a);
-  return kidx_vox(G.g, uint32_t(int64_t(k) + (sg ? st : -st)));
-}
-
 // absent_to_omega: no +inf cavity is enclosed (Euler count, see top_dual), so every absent top
 // cell lies in the outside vertex's component and hangs under it directly.
 __global__ void k_dual_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
@@ -711,16 +691,35 @@ __global__ void k_dual_parent(const uint32_t* __restrict__ births, const uint8_t
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
     parent[G.omega] = G.omega;
   if (!vox_of_thread(G.g, v, x, y, z)) return;
-  uint32_t p = v, k;
-  if (top_of_voxel(G.g, v, k)) {
+  // the top cell with base voxel v (odd on every active axis), from v's coordinates (no second
+  // decode of v or of the cell's kidx)
+  const uint32_t c[3] = {x, y, z};
+  const uint32_t n[3] = {uint32_t(G.g.nx), uint32_t(G.g.ny), uint32_t(G.g.nz)};
+  const uint32_t vs[3] = {1u, n[0], n[0] * n[1]};
+  bool has_top = true;
+  uint32_t K[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (n[a] > 1) {
+      has_top = has_top && c[a] + 1 < n[a];
+      K[a] = 2 * c[a] + 1;
+    } else {
+      K[a] = 0;
+    }
+  }
+  uint32_t p = v;
+  if (has_top) {
+    const uint32_t k = (K[2] * uint32_t(G.g.KY) + K[1]) * uint32_t(G.g.KX) + K[0];
     if (births[k] == ABSENT_ORD) {
       if (absent_to_omega) p = G.omega;
     } else {
       const uint8_t t = tags[k];
-      if (tag_kind(t) == KIND_DOWN) {  // dual apparent pair: hangs under its face's other coface
-        const int dir = tag_dir(t);
-        const uint32_t f = uint32_t(int64_t(k) + dir_offset(G.g, dir));
-        p = dual_side(G, f, dir >> 1, dir & 1);
+      if (tag_kind(t) == KIND_DOWN) {
+        // dual apparent pair (face f = k + dir, top cell k): k hangs under f's other coface, the
+        // top cell two steps along the axis -- base voxel v -/+ e_a, or OMEGA past the border
+        const int dir = tag_dir(t), a = dir >> 1;
+        if (dir & 1) p = c[a] + 2 < n[a] ? v + vs[a] : G.omega;
+        else p = c[a] > 0 ? v - vs[a] : G.omega;
       }
     }
   }
