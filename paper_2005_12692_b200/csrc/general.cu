@@ -29,14 +29,6 @@ Geom make_geom(const int64_t* shape, int ndim) {
 
 namespace {
 
-__device__ __forceinline__ void coords_of(const Geom& g, uint32_t k, uint32_t& X, uint32_t& Y,
-                                          uint32_t& Z) {
-  uint32_t KX = uint32_t(g.KX), KY = uint32_t(g.KY);
-  X = k % KX;
-  uint32_t r = k / KX;
-  Y = r % KY;
-  Z = r / KY;
-}
 
 // ---------------------------------------------------------------------------------------------
 // K1 + K2 fused (the default): births AND apparent-pair tags of every cell from one read of the
