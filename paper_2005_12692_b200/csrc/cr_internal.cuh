@@ -136,7 +136,7 @@ extern thread_local int64_t g_launch_count;
 
 // One thread per voxel: x within a block row, (y, z) from the grid -- no division per voxel.
 // Images whose y or z extent exceeds the grid limit fall back to a linear launch with division.
-constexpr int VOX_THREADS = 256;
+constexpr int VOX_THREADS = 128;  // measured (C5b H0 + sort + top dim): 64: 12.2 ms, 128: 9.6, 256: 10.0, 512: 10.9
 inline bool vox_grid_ok(const Geom& g) { return g.ny <= 65535 && g.nz <= 65535; }
 inline dim3 vox_grid(const Geom& g) {
   // (measured: a (row, y, z) grid of 128-thread rows was slower on C5b than the linear launch --

@@ -1103,7 +1103,7 @@ __device__ __forceinline__ void jitter_sleep(const RP& P, uint32_t a, uint32_t b
 #ifndef K5_MINB
 #define K5_MINB 2
 #endif
-constexpr size_t K5_SMEM = sizeof(uint64_t) * WPB * (2 * FCAP + 8 + STAGE);
+constexpr size_t K5_SMEM = sizeof(uint64_t) * WPB * (2 * FCAP + SMALLB + STAGE);
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1114,8 +1114,8 @@ template <bool DBG>
 __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
   extern __shared__ uint64_t k5_smem[];  // K5Smem
   uint64_t(*s_F)[2][FCAP] = reinterpret_cast<uint64_t(*)[2][FCAP]>(k5_smem);
-  uint64_t(*s_small)[8] = reinterpret_cast<uint64_t(*)[8]>(k5_smem + WPB * 2 * FCAP);
-  uint64_t(*s_stage)[STAGE] = reinterpret_cast<uint64_t(*)[STAGE]>(k5_smem + WPB * (2 * FCAP + 8));
+  uint64_t(*s_small)[SMALLB] = reinterpret_cast<uint64_t(*)[SMALLB]>(k5_smem + WPB * 2 * FCAP);
+  uint64_t(*s_stage)[STAGE] = reinterpret_cast<uint64_t(*)[STAGE]>(k5_smem + WPB * (2 * FCAP + SMALLB));
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t w = blockIdx.x * WPB + wib;
