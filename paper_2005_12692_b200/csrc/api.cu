@@ -86,6 +86,8 @@ cr_status fail(const Error& e) {
 
 // Stack `batch` images along the slowest axis with one +inf separator layer between them, so the
 // complexes are disjoint (cells touching a separator are absent, reading R5).
+
+
 __global__ void k_stack(const float* __restrict__ src, int64_t per_img, int64_t layer,
                         int64_t layers_per_img, int64_t nlayers, float* __restrict__ dst) {
   // one stacked layer per blockIdx.y step (its image and slot computed once per block, not per
@@ -212,7 +214,7 @@ void set_last_stats(const cr_stats& st) { commit_stats(st); }
 // stream, in up to 8 pieces, each piece's event telling run_general's filtration which z-planes
 // have arrived (the filtration of the first pieces overlaps the copy of the later ones).
 static void stage_host_batch(const float* host, int64_t batch, int64_t L, int64_t layer,
-                             float* simg, GeneralState& S, cudaStream_t s) {
+                             float* simg, GeneralState& S, cudaStream_t s, bool stacked) {
   int dev = 0;
   CR_CUDA(cudaGetDevice(&dev));
   // the copy stream and its events: one set per host thread, re-made on a device change and
@@ -245,7 +247,7 @@ static void stage_host_batch(const float* host, int64_t batch, int64_t L, int64_
   cudaEvent_t* ev = C.ev;
   CR_CUDA(cudaEventRecord(ev[16], s));  // the buffer's previous users on s come first
   CR_CUDA(cudaStreamWaitEvent(cs, ev[16], 0));
-  if (batch > 1) {
+  if (stacked && batch > 1) {  // 2D: separator rows written in place
     int64_t bx = (layer + 255) / 256;
     if (bx > 64) bx = 64;
     const unsigned by = unsigned(batch - 1 < 65535 ? batch - 1 : 65535);
@@ -257,14 +259,21 @@ static void stage_host_batch(const float* host, int64_t batch, int64_t L, int64_
   S.nready = 0;
   for (int64_t b0 = 0; b0 < batch; b0 += per) {
     const int64_t b1 = b0 + per < batch ? b0 + per : batch;
-    CR_CUDA(cudaMemcpy2DAsync(simg + b0 * (L + 1) * layer, size_t((L + 1) * layer) * sizeof(float),
-                              host + b0 * L * layer, size_t(L * layer) * sizeof(float),
-                              size_t(L * layer) * sizeof(float), size_t(b1 - b0),
+    if (stacked)
+      CR_CUDA(cudaMemcpy2DAsync(simg + b0 * (L + 1) * layer, size_t((L + 1) * layer) * sizeof(float),
+                                host + b0 * L * layer, size_t(L * layer) * sizeof(float),
+                                size_t(L * layer) * sizeof(float), size_t(b1 - b0),
+                                cudaMemcpyHostToDevice, cs));
+    else
+      CR_CUDA(cudaMemcpyAsync(simg + b0 * L * layer, host + b0 * L * layer,
+                              size_t((b1 - b0) * L * layer) * sizeof(float),
                               cudaMemcpyHostToDevice, cs));
     const int i = S.nready++;
     CR_CUDA(cudaEventRecord(ev[i], cs));
     S.ready_ev[i] = ev[i];
-    S.ready_z[i] = b1 * (L + 1);  // its volumes and the separator after them (written on s)
+    // 3D: the stacked planes of its images (+ the virtual separator after them); 2D: one plane,
+    // so the filtration waits for the last piece
+    S.ready_z[i] = stacked ? (b1 == batch ? 1 : 0) : b1 * (L + 1);
   }
 }
 
@@ -465,27 +474,43 @@ static cr_status batched_impl(const float* images, const float* host_images, int
     stacked[0] = batch * (L + 1) - 1;
     if (!valid_shape(stacked, ndim)) return CR_EINVAL;
     Geom g = make_geom(stacked, ndim);
-    const int64_t layers = L;
     Workspace ws(s);
     HostScalars hs;
     cr_stats st{};
     st.path = 3;
     prof_begin(s);
-    float* simg = ws.alloc<float>(g.nvox);
+    // 3D: the filtration reads the volumes unstacked (the separator planes are virtual:
+    // KfP::zper), so the batch is never copied into the stacked layout.  2D batches stack along
+    // y, which the filtration's plane walk does not see: they are copied into the stacked layout.
     GeneralState S;
-    if (host_images) {
-      stage_host_batch(host_images, batch, L, layer, simg, S, s);
+    const bool unstacked = ndim == 3;
+    const float* simg = images;
+    float* staged = nullptr;
+    if (unstacked) {
+      S.img_zper = uint32_t(L + 1);
+      S.img_zimg = uint32_t(L);
+      if (host_images) {
+        staged = ws.alloc<float>(batch * L * layer);
+        stage_host_batch(host_images, batch, L, layer, staged, S, s, false);
+        simg = staged;
+      }
     } else {
-      const int64_t nlayers = g.nvox / layer;
-      int64_t bx = (layer / 4 + 255) / 256;
-      if (bx < 1) bx = 1;
-      if (bx > 64) bx = 64;
-      const unsigned by = unsigned(nlayers < 65535 ? nlayers : 65535);
-      k_stack<<<dim3(unsigned(bx), by), 256, 0, s>>>(images, layers * layer, layer, layers,
-                                                     nlayers, simg);
+      staged = ws.alloc<float>(g.nvox);
+      if (host_images) {
+        stage_host_batch(host_images, batch, L, layer, staged, S, s, true);
+      } else {
+        const int64_t nlayers = g.nvox / layer;
+        int64_t bx = (layer / 4 + 255) / 256;
+        if (bx < 1) bx = 1;
+        if (bx > 64) bx = 64;
+        const unsigned by = unsigned(nlayers < 65535 ? nlayers : 65535);
+        k_stack<<<dim3(unsigned(bx), by), 256, 0, s>>>(images, L * layer, layer, L, nlayers,
+                                                       staged);
+        CR_CHECK_LAUNCH();
+      }
+      simg = staged;
+      prof_mark(s, "stack");
     }
-    CR_CHECK_LAUNCH();
-    prof_mark(s, "stack");  // its own stage: "filtration" then times k_filtration alone
     {  // Khalimsky cells per image period along the stacking axis: kidx / seg_cells = image
       uint64_t cl = 1;
       for (int i = 1; i < ndim; ++i) cl *= uint64_t(2 * shape[i] - 1);
@@ -493,7 +518,7 @@ static cr_status batched_impl(const float* images, const float* host_images, int
     }
     int dm = report_dmax(g1, maxdim);
     run_general(simg, g, dm, ws, hs, S, st);
-    ws.release(simg);
+    if (staged) ws.release(staged);
     // batched emission
     int64_t nrec = 0;
     for (int d = 0; d <= dm; ++d) nrec += S.R.n[d];

@@ -157,6 +157,9 @@ constexpr int KF_VCOLS = 33;
 struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsky grid < 2^32 cells)
   uint32_t nx, ny, nz, KX, KXY, plane, XB, YB, zc;
   uint32_t zb0;  // first z-chunk of this launch
+  // batches read unstacked: stacked plane zz is plane (zz % zper) of image zz / zper, and the
+  // separator (+inf) when zz % zper == zimg (zper = zimg + 1); zper == 0: planes as they are
+  uint32_t zper, zimg;
 };
 inline KfP kf_params(const Geom& g, int zc) {
   KfP p;
@@ -170,6 +173,7 @@ inline KfP kf_params(const Geom& g, int zc) {
   p.YB = 1;  // set by the launcher (rows per CTA)
   p.zc = uint32_t(zc);
   p.zb0 = 0;
+  p.zper = p.zimg = 0;
   return p;
 }
 
@@ -250,10 +254,29 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __res
   const int ys = y0 >= 0 ? y0 : 0;  // copies of row 0 / 1 are offsets of (x, ys) when valid
   const float* gsrc = img + (vx ? uint64_t(uint32_t(ys) * P.nx + uint32_t(x)) : 0ull);
   const int d0 = y0 >= 0 ? 0 : 1;   // y0 = -1 only for warp 0's halo row 0 (never copied)
+  // source plane of the next stacked plane >= 0 this thread issues (issue() is called for
+  // consecutive planes): image pb, plane pl of its period (one division here, increments after)
+  const int zfirst = z0 - 2 > 0 ? z0 - 2 : 0;
+  uint32_t pb = P.zper ? uint32_t(zfirst) / P.zper : 0u;
+  uint32_t pl = P.zper ? uint32_t(zfirst) - pb * P.zper : uint32_t(zfirst);
   auto issue = [&](int zz, uint32_t sl) {
-    if (zz >= 0 && zz < nz) {  // CTA-uniform
+    bool real = zz >= 0 && zz < nz;  // CTA-uniform
+    uint32_t src = 0;
+    if (zz >= 0) {
+      if (P.zper) {
+        real = real && pl != P.zimg;  // a separator plane is +inf
+        src = pb * P.zimg + pl;
+        if (++pl == P.zper) {
+          pl = 0;
+          ++pb;
+        }
+      } else {
+        src = pl++;
+      }
+    }
+    if (real) {
       const uint32_t a = sv0 + sl * SLOT;
-      const float* p = gsrc + uint64_t(uint32_t(zz)) * P.plane - (d0 ? P.nx : 0u);
+      const float* p = gsrc + uint64_t(src) * P.plane - (d0 ? P.nx : 0u);
       if (o0) kf_cp4(a, p);
       if (o0x) kf_cp4(a + 4 * c32, p + 1);
       if (o1) kf_cp4(a + ROW, p + P.nx);
@@ -1236,6 +1259,8 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       kf_attr_dev = ws.device();
     }
     KfP kp = kf2_params(g, L.zc);
+    kp.zper = S.img_zper;
+    kp.zimg = S.img_zimg;
     auto launch_kf = [&](unsigned grid) {
       k_filtration<<<grid, K2_THREADS, sizeof(Kf2Smem), s>>>(image, kp, S.births, S.tags, cnt,
                                                             nan_flag);

@@ -23,6 +23,9 @@ struct GeneralState {
   // Input arriving in pieces (cr_barcodes_batched_host): planes [0, ready_z[i]) of the image are
   // on the device once event ready_ev[i] has fired; the filtration launches its z-chunks as their
   // planes (and the 4 after them it reads) arrive instead of waiting for the whole copy.
+  // a stacked batch read unstacked by the filtration (see KfP::zper): planes per image period
+  // (images + separator) and per image; 0 = the image is laid out as the geometry says
+  uint32_t img_zper = 0, img_zimg = 0;
   int nready = 0;
   int64_t ready_z[16];
   cudaEvent_t ready_ev[16];
