@@ -532,7 +532,7 @@ __device__ __forceinline__ uint32_t vox_kidx(const Geom& g, uint32_t v) {
 // that are not the lower cell of an apparent pair) into *nbasins
 __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                             Geom g, uint32_t* __restrict__ parent, unsigned long long* nbasins,
-                            uint32_t vbase, uint32_t vend) {
+                            uint32_t vbase, uint32_t vend, uint32_t* __restrict__ basins) {
   // voxels [vbase, vend) (a piece of the image: see run_general)
   const uint64_t vv = uint64_t(vbase) + uint64_t(blockIdx.x) * VOX_THREADS + threadIdx.x;
   const uint32_t v = uint32_t(vv);
@@ -556,8 +556,47 @@ __global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* 
     }
     parent[v] = p;
   }
+  // the basins are listed (their count is the list's length): the final H0 roots are among them
+  // (k_h0_roots), so the essential classes need not be found by a scan of every voxel
   const unsigned mask = __ballot_sync(0xFFFFFFFFu, basin);
-  if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nbasins, (unsigned long long)__popc(mask));
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(nbasins, (unsigned long long)__popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+  if (basin) basins[base + __popc(mask & ((1u << lane) - 1))] = v;
+}
+
+// Essential H0 classes: the listed basins that are still roots after the merge rounds.
+__global__ void k_h0_roots(const uint32_t* __restrict__ basins,
+                           const unsigned long long* __restrict__ nbasins,
+                           const uint32_t* __restrict__ births, Geom g,
+                           const uint32_t* __restrict__ parent, uint64_t* rec,
+                           unsigned long long* nrec, unsigned long long* nroots) {
+  const unsigned long long n = *nbasins;
+  const unsigned long long stride = uint64_t(gridDim.x) * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long i0 = uint64_t(blockIdx.x) * blockDim.x; i0 < n; i0 += stride) {
+    const unsigned long long i = i0 + threadIdx.x;
+    bool emit = false;
+    uint32_t k = 0;
+    if (i < n) {
+      const uint32_t v = basins[i];
+      emit = parent[v] == v;
+      const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
+      const uint32_t r = v / nx, x = v - r * nx, z = r / ny, y = r - z * ny;
+      k = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
+    }
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
+    if (!mask) continue;
+    unsigned long long base = 0;
+    if (lane == __ffs(mask) - 1) {
+      base = atomicAdd(nrec, (unsigned long long)__popc(mask));
+      atomicAdd(nroots, (unsigned long long)__popc(mask));
+    }
+    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
+    if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
+  }
 }
 
 
@@ -648,27 +687,6 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
   return p;
 }
 
-__global__ void k_h0_essential(const uint32_t* __restrict__ births, Geom g,
-                               const uint32_t* __restrict__ parent, uint64_t* rec,
-                               unsigned long long* nrec, unsigned long long* nroots) {
-  uint32_t v, x, y, z;
-  bool emit = false;
-  uint32_t k = 0;
-  if (vox_of_thread(g, v, x, y, z)) {
-    k = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
-    emit = parent[v] == v && births[k] != ABSENT_ORD;
-  }
-  unsigned mask = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!mask) return;
-  int lane = threadIdx.x & 31;
-  unsigned long long base = 0;
-  if (lane == __ffs(mask) - 1) {
-    base = atomicAdd(nrec, (unsigned long long)__popc(mask));
-    if (nroots) atomicAdd(nroots, (unsigned long long)__popc(mask));
-  }
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (emit) rec[base + __popc(mask & ((1u << lane) - 1))] = (uint64_t(k) << 32) | NONE32;
-}
 
 // ---------------------------------------------------------------------------------------------
 // Top dimension D-1 by Alexander duality ("--top_dim").
@@ -1235,6 +1253,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   CR_CUDA(cudaMemsetAsync(cnt, 0, 32 * sizeof(unsigned long long), s));
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);  // H0 basin forest
+  uint32_t* basins = ws.alloc<uint32_t>(g.nvox);  // the forest's roots (non-apparent vertices)
   bool h0_forest_done = false;
   // H0 candidate edges, room for every edge of the grid (a bound known without reading the
   // finite-cell counts back: no host sync before the merge rounds, and pieces of a host batch
@@ -1275,7 +1294,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       if (zt <= forest_z) return;
       const int64_t v0 = forest_z * plane, v1 = zt * plane;
       k_h0_parent<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
-          S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1));
+          S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1), basins);
       CR_CHECK_LAUNCH();
       k_pointer_jump<<<grid_for(v1 - v0, 256), 256, 0, s>>>(parent, v0, v1);
       CR_CHECK_LAUNCH();
@@ -1340,7 +1359,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   if (!cand) cand = ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1);
   if (!h0_forest_done) {
     k_h0_parent<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
-        S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox));
+        S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox), basins);
     CR_CHECK_LAUNCH();
     k_pointer_jump<<<grid_for(g.nvox, 256), 256, 0, s>>>(parent, 0, g.nvox);
     CR_CHECK_LAUNCH();
@@ -1359,8 +1378,8 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   mm_rounds<false>(cand, ncand, nedges, parent, best, unsigned(g.nvox), alive, S.births, g,
                    DualG{g, uint32_t(g.nvox)}, S.tags, S.R.rec[0], nrec0, ctl, ws);
   // essential classes: the final roots (parent[v] == v holds exactly for them; no flattening)
-  k_h0_essential<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, g, parent, S.R.rec[0], nrec0,
-                                                    cnt + 22);
+  k_h0_roots<<<148 * 8, 256, 0, s>>>(basins, cnt + 8, S.births, g, parent, S.R.rec[0], nrec0,
+                                     cnt + 22);
   CR_CHECK_LAUNCH();
   // the one read of H0: NaN flag, cell / apparent / basin counts, records, roots, rounds
   CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1379,6 +1398,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   ws.release(best);
   ws.release(alive);
   ws.release(parent);
+  ws.release(basins);
 
   reduce_dims(S, g, dmax, ws, hs, st);
 }
