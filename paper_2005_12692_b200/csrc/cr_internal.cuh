@@ -205,15 +205,22 @@ __device__ __forceinline__ void block_append(const bool (&emit)[NI], const T (&i
 template <class T, int NI>
 __device__ __forceinline__ void warp_append(const bool (&emit)[NI], const T (&item)[NI],
                                             T* __restrict__ out, unsigned* __restrict__ n) {
+  // one atomic per warp for all NI slots (same-address atomics serialise at the L2 slice)
   const int lane = threadIdx.x & 31;
+  unsigned mask[NI], total = 0;
 #pragma unroll
   for (int i = 0; i < NI; ++i) {
-    const unsigned mask = __ballot_sync(0xFFFFFFFFu, emit[i]);
-    if (!mask) continue;
-    unsigned base = 0;
-    if (lane == __ffs(mask) - 1) base = atomicAdd(n, __popc(mask));
-    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-    if (emit[i]) out[base + __popc(mask & ((1u << lane) - 1))] = item[i];
+    mask[i] = __ballot_sync(0xFFFFFFFFu, emit[i]);
+    total += __popc(mask[i]);
+  }
+  if (!total) return;
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(n, total);
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    if (emit[i]) out[base + __popc(mask[i] & ((1u << lane) - 1))] = item[i];
+    base += __popc(mask[i]);
   }
 }
 
