@@ -203,6 +203,7 @@ typedef struct {
   int64_t additions[4];   /* column additions in the dim-d reduction                  */
   int64_t addlen[4];      /* sum over additions of the working column length          */
   int64_t maxlen[4];      /* longest working column in the dim-d reduction             */
+  int64_t kf_tma;         /* 1 if the filtration loaded its voxel planes by TMA       */
 } cr_stats;
 void cr_last_stats(cr_stats* out);
 
@@ -228,7 +229,9 @@ typedef enum {
   CR_OPT_TOP_REDUCE = 3,       /* top dimension by the coboundary reduction (not duality)       */
   CR_OPT_K5_BLOCKS_PER_SM = 4, /* resident blocks per SM of the reduction (0: occupancy limit)  */
   CR_OPT_K5_JITTER_NS = 5,     /* pseudo-random delays up to this many ns inside the reduction   */
-  CR_OPT_DEBUG = 6             /* per-stage counters printed to stderr                          */
+  CR_OPT_DEBUG = 6,            /* per-stage counters printed to stderr                          */
+  CR_OPT_KF_TMA = 7            /* filtration voxel ring by TMA (cp.async.bulk.tensor) when the row
+                                  pitch allows it, not per-thread cp.async (measured slower)      */
 } cr_option;
 cr_status cr_set_option(int option, int64_t value);
 

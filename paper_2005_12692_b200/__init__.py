@@ -38,13 +38,15 @@ class CrStats(ctypes.Structure):
                 ("rounds", _i64 * 4), ("pairs", _i64 * 4), ("essential", _i64 * 4),
                 ("path", _i64), ("nstages", ctypes.c_int32), ("stage_ms", ctypes.c_float * 16),
                 ("stage_name", (ctypes.c_char * 24) * 16), ("launches", _i64),
-                ("additions", _i64 * 4), ("addlen", _i64 * 4), ("maxlen", _i64 * 4)]
+                ("additions", _i64 * 4), ("addlen", _i64 * 4), ("maxlen", _i64 * 4),
+                ("kf_tma", _i64)]
 
     def as_dict(self):
         d = {f: list(getattr(self, f)) for f in ("cells", "apparent", "columns", "rounds", "pairs",
                                                   "essential", "additions", "addlen", "maxlen")}
         d["path"] = int(self.path)
         d["launches"] = int(self.launches)
+        d["kf_tma"] = int(self.kf_tma)
         d["stages"] = {self.stage_name[i].value.decode(): float(self.stage_ms[i])
                        for i in range(int(self.nstages))}
         return d
@@ -96,7 +98,7 @@ EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairin
 
 # cr_option (include/cr.h): validation / measurement switches, 0 = the product path
 OPTIONS = {"force_general": 1, "1d_tree": 2, "top_reduce": 3, "k5_blocks_per_sm": 4,
-           "k5_jitter_ns": 5, "debug": 6}
+           "k5_jitter_ns": 5, "debug": 6, "kf_tma": 7}
 
 
 class CrError(RuntimeError):

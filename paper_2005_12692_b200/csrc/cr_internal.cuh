@@ -81,6 +81,7 @@ enum OptKey {
   OPT_K5_BLOCKS_PER_SM = 4,  // resident K5 blocks per SM (<= the occupancy limit)
   OPT_K5_JITTER_NS = 5,      // pseudo-random K5 delays: perturb the schedule (tests)
   OPT_DEBUG = 6,             // per-stage counters on stderr
+  OPT_KF_TMA = 7,            // filtration ring by TMA instead of per-thread cp.async
   OPT_COUNT = 8
 };
 int64_t opt(int key);

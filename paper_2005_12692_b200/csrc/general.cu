@@ -3,6 +3,9 @@
 // The dims >= 1 reduction (K5) is in reduce.cu.
 #include <cooperative_groups.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cub/cub.cuh>
 
 #include "pipeline.cuh"
@@ -152,7 +155,31 @@ template <int N>
 __device__ __forceinline__ void kf_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 constexpr int KF_PF = 3, KF_RING = KF_PF + 1;  // voxel planes in flight, ring slots
-constexpr int KF_VCOLS = 33;
+
+// TMA ring (nx % 4 == 0: the tensor map's row pitch must be a multiple of 16 B): one elected
+// thread loads a CTA's (KF_TCOLS x K2_VROWS) voxel box of a plane with cp.async.bulk.tensor
+// against the slot's mbarrier; out-of-image voxels arrive as 0 and are replaced by +inf on read.
+__device__ __forceinline__ void kf_mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+}
+__device__ __forceinline__ void kf_tma_plane(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                             int z, uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void kf_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
 struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsky grid < 2^32 cells)
   uint32_t nx, ny, nz, KX, KXY, plane, XB, YB, zc;
@@ -188,8 +215,19 @@ inline KfP kf_params(const Geom& g, int zc) {
 #endif
 constexpr int K2_NW = K2_NWARPS, K2_THREADS = 32 * K2_NW, K2_ROWS = 2 * K2_NW - 2;
 constexpr int K2_VROWS = 2 * K2_NW + 1;
-struct Kf2Smem {
-  uint32_t v[KF_RING][K2_VROWS][KF_VCOLS];  // voxel ring (raw float bits)
+// ring slot: K2_VROWS rows of VCOLS voxels (33 used; the TMA box's rows are 36 wide = 144 B, a
+// multiple of 16 B, from a 16-B aligned column: the 33 start at column 1 or 3; slots start on
+// 128 B)
+template <bool TMA>
+struct KfRing {
+  static constexpr int VCOLS = TMA ? 36 : 33;
+  static constexpr int SLOTW = TMA ? ((K2_VROWS * VCOLS * 4 + 127) / 128) * 32 : K2_VROWS * VCOLS;
+  static constexpr uint32_t BOX_BYTES = K2_VROWS * VCOLS * 4;
+};
+template <bool TMA>
+struct alignas(128) Kf2Smem {
+  uint32_t v[KF_RING][KfRing<TMA>::SLOTW];  // voxel ring (raw float bits)
+  unsigned long long bar[KF_RING];           // TMA: the slots' mbarriers
   uint4 b0[2][K2_NW][32];    // row 0's j=0 births (i + 2k), for the warp below's row 1 (its U)
   uint4 b1[2][K2_NW][32];    // row 1's j=1 births, for the warp above's row 0 (its D)
   uint32_t c0[2][K2_NW][32];  // row 0's j=0 code word
@@ -202,14 +240,45 @@ inline KfP kf2_params(const Geom& g, int zc) {
   return p;
 }
 
-__global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __restrict__ img,
+// The image as a 3D tensor (nx, ny, nzsrc) of float32 for the TMA ring: box = one ring slot
+// (36 x K2_VROWS x 1), out-of-bounds voxels zero-filled.  false (-> the cp.async ring) when the
+// row pitch is not a multiple of 16 B, the base is not 16-B aligned, or the driver refuses.
+bool kf_tensor_map(CUtensorMap* map, const float* image, int64_t nx, int64_t ny, int64_t nzsrc) {
+  if (nx % 4 != 0 || (reinterpret_cast<uintptr_t>(image) & 15) != 0) return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t dims[3] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(nzsrc)};
+  const cuuint64_t strides[2] = {cuuint64_t(nx) * 4, cuuint64_t(nx * ny) * 4};
+  const cuuint32_t box[3] = {cuuint32_t(KfRing<true>::VCOLS), cuuint32_t(K2_VROWS), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(image), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool TMA>
+#ifndef K2_MINB
+#define K2_MINB 2
+#endif
+__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float* __restrict__ img,
                                                                const KfP P,
                                                                uint32_t* __restrict__ births,
                                                                uint8_t* __restrict__ tags,
                                                                unsigned long long* __restrict__ cnt,
-                                                               int* __restrict__ nan_flag) {
-  extern __shared__ uint4 kf_dyn[];
-  Kf2Smem& S = *reinterpret_cast<Kf2Smem*>(kf_dyn);
+                                                               int* __restrict__ nan_flag,
+                                                               const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) uint4 kf_dyn[];
+  Kf2Smem<TMA>& S = *reinterpret_cast<Kf2Smem<TMA>*>(kf_dyn);
+  constexpr int VC = KfRing<TMA>::VCOLS;
   const int nx = int(P.nx), ny = int(P.ny), nz = int(P.nz);
   uint32_t blk = blockIdx.x;
   const int xb = int(blk % P.XB);
@@ -233,23 +302,40 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __res
   if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
   constexpr uint32_t INF_BITS = 0x7F800000u;
   // Voxel ring: rows y0(w=0) .. y0(w=0) + 2 NW (the last copied by the last warp), cols x0-1 ..
-  // x0+31 (col 32 copied by lane 31).  A thread copies (x, y0 + r), lane 31 also (x+1, y0 + r);
-  // the last warp also the row after its row 1.  Outside the image: +inf, never copied.
+  // x0+31 (col 32 copied by lane 31).  cp.async ring: a thread copies (x, y0 + r), lane 31 also
+  // (x+1, y0 + r); the last warp also the row after its row 1; outside the image: +inf, never
+  // copied.  TMA ring: thread 0 loads the whole box; the voxels a thread "owns" (checks for
+  // all-+inf planes) are the same.
   const bool o0 = vx && vy[0], o1 = vx && vy[1], o0x = l31 && vx1 && vy[0],
              o1x = l31 && vx1 && vy[1], o2 = lastw && vx && vy2, o2x = lastw && l31 && vx1 && vy2;
-  uint32_t* const vown = &S.v[0][2 * w][lane];
+  // TMA: the box's first column must be 16-B aligned (x % 4 == 0; measured: other x fault), so
+  // it starts at xs = floor4(x0 - 1) and the CTA's columns sit at offset co = x0 - 1 - xs (1 or 3)
+  const int xs = (xb * 30 - 1) & ~3, co = TMA ? xb * 30 - 1 - xs : 0;
+  uint32_t* const vown = &S.v[0][2 * w * VC + lane + co];
   const uint32_t sv0 = uint32_t(__cvta_generic_to_shared(vown));
-  constexpr uint32_t SLOTW = K2_VROWS * KF_VCOLS, SLOT = SLOTW * 4, ROW = KF_VCOLS * 4;
+  constexpr uint32_t SLOTW = KfRing<TMA>::SLOTW, SLOT = SLOTW * 4, ROW = VC * 4;
   const int c32 = 32 - lane;
+  const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&S.bar[0]));
+  const uint32_t ring0 = uint32_t(__cvta_generic_to_shared(&S.v[0][0]));
+  uint32_t rmask = 0, phase = 0;  // TMA: slots holding a loaded plane; their mbarrier parities
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
 #pragma unroll
-  for (int q = 0; q < KF_RING; ++q) {
-    uint32_t* v = vown + q * SLOTW;
-    if (!o0) v[0] = INF_BITS;
-    if (!o1) v[KF_VCOLS] = INF_BITS;
-    if (l31 && !o0x) v[c32] = INF_BITS;
-    if (l31 && !o1x) v[KF_VCOLS + c32] = INF_BITS;
-    if (lastw && !o2) v[2 * KF_VCOLS] = INF_BITS;
-    if (lastw && l31 && !o2x) v[2 * KF_VCOLS + c32] = INF_BITS;
+      for (int q = 0; q < KF_RING; ++q) kf_mbar_init(bar0 + 8 * q);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int q = 0; q < KF_RING; ++q) {
+      uint32_t* v = vown + q * SLOTW;
+      if (!o0) v[0] = INF_BITS;
+      if (!o1) v[VC] = INF_BITS;
+      if (l31 && !o0x) v[c32] = INF_BITS;
+      if (l31 && !o1x) v[VC + c32] = INF_BITS;
+      if (lastw && !o2) v[2 * VC] = INF_BITS;
+      if (lastw && l31 && !o2x) v[2 * VC + c32] = INF_BITS;
+    }
   }
   const int ys = y0 >= 0 ? y0 : 0;  // copies of row 0 / 1 are offsets of (x, ys) when valid
   const float* gsrc = img + (vx ? uint64_t(uint32_t(ys) * P.nx + uint32_t(x)) : 0ull);
@@ -274,39 +360,71 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __res
         src = pl++;
       }
     }
-    if (real) {
-      const uint32_t a = sv0 + sl * SLOT;
-      const float* p = gsrc + uint64_t(src) * P.plane - (d0 ? P.nx : 0u);
-      if (o0) kf_cp4(a, p);
-      if (o0x) kf_cp4(a + 4 * c32, p + 1);
-      if (o1) kf_cp4(a + ROW, p + P.nx);
-      if (o1x) kf_cp4(a + ROW + 4 * c32, p + P.nx + 1);
-      if (lastw) {
-        if (o2) kf_cp4(a + 2 * ROW, p + 2 * P.nx);
-        if (o2x) kf_cp4(a + 2 * ROW + 4 * c32, p + 2 * P.nx + 1);
+    if constexpr (TMA) {
+      real = real && zz <= z1 + 2;  // the last plane the walk reads
+      rmask = real ? rmask | (1u << sl) : rmask & ~(1u << sl);
+      if (real && threadIdx.x == 0)
+        kf_tma_plane(ring0 + sl * SLOT, &tmap, xs, yb * K2_ROWS - 1, int(src),
+                     bar0 + 8 * sl, KfRing<TMA>::BOX_BYTES);
+    } else {
+      if (real) {
+        const uint32_t a = sv0 + sl * SLOT;
+        const float* p = gsrc + uint64_t(src) * P.plane - (d0 ? P.nx : 0u);
+        if (o0) kf_cp4(a, p);
+        if (o0x) kf_cp4(a + 4 * c32, p + 1);
+        if (o1) kf_cp4(a + ROW, p + P.nx);
+        if (o1x) kf_cp4(a + ROW + 4 * c32, p + P.nx + 1);
+        if (lastw) {
+          if (o2) kf_cp4(a + 2 * ROW, p + 2 * P.nx);
+          if (o2x) kf_cp4(a + 2 * ROW + 4 * c32, p + 2 * P.nx + 1);
+        }
+      } else {
+        uint32_t* v = vown + sl * SLOTW;
+        if (o0) v[0] = INF_BITS;
+        if (o1) v[VC] = INF_BITS;
+        if (o0x) v[c32] = INF_BITS;
+        if (o1x) v[VC + c32] = INF_BITS;
+        if (o2) v[2 * VC] = INF_BITS;
+        if (o2x) v[2 * VC + c32] = INF_BITS;
+      }
+      kf_commit();
+    }
+  };
+  // wait until slot sl's plane has arrived (cp.async: the oldest but KF_PF - 1 groups)
+  auto arrive = [&](uint32_t sl) {
+    if constexpr (TMA) {
+      if (rmask >> sl & 1) {
+        kf_mbar_wait(bar0 + 8 * sl, phase >> sl & 1);
+        phase ^= 1u << sl;
       }
     } else {
-      uint32_t* v = vown + sl * SLOTW;
-      if (o0) v[0] = INF_BITS;
-      if (o1) v[KF_VCOLS] = INF_BITS;
-      if (o0x) v[c32] = INF_BITS;
-      if (o1x) v[KF_VCOLS + c32] = INF_BITS;
-      if (o2) v[2 * KF_VCOLS] = INF_BITS;
-      if (o2x) v[2 * KF_VCOLS + c32] = INF_BITS;
+      kf_wait<KF_PF - 1>();
     }
-    kf_commit();
   };
   auto own_inf = [&](uint32_t sl) -> bool {
     const uint32_t* v = vown + sl * SLOTW;
-    bool r = v[0] == INF_BITS && v[KF_VCOLS] == INF_BITS;
-    if (l31) r = r && v[c32] == INF_BITS && v[KF_VCOLS + c32] == INF_BITS;
-    if (lastw) r = r && v[2 * KF_VCOLS] == INF_BITS && (!l31 || v[2 * KF_VCOLS + c32] == INF_BITS);
-    return r;
+    if constexpr (TMA) {  // out-of-image voxels are 0 in the slot: +inf by definition
+      if (!(rmask >> sl & 1)) return true;
+      bool r = (!o0 || v[0] == INF_BITS) && (!o1 || v[VC] == INF_BITS);
+      if (l31) r = r && (!o0x || v[c32] == INF_BITS) && (!o1x || v[VC + c32] == INF_BITS);
+      if (lastw) r = r && (!o2 || v[2 * VC] == INF_BITS) && (!o2x || v[2 * VC + c32] == INF_BITS);
+      return r;
+    } else {
+      bool r = v[0] == INF_BITS && v[VC] == INF_BITS;
+      if (l31) r = r && v[c32] == INF_BITS && v[VC + c32] == INF_BITS;
+      if (lastw) r = r && v[2 * VC] == INF_BITS && (!l31 || v[2 * VC + c32] == INF_BITS);
+      return r;
+    }
   };
+  // TMA: the 4 voxels a row's blocks read are valid (in the image) -- else +inf
+  bool m4[2][4];
+  m4[0][0] = vx && vy[0], m4[0][1] = vx1 && vy[0], m4[0][2] = vx && vy[1], m4[0][3] = vx1 && vy[1];
+  m4[1][0] = vx && vy[1], m4[1][1] = vx1 && vy[1], m4[1][2] = vx && vy2, m4[1][3] = vx1 && vy2;
+  const bool mall = m4[0][0] && m4[0][1] && m4[1][0] && m4[1][1] && m4[1][2] && m4[1][3];
   int z = z0 - 2;
 #pragma unroll
   for (int q = 0; q < KF_PF; ++q) issue(z + q, uint32_t(q));
-  kf_wait<KF_PF - 1>();
+  arrive(0);
   bool f2 = true, f1 = true, f0 = __syncthreads_and(own_inf(0));
   const int wm = max(w - 1, 0), wp = min(w + 1, K2_NW - 1);
   bool nan = false;
@@ -332,11 +450,17 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __res
     const int buf = z & 1;
     if (!fast) {
       const uint32_t* v = vown + rs * SLOTW;
+      const bool sr = !TMA || (rmask >> rs & 1);
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const uint32_t* vr = v + r * KF_VCOLS;
-        const float v00 = __uint_as_float(vr[0]), v10 = __uint_as_float(vr[1]);
-        const float v01 = __uint_as_float(vr[KF_VCOLS]), v11 = __uint_as_float(vr[KF_VCOLS + 1]);
+        const uint32_t* vr = v + r * VC;
+        uint32_t u[4] = {vr[0], vr[1], vr[VC], vr[VC + 1]};
+        if (TMA && !(sr && mall)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) u[q] = sr && m4[r][q] ? u[q] : INF_BITS;
+        }
+        const float v00 = __uint_as_float(u[0]), v10 = __uint_as_float(u[1]);
+        const float v01 = __uint_as_float(u[2]), v11 = __uint_as_float(u[3]);
         nan |= v00 != v00;
         const float ex = fmaxf(v00, v10);
         Pn[r][0] = kf_ord(v00);
@@ -362,8 +486,8 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __res
           Bk[r][q] = Bk[r][q + 4] = ABSENT_ORD;
         }
     }
-    kf_wait<KF_PF - 1>();
     const uint32_t rn = (rs + 1) & (KF_RING - 1);
+    arrive(rn);
     const bool fn = __syncthreads_and(own_inf(rn));
     uint32_t NC[2][2], T[2][2];
 #pragma unroll
@@ -490,7 +614,7 @@ __global__ void __launch_bounds__(K2_THREADS, 2) k_filtration(const float* __res
     f0 = fn;
     rs = rn;
   }
-  kf_wait<0>();
+  if constexpr (!TMA) kf_wait<0>();
   auto B8 = [](uint32_t v, int p) { return (v >> (8 * p)) & 0xFFu; };
   const uint32_t vv[7] = {B8(up0, 0),
                           B8(up0, 1) + B8(up0, 2) + B8(up1, 0),
@@ -1273,16 +1397,33 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     const KfLaunch L = kf_launch(g, K2_ROWS);
     static thread_local int kf_attr_dev = -1;
     if (kf_attr_dev != ws.device()) {
-      CR_CUDA(cudaFuncSetAttribute(k_filtration, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sizeof(Kf2Smem))));
+      CR_CUDA(cudaFuncSetAttribute(k_filtration<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(Kf2Smem<false>))));
+      CR_CUDA(cudaFuncSetAttribute(k_filtration<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(Kf2Smem<true>))));
       kf_attr_dev = ws.device();
     }
     KfP kp = kf2_params(g, L.zc);
     kp.zper = S.img_zper;
     kp.zimg = S.img_zimg;
+    // the source planes the filtration reads (a batch read unstacked has no separator planes)
+    const int64_t nzsrc = kp.zper ? (g.nz + 1) / kp.zper * kp.zimg : g.nz;
+    CUtensorMap tmap;
+    // TMA ring only on request: measured slower than the per-thread cp.async ring (C5b 2.94 vs
+    // 2.74 ms: 2.24 G vs 2.06 G warp instructions -- the +inf selects for the zero-filled
+    // out-of-image voxels and the mbarrier bookkeeping cost more than the 4-byte copies they
+    // replace; profiles/r02/s17)
+    const bool tma = opt(OPT_KF_TMA) != 0 && kf_tensor_map(&tmap, image, g.nx, g.ny, nzsrc);
+    st.kf_tma = tma ? 1 : 0;
     auto launch_kf = [&](unsigned grid) {
-      k_filtration<<<grid, K2_THREADS, sizeof(Kf2Smem), s>>>(image, kp, S.births, S.tags, cnt,
-                                                            nan_flag);
+      if (tma)
+        k_filtration<true><<<grid, K2_THREADS, sizeof(Kf2Smem<true>), s>>>(
+            image, kp, S.births, S.tags, cnt, nan_flag, tmap);
+      else
+        k_filtration<false><<<grid, K2_THREADS, sizeof(Kf2Smem<false>), s>>>(
+            image, kp, S.births, S.tags, cnt, nan_flag, tmap);
     };
     const uint32_t nzc = uint32_t((g.nz + L.zc - 1) / L.zc), xy = kp.XB * kp.YB;
     const int64_t plane = g.nx * g.ny;

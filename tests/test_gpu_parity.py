@@ -134,6 +134,57 @@ def test_filtration_tiles_ragged(cr):
         assert list(st["apparent"])[:3] == exp["apparent"][:3], k
 
 
+def test_filtration_tma_ring(cr):
+    """The TMA voxel ring (option kf_tma; nx % 4 == 0: one cp.async.bulk.tensor box per CTA and
+    plane from a 16-B aligned column, out-of-image voxels zero-filled by TMA and read as +inf)
+    against the oracle and against the per-thread cp.async ring (the product path) on the same
+    images: box edges past the image in x (nx < 36,
+    nx not a multiple of 30) and y (2D images of few rows), +inf masks, -0.0, planes that are +inf
+    over a CTA's footprint (the all-absent fast steps), a 3D batch read unstacked (separator
+    planes never loaded) and NaN detection."""
+    import torch
+    import apparent as ap
+    ball = gen.masked_grf((23, 40, 44), 2.0, 12.0, 31)
+    ball[:6] = np.inf                                              # all-+inf planes first
+    imgs = [gen.small_int_image((4, 4), 3, seed=40),
+            gen.small_int_image((3, 8), 3, seed=41, inf_frac=0.2),
+            gen.small_int_image((67, 36), 4, seed=42, inf_frac=0.05),
+            gen.small_int_image((9, 13, 32), 3, seed=43, inf_frac=0.05),
+            gen.masked_grf((17, 31, 64), 1.5, 10.0, 44),
+            gen.small_int_image((11, 7, 100), 3, seed=45),
+            gen.small_int_image((2, 3, 4), 2, seed=46),
+            ball,
+            np.array([[0.0, -0.0, 1.0, -0.0], [-0.0, 2.0, 0.0, 1.0]], np.float32)]
+    for k, img in enumerate(imgs):
+        o = oracle.ph(img, img.ndim - 1, partner=True)
+        t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        for tma in (0, 1):
+            with cr.options(kf_tma=tma):
+                p = cr.pairing(t).cpu().numpy().view(np.uint32)
+                assert np.array_equal(p, o.partner), (k, tma, np.flatnonzero(p != o.partner)[:10])
+                assert_bars_equal(gpu_bars(cr, img, img.ndim - 1), o, ctx=(k, tma))
+                st = cr.last_stats()
+                assert st["kf_tma"] == tma, (k, tma)
+                exp = ap.counts(img)
+                assert list(st["cells"]) == exp["cells"], k
+                assert list(st["apparent"])[:3] == exp["apparent"][:3], k
+    vs = np.stack([gen.masked_grf((12, 10, 8), 1.5, 4.5, 60 + s) for s in range(7)])
+    with cr.options(kf_tma=1):
+        bc, off = cr.barcodes_batched(torch.from_numpy(vs).cuda(), 2, cells=True)
+        assert cr.last_stats()["kf_tma"] == 1
+    d, b, e, c = bc.numpy()
+    off = off.cpu().numpy()
+    for i in range(len(vs)):
+        s = slice(off[i], off[i + 1])
+        assert_bars_equal((d[s], b[s], e[s], c[s]), oracle.ph(vs[i], 2), ctx=("batch", i))
+    for shape in ((8, 12), (5, 6, 40)):
+        img = gen.small_int_image(shape, 3, seed=70)
+        img.flat[img.size // 2] = np.nan
+        with cr.options(kf_tma=1), pytest.raises(cr.CrError) as ei:
+            cr.barcodes(torch.from_numpy(img).cuda(), len(shape) - 1)
+        assert ei.value.status == cr.CR_EINVAL
+
+
 def _cavity_cases():
     rng = np.random.default_rng(50)
     a = rng.random((20, 22)).astype(np.float32)
