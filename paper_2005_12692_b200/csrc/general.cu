@@ -401,21 +401,6 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
       kf_wait<KF_PF - 1>();
     }
   };
-  auto own_inf = [&](uint32_t sl) -> bool {
-    const uint32_t* v = vown + sl * SLOTW;
-    if constexpr (TMA) {  // out-of-image voxels are 0 in the slot: +inf by definition
-      if (!(rmask >> sl & 1)) return true;
-      bool r = (!o0 || v[0] == INF_BITS) && (!o1 || v[VC] == INF_BITS);
-      if (l31) r = r && (!o0x || v[c32] == INF_BITS) && (!o1x || v[VC + c32] == INF_BITS);
-      if (lastw) r = r && (!o2 || v[2 * VC] == INF_BITS) && (!o2x || v[2 * VC + c32] == INF_BITS);
-      return r;
-    } else {
-      bool r = v[0] == INF_BITS && v[VC] == INF_BITS;
-      if (l31) r = r && v[c32] == INF_BITS && v[VC + c32] == INF_BITS;
-      if (lastw) r = r && v[2 * VC] == INF_BITS && (!l31 || v[2 * VC + c32] == INF_BITS);
-      return r;
-    }
-  };
   // TMA: the 4 voxels a row's blocks read are valid (in the image) -- else +inf
   bool m4[2][4];
   m4[0][0] = vx && vy[0], m4[0][1] = vx1 && vy[0], m4[0][2] = vx && vy[1], m4[0][3] = vx1 && vy[1];
@@ -425,7 +410,10 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
 #pragma unroll
   for (int q = 0; q < KF_PF; ++q) issue(z + q, uint32_t(q));
   arrive(0);
-  bool f2 = true, f1 = true, f0 = __syncthreads_and(own_inf(0));
+  __syncthreads();
+  // warp-uniform all-absent steps: g1 / g2 = every thread's own voxels (x, y0), (x, y0 + 1) of
+  // plane z-1 / z-2 were +inf (then all its cells with base voxel there are absent)
+  bool g2 = true, g1 = true;
   const int wm = max(w - 1, 0), wp = min(w + 1, K2_NW - 1);
   bool nan = false;
   uint32_t P0[2][4], Zm[2][4], CC[2][2], CZm[2][2];
@@ -445,16 +433,24 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   uint32_t rs = 0;
   for (; z <= z1 + 1; ++z) {
     issue(z + KF_PF, (rs + KF_PF) & (KF_RING - 1));
-    const bool fast = f2 && f1 && f0;
+    const uint32_t* v = vown + rs * SLOTW;
+    const bool sr = !TMA || (rmask >> rs & 1);
+    uint32_t u0[2] = {v[0], v[VC]};  // own voxels (x, y0 + r) of plane z
+    if (TMA && !(sr && mall)) {
+      u0[0] = sr && m4[0][0] ? u0[0] : INF_BITS;
+      u0[1] = sr && m4[1][0] ? u0[1] : INF_BITS;
+    }
+    const bool g0 = __all_sync(0xFFFFFFFFu, u0[0] == INF_BITS && u0[1] == INF_BITS);
+    // a fast step: B(z-2), B(z-1) and plane z's cells of the whole warp are absent, so its births
+    // are ABSENT, codes 0x40, tags 0 -- no arithmetic, only the stores and the y-exchange
+    const bool fast = g2 && g1 && g0;
     uint32_t Pn[2][4], Bk[2][8];
     const int buf = z & 1;
     if (!fast) {
-      const uint32_t* v = vown + rs * SLOTW;
-      const bool sr = !TMA || (rmask >> rs & 1);
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const uint32_t* vr = v + r * VC;
-        uint32_t u[4] = {vr[0], vr[1], vr[VC], vr[VC + 1]};
+        uint32_t u[4] = {u0[r], vr[1], vr[VC], vr[VC + 1]};
         if (TMA && !(sr && mall)) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) u[q] = sr && m4[r][q] ? u[q] : INF_BITS;
@@ -473,10 +469,6 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
           Bk[r][q + 4] = max(P0[r][q], Pn[r][q]);
         }
       }
-      S.b0[buf][w][lane] = make_uint4(Bk[0][0], Bk[0][1], Bk[0][4], Bk[0][5]);
-      S.b1[buf][w][lane] = make_uint4(Bk[1][2], Bk[1][3], Bk[1][6], Bk[1][7]);
-      S.c0[buf][w][lane] = CC[0][0];
-      S.c1[buf][w][lane] = CC[1][1];
     } else {
 #pragma unroll
       for (int r = 0; r < 2; ++r)
@@ -486,9 +478,14 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
           Bk[r][q] = Bk[r][q + 4] = ABSENT_ORD;
         }
     }
+    // the y-exchange, also from fast warps (their neighbours may not be fast)
+    S.b0[buf][w][lane] = make_uint4(Bk[0][0], Bk[0][1], Bk[0][4], Bk[0][5]);
+    S.b1[buf][w][lane] = make_uint4(Bk[1][2], Bk[1][3], Bk[1][6], Bk[1][7]);
+    S.c0[buf][w][lane] = CC[0][0];
+    S.c1[buf][w][lane] = CC[1][1];
     const uint32_t rn = (rs + 1) & (KF_RING - 1);
     arrive(rn);
-    const bool fn = __syncthreads_and(own_inf(rn));
+    __syncthreads();
     uint32_t NC[2][2], T[2][2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) NC[r][0] = NC[r][1] = 0x40404040u, T[r][0] = T[r][1] = 0u;
@@ -609,9 +606,8 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
       CC[r][0] = NC[r][0];
       CC[r][1] = NC[r][1];
     }
-    f2 = f1;
-    f1 = f0;
-    f0 = fn;
+    g2 = g1;
+    g1 = g0;
     rs = rn;
   }
   if constexpr (!TMA) kf_wait<0>();
