@@ -1457,9 +1457,11 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
           ok = ok && c[a] + 1 < n[a];
           k += ks[a];
         }
-      if (ok) {
+      // the tag first (1 B; ~1 % of the cells are residual), the birth only for residual or
+      // absent ones (an absent cell's tag is 0 too)
+      if (ok && tag_kind(tags[k]) == KIND_RESIDUAL) {
         const uint32_t b = births[k];
-        if (b != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+        if (b != ABSENT_ORD) {
           emit[q] = true;
           key[q] = make_key(b, k);
         }
