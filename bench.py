@@ -198,9 +198,12 @@ def ncu_summary(kernel, config):
     for p in sorted(paths, key=key, reverse=True):
         try:
             with open(p) as f:
-                d = json.load(f)["kernels"][kernel]
-            return dict(d, source=os.path.relpath(p, ROOT))
-        except (KeyError, OSError, ValueError):
+                ks = json.load(f)["kernels"]
+            # template instances are summarised as name<args> (k_filtration<0>: the product's
+            # cp.async ring)
+            name = kernel if kernel in ks else next(k for k in ks if k.split("<")[0] == kernel)
+            return dict(ks[name], source=os.path.relpath(p, ROOT), kernel_instance=name)
+        except (KeyError, OSError, ValueError, StopIteration):
             continue
     return {}
 
@@ -487,6 +490,18 @@ def run_ours(args, rank, world, local_rank):
                 "alg_bytes_per_launch": alg, "avg_ms": round(stage_avg[roof_stage], 5),
                 "share_of_step": round(stage_avg[roof_stage] / ms_per_step, 4),
                 "peak_source": peak_src, "traffic_source": ncu.get("source")}
+        if ncu.get("warp_instructions"):
+            # what bounds the kernel as built: instruction issue (4 schedulers x SMs x clock),
+            # its warp instructions from the same ncu capture, timed live like `achieved`
+            sms = torch.cuda.get_device_properties(0).multi_processor_count
+            mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+            ipeak = 4 * sms * mhz * 1e6 / 1e9
+            iach = ncu["warp_instructions"] / (stage_avg[roof_stage] / 1e3) / 1e9
+            roof["issue"] = {"warp_instructions": ncu["warp_instructions"],
+                             "achieved": round(iach, 1), "peak": round(ipeak, 1),
+                             "unit": "G warp-instructions/s", "frac": round(iach / ipeak, 4),
+                             "alu_pipe_pct_ncu": ncu.get("alu_pipe_pct"),
+                             "note": "ALU-issue bound as built (DESIGN.md §6 K1+K2 fused)"}
     # the dominant stage (the dims >= 1 reduction for 3D): latency-bound, reported as throughput
     dominant = None
     if dom:

@@ -635,7 +635,8 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
 // K4: H0 by union-find with the elder rule.
 //  (1) every apparent vertex v (UP, paired with its earliest edge e_v) hangs under the other
 //      endpoint of e_v, which is older; roots are the non-apparent vertices ("basins").
-//  (2) pointer jumping flattens the forest.
+//  (2) the forest is not flattened: the endpoints of residual edges find their roots on demand
+//      (path halving), ~1 % of the edges.
 //  (3) a residual edge whose endpoints share a root is positive (a cycle); the others are
 //      inter-basin candidates.
 //  (4) mutual-minimum rounds: every component takes its minimum candidate edge; an edge that is
@@ -720,19 +721,6 @@ __global__ void k_h0_roots(const uint32_t* __restrict__ basins,
 }
 
 
-__global__ void k_pointer_jump(uint32_t* parent, int64_t vbase, int64_t n) {
-  int64_t vv = vbase + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (vv >= n) return;
-  uint32_t v = uint32_t(vv);
-  uint32_t p = parent[v];
-  while (true) {
-    uint32_t pp = *(volatile uint32_t*)(parent + p);
-    if (pp == p) break;
-    p = pp;
-    parent[v] = p;
-  }
-}
-
 // Root of x in a forest whose links only ever point to ancestors, with path halving (plain
 // stores: a racing writer also stores an ancestor).  Used instead of flattening the whole forest:
 // only the endpoints of the few residual edges need roots (C5b: ~2 M of 172 M edges).
@@ -748,15 +736,12 @@ __device__ __forceinline__ uint32_t find_halve(uint32_t* parent, uint32_t x) {
   return x;
 }
 
-struct Cand {
-  uint64_t key;  // edge key
-  uint32_t a, b; // current component roots (voxel ids)
-};
+using Cand = H0Cand;  // key: the edge's (dual: complemented face's) key; a, b: endpoints / roots
 
 
 
-// Inter-basin candidate edges: residual edges whose endpoints have different roots (after
-// pointer jumping).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
+// Inter-basin candidate edges: residual edges whose endpoints have different roots (finds with
+// path halving).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
 __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                            Geom g, uint32_t* parent, Cand* __restrict__ cand,
                            unsigned int* __restrict__ ncand, uint32_t vbase, uint32_t vend) {
@@ -772,7 +757,6 @@ __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* _
   const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
   const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
   const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
-  uint32_t ra = NONE32;  // v's root
   bool emit[3];
   Cand cd[3];
 #pragma unroll
@@ -782,14 +766,12 @@ __global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* _
       const uint32_t k = kb + ks[a];
       const uint32_t bo = births[k];
       if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-        if (ra == NONE32) ra = parent[v];  // flattened: roots
-        const uint32_t rb = parent[v + vs[a]];
-        if (ra != rb) {
-          emit[a] = true;
-          cd[a].key = make_key(bo, k);
-          cd[a].a = ra;
-          cd[a].b = rb;
-        }
+        // every residual edge, with its endpoints: k_mm_rounds finds their roots (a pass that
+        // streams the grid is not held up by the few long finds)
+        emit[a] = true;
+        cd[a].key = make_key(bo, k);
+        cd[a].a = v;
+        cd[a].b = v + vs[a];
       }
     }
   }
@@ -990,6 +972,9 @@ __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t*
       if (ok) {
         const uint32_t bo = births[k];
         if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
+          // the roots of the face's two sides found here (the dual forest is shallow; leaving
+          // the finds -- and the same-root faces -- to k_mm_rounds as H0 does measured slower:
+          // C5b top dimension 3.16 -> 3.9 ms)
           const uint32_t ra = c[a] > 0 ? find_halve(parent, v - vs[a]) : G.omega;
           if (rv == NONE32 && c[a] + 1 < n[a]) rv = find_halve(parent, v);
           const uint32_t rb = c[a] + 1 < n[a] ? rv : G.omega;
@@ -1052,12 +1037,22 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
   // Initialise the two minima buffers at the roots the candidates touch, and the alive flags,
   // instead of memsetting 2 x nbest words (2.2 GB on C5b): every root a later find returns is
   // an endpoint root of some candidate (links only join two candidates' endpoint roots).
+  // The candidates arrive with their endpoints (H0: voxels; the dual's k_dual_edges already
+  // passes roots): their roots in the apparent forest are found here (path halving), the
+  // same-root ones dropped (H0: the edge closes a cycle of older edges).
   for (unsigned i = gt; i < n; i += gs) {
     const Cand c = cur[i];
-    A.best[c.a] = NONE64;
-    A.best[c.b] = NONE64;
-    A.best[A.nbest + c.a] = NONE64;
-    A.best[A.nbest + c.b] = NONE64;
+    const uint32_t a = find_halve(A.parent, c.a), b = find_halve(A.parent, c.b);
+    if (a == b) {
+      A.alive[i] = 0;
+      continue;
+    }
+    cur[i].a = a;
+    cur[i].b = b;
+    A.best[a] = NONE64;
+    A.best[b] = NONE64;
+    A.best[A.nbest + a] = NONE64;
+    A.best[A.nbest + b] = NONE64;
     A.alive[i] = 1;
   }
   grid.sync();
@@ -1433,8 +1428,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       k_h0_parent<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
           S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1), basins);
       CR_CHECK_LAUNCH();
-      k_pointer_jump<<<grid_for(v1 - v0, 256), 256, 0, s>>>(parent, v0, v1);
-      CR_CHECK_LAUNCH();
       k_h0_edges<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
           S.births, S.tags, g, parent, cand, ncand, uint32_t(v0), uint32_t(v1));
       CR_CHECK_LAUNCH();
@@ -1490,15 +1483,13 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   }
 
   // ---- H0
-  // basin forest, flattened (H0 chains are long: flattening once beats finds per edge end,
-  // measured; the dual forest is shallow and takes on-demand finds in k_dual_edges instead).
+  // basin forest, not flattened: k_h0_edges finds the roots of residual edges' endpoints on
+  // demand (a pointer-jumping pass over every voxel took longer: C5b h0 4.23 -> 4.13 ms without it).
   // Pieces of a batch arriving from the host were done in the filtration loop above.
   if (!cand) cand = ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1);
   if (!h0_forest_done) {
     k_h0_parent<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
         S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox), basins);
-    CR_CHECK_LAUNCH();
-    k_pointer_jump<<<grid_for(g.nvox, 256), 256, 0, s>>>(parent, 0, g.nvox);
     CR_CHECK_LAUNCH();
     k_h0_edges<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
         S.births, S.tags, g, parent, cand, ncand, 0u, uint32_t(g.nvox));
@@ -1531,13 +1522,24 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   st.essential[0] = int64_t(hs.p[22]);
   st.rounds[0] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 20)[2]);
   prof_mark(s, "h0");
-  ws.release(cand);
+  // the candidates (all residual edges) stay for the dim-1 columns if K5 reduces dimension 1
+  const bool keep_cand = dmax >= 1 && !use_dual(g, 1);
+  if (keep_cand) {
+    S.h0_cand = cand;
+    S.h0_ncand = reinterpret_cast<const unsigned*>(hs.p + 12)[0];
+  } else {
+    ws.release(cand);
+  }
   ws.release(best);
   ws.release(alive);
   ws.release(parent);
   ws.release(basins);
 
   reduce_dims(S, g, dmax, ws, hs, st);
+  if (S.h0_cand) {  // (not consumed: an error path)
+    ws.release(const_cast<Cand*>(S.h0_cand));
+    S.h0_cand = nullptr;
+  }
 }
 
 int64_t emit_bars(const GeneralState& S, int maxdim, cr_pair* out, uint32_t* out_cells,

@@ -12,6 +12,11 @@ struct Records {
   int64_t n[4] = {0, 0, 0, 0};
 };
 
+struct H0Cand {   // an H0 candidate edge (general.cu): its key and two current component roots
+  uint64_t key;
+  uint32_t a, b;
+};
+
 struct GeneralState {
   Geom g;
   uint32_t* births = nullptr;  // ord(birth) per kidx, ABSENT_ORD for +inf
@@ -26,6 +31,11 @@ struct GeneralState {
   // a stacked batch read unstacked by the filtration (see KfP::zper): planes per image period
   // (images + separator) and per image; 0 = the image is laid out as the geometry says
   uint32_t img_zper = 0, img_zimg = 0;
+  // H0's candidate list, kept for the dim-1 columns: every residual edge is an H0 candidate
+  // (k_h0_edges), and the residual edges that H0 did not clear are exactly the dim-1 columns, so
+  // reduce_dimension(1) compacts this list instead of scanning the grid (nullptr: scan)
+  const H0Cand* h0_cand = nullptr;
+  uint32_t h0_ncand = 0;
   int nready = 0;
   int64_t ready_z[16];
   cudaEvent_t ready_ev[16];

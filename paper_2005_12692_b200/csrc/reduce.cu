@@ -1472,6 +1472,21 @@ __global__ void k_collect_columns(const uint32_t* __restrict__ births,
   warp_append(emit, key, cols, ncols);
 }
 
+// Dim-1 columns from H0's candidates: the edges whose tag is still residual (not cleared by an
+// H0 merge).  One thread per candidate, one append atomic per warp.
+__global__ void k_cols_from_cands(const H0Cand* __restrict__ cand, uint32_t n,
+                                  const uint8_t* __restrict__ tags, uint64_t* __restrict__ cols,
+                                  unsigned* __restrict__ ncols) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool emit[1] = {false};
+  uint64_t key[1] = {0};
+  if (i < n) {
+    key[0] = cand[i].key;
+    emit[0] = tag_kind(tags[key_kidx(key[0])]) == KIND_RESIDUAL;
+  }
+  warp_append(emit, key, cols, ncols);
+}
+
 __global__ void k_seg_keys(const uint64_t* __restrict__ cols, unsigned n, uint32_t seg_cells,
                            uint32_t* __restrict__ segk) {
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1602,9 +1617,19 @@ void reduce_dimension(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr
   unsigned long long* ctr = ws.alloc<unsigned long long>(16);
   CR_CUDA(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
   uint64_t* cols = ws.alloc<uint64_t>(nd + 1);
-  k_collect_columns<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, d, cols,
-                                                        reinterpret_cast<unsigned*>(ctr));
-  CR_CHECK_LAUNCH();
+  if (d == 1 && S.h0_cand) {
+    // the residual edges H0 did not clear, from H0's candidate list (every residual edge)
+    if (S.h0_ncand)
+      k_cols_from_cands<<<grid_for(S.h0_ncand, 256), 256, 0, s>>>(
+          S.h0_cand, S.h0_ncand, S.tags, cols, reinterpret_cast<unsigned*>(ctr));
+    CR_CHECK_LAUNCH();
+    ws.release(const_cast<H0Cand*>(S.h0_cand));
+    S.h0_cand = nullptr;
+  } else {
+    k_collect_columns<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, g, d, cols,
+                                                          reinterpret_cast<unsigned*>(ctr));
+    CR_CHECK_LAUNCH();
+  }
   const unsigned ncols = read_scalar(reinterpret_cast<unsigned*>(ctr), s, hs);
   st.columns[d] = ncols;
   if (ncols > 0) {
