@@ -230,8 +230,10 @@ typedef enum {
   CR_OPT_K5_BLOCKS_PER_SM = 4, /* resident blocks per SM of the reduction (0: occupancy limit)  */
   CR_OPT_K5_JITTER_NS = 5,     /* pseudo-random delays up to this many ns inside the reduction   */
   CR_OPT_DEBUG = 6,            /* per-stage counters printed to stderr                          */
-  CR_OPT_KF_TMA = 7            /* filtration voxel ring by TMA (cp.async.bulk.tensor) when the row
+  CR_OPT_KF_TMA = 7,           /* filtration voxel ring by TMA (cp.async.bulk.tensor) when the row
                                   pitch allows it, not per-thread cp.async (measured slower)      */
+  CR_OPT_KF_RCAP = 8           /* residual edges a filtration CTA stages in shared memory before
+                                  appending to the global list directly (0: 1024; tests)         */
 } cr_option;
 cr_status cr_set_option(int option, int64_t value);
 

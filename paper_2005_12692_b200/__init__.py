@@ -98,7 +98,7 @@ EXPORTED = ["cr_barcodes", "cr_barcodes_host", "cr_barcodes_batched", "cr_pairin
 
 # cr_option (include/cr.h): validation / measurement switches, 0 = the product path
 OPTIONS = {"force_general": 1, "1d_tree": 2, "top_reduce": 3, "k5_blocks_per_sm": 4,
-           "k5_jitter_ns": 5, "debug": 6, "kf_tma": 7}
+           "k5_jitter_ns": 5, "debug": 6, "kf_tma": 7, "kf_rcap": 8}
 
 
 class CrError(RuntimeError):

@@ -82,7 +82,8 @@ enum OptKey {
   OPT_K5_JITTER_NS = 5,      // pseudo-random K5 delays: perturb the schedule (tests)
   OPT_DEBUG = 6,             // per-stage counters on stderr
   OPT_KF_TMA = 7,            // filtration ring by TMA instead of per-thread cp.async
-  OPT_COUNT = 8
+  OPT_KF_RCAP = 8,           // residual edges staged per filtration CTA (tests: the overflow path)
+  OPT_COUNT = 9
 };
 int64_t opt(int key);
 

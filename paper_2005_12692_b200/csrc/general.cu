@@ -155,6 +155,7 @@ template <int N>
 __device__ __forceinline__ void kf_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 constexpr int KF_PF = 3, KF_RING = KF_PF + 1;  // voxel planes in flight, ring slots
+constexpr uint32_t KF_RCAP = 1024;  // residual edges a CTA stages in shared memory
 
 // TMA ring (nx % 4 == 0: the tensor map's row pitch must be a multiple of 16 B): one elected
 // thread loads a CTA's (KF_TCOLS x K2_VROWS) voxel box of a plane with cp.async.bulk.tensor
@@ -187,6 +188,11 @@ struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsk
   // batches read unstacked: stacked plane zz is plane (zz % zper) of image zz / zper, and the
   // separator (+inf) when zz % zper == zimg (zper = zimg + 1); zper == 0: planes as they are
   uint32_t zper, zimg;
+  // residual present edges (dimension 1) found by the tags pass: their kidx are appended to res1
+  // (count *nres1) -- the H0 candidates and, uncleared, the dim-1 columns; nullptr: none kept
+  uint32_t* res1;
+  unsigned* nres1;
+  uint32_t rcap;  // residual edges staged per CTA (<= KF_RCAP; smaller only to test the overflow)
 };
 inline KfP kf_params(const Geom& g, int zc) {
   KfP p;
@@ -201,6 +207,9 @@ inline KfP kf_params(const Geom& g, int zc) {
   p.zc = uint32_t(zc);
   p.zb0 = 0;
   p.zper = p.zimg = 0;
+  p.res1 = nullptr;
+  p.nres1 = nullptr;
+  p.rcap = KF_RCAP;
   return p;
 }
 
@@ -233,6 +242,9 @@ struct alignas(128) Kf2Smem {
   uint32_t c0[2][K2_NW][32];  // row 0's j=0 code word
   uint32_t c1[2][K2_NW][32];  // row 1's j=1 code word
   uint32_t cnt[8];
+  uint32_t rcnt;              // residual edges listed by the CTA (rbuf holds the first KF_RCAP)
+  uint32_t rbase;             // their offset in the global list
+  uint32_t rbuf[KF_RCAP];
 };
 inline KfP kf2_params(const Geom& g, int zc) {
   KfP p = kf_params(g, zc);
@@ -267,7 +279,7 @@ bool kf_tensor_map(CUtensorMap* map, const float* image, int64_t nx, int64_t ny,
 
 template <bool TMA>
 #ifndef K2_MINB
-#define K2_MINB 2
+#define K2_MINB 4  // 4 CTAs of 4 warps per SM: <= 128 registers
 #endif
 __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float* __restrict__ img,
                                                                const KfP P,
@@ -300,6 +312,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   }
   const bool vy2 = y0 + 2 < ny;  // the extra ring row (last warp)
   if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) S.rcnt = 0;
   constexpr uint32_t INF_BITS = 0x7F800000u;
   // Voxel ring: rows y0(w=0) .. y0(w=0) + 2 NW (the last copied by the last warp), cols x0-1 ..
   // x0+31 (col 32 copied by lane 31).  cp.async ring: a thread copies (x, y0 + r), lane 31 also
@@ -594,6 +607,27 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
         }
       }
     }
+    // residual present edges of B(z-2): a byte of q is 0 iff its cell is present (code bit 6
+    // clear) and residual (tag kind 0); cells past the grid are absent in the codes
+    // (rare: ~1 % of the edges; staged per CTA in shared memory, flushed at the end, the
+    // overflow past KF_RCAP appended to the global list directly)
+    if (!fast && P.res1 && z - 2 >= z0 && z - 2 < z1) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (!out[r]) continue;
+        const uint32_t q0 = (T[r][0] & 0xC0C0C0C0u) | (CC[r][0] & 0x40404040u);
+        const uint32_t q1 = (T[r][1] & 0xC0C0C0C0u) | (CC[r][1] & 0x40404040u);
+        const uint32_t kv = uint32_t(z - 2) * 2u * P.KXY + rowbase[r];
+        auto put = [&](uint32_t k) {
+          const uint32_t i = atomicAdd(&S.rcnt, 1u);
+          if (i < P.rcap) S.rbuf[i] = k;
+          else P.res1[atomicAdd(P.nres1, 1u)] = k;
+        };
+        if (!(q0 & 0x0000FF00u)) put(kv + 1);       // x-edge (1,0,0)
+        if (!(q0 & 0x00FF0000u)) put(kv + P.KXY);   // z-edge (0,0,1)
+        if (!(q1 & 0x000000FFu)) put(kv + P.KX);    // y-edge (0,1,0)
+      }
+    }
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
 #pragma unroll
@@ -627,6 +661,15 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   const bool anynan = __any_sync(0xFFFFFFFFu, nan);
   if (lane == 0 && anynan) atomicOr(nan_flag, 1);
   __syncthreads();
+  if (P.res1) {  // the CTA's staged residual edges: one global atomic
+    const uint32_t nr = min(S.rcnt, P.rcap);
+    if (nr) {
+      if (threadIdx.x == 0) S.rbase = atomicAdd(P.nres1, nr);
+      __syncthreads();
+      const uint32_t rb = S.rbase;
+      for (uint32_t i = threadIdx.x; i < nr; i += K2_THREADS) P.res1[rb + i] = S.rbuf[i];
+    }
+  }
   if (threadIdx.x < 7 && S.cnt[threadIdx.x])
     atomicAdd(cnt + (threadIdx.x < 3 ? threadIdx.x : threadIdx.x + 1),
               (unsigned long long)S.cnt[threadIdx.x]);
@@ -740,42 +783,20 @@ using Cand = H0Cand;  // key: the edge's (dual: complemented face's) key; a, b: 
 
 
 
-// Inter-basin candidate edges: residual edges whose endpoints have different roots (finds with
-// path halving).  One thread per voxel v enumerates the (up to 3) edges whose lower vertex v is.
-__global__ void k_h0_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                           Geom g, uint32_t* parent, Cand* __restrict__ cand,
-                           unsigned int* __restrict__ ncand, uint32_t vbase, uint32_t vend) {
-  // voxels [vbase, vend) (a piece of the image: see run_general)
-  const uint64_t vv = uint64_t(vbase) + uint64_t(blockIdx.x) * VOX_THREADS + threadIdx.x;
-  const uint32_t v = uint32_t(vv);
-  const bool in0 = vv < vend;
-  const uint32_t nxx = uint32_t(g.nx), nyy = uint32_t(g.ny);
-  const uint32_t rr = v / nxx, x = v - rr * nxx, z = rr / nyy, y = rr - z * nyy;
-  const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
-  // every edge with base voxel v contains v: an absent v skips them all
-  const bool in = in0 && births[kb] != ABSENT_ORD;
-  const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
-  const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
-  const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
-  bool emit[3];
-  Cand cd[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    emit[a] = false;
-    if (in && c[a] + 1 < n[a]) {
-      const uint32_t k = kb + ks[a];
-      const uint32_t bo = births[k];
-      if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-        // every residual edge, with its endpoints: k_mm_rounds finds their roots (a pass that
-        // streams the grid is not held up by the few long finds)
-        emit[a] = true;
-        cd[a].key = make_key(bo, k);
-        cd[a].a = v;
-        cd[a].b = v + vs[a];
-      }
-    }
+// H0 candidates from the filtration's list of residual present edges: key and endpoints (the
+// lower voxel and its neighbour along the edge's odd axis); k_mm_rounds finds the roots.
+__global__ void k_h0_cands(const uint32_t* __restrict__ list, const unsigned* __restrict__ n,
+                           const uint32_t* __restrict__ births, Geom g, Cand* __restrict__ cand) {
+  const unsigned N = *n;
+  const uint32_t KX = uint32_t(g.KX), KXY = uint32_t(g.KX * g.KY);
+  const uint32_t nx = uint32_t(g.nx), nxy = uint32_t(g.nx * g.ny);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const uint32_t k = list[i];
+    const uint32_t Z = k / KXY, rm = k - Z * KXY, Y = rm / KX, X = rm - Y * KX;
+    const uint32_t v = (Z >> 1) * nxy + (Y >> 1) * nx + (X >> 1);
+    const uint32_t vs = (X & 1) ? 1u : ((Y & 1) ? nx : nxy);
+    cand[i] = Cand{make_key(births[k], k), v, v + vs};
   }
-  warp_append(emit, cd, cand, ncand);
 }
 
 __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
@@ -1381,6 +1402,8 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   }
   Cand* cand = S.nready ? ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1) : nullptr;
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
+  // residual present edges, listed by the filtration (kidx; at most every edge of the grid)
+  uint32_t* res1 = ws.alloc<uint32_t>(nedges_max > 0 ? nedges_max : 1);
 
   // K1 + K2 in one streaming kernel (round 1 measured the split alternatives, profiles/r01/s3:
   // C5 0.52 + 3.60 ms as separate births + apparent-pair kernels)
@@ -1399,6 +1422,9 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     KfP kp = kf2_params(g, L.zc);
     kp.zper = S.img_zper;
     kp.zimg = S.img_zimg;
+    kp.res1 = res1;
+    kp.nres1 = ncand;
+    if (opt(OPT_KF_RCAP) > 0 && opt(OPT_KF_RCAP) < KF_RCAP) kp.rcap = uint32_t(opt(OPT_KF_RCAP));
     // the source planes the filtration reads (a batch read unstacked has no separator planes)
     const int64_t nzsrc = kp.zper ? (g.nz + 1) / kp.zper * kp.zimg : g.nz;
     CUtensorMap tmap;
@@ -1427,9 +1453,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
       const int64_t v0 = forest_z * plane, v1 = zt * plane;
       k_h0_parent<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
           S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1), basins);
-      CR_CHECK_LAUNCH();
-      k_h0_edges<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
-          S.births, S.tags, g, parent, cand, ncand, uint32_t(v0), uint32_t(v1));
       CR_CHECK_LAUNCH();
       forest_z = zt;
     };
@@ -1483,18 +1506,20 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   }
 
   // ---- H0
-  // basin forest, not flattened: k_h0_edges finds the roots of residual edges' endpoints on
-  // demand (a pointer-jumping pass over every voxel took longer: C5b h0 4.23 -> 4.13 ms without it).
+  // basin forest, not flattened: k_mm_rounds finds the roots of the residual edges' endpoints
+  // (a pointer-jumping pass over every voxel took longer: C5b h0 4.23 -> 4.13 ms without it);
+  // the residual edges come listed from the filtration (no per-voxel edge scan: 3.3 -> ? ms).
   // Pieces of a batch arriving from the host were done in the filtration loop above.
   if (!cand) cand = ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1);
   if (!h0_forest_done) {
     k_h0_parent<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
         S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox), basins);
     CR_CHECK_LAUNCH();
-    k_h0_edges<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
-        S.births, S.tags, g, parent, cand, ncand, 0u, uint32_t(g.nvox));
-    CR_CHECK_LAUNCH();
   }
+  // H0 candidates: every residual present edge (the filtration's list) with its endpoints
+  k_h0_cands<<<148 * 8, 256, 0, s>>>(res1, ncand, S.births, g, cand);
+  CR_CHECK_LAUNCH();
+  ws.release(res1);
   const int64_t nedges = nedges_max;
 
   // vertex records: at most one per vertex

@@ -185,6 +185,34 @@ def test_filtration_tma_ring(cr):
         assert ei.value.status == cr.CR_EINVAL
 
 
+def test_residual_edge_list_overflow(cr):
+    """The filtration lists the residual edges (H0's candidates and, uncleared, the dim-1
+    columns), staged per CTA in shared memory; past the stage's capacity (option kf_rcap = 1, 3)
+    entries go straight to the global list.  Same pairing and bars as the oracle either way, on
+    tie-heavy and iid images (many residual edges per CTA), a masked GRF and a 3D batch."""
+    import torch
+    imgs = [gen.small_int_image((14, 33, 40), 3, seed=80, inf_frac=0.05),
+            gen.iid_uniform((9, 20, 64), 81),
+            gen.masked_grf((21, 22, 23), 1.5, 9.0, 82),
+            gen.iid_uniform((70, 90), 83)]
+    for k, img in enumerate(imgs):
+        o = oracle.ph(img, img.ndim - 1, partner=True)
+        t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+        for cap in (0, 1, 3):
+            with cr.options(kf_rcap=cap):
+                p = cr.pairing(t).cpu().numpy().view(np.uint32)
+                assert np.array_equal(p, o.partner), (k, cap, np.flatnonzero(p != o.partner)[:10])
+                assert_bars_equal(gpu_bars(cr, img, img.ndim - 1), o, ctx=(k, cap))
+    vs = np.stack([gen.iid_uniform((6, 7, 8), 90 + s) for s in range(9)])
+    with cr.options(kf_rcap=2):
+        bc, off = cr.barcodes_batched(torch.from_numpy(vs).cuda(), 2, cells=True)
+    d, b, e, c = bc.numpy()
+    off = off.cpu().numpy()
+    for i in range(len(vs)):
+        s = slice(off[i], off[i + 1])
+        assert_bars_equal((d[s], b[s], e[s], c[s]), oracle.ph(vs[i], 2), ctx=("batch", i))
+
+
 def _cavity_cases():
     rng = np.random.default_rng(50)
     a = rng.random((20, 22)).astype(np.float32)
