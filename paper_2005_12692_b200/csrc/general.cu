@@ -144,7 +144,9 @@ __device__ __forceinline__ uint32_t kf_tags_word(uint32_t own, uint32_t xm, uint
 
 __device__ __forceinline__ uint32_t kf_ord(float f) {
   const uint32_t u = __float_as_uint(f + 0.0f);  // -0 + 0 = +0 (reading R7); NaN stays NaN
-  return u ^ (uint32_t(int32_t(u) >> 31) | 0x80000000u);
+  // a (positive) NaN would order above +inf and make the cells past the grid present: it is
+  // clamped to +inf's key (the call fails with CR_EINVAL anyway; this keeps it memory-safe)
+  return min(u ^ (uint32_t(int32_t(u) >> 31) | 0x80000000u), ABSENT_ORD);
 }
 
 __device__ __forceinline__ void kf_cp4(uint32_t saddr, const float* g) {
@@ -193,6 +195,9 @@ struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsk
   uint32_t* res1;
   unsigned* nres1;
   uint32_t rcap;  // residual edges staged per CTA (<= KF_RCAP; smaller only to test the overflow)
+  // residual present squares (dimension 2; 3D: the faces of the top-dimension dual), likewise
+  uint32_t* res2;
+  unsigned* nres2;
 };
 inline KfP kf_params(const Geom& g, int zc) {
   KfP p;
@@ -210,6 +215,8 @@ inline KfP kf_params(const Geom& g, int zc) {
   p.res1 = nullptr;
   p.nres1 = nullptr;
   p.rcap = KF_RCAP;
+  p.res2 = nullptr;
+  p.nres2 = nullptr;
   return p;
 }
 
@@ -242,9 +249,10 @@ struct alignas(128) Kf2Smem {
   uint32_t c0[2][K2_NW][32];  // row 0's j=0 code word
   uint32_t c1[2][K2_NW][32];  // row 1's j=1 code word
   uint32_t cnt[8];
-  uint32_t rcnt;              // residual edges listed by the CTA (rbuf holds the first KF_RCAP)
-  uint32_t rbase;             // their offset in the global list
+  uint32_t rcnt, rcnt2;       // residual edges / squares listed by the CTA (rbuf* hold the first
+  uint32_t rbase, rbase2;     // rcap), their offsets in the global lists
   uint32_t rbuf[KF_RCAP];
+  uint32_t rbuf2[KF_RCAP];
 };
 inline KfP kf2_params(const Geom& g, int zc) {
   KfP p = kf_params(g, zc);
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   }
   const bool vy2 = y0 + 2 < ny;  // the extra ring row (last warp)
   if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) S.rcnt = 0;
+  if (threadIdx.x == 0) S.rcnt = S.rcnt2 = 0;
   constexpr uint32_t INF_BITS = 0x7F800000u;
   // Voxel ring: rows y0(w=0) .. y0(w=0) + 2 NW (the last copied by the last warp), cols x0-1 ..
   // x0+31 (col 32 copied by lane 31).  cp.async ring: a thread copies (x, y0 + r), lane 31 also
@@ -617,15 +625,29 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
         if (!out[r]) continue;
         const uint32_t q0 = (T[r][0] & 0xC0C0C0C0u) | (CC[r][0] & 0x40404040u);
         const uint32_t q1 = (T[r][1] & 0xC0C0C0C0u) | (CC[r][1] & 0x40404040u);
+        // bit 7 of a byte: the byte is 0 (its bytes are 0x00 / 0x40 / 0x80 / 0xC0); word 0:
+        // x-edge (1,0,0) byte 1, z-edge (0,0,1) byte 2, xz-square (1,0,1) byte 3; word 1: y-edge
+        // (0,1,0) byte 0, xy-square (1,1,0) byte 1, yz-square (0,1,1) byte 2
+        const uint32_t z0 = ~(q0 | (q0 << 1)) & (P.res2 ? 0x80808000u : 0x00808000u);
+        const uint32_t z1 = ~(q1 | (q1 << 1)) & (P.res2 ? 0x00808080u : 0x00000080u);
+        if (!(z0 | z1)) continue;  // the common case
         const uint32_t kv = uint32_t(z - 2) * 2u * P.KXY + rowbase[r];
         auto put = [&](uint32_t k) {
           const uint32_t i = atomicAdd(&S.rcnt, 1u);
           if (i < P.rcap) S.rbuf[i] = k;
           else P.res1[atomicAdd(P.nres1, 1u)] = k;
         };
-        if (!(q0 & 0x0000FF00u)) put(kv + 1);       // x-edge (1,0,0)
-        if (!(q0 & 0x00FF0000u)) put(kv + P.KXY);   // z-edge (0,0,1)
-        if (!(q1 & 0x000000FFu)) put(kv + P.KX);    // y-edge (0,1,0)
+        auto put2 = [&](uint32_t k) {
+          const uint32_t i = atomicAdd(&S.rcnt2, 1u);
+          if (i < P.rcap) S.rbuf2[i] = k;
+          else P.res2[atomicAdd(P.nres2, 1u)] = k;
+        };
+        if (z0 & 0x00008000u) put(kv + 1);                // x-edge
+        if (z0 & 0x00800000u) put(kv + P.KXY);            // z-edge
+        if (z1 & 0x00000080u) put(kv + P.KX);             // y-edge
+        if (z0 & 0x80000000u) put2(kv + P.KXY + 1);       // xz-square
+        if (z1 & 0x00008000u) put2(kv + P.KX + 1);        // xy-square
+        if (z1 & 0x00800000u) put2(kv + P.KX + P.KXY);    // yz-square
       }
     }
 #pragma unroll
@@ -661,13 +683,15 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   const bool anynan = __any_sync(0xFFFFFFFFu, nan);
   if (lane == 0 && anynan) atomicOr(nan_flag, 1);
   __syncthreads();
-  if (P.res1) {  // the CTA's staged residual edges: one global atomic
-    const uint32_t nr = min(S.rcnt, P.rcap);
-    if (nr) {
-      if (threadIdx.x == 0) S.rbase = atomicAdd(P.nres1, nr);
+  if (P.res1) {  // the CTA's staged residual edges (and squares): one global atomic per list
+    const uint32_t nr = min(S.rcnt, P.rcap), nr2 = P.res2 ? min(S.rcnt2, P.rcap) : 0u;
+    if (nr | nr2) {
+      if (threadIdx.x == 0 && nr) S.rbase = atomicAdd(P.nres1, nr);
+      if (threadIdx.x == 32 && nr2) S.rbase2 = atomicAdd(P.nres2, nr2);
       __syncthreads();
-      const uint32_t rb = S.rbase;
+      const uint32_t rb = S.rbase, rb2 = S.rbase2;
       for (uint32_t i = threadIdx.x; i < nr; i += K2_THREADS) P.res1[rb + i] = S.rbuf[i];
+      for (uint32_t i = threadIdx.x; i < nr2; i += K2_THREADS) P.res2[rb2 + i] = S.rbuf2[i];
     }
   }
   if (threadIdx.x < 7 && S.cnt[threadIdx.x])
@@ -842,11 +866,33 @@ __device__ __forceinline__ bool top_of_voxel(const Geom& g, uint32_t v, uint32_t
 // absent_to_omega: no +inf cavity is enclosed (Euler count, see top_dual), so every absent top
 // cell lies in the outside vertex's component and hangs under it directly.
 __global__ void k_dual_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                              DualG G, uint32_t* __restrict__ parent, int absent_to_omega) {
+                              DualG G, uint32_t* __restrict__ parent, int absent_to_omega,
+                              unsigned long long* __restrict__ nroots) {
   uint32_t v, x, y, z;
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
     parent[G.omega] = G.omega;
-  if (!vox_of_thread(G.g, v, x, y, z)) return;
+  const bool in = vox_of_thread(G.g, v, x, y, z);
+  if (nroots) {  // top cells that are roots (final when absent ones hang under OMEGA)
+    bool root = false;
+    if (in) {
+      const uint32_t c[3] = {x, y, z};
+      const uint32_t n[3] = {uint32_t(G.g.nx), uint32_t(G.g.ny), uint32_t(G.g.nz)};
+      bool has_top = true;
+      uint32_t K[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        has_top = has_top && (n[a] == 1 || c[a] + 1 < n[a]);
+        K[a] = n[a] > 1 ? 2 * c[a] + 1 : 0;
+      }
+      if (has_top) {
+        const uint32_t k = (K[2] * uint32_t(G.g.KY) + K[1]) * uint32_t(G.g.KX) + K[0];
+        root = births[k] != ABSENT_ORD && tag_kind(tags[k]) != KIND_DOWN;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, root);
+    if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nroots, (unsigned long long)__popc(mask));
+  }
+  if (!in) return;
   // the top cell with base voxel v (odd on every active axis), from v's coordinates (no second
   // decode of v or of the cell's kidx)
   const uint32_t c[3] = {x, y, z};
@@ -945,6 +991,65 @@ __global__ void k_dual_absent_vox(const uint32_t* __restrict__ births, DualG G,
 // have different roots.  One thread per voxel v enumerates the (D-1)-cells with base voxel v (one
 // per active normal axis a: even on a, odd on the other active axes), whose cofaces are the top
 // cells with base voxels v - e_a and v.  The same threads count the dual roots into *nroots.
+// Top cells that are roots after the absent cells' union-find (the cavity case).
+__global__ void k_dual_roots(DualG G, const uint32_t* __restrict__ parent,
+                             unsigned long long* __restrict__ nroots) {
+  uint32_t v, x, y, z;
+  const bool in = vox_of_thread(G.g, v, x, y, z);
+  const uint32_t c[3] = {x, y, z};
+  const uint32_t n[3] = {uint32_t(G.g.nx), uint32_t(G.g.ny), uint32_t(G.g.nz)};
+  bool has_top = in;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) has_top = has_top && (n[a] == 1 || c[a] + 1 < n[a]);
+  const bool root = has_top && parent[v] == v;
+  const unsigned mask = __ballot_sync(0xFFFFFFFFu, root);
+  if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nroots, (unsigned long long)__popc(mask));
+}
+
+// Dual candidates from the filtration's list of residual present (D-1)-cells: faces not cleared
+// by the dimension below, whose two sides (the top cells across the face's normal axis, or OMEGA
+// past the border) have different roots (path halving).  OMEGA is always a root: the absent
+// cells' union-find links smaller indices under larger ones.
+__global__ void k_dual_cands(const uint32_t* __restrict__ list, const unsigned* __restrict__ n_dev,
+                             const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
+                             DualG G, uint32_t* parent, Cand* __restrict__ cand,
+                             unsigned* __restrict__ ncand, unsigned long long* nroots) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(nroots, 1ull);  // OMEGA
+  const unsigned N = *n_dev;
+  const Geom& g = G.g;
+  const uint32_t KX = uint32_t(g.KX), KXY = uint32_t(g.KX * g.KY);
+  const uint32_t n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
+  const uint32_t vs[3] = {1u, n[0], n[0] * n[1]};
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned i0 = blockIdx.x * blockDim.x; i0 < N; i0 += stride) {  // warp-uniform trips
+    const unsigned i = i0 + threadIdx.x;
+    bool emit[1] = {false};
+    Cand cd[1];
+    if (i < N) {
+      const uint32_t k = list[i];
+      if (tag_kind(tags[k]) == KIND_RESIDUAL) {  // not cleared by the dimension below
+        const uint32_t Z = k / KXY, rm = k - Z * KXY, Y = rm / KX, X = rm - Y * KX;
+        const uint32_t C[3] = {X, Y, Z};
+        int a = 0;  // the normal axis: the active axis along which the face is even
+#pragma unroll
+        for (int b = 2; b >= 0; --b)
+          if (n[b] > 1 && !(C[b] & 1)) a = b;
+        const uint32_t v = (Z >> 1) * vs[2] + (Y >> 1) * vs[1] + (X >> 1);
+        const uint32_t ca = C[a] >> 1;
+        const uint32_t ra = ca > 0 ? find_halve(parent, v - vs[a]) : G.omega;
+        const uint32_t rb = ca + 1 < n[a] ? find_halve(parent, v) : G.omega;
+        if (ra != rb) {
+          emit[0] = true;
+          cd[0].key = ~make_key(births[k], k);  // ascending ~key = decreasing key
+          cd[0].a = ra;
+          cd[0].b = rb;
+        }
+      }
+    }
+    warp_append(emit, cd, cand, ncand);
+  }
+}
+
 __global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
                              DualG G, uint32_t* parent, Cand* __restrict__ cand,
                              unsigned int* __restrict__ ncand, unsigned long long* nroots) {
@@ -1213,19 +1318,31 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     const int64_t ess_top = (d & 1) ? low - chi : chi - low;
     no_cavity = ess_top == 0;
   }
+  const bool listed = S.res_faces != nullptr;
   k_dual_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent,
-                                                    no_cavity ? 1 : 0);
+                                                    no_cavity ? 1 : 0,
+                                                    listed && no_cavity ? cnt + 1 : nullptr);
   CR_CHECK_LAUNCH();
   if (!no_cavity) {
     k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
     CR_CHECK_LAUNCH();
+    if (listed) {
+      k_dual_roots<<<vox_grid(g), VOX_THREADS, 0, s>>>(G, parent, cnt + 1);
+      CR_CHECK_LAUNCH();
+    }
   }
   // (no flattening: k_dual_edges finds the roots of the residual faces' sides on demand)
   Cand* cand = ws.alloc<Cand>(st.cells[d] + 1);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt);
-  k_dual_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
-                                                  cnt + 1);
-  CR_CHECK_LAUNCH();
+  if (listed) {  // the residual faces listed by the filtration (no per-voxel face scan)
+    k_dual_cands<<<148 * 8, 256, 0, s>>>(S.res_faces, S.nres_faces, S.births, S.tags, G, parent,
+                                         cand, ncand, cnt + 1);
+    CR_CHECK_LAUNCH();
+  } else {
+    k_dual_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
+                                                    cnt + 1);
+    CR_CHECK_LAUNCH();
+  }
   // candidates <= the finite d-cells (known since H0's read): no host read before the rounds
   const int64_t n = st.cells[d] + 1;
   unsigned long long* nrec = cnt + 2;
@@ -1402,8 +1519,13 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   }
   Cand* cand = S.nready ? ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1) : nullptr;
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt + 12);
-  // residual present edges, listed by the filtration (kidx; at most every edge of the grid)
+  // residual present edges, listed by the filtration (kidx; at most every edge of the grid), and
+  // in 3D the residual present squares (the top-dimension dual's faces; in 2D those are edges)
   uint32_t* res1 = ws.alloc<uint32_t>(nedges_max > 0 ? nedges_max : 1);
+  uint32_t* res2 = nullptr;
+  if (g.D == 3) res2 = ws.alloc<uint32_t>(3 * g.nvox);
+  S.res_faces = g.D == 3 ? res2 : (g.D == 2 ? res1 : nullptr);
+  S.nres_faces = reinterpret_cast<const unsigned*>(g.D == 3 ? cnt + 14 : cnt + 12);
 
   // K1 + K2 in one streaming kernel (round 1 measured the split alternatives, profiles/r01/s3:
   // C5 0.52 + 3.60 ms as separate births + apparent-pair kernels)
@@ -1424,6 +1546,8 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     kp.zimg = S.img_zimg;
     kp.res1 = res1;
     kp.nres1 = ncand;
+    kp.res2 = res2;
+    kp.nres2 = reinterpret_cast<unsigned*>(cnt + 14);
     if (opt(OPT_KF_RCAP) > 0 && opt(OPT_KF_RCAP) < KF_RCAP) kp.rcap = uint32_t(opt(OPT_KF_RCAP));
     // the source planes the filtration reads (a batch read unstacked has no separator planes)
     const int64_t nzsrc = kp.zper ? (g.nz + 1) / kp.zper * kp.zimg : g.nz;
@@ -1508,7 +1632,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // ---- H0
   // basin forest, not flattened: k_mm_rounds finds the roots of the residual edges' endpoints
   // (a pointer-jumping pass over every voxel took longer: C5b h0 4.23 -> 4.13 ms without it);
-  // the residual edges come listed from the filtration (no per-voxel edge scan: 3.3 -> ? ms).
+  // the residual edges come listed from the filtration (no per-voxel edge scan: 3.25 -> 1.91 ms).
   // Pieces of a batch arriving from the host were done in the filtration loop above.
   if (!cand) cand = ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1);
   if (!h0_forest_done) {
@@ -1519,7 +1643,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // H0 candidates: every residual present edge (the filtration's list) with its endpoints
   k_h0_cands<<<148 * 8, 256, 0, s>>>(res1, ncand, S.births, g, cand);
   CR_CHECK_LAUNCH();
-  ws.release(res1);
+  if (S.res_faces != res1) ws.release(res1);  // (2D: the dual's faces)
   const int64_t nedges = nedges_max;
 
   // vertex records: at most one per vertex
@@ -1564,6 +1688,10 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   if (S.h0_cand) {  // (not consumed: an error path)
     ws.release(const_cast<Cand*>(S.h0_cand));
     S.h0_cand = nullptr;
+  }
+  if (S.res_faces) {
+    ws.release(S.res_faces);
+    S.res_faces = nullptr;
   }
 }
 

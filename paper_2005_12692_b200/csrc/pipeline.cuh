@@ -36,6 +36,10 @@ struct GeneralState {
   // reduce_dimension(1) compacts this list instead of scanning the grid (nullptr: scan)
   const H0Cand* h0_cand = nullptr;
   uint32_t h0_ncand = 0;
+  // the residual present (D-1)-cells listed by the filtration (kidx; device count): the faces of
+  // the top-dimension dual (cleared ones are skipped there); nullptr: not listed
+  uint32_t* res_faces = nullptr;
+  const unsigned* nres_faces = nullptr;
   int nready = 0;
   int64_t ready_z[16];
   cudaEvent_t ready_ev[16];
