@@ -198,6 +198,16 @@ struct KfP {  // 32-bit geometry for k_filtration (image < 2^32 voxels, Khalimsk
   // residual present squares (dimension 2; 3D: the faces of the top-dimension dual), likewise
   uint32_t* res2;
   unsigned* nres2;
+  // the forests, from the tags of B(z-2): H0 (h0par[v] = the partner edge's other vertex for an
+  // apparent (UP) vertex v, else v; the non-apparent present vertices, the basins, appended to
+  // basins / *nbasins) and the top-dimension dual (dpar[v] for the top cell with base voxel v:
+  // the top cell across its apparent face, OMEGA = nvox past the border or for an absent top
+  // cell, else v); nullptr: not built here
+  uint32_t* h0par;
+  uint32_t* basins;
+  unsigned long long* nbasins;
+  uint32_t* dpar;
+  uint32_t topw, topb;  // the top cell's tag: word j, byte i + 2k of (i, j, k) = active axes
 };
 inline KfP kf_params(const Geom& g, int zc) {
   KfP p;
@@ -217,6 +227,10 @@ inline KfP kf_params(const Geom& g, int zc) {
   p.rcap = KF_RCAP;
   p.res2 = nullptr;
   p.nres2 = nullptr;
+  p.h0par = p.basins = p.dpar = nullptr;
+  p.nbasins = nullptr;
+  p.topw = g.ny > 1 ? 1u : 0u;
+  p.topb = (g.nx > 1 ? 1u : 0u) + (g.nz > 1 ? 2u : 0u);
   return p;
 }
 
@@ -253,6 +267,8 @@ struct alignas(128) Kf2Smem {
   uint32_t rbase, rbase2;     // rcap), their offsets in the global lists
   uint32_t rbuf[KF_RCAP];
   uint32_t rbuf2[KF_RCAP];
+  uint32_t bcnt, bbase;       // basins listed by the CTA (bbuf holds the first rcap)
+  uint32_t bbuf[KF_RCAP];
 };
 inline KfP kf2_params(const Geom& g, int zc) {
   KfP p = kf_params(g, zc);
@@ -320,7 +336,8 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   }
   const bool vy2 = y0 + 2 < ny;  // the extra ring row (last warp)
   if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) S.rcnt = S.rcnt2 = 0;
+  if (threadIdx.x == 0) S.rcnt = S.rcnt2 = S.bcnt = 0;
+  if (P.dpar && blockIdx.x == 0 && threadIdx.x == 0) P.dpar[P.nx * P.ny * P.nz] = P.nx * P.ny * P.nz;
   constexpr uint32_t INF_BITS = 0x7F800000u;
   // Voxel ring: rows y0(w=0) .. y0(w=0) + 2 NW (the last copied by the last warp), cols x0-1 ..
   // x0+31 (col 32 copied by lane 31).  cp.async ring: a thread copies (x, y0 + r), lane 31 also
@@ -613,6 +630,40 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
           if (hy[r]) p3[0] = uint8_t(T[r][1] >> 16);
           if (hx && hy[r]) p3[1] = uint8_t(T[r][1] >> 24);
         }
+        if (P.h0par) {  // (branch-free but for the rare basin staging)
+          const uint32_t y = uint32_t(y0 + r), zz = uint32_t(zb2);
+          const uint32_t v = zz * P.plane + y * P.nx + uint32_t(x);
+          auto step = [&](uint32_t t) {  // voxel offset of the tag's direction
+            const uint32_t a = (t & 7u) >> 1;
+            return a == 0 ? 1u : (a == 1 ? P.nx : P.plane);
+          };
+          // H0: an apparent vertex hangs under its partner edge's other vertex (absent cells
+          // have tag 0: never UP)
+          const uint32_t vt = T[r][0] & 0xFFu;
+          const bool vup = (vt >> 6) == KIND_UP;
+          const uint32_t sv = step(vt);
+          P.h0par[v] = vup ? ((vt & 1u) ? v + sv : v - sv) : v;
+          if (!vup && !(CC[r][0] & 0x40u)) {  // a present basin (rare)
+            const uint32_t i = atomicAdd(&S.bcnt, 1u);
+            if (i < P.rcap) S.bbuf[i] = v;
+            else P.basins[atomicAdd(P.nbasins, 1ull)] = v;
+          }
+          if (P.dpar) {  // the dual: a top cell hangs under the top cell across its apparent face
+            const uint32_t OMEGA = P.nx * P.ny * P.nz;
+            const bool has_top = (P.nx == 1 || hx) && (P.ny == 1 || hy[r]) && (P.nz == 1 || hz);
+            const uint32_t tw = P.topw ? T[r][1] : T[r][0], cw = P.topw ? CC[r][1] : CC[r][0];
+            const uint32_t tt = (tw >> (8 * P.topb)) & 0xFFu;
+            const bool tabs = (cw >> (8 * P.topb)) & 0x40u;
+            const bool tdown = (tt >> 6) == KIND_DOWN;
+            const uint32_t a = (tt & 7u) >> 1, st = step(tt);
+            const uint32_t ca = a == 0 ? uint32_t(x) : (a == 1 ? y : zz);
+            const uint32_t na = a == 0 ? P.nx : (a == 1 ? P.ny : P.nz);
+            const uint32_t across = (tt & 1u) ? (ca + 2 < na ? v + st : OMEGA)
+                                              : (ca > 0 ? v - st : OMEGA);
+            // absent top cells hang under OMEGA (a cavity call rebuilds the forest)
+            P.dpar[v] = !has_top ? v : (tabs ? OMEGA : (tdown ? across : v));
+          }
+        }
       }
     }
     // residual present edges of B(z-2): a byte of q is 0 iff its cell is present (code bit 6
@@ -683,15 +734,18 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   const bool anynan = __any_sync(0xFFFFFFFFu, nan);
   if (lane == 0 && anynan) atomicOr(nan_flag, 1);
   __syncthreads();
-  if (P.res1) {  // the CTA's staged residual edges (and squares): one global atomic per list
+  if (P.res1) {  // the CTA's staged residual cells and basins: one global atomic per list
     const uint32_t nr = min(S.rcnt, P.rcap), nr2 = P.res2 ? min(S.rcnt2, P.rcap) : 0u;
-    if (nr | nr2) {
+    const uint32_t nb = P.h0par ? min(S.bcnt, P.rcap) : 0u;
+    if (nr | nr2 | nb) {
       if (threadIdx.x == 0 && nr) S.rbase = atomicAdd(P.nres1, nr);
       if (threadIdx.x == 32 && nr2) S.rbase2 = atomicAdd(P.nres2, nr2);
+      if (threadIdx.x == 64 && nb) S.bbase = uint32_t(atomicAdd(P.nbasins, (unsigned long long)nb));
       __syncthreads();
-      const uint32_t rb = S.rbase, rb2 = S.rbase2;
+      const uint32_t rb = S.rbase, rb2 = S.rbase2, bb = S.bbase;
       for (uint32_t i = threadIdx.x; i < nr; i += K2_THREADS) P.res1[rb + i] = S.rbuf[i];
       for (uint32_t i = threadIdx.x; i < nr2; i += K2_THREADS) P.res2[rb2 + i] = S.rbuf2[i];
+      for (uint32_t i = threadIdx.x; i < nb; i += K2_THREADS) P.basins[bb + i] = S.bbuf[i];
     }
   }
   if (threadIdx.x < 7 && S.cnt[threadIdx.x])
@@ -718,43 +772,6 @@ __device__ __forceinline__ uint32_t vox_kidx(const Geom& g, uint32_t v) {
 
 // parent of every voxel in the apparent-pair forest, and the number of basins (present vertices
 // that are not the lower cell of an apparent pair) into *nbasins
-__global__ void k_h0_parent(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                            Geom g, uint32_t* __restrict__ parent, unsigned long long* nbasins,
-                            uint32_t vbase, uint32_t vend, uint32_t* __restrict__ basins) {
-  // voxels [vbase, vend) (a piece of the image: see run_general)
-  const uint64_t vv = uint64_t(vbase) + uint64_t(blockIdx.x) * VOX_THREADS + threadIdx.x;
-  const uint32_t v = uint32_t(vv);
-  const bool in = vv < vend;
-  const uint32_t nx = uint32_t(g.nx), ny = uint32_t(g.ny);
-  const uint32_t r = v / nx, x = v - r * nx, z = r / ny, y = r - z * ny;
-  bool basin = false;
-  if (in) {
-    const uint32_t k = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
-    const bool present = births[k] != ABSENT_ORD;
-    uint32_t p = v;
-    if (present) {
-      const uint8_t t = tags[k];
-      if (tag_kind(t) == KIND_UP) {
-        const int d = tag_dir(t);
-        const int64_t vs = (d >> 1) == 0 ? 1 : ((d >> 1) == 1 ? g.nx : g.nx * g.ny);
-        p = uint32_t(int64_t(v) + ((d & 1) ? vs : -vs));
-      } else {
-        basin = true;
-      }
-    }
-    parent[v] = p;
-  }
-  // the basins are listed (their count is the list's length): the final H0 roots are among them
-  // (k_h0_roots), so the essential classes need not be found by a scan of every voxel
-  const unsigned mask = __ballot_sync(0xFFFFFFFFu, basin);
-  if (!mask) return;
-  const int lane = threadIdx.x & 31;
-  unsigned long long base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(nbasins, (unsigned long long)__popc(mask));
-  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(mask) - 1);
-  if (basin) basins[base + __popc(mask & ((1u << lane) - 1))] = v;
-}
-
 // Essential H0 classes: the listed basins that are still roots after the merge rounds.
 __global__ void k_h0_roots(const uint32_t* __restrict__ basins,
                            const unsigned long long* __restrict__ nbasins,
@@ -1304,7 +1321,9 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   S.R.n[d] = 0;
   unsigned long long* cnt = ws.alloc<unsigned long long>(8);
   CR_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), s));
-  uint32_t* parent = ws.alloc<uint32_t>(nv);
+  // the dual forest: the filtration's (absent top cells under OMEGA), rebuilt below when an
+  // enclosed cavity is possible
+  uint32_t* parent = S.dual_parent ? S.dual_parent : ws.alloc<uint32_t>(nv);
   // Enclosed +inf cavities (absent components that do not reach the outside) give the essential
   // classes of the top dimension d = D-1, and by the Euler-Poincare relation their number is
   //   ess[d] = (-1)^d (chi - sum_{e<d} (-1)^e ess[e]),  chi = sum_e (-1)^e #(finite e-cells),
@@ -1319,10 +1338,15 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     no_cavity = ess_top == 0;
   }
   const bool listed = S.res_faces != nullptr;
-  k_dual_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent,
-                                                    no_cavity ? 1 : 0,
-                                                    listed && no_cavity ? cnt + 1 : nullptr);
-  CR_CHECK_LAUNCH();
+  // with the filtration's forest the roots among the top cells are counted from its counters:
+  // the present top cells that are not the upper cell of an apparent pair (face, top)
+  const bool forest_given = S.dual_parent != nullptr && no_cavity && d == g.D - 1;
+  if (!forest_given) {
+    k_dual_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent,
+                                                      no_cavity ? 1 : 0,
+                                                      listed && no_cavity ? cnt + 1 : nullptr);
+    CR_CHECK_LAUNCH();
+  }
   if (!no_cavity) {
     k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
     CR_CHECK_LAUNCH();
@@ -1354,12 +1378,14 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
   CR_CUDA(cudaMemcpyAsync(hs.p, cnt, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CR_CUDA(cudaStreamSynchronize(s));
   st.columns[d] = int64_t(hs.p[1]);  // dual roots
+  if (forest_given) st.columns[d] += st.cells[d + 1] - st.apparent[d];
   S.R.n[d] = int64_t(hs.p[2]);
   st.rounds[d] = int64_t(reinterpret_cast<const unsigned*>(hs.p + 6)[2]);
   ws.release(best);
   ws.release(alive);
   ws.release(cand);
   ws.release(parent);
+  if (parent == S.dual_parent) S.dual_parent = nullptr;
   return true;
 }
 
@@ -1507,7 +1533,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   int* nan_flag = reinterpret_cast<int*>(cnt + 31);
   uint32_t* parent = ws.alloc<uint32_t>(g.nvox);  // H0 basin forest
   uint32_t* basins = ws.alloc<uint32_t>(g.nvox);  // the forest's roots (non-apparent vertices)
-  bool h0_forest_done = false;
   // H0 candidate edges, room for every edge of the grid (a bound known without reading the
   // finite-cell counts back: no host sync before the merge rounds, and pieces of a host batch
   // enumerate their candidates as they arrive)
@@ -1524,6 +1549,8 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   uint32_t* res1 = ws.alloc<uint32_t>(nedges_max > 0 ? nedges_max : 1);
   uint32_t* res2 = nullptr;
   if (g.D == 3) res2 = ws.alloc<uint32_t>(3 * g.nvox);
+  // the top-dimension dual forest, written by the filtration (OMEGA = nvox)
+  S.dual_parent = g.D >= 2 ? ws.alloc<uint32_t>(g.nvox + 1) : nullptr;
   S.res_faces = g.D == 3 ? res2 : (g.D == 2 ? res1 : nullptr);
   S.nres_faces = reinterpret_cast<const unsigned*>(g.D == 3 ? cnt + 14 : cnt + 12);
 
@@ -1548,6 +1575,10 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
     kp.nres1 = ncand;
     kp.res2 = res2;
     kp.nres2 = reinterpret_cast<unsigned*>(cnt + 14);
+    kp.h0par = parent;
+    kp.basins = basins;
+    kp.nbasins = cnt + 8;
+    kp.dpar = S.dual_parent;
     if (opt(OPT_KF_RCAP) > 0 && opt(OPT_KF_RCAP) < KF_RCAP) kp.rcap = uint32_t(opt(OPT_KF_RCAP));
     // the source planes the filtration reads (a batch read unstacked has no separator planes)
     const int64_t nzsrc = kp.zper ? (g.nz + 1) / kp.zper * kp.zimg : g.nz;
@@ -1567,19 +1598,6 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
             image, kp, S.births, S.tags, cnt, nan_flag, tmap);
     };
     const uint32_t nzc = uint32_t((g.nz + L.zc - 1) / L.zc), xy = kp.XB * kp.YB;
-    const int64_t plane = g.nx * g.ny;
-    int64_t forest_z = 0;  // planes [0, forest_z) have their basin forest
-    // the basin forest of planes [forest_z, zt): pieces are whole images plus separators, and
-    // apparent vertex-edge pairs never cross a separator (its cells are absent), so the forest
-    // of a piece is closed
-    auto forest_upto = [&](int64_t zt) {
-      if (zt <= forest_z) return;
-      const int64_t v0 = forest_z * plane, v1 = zt * plane;
-      k_h0_parent<<<unsigned((v1 - v0 + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
-          S.births, S.tags, g, parent, cnt + 8, uint32_t(v0), uint32_t(v1), basins);
-      CR_CHECK_LAUNCH();
-      forest_z = zt;
-    };
     if (S.nready == 0) {
       launch_kf(L.grid);
       CR_CHECK_LAUNCH();
@@ -1598,16 +1616,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
         launch_kf((c1 - c0) * xy);
         CR_CHECK_LAUNCH();
         c0 = c1;
-        // births and tags are final for the planes below c0 zc - 1 (the last output plane's
-        // tags need the next block's codes): the forest of the pieces entirely below it
-        const int64_t zdone = c0 >= nzc ? g.nz : int64_t(c0) * L.zc - 1;
-        int64_t zt = forest_z;
-        for (int k = 0; k < S.nready; ++k)
-          if (S.ready_z[k] <= zdone) zt = S.ready_z[k] > zt ? S.ready_z[k] : zt;
-        if (c0 >= nzc) zt = g.nz;
-        forest_upto(zt);
       }
-      h0_forest_done = true;
     }
     prof_mark(s, "filtration");
   }
@@ -1635,11 +1644,7 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   // the residual edges come listed from the filtration (no per-voxel edge scan: 3.25 -> 1.91 ms).
   // Pieces of a batch arriving from the host were done in the filtration loop above.
   if (!cand) cand = ws.alloc<Cand>(nedges_max > 0 ? nedges_max : 1);
-  if (!h0_forest_done) {
-    k_h0_parent<<<unsigned((g.nvox + VOX_THREADS - 1) / VOX_THREADS), VOX_THREADS, 0, s>>>(
-        S.births, S.tags, g, parent, cnt + 8, 0u, uint32_t(g.nvox), basins);
-    CR_CHECK_LAUNCH();
-  }
+  // (the basin forest and its basins list were written by the filtration)
   // H0 candidates: every residual present edge (the filtration's list) with its endpoints
   k_h0_cands<<<148 * 8, 256, 0, s>>>(res1, ncand, S.births, g, cand);
   CR_CHECK_LAUNCH();
@@ -1692,6 +1697,10 @@ void run_general(const float* image, const Geom& g, int dmax, Workspace& ws, Hos
   if (S.res_faces) {
     ws.release(S.res_faces);
     S.res_faces = nullptr;
+  }
+  if (S.dual_parent) {
+    ws.release(S.dual_parent);
+    S.dual_parent = nullptr;
   }
 }
 

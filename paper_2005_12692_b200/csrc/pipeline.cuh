@@ -40,6 +40,7 @@ struct GeneralState {
   // the top-dimension dual (cleared ones are skipped there); nullptr: not listed
   uint32_t* res_faces = nullptr;
   const unsigned* nres_faces = nullptr;
+  uint32_t* dual_parent = nullptr;  // the top-dimension dual forest built by the filtration
   int nready = 0;
   int64_t ready_z[16];
   cudaEvent_t ready_ev[16];
