@@ -166,7 +166,7 @@ def stacked_shape(shape, batch):
     return (batch * (int(shape[0]) + 1) - 1,) + tuple(int(v) for v in shape[1:])
 
 
-def algorithmic_bytes(stage, nvox, kcells, n_out, K=0):
+def algorithmic_bytes(stage, nvox, kcells, n_out, K=0, D=3):
     """Bytes a stage must move once."""
     if stage == "1d_level1":
         return 4 * nvox + 8 * n_out               # read the series, stage (birth, death) per bar
@@ -176,8 +176,11 @@ def algorithmic_bytes(stage, nvox, kcells, n_out, K=0):
         return 12 * nvox + (8 * nvox if stage == "f64_rank" else 0)
     if stage == "f64_map":
         return 12 * n_out + 24 * n_out
-    if stage == "filtration":                     # K1+K2 fused: read the image, write births+tags
-        return 4 * nvox + 5 * kcells
+    if stage == "filtration":
+        # K1+K2 fused: read the image, write births + tags, the H0 basin forest and (D >= 2) the
+        # top-dimension dual forest (4 B per voxel each), and list the residual present edges
+        # (and, 3D, squares) -- 4 B each, K of them
+        return 4 * nvox + 5 * kcells + 4 * nvox + (4 * nvox if D >= 2 else 0) + 4 * K
     return None
 
 
@@ -477,7 +480,12 @@ def run_ours(args, rank, world, local_rank):
     # the kernel north_star's bandwidth target names; 1D configs: the dominant 1D kernel
     roof_stage = "filtration" if "filtration" in stage_avg else dom
     roof = None
-    alg = algorithmic_bytes(roof_stage, nvox_dev, kcells, n_out) if roof_stage else None
+    listed, D = 0, sum(1 for n in (kshape if batched else shape) if n > 1)
+    if st and st.get("cells") and st.get("apparent"):
+        c, a = st["cells"], st["apparent"]
+        listed = max(c[1] - a[0] - a[1], 0) + (max(c[2] - a[1] - a[2], 0) if D == 3 else 0)
+    alg = (algorithmic_bytes(roof_stage, nvox_dev, kcells, n_out, K=listed, D=D)
+           if roof_stage else None)
     if alg:
         ach = alg / (stage_avg[roof_stage] / 1e3) / 1e9
         ncu = ncu_summary(NCU_KERNEL.get(roof_stage, ""), args.config)

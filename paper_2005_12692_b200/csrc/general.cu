@@ -268,6 +268,7 @@ struct alignas(128) Kf2Smem {
   uint32_t rbuf[KF_RCAP];
   uint32_t rbuf2[KF_RCAP];
   uint32_t bcnt, bbase;       // basins listed by the CTA (bbuf holds the first rcap)
+  uint32_t doff[8];           // voxel offset of each direction (the forests)
   uint32_t bbuf[KF_RCAP];
 };
 inline KfP kf2_params(const Geom& g, int zc) {
@@ -337,6 +338,10 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
   const bool vy2 = y0 + 2 < ny;  // the extra ring row (last warp)
   if (threadIdx.x < 8) S.cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) S.rcnt = S.rcnt2 = S.bcnt = 0;
+  if (threadIdx.x < 8) {  // voxel offset of direction d: -x +x -y +y -z +z (two's complement)
+    const uint32_t d = threadIdx.x, o = d < 2 ? 1u : (d < 4 ? P.nx : P.plane);
+    S.doff[d] = d < 6 ? ((d & 1) ? o : 0u - o) : 0u;
+  }
   if (P.dpar && blockIdx.x == 0 && threadIdx.x == 0) P.dpar[P.nx * P.ny * P.nz] = P.nx * P.ny * P.nz;
   constexpr uint32_t INF_BITS = 0x7F800000u;
   // Voxel ring: rows y0(w=0) .. y0(w=0) + 2 NW (the last copied by the last warp), cols x0-1 ..
@@ -468,6 +473,18 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
     rowbase[r] = uint32_t(2 * max(y0 + r, 0)) * P.KX + uint32_t(2 * max(x, 0));
   const bool hx = x + 1 < nx;
   const bool hy[2] = {y0 + 1 < ny, y0 + 2 < ny};
+  // the forests: the row's voxel index in its plane; the top cell exists in x / y; the
+  // directions (bit = dir: -x +x -y +y) whose top cell two steps away exists
+  uint32_t vrow[2], dok[2];
+  bool dtop[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int yr = y0 + r;
+    vrow[r] = uint32_t(max(yr, 0)) * P.nx + uint32_t(max(x, 0));
+    dtop[r] = (nx == 1 || hx) && (ny == 1 || hy[r]);
+    dok[r] = (x > 0 ? 1u : 0u) | (x + 2 < nx ? 2u : 0u) | (yr > 0 ? 4u : 0u) |
+             (yr + 2 < ny ? 8u : 0u);
+  }
   uint32_t rs = 0;
   for (; z <= z1 + 1; ++z) {
     issue(z + KF_PF, (rs + KF_PF) & (KF_RING - 1));
@@ -631,35 +648,28 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
           if (hx && hy[r]) p3[1] = uint8_t(T[r][1] >> 24);
         }
         if (P.h0par) {  // (branch-free but for the rare basin staging)
-          const uint32_t y = uint32_t(y0 + r), zz = uint32_t(zb2);
-          const uint32_t v = zz * P.plane + y * P.nx + uint32_t(x);
-          auto step = [&](uint32_t t) {  // voxel offset of the tag's direction
-            const uint32_t a = (t & 7u) >> 1;
-            return a == 0 ? 1u : (a == 1 ? P.nx : P.plane);
-          };
+          const uint32_t v = uint32_t(zb2) * P.plane + vrow[r];
           // H0: an apparent vertex hangs under its partner edge's other vertex (absent cells
-          // have tag 0: never UP)
+          // have tag 0: never UP); S.doff[dir] = the voxel offset of direction dir
           const uint32_t vt = T[r][0] & 0xFFu;
           const bool vup = (vt >> 6) == KIND_UP;
-          const uint32_t sv = step(vt);
-          P.h0par[v] = vup ? ((vt & 1u) ? v + sv : v - sv) : v;
+          P.h0par[v] = vup ? v + S.doff[vt & 7u] : v;
           if (!vup && !(CC[r][0] & 0x40u)) {  // a present basin (rare)
             const uint32_t i = atomicAdd(&S.bcnt, 1u);
             if (i < P.rcap) S.bbuf[i] = v;
             else P.basins[atomicAdd(P.nbasins, 1ull)] = v;
           }
           if (P.dpar) {  // the dual: a top cell hangs under the top cell across its apparent face
-            const uint32_t OMEGA = P.nx * P.ny * P.nz;
-            const bool has_top = (P.nx == 1 || hx) && (P.ny == 1 || hy[r]) && (P.nz == 1 || hz);
             const uint32_t tw = P.topw ? T[r][1] : T[r][0], cw = P.topw ? CC[r][1] : CC[r][0];
             const uint32_t tt = (tw >> (8 * P.topb)) & 0xFFu;
             const bool tabs = (cw >> (8 * P.topb)) & 0x40u;
             const bool tdown = (tt >> 6) == KIND_DOWN;
-            const uint32_t a = (tt & 7u) >> 1, st = step(tt);
-            const uint32_t ca = a == 0 ? uint32_t(x) : (a == 1 ? y : zz);
-            const uint32_t na = a == 0 ? P.nx : (a == 1 ? P.ny : P.nz);
-            const uint32_t across = (tt & 1u) ? (ca + 2 < na ? v + st : OMEGA)
-                                              : (ca > 0 ? v - st : OMEGA);
+            // directions whose top cell two steps away exists: x / y bits per row, z per plane
+            const uint32_t okm = dok[r] | (zb2 > 0 ? 0x10u : 0u) |
+                                 (uint32_t(zb2) + 2 < P.nz ? 0x20u : 0u);
+            const uint32_t OMEGA = P.nx * P.ny * P.nz;
+            const uint32_t across = (okm >> (tt & 7u)) & 1u ? v + S.doff[tt & 7u] : OMEGA;
+            const bool has_top = dtop[r] && (P.nz == 1 || hz);
             // absent top cells hang under OMEGA (a cavity call rebuilds the forest)
             P.dpar[v] = !has_top ? v : (tabs ? OMEGA : (tdown ? across : v));
           }
