@@ -12,6 +12,9 @@ sys.path.insert(1, HERE)
 import numpy as np, torch
 import paper_2005_12692_b200 as cr
 from workloads import generators as gen
+opts = dict(kv.split("=") for kv in (os.environ.get("OPTS") or "").split() if kv)
+for k, v in opts.items():
+    cr.set_option(k, int(v))
 for name in (os.environ.get("CFGS") or "c5b c5 c4").split():
     img, md = gen.config(name)
     t = torch.from_numpy(img).cuda()
@@ -24,5 +27,5 @@ for name in (os.environ.get("CFGS") or "c5b c5 c4").split():
         runs.append(cr.last_stats()["stages"])
     cr.set_profiling(False)
     med = {k: round(float(np.median([r[k] for r in runs])), 4) for k in runs[0]}
-    print(json.dumps({"root": root, "cfg": name, "total": round(sum(med.values()), 3), "stages": med}), flush=True)
+    print(json.dumps({"root": root, "opts": opts, "cfg": name, "total": round(sum(med.values()), 3), "stages": med}), flush=True)
     del t
