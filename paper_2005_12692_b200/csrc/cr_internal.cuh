@@ -165,45 +165,8 @@ __device__ __forceinline__ bool vox_of_thread(const Geom& g, uint32_t& v, uint32
   return vv < uint64_t(g.nvox);
 }
 
-// Append up to NI items per thread to out[] behind the counter *n with ONE global atomic per
-// block (a block scan of the per-thread counts): the per-voxel passes emit ~1M items, and an
-// atomic per emitting warp and item slot serialised on the one counter.  Item order is
-// arbitrary.  Every thread of the block must call it; blockDim.x <= 1024.
-template <class T, int NI>
-__device__ __forceinline__ void block_append(const bool (&emit)[NI], const T (&item)[NI],
-                                             T* __restrict__ out, unsigned* __restrict__ n) {
-  __shared__ unsigned s_warp[33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
-  unsigned cnt = 0;
-#pragma unroll
-  for (int i = 0; i < NI; ++i) cnt += emit[i] ? 1u : 0u;
-  if (!__syncthreads_or(cnt != 0)) return;  // most blocks emit nothing: one barrier
-  unsigned incl = cnt;  // inclusive warp scan
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned run = 0;
-    for (int w = 0; w < nwarps; ++w) {
-      const unsigned c = s_warp[w];
-      s_warp[w] = run;
-      run += c;
-    }
-    s_warp[32] = run ? atomicAdd(n, run) : 0u;
-  }
-  __syncthreads();
-  unsigned pos = s_warp[32] + s_warp[warp] + incl - cnt;
-#pragma unroll
-  for (int i = 0; i < NI; ++i)
-    if (emit[i]) out[pos++] = item[i];
-}
-
-// The same with one atomic per emitting warp and item slot (measured faster where the items are
-// spread over most blocks: H0 candidates, K5 columns; block_append wins for the dual edges).
+// Append up to NI items per thread to out[] behind the counter *n with one atomic per emitting
+// warp for all NI slots.  Item order is arbitrary.  Every lane of the warp must call it.
 template <class T, int NI>
 __device__ __forceinline__ void warp_append(const bool (&emit)[NI], const T (&item)[NI],
                                             T* __restrict__ out, unsigned* __restrict__ n) {

@@ -1077,72 +1077,6 @@ __global__ void k_dual_cands(const uint32_t* __restrict__ list, const unsigned* 
   }
 }
 
-__global__ void k_dual_edges(const uint32_t* __restrict__ births, const uint8_t* __restrict__ tags,
-                             DualG G, uint32_t* parent, Cand* __restrict__ cand,
-                             unsigned int* __restrict__ ncand, unsigned long long* nroots) {
-  const Geom& g = G.g;
-  uint32_t v, x, y, z;
-  const bool in = vox_of_thread(g, v, x, y, z);
-  const uint32_t kb = (2 * z * uint32_t(g.KY) + 2 * y) * uint32_t(g.KX) + 2 * x;
-  // every face with base voxel v contains v: an absent v has no face to emit (roots still count)
-  const bool vpres = in && births[kb] != ABSENT_ORD;
-  const uint32_t c[3] = {x, y, z}, n[3] = {uint32_t(g.nx), uint32_t(g.ny), uint32_t(g.nz)};
-  const uint32_t ks[3] = {1u, uint32_t(g.KX), uint32_t(g.KX * g.KY)};
-  const uint32_t vs[3] = {1u, uint32_t(g.nx), uint32_t(g.nx * g.ny)};
-  // the top cell with base voxel v exists iff c_b + 1 < n_b on every active axis b
-  bool has_top = in;
-  uint32_t kt = kb;
-#pragma unroll
-  for (int b = 0; b < 3; ++b)
-    if (n[b] > 1) {
-      has_top = has_top && c[b] + 1 < n[b];
-      kt += ks[b];
-    }
-  const uint32_t pv = in ? parent[v] : 0u;  // the top cell at v is a root iff pv == v
-  uint32_t rv = NONE32;                      // its root, found on the first residual face
-  {
-    const bool root = has_top && pv == v;
-    const unsigned mask = __ballot_sync(0xFFFFFFFFu, root);
-    if ((threadIdx.x & 31) == 0 && mask) atomicAdd(nroots, (unsigned long long)__popc(mask));
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 &&
-        parent[G.omega] == G.omega)
-      atomicAdd(nroots, 1ull);
-  }
-  bool emit[3];
-  Cand cd[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    emit[a] = false;
-    if (vpres && n[a] > 1) {
-      bool ok = true;
-      uint32_t k = kb;
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-        if (b != a && n[b] > 1) {
-          ok = ok && c[b] + 1 < n[b];
-          k += ks[b];
-        }
-      if (ok) {
-        const uint32_t bo = births[k];
-        if (bo != ABSENT_ORD && tag_kind(tags[k]) == KIND_RESIDUAL) {
-          // the roots of the face's two sides found here (the dual forest is shallow; leaving
-          // the finds -- and the same-root faces -- to k_mm_rounds as H0 does measured slower:
-          // C5b top dimension 3.16 -> 3.9 ms)
-          const uint32_t ra = c[a] > 0 ? find_halve(parent, v - vs[a]) : G.omega;
-          if (rv == NONE32 && c[a] + 1 < n[a]) rv = find_halve(parent, v);
-          const uint32_t rb = c[a] + 1 < n[a] ? rv : G.omega;
-          if (ra != rb) {
-            emit[a] = true;
-            cd[a].key = ~make_key(bo, k);  // ascending ~key = decreasing key
-            cd[a].a = ra;
-            cd[a].b = rb;
-          }
-        }
-      }
-    }
-  }
-  block_append(emit, cd, cand, ncand);
-}
 
 // key of a dual root (larger = elder): OMEGA the largest, absent top cells next
 __device__ __forceinline__ uint64_t dual_root_key(const uint32_t* __restrict__ births, const DualG& G,
@@ -1190,7 +1124,7 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
   // Initialise the two minima buffers at the roots the candidates touch, and the alive flags,
   // instead of memsetting 2 x nbest words (2.2 GB on C5b): every root a later find returns is
   // an endpoint root of some candidate (links only join two candidates' endpoint roots).
-  // The candidates arrive with their endpoints (H0: voxels; the dual's k_dual_edges already
+  // The candidates arrive with their endpoints (H0: voxels; the dual's k_dual_cands already
   // passes roots): their roots in the apparent forest are found here (path halving), the
   // same-root ones dropped (H0: the edge closes a cycle of older edges).
   for (unsigned i = gt; i < n; i += gs) {
@@ -1347,36 +1281,29 @@ bool top_dual(GeneralState& S, int d, Workspace& ws, HostScalars& hs, cr_stats& 
     const int64_t ess_top = (d & 1) ? low - chi : chi - low;
     no_cavity = ess_top == 0;
   }
-  const bool listed = S.res_faces != nullptr;
+  if (!S.res_faces) throw Error{CR_EINTERNAL, "top_dual: the residual faces were not listed"};
   // with the filtration's forest the roots among the top cells are counted from its counters:
   // the present top cells that are not the upper cell of an apparent pair (face, top)
   const bool forest_given = S.dual_parent != nullptr && no_cavity && d == g.D - 1;
   if (!forest_given) {
     k_dual_parent<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent,
                                                       no_cavity ? 1 : 0,
-                                                      listed && no_cavity ? cnt + 1 : nullptr);
+                                                      no_cavity ? cnt + 1 : nullptr);
     CR_CHECK_LAUNCH();
   }
   if (!no_cavity) {
     k_dual_absent_vox<<<grid_for(g.nvox, B), B, 0, s>>>(S.births, G, parent);
     CR_CHECK_LAUNCH();
-    if (listed) {
-      k_dual_roots<<<vox_grid(g), VOX_THREADS, 0, s>>>(G, parent, cnt + 1);
-      CR_CHECK_LAUNCH();
-    }
+    k_dual_roots<<<vox_grid(g), VOX_THREADS, 0, s>>>(G, parent, cnt + 1);
+    CR_CHECK_LAUNCH();
   }
-  // (no flattening: k_dual_edges finds the roots of the residual faces' sides on demand)
+  // the residual faces listed by the filtration (no per-voxel face scan); the roots of their
+  // sides found on demand (no flattening)
   Cand* cand = ws.alloc<Cand>(st.cells[d] + 1);
   unsigned* ncand = reinterpret_cast<unsigned*>(cnt);
-  if (listed) {  // the residual faces listed by the filtration (no per-voxel face scan)
-    k_dual_cands<<<148 * 8, 256, 0, s>>>(S.res_faces, S.nres_faces, S.births, S.tags, G, parent,
-                                         cand, ncand, cnt + 1);
-    CR_CHECK_LAUNCH();
-  } else {
-    k_dual_edges<<<vox_grid(g), VOX_THREADS, 0, s>>>(S.births, S.tags, G, parent, cand, ncand,
-                                                    cnt + 1);
-    CR_CHECK_LAUNCH();
-  }
+  k_dual_cands<<<148 * 8, 256, 0, s>>>(S.res_faces, S.nres_faces, S.births, S.tags, G, parent,
+                                       cand, ncand, cnt + 1);
+  CR_CHECK_LAUNCH();
   // candidates <= the finite d-cells (known since H0's read): no host read before the rounds
   const int64_t n = st.cells[d] + 1;
   unsigned long long* nrec = cnt + 2;
