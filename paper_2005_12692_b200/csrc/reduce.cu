@@ -954,6 +954,18 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
 
 // ---------------------------------------------------------------- the asynchronous commit rule
 
+// Release / acquire fences at GPU scope.  __threadfence (fence.sc) also invalidates the SM's L1
+// (SASS CCTL.IVALL), which drops every warp's cached births and tags; a release needs only the
+// MEMBAR (fence.release.gpu, no CCTL), and the one acquire site uses fence.acquire.gpu (CCTL
+// only).  Every load of data other warps write (lv, the owner table, the pool) is L2-coherent
+// (ld.relaxed.gpu / ld.cg), so L1 holds only read-only data.
+__device__ __forceinline__ void fence_release() {
+  asm volatile("fence.release.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void fence_acquire() {
+  asm volatile("fence.acquire.gpu;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t ld_rlx(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1044,7 +1056,7 @@ __device__ __forceinline__ uint32_t find_blocker(const RP& P, uint32_t x, uint32
 __device__ __forceinline__ void finish_column(const RP& P, uint32_t j, int lane) {
   __syncwarp();
   if (lane == 0) {
-    __threadfence();  // the owner entry and the record are visible before "finished"
+    fence_release();  // the owner entry and the record are visible before "finished"
     st_rlx(P.lv[0] + j, NONE64);
   }
   __syncwarp();
@@ -1057,7 +1069,7 @@ __device__ __forceinline__ void finish_column(const RP& P, uint32_t j, int lane)
     const uint64_t mn = bag_min(cv);  // two 32-bit reductions instead of five 64-bit shuffles
     if (lane == 0 && mn > ld_rlx(P.lv[L] + e)) {
       atomicMax(reinterpret_cast<unsigned long long*>(P.lv[L] + e), mn);
-      __threadfence();
+      fence_release();
     }
     __syncwarp();
     if (mn != NONE64) break;
@@ -1293,7 +1305,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
         if (!owned) {  // every earlier column is finished or beyond piv: final check, commit
           uint64_t o = 0;
           if (lane == 0) {
-            __threadfence();
+            fence_acquire();  // the owner entries published before the "finished" flags seen
             o = owner_of_rlx(P.otab, P.omask, pk);
           }
           owned = __shfl_sync(0xFFFFFFFFu, o, 0) != NONE64;
@@ -1340,9 +1352,10 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           n = merge_chunked<false>(c.Mc + c.h, c.nm - c.h, c.Fc + c.f0, c.nf - c.f0,
                                    P.pool + off, c.Fa, nullptr, lane);
         }
+        __syncwarp();  // every lane's pool writes before lane 0's release
         if (lane == 0) {
           if (n >> OI_LEN_BITS) atomicOr(P.err, 4);  // a reduced column of >= 2^24 entries
-          __threadfence();
+          fence_release();
           owner_insert(P.otab, P.omask, pk, (uint64_t(off) << OI_LEN_BITS) | n);
           P.rec[j] = (uint64_t(cell) << 32) | pk;  // (birth cell, death cell)
         }
