@@ -959,6 +959,12 @@ __device__ __forceinline__ bool add_column(CT& c, const uint64_t* B, uint32_t nb
 // MEMBAR (fence.release.gpu, no CCTL), and the one acquire site uses fence.acquire.gpu (CCTL
 // only).  Every load of data other warps write (lv, the owner table, the pool) is L2-coherent
 // (ld.relaxed.gpu / ld.cg), so L1 holds only read-only data.
+#ifndef K5_SLEEP_MAX
+#define K5_SLEEP_MAX 2048  // ns: the back-off of a column waiting on an earlier one
+#endif
+#ifndef K5_SLEEP0
+#define K5_SLEEP0 64
+#endif
 __device__ __forceinline__ void fence_release() {
   asm volatile("fence.release.gpu;" ::: "memory");
 }
@@ -1278,7 +1284,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
           // All lanes read the same word (one transaction, the same value in every lane: no
           // shuffles); the owner entry and the error flag are looked at every 8th try; the
           // back-off grows to 2 us.
-          unsigned ns = 64;
+          unsigned ns = K5_SLEEP0;
           for (int it = 1;; ++it) {
             if (ld_rlx(P.lv[0] + b) > piv) break;
             if ((it & 7) == 0) {
@@ -1292,7 +1298,7 @@ __global__ void __launch_bounds__(THREADS, K5_MINB) k_reduce(RP P) {
               }
             }
             __nanosleep(ns);
-            if (ns < 2048) ns <<= 1;
+            if (ns < K5_SLEEP_MAX) ns <<= 1;
           }
           if (DBG) {
             wcyc += clock64() - t0;
