@@ -850,16 +850,6 @@ __global__ void k_h0_cands(const uint32_t* __restrict__ list, const unsigned* __
   }
 }
 
-__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
-  uint32_t p = *(volatile uint32_t*)(parent + v);
-  if (p == v) return v;
-  while (true) {
-    uint32_t pp = *(volatile uint32_t*)(parent + p);
-    if (pp == p) break;
-    p = pp;
-  }
-  return p;
-}
 
 
 // ---------------------------------------------------------------------------------------------
@@ -1156,7 +1146,9 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
         st &= 1;
       }
       if (st & 1) {
-        const uint32_t a = uf_find(A.parent, c.a), b = uf_find(A.parent, c.b);
+        // path halving (only ancestor pointers are written in the find phase; links are made
+        // in the commit phase, after the grid barrier): C5b H0 1.26 -> 1.09 ms over plain finds
+        const uint32_t a = find_halve(A.parent, c.a), b = find_halve(A.parent, c.b);
         if (a == b) {  // connected through strictly smaller edges: positive
           st = 0;
         } else {
