@@ -32,8 +32,9 @@ struct GeneralState {
   // (images + separator) and per image; 0 = the image is laid out as the geometry says
   uint32_t img_zper = 0, img_zimg = 0;
   // H0's candidate list, kept for the dim-1 columns: every residual edge is an H0 candidate
-  // (k_h0_edges), and the residual edges that H0 did not clear are exactly the dim-1 columns, so
-  // reduce_dimension(1) compacts this list instead of scanning the grid (nullptr: scan)
+  // (listed by k_filtration), and the residual edges that H0 did not clear are exactly the dim-1
+  // columns, so reduce_dimension(1) compacts this list instead of scanning the grid (nullptr:
+  // scan)
   const H0Cand* h0_cand = nullptr;
   uint32_t h0_ncand = 0;
   // the residual present (D-1)-cells listed by the filtration (kidx; device count): the faces of
