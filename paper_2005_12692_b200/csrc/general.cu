@@ -649,29 +649,37 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_filtration(const float*
         }
         if (P.h0par) {  // (branch-free but for the rare basin staging)
           const uint32_t v = uint32_t(zb2) * P.plane + vrow[r];
-          // H0: an apparent vertex hangs under its partner edge's other vertex (absent cells
-          // have tag 0: never UP); S.doff[dir] = the voxel offset of direction dir
-          const uint32_t vt = T[r][0] & 0xFFu;
-          const bool vup = (vt >> 6) == KIND_UP;
-          P.h0par[v] = vup ? v + S.doff[vt & 7u] : v;
-          if (!vup && !(CC[r][0] & 0x40u)) {  // a present basin (rare)
-            const uint32_t i = atomicAdd(&S.bcnt, 1u);
-            if (i < P.rcap) S.bbuf[i] = v;
-            else P.basins[atomicAdd(P.nbasins, 1ull)] = v;
-          }
-          if (P.dpar) {  // the dual: a top cell hangs under the top cell across its apparent face
-            const uint32_t tw = P.topw ? T[r][1] : T[r][0], cw = P.topw ? CC[r][1] : CC[r][0];
-            const uint32_t tt = (tw >> (8 * P.topb)) & 0xFFu;
-            const bool tabs = (cw >> (8 * P.topb)) & 0x40u;
-            const bool tdown = (tt >> 6) == KIND_DOWN;
-            // directions whose top cell two steps away exists: x / y bits per row, z per plane
-            const uint32_t okm = dok[r] | (zb2 > 0 ? 0x10u : 0u) |
-                                 (uint32_t(zb2) + 2 < P.nz ? 0x20u : 0u);
-            const uint32_t OMEGA = P.nx * P.ny * P.nz;
-            const uint32_t across = (okm >> (tt & 7u)) & 1u ? v + S.doff[tt & 7u] : OMEGA;
-            const bool has_top = dtop[r] && (P.nz == 1 || hz);
-            // absent top cells hang under OMEGA (a cavity call rebuilds the forest)
-            P.dpar[v] = !has_top ? v : (tabs ? OMEGA : (tdown ? across : v));
+          const uint32_t OMEGA = P.nx * P.ny * P.nz;
+          const bool has_top = dtop[r] && (P.nz == 1 || hz);
+          if (fast) {  // the warp's cells of B(z-2) are all absent (warp-uniform)
+            P.h0par[v] = v;
+            if (P.dpar) P.dpar[v] = has_top ? OMEGA : v;
+          } else {
+            // H0: an apparent vertex hangs under its partner edge's other vertex (absent cells
+            // have tag 0: never UP); S.doff[dir] = the voxel offset of direction dir
+            const uint32_t vt = T[r][0] & 0xFFu;
+            const bool vup = (vt >> 6) == KIND_UP;
+            P.h0par[v] = vup ? v + S.doff[vt & 7u] : v;
+            if (!vup && !(CC[r][0] & 0x40u)) {  // a present basin (rare)
+              const uint32_t i = atomicAdd(&S.bcnt, 1u);
+              if (i < P.rcap) S.bbuf[i] = v;
+              else P.basins[atomicAdd(P.nbasins, 1ull)] = v;
+            }
+            if (P.dpar) {  // the dual: a top cell hangs under the top cell across its apparent face
+              // (3D: the cube, byte 3 of word 1; else the top cell's word and byte)
+              const bool d3 = P.topw == 1 && P.topb == 3;
+              const uint32_t tw = d3 ? T[r][1] >> 24 : ((P.topw ? T[r][1] : T[r][0]) >> (8 * P.topb));
+              const uint32_t cw = d3 ? CC[r][1] >> 24 : ((P.topw ? CC[r][1] : CC[r][0]) >> (8 * P.topb));
+              const uint32_t tt = tw & 0xFFu;
+              const bool tabs = cw & 0x40u;
+              const bool tdown = (tt >> 6) == KIND_DOWN;
+              // directions whose top cell two steps away exists: x / y bits per row, z per plane
+              const uint32_t okm = dok[r] | (zb2 > 0 ? 0x10u : 0u) |
+                                   (uint32_t(zb2) + 2 < P.nz ? 0x20u : 0u);
+              const uint32_t across = (okm >> (tt & 7u)) & 1u ? v + S.doff[tt & 7u] : OMEGA;
+              // absent top cells hang under OMEGA (a cavity call rebuilds the forest)
+              P.dpar[v] = !has_top ? v : (tabs ? OMEGA : (tdown ? across : v));
+            }
           }
         }
       }
