@@ -1162,8 +1162,11 @@ __global__ void __launch_bounds__(256) k_mm_rounds(MMArgs A) {
         } else {
           cur[i].a = a;
           cur[i].b = b;
-          atomicMin(bc + a, (unsigned long long)c.key);
-          atomicMin(bc + b, (unsigned long long)c.key);
+          // test before the atomic: a root's minimum only decreases within the round, so a key
+          // not below the value read cannot be it (the true minimum always reads a larger value:
+          // keys are unique); the atomics on a large component's root no longer serialise
+          if (c.key < __ldcg(bc + a)) atomicMin(bc + a, (unsigned long long)c.key);
+          if (c.key < __ldcg(bc + b)) atomicMin(bc + b, (unsigned long long)c.key);
           st = 3;
         }
       }
