@@ -854,6 +854,8 @@ __global__ void k_h0_cands(const uint32_t* __restrict__ list, const unsigned* __
     const uint32_t Z = k / KXY, rm = k - Z * KXY, Y = rm / KX, X = rm - Y * KX;
     const uint32_t v = (Z >> 1) * nxy + (Y >> 1) * nx + (X >> 1);
     const uint32_t vs = (X & 1) ? 1u : ((Y & 1) ? nx : nxy);
+    CR_DASSERT(uint64_t(k) < uint64_t(g.ncells) && ((X & 1) + (Y & 1) + (Z & 1)) == 1);
+    CR_DASSERT(uint64_t(v) + vs < uint64_t(g.nvox));
     cand[i] = Cand{make_key(births[k], k), v, v + vs};
   }
 }
@@ -1052,6 +1054,7 @@ __global__ void k_dual_cands(const uint32_t* __restrict__ list, const unsigned* 
     Cand cd[1];
     if (i < N) {
       const uint32_t k = list[i];
+      CR_DASSERT(uint64_t(k) < uint64_t(g.ncells));
       if (tag_kind(tags[k]) == KIND_RESIDUAL) {  // not cleared by the dimension below
         const uint32_t Z = k / KXY, rm = k - Z * KXY, Y = rm / KX, X = rm - Y * KX;
         const uint32_t C[3] = {X, Y, Z};
@@ -1061,6 +1064,7 @@ __global__ void k_dual_cands(const uint32_t* __restrict__ list, const unsigned* 
           if (n[b] > 1 && !(C[b] & 1)) a = b;
         const uint32_t v = (Z >> 1) * vs[2] + (Y >> 1) * vs[1] + (X >> 1);
         const uint32_t ca = C[a] >> 1;
+        CR_DASSERT(v < G.omega && ca < n[a] && births[k] != ABSENT_ORD);
         const uint32_t ra = ca > 0 ? find_halve(parent, v - vs[a]) : G.omega;
         const uint32_t rb = ca + 1 < n[a] ? find_halve(parent, v) : G.omega;
         if (ra != rb) {

@@ -1501,6 +1501,7 @@ __global__ void k_cols_from_cands(const H0Cand* __restrict__ cand, uint32_t n,
   uint64_t key[1] = {0};
   if (i < n) {
     key[0] = cand[i].key;
+    CR_DASSERT(key_ord(key[0]) != ABSENT_ORD);
     emit[0] = tag_kind(tags[key_kidx(key[0])]) == KIND_RESIDUAL;
   }
   warp_append(emit, key, cols, ncols);
