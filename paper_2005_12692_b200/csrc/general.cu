@@ -63,9 +63,12 @@ struct KfLaunch {
   unsigned grid;
   int zc;
 };
+#ifndef KF_ZC0
+#define KF_ZC0 64  // planes a CTA walks (halved while the grid is below 4 CTAs per SM)
+#endif
 inline KfLaunch kf_launch(const Geom& g, int rows) {
   const int64_t xy = ((g.nx + 29) / 30) * ((g.ny + rows - 1) / rows);
-  int zc = 64;
+  int zc = KF_ZC0;
   while (zc > 8 && xy * ((g.nz + zc - 1) / zc) < 4 * 148) zc >>= 1;
   return {unsigned(xy * ((g.nz + zc - 1) / zc)), zc};
 }
